@@ -1,0 +1,87 @@
+"""ctypes binding of libpp200.so (include/pp200.h).
+
+The library is the only compute path: there is no CPU or eager-PyTorch
+fallback.  ``lib()`` raises ``RuntimeError`` when the shared object is
+missing, and every wrapper raises ``ExecutorFault``-compatible
+``PC Error`` on a non-zero status.
+"""
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = HERE / "libpp200.so"
+
+PC_F32, PC_F64, PC_BF16, PC_I32 = 0, 1, 2, 3
+
+EPI_BIAS = 1
+EPI_GELU = 2
+EPI_RESIDUAL = 4
+EPI_GELU_GRAD = 8
+EPI_ACCUM = 16
+EPI_RELU = 32
+EPI_RELU_GRAD = 64
+
+_c_i = ctypes.c_int
+_c_i64 = ctypes.c_int64
+_c_p = ctypes.c_void_p
+_c_f = ctypes.c_float
+_c_d = ctypes.c_double
+
+# name -> argtypes (all return int status unless listed in _RESTYPES)
+SIGNATURES: dict[str, list] = {
+    "pc_version": [],
+    "pc_device_sm_count": [],
+    "pc_gemm": [_c_i, _c_i, _c_i, _c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64,
+                _c_p, _c_i64, _c_i, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p],
+    "pc_gemm_set_tile_n": [_c_i],
+}
+_RESTYPES = {"pc_last_error": ctypes.c_char_p}
+
+
+class PCError(RuntimeError):
+    """Non-zero status from a libpp200 entry point."""
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib_path() -> pathlib.Path:
+    return LIB_PATH
+
+
+def lib():
+    """Load libpp200.so once; fail loudly if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2412_14374_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        L.pc_last_error.restype = ctypes.c_char_p
+        L.pc_last_error.argtypes = []
+        for name, args in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        _lib = L
+        return _lib
+
+
+def exported_symbols() -> list[str]:
+    return ["pc_last_error", *SIGNATURES]
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().pc_last_error().decode(errors="replace")
+        raise PCError(f"{name} failed ({rc}): {msg}")

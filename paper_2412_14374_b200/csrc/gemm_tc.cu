@@ -1,0 +1,420 @@
+// tcgen05 / TMEM / TMA bf16 GEMM for sm_100a with fused epilogues.
+//
+// Replaces the `matmul` rule of the reference interpreter (a @ b,
+// pkg/src/pipecraft/executor.py:66-67) and the explicit `transpose` ops the
+// backward rules emit before it (ir.py:519-529, executor.py:78-79): a
+// transpose is an operand major (K-major vs MN-major shared-memory
+// descriptor), never a copy.
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring (STAGES deep)
+//   warp 1      MMA issuer: one thread issues tcgen05.mma 128xBNx16 into TMEM
+//   warp 2      TMEM allocator (2 accumulator buffers of BN fp32 columns)
+//   warps 4..7  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue -> HBM
+// The two TMEM accumulators let the epilogue of tile i overlap the MMAs of
+// tile i+1.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace pp200 {
+
+namespace {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int TC_THREADS = 256;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
+constexpr int TC_MN_CHUNK_BYTES = TC_BK * 128;  // one 64-wide MN box of BK rows
+
+struct TcEpi {
+  void* C;
+  int64_t ldc;
+  const float* bias;
+  const void* aux;
+  int64_t ldaux;
+  void* aux_out;
+  int64_t ldaux_out;
+  int M, N, flags, out_f32;
+};
+
+template <int BN>
+struct TcCfg {
+  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int STAGE_BYTES = TC_A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+__device__ __forceinline__ void load16(const void* base, bool f32, int64_t off, int nvalid,
+                                       float* v) {
+  if (f32) {
+    const float* p = static_cast<const float*>(base) + off;
+    if (nvalid == 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float4 t = reinterpret_cast<const float4*>(p)[i];
+        v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+      }
+    } else {
+      for (int i = 0; i < 16; ++i) v[i] = i < nvalid ? p[i] : 0.f;
+    }
+  } else {
+    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + off;
+    if (nvalid == 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint4 t = reinterpret_cast<const uint4*>(p)[i];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 f = __bfloat1622float2(h[j]);
+          v[8 * i + 2 * j] = f.x;
+          v[8 * i + 2 * j + 1] = f.y;
+        }
+      }
+    } else {
+      for (int i = 0; i < 16; ++i) v[i] = i < nvalid ? __bfloat162float(p[i]) : 0.f;
+    }
+  }
+}
+
+__device__ __forceinline__ void store16(void* base, bool f32, int64_t off, int nvalid,
+                                        const float* v) {
+  if (f32) {
+    float* p = static_cast<float*>(base) + off;
+    if (nvalid == 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(p)[i] =
+            make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+      for (int i = 0; i < nvalid; ++i) p[i] = v[i];
+    }
+  } else {
+    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + off;
+    if (nvalid == 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint4 t;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          h[j] = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+        reinterpret_cast<uint4*>(p)[i] = t;
+      }
+    } else {
+      for (int i = 0; i < nvalid; ++i) p[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+__device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, float* v) {
+  const int nvalid = min(16, ep.N - col);
+  const bool f32 = ep.out_f32 != 0;
+  const int fl = ep.flags;
+  if (fl & PC_EPI_ACCUM) {
+    float old[16];
+    load16(ep.C, true, static_cast<int64_t>(row) * ep.ldc + col, nvalid, old);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += old[i];
+    store16(ep.C, true, static_cast<int64_t>(row) * ep.ldc + col, nvalid, v);
+    return;
+  }
+  if (fl & PC_EPI_BIAS) {
+    for (int i = 0; i < 16; ++i) v[i] += i < nvalid ? ep.bias[col + i] : 0.f;
+  }
+  if (fl & (PC_EPI_GELU | PC_EPI_RELU)) {
+    store16(ep.aux_out, f32, static_cast<int64_t>(row) * ep.ldaux_out + col, nvalid, v);
+    if (fl & PC_EPI_GELU) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = gelu_tanh(v[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+    }
+  }
+  if (fl & (PC_EPI_RESIDUAL | PC_EPI_GELU_GRAD | PC_EPI_RELU_GRAD)) {
+    float a[16];
+    load16(ep.aux, f32, static_cast<int64_t>(row) * ep.ldaux + col, nvalid, a);
+    if (fl & PC_EPI_RESIDUAL) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] += a[i];
+    } else if (fl & PC_EPI_GELU_GRAD) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] *= gelu_tanh_grad(a[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = a[i] > 0.f ? v[i] : 0.f;
+    }
+  }
+  store16(ep.C, f32, static_cast<int64_t>(row) * ep.ldc + col, nvalid, v);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, TcEpi ep) {
+  using Cfg = TcCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * TC_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + TC_BM - 1) / TC_BM, num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int nk = (K + TC_BK - 1) / TC_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tslot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          uint8_t* a = sA + stage * TC_A_BYTES;
+          uint8_t* b = sB + stage * Cfg::B_BYTES;
+          const int k0 = kb * TC_BK;
+          if (!A_MN) {
+            tma_load_2d(a, &tmA, &full[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < TC_BM / 64; ++j)
+              tma_load_2d(a + j * TC_MN_CHUNK_BYTES, &tmA, &full[stage], m0 + 64 * j, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(b, &tmB, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(b + j * TC_MN_CHUNK_BYTES, &tmB, &full[stage], n0 + 64 * j, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * TC_A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_sdesc_sw128(a_addr + k * 2048, TC_MN_CHUNK_BYTES, 1024)
+                                     : umma_sdesc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_sdesc_sw128(b_addr + k * 2048, TC_MN_CHUNK_BYTES, 1024)
+                                     : umma_sdesc_sw128(b_addr + k * 32, 16, 1024);
+            tc_mma_f16(d, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * BN;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const uint32_t tb =
+          tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld16(tb + c, r);
+        tmem_ld16(tb + c + 16, r + 16);
+        tc_wait_ld();
+        if (row < M) {
+          if (n0 + c < N) epilogue16(ep, row, n0 + c, reinterpret_cast<float*>(r));
+          if (n0 + c + 16 < N) epilogue16(ep, row, n0 + c + 16, reinterpret_cast<float*>(r + 16));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [outer, inner] view with leading
+// dimension `ld` elements, 128B-swizzled boxes of {64, box_outer}.
+int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int64_t ld,
+              int box_outer) {
+  auto enc = tmap_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return PC_ERR_CUDA;
+  }
+  PP_CHECK_ARG((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "TMA operand not 16B aligned");
+  PP_CHECK_ARG((ld * 2) % 16 == 0, "TMA leading dimension %lld not a multiple of 8", (long long)ld);
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return PC_ERR_CUDA;
+  }
+  return PC_OK;
+}
+
+int g_force_bn = 0;
+
+template <int BN, bool A_MN, bool B_MN>
+int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const TcEpi& ep,
+              cudaStream_t st) {
+  using Cfg = TcCfg<BN>;
+  static bool attr_set = false;  // benign race: idempotent attribute write
+  if (!attr_set) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
+  return check_launch("tc_gemm_kernel");
+}
+
+template <int BN>
+int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb, int M,
+                    int N, int K, const TcEpi& ep, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, M, N, K, ep, st);
+  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, M, N, K, ep, st);
+  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, M, N, K, ep, st);
+  return launch_tc<BN, true, true>(ta, tb, M, N, K, ep, st);
+}
+
+}  // namespace
+
+int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                 const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                 int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
+                 int64_t ldaux_out, cudaStream_t st) {
+  PP_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem");
+  PP_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
+  int bn = g_force_bn;
+  if (bn == 0) {
+    const int sms = num_sms();
+    const int64_t mt = (M + TC_BM - 1) / TC_BM;
+    if (N >= 256 && mt * ((N + 255) / 256) >= sms)
+      bn = 256;
+    else if (N >= 128 && mt * ((N + 127) / 128) >= sms / 2)
+      bn = 128;
+    else
+      bn = 64;
+  }
+  // op(A) is [M,K]: transA=0 -> stored [M,K] (K-major); transA=1 -> stored [K,M] (MN-major).
+  // op(B) is [K,N]: transB=0 -> stored [K,N] (MN-major); transB=1 -> stored [N,K] (K-major).
+  const bool a_mn = transA != 0;
+  const bool b_mn = transB == 0;
+  CUtensorMap ta, tb;
+  int rc;
+  if (!a_mn)
+    rc = make_tmap(&ta, A, K, M, lda, TC_BM);
+  else
+    rc = make_tmap(&ta, A, M, K, lda, TC_BK);
+  if (rc) return rc;
+  if (!b_mn)
+    rc = make_tmap(&tb, B, K, N, ldb, bn);
+  else
+    rc = make_tmap(&tb, B, N, K, ldb, TC_BK);
+  if (rc) return rc;
+  TcEpi ep{C, ldc, static_cast<const float*>(bias), aux, ldaux, aux_out, ldaux_out,
+           static_cast<int>(M), static_cast<int>(N), epi, out_f32};
+  switch (bn) {
+    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, (int)M, (int)N, (int)K, ep, st);
+    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, (int)M, (int)N, (int)K, ep, st);
+    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, (int)M, (int)N, (int)K, ep, st);
+    default: set_error("gemm: bad tile width %d", bn); return PC_ERR_ARG;
+  }
+}
+
+}  // namespace pp200
+
+extern "C" int pc_gemm_set_tile_n(int bn) {
+  if (bn != 0 && bn != 64 && bn != 128 && bn != 256) {
+    pp200::set_error("tile width must be 0, 64, 128 or 256");
+    return PC_ERR_ARG;
+  }
+  pp200::g_force_bn = bn;
+  return PC_OK;
+}

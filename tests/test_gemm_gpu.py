@@ -1,0 +1,117 @@
+"""GEMM numerics through the C-ABI (pc_gemm) against a torch fp32/fp64 reference.
+
+Covers every operand-major combination of the tcgen05 bf16 kernel (the
+reference's explicit transposes, ir.py:519-529, become majors), ragged
+shapes that exercise TMA out-of-bounds fill and epilogue guards, every tile
+width, and each fused epilogue.
+"""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2412_14374_b200 import _lib  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = a.double()
+    b = b.double()
+    scale = max(a.abs().max().item(), b.abs().max().item(), 1e-30)
+    return (a - b).abs().max().item() / scale
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+def run_gemm(A, B, ta, tb, M, N, K, out_dtype, epi=0, bias=None, aux=None, aux_out=None, C=None):
+    dev = A.device
+    dt_in = {torch.bfloat16: _lib.PC_BF16, torch.float32: _lib.PC_F32,
+             torch.float64: _lib.PC_F64}[A.dtype]
+    dt_out = {torch.bfloat16: _lib.PC_BF16, torch.float32: _lib.PC_F32,
+              torch.float64: _lib.PC_F64}[out_dtype]
+    if C is None:
+        C = torch.empty(M, N, dtype=out_dtype, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("pc_gemm", dt_in, dt_out, ta, tb, M, N, K, _ptr(A), A.stride(0), _ptr(B),
+              B.stride(0), _ptr(C), C.stride(0), epi, _ptr(bias), _ptr(aux),
+              aux.stride(0) if aux is not None else 0, _ptr(aux_out),
+              aux_out.stride(0) if aux_out is not None else 0, st)
+    return C
+
+
+def make_operands(M, N, K, ta, tb, dtype, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = torch.randn((K, M) if ta else (M, K), device="cuda", generator=g).to(dtype)
+    B = torch.randn((N, K) if tb else (K, N), device="cuda", generator=g).to(dtype)
+    opA = A.double().t() if ta else A.double()
+    opB = B.double().t() if tb else B.double()
+    return A, B, opA @ opB
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (200, 136, 72), (1024, 768, 768)])
+def test_bf16_tcgen05_majors(ta, tb, bn, shape):
+    M, N, K = shape
+    A, B, ref = make_operands(M, N, K, ta, tb, torch.bfloat16)
+    _lib.call("pc_gemm_set_tile_n", bn)
+    try:
+        C32 = run_gemm(A, B, ta, tb, M, N, K, torch.float32)
+        C16 = run_gemm(A, B, ta, tb, M, N, K, torch.bfloat16)
+    finally:
+        _lib.call("pc_gemm_set_tile_n", 0)
+    torch.cuda.synchronize()
+    assert rel(C32, ref) < 1e-5
+    assert rel(C16, ref) < 1e-2
+
+
+def test_bf16_large_persistent():
+    M, N, K = 8192, 2304, 768
+    A, B, ref = make_operands(M, N, K, 0, 1, torch.bfloat16, seed=3)
+    C = run_gemm(A, B, 0, 1, M, N, K, torch.float32)
+    torch.cuda.synchronize()
+    assert rel(C, ref) < 1e-5
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.float64, 1e-13)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_simt_gemm(dtype, tol, ta, tb):
+    M, N, K = 70, 45, 33
+    A, B, ref = make_operands(M, N, K, ta, tb, dtype, seed=1)
+    C = run_gemm(A, B, ta, tb, M, N, K, dtype)
+    torch.cuda.synchronize()
+    assert rel(C, ref) < tol
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_epilogues(dtype):
+    M, N, K = 256, 192, 128
+    A, B, ref = make_operands(M, N, K, 0, 1, dtype, seed=2)
+    out = torch.bfloat16 if dtype == torch.bfloat16 else torch.float32
+    tol = 2e-2 if dtype == torch.bfloat16 else 1e-5
+    bias = torch.randn(N, device="cuda", dtype=torch.float32)
+    pre = torch.empty(M, N, device="cuda", dtype=out)
+    C = run_gemm(A, B, 0, 1, M, N, K, out, epi=_lib.EPI_BIAS | _lib.EPI_GELU, bias=bias,
+                 aux_out=pre)
+    z = ref + bias.double()
+    assert rel(pre, z) < tol
+    assert rel(C, torch.nn.functional.gelu(z, approximate="tanh")) < tol
+    aux = torch.randn(M, N, device="cuda").to(out)
+    C = run_gemm(A, B, 0, 1, M, N, K, out, epi=_lib.EPI_RESIDUAL, aux=aux)
+    assert rel(C, ref + aux.double()) < tol
+    u = aux.double().requires_grad_(True)
+    gelu_u = torch.nn.functional.gelu(u, approximate="tanh")
+    (dgelu,) = torch.autograd.grad(gelu_u.sum(), u)
+    C = run_gemm(A, B, 0, 1, M, N, K, out, epi=_lib.EPI_GELU_GRAD, aux=aux)
+    assert rel(C, ref * dgelu) < tol
+    C = run_gemm(A, B, 0, 1, M, N, K, out, epi=_lib.EPI_RELU, aux_out=pre)
+    assert rel(C, ref.clamp_min(0)) < tol
+    C = run_gemm(A, B, 0, 1, M, N, K, out, epi=_lib.EPI_RELU_GRAD, aux=aux)
+    assert rel(C, ref * (aux.double() > 0)) < tol
+    acc = torch.randn(M, N, device="cuda", dtype=torch.float32)
+    want = acc.double() + ref
+    run_gemm(A, B, 0, 1, M, N, K, torch.float32, epi=_lib.EPI_ACCUM, C=acc)
+    torch.cuda.synchronize()
+    assert rel(acc, want) < (1e-5 if dtype != torch.bfloat16 else 1e-5)
