@@ -66,6 +66,70 @@ int pc_gemm(int dtype_in, int dtype_out, int transA, int transB, int64_t M, int6
 /* Force the tcgen05 GEMM tile width (0 = heuristic, else 64/128/256). Test hook. */
 int pc_gemm_set_tile_n(int bn);
 
+/* ---- elementwise / reductions (executor.py:59-96 numpy expressions) ---- */
+enum pc_ewise_op {
+  PC_EW_ADD = 1,      /* out = a + b      ("add", executor.py:68-69; grad-merge add :335-336) */
+  PC_EW_MUL = 2,      /* out = a * b      ("scale"/"mul", :76-77, :86-87); b_n==1 broadcasts */
+  PC_EW_RELU = 3,     /* out = max(a, 0)  (:70-71)                                         */
+  PC_EW_RELU_GRAD = 4 /* out = a * (b>0)  (:88-90)                                         */
+};
+int pc_fill(int dtype, int64_t n, double value, void* out, void* stream);
+int pc_ewise(int op, int dtype, int64_t n, const void* a, const void* b, int64_t b_n, void* out,
+             void* stream);
+/* *out = 0.5 * sum(x*x): "sub-sample-loss" (executor.py:72-75); deterministic. */
+int pc_sumsq_half(int dtype, int64_t n, const void* x, void* out, void* stream);
+int pc_sum_f32(int64_t n, const float* x, float* out, void* stream);
+/* out[c] (+)= sum_r x[r,c]: "sum-to" (executor.py:50-56) and bias gradients. */
+int pc_col_sum(int dtype_in, int dtype_out, int64_t rows, int64_t cols, const void* x,
+               int64_t ldx, void* out, int accumulate, void* stream);
+/* dst = src or src^T (slice / concat / broadcast materialisation, :78-95). */
+int pc_copy2d(int dtype, int64_t rows, int64_t cols, const void* src, int64_t lds, int trans,
+              void* dst, int64_t ldd, void* stream);
+/* acc += part in place: the fused fp32 gradient accumulator replacing the
+ * grad-merge chain (taskgraph.py:369-433, executor.py:335-336). */
+int pc_accumulate(int dtype_acc, int dtype_part, int64_t n, void* acc, const void* part,
+                  void* stream);
+/* w_out = w - lr*g (executor.py:340-344); optional bf16 shadow copy of w_out. */
+int pc_sgd_update(int dtype, int64_t n, const void* w, const void* g, double lr, void* w_out,
+                  void* shadow_bf16, void* stream);
+int pc_cast(int dtype_in, int dtype_out, int64_t n, const void* in, void* out, void* stream);
+
+/* ---- GPT vocabulary (oracle/gpt.py semantics; no reference counterpart) ---- */
+int pc_layernorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const float* gamma,
+                     const float* beta, void* y, float* mean, float* rstd, float eps,
+                     void* stream);
+/* dx = dres + LN_bwd(dy); dgamma, dbeta written (fp32). dres may be NULL. */
+int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
+                     const float* gamma, const float* mean, const float* rstd, const void* dres,
+                     void* dx, float* dgamma, float* dbeta, void* stream);
+int pc_embedding_fwd(int dtype, int64_t T, int64_t d, int64_t seq, const int32_t* tokens,
+                     const float* wte, const float* wpe, void* out, void* stream);
+int pc_embedding_bwd_workspace_bytes(int64_t T, int64_t* bytes);
+int pc_embedding_bwd(int dtype, int64_t T, int64_t d, int64_t seq, int64_t vocab,
+                     const int32_t* tokens, const void* dh, float* dwte, float* dwpe,
+                     void* workspace, int64_t ws_bytes, void* stream);
+/* Next-token cross-entropy per row (targets = tokens shifted by one inside each
+ * sequence); overwrites logits with dlogits = softmax - onehot. */
+int pc_xent_fwd_bwd(int dtype, int64_t rows, int64_t V, int64_t seq, void* logits, int64_t ld,
+                    const int32_t* tokens, float* row_loss, void* stream);
+/* Causal attention over packed qkv [B*S, ld_qkv]; lse/delta are [B,H,S] fp32. */
+int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const void* qkv, int64_t ld_qkv,
+                     void* o, int64_t ld_o, float* lse, void* stream);
+int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const void* qkv, int64_t ld_qkv,
+                     const void* o, const void* dO, int64_t ld_o, const float* lse, float* delta,
+                     void* dqkv, int64_t ld_dqkv, void* stream);
+/* 0 = auto (tensor-core path for bf16 when supported), 1 = force exact SIMT. Test hook. */
+int pc_attention_set_impl(int impl);
+
+/* ---- inter-stage transport (Channel, executor.py:201-254) over NCCL ---- */
+int pc_p2p_available(void);
+int pc_p2p_unique_id(void* out128);
+int pc_p2p_comm_init(void** comm, int nranks, const void* id128, int rank);
+int pc_p2p_send(void* comm, const void* buf, int64_t bytes, int peer, void* stream);
+int pc_p2p_recv(void* comm, void* buf, int64_t bytes, int peer, void* stream);
+int pc_p2p_abort(void* comm);
+int pc_p2p_destroy(void* comm);
+
 #ifdef __cplusplus
 }
 #endif

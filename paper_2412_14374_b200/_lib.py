@@ -37,7 +37,37 @@ SIGNATURES: dict[str, list] = {
     "pc_gemm": [_c_i, _c_i, _c_i, _c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64,
                 _c_p, _c_i64, _c_i, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p],
     "pc_gemm_set_tile_n": [_c_i],
+    "pc_fill": [_c_i, _c_i64, _c_d, _c_p, _c_p],
+    "pc_ewise": [_c_i, _c_i, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p],
+    "pc_sumsq_half": [_c_i, _c_i64, _c_p, _c_p, _c_p],
+    "pc_sum_f32": [_c_i64, _c_p, _c_p, _c_p],
+    "pc_col_sum": [_c_i, _c_i, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i, _c_p],
+    "pc_copy2d": [_c_i, _c_i64, _c_i64, _c_p, _c_i64, _c_i, _c_p, _c_i64, _c_p],
+    "pc_accumulate": [_c_i, _c_i, _c_i64, _c_p, _c_p, _c_p],
+    "pc_sgd_update": [_c_i, _c_i64, _c_p, _c_p, _c_d, _c_p, _c_p, _c_p],
+    "pc_cast": [_c_i, _c_i, _c_i64, _c_p, _c_p, _c_p],
+    "pc_layernorm_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_f, _c_p],
+    "pc_layernorm_bwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                         _c_p, _c_p],
+    "pc_embedding_fwd": [_c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p],
+    "pc_embedding_bwd_workspace_bytes": [_c_i64, ctypes.POINTER(_c_i64)],
+    "pc_embedding_bwd": [_c_i, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                         _c_i64, _c_p],
+    "pc_xent_fwd_bwd": [_c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p],
+    "pc_attention_fwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p],
+    "pc_attention_bwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p,
+                         _c_p, _c_p, _c_i64, _c_p],
+    "pc_attention_set_impl": [_c_i],
+    "pc_p2p_available": [],
+    "pc_p2p_unique_id": [_c_p],
+    "pc_p2p_comm_init": [ctypes.POINTER(_c_p), _c_i, _c_p, _c_i],
+    "pc_p2p_send": [_c_p, _c_p, _c_i64, _c_i, _c_p],
+    "pc_p2p_recv": [_c_p, _c_p, _c_i64, _c_i, _c_p],
+    "pc_p2p_abort": [_c_p],
+    "pc_p2p_destroy": [_c_p],
 }
+
+EW_ADD, EW_MUL, EW_RELU, EW_RELU_GRAD = 1, 2, 3, 4
 _RESTYPES = {"pc_last_error": ctypes.c_char_p}
 
 

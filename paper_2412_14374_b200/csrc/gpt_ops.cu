@@ -1,0 +1,343 @@
+// GPT vocabulary kernels: LayerNorm fwd/bwd, token+position embedding fwd/bwd,
+// fused next-token cross-entropy (loss + in-place dlogits).
+//
+// The reference has no GPT ops (SURVEY.md key fact 5); these implement the
+// semantics of oracle/gpt.py (layer_norm, head_loss, embedding) on B200.
+// Row-parallel kernels give one warp per row with coalesced, vectorised
+// (16 B) loads; parameter reductions (dgamma, dbeta, dwpe, dwte) use fixed
+// summation orders so every result is bitwise reproducible.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace pp200 {
+namespace {
+
+template <typename T> __device__ __forceinline__ float ldf(const T* p, int64_t i) {
+  return static_cast<float>(p[i]);
+}
+template <> __device__ __forceinline__ float ldf(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+template <typename T> __device__ __forceinline__ void stf(T* p, int64_t i, float v) {
+  p[i] = static_cast<T>(v);
+}
+template <> __device__ __forceinline__ void stf(__nv_bfloat16* p, int64_t i, float v) {
+  p[i] = __float2bfloat16_rn(v);
+}
+
+constexpr int ROWS_PER_BLOCK = 8;  // one warp per row
+
+template <typename T>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(int64_t rows, int d, const T* __restrict__ x,
+                                                     const float* __restrict__ g,
+                                                     const float* __restrict__ b, T* __restrict__ y,
+                                                     float* __restrict__ mean,
+                                                     float* __restrict__ rstd, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)ROWS_PER_BLOCK + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const T* xr = x + r * d;
+  float s = 0.f;
+  for (int c = lane; c < d; c += 32) s += ldf(xr, c);
+  const float mu = warp_sum(s) / d;
+  float v = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float t = ldf(xr, c) - mu;
+    v += t * t;
+  }
+  const float rs = rsqrtf(warp_sum(v) / d + eps);
+  T* yr = y + r * d;
+  for (int c = lane; c < d; c += 32) stf(yr, c, (ldf(xr, c) - mu) * rs * g[c] + b[c]);
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
+// dx = dres + rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)),  dxh = dy * g
+template <typename T>
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(int64_t rows, int d, const T* __restrict__ dy,
+                                                        const T* __restrict__ x,
+                                                        const float* __restrict__ g,
+                                                        const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd,
+                                                        const T* __restrict__ dres,
+                                                        T* __restrict__ dx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)ROWS_PER_BLOCK + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const T* dyr = dy + r * d;
+  const T* xr = x + r * d;
+  const float mu = mean[r], rs = rstd[r];
+  float s1 = 0.f, s2 = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float dxh = ldf(dyr, c) * g[c];
+    const float xh = (ldf(xr, c) - mu) * rs;
+    s1 += dxh;
+    s2 += dxh * xh;
+  }
+  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+  T* dxr = dx + r * d;
+  const T* rr = dres ? dres + r * d : nullptr;
+  for (int c = lane; c < d; c += 32) {
+    const float dxh = ldf(dyr, c) * g[c];
+    const float xh = (ldf(xr, c) - mu) * rs;
+    float v = rs * (dxh - m1 - xh * m2);
+    if (rr) v += ldf(rr, c);
+    stf(dxr, c, v);
+  }
+}
+
+// dgamma[c] = sum_r dy[r,c] * xh[r,c]; dbeta[c] = sum_r dy[r,c]  (fixed order)
+template <typename T>
+__global__ void __launch_bounds__(1024) ln_bwd_param_kernel(int64_t rows, int d,
+                                                            const T* __restrict__ dy,
+                                                            const T* __restrict__ x,
+                                                            const float* __restrict__ mean,
+                                                            const float* __restrict__ rstd,
+                                                            float* dgamma, float* dbeta) {
+  __shared__ float sg[32][33], sb[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  float a = 0.f, bsum = 0.f;
+  if (c < d)
+    for (int64_t r = ty; r < rows; r += 32) {
+      const float gy = ldf(dy, r * d + c);
+      a += gy * (ldf(x, r * d + c) - mean[r]) * rstd[r];
+      bsum += gy;
+    }
+  sg[ty][tx] = a;
+  sb[ty][tx] = bsum;
+  __syncthreads();
+  if (ty == 0 && c < d) {
+    float ta = 0.f, tb = 0.f;
+    for (int k = 0; k < 32; ++k) {
+      ta += sg[k][tx];
+      tb += sb[k][tx];
+    }
+    dgamma[c] = ta;
+    dbeta[c] = tb;
+  }
+}
+
+// out[t,:] = wte[tok[t],:] + wpe[t % seq,:]   (fp32 master tables)
+template <typename T>
+__global__ void __launch_bounds__(256) embed_fwd_kernel(int64_t T_, int d, int seq,
+                                                        const int32_t* __restrict__ tok,
+                                                        const float* __restrict__ wte,
+                                                        const float* __restrict__ wpe,
+                                                        T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x * (int64_t)ROWS_PER_BLOCK + (threadIdx.x >> 5);
+  if (t >= T_) return;
+  const float* a = wte + static_cast<int64_t>(tok[t]) * d;
+  const float* p = wpe + static_cast<int64_t>(t % seq) * d;
+  T* o = out + t * d;
+  for (int c = lane; c < d; c += 32) stf(o, c, a[c] + p[c]);
+}
+
+__global__ void iota_kernel(int n, int32_t* v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+// One warp per sorted position; segment heads sum their rows (ascending row
+// order from the stable sort) into dwte[token].  Rows of absent tokens are
+// zeroed beforehand.
+template <typename T>
+__global__ void __launch_bounds__(256) embed_bwd_wte_kernel(int n, int d,
+                                                            const int32_t* __restrict__ keys,
+                                                            const int32_t* __restrict__ rows,
+                                                            const T* __restrict__ dh,
+                                                            float* __restrict__ dwte) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * ROWS_PER_BLOCK + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int key = keys[i];
+  if (i > 0 && keys[i - 1] == key) return;
+  int j = i + 1;
+  while (j < n && keys[j] == key) ++j;
+  float* out = dwte + static_cast<int64_t>(key) * d;
+  for (int c = lane; c < d; c += 32) {
+    float s = 0.f;
+    for (int k = i; k < j; ++k) s += ldf(dh, static_cast<int64_t>(rows[k]) * d + c);
+    out[c] = s;
+  }
+}
+
+// dwpe[s,c] = sum_b dh[b*seq + s, c]
+template <typename T>
+__global__ void embed_bwd_wpe_kernel(int64_t T_, int d, int seq, const T* __restrict__ dh,
+                                     float* __restrict__ dwpe) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(seq) * d) return;
+  const int64_t s = i / d, c = i % d;
+  float acc = 0.f;
+  for (int64_t t = s; t < T_; t += seq) acc += ldf(dh, t * d + c);
+  dwpe[i] = acc;
+}
+
+// Per row: online (max, sum) over the vocab, loss = lse - logit[target], then
+// overwrite the row with dlogits = softmax - onehot (zeros for the last
+// position of each sequence, which has no target).
+template <typename T>
+__global__ void __launch_bounds__(512) xent_kernel(int64_t rows, int V, int seq, T* logits,
+                                                   int64_t ld, const int32_t* __restrict__ tok,
+                                                   float* __restrict__ row_loss) {
+  __shared__ float sm[32], ss[32];
+  const int64_t r = blockIdx.x;
+  T* row = logits + r * ld;
+  const bool valid = (r % seq) != seq - 1;
+  if (!valid) {
+    for (int c = threadIdx.x; c < V; c += blockDim.x) stf(row, c, 0.f);
+    if (threadIdx.x == 0) row_loss[r] = 0.f;
+    return;
+  }
+  const int target = tok[r + 1];
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float v = ldf(row, c);
+    if (v > m) {
+      s = s * __expf(m - v) + 1.f;
+      m = v;
+    } else {
+      s += __expf(v - m);
+    }
+  }
+  // warp combine
+  for (int o = 16; o > 0; o >>= 1) {
+    const float mo = __shfl_xor_sync(0xffffffffu, m, o), so = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mn = fmaxf(m, mo);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+    m = mn;
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sm[w] = m;
+    ss[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < nw ? sm[threadIdx.x] : -INFINITY;
+    s = threadIdx.x < nw ? ss[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float mo = __shfl_xor_sync(0xffffffffu, m, o), so = __shfl_xor_sync(0xffffffffu, s, o);
+      const float mn = fmaxf(m, mo);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+      m = mn;
+    }
+    if (threadIdx.x == 0) {
+      sm[0] = m;
+      ss[0] = s;
+    }
+  }
+  __syncthreads();
+  const float lse = sm[0] + logf(ss[0]);
+  __syncthreads();
+  if (threadIdx.x == 0) row_loss[r] = lse - ldf(row, target);
+  __syncthreads();
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float p = __expf(ldf(row, c) - lse);
+    stf(row, c, c == target ? p - 1.f : p);
+  }
+}
+
+}  // namespace
+}  // namespace pp200
+
+using namespace pp200;
+
+#define PP_DISPATCH_FB(dtype, T, ...)                                 \
+  switch (dtype) {                                                    \
+    case PC_F32: { using T = float; __VA_ARGS__; break; }            \
+    case PC_BF16: { using T = __nv_bfloat16; __VA_ARGS__; break; }   \
+    default: set_error("unsupported dtype %d (f32/bf16 only)", dtype); return PC_ERR_UNSUPPORTED; \
+  }
+
+static inline unsigned row_blocks(int64_t rows) {
+  return static_cast<unsigned>((rows + ROWS_PER_BLOCK - 1) / ROWS_PER_BLOCK);
+}
+
+extern "C" int pc_layernorm_fwd(int dtype, int64_t rows, int64_t d, const void* x,
+                                const float* gamma, const float* beta, void* y, float* mean,
+                                float* rstd, float eps, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= 0) return PC_OK;
+  PP_DISPATCH_FB(dtype, T, ln_fwd_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, beta, static_cast<T*>(y), mean, rstd, eps));
+  return check_launch("layernorm_fwd");
+}
+
+extern "C" int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
+                                const float* gamma, const float* mean, const float* rstd,
+                                const void* dres, void* dx, float* dgamma, float* dbeta,
+                                void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= 0) return PC_OK;
+  PP_DISPATCH_FB(dtype, T,
+    ln_bwd_dx_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
+    ln_bwd_param_kernel<T><<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), mean, rstd, dgamma, dbeta));
+  return check_launch("layernorm_bwd");
+}
+
+extern "C" int pc_embedding_fwd(int dtype, int64_t T_, int64_t d, int64_t seq,
+                                const int32_t* tokens, const float* wte, const float* wpe,
+                                void* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (T_ <= 0) return PC_OK;
+  PP_DISPATCH_FB(dtype, T, embed_fwd_kernel<T><<<row_blocks(T_), 256, 0, st>>>(T_, (int)d, (int)seq, tokens, wte, wpe, static_cast<T*>(out)));
+  return check_launch("embedding_fwd");
+}
+
+static size_t cub_sort_bytes(int n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, n);
+  return bytes;
+}
+
+extern "C" int pc_embedding_bwd_workspace_bytes(int64_t T_, int64_t* bytes) {
+  PP_CHECK_ARG(T_ > 0 && T_ < (1ll << 31), "embedding_bwd: bad token count");
+  *bytes = static_cast<int64_t>(3 * ((T_ * 4 + 255) / 256 * 256) + cub_sort_bytes((int)T_) + 256);
+  return PC_OK;
+}
+
+extern "C" int pc_embedding_bwd(int dtype, int64_t T_, int64_t d, int64_t seq, int64_t vocab,
+                                const int32_t* tokens, const void* dh, float* dwte, float* dwpe,
+                                void* workspace, int64_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t need = 0;
+  int rc = pc_embedding_bwd_workspace_bytes(T_, &need);
+  if (rc) return rc;
+  PP_CHECK_ARG(ws_bytes >= need, "embedding_bwd: workspace %lld < %lld", (long long)ws_bytes, (long long)need);
+  const int n = static_cast<int>(T_);
+  const size_t slab = (T_ * 4 + 255) / 256 * 256;
+  uint8_t* w = static_cast<uint8_t*>(workspace);
+  int32_t* vals = reinterpret_cast<int32_t*>(w);
+  int32_t* keys_out = reinterpret_cast<int32_t*>(w + slab);
+  int32_t* vals_out = reinterpret_cast<int32_t*>(w + 2 * slab);
+  void* temp = w + 3 * slab;
+  size_t temp_bytes = cub_sort_bytes(n);
+  int end_bit = 1;
+  while ((1ll << end_bit) < vocab) ++end_bit;
+  iota_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, vals);
+  if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, tokens, keys_out, vals, vals_out, n, 0,
+                                      end_bit, st) != cudaSuccess) {
+    set_error("embedding_bwd: radix sort failed");
+    return PC_ERR_CUDA;
+  }
+  PP_CUDA_TRY(cudaMemsetAsync(dwte, 0, static_cast<size_t>(vocab) * d * 4, st));
+  PP_DISPATCH_FB(dtype, T,
+    embed_bwd_wte_kernel<T><<<row_blocks(T_), 256, 0, st>>>(n, (int)d, keys_out, vals_out, static_cast<const T*>(dh), dwte);
+    embed_bwd_wpe_kernel<T><<<(unsigned)((seq * d + 255) / 256), 256, 0, st>>>(T_, (int)d, (int)seq, static_cast<const T*>(dh), dwpe));
+  return check_launch("embedding_bwd");
+}
+
+extern "C" int pc_xent_fwd_bwd(int dtype, int64_t rows, int64_t V, int64_t seq, void* logits,
+                               int64_t ld, const int32_t* tokens, float* row_loss, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= 0) return PC_OK;
+  PP_CHECK_ARG(rows % seq == 0, "xent: rows must be a multiple of seq");
+  PP_DISPATCH_FB(dtype, T, xent_kernel<T><<<(unsigned)rows, 512, 0, st>>>(rows, (int)V, (int)seq, static_cast<T*>(logits), ld, tokens, row_loss));
+  return check_launch("xent");
+}

@@ -1,0 +1,316 @@
+// Elementwise, reduction, accumulation and optimizer kernels.
+//
+// Each replaces one numpy expression of the reference interpreter:
+//   add / scale / mul        executor.py:68-69, 76-77, 86-87
+//   relu / relu-grad         executor.py:70-71, 88-90
+//   sub-sample-loss          executor.py:72-75 (0.5 * sum(h*h))
+//   sum-to                   executor.py:50-56, 90-91
+//   grad-merge `add` task    executor.py:335-336 (in-place fp32 accumulate)
+//   sgd-update               executor.py:340-344 (w - lr * g)
+// Reductions use a fixed tree order: results are bitwise reproducible.
+// fp64 paths use explicit _rn intrinsics so no FMA contraction changes the
+// rounding of the reference's separate multiply and add.
+#include "common.cuh"
+
+namespace pp200 {
+namespace {
+
+template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
+template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+
+// Compute type: double for double, float otherwise.
+template <typename T> struct Acc { using type = float; };
+template <> struct Acc<double> { using type = double; };
+
+template <typename T>
+__device__ __forceinline__ typename Acc<T>::type ldv(const T* p, int64_t i) {
+  return static_cast<typename Acc<T>::type>(p[i]);
+}
+template <>
+__device__ __forceinline__ float ldv(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+template <typename T>
+__device__ __forceinline__ void stv(T* p, int64_t i, typename Acc<T>::type v) {
+  p[i] = static_cast<T>(v);
+}
+template <>
+__device__ __forceinline__ void stv(__nv_bfloat16* p, int64_t i, float v) {
+  p[i] = __float2bfloat16_rn(v);
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<int>(b);
+}
+
+template <typename T>
+__global__ void fill_kernel(int64_t n, T v, T* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
+template <typename T>
+__global__ void ewise_kernel(int op, int64_t n, const T* __restrict__ a, const T* __restrict__ b,
+                             int64_t b_n, T* out) {
+  using C = typename Acc<T>::type;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    C x = ldv(a, i);
+    C r;
+    switch (op) {
+      case PC_EW_ADD: r = add_rn(x, ldv(b, b_n == 1 ? 0 : i)); break;
+      case PC_EW_MUL: r = mul_rn(x, ldv(b, b_n == 1 ? 0 : i)); break;
+      case PC_EW_RELU: r = x > C(0) ? x : C(0); break;
+      case PC_EW_RELU_GRAD: r = ldv(b, i) > C(0) ? x : C(0) * x; break;
+      default: r = x; break;
+    }
+    stv(out, i, r);
+  }
+}
+
+// 0.5 * sum(x*x) with one 1024-thread block and a fixed reduction tree.
+template <typename T>
+__global__ void __launch_bounds__(1024) sumsq_half_kernel(int64_t n, const T* __restrict__ x,
+                                                          T* out) {
+  using C = typename Acc<T>::type;
+  __shared__ C part[32];
+  C s = C(0);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    C v = ldv(x, i);
+    s = add_rn(s, mul_rn(v, v));
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    C v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : C(0);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) stv(out, 0, mul_rn(C(0.5), v));
+  }
+}
+
+// Sum of n floats into *out (deterministic; loss reduction).
+__global__ void __launch_bounds__(1024) sum_f32_kernel(int64_t n, const float* __restrict__ x,
+                                                       float* out) {
+  __shared__ float part[32];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *out = v;
+  }
+}
+
+// out[c] = sum_r x[r, c]: one block per 32 columns, 32 row lanes, fixed order.
+template <typename T, typename O>
+__global__ void __launch_bounds__(1024) col_sum_kernel(int64_t rows, int64_t cols,
+                                                       const T* __restrict__ x, int64_t ldx,
+                                                       O* out, int accumulate) {
+  using C = typename Acc<T>::type;
+  __shared__ C sm[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32ll + tx;
+  C s = C(0);
+  if (c < cols)
+    for (int64_t r = ty; r < rows; r += 32) s = add_rn(s, ldv(x, r * ldx + c));
+  sm[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    C t = C(0);
+    for (int k = 0; k < 32; ++k) t = add_rn(t, sm[k][tx]);
+    if (accumulate) t = add_rn(t, static_cast<C>(out[c]));
+    out[c] = static_cast<O>(t);
+  }
+}
+
+template <typename T>
+__global__ void copy2d_kernel(int64_t rows, int64_t cols, const T* __restrict__ src, int64_t lds,
+                              int trans, T* __restrict__ dst, int64_t ldd) {
+  // dst[r, c] = trans ? src[c, r] : src[r, c]
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * ldd + c] = trans ? src[c * lds + r] : src[r * lds + c];
+  }
+}
+
+// acc[i] += part[i]; acc fp32/fp64, part same or bf16.  Vectorised for fp32.
+template <typename A, typename P>
+__global__ void accumulate_kernel(int64_t n, A* __restrict__ acc, const P* __restrict__ part) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc[i] = add_rn(acc[i], static_cast<A>(ldv(part, i)));
+}
+__global__ void accumulate_f32x4_kernel(int64_t n4, float4* __restrict__ acc,
+                                        const float4* __restrict__ part) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = acc[i], b = part[i];
+    a.x = __fadd_rn(a.x, b.x); a.y = __fadd_rn(a.y, b.y);
+    a.z = __fadd_rn(a.z, b.z); a.w = __fadd_rn(a.w, b.w);
+    acc[i] = a;
+  }
+}
+
+// w_out = w - lr*g (product rounded first, as numpy does); optional bf16 shadow.
+template <typename T>
+__global__ void sgd_kernel(int64_t n, const T* __restrict__ w, const T* __restrict__ g, T lr,
+                           T* w_out, __nv_bfloat16* shadow) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T v = add_rn(w[i], -mul_rn(lr, g[i]));
+    w_out[i] = v;
+    if (shadow) shadow[i] = __float2bfloat16_rn(static_cast<float>(v));
+  }
+}
+
+template <typename I, typename O>
+__global__ void cast_kernel(int64_t n, const I* __restrict__ in, O* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    stv(out, i, static_cast<typename Acc<O>::type>(ldv(in, i)));
+}
+
+}  // namespace
+}  // namespace pp200
+
+using namespace pp200;
+
+#define PP_DISPATCH3(dtype, T, ...)                                   \
+  switch (dtype) {                                                    \
+    case PC_F32: { using T = float; __VA_ARGS__; break; }            \
+    case PC_F64: { using T = double; __VA_ARGS__; break; }           \
+    case PC_BF16: { using T = __nv_bfloat16; __VA_ARGS__; break; }   \
+    default: set_error("unsupported dtype %d", dtype); return PC_ERR_UNSUPPORTED; \
+  }
+
+extern "C" int pc_fill(int dtype, int64_t n, double value, void* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n <= 0) return PC_OK;
+  PP_DISPATCH3(dtype, T, fill_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(n, static_cast<T>(static_cast<float>(value)), static_cast<T*>(out)));
+  return check_launch("fill");
+}
+
+extern "C" int pc_ewise(int op, int dtype, int64_t n, const void* a, const void* b, int64_t b_n,
+                        void* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n <= 0) return PC_OK;
+  PP_CHECK_ARG(op >= PC_EW_ADD && op <= PC_EW_RELU_GRAD, "ewise: bad op %d", op);
+  PP_CHECK_ARG(op == PC_EW_RELU || b != nullptr, "ewise: missing second operand");
+  PP_DISPATCH3(dtype, T, ewise_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(op, n, static_cast<const T*>(a), static_cast<const T*>(b), b_n, static_cast<T*>(out)));
+  return check_launch("ewise");
+}
+
+extern "C" int pc_sumsq_half(int dtype, int64_t n, const void* x, void* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PP_DISPATCH3(dtype, T, sumsq_half_kernel<T><<<1, 1024, 0, st>>>(n, static_cast<const T*>(x), static_cast<T*>(out)));
+  return check_launch("sumsq_half");
+}
+
+extern "C" int pc_sum_f32(int64_t n, const float* x, float* out, void* stream) {
+  sum_f32_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, x, out);
+  return check_launch("sum_f32");
+}
+
+extern "C" int pc_col_sum(int dtype_in, int dtype_out, int64_t rows, int64_t cols, const void* x,
+                          int64_t ldx, void* out, int accumulate, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cols <= 0) return PC_OK;
+  dim3 grid(static_cast<unsigned>((cols + 31) / 32));
+  if (dtype_in == PC_BF16 && dtype_out == PC_F32) {
+    col_sum_kernel<__nv_bfloat16, float><<<grid, 1024, 0, st>>>(rows, cols, static_cast<const __nv_bfloat16*>(x), ldx, static_cast<float*>(out), accumulate);
+  } else if (dtype_in == PC_F32 && dtype_out == PC_F32) {
+    col_sum_kernel<float, float><<<grid, 1024, 0, st>>>(rows, cols, static_cast<const float*>(x), ldx, static_cast<float*>(out), accumulate);
+  } else if (dtype_in == PC_F64 && dtype_out == PC_F64) {
+    col_sum_kernel<double, double><<<grid, 1024, 0, st>>>(rows, cols, static_cast<const double*>(x), ldx, static_cast<double*>(out), accumulate);
+  } else {
+    set_error("col_sum: unsupported dtypes %d->%d", dtype_in, dtype_out);
+    return PC_ERR_UNSUPPORTED;
+  }
+  return check_launch("col_sum");
+}
+
+extern "C" int pc_copy2d(int dtype, int64_t rows, int64_t cols, const void* src, int64_t lds,
+                         int trans, void* dst, int64_t ldd, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= 0 || cols <= 0) return PC_OK;
+  if (dtype == PC_I32) {
+    copy2d_kernel<int32_t><<<grid_for(rows * cols, 256), 256, 0, st>>>(rows, cols, static_cast<const int32_t*>(src), lds, trans, static_cast<int32_t*>(dst), ldd);
+    return check_launch("copy2d");
+  }
+  PP_DISPATCH3(dtype, T, copy2d_kernel<T><<<grid_for(rows * cols, 256), 256, 0, st>>>(rows, cols, static_cast<const T*>(src), lds, trans, static_cast<T*>(dst), ldd));
+  return check_launch("copy2d");
+}
+
+extern "C" int pc_accumulate(int dtype_acc, int dtype_part, int64_t n, void* acc, const void* part,
+                             void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n <= 0) return PC_OK;
+  if (dtype_acc == PC_F32 && dtype_part == PC_F32) {
+    const bool vec = (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(part)) & 15) == 0;
+    if (vec)
+      accumulate_f32x4_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(n / 4, static_cast<float4*>(acc), static_cast<const float4*>(part));
+    else
+      accumulate_kernel<float, float><<<grid_for(n, 256), 256, 0, st>>>(n, static_cast<float*>(acc), static_cast<const float*>(part));
+  } else if (dtype_acc == PC_F32 && dtype_part == PC_BF16) {
+    accumulate_kernel<float, __nv_bfloat16><<<grid_for(n, 256), 256, 0, st>>>(n, static_cast<float*>(acc), static_cast<const __nv_bfloat16*>(part));
+  } else if (dtype_acc == PC_F64 && dtype_part == PC_F64) {
+    accumulate_kernel<double, double><<<grid_for(n, 256), 256, 0, st>>>(n, static_cast<double*>(acc), static_cast<const double*>(part));
+  } else {
+    set_error("accumulate: unsupported dtypes %d += %d", dtype_acc, dtype_part);
+    return PC_ERR_UNSUPPORTED;
+  }
+  return check_launch("accumulate");
+}
+
+extern "C" int pc_sgd_update(int dtype, int64_t n, const void* w, const void* g, double lr,
+                             void* w_out, void* shadow_bf16, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n <= 0) return PC_OK;
+  if (dtype == PC_F32)
+    sgd_kernel<float><<<grid_for(n, 256), 256, 0, st>>>(n, static_cast<const float*>(w), static_cast<const float*>(g), static_cast<float>(lr), static_cast<float*>(w_out), static_cast<__nv_bfloat16*>(shadow_bf16));
+  else if (dtype == PC_F64)
+    sgd_kernel<double><<<grid_for(n, 256), 256, 0, st>>>(n, static_cast<const double*>(w), static_cast<const double*>(g), lr, static_cast<double*>(w_out), static_cast<__nv_bfloat16*>(shadow_bf16));
+  else {
+    set_error("sgd: master weights must be f32/f64");
+    return PC_ERR_UNSUPPORTED;
+  }
+  return check_launch("sgd");
+}
+
+extern "C" int pc_cast(int dtype_in, int dtype_out, int64_t n, const void* in, void* out,
+                       void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n <= 0) return PC_OK;
+  const int g = grid_for(n, 256);
+#define PP_CAST(I, O) cast_kernel<I, O><<<g, 256, 0, st>>>(n, static_cast<const I*>(in), static_cast<O*>(out))
+  if (dtype_in == PC_F32 && dtype_out == PC_BF16) PP_CAST(float, __nv_bfloat16);
+  else if (dtype_in == PC_BF16 && dtype_out == PC_F32) PP_CAST(__nv_bfloat16, float);
+  else if (dtype_in == PC_F64 && dtype_out == PC_F32) PP_CAST(double, float);
+  else if (dtype_in == PC_F32 && dtype_out == PC_F64) PP_CAST(float, double);
+  else if (dtype_in == PC_F64 && dtype_out == PC_BF16) PP_CAST(double, __nv_bfloat16);
+  else if (dtype_in == dtype_out) {
+    size_t es = dtype_in == PC_F64 ? 8 : dtype_in == PC_BF16 ? 2 : 4;
+    PP_CUDA_TRY(cudaMemcpyAsync(out, in, n * es, cudaMemcpyDeviceToDevice, st));
+    return PC_OK;
+  } else {
+    set_error("cast: unsupported %d->%d", dtype_in, dtype_out);
+    return PC_ERR_UNSUPPORTED;
+  }
+#undef PP_CAST
+  return check_launch("cast");
+}

@@ -1,0 +1,606 @@
+"""Stage compute on one B200: the GPU counterpart of the reference's op
+interpreter (``eval_op``/``evaluate_ops``, pkg/src/pipecraft/executor.py:59-103)
+and task payloads (``_run_task``, executor.py:316-346).
+
+Every op is a libpp200 launch on the actor's compute stream (no host sync, no
+torch compute kernels; torch only allocates memory).  Values are device
+tensors; a transposed value is a zero-copy view that becomes a GEMM operand
+major; ``Act`` carries the saved-for-backward tensors an op attaches to its
+first operand (the stash keeps that value alive, exactly the reference's stash
+dict, executor.py:326-327).
+
+Compute modes
+  fp64  float64 everywhere (FFN oracle mode: the reference's own 1e-12 tests)
+  fp32  float32, FFMA GEMMs (no TF32), fp32 parity mode (rtol 1e-5)
+  bf16  bf16 activations, tcgen05 GEMMs with fp32 accumulation, fp32 master
+        params + bf16 shadow, fp32 gradients and accumulators (rtol 2e-2)
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+from .ir import GPTConfig, OpNode, StagePartition, layout_size
+
+LN_EPS = 1e-5
+
+_PC = {torch.float32: _lib.PC_F32, torch.float64: _lib.PC_F64, torch.bfloat16: _lib.PC_BF16,
+       torch.int32: _lib.PC_I32}
+
+
+@dataclass(frozen=True)
+class Mode:
+    name: str
+    act: torch.dtype       # activations / activation gradients
+    master: torch.dtype    # parameters and parameter gradients
+
+    @property
+    def pc_act(self) -> int:
+        return _PC[self.act]
+
+    @property
+    def pc_master(self) -> int:
+        return _PC[self.master]
+
+
+MODES = {
+    "fp64": Mode("fp64", torch.float64, torch.float64),
+    "fp32": Mode("fp32", torch.float32, torch.float32),
+    "bf16": Mode("bf16", torch.bfloat16, torch.float32),
+}
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class Trans:
+    """Lazy transpose of a 2-D value (reference `transpose`, executor.py:78-79)."""
+
+    __slots__ = ("base",)
+
+    def __init__(self, base):
+        self.base = base
+
+
+class Act:
+    """A device activation plus tensors saved for backward, keyed by op id."""
+
+    __slots__ = ("t", "saved")
+
+    def __init__(self, t: torch.Tensor):
+        self.t = t
+        self.saved: dict = {}
+
+
+@dataclass
+class Param:
+    """A parameter as stored on an actor: fp32 master (+ bf16 shadow in bf16 mode)."""
+
+    master: torch.Tensor
+    shadow: torch.Tensor | None = None
+
+    def compute(self) -> torch.Tensor:
+        return self.shadow if self.shadow is not None else self.master
+
+
+def tensor_of(v) -> torch.Tensor:
+    if isinstance(v, Act):
+        return v.t
+    if isinstance(v, Param):
+        return v.compute()
+    if isinstance(v, Trans):
+        raise TypeError("transposed view used where a tensor is required")
+    return v
+
+
+def strip(v):
+    """The wire form of a value: what crosses a channel (no saved state)."""
+    if isinstance(v, Act):
+        return v.t
+    return v
+
+
+@dataclass
+class _StagePlan:
+    fused_into_prev: set = field(default_factory=set)     # op indices skipped
+    epilogue: dict = field(default_factory=dict)          # op index -> (kind, partner idx)
+
+
+class DeviceOps:
+    """Executes stage programs and task payloads for one actor on one device."""
+
+    def __init__(self, p: StagePartition, mode: Mode, device: torch.device,
+                 stream: torch.cuda.Stream, gpt: GPTConfig | None = None):
+        self.p = p
+        self.mode = mode
+        self.device = device
+        self.stream = stream
+        self.gpt = gpt
+        self._plans: dict[int, _StagePlan] = {}
+        self._consumers = {}
+        for op in p.graph.ops:
+            for v in op.operands:
+                self._consumers.setdefault(v, []).append(op)
+        self._stage_outputs = set()
+        for bp in p.bwd_programs:
+            self._stage_outputs.update(bp.grads_out)
+        for fp in p.fwd_programs:
+            self._stage_outputs.update(fp.boundary_out)
+            self._stage_outputs.update(fp.stash)
+        if gpt is not None:
+            self._elay = gpt.embed_layout()
+            self._blay = {False: gpt.block_layout(False), True: gpt.block_layout(True)}
+        self._emb_ws = None
+
+    # ------------------------------------------------------------------ alloc
+    def empty(self, shape, dtype) -> torch.Tensor:
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def zeros(self, shape, dtype) -> torch.Tensor:
+        t = self.empty(shape, dtype)
+        call("pc_fill", _PC[dtype], t.numel(), 0.0, t.data_ptr(), self.st)
+        return t
+
+    @property
+    def st(self) -> int:
+        return self.stream.cuda_stream
+
+    # ---------------------------------------------------------- stage programs
+    def run_ops(self, ops: list[OpNode], env: dict) -> dict:
+        plan = self._plan(ops)
+        for k, op in enumerate(ops):
+            if k in plan.fused_into_prev:
+                continue
+            self._eval(op, env, k, ops, plan)
+        return env
+
+    def _plan(self, ops: list[OpNode]) -> _StagePlan:
+        """Peephole fusion over one stage program: matmul -> relu becomes one
+        GEMM with a ReLU epilogue; a dX matmul whose only consumer is a
+        relu-grad becomes one GEMM with a relu-grad epilogue."""
+        key = id(ops)
+        plan = self._plans.get(key)
+        if plan is not None:
+            return plan
+        plan = _StagePlan()
+        idx = {op.result: k for k, op in enumerate(ops)}
+        for k, op in enumerate(ops):
+            if op.kind != "matmul":
+                continue
+            users = self._consumers.get(op.result, [])
+            local = [u for u in users if u.result in idx and idx[u.result] > k]
+            relu = [u for u in local if u.kind == "relu"]
+            if relu:
+                # z stays materialised (aux_out), so other readers are fine.
+                j = idx[relu[0].result]
+                plan.epilogue[k] = ("relu", j)
+                plan.fused_into_prev.add(j)
+                continue
+            if len(users) != 1 or not local or op.result in self._stage_outputs:
+                continue
+            u = local[0]
+            if u.kind == "relu-grad" and u.operands[0] == op.result and u.operands[1] != op.result:
+                aux_src = u.operands[1]
+                # the mask operand must already exist when the matmul runs
+                if aux_src not in idx or idx[aux_src] < k:
+                    plan.epilogue[k] = ("relu-grad", idx[u.result])
+                    plan.fused_into_prev.add(idx[u.result])
+        self._plans[key] = plan
+        return plan
+
+    def _eval(self, op: OpNode, env: dict, k: int, ops, plan: _StagePlan):
+        kind = op.kind
+        if kind in ("parameter-read", "input-read"):
+            if op.result not in env:
+                raise KeyError(f"{kind} {op.id}: value {op.result} was not fed")
+            return
+        a = env[op.operands[0]] if op.operands else None
+        if kind == "yield-marker":
+            env[op.result] = a
+        elif kind == "transpose":
+            env[op.result] = a.base if isinstance(a, Trans) else Trans(a)
+        elif kind == "matmul":
+            self._matmul(op, env, plan.epilogue.get(k), ops)
+        elif kind == "relu":
+            x = tensor_of(a)
+            out = self.empty(x.shape, x.dtype)
+            call("pc_ewise", _lib.EW_RELU, _PC[x.dtype], x.numel(), x.data_ptr(), None, 0,
+                 out.data_ptr(), self.st)
+            env[op.result] = out
+        elif kind == "relu-grad":
+            x, z = tensor_of(a), tensor_of(env[op.operands[1]])
+            out = self.empty(x.shape, x.dtype)
+            call("pc_ewise", _lib.EW_RELU_GRAD, _PC[x.dtype], x.numel(), x.data_ptr(),
+                 z.data_ptr(), z.numel(), out.data_ptr(), self.st)
+            env[op.result] = out
+        elif kind in ("add", "scale", "mul"):
+            x, y = tensor_of(a), tensor_of(env[op.operands[1]])
+            out = self.empty(x.shape, x.dtype)
+            opc = _lib.EW_ADD if kind == "add" else _lib.EW_MUL
+            call("pc_ewise", opc, _PC[x.dtype], x.numel(), x.data_ptr(), y.data_ptr(), y.numel(),
+                 out.data_ptr(), self.st)
+            env[op.result] = out
+        elif kind == "sub-sample-loss":
+            x = tensor_of(a)
+            out = self.empty((), x.dtype)
+            call("pc_sumsq_half", _PC[x.dtype], x.numel(), x.data_ptr(), out.data_ptr(), self.st)
+            env[op.result] = out
+        elif kind == "sum-to":
+            env[op.result] = self._sum_to(tensor_of(a), op.result_spec.dims)
+        elif kind == "broadcast":
+            env[op.result] = self._broadcast(tensor_of(a), op.result_spec.dims)
+        elif kind == "slice":
+            x = tensor_of(a)
+            off, ln = op.attr("offset"), op.attr("length")
+            env[op.result] = x.reshape(-1)[off:off + ln] if x.dim() == 1 else x[off:off + ln]
+        elif kind == "concat":
+            env[op.result] = self._concat([tensor_of(env[v]) for v in op.operands])
+        elif kind == "tuple-get":
+            env[op.result] = a[op.attr("index")]
+        elif kind == "embed":
+            env[op.result] = Act(self._embed(env))
+        elif kind == "gpt-block":
+            self._block_fwd(op, env)
+        elif kind == "gpt-block-grad":
+            env[op.result] = self._block_bwd(op, env)
+        elif kind == "lmhead-xent":
+            env[op.result] = self._head_fwd(op, env)
+        elif kind == "lmhead-xent-grad":
+            env[op.result] = self._head_bwd(op, env)
+        elif kind == "embed-grad":
+            env[op.result] = self._embed_bwd(op, env)
+        else:
+            raise ValueError(f"no device rule for op kind {kind!r}")
+
+    # ------------------------------------------------------------- FFN pieces
+    @staticmethod
+    def _operand(v):
+        if isinstance(v, Trans):
+            t = tensor_of(v.base)
+            return t, 1, t.shape[1], t.shape[0]  # op(A) = A^T: rows = cols of base
+        t = tensor_of(v)
+        return t, 0, t.shape[0], t.shape[1]
+
+    def _matmul(self, op: OpNode, env: dict, fuse, ops):
+        A, ta, m, ka = self._operand(env[op.operands[0]])
+        B, tb, kb, n = self._operand(env[op.operands[1]])
+        if ka != kb:
+            raise ValueError(f"matmul {op.id}: inner dims {ka} != {kb}")
+        if not A.is_contiguous() or not B.is_contiguous():
+            A, B = A.contiguous(), B.contiguous()
+        dt = A.dtype
+        out = self.empty((m, n), dt)
+        epi, aux, aux_out = 0, None, None
+        if fuse is not None:
+            tag, j = fuse
+            partner = ops[j]
+            if tag == "relu":
+                epi, aux_out = _lib.EPI_RELU, self.empty((m, n), dt)
+            else:
+                epi, aux = _lib.EPI_RELU_GRAD, tensor_of(env[partner.operands[1]])
+        call("pc_gemm", _PC[dt], _PC[dt], ta, tb, m, n, ka, A.data_ptr(), A.shape[1],
+             B.data_ptr(), B.shape[1], out.data_ptr(), n, epi, None, ptr(aux), n if aux is not None else 0,
+             ptr(aux_out), n if aux_out is not None else 0, self.st)
+        if fuse is None:
+            env[op.result] = out
+        elif fuse[0] == "relu":
+            env[op.result] = aux_out           # z (pre-activation)
+            env[ops[fuse[1]].result] = out     # relu(z)
+        else:
+            env[ops[fuse[1]].result] = out     # relu-grad(dX, z); dX never materialised
+
+    def _sum_to(self, x: torch.Tensor, dims) -> torch.Tensor:
+        dims = tuple(dims)
+        if tuple(x.shape) == dims:
+            return x
+        if x.dim() == 2 and (dims == (x.shape[1],) or dims == (1, x.shape[1])):
+            out = self.empty(dims, x.dtype)
+            call("pc_col_sum", _PC[x.dtype], _PC[x.dtype], x.shape[0], x.shape[1], x.data_ptr(),
+                 x.shape[1], out.data_ptr(), 0, self.st)
+            return out
+        if len(dims) == 0 or math.prod(dims) == 1:
+            out = self.empty(dims, x.dtype)
+            flat = x.reshape(1, -1) if x.is_contiguous() else x.contiguous().reshape(1, -1)
+            tmp = self.empty((flat.shape[1],), x.dtype)
+            call("pc_copy2d", _PC[x.dtype], 1, flat.shape[1], flat.data_ptr(), flat.shape[1], 0,
+                 tmp.data_ptr(), flat.shape[1], self.st)
+            col = tmp.reshape(-1, 1)
+            call("pc_col_sum", _PC[x.dtype], _PC[x.dtype], col.shape[0], 1, col.data_ptr(), 1,
+                 out.data_ptr(), 0, self.st)
+            return out
+        raise ValueError(f"sum-to {tuple(x.shape)} -> {dims} unsupported on device")
+
+    def _broadcast(self, x: torch.Tensor, dims) -> torch.Tensor:
+        dims = tuple(dims)
+        out = self.empty(dims, x.dtype)
+        if len(dims) == 2 and x.numel() == dims[1]:
+            for r in range(dims[0]):  # small; generic vocabulary only
+                call("pc_copy2d", _PC[x.dtype], 1, dims[1], x.data_ptr(), dims[1], 0,
+                     out[r].data_ptr(), dims[1], self.st)
+            return out
+        if x.numel() == 1:
+            flat = out.reshape(-1)
+            for i in range(flat.numel()):
+                call("pc_copy2d", _PC[x.dtype], 1, 1, x.data_ptr(), 1, 0, flat[i].data_ptr(), 1,
+                     self.st)
+            return out
+        raise ValueError(f"broadcast {tuple(x.shape)} -> {dims} unsupported on device")
+
+    def _concat(self, parts: list[torch.Tensor]) -> torch.Tensor:
+        rows = [p.reshape(1) if p.dim() == 0 else p for p in parts]
+        tail = rows[0].shape[1:]
+        out = self.empty((sum(r.shape[0] for r in rows), *tail), rows[0].dtype)
+        width = int(math.prod(tail)) if tail else 1
+        off = 0
+        for r in rows:
+            call("pc_copy2d", _PC[r.dtype], r.shape[0], width, r.data_ptr(), width, 0,
+                 out.data_ptr() + off * width * r.element_size(), width, self.st)
+            off += r.shape[0]
+        return out
+
+    # ------------------------------------------------------------ task payloads
+    def add(self, lhs, rhs, inplace: bool):
+        """Grad-merge `add` (executor.py:335-336).  In place into ``lhs`` when
+        the planner's chain guarantees it has no other reader."""
+        x, y = tensor_of(lhs), tensor_of(rhs)
+        if inplace and x.dtype in (torch.float32, torch.float64) and y.dtype == x.dtype:
+            call("pc_accumulate", _PC[x.dtype], _PC[y.dtype], x.numel(), x.data_ptr(),
+                 y.data_ptr(), self.st)
+            return lhs
+        out = self.empty(x.shape, x.dtype)
+        call("pc_ewise", _lib.EW_ADD, _PC[x.dtype], x.numel(), x.data_ptr(), y.data_ptr(),
+             y.numel(), out.data_ptr(), self.st)
+        return out
+
+    def concat_losses(self, parts) -> torch.Tensor:
+        return self._concat([tensor_of(p) for p in parts])
+
+    def sgd(self, w, g, lr: float):
+        """executor.py:340-344: w - lr*g (fp32/fp64 master; bf16 shadow refreshed)."""
+        if isinstance(w, Param):
+            master = w.master
+            newm = self.empty(master.shape, master.dtype)
+            shadow = self.empty(master.shape, torch.bfloat16) if w.shadow is not None else None
+            call("pc_sgd_update", _PC[master.dtype], master.numel(), master.data_ptr(),
+                 tensor_of(g).data_ptr(), float(lr), newm.data_ptr(), ptr(shadow), self.st)
+            return Param(newm, shadow)
+        wt = tensor_of(w)
+        out = self.empty(wt.shape, wt.dtype)
+        call("pc_sgd_update", _PC[wt.dtype], wt.numel(), wt.data_ptr(), tensor_of(g).data_ptr(),
+             float(lr), out.data_ptr(), None, self.st)
+        return out
+
+    # ------------------------------------------------------------- GPT pieces
+    def _slice(self, flat: torch.Tensor, layout, name):
+        off, dims = layout[name]
+        return flat[off:off + math.prod(dims)].view(*dims)
+
+    def _gemm(self, out_dtype, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, epi=0, bias=None,
+              aux=None, ldaux=0, aux_out=None, ldaux_out=0):
+        call("pc_gemm", self.mode.pc_act, _PC[out_dtype], ta, tb, M, N, K, A.data_ptr(), lda,
+             B.data_ptr(), ldb, C.data_ptr(), ldc, epi, ptr(bias), ptr(aux), ldaux, ptr(aux_out),
+             ldaux_out, self.st)
+
+    def _embed(self, env):
+        cfg = self.gpt
+        x = tensor_of(env["x"])
+        w0: Param = env["w0"]
+        T, d = cfg.tokens, cfg.d_model
+        out = self.empty((T, d), self.mode.act)
+        wte = self._slice(w0.master, self._elay, "wte")
+        wpe = self._slice(w0.master, self._elay, "wpe")
+        call("pc_embedding_fwd", self.mode.pc_act, T, d, cfg.seq_len, x.data_ptr(),
+             wte.data_ptr(), wpe.data_ptr(), out.data_ptr(), self.st)
+        return out
+
+    def _embed_bwd(self, op, env):
+        cfg = self.gpt
+        g = tensor_of(env[op.operands[0]])
+        x = tensor_of(env[op.operands[1]])
+        n = layout_size(self._elay)
+        dw = self.zeros((n,), torch.float32)
+        T, d = cfg.tokens, cfg.d_model
+        if self._emb_ws is None:
+            nb = ctypes.c_int64(0)
+            call("pc_embedding_bwd_workspace_bytes", T, ctypes.byref(nb))
+            self._emb_ws = self.empty((nb.value,), torch.uint8)
+        ws = self._emb_ws
+        call("pc_embedding_bwd", self.mode.pc_act, T, d, cfg.seq_len, cfg.vocab, x.data_ptr(),
+             g.data_ptr(), self._slice(dw, self._elay, "wte").data_ptr(),
+             self._slice(dw, self._elay, "wpe").data_ptr(), ws.data_ptr(), ws.numel(), self.st)
+        ws.record_stream(self.stream)
+        return dw
+
+    def _block_fwd(self, op, env):
+        cfg = self.gpt
+        final = bool(op.attr("final_ln"))
+        lay = self._blay[final]
+        hv = env[op.operands[0]]
+        if not isinstance(hv, Act):
+            hv = env[op.operands[0]] = Act(tensor_of(hv))
+        h = hv.t
+        w: Param = env[op.operands[1]]
+        W, Mst = w.compute(), w.master
+        T, d, f, H = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.n_heads
+        act = self.mode.act
+        sl = lambda name: self._slice(W, lay, name)
+        ms = lambda name: self._slice(Mst, lay, name)
+        a = self.empty((T, d), act)
+        mean1 = self.empty((T,), torch.float32)
+        rstd1 = self.empty((T,), torch.float32)
+        call("pc_layernorm_fwd", self.mode.pc_act, T, d, h.data_ptr(), ms("ln1_g").data_ptr(),
+             ms("ln1_b").data_ptr(), a.data_ptr(), mean1.data_ptr(), rstd1.data_ptr(), LN_EPS,
+             self.st)
+        qkv = self.empty((T, 3 * d), act)
+        self._gemm(act, 0, 1, T, 3 * d, d, a, d, sl("w_qkv"), d, qkv, 3 * d, _lib.EPI_BIAS,
+                   bias=ms("b_qkv"))
+        o = self.empty((T, d), act)
+        lse = self.empty((cfg.microbatch_size * H * cfg.seq_len,), torch.float32)
+        call("pc_attention_fwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
+             cfg.head_dim, qkv.data_ptr(), 3 * d, o.data_ptr(), d, lse.data_ptr(), self.st)
+        h1 = self.empty((T, d), act)
+        self._gemm(act, 0, 1, T, d, d, o, d, sl("w_o"), d, h1, d,
+                   _lib.EPI_BIAS | _lib.EPI_RESIDUAL, bias=ms("b_o"), aux=h, ldaux=d)
+        a2 = self.empty((T, d), act)
+        mean2 = self.empty((T,), torch.float32)
+        rstd2 = self.empty((T,), torch.float32)
+        call("pc_layernorm_fwd", self.mode.pc_act, T, d, h1.data_ptr(), ms("ln2_g").data_ptr(),
+             ms("ln2_b").data_ptr(), a2.data_ptr(), mean2.data_ptr(), rstd2.data_ptr(), LN_EPS,
+             self.st)
+        u = self.empty((T, f), act)
+        gu = self.empty((T, f), act)
+        self._gemm(act, 0, 1, T, f, d, a2, d, sl("w_fc1"), d, gu, f,
+                   _lib.EPI_BIAS | _lib.EPI_GELU, bias=ms("b_fc1"), aux_out=u, ldaux_out=f)
+        out = self.empty((T, d), act)
+        self._gemm(act, 0, 1, T, d, f, gu, f, sl("w_fc2"), f, out, d,
+                   _lib.EPI_BIAS | _lib.EPI_RESIDUAL, bias=ms("b_fc2"), aux=h1, ldaux=d)
+        saved = dict(a=a, mean1=mean1, rstd1=rstd1, qkv=qkv, o=o, lse=lse, h1=h1, a2=a2,
+                     mean2=mean2, rstd2=rstd2, u=u, gu=gu)
+        if final:
+            z = self.empty((T, d), act)
+            meanf = self.empty((T,), torch.float32)
+            rstdf = self.empty((T,), torch.float32)
+            call("pc_layernorm_fwd", self.mode.pc_act, T, d, out.data_ptr(),
+                 ms("lnf_g").data_ptr(), ms("lnf_b").data_ptr(), z.data_ptr(), meanf.data_ptr(),
+                 rstdf.data_ptr(), LN_EPS, self.st)
+            saved.update(out=out, meanf=meanf, rstdf=rstdf)
+            out = z
+        hv.saved[op.id] = saved
+        env[op.result] = Act(out)
+
+    def _block_bwd(self, op, env):
+        cfg = self.gpt
+        final = bool(op.attr("final_ln"))
+        lay = self._blay[final]
+        fwd_id = f"block{op.attr('layer')}"
+        dz = tensor_of(env[op.operands[0]])
+        hv = env[op.operands[1]]
+        h = tensor_of(hv)
+        sv = hv.saved[fwd_id]
+        w: Param = env[op.operands[2]]
+        W, Mst = w.compute(), w.master
+        T, d, f, H = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.n_heads
+        act = self.mode.act
+        f32 = torch.float32
+        sl = lambda name: self._slice(W, lay, name)
+        ms = lambda name: self._slice(Mst, lay, name)
+        dW = self.zeros((layout_size(lay),), f32)
+        gs = lambda name: self._slice(dW, lay, name)
+        if final:
+            dout = self.empty((T, d), act)
+            call("pc_layernorm_bwd", self.mode.pc_act, T, d, dz.data_ptr(), sv["out"].data_ptr(),
+                 ms("lnf_g").data_ptr(), sv["meanf"].data_ptr(), sv["rstdf"].data_ptr(), None,
+                 dout.data_ptr(), gs("lnf_g").data_ptr(), gs("lnf_b").data_ptr(), self.st)
+        else:
+            dout = dz
+        # MLP
+        self._gemm(f32, 1, 0, d, f, T, dout, d, sv["gu"], f, gs("w_fc2"), f)
+        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dout.data_ptr(), d,
+             gs("b_fc2").data_ptr(), 0, self.st)
+        du = self.empty((T, f), act)
+        self._gemm(act, 0, 0, T, f, d, dout, d, sl("w_fc2"), f, du, f, _lib.EPI_GELU_GRAD,
+                   aux=sv["u"], ldaux=f)
+        self._gemm(f32, 1, 0, f, d, T, du, f, sv["a2"], d, gs("w_fc1"), d)
+        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, f, du.data_ptr(), f,
+             gs("b_fc1").data_ptr(), 0, self.st)
+        da2 = self.empty((T, d), act)
+        self._gemm(act, 0, 0, T, d, f, du, f, sl("w_fc1"), d, da2, d)
+        dh1 = self.empty((T, d), act)
+        call("pc_layernorm_bwd", self.mode.pc_act, T, d, da2.data_ptr(), sv["h1"].data_ptr(),
+             ms("ln2_g").data_ptr(), sv["mean2"].data_ptr(), sv["rstd2"].data_ptr(),
+             dout.data_ptr(), dh1.data_ptr(), gs("ln2_g").data_ptr(), gs("ln2_b").data_ptr(),
+             self.st)
+        # attention
+        self._gemm(f32, 1, 0, d, d, T, dh1, d, sv["o"], d, gs("w_o"), d)
+        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dh1.data_ptr(), d,
+             gs("b_o").data_ptr(), 0, self.st)
+        do = self.empty((T, d), act)
+        self._gemm(act, 0, 0, T, d, d, dh1, d, sl("w_o"), d, do, d)
+        dqkv = self.empty((T, 3 * d), act)
+        delta = self.empty((cfg.microbatch_size * H * cfg.seq_len,), f32)
+        call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
+             cfg.head_dim, sv["qkv"].data_ptr(), 3 * d, sv["o"].data_ptr(), do.data_ptr(), d,
+             sv["lse"].data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, self.st)
+        self._gemm(f32, 1, 0, 3 * d, d, T, dqkv, 3 * d, sv["a"], d, gs("w_qkv"), d)
+        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, 3 * d, dqkv.data_ptr(), 3 * d,
+             gs("b_qkv").data_ptr(), 0, self.st)
+        da = self.empty((T, d), act)
+        self._gemm(act, 0, 0, T, d, 3 * d, dqkv, 3 * d, sl("w_qkv"), d, da, d)
+        dh = self.empty((T, d), act)
+        call("pc_layernorm_bwd", self.mode.pc_act, T, d, da.data_ptr(), h.data_ptr(),
+             ms("ln1_g").data_ptr(), sv["mean1"].data_ptr(), sv["rstd1"].data_ptr(),
+             dh1.data_ptr(), dh.data_ptr(), gs("ln1_g").data_ptr(), gs("ln1_b").data_ptr(),
+             self.st)
+        return (dh, dW)
+
+    def _head_fwd(self, op, env):
+        cfg = self.gpt
+        hv = env[op.operands[0]]
+        if not isinstance(hv, Act):
+            hv = env[op.operands[0]] = Act(tensor_of(hv))
+        h = hv.t
+        w0: Param = env[op.operands[1]]
+        x = tensor_of(env[op.operands[2]])
+        T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
+        logits = self.empty((T, V), self.mode.act)
+        self._gemm(self.mode.act, 0, 1, T, V, d, h, d, self._slice(w0.compute(), self._elay, "wte"),
+                   d, logits, V)
+        rows = self.empty((T,), torch.float32)
+        call("pc_xent_fwd_bwd", self.mode.pc_act, T, V, cfg.seq_len, logits.data_ptr(), V,
+             x.data_ptr(), rows.data_ptr(), self.st)
+        loss = self.empty((), torch.float32)
+        call("pc_sum_f32", T, rows.data_ptr(), loss.data_ptr(), self.st)
+        hv.saved[op.id] = dict(dlogits=logits)
+        return loss
+
+    def _head_bwd(self, op, env):
+        cfg = self.gpt
+        hv = env[op.operands[0]]
+        h = tensor_of(hv)
+        dlogits = hv.saved["head"]["dlogits"]
+        w0: Param = env[op.operands[1]]
+        T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
+        dh = self.empty((T, d), self.mode.act)
+        wte = self._slice(w0.compute(), self._elay, "wte")
+        self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V, wte, d, dh, d)
+        dw = self.zeros((layout_size(self._elay),), torch.float32)
+        self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
+                   self._slice(dw, self._elay, "wte"), d)
+        return (dh, dw)
+
+
+# ---------------------------------------------------------------- host <-> device
+
+
+def to_device_param(value, mode: Mode, device, gpt: bool):
+    """Step-input parameter on an actor: fp32/fp64 master (+ bf16 shadow)."""
+    if isinstance(value, Param):
+        return value
+    if isinstance(value, np.ndarray):
+        t = torch.from_numpy(np.ascontiguousarray(value)).to(device=device, dtype=mode.master,
+                                                             non_blocking=True)
+    else:
+        t = value.to(device=device, dtype=mode.master, non_blocking=True)
+    if not gpt:
+        return t
+    if mode.act == torch.bfloat16:
+        sh = torch.empty(t.shape, dtype=torch.bfloat16, device=device)
+        call("pc_cast", _PC[t.dtype], _lib.PC_BF16, t.numel(), t.data_ptr(), sh.data_ptr(),
+             torch.cuda.current_stream(device).cuda_stream)
+        return Param(t, sh)
+    return Param(t, None)
+
+
+def to_device_input(value, mode: Mode, device, is_tokens: bool):
+    if isinstance(value, np.ndarray):
+        value = torch.from_numpy(np.ascontiguousarray(value))
+    if is_tokens:
+        return value.to(device=device, dtype=torch.int32, non_blocking=True)
+    return value.to(device=device, dtype=mode.act, non_blocking=True)

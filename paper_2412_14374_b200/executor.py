@@ -1,0 +1,752 @@
+"""B200 pipeline runtime: the drop-in replacement for the reference hot path
+``run_pipelined`` (pkg/src/pipecraft/executor.py:387-483).
+
+Same boundary as the reference:
+
+    run_pipelined(cp, tg, params, batch, lr=0.1, timeout_s=30.0, delay_fn=None,
+                  strict_store=True) -> ExecutionResult(grads, losses, new_params, stats)
+
+with identical ``RunStats`` semantics (driver messages = one dispatch + one
+gather per actor, per-channel message counts, sent buffers, peak live / stash
+counts, final live sets) and the same fault types (``ExecutorFault``,
+``LivenessFault``, ``ChannelOrderFault``).  What changes is underneath:
+
+* each actor's fused program is issued by one host thread onto that actor's
+  CUDA compute stream, asynchronously (no host sync inside the step);
+  ``RunTask`` launches libpp200 kernels (device.DeviceOps);
+* a channel is either a zero-copy ``LocalChannel`` (actors sharing a GPU,
+  events order the streams) or an ``NcclChannel`` (one 2-rank NCCL
+  communicator and one send / one recv stream per directed pair; RecvStart
+  posts the receive = real prefetch; RecvWait / SendWait are stream waits);
+* gradient-merge chains accumulate in place (fp32 accumulator per param and
+  stage) whenever the plan proves the running sum has no other reader;
+* a watchdog turns host blocking and device hangs into ``LivenessFault``
+  (device hangs abort the NCCL communicators first).
+
+In a multi-process launch (torchrun, one process per GPU, world size == P)
+each rank executes only its own actor's program; otherwise all actors run as
+threads of this process (all on one GPU unless ``devices`` says otherwise).
+"""
+from __future__ import annotations
+
+import itertools
+import threading
+import time
+from collections import deque
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .comms import (
+    CommPlan,
+    Delete,
+    FlushPendingDeletes,
+    RecvStart,
+    RecvWait,
+    RunTask,
+    SendStart,
+    SendWait,
+    _brief,
+)
+from .device import MODES, Act, DeviceOps, Mode, Param, strip, tensor_of, to_device_input, \
+    to_device_param
+from .ir import GPTConfig
+from .taskgraph import GRAD_TOTAL, OPT_STATE, PARAM, STASH, TaskGraph
+
+
+class ExecutorFault(RuntimeError):
+    """Liveness or consistency failure inside the runtime."""
+
+
+class ChannelOrderFault(ExecutorFault):
+    pass
+
+
+class LivenessFault(ExecutorFault):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# Results and statistics (executor.py:141-165)
+
+
+@dataclass
+class RunStats:
+    driver_messages: int = 0
+    channel_counts: dict = field(default_factory=dict)     # (src, dst) -> int
+    sent_buffers: list = field(default_factory=list)       # (src, dst, buffer id)
+    peak_live: dict = field(default_factory=dict)          # actor -> int
+    peak_stash: dict = field(default_factory=dict)         # (actor, stage) -> int
+    final_live: dict = field(default_factory=dict)         # actor -> sorted buffer ids
+    timeline: list = field(default_factory=list)           # (actor, kind, uid, start_ms, end_ms)
+
+    @property
+    def channel_messages(self) -> int:
+        return sum(self.channel_counts.values())
+
+    def messages_for_param(self, tg: TaskGraph, param: str) -> int:
+        return sum(1 for _, _, bid in self.sent_buffers
+                   if tg.buffers[bid].meta.get("param") == param
+                   and tg.buffers[bid].kind.startswith("param-grad"))
+
+    def bubble_fraction(self, num_actors: int) -> float:
+        """Idle share of the loop window (simulator.py:241-270 definition) from
+        the measured per-task CUDA-event intervals."""
+        loop = [e for e in self.timeline if e[1] in ("fwd", "bwd")]
+        if not loop:
+            return 0.0
+        lo = min(e[3] for e in loop)
+        hi = max(e[4] for e in loop)
+        span = hi - lo
+        if span <= 0:
+            return 0.0
+        busy = [0.0] * num_actors
+        for a, _, _, s, e in self.timeline:
+            busy[a] += max(0.0, min(e, hi) - max(s, lo))
+        return sum(span - b for b in busy) / (num_actors * span)
+
+
+@dataclass
+class ExecutionResult:
+    grads: dict
+    losses: object
+    new_params: dict
+    stats: RunStats
+
+
+def instrument(result: ExecutionResult) -> RunStats:
+    return result.stats
+
+
+# ---------------------------------------------------------------------------
+# Control (executor.py:172-197)
+
+
+class _Aborted(Exception):
+    pass
+
+
+class _Control:
+    def __init__(self, timeout_s: float):
+        self.deadline = time.monotonic() + timeout_s
+        self.abort = threading.Event()
+        self.heartbeat: dict[int, str] = {}
+        self.faults: list[BaseException] = []
+        self.lock = threading.Lock()
+
+    def remaining(self) -> float:
+        return self.deadline - time.monotonic()
+
+    def fail(self, exc: BaseException):
+        with self.lock:
+            self.faults.append(exc)
+        self.abort.set()
+
+    def check(self, actor: int):
+        if self.abort.is_set():
+            raise _Aborted()
+        if self.remaining() <= 0:
+            raise LivenessFault(f"actor {actor} timed out")
+
+
+# ---------------------------------------------------------------------------
+# Channels
+
+
+class LocalChannel:
+    """Directed FIFO between two actors on the same GPU (reference Channel,
+    executor.py:201-254, semantics kept exactly).  The payload is the device
+    tensor itself (zero copy) plus the CUDA event after which it is valid on
+    the sender's stream; the receiver orders its stream on that event."""
+
+    def __init__(self, src: int, dst: int):
+        self.src, self.dst = src, dst
+        self.q: deque = deque()
+        self.mailbox: dict[int, tuple] = {}
+        self.consumed: set[int] = set()
+        self.cond = threading.Condition()
+
+    def send(self, seq: int, bid: str, value, stream: torch.cuda.Stream):
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        with self.cond:
+            if self.q and self.q[-1][0] >= seq:
+                raise ChannelOrderFault(
+                    f"channel {self.src}->{self.dst}: send seq {seq} out of order")
+            self.q.append((seq, bid, strip(value), ev))
+            self.cond.notify_all()
+
+    def post_recv(self, seq: int, bid: str):
+        pass
+
+    def recv(self, seq: int, ctl: _Control, actor: int, stream: torch.cuda.Stream):
+        with self.cond:
+            while True:
+                if seq in self.mailbox:
+                    bid, value, ev = self.mailbox.pop(seq)
+                    break
+                while not self.q:
+                    ctl.check(actor)
+                    self.cond.wait(timeout=min(0.05, max(ctl.remaining(), 0.001)))
+                head, bid, value, ev = self.q.popleft()
+                self.consumed.add(head)
+                self.cond.notify_all()
+                if head == seq:
+                    break
+                if head > seq:
+                    raise ChannelOrderFault(
+                        f"channel {self.src}->{self.dst}: receive expected seq {seq} "
+                        f"but the channel already advanced to {head} ({bid})")
+                self.mailbox[head] = (bid, value, ev)
+        stream.wait_event(ev)
+        if isinstance(value, torch.Tensor):
+            value.record_stream(stream)
+        return bid, value
+
+    def wait_consumed(self, seq: int, ctl: _Control, actor: int, stream):
+        with self.cond:
+            while seq not in self.consumed:
+                ctl.check(actor)
+                self.cond.wait(timeout=min(0.05, max(ctl.remaining(), 0.001)))
+
+    def is_consumed(self, seq: int) -> bool:
+        with self.cond:
+            return seq in self.consumed
+
+    def drained(self) -> bool:
+        with self.cond:
+            return not self.q and not self.mailbox
+
+    def abort(self):
+        pass
+
+
+class NcclChannel:
+    """One side of a directed channel between two processes: a dedicated
+    2-rank NCCL communicator (src = rank 0, dst = rank 1) and a dedicated
+    stream on this side.  Sends and receives are posted in sequence order on
+    that stream, which is the per-pair FIFO of the deadlock checker."""
+
+    def __init__(self, src: int, dst: int, me: int, comm, device, wire_meta):
+        self.src, self.dst, self.me = src, dst, me
+        self.comm = comm
+        self.stream = torch.cuda.Stream(device=device)
+        self.wire_meta = wire_meta
+        self.sent: dict[int, torch.cuda.Event] = {}
+        self.posted: dict[int, tuple] = {}
+        self.last_seq = -1
+        self.consumed: set[int] = set()
+
+    def send(self, seq: int, bid: str, value, stream: torch.cuda.Stream):
+        if seq <= self.last_seq:
+            raise ChannelOrderFault(f"channel {self.src}->{self.dst}: send seq {seq} out of order")
+        self.last_seq = seq
+        t = strip(value)
+        t = t if t.is_contiguous() else t.contiguous()
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        self.stream.wait_event(ready)
+        _lib.call("pc_p2p_send", self.comm, t.data_ptr(), t.numel() * t.element_size(), 1,
+                  self.stream.cuda_stream)
+        t.record_stream(self.stream)
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        self.sent[seq] = done
+
+    def post_recv(self, seq: int, bid: str):
+        shape, dtype = self.wire_meta(bid)
+        with torch.cuda.stream(self.stream):
+            buf = torch.empty(shape, dtype=dtype, device=self.stream.device)
+        _lib.call("pc_p2p_recv", self.comm, buf.data_ptr(), buf.numel() * buf.element_size(), 0,
+                  self.stream.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        self.posted[seq] = (bid, buf, ev)
+
+    def recv(self, seq: int, ctl: _Control, actor: int, stream: torch.cuda.Stream):
+        if seq not in self.posted:
+            raise ChannelOrderFault(
+                f"channel {self.src}->{self.dst}: wait on seq {seq} that was never posted")
+        bid, buf, ev = self.posted.pop(seq)
+        self.consumed.add(seq)
+        stream.wait_event(ev)
+        buf.record_stream(stream)
+        return bid, buf
+
+    def wait_consumed(self, seq: int, ctl: _Control, actor: int, stream):
+        ev = self.sent.get(seq)
+        if ev is not None:
+            stream.wait_event(ev)
+
+    def is_consumed(self, seq: int) -> bool:
+        ev = self.sent.get(seq)
+        return ev is None or ev.query()
+
+    def drained(self) -> bool:
+        return not self.posted
+
+    def abort(self):
+        if self.comm:
+            try:
+                _lib.call("pc_p2p_abort", self.comm)
+            finally:
+                self.comm = None
+
+
+# ---------------------------------------------------------------------------
+# Per-actor store (executor.py:257-313)
+
+
+class DeviceStore:
+    """Buffer id -> device value, with the reference's pending-deletions queue
+    for buffers whose sends are still in flight."""
+
+    def __init__(self, actor: int, tg: TaskGraph, stats: RunStats):
+        self.actor = actor
+        self.tg = tg
+        self.stats = stats
+        self.data: dict[str, object] = {}
+        self.pending: deque[str] = deque()
+        self.outstanding: dict[str, list] = {}
+        self.received: set[str] = set()
+        self._stash_stage = {bid: b.meta["stage"] for bid, b in tg.buffers.items()
+                             if b.kind == STASH}
+
+    def put(self, bid: str, value):
+        self.data[bid] = value
+        self._track()
+
+    def get(self, bid: str, at: str):
+        if bid not in self.data:
+            raise LivenessFault(f"actor {self.actor} at {at}: missing buffer {bid}")
+        return self.data[bid]
+
+    def note_send(self, bid: str, ch, seq: int):
+        self.outstanding.setdefault(bid, []).append((ch, seq))
+
+    def sends_done(self, bid: str) -> bool:
+        return all(ch.is_consumed(seq) for ch, seq in self.outstanding.get(bid, ()))
+
+    def delete(self, bid: str, at: str):
+        if bid not in self.data:
+            raise LivenessFault(f"actor {self.actor} at {at}: delete of absent buffer {bid}")
+        if self.sends_done(bid):
+            del self.data[bid]
+        else:
+            self.pending.append(bid)
+
+    def flush(self):
+        keep = deque()
+        while self.pending:
+            bid = self.pending.popleft()
+            if self.sends_done(bid):
+                self.data.pop(bid, None)
+            else:
+                keep.append(bid)
+        self.pending = keep
+
+    def _track(self):
+        a = self.actor
+        self.stats.peak_live[a] = max(self.stats.peak_live.get(a, 0), len(self.data))
+        by_stage: dict[int, int] = {}
+        for bid in self.data:
+            st = self._stash_stage.get(bid)
+            if st is not None:
+                by_stage[st] = by_stage.get(st, 0) + 1
+        for st, n in by_stage.items():
+            key = (a, st)
+            self.stats.peak_stash[key] = max(self.stats.peak_stash.get(key, 0), n)
+
+
+# ---------------------------------------------------------------------------
+# Actor
+
+
+class _Actor:
+    def __init__(self, actor: int, tg: TaskGraph, mode: Mode, device: torch.device,
+                 gpt: GPTConfig | None, stats: RunStats, timeline: bool):
+        self.actor = actor
+        self.tg = tg
+        self.device = device
+        self.stream = torch.cuda.Stream(device=device)
+        self.ops = DeviceOps(tg.partition, mode, device, self.stream, gpt)
+        self.store = DeviceStore(actor, tg, stats)
+        self.timeline = timeline
+        self.events: list = []
+        self.base_event = None
+        self.end_event = None
+        self.last_issued = -1
+
+    def run_task(self, task, at: str):
+        ex = task.exec
+        kind = ex["type"]
+        st = self.store
+        p = self.tg.partition
+        if self.timeline:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+        if kind == "stage-fwd":
+            prog = p.fwd_programs[ex["stage"]]
+            env = {v: st.get(bid, at) for v, bid in ex["feeds"].items()}
+            self.ops.run_ops(prog.ops, env)
+            for v, bid in ex["outs"].items():
+                st.put(bid, env[v])
+            if ex["stash_out"]:
+                st.put(ex["stash_out"], {v: env[v] for v in prog.stash})
+        elif kind == "stage-bwd":
+            prog = p.bwd_programs[ex["stage"]]
+            env = {v: st.get(bid, at) for v, bid in ex["feeds"].items()}
+            if ex["stash_in"]:
+                env.update(st.get(ex["stash_in"], at))
+            self.ops.run_ops(prog.ops, env)
+            for v, bid in ex["outs"].items():
+                st.put(bid, env[v])
+        elif kind == "add":
+            lhs = ex["lhs"]
+            st.put(ex["out"], self.ops.add(st.get(lhs, at), st.get(ex["rhs"], at),
+                                           inplace=self._may_overwrite(lhs, task.uid)))
+        elif kind == "concat":
+            st.put(ex["out"], self.ops.concat_losses([st.get(b, at) for b in ex["parts"]]))
+        elif kind == "sgd-update":
+            st.put(ex["out"], self.ops.sgd(st.get(ex["param"], at), st.get(ex["grad"], at),
+                                           st.get(ex["lr"], at)))
+        else:
+            raise ExecutorFault(f"unknown task payload {kind!r}")
+        if self.timeline:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(self.stream)
+            self.events.append((task.kind if task.is_loop else "aux", task.uid, e0, e1))
+
+    def _may_overwrite(self, bid: str, uid: str) -> bool:
+        """True when ``bid``'s only reader is this task, it is not a step output,
+        not a received buffer, and has no send in flight: then the running sum
+        can be updated in place (the fused accumulator)."""
+        b = self.tg.buffers[bid]
+        return (b.consumers == {uid} and not b.is_output and b.kind not in (PARAM, OPT_STATE)
+                and bid not in self.store.received and not self.store.outstanding.get(bid))
+
+
+def _wire_meta_fn(tg: TaskGraph, mode: Mode):
+    g = tg.partition.graph
+
+    def meta(bid: str):
+        b = tg.buffers[bid]
+        v = b.meta.get("value")
+        if v is not None:
+            spec = g.spec_of(v)
+            op = g.producer(v)
+            if op.kind == "input-read" and op.attr_or("token_ids", 0):
+                return tuple(spec.dims), torch.int32
+            if v in g.params:
+                return tuple(spec.dims), mode.master
+            return tuple(spec.dims), mode.act
+        q = b.meta.get("param")
+        if q is not None:
+            return tuple(g.spec_of(q).dims), mode.master
+        raise ExecutorFault(f"no wire layout for buffer {bid}")
+    return meta
+
+
+def _worker(act: _Actor, instrs, tg: TaskGraph, channels: dict, ctl: _Control, delay_fn,
+            counting):
+    a = act.actor
+    try:
+        with torch.cuda.device(act.device), torch.cuda.stream(act.stream):
+            if act.timeline:
+                act.base_event = torch.cuda.Event(enable_timing=True)
+                act.base_event.record(act.stream)
+            for idx, ins in enumerate(instrs):
+                ctl.heartbeat[a] = f"[{idx}] {_brief(ins)}"
+                if delay_fn is not None:
+                    d = delay_fn(a, idx)
+                    if d:
+                        time.sleep(d)
+                ctl.check(a)
+                at = f"instruction {idx}"
+                if isinstance(ins, RunTask):
+                    act.run_task(tg.tasks[ins.task], at)
+                elif isinstance(ins, SendStart):
+                    ch = channels[(a, ins.dst)]
+                    value = act.store.get(ins.buffer, at)
+                    act.store.note_send(ins.buffer, ch, ins.seq)
+                    counting(a, ins.dst, ins.buffer)
+                    ch.send(ins.seq, ins.buffer, value, act.stream)
+                elif isinstance(ins, SendWait):
+                    channels[(a, ins.dst)].wait_consumed(ins.seq, ctl, a, act.stream)
+                elif isinstance(ins, RecvStart):
+                    channels[(ins.src, a)].post_recv(ins.seq, ins.buffer)
+                elif isinstance(ins, RecvWait):
+                    bid, value = channels[(ins.src, a)].recv(ins.seq, ctl, a, act.stream)
+                    act.store.received.add(bid)
+                    act.store.put(bid, value)
+                elif isinstance(ins, Delete):
+                    act.store.delete(ins.buffer, at)
+                elif isinstance(ins, FlushPendingDeletes):
+                    act.store.flush()
+                else:
+                    raise ExecutorFault(f"actor {a}: unknown instruction {ins!r}")
+                act.last_issued = idx
+            act.end_event = torch.cuda.Event()
+            act.end_event.record(act.stream)
+        ctl.heartbeat[a] = "done"
+    except _Aborted:
+        pass
+    except BaseException as e:  # noqa: BLE001 - forwarded to the driver
+        ctl.fail(e)
+
+
+# ---------------------------------------------------------------------------
+# Engine
+
+
+_ENGINE_IDS = itertools.count()
+
+
+def _dist_world():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return dist.get_rank(), dist.get_world_size()
+    return None
+
+
+class PipelineEngine:
+    """Reusable executor for one (CommPlan, TaskGraph): streams, channels and
+    NCCL communicators are created once; ``step`` runs one training step."""
+
+    def __init__(self, cp: CommPlan, tg: TaskGraph, mode: str | Mode = "fp64",
+                 gpt: GPTConfig | None = None, devices=None, timeline: bool = False):
+        if not cp.fused:
+            raise ExecutorFault("plan must be fused before execution")
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2412_14374_b200 needs a CUDA device (no CPU fallback)")
+        _lib.lib()  # fail loudly if the extension is missing
+        self.cp, self.tg = cp, tg
+        self.mode = MODES[mode] if isinstance(mode, str) else mode
+        self.gpt = gpt
+        self.P = cp.num_actors
+        self.timeline = timeline
+        dw = _dist_world()
+        self.distributed = dw is not None
+        self.stats = RunStats()
+        if self.distributed:
+            rank, world = dw
+            if world != self.P:
+                raise ExecutorFault(f"world size {world} != plan actors {self.P}")
+            self.local = [rank]
+            dev = torch.device("cuda", torch.cuda.current_device())
+            self.devices = {rank: dev}
+        else:
+            self.local = list(range(self.P))
+            if devices is None:
+                devices = [torch.cuda.current_device()]
+            devs = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d)
+                    for d in devices]
+            self.devices = {a: devs[a % len(devs)] for a in self.local}
+            if len({self.devices[a] for a in self.local}) > 1 and cp.channels:
+                raise ExecutorFault("single-process multi-GPU channels are not supported; "
+                                    "launch one process per GPU (torchrun)")
+        self._wire_meta = _wire_meta_fn(tg, self.mode)
+        self._channels = self._make_channels()
+
+    def _make_channels(self):
+        if not self.distributed:
+            return {key: LocalChannel(*key) for key in self.cp.channels}
+        import torch.distributed as dist
+        store = dist.distributed_c10d._get_default_store()
+        tag = next(_ENGINE_IDS)
+        me = self.local[0]
+        dev = self.devices[me]
+        out = {}
+        import ctypes
+        for src, dst in sorted(self.cp.channels):
+            if me not in (src, dst):
+                continue
+            key = f"pp200/e{tag}/{src}->{dst}"
+            if me == src:
+                uid = (ctypes.c_char * 128)()
+                _lib.call("pc_p2p_unique_id", uid)
+                store.set(key, bytes(uid))
+                raw = bytes(uid)
+            else:
+                raw = store.get(key)
+            idbuf = (ctypes.c_char * 128).from_buffer_copy(raw)
+            comm = ctypes.c_void_p()
+            with torch.cuda.device(dev):
+                _lib.call("pc_p2p_comm_init", ctypes.byref(comm), 2, idbuf, 0 if me == src else 1)
+            out[(src, dst)] = NcclChannel(src, dst, me, comm, dev, self._wire_meta)
+        return out
+
+    def close(self):
+        for ch in self._channels.values():
+            if isinstance(ch, NcclChannel) and ch.comm:
+                _lib.call("pc_p2p_destroy", ch.comm)
+                ch.comm = None
+
+    # -- seeding (executor.py:405-414) --
+    def _seed(self, actors: dict, params, batch, lr):
+        tg = self.tg
+        p = tg.partition
+        M = tg.schedule.num_microbatches
+        (x_in,) = sorted(p.graph.inputs)
+        tokens = p.graph.producer(x_in).attr_or("token_ids", 0) == 1
+        mbs = split_batch(batch, M)
+        is_gpt = self.gpt is not None
+        for bid, buf in tg.buffers.items():
+            if buf.producer is not None or buf.home not in actors:
+                continue
+            act = actors[buf.home]
+            with torch.cuda.device(act.device), torch.cuda.stream(act.stream):
+                if buf.kind == PARAM:
+                    v = to_device_param(params[buf.meta["param"]], self.mode, act.device, is_gpt)
+                elif buf.kind == OPT_STATE:
+                    v = float(lr)
+                else:
+                    v = to_device_input(mbs[buf.meta["microbatch"]], self.mode, act.device,
+                                        tokens)
+                act.store.put(bid, v)
+
+    def step(self, params, batch, lr: float = 0.1, timeout_s: float = 30.0, delay_fn=None,
+             strict_store: bool = True, to_host: bool = True) -> ExecutionResult:
+        stats = RunStats()
+        ctl = _Control(timeout_s)
+        actors = {a: _Actor(a, self.tg, self.mode, self.devices[a], self.gpt, stats,
+                            self.timeline) for a in self.local}
+        for a, act in actors.items():
+            # params / inputs are copied on the current stream; the actor stream waits
+            with torch.cuda.device(act.device):
+                act.stream.wait_stream(torch.cuda.current_stream(act.device))
+        self._seed(actors, params, batch, lr)
+        lock = threading.Lock()
+
+        def counting(src, dst, bid):
+            with lock:
+                stats.channel_counts[(src, dst)] = stats.channel_counts.get((src, dst), 0) + 1
+                stats.sent_buffers.append((src, dst, bid))
+
+        if self.distributed:
+            import torch.distributed as dist
+            dist.barrier()
+        workers = []
+        for a in self.local:
+            stats.driver_messages += 1  # program dispatch
+            w = threading.Thread(target=_worker, name=f"actor-{a}",
+                                 args=(actors[a], self.cp.programs[a].instrs, self.tg,
+                                       self._channels, ctl, delay_fn, counting), daemon=True)
+            workers.append(w)
+            w.start()
+        for w in workers:
+            w.join(timeout=max(ctl.remaining(), 0.0) + 1.0)
+        hung = [w for w in workers if w.is_alive()]
+        if hung:
+            ctl.abort.set()
+            self._abort_channels()
+            dump = ", ".join(f"actor {a}: {ctl.heartbeat.get(a, '?')}" for a in self.local)
+            raise LivenessFault(f"watchdog timeout; blocked instructions: {dump}")
+        if ctl.faults:
+            raise ctl.faults[0]
+        self._wait_devices(actors, ctl)
+        for key, ch in self._channels.items():
+            if not ch.drained():
+                raise ChannelOrderFault(f"channel {key} holds undelivered messages at step end")
+        # after the device finished, in-flight sends are complete: final flush
+        for act in actors.values():
+            act.store.flush()
+        return self._gather(actors, stats, strict_store, to_host)
+
+    def _abort_channels(self):
+        for ch in self._channels.values():
+            ch.abort()
+
+    def _wait_devices(self, actors, ctl: _Control):
+        """Device-side watchdog: a stream that never drains (e.g. a receive
+        whose send was dropped) aborts the communicators and raises."""
+        pending = {a: act for a, act in actors.items() if act.end_event is not None}
+        while pending:
+            for a in list(pending):
+                if pending[a].end_event.query():
+                    del pending[a]
+            if not pending:
+                break
+            if ctl.remaining() <= 0:
+                self._abort_channels()
+                dump = ", ".join(
+                    f"actor {a}: device stream stalled after issuing [{act.last_issued}] "
+                    f"{ctl.heartbeat.get(a, '?')}" for a, act in pending.items())
+                raise LivenessFault(f"watchdog timeout; blocked instructions: {dump}")
+            time.sleep(0.0005)
+
+    def _gather(self, actors, stats: RunStats, strict_store: bool, to_host: bool):
+        tg = self.tg
+        grads, new_params, losses = {}, {}, None
+
+        def out(v):
+            t = v.master if isinstance(v, Param) else tensor_of(v)
+            return t.detach().cpu().numpy() if to_host else t
+
+        for a in sorted(actors):
+            act = actors[a]
+            store = act.store
+            stats.driver_messages += 1  # result gather
+            stats.final_live[a] = sorted(store.data)
+            for bid in stats.final_live[a]:
+                b = tg.buffers[bid]
+                if b.kind == GRAD_TOTAL:
+                    grads[b.meta["param"]] = out(store.data[bid])
+                elif bid.startswith("wnew:"):
+                    new_params[b.meta["param"]] = out(store.data[bid])
+                elif bid == "loss:all":
+                    losses = out(store.data[bid])
+            if act.timeline and act.base_event is not None:
+                for kind, uid, e0, e1 in act.events:
+                    stats.timeline.append((a, kind, uid, act.base_event.elapsed_time(e0),
+                                           act.base_event.elapsed_time(e1)))
+        if strict_store:
+            for a in sorted(actors):
+                store = actors[a].store
+                extra = [bid for bid in store.data
+                         if tg.buffers[bid].kind not in (PARAM, OPT_STATE)
+                         and not tg.buffers[bid].is_output]
+                if extra or store.pending:
+                    raise ExecutorFault(
+                        f"actor {a} leaked buffers at step end: {sorted(extra)} "
+                        f"pending={sorted(store.pending)}")
+        if not self.distributed:
+            missing = set(tg.partition.graph.params) - set(grads)
+            if missing or losses is None:
+                raise ExecutorFault(f"step outputs incomplete: grads missing {sorted(missing)}")
+        self.stats = stats
+        return ExecutionResult(grads=grads, losses=losses, new_params=new_params, stats=stats)
+
+
+def split_batch(batch, M: int):
+    """executor.py:110-114 (rows split into M equal microbatches)."""
+    n = batch.shape[0]
+    if n % M != 0:
+        raise ValueError(f"batch of {n} rows does not split into {M} microbatches")
+    step = n // M
+    return [batch[i * step:(i + 1) * step] for i in range(M)]
+
+
+def run_pipelined(cp: CommPlan, tg: TaskGraph, params, batch, lr: float = 0.1,
+                  timeout_s: float = 30.0, delay_fn=None, strict_store: bool = True,
+                  mode: str | None = None, gpt: GPTConfig | None = None, devices=None,
+                  timeline: bool = False, to_host: bool = True) -> ExecutionResult:
+    """Execute a fused plan on B200(s).  Drop-in for executor.py:387-483.
+
+    ``mode`` defaults from the parameter dtype (float64 -> "fp64", float32 ->
+    "fp32"); GPT graphs (``gpt`` given) default to "bf16".
+    """
+    if mode is None:
+        if gpt is not None:
+            mode = "bf16"
+        else:
+            any_p = next(iter(params.values()))
+            mode = "fp32" if getattr(any_p, "dtype", None) in (np.float32, torch.float32) else "fp64"
+    eng = PipelineEngine(cp, tg, mode=mode, gpt=gpt, devices=devices, timeline=timeline)
+    try:
+        return eng.step(params, batch, lr=lr, timeout_s=timeout_s, delay_fn=delay_fn,
+                        strict_store=strict_store, to_host=to_host)
+    finally:
+        eng.close()

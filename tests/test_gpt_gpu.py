@@ -1,0 +1,203 @@
+"""GPT path on the GPU vs the float64 numpy oracle (oracle/gpt.py).
+
+fp32 mode: rel < 1e-5 (north_star).  bf16 mode: rel < 2e-2 (north_star).
+The pipeline runs the tied-embedding GPT graph (ir.build_gpt) through the
+same planner and runtime as the FFN tests: GPipe / 1F1B / interleaved on one
+GPU with local channels, including the non-adjacent token skip to the last
+stage and the commuted tied-weight gradient.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import ffn, gpt  # noqa: E402
+from paper_2412_14374_b200 import _lib  # noqa: E402
+from paper_2412_14374_b200 import comms as C  # noqa: E402
+from paper_2412_14374_b200 import ir as I  # noqa: E402
+from paper_2412_14374_b200 import schedules as S  # noqa: E402
+from paper_2412_14374_b200 import taskgraph as T  # noqa: E402
+from paper_2412_14374_b200.executor import run_pipelined  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def plan(cfg: I.GPTConfig, fam, P, M, V=1):
+    p = I.derive_backward(I.partition_stages(I.build_gpt(cfg)))
+    s = {"gpipe": lambda: S.gpipe(P, M), "1f1b": lambda: S.one_f_one_b(P, M),
+         "interleaved": lambda: S.interleaved_1f1b(P, M, V)}[fam]()
+    tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
+    cp = C.infer_comms(tg, s)
+    assert C.check_deadlock_free(cp).ok
+    return p, tg, C.fuse(C.insert_deletions(cp, tg), tg)
+
+
+def oracle_cfg(cfg: I.GPTConfig):
+    return dict(layers=cfg.layers, d=cfg.d_model, heads=cfg.n_heads, ff=cfg.d_ff,
+                vocab=cfg.vocab, seq=cfg.seq_len, mbs=cfg.microbatch_size)
+
+
+def run_case(cfg, fam, P, M, V, mode, seed=0, std=0.02):
+    p, tg, cp = plan(cfg, fam, P, M, V)
+    oc = oracle_cfg(cfg)
+    rng = np.random.default_rng(seed)
+    params = gpt.init_params(oc, rng, std=std)
+    tokens = gpt.init_tokens(oc, M, rng)
+    g, l, w = gpt.run_reference_gpt(params, tokens, oc)
+    res = run_pipelined(cp, tg, {q: v.astype(np.float32) for q, v in params.items()},
+                        tokens.reshape(M * cfg.microbatch_size, cfg.seq_len), mode=mode, gpt=cfg)
+    return res, g, l, w
+
+
+TINY = dict(layers=4, d_model=64, n_heads=4, d_ff=256, vocab=96, seq_len=32, microbatch_size=2)
+
+
+@pytest.mark.parametrize("fam,P,M,V,yields", [
+    ("gpipe", 1, 2, 1, None), ("gpipe", 2, 4, 1, (3,)), ("1f1b", 4, 4, 1, (2, 3, 5)),
+    ("interleaved", 2, 4, 2, (1, 3, 4))])
+def test_gpt_fp32_matches_oracle(fam, P, M, V, yields):
+    cfg = I.GPTConfig(**TINY, yields=yields, yield_every=TINY["layers"] + 2, elem_bytes=4)
+    res, g, l, w = run_case(cfg, fam, P, M, V, "fp32", std=0.1)
+    assert ffn.rel(res.losses, l) < 1e-5
+    for q in g:
+        assert ffn.rel(res.grads[q], g[q]) < 1e-5, q
+        assert ffn.rel(res.new_params[q], w[q]) < 1e-5, q
+
+
+@pytest.mark.parametrize("fam,P,M,yields", [("gpipe", 2, 4, (3,)), ("1f1b", 4, 8, (2, 3, 5))])
+def test_gpt_bf16_matches_oracle(fam, P, M, yields):
+    cfg = I.GPTConfig(**dict(TINY, d_model=128, n_heads=2, d_ff=512, vocab=256, seq_len=64),
+                      yields=yields, yield_every=TINY["layers"] + 2, elem_bytes=2)
+    res, g, l, w = run_case(cfg, fam, P, M, 1, "bf16", std=0.05)
+    assert ffn.rel(res.losses, l) < 2e-2
+    for q in g:
+        assert ffn.rel(res.grads[q], g[q]) < 2e-2, q
+        assert ffn.rel(res.new_params[q], w[q]) < 2e-2, q
+
+
+def test_gpt_bf16_deterministic_rerun():
+    cfg = I.GPTConfig(**TINY, yields=(3,), yield_every=TINY["layers"] + 2)
+    a, *_ = run_case(cfg, "1f1b", 2, 4, 1, "bf16")
+    b, *_ = run_case(cfg, "1f1b", 2, 4, 1, "bf16")
+    for q in a.grads:
+        assert np.array_equal(a.grads[q], b.grads[q])
+    assert np.array_equal(a.losses, b.losses)
+
+
+# ---------------------------------------------------------------- kernels
+
+
+def _t(x, dt=torch.float32):
+    return torch.tensor(x, device="cuda", dtype=dt)
+
+
+@pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_attention_kernels(dt, tol, impl):
+    B, H, S, hd = 2, 3, 80, 64
+    rng = np.random.default_rng(3)
+    qkv = rng.standard_normal((B * S, 3 * H * hd)) * 0.5
+    do = rng.standard_normal((B * S, H * hd))
+    d = H * hd
+    q, k, v = (qkv[:, i * d:(i + 1) * d].reshape(B, S, H, hd).transpose(0, 2, 1, 3) for i in range(3))
+    o4, p = gpt.attention(q, k, v)
+    dq, dk, dv = gpt.attention_bwd(do.reshape(B, S, H, hd).transpose(0, 2, 1, 3), q, k, v, p)
+    merge = lambda t: t.transpose(0, 2, 1, 3).reshape(B * S, d)
+    tq = _t(qkv, dt)
+    o = torch.empty(B * S, d, device="cuda", dtype=dt)
+    lse = torch.empty(B * H * S, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("pc_attention_set_impl", impl)
+    try:
+        _lib.call("pc_attention_fwd", _lib.PC_F32 if dt == torch.float32 else _lib.PC_BF16, B, H,
+                  S, hd, tq.data_ptr(), 3 * d, o.data_ptr(), d, lse.data_ptr(), st)
+        tdo = _t(do, dt)
+        dqkv = torch.empty(B * S, 3 * d, device="cuda", dtype=dt)
+        delta = torch.empty(B * H * S, device="cuda")
+        _lib.call("pc_attention_bwd", _lib.PC_F32 if dt == torch.float32 else _lib.PC_BF16, B, H,
+                  S, hd, tq.data_ptr(), 3 * d, o.data_ptr(), tdo.data_ptr(), d, lse.data_ptr(),
+                  delta.data_ptr(), dqkv.data_ptr(), 3 * d, st)
+    finally:
+        _lib.call("pc_attention_set_impl", 0)
+    torch.cuda.synchronize()
+    assert ffn.rel(o.double().cpu().numpy(), merge(o4)) < tol
+    got = dqkv.double().cpu().numpy()
+    assert ffn.rel(got[:, :d], merge(dq)) < tol
+    assert ffn.rel(got[:, d:2 * d], merge(dk)) < tol
+    assert ffn.rel(got[:, 2 * d:], merge(dv)) < tol
+
+
+def test_layernorm_and_xent_kernels():
+    rows, d, V, seq = 64, 96, 50, 16
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((rows, d))
+    g, b = rng.standard_normal(d), rng.standard_normal(d)
+    dy = rng.standard_normal((rows, d))
+    y, cache = gpt.layer_norm(x, g, b)
+    dx, dg, db = gpt.layer_norm_bwd(dy, g, cache)
+    tx, tg_, tb, tdy = _t(x), _t(g), _t(b), _t(dy)
+    ty = torch.empty_like(tx)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("pc_layernorm_fwd", _lib.PC_F32, rows, d, tx.data_ptr(), tg_.data_ptr(),
+              tb.data_ptr(), ty.data_ptr(), mean.data_ptr(), rstd.data_ptr(), 1e-5, st)
+    tdx = torch.empty_like(tx)
+    tdg = torch.empty(d, device="cuda")
+    tdb = torch.empty(d, device="cuda")
+    _lib.call("pc_layernorm_bwd", _lib.PC_F32, rows, d, tdy.data_ptr(), tx.data_ptr(),
+              tg_.data_ptr(), mean.data_ptr(), rstd.data_ptr(), None, tdx.data_ptr(),
+              tdg.data_ptr(), tdb.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert ffn.rel(ty.cpu().numpy(), y) < 1e-5
+    assert ffn.rel(tdx.cpu().numpy(), dx) < 1e-5
+    assert ffn.rel(tdg.cpu().numpy(), dg) < 1e-5
+    assert ffn.rel(tdb.cpu().numpy(), db) < 1e-5
+    # cross-entropy against the oracle head (identity "wte" so logits = h)
+    h = rng.standard_normal((rows, V))
+    tokens = rng.integers(0, V, size=(rows // seq, seq)).astype(np.int32)
+    loss, dh, _ = gpt.head_loss(h, np.eye(V), tokens)
+    tl = _t(h)
+    tt = torch.tensor(tokens, device="cuda")
+    row_loss = torch.empty(rows, device="cuda")
+    _lib.call("pc_xent_fwd_bwd", _lib.PC_F32, rows, V, seq, tl.data_ptr(), V, tt.data_ptr(),
+              row_loss.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert abs(row_loss.sum().item() - loss) < 1e-4 * abs(loss)
+    assert ffn.rel(tl.cpu().numpy(), dh) < 1e-5
+
+
+def test_embedding_kernels_deterministic():
+    T_, d, seq, V = 256, 64, 32, 40
+    rng = np.random.default_rng(5)
+    wte = rng.standard_normal((V, d))
+    wpe = rng.standard_normal((seq, d))
+    tokens = rng.integers(0, V, size=T_).astype(np.int32)
+    dh = rng.standard_normal((T_, d))
+    st = torch.cuda.current_stream().cuda_stream
+    tt = torch.tensor(tokens, device="cuda")
+    out = torch.empty(T_, d, device="cuda")
+    _lib.call("pc_embedding_fwd", _lib.PC_F32, T_, d, seq, tt.data_ptr(), _t(wte).data_ptr(),
+              _t(wpe).data_ptr(), out.data_ptr(), st)
+    torch.cuda.synchronize()
+    ref = wte[tokens] + wpe[np.arange(T_) % seq]
+    assert ffn.rel(out.cpu().numpy(), ref) < 1e-6
+    import ctypes
+    nb = ctypes.c_int64()
+    _lib.call("pc_embedding_bwd_workspace_bytes", T_, ctypes.byref(nb))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        dwte = torch.empty(V, d, device="cuda")
+        dwpe = torch.empty(seq, d, device="cuda")
+        _lib.call("pc_embedding_bwd", _lib.PC_F32, T_, d, seq, V, tt.data_ptr(), _t(dh).data_ptr(),
+                  dwte.data_ptr(), dwpe.data_ptr(), ws.data_ptr(), nb.value, st)
+        torch.cuda.synchronize()
+        outs.append((dwte.cpu().numpy(), dwpe.cpu().numpy()))
+    want_te = np.zeros((V, d))
+    np.add.at(want_te, tokens, dh)
+    want_pe = np.zeros((seq, d))
+    np.add.at(want_pe, np.arange(T_) % seq, dh)
+    assert ffn.rel(outs[0][0], want_te) < 1e-5
+    assert ffn.rel(outs[0][1], want_pe) < 1e-5
+    assert np.array_equal(outs[0][0], outs[1][0])
