@@ -1,0 +1,405 @@
+"""Benchmark: one pipelined GPT training step on N B200s (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1], "C2"): GPT-2 small (12 layers, d=768, 12
+heads, d_ff=3072, vocab 50304, seq 1024), 1F1B over 8 microbatches of 8x1024
+tokens, bf16 compute / fp32 master + accumulators, SGD update inside the step,
+random-init weights and synthetic uniform tokens.  N GPUs = N pipeline stages
+(stage boundaries balanced by FLOPs); total work per step is fixed as N grows
+("scaling": "strong").  Inputs exceed L2 (activations of one stage ~1.5 GB per
+microbatch), so no explicit flush is needed between steps.
+
+Prints one JSON line (rank 0): value = tokens/s for the whole job, plus
+model TFLOPS/GPU, measured vs ideal bubble, roofline of the dominant kernel
+(the tcgen05 GEMM), the numpy CPU baseline, the e2e number through the public
+API with host<->device copies, clocks, and libpp200 launch count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2 = dict(layers=12, d_model=768, n_heads=12, d_ff=3072, vocab=50304, seq_len=1024,
+          microbatch_size=8)
+M_MICRO = 8
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained"), d["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def block_costs(cfg):
+    blk = cfg.block_fwd_flops()
+    return [float(cfg.tokens * cfg.d_model)] + [blk] * cfg.layers + [cfg.head_fwd_flops()]
+
+
+def build_plan(P, cfg_kw, M, mode="bf16"):
+    from paper_2412_14374_b200 import comms as C
+    from paper_2412_14374_b200 import ir as I
+    from paper_2412_14374_b200 import schedules as S
+    from paper_2412_14374_b200 import taskgraph as T
+    base = I.GPTConfig(**cfg_kw, yield_every=cfg_kw["layers"] + 2)
+    yields = I.balanced_yields(block_costs(base), P) if P > 1 else None
+    cfg = I.GPTConfig(**cfg_kw, yields=yields, yield_every=cfg_kw["layers"] + 2,
+                      elem_bytes=2 if mode == "bf16" else 4)
+    p = I.derive_backward(I.partition_stages(I.build_gpt(cfg)))
+    s = S.one_f_one_b(P, M)
+    tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
+    cp = C.infer_comms(tg, s)
+    rep = C.check_deadlock_free(cp)
+    assert rep.ok, str(rep)
+    return cfg, tg, C.fuse(C.insert_deletions(cp, tg), tg)
+
+
+def init_params_device(cfg, device, seed=0):
+    """N(0, 0.02) weights (out projections / sqrt(2L)), LN gamma=1, on device."""
+    import torch
+    from paper_2412_14374_b200 import _lib
+    from paper_2412_14374_b200.device import Param
+    from paper_2412_14374_b200.ir import layout_size
+    g = torch.Generator(device=device).manual_seed(seed)
+    out = {}
+    st = torch.cuda.current_stream(device).cuda_stream
+
+    def make(layout, name_filter):
+        n = layout_size(layout)
+        m = torch.zeros(n, device=device)
+        for name, (off, dims) in layout.items():
+            if name == "__size__":
+                continue
+            sz = int(np.prod(dims))
+            if name.endswith("_g"):
+                m[off:off + sz] = 1.0
+            elif name.startswith("w"):
+                std = 0.02 / np.sqrt(2 * cfg.layers) if name in ("w_o", "w_fc2") else 0.02
+                m[off:off + sz] = torch.randn(sz, device=device, generator=g) * std
+        sh = torch.empty(n, device=device, dtype=torch.bfloat16)
+        _lib.call("pc_cast", _lib.PC_F32, _lib.PC_BF16, n, m.data_ptr(), sh.data_ptr(), st)
+        return Param(m, sh)
+
+    out["w0"] = make(cfg.embed_layout(), None)
+    for k in range(1, cfg.layers + 1):
+        out[f"w{k}"] = make(cfg.block_layout(k == cfg.layers), None)
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
+    """Average achieved TFLOP/s of the tcgen05 GEMM over the shape mix of one
+    stage step, each shape timed with CUDA events on its launch stream (warm,
+    back to back); share of the step it accounts for."""
+    import torch
+    from paper_2412_14374_b200 import _lib
+    T, d, f, V = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.vocab
+    # (M, N, K, ta, tb, launches per microbatch per block) for one GPT block fwd+bwd
+    shapes = [(T, 3 * d, d, 0, 1), (T, d, d, 0, 1), (T, f, d, 0, 1), (T, d, f, 0, 1),   # fwd
+              (d, f, T, 1, 0), (T, f, d, 0, 0), (f, d, T, 1, 0), (T, d, f, 0, 0),       # bwd mlp
+              (d, d, T, 1, 0), (T, d, d, 0, 0), (3 * d, d, T, 1, 0), (T, d, 3 * d, 0, 0)]
+    head = [(T, V, d, 0, 1), (T, d, V, 0, 0), (V, d, T, 1, 0)]
+    st = torch.cuda.current_stream()
+    tot_flops = tot_ms = 0.0
+    per = []
+    for (Mm, N, K, ta, tb), count in [(s, stage_blocks) for s in shapes] + [(s, 1 if P == 1 else 0) for s in head]:
+        if count == 0:
+            continue
+        A = torch.randn((K, Mm) if ta else (Mm, K), device="cuda").bfloat16()
+        B = torch.randn((N, K) if tb else (K, N), device="cuda").bfloat16()
+        out_f32 = ta == 1
+        C = torch.empty(Mm, N, device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
+        args = (_lib.PC_BF16, _lib.PC_F32 if out_f32 else _lib.PC_BF16, ta, tb, Mm, N, K,
+                A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, 0, None,
+                None, 0, None, 0, st.cuda_stream)
+        for _ in range(3):
+            _lib.call("pc_gemm", *args)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record(st)
+        for _ in range(reps):
+            _lib.call("pc_gemm", *args)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        fl = 2.0 * Mm * N * K
+        per.append({"shape": [Mm, N, K, ta, tb], "ms": round(ms, 4),
+                    "tflops": round(fl / ms / 1e9, 1), "launches_per_mb": count})
+        tot_flops += fl * count * M_MICRO
+        tot_ms += ms * count * M_MICRO
+        del A, B, C
+    achieved = tot_flops / tot_ms / 1e9 if tot_ms else 0.0
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "tc_gemm_kernel (tcgen05.mma kind::f16, TMA, TMEM)",
+            "share_of_step": round(tot_ms / step_ms, 3) if step_ms else None,
+            "shapes": per}
+
+
+def cpu_baseline(cfg_kw, seconds_hint=True):
+    """The numpy float64 oracle (oracle/gpt.py) on a bounded sample of the same
+    workload: one sequence (1 x 1024 tokens) through the full 12-layer model,
+    forward + backward, timed on the host cores."""
+    from oracle import gpt as og
+    oc = dict(layers=cfg_kw["layers"], d=cfg_kw["d_model"], heads=cfg_kw["n_heads"],
+              ff=cfg_kw["d_ff"], vocab=cfg_kw["vocab"], seq=cfg_kw["seq_len"], mbs=1)
+    rng = np.random.default_rng(0)
+    params = og.init_params(oc, rng)
+    tokens = og.init_tokens(oc, 1, rng)
+    t0 = time.perf_counter()
+    og.run_reference_gpt(params, tokens, oc)
+    dt = time.perf_counter() - t0
+    ntok = oc["seq"]
+    return {"value": round(ntok / dt, 2), "unit": "tokens/s", "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"oracle/gpt.py float64 numpy fwd+bwd+SGD of GPT-2-small, 1 sequence x "
+                      f"{ntok} tokens ({dt:.1f} s)"}
+
+
+def run_reference_impl(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path (the
+    numpy oracle port; the Python reference cannot travel to the GPU box)."""
+    if rank != 0:
+        return 0
+    from oracle import gpt as og
+    oc = dict(layers=C2["layers"], d=C2["d_model"], heads=C2["n_heads"], ff=C2["d_ff"],
+              vocab=C2["vocab"], seq=C2["seq_len"], mbs=1)
+    rng = np.random.default_rng(0)
+    params = og.init_params(oc, rng)
+    tokens = og.init_tokens(oc, 1, rng)
+    for _ in range(args.warmup):
+        og.gpt_step(params, tokens[0], oc)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        og.run_reference_gpt(params, tokens, oc)
+        times.append(time.perf_counter() - t0)
+    ms = 1000 * float(np.mean(times))
+    tok_s = oc["seq"] / (ms / 1000)
+    from paper_2412_14374_b200.ir import GPTConfig
+    cfg = GPTConfig(**C2)
+    line = {
+        "impl": "reference", "metric": "tokens/s (model TFLOPS/GPU alongside)",
+        "value": round(tok_s, 2), "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024, 1F1B",
+                   "sample": "1 sequence x 1024 tokens per step (bounded CPU sample)"},
+        "model_tflops_per_gpu": round(cfg.flops_per_token() * tok_s / 1e12, 5),
+        "cpu_baseline": {"value": round(tok_s, 2), "unit": "tokens/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": "oracle/gpt.py float64 numpy, 1 x 1024 tokens per step"},
+        "e2e": {"value": round(tok_s, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--microbatches", type=int, default=M_MICRO)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_impl(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2412_14374_b200 import _lib
+    from paper_2412_14374_b200.executor import PipelineEngine
+
+    P = world
+    M = args.microbatches
+    cfg, tg, cp = build_plan(P, C2, M)
+    dev = torch.device("cuda", local)
+    params = init_params_device(cfg, dev)
+    rng = np.random.default_rng(1234)
+    tokens_host = rng.integers(0, cfg.vocab, size=(M * cfg.microbatch_size, cfg.seq_len),
+                               dtype=np.int32)
+    tokens_dev = torch.from_numpy(tokens_host).to(dev)
+    tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
+    eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
+    run = lambda b: eng.step(params, b, lr=1e-4, timeout_s=600, to_host=False)
+
+    for _ in range(max(args.warmup, 3)):
+        run(tokens_dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    # ---- device-resident timed region ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    launches0 = _lib.launch_count
+    t0 = time.perf_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        run(tokens_dev)
+    ev1.record()
+    barrier()
+    wall = time.perf_counter() - t0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    launches = int((_lib.launch_count - launches0) / args.steps)
+    clk = clocks.stop()
+
+    # ---- e2e through the public API: pinned host tokens -> device, losses -> host ----
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        res = eng.step(params, tokens_pinned, lr=1e-4, timeout_s=600, to_host=False)
+        if res.losses is not None:
+            res.losses.cpu()
+    e1.record()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    # ---- one instrumented step for the bubble ----
+    eng_tl = PipelineEngine(cp, tg, mode="bf16", gpt=cfg, timeline=True)
+    eng_tl.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False)
+    timeline = eng_tl.stats.timeline
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, timeline)
+        timeline = [e for part in gathered for e in part]
+    from paper_2412_14374_b200.executor import RunStats
+    bubble = RunStats(timeline=timeline).bubble_fraction(P)
+    # per-GPU busy time in the loop window, for the balance diagnostic
+    eng_tl.close()
+
+    tokens_per_step = M * cfg.tokens
+    value = tokens_per_step / (ms / 1000)
+    e2e = tokens_per_step / (e2e_ms / 1000)
+    flops_step = cfg.flops_per_token() * tokens_per_step
+    tflops_gpu = flops_step / (ms / 1000) / P / 1e12
+    burst, sustained, hbm, peak_kind = peaks()
+    ideal = (P - 1) / (M + P - 1)
+
+    if rank == 0:
+        stage_blocks = sum(1 for op in tg.partition.fwd_programs[0].ops if op.kind == "gpt-block")
+        roof = gemm_roofline(cfg, P, stage_blocks, ms, burst)
+        roof["peak_kind"] = peak_kind
+        cpu = None if args.no_cpu_baseline else cpu_baseline(C2)
+        line = {
+            "metric": "tokens/s (model TFLOPS/GPU and bubble alongside)",
+            "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic tokens, random-init weights",
+            "config": {"workload": "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024",
+                       "global_batch": M * cfg.microbatch_size, "seq_len": cfg.seq_len,
+                       "microbatches": M, "microbatch_size": cfg.microbatch_size,
+                       "schedule": "1f1b", "stages": P, "yields": list(cfg.yields or []),
+                       "parallelism": f"pp{P}", "l2": "inputs > L2 (no flush needed)"},
+            "model_tflops_per_gpu": round(tflops_gpu, 1),
+            "frac_of_bf16_peak": round(tflops_gpu / burst, 4),
+            "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e, 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(tokens_host.nbytes), "d2h_bytes_per_step": 4 * M},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "wall_s": round(wall, 3),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -110,7 +110,17 @@ def exported_symbols() -> list[str]:
     return ["pc_last_error", *SIGNATURES]
 
 
+# C-ABI calls that launch at least one kernel, counted for bench.py's gpu_launches.
+_NON_LAUNCH = {"pc_version", "pc_device_sm_count", "pc_gemm_set_tile_n", "pc_attention_set_impl",
+               "pc_embedding_bwd_workspace_bytes", "pc_p2p_available", "pc_p2p_unique_id",
+               "pc_p2p_comm_init", "pc_p2p_abort", "pc_p2p_destroy"}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
+    if name not in _NON_LAUNCH:
+        launch_count += 1
     rc = getattr(lib(), name)(*args)
     if rc != 0:
         msg = lib().pc_last_error().decode(errors="replace")

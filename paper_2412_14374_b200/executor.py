@@ -163,10 +163,13 @@ class LocalChannel:
 
     def __init__(self, src: int, dst: int):
         self.src, self.dst = src, dst
+        self.cond = threading.Condition()
+        self.reset()
+
+    def reset(self):
         self.q: deque = deque()
         self.mailbox: dict[int, tuple] = {}
         self.consumed: set[int] = set()
-        self.cond = threading.Condition()
 
     def send(self, seq: int, bid: str, value, stream: torch.cuda.Stream):
         ev = torch.cuda.Event()
@@ -234,6 +237,9 @@ class NcclChannel:
         self.comm = comm
         self.stream = torch.cuda.Stream(device=device)
         self.wire_meta = wire_meta
+        self.reset()
+
+    def reset(self):
         self.sent: dict[int, torch.cuda.Event] = {}
         self.posted: dict[int, tuple] = {}
         self.last_seq = -1
@@ -365,13 +371,13 @@ class DeviceStore:
 
 
 class _Actor:
-    def __init__(self, actor: int, tg: TaskGraph, mode: Mode, device: torch.device,
-                 gpt: GPTConfig | None, stats: RunStats, timeline: bool):
+    def __init__(self, actor: int, tg: TaskGraph, ops: DeviceOps, stats: RunStats,
+                 timeline: bool):
         self.actor = actor
         self.tg = tg
-        self.device = device
-        self.stream = torch.cuda.Stream(device=device)
-        self.ops = DeviceOps(tg.partition, mode, device, self.stream, gpt)
+        self.device = ops.device
+        self.stream = ops.stream
+        self.ops = ops
         self.store = DeviceStore(actor, tg, stats)
         self.timeline = timeline
         self.events: list = []
@@ -548,6 +554,9 @@ class PipelineEngine:
                 raise ExecutorFault("single-process multi-GPU channels are not supported; "
                                     "launch one process per GPU (torchrun)")
         self._wire_meta = _wire_meta_fn(tg, self.mode)
+        self._ops = {a: DeviceOps(tg.partition, self.mode, self.devices[a],
+                                  torch.cuda.Stream(device=self.devices[a]), gpt)
+                     for a in self.local}
         self._channels = self._make_channels()
 
     def _make_channels(self):
@@ -611,8 +620,9 @@ class PipelineEngine:
              strict_store: bool = True, to_host: bool = True) -> ExecutionResult:
         stats = RunStats()
         ctl = _Control(timeout_s)
-        actors = {a: _Actor(a, self.tg, self.mode, self.devices[a], self.gpt, stats,
-                            self.timeline) for a in self.local}
+        for ch in self._channels.values():
+            ch.reset()
+        actors = {a: _Actor(a, self.tg, self._ops[a], stats, self.timeline) for a in self.local}
         for a, act in actors.items():
             # params / inputs are copied on the current stream; the actor stream waits
             with torch.cuda.device(act.device):

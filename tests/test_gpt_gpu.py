@@ -177,8 +177,9 @@ def test_embedding_kernels_deterministic():
     st = torch.cuda.current_stream().cuda_stream
     tt = torch.tensor(tokens, device="cuda")
     out = torch.empty(T_, d, device="cuda")
-    _lib.call("pc_embedding_fwd", _lib.PC_F32, T_, d, seq, tt.data_ptr(), _t(wte).data_ptr(),
-              _t(wpe).data_ptr(), out.data_ptr(), st)
+    twte, twpe, tdh = _t(wte), _t(wpe), _t(dh)   # keep alive across the async launches
+    _lib.call("pc_embedding_fwd", _lib.PC_F32, T_, d, seq, tt.data_ptr(), twte.data_ptr(),
+              twpe.data_ptr(), out.data_ptr(), st)
     torch.cuda.synchronize()
     ref = wte[tokens] + wpe[np.arange(T_) % seq]
     assert ffn.rel(out.cpu().numpy(), ref) < 1e-6
@@ -190,7 +191,7 @@ def test_embedding_kernels_deterministic():
     for _ in range(2):
         dwte = torch.empty(V, d, device="cuda")
         dwpe = torch.empty(seq, d, device="cuda")
-        _lib.call("pc_embedding_bwd", _lib.PC_F32, T_, d, seq, V, tt.data_ptr(), _t(dh).data_ptr(),
+        _lib.call("pc_embedding_bwd", _lib.PC_F32, T_, d, seq, V, tt.data_ptr(), tdh.data_ptr(),
                   dwte.data_ptr(), dwpe.data_ptr(), ws.data_ptr(), nb.value, st)
         torch.cuda.synchronize()
         outs.append((dwte.cpu().numpy(), dwpe.cpu().numpy()))
