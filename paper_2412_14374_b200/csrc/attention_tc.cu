@@ -493,11 +493,13 @@ __global__ void __launch_bounds__(128) fa_bwd_dq(const bf16* __restrict__ qkv, i
   }
 }
 
-template <typename K>
-int set_smem(K kernel, int bytes) {
+// One flag per kernel instantiation (kernels with equal signatures share a
+// function-pointer type, so the flag must be keyed on the kernel itself).
+template <auto Kernel>
+int set_smem(int bytes) {
   static bool done = false;
   if (!done) {
-    PP_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PP_CUDA_TRY(cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     done = true;
   }
   return PC_OK;
@@ -507,7 +509,7 @@ template <int HD>
 int fwd_impl(int B, int H, int S, const void* qkv, int64_t ldq, void* o, int64_t ldo, float* lse,
              cudaStream_t st) {
   using C = FwdCfg<HD>;
-  int rc = set_smem(fa_fwd<HD>, C::SMEM);
+  int rc = set_smem<fa_fwd<HD>>(C::SMEM);
   if (rc) return rc;
   dim3 grid((S + C::BM - 1) / C::BM, B * H);
   const float sl2 = LOG2E / sqrtf(static_cast<float>(HD));
@@ -522,9 +524,9 @@ int bwd_impl(int B, int H, int S, const void* qkv, int64_t ldq, const void* o, c
   using C = BwdCfg<HD>;
   int rc = attention_delta(PC_BF16, B, H, S, HD, o, dO, ldo, delta, st);
   if (rc) return rc;
-  rc = set_smem(fa_bwd_dkdv<HD>, C::SMEM_KV);
+  rc = set_smem<fa_bwd_dkdv<HD>>(C::SMEM_KV);
   if (rc) return rc;
-  rc = set_smem(fa_bwd_dq<HD>, C::SMEM_Q);
+  rc = set_smem<fa_bwd_dq<HD>>(C::SMEM_Q);
   if (rc) return rc;
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
   const float sl2 = scale * LOG2E;

@@ -510,6 +510,29 @@ def _worker(act: _Actor, instrs, tg: TaskGraph, channels: dict, ctl: _Control, d
 _ENGINE_IDS = itertools.count()
 
 
+def exchange_channel_ids(store, tag: str, me: int, channels, new_id) -> dict:
+    """Rendezvous for the per-directed-channel communicators.
+
+    For every plan channel (src, dst) this rank belongs to, the sender creates
+    the 128-byte NCCL unique id and publishes it under ``pp200/<tag>/src->dst``;
+    the receiver reads it.  Channels are visited in one global sorted order on
+    every rank, so the pairwise communicator inits that follow cannot wait on
+    each other in a cycle.  Returns {(src, dst): id bytes} for this rank.
+    """
+    out = {}
+    for src, dst in sorted(channels):
+        if me not in (src, dst):
+            continue
+        key = f"pp200/{tag}/{src}->{dst}"
+        if me == src:
+            raw = new_id()
+            store.set(key, raw)
+        else:
+            raw = store.get(key)
+        out[(src, dst)] = bytes(raw)
+    return out
+
+
 def _dist_world():
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
@@ -562,24 +585,22 @@ class PipelineEngine:
     def _make_channels(self):
         if not self.distributed:
             return {key: LocalChannel(*key) for key in self.cp.channels}
+        import ctypes
+
         import torch.distributed as dist
         store = dist.distributed_c10d._get_default_store()
         tag = next(_ENGINE_IDS)
         me = self.local[0]
         dev = self.devices[me]
+
+        def new_id() -> bytes:
+            uid = (ctypes.c_char * 128)()
+            _lib.call("pc_p2p_unique_id", uid)
+            return bytes(uid)
+
         out = {}
-        import ctypes
-        for src, dst in sorted(self.cp.channels):
-            if me not in (src, dst):
-                continue
-            key = f"pp200/e{tag}/{src}->{dst}"
-            if me == src:
-                uid = (ctypes.c_char * 128)()
-                _lib.call("pc_p2p_unique_id", uid)
-                store.set(key, bytes(uid))
-                raw = bytes(uid)
-            else:
-                raw = store.get(key)
+        for (src, dst), raw in exchange_channel_ids(store, f"e{tag}", me, self.cp.channels,
+                                                    new_id).items():
             idbuf = (ctypes.c_char * 128).from_buffer_copy(raw)
             comm = ctypes.c_void_p()
             with torch.cuda.device(dev):
