@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(const bf16* __restrict__ qkv,
           const int ql = nt * 8 + tg * 2 + (e & 1);
           const int q = m0 + ql;
           const int key = e < 2 ? keyA : keyB;
-          const float p = (q >= key && q < S) ? exp2f(st[nt][e] * sl2 - sLb[ql]) : 0.f;
+          const float p = (q >= key && q < S) ? exp2f(st[nt][e] * sl2 - sLb[ql] * LOG2E) : 0.f;
           st[nt][e] = p;
           dpt[nt][e] = p * (dpt[nt][e] - sDb[ql]);
         }
