@@ -345,18 +345,16 @@ def main():
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
-    # ---- one instrumented step for the bubble ----
-    eng_tl = PipelineEngine(cp, tg, mode="bf16", gpt=cfg, timeline=True)
-    eng_tl.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False)
-    timeline = eng_tl.stats.timeline
+    # ---- one instrumented step (same warmed engine) for the bubble ----
+    barrier()
+    timeline = eng.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False,
+                        timeline=True).stats.timeline
     if world > 1:
         gathered = [None] * world
         dist.all_gather_object(gathered, timeline)
         timeline = [e for part in gathered for e in part]
     from paper_2412_14374_b200.executor import RunStats
     bubble = RunStats(timeline=timeline).bubble_fraction(P)
-    # per-GPU busy time in the loop window, for the balance diagnostic
-    eng_tl.close()
 
     tokens_per_step = M * cfg.tokens
     value = tokens_per_step / (ms / 1000)

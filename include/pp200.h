@@ -81,7 +81,10 @@ int pc_sumsq_half(int dtype, int64_t n, const void* x, void* out, void* stream);
 int pc_sum_f32(int64_t n, const float* x, float* out, void* stream);
 /* out[c] (+)= sum_r x[r,c]: "sum-to" (executor.py:50-56) and bias gradients. */
 int pc_col_sum(int dtype_in, int dtype_out, int64_t rows, int64_t cols, const void* x,
-               int64_t ldx, void* out, int accumulate, void* stream);
+               int64_t ldx, void* out, int accumulate, void* ws, int64_t ws_bytes, void* stream);
+/* Scratch for the two-stage (many-CTA, fixed-order) column reductions used by
+ * pc_col_sum and pc_layernorm_bwd; with ws == NULL they fall back to one stage. */
+int pc_reduce_workspace_bytes(int64_t rows, int64_t cols, int64_t* bytes);
 /* dst = src or src^T (slice / concat / broadcast materialisation, :78-95). */
 int pc_copy2d(int dtype, int64_t rows, int64_t cols, const void* src, int64_t lds, int trans,
               void* dst, int64_t ldd, void* stream);
@@ -101,7 +104,8 @@ int pc_layernorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const fl
 /* dx = dres + LN_bwd(dy); dgamma, dbeta written (fp32). dres may be NULL. */
 int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
                      const float* gamma, const float* mean, const float* rstd, const void* dres,
-                     void* dx, float* dgamma, float* dbeta, void* stream);
+                     void* dx, float* dgamma, float* dbeta, void* ws, int64_t ws_bytes,
+                     void* stream);
 int pc_embedding_fwd(int dtype, int64_t T, int64_t d, int64_t seq, const int32_t* tokens,
                      const float* wte, const float* wpe, void* out, void* stream);
 int pc_embedding_bwd_workspace_bytes(int64_t T, int64_t* bytes);

@@ -243,6 +243,88 @@ __global__ void __launch_bounds__(512) xent_kernel(int64_t rows, int V, int seq,
   }
 }
 
+
+// (m, s) running softmax statistics merge
+__device__ __forceinline__ void ms_merge(float& m, float& s, float mo, float so) {
+  const float mn = fmaxf(m, mo);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+  m = mn;
+}
+
+// bf16 rows with V % 8 == 0 and 16 B aligned rows: 16-byte loads and stores.
+__global__ void __launch_bounds__(512) xent_bf16_vec_kernel(int64_t rows, int V, int seq,
+                                                            __nv_bfloat16* logits, int64_t ld,
+                                                            const int32_t* __restrict__ tok,
+                                                            float* __restrict__ row_loss) {
+  __shared__ float sm[16], ss[16];
+  __shared__ float s_lse;
+  const int64_t r = blockIdx.x;
+  uint4* row = reinterpret_cast<uint4*>(logits + r * ld);
+  const int nv = V / 8;
+  const bool valid = (r % seq) != seq - 1;
+  if (!valid) {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int c = threadIdx.x; c < nv; c += blockDim.x) row[c] = z;
+    if (threadIdx.x == 0) row_loss[r] = 0.f;
+    return;
+  }
+  const int target = tok[r + 1];
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    const uint4 u = row[c];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    }
+    float bm = v[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) bm = fmaxf(bm, v[j]);
+    float bs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bs += __expf(v[j] - bm);
+    ms_merge(m, s, bm, bs);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    ms_merge(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sm[w] = m;
+    ss[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < nw ? sm[threadIdx.x] : -INFINITY;
+    s = threadIdx.x < nw ? ss[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      ms_merge(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
+    if (threadIdx.x == 0) {
+      const float lse = m + logf(s);
+      s_lse = lse;
+      row_loss[r] = lse - __bfloat162float(logits[r * ld + target]);
+    }
+  }
+  __syncthreads();
+  const float lse = s_lse;
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    uint4 u = row[c];
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      float p0 = __expf(f.x - lse), p1 = __expf(f.y - lse);
+      if (c * 8 + 2 * j == target) p0 -= 1.f;
+      if (c * 8 + 2 * j + 1 == target) p1 -= 1.f;
+      h[j] = __floats2bfloat162_rn(p0, p1);
+    }
+    row[c] = u;
+  }
+}
 }  // namespace
 }  // namespace pp200
 
@@ -268,15 +350,23 @@ extern "C" int pc_layernorm_fwd(int dtype, int64_t rows, int64_t d, const void* 
   return check_launch("layernorm_fwd");
 }
 
+namespace pp200 {
+template <typename T>
+bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda, const T* x,
+                   const float* mean, const float* rstd, float* out1, float* out2,
+                   int accumulate, void* ws, int64_t ws_bytes, cudaStream_t st);
+}
+
 extern "C" int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
                                 const float* gamma, const float* mean, const float* rstd,
                                 const void* dres, void* dx, float* dgamma, float* dbeta,
-                                void* stream) {
+                                void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= 0) return PC_OK;
   PP_DISPATCH_FB(dtype, T,
     ln_bwd_dx_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
-    ln_bwd_param_kernel<T><<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), mean, rstd, dgamma, dbeta));
+    if (!colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), mean, rstd, dgamma, dbeta, 0, ws, ws_bytes, st))
+      ln_bwd_param_kernel<T><<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), mean, rstd, dgamma, dbeta));
   return check_launch("layernorm_bwd");
 }
 
@@ -338,6 +428,10 @@ extern "C" int pc_xent_fwd_bwd(int dtype, int64_t rows, int64_t V, int64_t seq, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= 0) return PC_OK;
   PP_CHECK_ARG(rows % seq == 0, "xent: rows must be a multiple of seq");
+  if (dtype == PC_BF16 && V % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+    xent_bf16_vec_kernel<<<(unsigned)rows, 512, 0, st>>>(rows, (int)V, (int)seq, static_cast<__nv_bfloat16*>(logits), ld, tokens, row_loss);
+    return check_launch("xent_vec");
+  }
   PP_DISPATCH_FB(dtype, T, xent_kernel<T><<<(unsigned)rows, 512, 0, st>>>(rows, (int)V, (int)seq, static_cast<T*>(logits), ld, tokens, row_loss));
   return check_launch("xent");
 }

@@ -136,6 +136,73 @@ __global__ void __launch_bounds__(1024) col_sum_kernel(int64_t rows, int64_t col
   }
 }
 
+// Two-stage deterministic column reduction over many CTAs.
+// Stage 1: grid (ceil(cols/64), R); a warp covers 64 columns (2 per lane) and
+// strides over the CTA's row chunk; the 8 warps combine in fixed order into
+// ws[chunk][col] (and ws2 for the LayerNorm second statistic).
+// MODE 0: s1 = sum x.   MODE 1 (LayerNorm params): s1 = sum dy*xhat, s2 = sum dy
+// with xhat = (x - mean[r]) * rstd[r].
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols, int64_t chunk,
+                                                     const T* __restrict__ a, int64_t lda,
+                                                     const T* __restrict__ x,
+                                                     const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd,
+                                                     float* __restrict__ ws1,
+                                                     float* __restrict__ ws2) {
+  __shared__ float sm1[8][64], sm2[8][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = blockIdx.x * 64ll + lane * 2;
+  const int64_t r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
+  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+  for (int64_t r = r0 + w; r < r1; r += 8) {
+    const T* ar = a + r * lda;
+    const float v0 = c0 < cols ? static_cast<float>(ldv(ar, c0)) : 0.f;
+    const float v1 = c0 + 1 < cols ? static_cast<float>(ldv(ar, c0 + 1)) : 0.f;
+    if (MODE == 0) {
+      a0 += v0;
+      a1 += v1;
+    } else {
+      const T* xr = x + r * lda;
+      const float mu = mean[r], rs = rstd[r];
+      const float x0 = c0 < cols ? (static_cast<float>(ldv(xr, c0)) - mu) * rs : 0.f;
+      const float x1 = c0 + 1 < cols ? (static_cast<float>(ldv(xr, c0 + 1)) - mu) * rs : 0.f;
+      a0 += v0 * x0;
+      a1 += v1 * x1;
+      b0 += v0;
+      b1 += v1;
+    }
+  }
+  sm1[w][lane * 2] = a0;
+  sm1[w][lane * 2 + 1] = a1;
+  if (MODE == 1) {
+    sm2[w][lane * 2] = b0;
+    sm2[w][lane * 2 + 1] = b1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int64_t c = blockIdx.x * 64ll + threadIdx.x;
+    float t1 = 0.f, t2 = 0.f;
+    for (int k = 0; k < 8; ++k) {
+      t1 += sm1[k][threadIdx.x];
+      if (MODE == 1) t2 += sm2[k][threadIdx.x];
+    }
+    if (c < cols) {
+      ws1[blockIdx.y * cols + c] = t1;
+      if (MODE == 1) ws2[blockIdx.y * cols + c] = t2;
+    }
+  }
+}
+
+__global__ void colred_stage2(int64_t nchunks, int64_t cols, const float* __restrict__ ws,
+                              float* __restrict__ out, int accumulate) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float t = 0.f;
+  for (int64_t k = 0; k < nchunks; ++k) t += ws[k * cols + c];
+  out[c] = accumulate ? out[c] + t : t;
+}
+
 template <typename T>
 __global__ void copy2d_kernel(int64_t rows, int64_t cols, const T* __restrict__ src, int64_t lds,
                               int trans, T* __restrict__ dst, int64_t ldd) {
@@ -186,6 +253,40 @@ __global__ void cast_kernel(int64_t n, const I* __restrict__ in, O* __restrict__
 }
 
 }  // namespace
+
+int64_t colred_chunks(int64_t rows) {
+  int64_t r = (rows + 63) / 64;
+  return r < 1 ? 1 : (r > 128 ? 128 : r);
+}
+int64_t colred_ws_bytes(int64_t rows, int64_t cols) { return 2 * colred_chunks(rows) * cols * 4; }
+
+// Sum over rows of a (MODE 0) or LayerNorm parameter statistics (MODE 1) into
+// out1 (/out2) via ws; returns false if ws is too small (caller falls back).
+template <typename T>
+bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda, const T* x,
+                   const float* mean, const float* rstd, float* out1, float* out2,
+                   int accumulate, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  if (ws == nullptr || ws_bytes < colred_ws_bytes(rows, cols) || rows <= 0) return false;
+  const int64_t R = colred_chunks(rows), chunk = (rows + R - 1) / R;
+  float* w1 = static_cast<float*>(ws);
+  float* w2 = w1 + R * cols;
+  dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(R));
+  if (mode == 0)
+    colred_stage1<T, 0><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2);
+  else
+    colred_stage1<T, 1><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2);
+  const unsigned g2 = static_cast<unsigned>((cols + 255) / 256);
+  colred_stage2<<<g2, 256, 0, st>>>(R, cols, w1, out1, accumulate);
+  if (mode == 1) colred_stage2<<<g2, 256, 0, st>>>(R, cols, w2, out2, 0);
+  return true;
+}
+template bool colred_launch<float>(int, int64_t, int64_t, const float*, int64_t, const float*,
+                                   const float*, const float*, float*, float*, int, void*, int64_t,
+                                   cudaStream_t);
+template bool colred_launch<__nv_bfloat16>(int, int64_t, int64_t, const __nv_bfloat16*, int64_t,
+                                           const __nv_bfloat16*, const float*, const float*,
+                                           float*, float*, int, void*, int64_t, cudaStream_t);
+
 }  // namespace pp200
 
 using namespace pp200;
@@ -226,10 +327,27 @@ extern "C" int pc_sum_f32(int64_t n, const float* x, float* out, void* stream) {
   return check_launch("sum_f32");
 }
 
+extern "C" int pc_reduce_workspace_bytes(int64_t rows, int64_t cols, int64_t* bytes) {
+  *bytes = colred_ws_bytes(rows, cols);
+  return PC_OK;
+}
+
 extern "C" int pc_col_sum(int dtype_in, int dtype_out, int64_t rows, int64_t cols, const void* x,
-                          int64_t ldx, void* out, int accumulate, void* stream) {
+                          int64_t ldx, void* out, int accumulate, void* ws, int64_t ws_bytes,
+                          void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cols <= 0) return PC_OK;
+  if (dtype_out == PC_F32 && (dtype_in == PC_BF16 || dtype_in == PC_F32)) {
+    const bool done =
+        dtype_in == PC_BF16
+            ? colred_launch<__nv_bfloat16>(0, rows, cols, static_cast<const __nv_bfloat16*>(x), ldx,
+                                           nullptr, nullptr, nullptr, static_cast<float*>(out),
+                                           nullptr, accumulate, ws, ws_bytes, st)
+            : colred_launch<float>(0, rows, cols, static_cast<const float*>(x), ldx, nullptr,
+                                   nullptr, nullptr, static_cast<float*>(out), nullptr, accumulate,
+                                   ws, ws_bytes, st);
+    if (done) return check_launch("col_sum");
+  }
   dim3 grid(static_cast<unsigned>((cols + 31) / 32));
   if (dtype_in == PC_BF16 && dtype_out == PC_F32) {
     col_sum_kernel<__nv_bfloat16, float><<<grid, 1024, 0, st>>>(rows, cols, static_cast<const __nv_bfloat16*>(x), ldx, static_cast<float*>(out), accumulate);

@@ -138,8 +138,18 @@ class DeviceOps:
             self._elay = gpt.embed_layout()
             self._blay = {False: gpt.block_layout(False), True: gpt.block_layout(True)}
         self._emb_ws = None
+        self._red = None
 
     # ------------------------------------------------------------------ alloc
+    def red_ws(self, rows: int, cols: int) -> tuple[int, int]:
+        """Scratch for the two-stage column reductions (kept per actor; reuse
+        is ordered by the actor's single compute stream)."""
+        nb = ctypes.c_int64(0)
+        call("pc_reduce_workspace_bytes", rows, cols, ctypes.byref(nb))
+        if self._red is None or self._red.numel() < nb.value:
+            self._red = self.empty((nb.value,), torch.uint8)
+        return self._red.data_ptr(), self._red.numel()
+
     def empty(self, shape, dtype) -> torch.Tensor:
         return torch.empty(shape, dtype=dtype, device=self.device)
 
@@ -303,7 +313,7 @@ class DeviceOps:
         if x.dim() == 2 and (dims == (x.shape[1],) or dims == (1, x.shape[1])):
             out = self.empty(dims, x.dtype)
             call("pc_col_sum", _PC[x.dtype], _PC[x.dtype], x.shape[0], x.shape[1], x.data_ptr(),
-                 x.shape[1], out.data_ptr(), 0, self.st)
+                 x.shape[1], out.data_ptr(), 0, None, 0, self.st)
             return out
         if len(dims) == 0 or math.prod(dims) == 1:
             out = self.empty(dims, x.dtype)
@@ -313,7 +323,7 @@ class DeviceOps:
                  tmp.data_ptr(), flat.shape[1], self.st)
             col = tmp.reshape(-1, 1)
             call("pc_col_sum", _PC[x.dtype], _PC[x.dtype], col.shape[0], 1, col.data_ptr(), 1,
-                 out.data_ptr(), 0, self.st)
+                 out.data_ptr(), 0, None, 0, self.st)
             return out
         raise ValueError(f"sum-to {tuple(x.shape)} -> {dims} unsupported on device")
 
@@ -497,30 +507,30 @@ class DeviceOps:
             dout = self.empty((T, d), act)
             call("pc_layernorm_bwd", self.mode.pc_act, T, d, dz.data_ptr(), sv["out"].data_ptr(),
                  ms("lnf_g").data_ptr(), sv["meanf"].data_ptr(), sv["rstdf"].data_ptr(), None,
-                 dout.data_ptr(), gs("lnf_g").data_ptr(), gs("lnf_b").data_ptr(), self.st)
+                 dout.data_ptr(), gs("lnf_g").data_ptr(), gs("lnf_b").data_ptr(), *self.red_ws(T, d), self.st)
         else:
             dout = dz
         # MLP
         self._gemm(f32, 1, 0, d, f, T, dout, d, sv["gu"], f, gs("w_fc2"), f)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dout.data_ptr(), d,
-             gs("b_fc2").data_ptr(), 0, self.st)
+             gs("b_fc2").data_ptr(), 0, *self.red_ws(T, d), self.st)
         du = self.empty((T, f), act)
         self._gemm(act, 0, 0, T, f, d, dout, d, sl("w_fc2"), f, du, f, _lib.EPI_GELU_GRAD,
                    aux=sv["u"], ldaux=f)
         self._gemm(f32, 1, 0, f, d, T, du, f, sv["a2"], d, gs("w_fc1"), d)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, f, du.data_ptr(), f,
-             gs("b_fc1").data_ptr(), 0, self.st)
+             gs("b_fc1").data_ptr(), 0, *self.red_ws(T, f), self.st)
         da2 = self.empty((T, d), act)
         self._gemm(act, 0, 0, T, d, f, du, f, sl("w_fc1"), d, da2, d)
         dh1 = self.empty((T, d), act)
         call("pc_layernorm_bwd", self.mode.pc_act, T, d, da2.data_ptr(), sv["h1"].data_ptr(),
              ms("ln2_g").data_ptr(), sv["mean2"].data_ptr(), sv["rstd2"].data_ptr(),
              dout.data_ptr(), dh1.data_ptr(), gs("ln2_g").data_ptr(), gs("ln2_b").data_ptr(),
-             self.st)
+             *self.red_ws(T, d), self.st)
         # attention
         self._gemm(f32, 1, 0, d, d, T, dh1, d, sv["o"], d, gs("w_o"), d)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dh1.data_ptr(), d,
-             gs("b_o").data_ptr(), 0, self.st)
+             gs("b_o").data_ptr(), 0, *self.red_ws(T, d), self.st)
         do = self.empty((T, d), act)
         self._gemm(act, 0, 0, T, d, d, dh1, d, sl("w_o"), d, do, d)
         dqkv = self.empty((T, 3 * d), act)
@@ -530,14 +540,14 @@ class DeviceOps:
              sv["lse"].data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, self.st)
         self._gemm(f32, 1, 0, 3 * d, d, T, dqkv, 3 * d, sv["a"], d, gs("w_qkv"), d)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, 3 * d, dqkv.data_ptr(), 3 * d,
-             gs("b_qkv").data_ptr(), 0, self.st)
+             gs("b_qkv").data_ptr(), 0, *self.red_ws(T, 3 * d), self.st)
         da = self.empty((T, d), act)
         self._gemm(act, 0, 0, T, d, 3 * d, dqkv, 3 * d, sl("w_qkv"), d, da, d)
         dh = self.empty((T, d), act)
         call("pc_layernorm_bwd", self.mode.pc_act, T, d, da.data_ptr(), h.data_ptr(),
              ms("ln1_g").data_ptr(), sv["mean1"].data_ptr(), sv["rstd1"].data_ptr(),
              dh1.data_ptr(), dh.data_ptr(), gs("ln1_g").data_ptr(), gs("ln1_b").data_ptr(),
-             self.st)
+             *self.red_ws(T, d), self.st)
         return (dh, dW)
 
     def _head_fwd(self, op, env):

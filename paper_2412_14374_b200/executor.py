@@ -638,12 +638,14 @@ class PipelineEngine:
                 act.store.put(bid, v)
 
     def step(self, params, batch, lr: float = 0.1, timeout_s: float = 30.0, delay_fn=None,
-             strict_store: bool = True, to_host: bool = True) -> ExecutionResult:
+             strict_store: bool = True, to_host: bool = True,
+             timeline: bool | None = None) -> ExecutionResult:
         stats = RunStats()
+        tl = self.timeline if timeline is None else timeline
         ctl = _Control(timeout_s)
         for ch in self._channels.values():
             ch.reset()
-        actors = {a: _Actor(a, self.tg, self._ops[a], stats, self.timeline) for a in self.local}
+        actors = {a: _Actor(a, self.tg, self._ops[a], stats, tl) for a in self.local}
         for a, act in actors.items():
             # params / inputs are copied on the current stream; the actor stream waits
             with torch.cuda.device(act.device):

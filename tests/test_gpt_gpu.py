@@ -147,12 +147,32 @@ def test_layernorm_and_xent_kernels():
     tdb = torch.empty(d, device="cuda")
     _lib.call("pc_layernorm_bwd", _lib.PC_F32, rows, d, tdy.data_ptr(), tx.data_ptr(),
               tg_.data_ptr(), mean.data_ptr(), rstd.data_ptr(), None, tdx.data_ptr(),
-              tdg.data_ptr(), tdb.data_ptr(), st)
+              tdg.data_ptr(), tdb.data_ptr(), None, 0, st)
+    # the many-CTA two-stage reduction (with workspace) gives the same parameter grads
+    import ctypes
+    nb = ctypes.c_int64()
+    _lib.call("pc_reduce_workspace_bytes", rows, d, ctypes.byref(nb))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    tdg2, tdb2 = torch.empty(d, device="cuda"), torch.empty(d, device="cuda")
+    _lib.call("pc_layernorm_bwd", _lib.PC_F32, rows, d, tdy.data_ptr(), tx.data_ptr(),
+              tg_.data_ptr(), mean.data_ptr(), rstd.data_ptr(), None, tdx.data_ptr(),
+              tdg2.data_ptr(), tdb2.data_ptr(), ws.data_ptr(), nb.value, st)
     torch.cuda.synchronize()
     assert ffn.rel(ty.cpu().numpy(), y) < 1e-5
     assert ffn.rel(tdx.cpu().numpy(), dx) < 1e-5
     assert ffn.rel(tdg.cpu().numpy(), dg) < 1e-5
     assert ffn.rel(tdb.cpu().numpy(), db) < 1e-5
+    assert ffn.rel(tdg2.cpu().numpy(), dg) < 1e-5
+    assert ffn.rel(tdb2.cpu().numpy(), db) < 1e-5
+    # column sums (bias gradients), single- and two-stage
+    cs1, cs2 = torch.empty(d, device="cuda"), torch.empty(d, device="cuda")
+    _lib.call("pc_col_sum", _lib.PC_F32, _lib.PC_F32, rows, d, tdy.data_ptr(), d, cs1.data_ptr(),
+              0, None, 0, st)
+    _lib.call("pc_col_sum", _lib.PC_F32, _lib.PC_F32, rows, d, tdy.data_ptr(), d, cs2.data_ptr(),
+              0, ws.data_ptr(), nb.value, st)
+    torch.cuda.synchronize()
+    assert ffn.rel(cs1.cpu().numpy(), dy.sum(0)) < 1e-5
+    assert ffn.rel(cs2.cpu().numpy(), dy.sum(0)) < 1e-5
     # cross-entropy against the oracle head (identity "wte" so logits = h)
     h = rng.standard_normal((rows, V))
     tokens = rng.integers(0, V, size=(rows // seq, seq)).astype(np.int32)
@@ -202,3 +222,20 @@ def test_embedding_kernels_deterministic():
     assert ffn.rel(outs[0][0], want_te) < 1e-5
     assert ffn.rel(outs[0][1], want_pe) < 1e-5
     assert np.array_equal(outs[0][0], outs[1][0])
+
+
+def test_xent_bf16_vectorised_path():
+    rows, V, seq = 96, 136, 24
+    rng = np.random.default_rng(6)
+    h = rng.standard_normal((rows, V)) * 2
+    tokens = rng.integers(0, V, size=(rows // seq, seq)).astype(np.int32)
+    tl = _t(h, torch.bfloat16)
+    hb = tl.double().cpu().numpy()
+    loss, dh, _ = gpt.head_loss(hb, np.eye(V), tokens)
+    tt = torch.tensor(tokens, device="cuda")
+    row_loss = torch.empty(rows, device="cuda")
+    _lib.call("pc_xent_fwd_bwd", _lib.PC_BF16, rows, V, seq, tl.data_ptr(), V, tt.data_ptr(),
+              row_loss.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert abs(row_loss.sum().item() - loss) < 1e-4 * abs(loss)
+    assert ffn.rel(tl.double().cpu().numpy(), dh) < 1e-2
