@@ -272,6 +272,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--microbatches", type=int, default=M_MICRO)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="issue every step from Python instead of replaying the captured graph")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -298,8 +300,15 @@ def main():
     tokens_dev = torch.from_numpy(tokens_host).to(dev)
     tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
     eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
-    run = lambda b: eng.step(params, b, lr=1e-4, timeout_s=600, to_host=False)
-
+    use_graph = not args.no_graph
+    for _ in range(2):   # eager warm-up: NCCL connections, kernel attributes, allocator
+        eng.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False)
+    torch.cuda.synchronize()
+    if use_graph:
+        cap = eng.capture(params, tokens_dev, lr=1e-4)
+        run = lambda b: cap.replay(None if b is tokens_dev else b)
+    else:
+        run = lambda b: eng.step(params, b, lr=1e-4, timeout_s=600, to_host=False)
     for _ in range(max(args.warmup, 3)):
         run(tokens_dev)
     torch.cuda.synchronize()
@@ -330,7 +339,7 @@ def main():
     barrier()
     wall = time.perf_counter() - t0
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    launches = int((_lib.launch_count - launches0) / args.steps)
+    launches = cap.launches if use_graph else int((_lib.launch_count - launches0) / args.steps)
     clk = clocks.stop()
 
     # ---- e2e through the public API: pinned host tokens -> device, losses -> host ----
@@ -338,7 +347,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        res = eng.step(params, tokens_pinned, lr=1e-4, timeout_s=600, to_host=False)
+        res = run(tokens_pinned)
         if res.losses is not None:
             res.losses.cpu()
     e1.record()
@@ -347,8 +356,16 @@ def main():
 
     # ---- one instrumented step (same warmed engine) for the bubble ----
     barrier()
-    timeline = eng.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False,
-                        timeline=True).stats.timeline
+    if use_graph:
+        cap_tl = eng.capture(params, tokens_dev, lr=1e-4, timeline=True)
+        barrier()
+        cap_tl.replay()
+        barrier()
+        timeline = cap_tl.timeline()
+        del cap_tl
+    else:
+        timeline = eng.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False,
+                            timeline=True).stats.timeline
     if world > 1:
         gathered = [None] * world
         dist.all_gather_object(gathered, timeline)
@@ -379,7 +396,8 @@ def main():
                        "global_batch": M * cfg.microbatch_size, "seq_len": cfg.seq_len,
                        "microbatches": M, "microbatch_size": cfg.microbatch_size,
                        "schedule": "1f1b", "stages": P, "yields": list(cfg.yields or []),
-                       "parallelism": f"pp{P}", "l2": "inputs > L2 (no flush needed)"},
+                       "parallelism": f"pp{P}", "l2": "inputs > L2 (no flush needed)",
+                       "issue": "cuda-graph replay per actor" if use_graph else "python per op"},
             "model_tflops_per_gpu": round(tflops_gpu, 1),
             "frac_of_bf16_peak": round(tflops_gpu / burst, 4),
             "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4)},

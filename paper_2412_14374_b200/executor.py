@@ -181,7 +181,7 @@ class LocalChannel:
             self.q.append((seq, bid, strip(value), ev))
             self.cond.notify_all()
 
-    def post_recv(self, seq: int, bid: str):
+    def post_recv(self, seq: int, bid: str, stream=None):
         pass
 
     def recv(self, seq: int, ctl: _Control, actor: int, stream: torch.cuda.Stream):
@@ -261,8 +261,14 @@ class NcclChannel:
         done.record(self.stream)
         self.sent[seq] = done
 
-    def post_recv(self, seq: int, bid: str):
+    def post_recv(self, seq: int, bid: str, stream: torch.cuda.Stream | None = None):
         shape, dtype = self.wire_meta(bid)
+        if stream is not None and torch.cuda.is_current_stream_capturing():
+            # join the recv stream into the capture: the receive is posted in
+            # program order, which is exactly the checker's model of RecvStart
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            self.stream.wait_event(fork)
         with torch.cuda.stream(self.stream):
             buf = torch.empty(shape, dtype=dtype, device=self.stream.device)
         _lib.call("pc_p2p_recv", self.comm, buf.data_ptr(), buf.numel() * buf.element_size(), 0,
@@ -288,7 +294,11 @@ class NcclChannel:
 
     def is_consumed(self, seq: int) -> bool:
         ev = self.sent.get(seq)
-        return ev is None or ev.query()
+        if ev is None:
+            return True
+        if torch.cuda.is_current_stream_capturing():
+            return False  # resolved by the flush after capture
+        return ev.query()
 
     def drained(self) -> bool:
         return not self.posted
@@ -482,7 +492,7 @@ def _worker(act: _Actor, instrs, tg: TaskGraph, channels: dict, ctl: _Control, d
                 elif isinstance(ins, SendWait):
                     channels[(a, ins.dst)].wait_consumed(ins.seq, ctl, a, act.stream)
                 elif isinstance(ins, RecvStart):
-                    channels[(ins.src, a)].post_recv(ins.seq, ins.buffer)
+                    channels[(ins.src, a)].post_recv(ins.seq, ins.buffer, act.stream)
                 elif isinstance(ins, RecvWait):
                     bid, value = channels[(ins.src, a)].recv(ins.seq, ctl, a, act.stream)
                     act.store.received.add(bid)
@@ -688,6 +698,61 @@ class PipelineEngine:
             act.store.flush()
         return self._gather(actors, stats, strict_store, to_host)
 
+    def capture(self, params, batch, lr: float = 0.1, timeout_s: float = 600.0,
+                timeline: bool = False):
+        """Capture this process's actor program as one CUDA graph.
+
+        The host-side interpreter (store, deletions, channel bookkeeping) runs
+        once while every launch -- libpp200 kernels, NCCL sends/receives on the
+        channel streams, event waits -- is recorded; ``CapturedStep.replay``
+        then re-issues the whole fused program with a single launch (the
+        paper's one-dispatch-per-actor fusion, at zero host
+        cost).  Needs one actor per process (P=1, or a torchrun launch) and a
+        prior warm-up step (NCCL connects lazily).
+        """
+        if len(self.local) != 1:
+            raise ExecutorFault("graph capture needs exactly one actor per process")
+        a = self.local[0]
+        stats = RunStats()
+        ctl = _Control(timeout_s)
+        for ch in self._channels.values():
+            ch.reset()
+        act = _Actor(a, self.tg, self._ops[a], stats, timeline)
+        actors = {a: act}
+        with torch.cuda.device(act.device):
+            act.stream.wait_stream(torch.cuda.current_stream(act.device))
+        self._seed(actors, params, batch, lr)
+        inputs = {bid: v for bid, v in act.store.data.items()
+                  if self.tg.buffers[bid].kind not in (PARAM, OPT_STATE)}
+        lock = threading.Lock()
+
+        def counting(src, dst, bid):
+            with lock:
+                stats.channel_counts[(src, dst)] = stats.channel_counts.get((src, dst), 0) + 1
+                stats.sent_buffers.append((src, dst, bid))
+
+        if self.distributed:
+            import torch.distributed as dist
+            dist.barrier()
+        stats.driver_messages += 1
+        launches0 = _lib.launch_count
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.device(act.device):
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=act.stream):
+                _worker(act, self.cp.programs[a].instrs, self.tg, self._channels, ctl, None,
+                        counting)
+        if ctl.faults:
+            raise ctl.faults[0]
+        act.store.flush()
+        act_events, act.events = act.events, []
+        result = self._gather(actors, stats, strict_store=False, to_host=False)
+        cs = CapturedStep(self, graph, act, inputs, result)
+        cs.events = act_events
+        cs.base_event = act.base_event
+        cs.launches = _lib.launch_count - launches0   # libpp200 calls recorded per replay
+        return cs
+
     def _abort_channels(self):
         for ch in self._channels.values():
             ch.abort()
@@ -751,6 +816,46 @@ class PipelineEngine:
                 raise ExecutorFault(f"step outputs incomplete: grads missing {sorted(missing)}")
         self.stats = stats
         return ExecutionResult(grads=grads, losses=losses, new_params=new_params, stats=stats)
+
+
+class CapturedStep:
+    """A captured actor program: ``replay`` runs one full training step.
+
+    ``result`` holds the step outputs (grads, losses, new params on this
+    process's actor); their device memory belongs to the graph and is
+    rewritten by every replay.  ``set_inputs`` copies a new batch into the
+    graph's static input buffers (stream-ordered, before the replay)."""
+
+    def __init__(self, engine, graph, act, inputs, result):
+        self.engine, self.graph, self.act = engine, graph, act
+        self.inputs = inputs
+        self.result = result
+
+    def set_inputs(self, batch):
+        tg = self.engine.tg
+        M = tg.schedule.num_microbatches
+        mbs = split_batch(batch, M)
+        for bid, dst in self.inputs.items():
+            src = mbs[tg.buffers[bid].meta["microbatch"]]
+            if isinstance(src, np.ndarray):
+                src = torch.from_numpy(np.ascontiguousarray(src))
+            dst = tensor_of(dst)
+            dst.copy_(src.to(dst.dtype) if src.dtype != dst.dtype else src, non_blocking=True)
+
+    def replay(self, batch=None):
+        if batch is not None:
+            self.set_inputs(batch)
+        self.graph.replay()
+        return self.result
+
+    def timeline(self) -> list:
+        """(actor, kind, uid, start_ms, end_ms) of the last replay, when the
+        step was captured with ``timeline=True`` (event nodes in the graph)."""
+        if not getattr(self, "events", None) or self.base_event is None:
+            return []
+        a = self.act.actor
+        return [(a, kind, uid, self.base_event.elapsed_time(e0), self.base_event.elapsed_time(e1))
+                for kind, uid, e0, e1 in self.events]
 
 
 def split_batch(batch, M: int):
