@@ -65,6 +65,8 @@ int pc_gemm(int dtype_in, int dtype_out, int transA, int transB, int64_t M, int6
 
 /* Force the tcgen05 GEMM tile width (0 = heuristic, else 64/128/256). Test hook. */
 int pc_gemm_set_tile_n(int bn);
+/* 1 (default) = write C through smem + TMA bulk store when legal; 0 = direct stores. Test hook. */
+int pc_gemm_set_tma_store(int on);
 
 /* ---- elementwise / reductions (executor.py:59-96 numpy expressions) ---- */
 enum pc_ewise_op {
@@ -96,6 +98,8 @@ int pc_accumulate(int dtype_acc, int dtype_part, int64_t n, void* acc, const voi
 int pc_sgd_update(int dtype, int64_t n, const void* w, const void* g, double lr, void* w_out,
                   void* shadow_bf16, void* stream);
 int pc_cast(int dtype_in, int dtype_out, int64_t n, const void* in, void* out, void* stream);
+/* *slot = %globaltimer (ns), stream-ordered; the measured task timeline (bubble). */
+int pc_timestamp(void* slot, void* stream);
 
 /* ---- GPT vocabulary (oracle/gpt.py semantics; no reference counterpart) ---- */
 int pc_layernorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const float* gamma,

@@ -10,7 +10,9 @@
 //   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring (STAGES deep)
 //   warp 1      MMA issuer: one thread issues tcgen05.mma 128xBNx16 into TMEM
 //   warp 2      TMEM allocator (2 accumulator buffers of BN fp32 columns)
-//   warps 4..7  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue -> HBM
+//   warps 4..11 epilogue (2 per TMEM lane quarter, one per column half):
+//               tcgen05.ld TMEM -> registers -> fused epilogue -> 128B-swizzled
+//               smem stage -> TMA bulk tensor store (cp.async.bulk.tensor)
 // The two TMEM accumulators let the epilogue of tile i overlap the MMAs of
 // tile i+1.
 #include <cudaTypedefs.h>
@@ -25,11 +27,14 @@ namespace {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 384;  // 4 control warps + 8 epilogue warps
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_STAGE_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_MN_CHUNK_BYTES = TC_BK * 128;  // one 64-wide MN box of BK rows
 
 struct TcEpi {
+  int tma_c;  // C written through smem + TMA bulk tensor store
   void* C;
   int64_t ldc;
   const float* bias;
@@ -45,7 +50,8 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = TC_A_BYTES + B_BYTES;
   static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + TC_EPI_WARPS * TC_STAGE_BYTES +
+                               1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -112,7 +118,8 @@ __device__ __forceinline__ void store16(void* base, bool f32, int64_t off, int n
   }
 }
 
-__device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, float* v) {
+__device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, float* v,
+                                           bool store_c) {
   const int nvalid = min(16, ep.N - col);
   const bool f32 = ep.out_f32 != 0;
   const int fl = ep.flags;
@@ -131,7 +138,7 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
     store16(ep.aux_out, f32, static_cast<int64_t>(row) * ep.ldaux_out + col, nvalid, v);
     if (fl & PC_EPI_GELU) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = gelu_tanh(v[i]);
+      for (int i = 0; i < 16; ++i) v[i] = gelu_tanh_fast(v[i]);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
@@ -145,19 +152,24 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
       for (int i = 0; i < 16; ++i) v[i] += a[i];
     } else if (fl & PC_EPI_GELU_GRAD) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] *= gelu_tanh_grad(a[i]);
+      for (int i = 0; i < 16; ++i) v[i] *= gelu_tanh_grad_fast(a[i]);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = a[i] > 0.f ? v[i] : 0.f;
     }
   }
-  store16(ep.C, f32, static_cast<int64_t>(row) * ep.ldc + col, nvalid, v);
+  if (store_c) store16(ep.C, f32, static_cast<int64_t>(row) * ep.ldc + col, nvalid, v);
+}
+
+// 16 B chunk `j` of row `r` inside a 128B-swizzled [32 x 128 B] staging tile.
+__device__ __forceinline__ uint4* stage_chunk(uint8_t* stg, int r, int j) {
+  return reinterpret_cast<uint4*>(stg + r * 128 + ((j ^ (r & 7)) << 4));
 }
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int M, int N, int K, TcEpi ep) {
+                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, TcEpi ep) {
   using Cfg = TcCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -165,7 +177,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * TC_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint8_t* sEpi = sB + STAGES * Cfg::B_BYTES;  // 1024-aligned: 8 x 4 KB staging tiles
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + TC_EPI_WARPS * TC_STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -185,7 +198,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], TC_EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -262,7 +275,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // 8 epilogue warps: warp & 3 selects the TMEM lane quarter (rows), the
+    // warp-group half selects which half of the tile's columns it drains.
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    constexpr int HALF = BN / 2;
+    uint8_t* stg = sEpi + (warp - 4) * TC_STAGE_BYTES;
+    const bool f32 = ep.out_f32 != 0;
+    const bool tma = ep.tma_c != 0;
     int acc = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -273,14 +293,54 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t tb =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < HALF; c += 32) {
+        const int cc = half * HALF + c;
         uint32_t r[32];
-        tmem_ld16(tb + c, r);
-        tmem_ld16(tb + c + 16, r + 16);
+        tmem_ld16(tb + cc, r);
+        tmem_ld16(tb + cc + 16, r + 16);
         tc_wait_ld();
+        float* v = reinterpret_cast<float*>(r);
         if (row < M) {
-          if (n0 + c < N) epilogue16(ep, row, n0 + c, reinterpret_cast<float*>(r));
-          if (n0 + c + 16 < N) epilogue16(ep, row, n0 + c + 16, reinterpret_cast<float*>(r + 16));
+          if (n0 + cc < N) epilogue16(ep, row, n0 + cc, v, !tma);
+          if (n0 + cc + 16 < N) epilogue16(ep, row, n0 + cc + 16, v + 16, !tma);
+        }
+        if (!tma) continue;
+        if (f32) {
+          // 32 fp32 = one 128 B staging row per thread; one TMA box per chunk
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *stage_chunk(stg, lane, j) = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+            bulk_commit();
+          }
+        } else {
+          // 32 bf16 = half a staging row; a 64-column box is stored per two chunks
+          const int sub = (c >> 5) & 1;
+          if (sub == 0) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 u;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+            *stage_chunk(stg, lane, 4 * sub + j) = u;
+          }
+          if (sub == 1 || c + 32 >= HALF) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, stg, n0 + cc - 32 * sub, m0 + q * 32);
+              bulk_commit();
+            }
+          }
         }
       }
       tc_fence_before();
@@ -289,6 +349,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
+    if (tma && lane == 0) bulk_wait0();
   }
 
   tc_fence_before();
@@ -336,11 +397,36 @@ int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int
   return PC_OK;
 }
 
+// Store-side tensor map for C: [M, N] row-major, boxes of 128 B x 32 rows
+// (64 bf16 or 32 fp32 columns), 128B swizzle matching the staging tiles.
+int make_tmap_c(CUtensorMap* m, void* ptr, int64_t N, int64_t M, int64_t ldc, bool f32) {
+  auto enc = tmap_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return PC_ERR_CUDA;
+  }
+  const int es = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc * es)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (C) failed (%d)", static_cast<int>(r));
+    return PC_ERR_CUDA;
+  }
+  return PC_OK;
+}
+
 int g_force_bn = 0;
+int g_tma_store = 1;
 
 template <int BN, bool A_MN, bool B_MN>
-int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const TcEpi& ep,
-              cudaStream_t st) {
+int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, int M, int N,
+              int K, const TcEpi& ep, cudaStream_t st) {
   using Cfg = TcCfg<BN>;
   static bool attr_set = false;  // benign race: idempotent attribute write
   if (!attr_set) {
@@ -350,17 +436,17 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
   }
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
+  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, M, N, K, ep);
   return check_launch("tc_gemm_kernel");
 }
 
 template <int BN>
-int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb, int M,
-                    int N, int K, const TcEpi& ep, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, M, N, K, ep, st);
-  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, M, N, K, ep, st);
-  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, M, N, K, ep, st);
-  return launch_tc<BN, true, true>(ta, tb, M, N, K, ep, st);
+int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                    const CUtensorMap& tc, int M, int N, int K, const TcEpi& ep, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, tc, M, N, K, ep, st);
+  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, tc, M, N, K, ep, st);
+  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, tc, M, N, K, ep, st);
+  return launch_tc<BN, true, true>(ta, tb, tc, M, N, K, ep, st);
 }
 
 }  // namespace
@@ -398,12 +484,24 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   else
     rc = make_tmap(&tb, B, N, K, ldb, TC_BK);
   if (rc) return rc;
-  TcEpi ep{C, ldc, static_cast<const float*>(bias), aux, ldaux, aux_out, ldaux_out,
+  // C through smem + TMA store when legal: 16 B aligned rows, no read-modify-
+  // write epilogue, and bf16 boxes (64 columns) never straddle the two column
+  // halves drained by different warp groups (BN >= 128).
+  const int es = out_f32 ? 4 : 2;
+  const bool tma_c = g_tma_store && !(epi & PC_EPI_ACCUM) && (out_f32 || bn >= 128) &&
+                     (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
+  CUtensorMap tc;
+  memset(&tc, 0, sizeof(tc));
+  if (tma_c) {
+    rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0);
+    if (rc) return rc;
+  }
+  TcEpi ep{tma_c ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux, aux_out, ldaux_out,
            static_cast<int>(M), static_cast<int>(N), epi, out_f32};
   switch (bn) {
-    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, (int)M, (int)N, (int)K, ep, st);
-    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, (int)M, (int)N, (int)K, ep, st);
-    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, (int)M, (int)N, (int)K, ep, st);
+    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, (int)M, (int)N, (int)K, ep, st);
+    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, tc, (int)M, (int)N, (int)K, ep, st);
+    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, tc, (int)M, (int)N, (int)K, ep, st);
     default: set_error("gemm: bad tile width %d", bn); return PC_ERR_ARG;
   }
 }
@@ -416,5 +514,10 @@ extern "C" int pc_gemm_set_tile_n(int bn) {
     return PC_ERR_ARG;
   }
   pp200::g_force_bn = bn;
+  return PC_OK;
+}
+
+extern "C" int pc_gemm_set_tma_store(int on) {
+  pp200::g_tma_store = on ? 1 : 0;
   return PC_OK;
 }

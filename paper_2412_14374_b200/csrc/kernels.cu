@@ -432,3 +432,22 @@ extern "C" int pc_cast(int dtype_in, int dtype_out, int64_t n, const void* in, v
 #undef PP_CAST
   return check_launch("cast");
 }
+
+// ---------------------------------------------------------------------------
+// Device timestamps for the measured timeline (bubble fraction): one thread
+// writes %globaltimer (ns) into slot; works inside captured CUDA graphs.
+namespace pp200 {
+namespace {
+__global__ void timestamp_kernel(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+}  // namespace
+}  // namespace pp200
+
+extern "C" int pc_timestamp(void* slot, void* stream) {
+  pp200::timestamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<unsigned long long*>(slot));
+  return pp200::check_launch("timestamp");
+}

@@ -390,10 +390,25 @@ class _Actor:
         self.ops = ops
         self.store = DeviceStore(actor, tg, stats)
         self.timeline = timeline
-        self.events: list = []
-        self.base_event = None
+        self.events: list = []       # (kind, uid, start slot, end slot)
+        self.ts = None               # int64 device buffer of %globaltimer stamps
+        if timeline:
+            n = 2 * sum(1 for t in tg.tasks.values() if t.actor == actor) + 1
+            self.ts = torch.empty(n, dtype=torch.int64, device=self.device)
         self.end_event = None
         self.last_issued = -1
+
+    def stamp(self, slot: int):
+        _lib.call("pc_timestamp", self.ts.data_ptr() + 8 * slot, self.stream.cuda_stream)
+
+    def read_timeline(self) -> list:
+        """(actor, kind, uid, start_ms, end_ms) relative to this actor's program start."""
+        if self.ts is None:
+            return []
+        t = self.ts.cpu().tolist()
+        base = t[0]
+        return [(self.actor, kind, uid, (t[s0] - base) / 1e6, (t[s1] - base) / 1e6)
+                for kind, uid, s0, s1 in self.events]
 
     def run_task(self, task, at: str):
         ex = task.exec
@@ -401,8 +416,8 @@ class _Actor:
         st = self.store
         p = self.tg.partition
         if self.timeline:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e0.record(self.stream)
+            s0 = 1 + 2 * len(self.events)
+            self.stamp(s0)
         if kind == "stage-fwd":
             prog = p.fwd_programs[ex["stage"]]
             env = {v: st.get(bid, at) for v, bid in ex["feeds"].items()}
@@ -431,9 +446,8 @@ class _Actor:
         else:
             raise ExecutorFault(f"unknown task payload {kind!r}")
         if self.timeline:
-            e1 = torch.cuda.Event(enable_timing=True)
-            e1.record(self.stream)
-            self.events.append((task.kind if task.is_loop else "aux", task.uid, e0, e1))
+            self.stamp(s0 + 1)
+            self.events.append((task.kind if task.is_loop else "aux", task.uid, s0, s0 + 1))
 
     def _may_overwrite(self, bid: str, uid: str) -> bool:
         """True when ``bid``'s only reader is this task, it is not a step output,
@@ -471,8 +485,7 @@ def _worker(act: _Actor, instrs, tg: TaskGraph, channels: dict, ctl: _Control, d
     try:
         with torch.cuda.device(act.device), torch.cuda.stream(act.stream):
             if act.timeline:
-                act.base_event = torch.cuda.Event(enable_timing=True)
-                act.base_event.record(act.stream)
+                act.stamp(0)
             for idx, ins in enumerate(instrs):
                 ctl.heartbeat[a] = f"[{idx}] {_brief(ins)}"
                 if delay_fn is not None:
@@ -745,11 +758,10 @@ class PipelineEngine:
         if ctl.faults:
             raise ctl.faults[0]
         act.store.flush()
-        act_events, act.events = act.events, []
+        tl_on, act.timeline = act.timeline, False   # timestamps are read after a replay
         result = self._gather(actors, stats, strict_store=False, to_host=False)
+        act.timeline = tl_on
         cs = CapturedStep(self, graph, act, inputs, result)
-        cs.events = act_events
-        cs.base_event = act.base_event
         cs.launches = _lib.launch_count - launches0   # libpp200 calls recorded per replay
         return cs
 
@@ -796,10 +808,8 @@ class PipelineEngine:
                     new_params[b.meta["param"]] = out(store.data[bid])
                 elif bid == "loss:all":
                     losses = out(store.data[bid])
-            if act.timeline and act.base_event is not None:
-                for kind, uid, e0, e1 in act.events:
-                    stats.timeline.append((a, kind, uid, act.base_event.elapsed_time(e0),
-                                           act.base_event.elapsed_time(e1)))
+            if act.timeline:
+                stats.timeline.extend(act.read_timeline())
         if strict_store:
             for a in sorted(actors):
                 store = actors[a].store
@@ -850,12 +860,9 @@ class CapturedStep:
 
     def timeline(self) -> list:
         """(actor, kind, uid, start_ms, end_ms) of the last replay, when the
-        step was captured with ``timeline=True`` (event nodes in the graph)."""
-        if not getattr(self, "events", None) or self.base_event is None:
-            return []
-        a = self.act.actor
-        return [(a, kind, uid, self.base_event.elapsed_time(e0), self.base_event.elapsed_time(e1))
-                for kind, uid, e0, e1 in self.events]
+        step was captured with ``timeline=True`` (timestamp kernels in the graph)."""
+        torch.cuda.synchronize(self.act.device)
+        return self.act.read_timeline()
 
 
 def split_batch(batch, M: int):

@@ -50,18 +50,21 @@ def make_operands(M, N, K, ta, tb, dtype, seed=0):
     return A, B, opA @ opB
 
 
+@pytest.mark.parametrize("tma", [1, 0])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("bn", [64, 128, 256])
 @pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (200, 136, 72), (1024, 768, 768)])
-def test_bf16_tcgen05_majors(ta, tb, bn, shape):
+def test_bf16_tcgen05_majors(ta, tb, bn, shape, tma):
     M, N, K = shape
     A, B, ref = make_operands(M, N, K, ta, tb, torch.bfloat16)
     _lib.call("pc_gemm_set_tile_n", bn)
+    _lib.call("pc_gemm_set_tma_store", tma)
     try:
         C32 = run_gemm(A, B, ta, tb, M, N, K, torch.float32)
         C16 = run_gemm(A, B, ta, tb, M, N, K, torch.bfloat16)
     finally:
         _lib.call("pc_gemm_set_tile_n", 0)
+        _lib.call("pc_gemm_set_tma_store", 1)
     torch.cuda.synchronize()
     assert rel(C32, ref) < 1e-5
     assert rel(C16, ref) < 1e-2
