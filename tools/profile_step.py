@@ -31,8 +31,15 @@ t1 = time.perf_counter()
 print(f"host issue {1000*(stamps['issued']-t0):.1f} ms, step wall {1000*(t1-t0):.1f} ms")
 E.PipelineEngine._wait_devices = orig
 from torch.profiler import profile, ProfilerActivity
+cap = eng.capture(params, tok, lr=1e-4)
+for _ in range(2):
+    cap.replay()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); cap.replay(); e1.record(); torch.cuda.synchronize()
+print(f"graph replay step {e0.elapsed_time(e1):.2f} ms")
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    eng.step(params, tok, lr=1e-4, timeout_s=600, to_host=False)
+    cap.replay()
     torch.cuda.synchronize()
 agg = collections.defaultdict(lambda: [0, 0.0])
 for ev in prof.events():
