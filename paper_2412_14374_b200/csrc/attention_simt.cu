@@ -87,22 +87,24 @@ __global__ void __launch_bounds__(256) attn_fwd_simt(AttnDims a, const T* __rest
   if (lane == 0) lse[gw] = m + logf(l);
 }
 
-// delta[b,h,i] = sum_c dO[i,c] * O[i,c]
+// delta[b,h,i] = sum_c dO[i,c] * O[i,c]: one warp per token row walks all
+// heads (contiguous, coalesced reads of the whole row).
 template <typename T>
 __global__ void __launch_bounds__(256) attn_delta(AttnDims a, const T* __restrict__ o,
                                                   const T* __restrict__ dO,
                                                   float* __restrict__ delta) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = blockIdx.x * 8ll + (threadIdx.x >> 5);
-  if (gw >= static_cast<int64_t>(a.B) * a.H * a.S) return;
-  const int i = static_cast<int>(gw % a.S);
-  const int h = static_cast<int>((gw / a.S) % a.H);
-  const int b = static_cast<int>(gw / (static_cast<int64_t>(a.S) * a.H));
-  const int64_t off = (static_cast<int64_t>(b) * a.S + i) * a.ld_o + h * a.hd;
-  float s = 0.f;
-  for (int c = lane; c < a.hd; c += 32) s += lf(o, off + c) * lf(dO, off + c);
-  s = warp_sum(s);
-  if (lane == 0) delta[gw] = s;
+  const int64_t row = blockIdx.x * 8ll + (threadIdx.x >> 5);  // b*S + i
+  if (row >= static_cast<int64_t>(a.B) * a.S) return;
+  const int b = static_cast<int>(row / a.S), i = static_cast<int>(row % a.S);
+  const T* orow = o + row * a.ld_o;
+  const T* grow = dO + row * a.ld_o;
+  for (int h = 0; h < a.H; ++h) {
+    float s = 0.f;
+    for (int c = lane; c < a.hd; c += 32) s += lf(orow, h * a.hd + c) * lf(grow, h * a.hd + c);
+    s = warp_sum(s);
+    if (lane == 0) delta[(static_cast<int64_t>(b) * a.H + h) * a.S + i] = s;
+  }
 }
 
 // dQ_i = scale * sum_{j<=i} p_ij (dp_ij - delta_i) k_j
@@ -240,7 +242,7 @@ int attention_fwd_simt(int dtype, int B, int H, int S, int hd, const void* qkv, 
 int attention_delta(int dtype, int B, int H, int S, int hd, const void* o, const void* dO,
                     int64_t ld_o, float* delta, cudaStream_t st) {
   AttnDims a{B, H, S, hd, 0, ld_o, 0.f};
-  const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(B) * H * S + 7) / 8);
+  const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(B) * S + 7) / 8);
   if (dtype == PC_F32)
     attn_delta<float><<<blocks, 256, 0, st>>>(a, static_cast<const float*>(o), static_cast<const float*>(dO), delta);
   else

@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
                                                      const float* __restrict__ mean,
                                                      const float* __restrict__ rstd,
                                                      float* __restrict__ ws1,
-                                                     float* __restrict__ ws2) {
+                                                     float* __restrict__ ws2,
+                                                     unsigned int* __restrict__ counters,
+                                                     float* __restrict__ out1,
+                                                     float* __restrict__ out2, int accumulate) {
   __shared__ float sm1[8][64], sm2[8][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c0 = blockIdx.x * 64ll + lane * 2;
@@ -192,16 +195,30 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
       if (MODE == 1) ws2[blockIdx.y * cols + c] = t2;
     }
   }
+  // Last CTA of this column group folds the per-chunk partials in chunk order
+  // (fixed order => bitwise reproducible) and re-arms the counter.
+  __shared__ unsigned int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&counters[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 64) {
+    const int64_t c = blockIdx.x * 64ll + threadIdx.x;
+    if (c < cols) {
+      float t1 = 0.f, t2 = 0.f;
+      for (int k = 0; k < static_cast<int>(gridDim.y); ++k) {
+        t1 += __ldcg(ws1 + k * cols + c);
+        if (MODE == 1) t2 += __ldcg(ws2 + k * cols + c);
+      }
+      out1[c] = accumulate ? out1[c] + t1 : t1;
+      if (MODE == 1) out2[c] = t2;
+    }
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
 
-__global__ void colred_stage2(int64_t nchunks, int64_t cols, const float* __restrict__ ws,
-                              float* __restrict__ out, int accumulate) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float t = 0.f;
-  for (int64_t k = 0; k < nchunks; ++k) t += ws[k * cols + c];
-  out[c] = accumulate ? out[c] + t : t;
-}
 
 template <typename T>
 __global__ void copy2d_kernel(int64_t rows, int64_t cols, const T* __restrict__ src, int64_t lds,
@@ -258,7 +275,12 @@ int64_t colred_chunks(int64_t rows) {
   int64_t r = (rows + 63) / 64;
   return r < 1 ? 1 : (r > 128 ? 128 : r);
 }
-int64_t colred_ws_bytes(int64_t rows, int64_t cols) { return 2 * colred_chunks(rows) * cols * 4; }
+// partials (2 x chunks x cols fp32) + one arrival counter per 64-column group;
+// the counters must start zeroed (callers zero the workspace once; every
+// launch leaves them zero again).
+int64_t colred_ws_bytes(int64_t rows, int64_t cols) {
+  return 2 * colred_chunks(rows) * cols * 4 + ((cols + 63) / 64) * 4;
+}
 
 // Sum over rows of a (MODE 0) or LayerNorm parameter statistics (MODE 1) into
 // out1 (/out2) via ws; returns false if ws is too small (caller falls back).
@@ -270,14 +292,14 @@ bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda
   const int64_t R = colred_chunks(rows), chunk = (rows + R - 1) / R;
   float* w1 = static_cast<float*>(ws);
   float* w2 = w1 + R * cols;
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(w2 + R * cols);
   dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(R));
   if (mode == 0)
-    colred_stage1<T, 0><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2);
+    colred_stage1<T, 0><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2,
+                                               ctr, out1, out2, accumulate);
   else
-    colred_stage1<T, 1><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2);
-  const unsigned g2 = static_cast<unsigned>((cols + 255) / 256);
-  colred_stage2<<<g2, 256, 0, st>>>(R, cols, w1, out1, accumulate);
-  if (mode == 1) colred_stage2<<<g2, 256, 0, st>>>(R, cols, w2, out2, 0);
+    colred_stage1<T, 1><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2,
+                                               ctr, out1, out2, accumulate);
   return true;
 }
 template bool colred_launch<float>(int, int64_t, int64_t, const float*, int64_t, const float*,

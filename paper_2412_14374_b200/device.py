@@ -147,7 +147,9 @@ class DeviceOps:
         nb = ctypes.c_int64(0)
         call("pc_reduce_workspace_bytes", rows, cols, ctypes.byref(nb))
         if self._red is None or self._red.numel() < nb.value:
-            self._red = self.empty((nb.value,), torch.uint8)
+            n = (nb.value + 3) // 4 * 4
+            self._red = self.empty((n,), torch.uint8)
+            call("pc_fill", _lib.PC_F32, n // 4, 0.0, self._red.data_ptr(), self.st)  # counters
         return self._red.data_ptr(), self._red.numel()
 
     def empty(self, shape, dtype) -> torch.Tensor:

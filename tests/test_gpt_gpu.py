@@ -152,7 +152,7 @@ def test_layernorm_and_xent_kernels():
     import ctypes
     nb = ctypes.c_int64()
     _lib.call("pc_reduce_workspace_bytes", rows, d, ctypes.byref(nb))
-    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")  # arrival counters start at 0
     tdg2, tdb2 = torch.empty(d, device="cuda"), torch.empty(d, device="cuda")
     _lib.call("pc_layernorm_bwd", _lib.PC_F32, rows, d, tdy.data_ptr(), tx.data_ptr(),
               tg_.data_ptr(), mean.data_ptr(), rstd.data_ptr(), None, tdx.data_ptr(),
@@ -206,7 +206,7 @@ def test_embedding_kernels_deterministic():
     import ctypes
     nb = ctypes.c_int64()
     _lib.call("pc_embedding_bwd_workspace_bytes", T_, ctypes.byref(nb))
-    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")  # arrival counters start at 0
     outs = []
     for _ in range(2):
         dwte = torch.empty(V, d, device="cuda")
