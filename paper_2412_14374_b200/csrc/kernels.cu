@@ -275,11 +275,12 @@ int64_t colred_chunks(int64_t rows) {
   int64_t r = (rows + 63) / 64;
   return r < 1 ? 1 : (r > 128 ? 128 : r);
 }
-// partials (2 x chunks x cols fp32) + one arrival counter per 64-column group;
-// the counters must start zeroed (callers zero the workspace once; every
-// launch leaves them zero again).
+// Layout: [arrival counters, fixed 4 KB at offset 0][partials 2 x chunks x cols fp32].
+// The counters sit at a fixed place whatever (rows, cols) a call uses, so
+// zeroing the workspace once suffices: every launch leaves them zero again.
+constexpr int64_t COLRED_COUNTERS = 1024;
 int64_t colred_ws_bytes(int64_t rows, int64_t cols) {
-  return 2 * colred_chunks(rows) * cols * 4 + ((cols + 63) / 64) * 4;
+  return COLRED_COUNTERS * 4 + 2 * colred_chunks(rows) * cols * 4;
 }
 
 // Sum over rows of a (MODE 0) or LayerNorm parameter statistics (MODE 1) into
@@ -288,11 +289,13 @@ template <typename T>
 bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda, const T* x,
                    const float* mean, const float* rstd, float* out1, float* out2,
                    int accumulate, void* ws, int64_t ws_bytes, cudaStream_t st) {
-  if (ws == nullptr || ws_bytes < colred_ws_bytes(rows, cols) || rows <= 0) return false;
+  if (ws == nullptr || ws_bytes < colred_ws_bytes(rows, cols) || rows <= 0 ||
+      (cols + 63) / 64 > COLRED_COUNTERS)
+    return false;
   const int64_t R = colred_chunks(rows), chunk = (rows + R - 1) / R;
-  float* w1 = static_cast<float*>(ws);
+  unsigned int* ctr = static_cast<unsigned int*>(ws);
+  float* w1 = reinterpret_cast<float*>(ctr + COLRED_COUNTERS);
   float* w2 = w1 + R * cols;
-  unsigned int* ctr = reinterpret_cast<unsigned int*>(w2 + R * cols);
   dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(R));
   if (mode == 0)
     colred_stage1<T, 0><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2,
