@@ -121,6 +121,133 @@ __global__ void __launch_bounds__(1024) ln_bwd_param_kernel(int64_t rows, int d,
   }
 }
 
+// ---- vectorised LayerNorm (d = 256*NCH, NCH <= 4): the row lives in registers,
+// one 16 B load / store per 8 elements.
+template <typename T>
+__device__ __forceinline__ void ld8(const T* p, float* v) {
+  if (sizeof(T) == 2) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    }
+  } else {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const float* v) {
+  if (sizeof(T) == 2) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+  } else {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+__device__ __forceinline__ void ldf8(const float* p, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) ln_fwd_vec(int64_t rows, int d, const T* __restrict__ x,
+                                                  const float* __restrict__ g,
+                                                  const float* __restrict__ b, T* __restrict__ y,
+                                                  float* __restrict__ mean,
+                                                  float* __restrict__ rstd, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)ROWS_PER_BLOCK + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  float v[NCH][8];
+  float s = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    ld8(x + r * d + ch * 256 + lane * 8, v[ch]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[ch][j];
+  }
+  const float mu = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float t = v[ch][j] - mu;
+      q += t * t;
+    }
+  const float rs = rsqrtf(warp_sum(q) / d + eps);
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int c = ch * 256 + lane * 8;
+    float gg[8], bb[8], o[8];
+    ldf8(g + c, gg);
+    ldf8(b + c, bb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (v[ch][j] - mu) * rs * gg[j] + bb[j];
+    st8(y + r * d + c, o);
+  }
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) ln_bwd_dx_vec(int64_t rows, int d, const T* __restrict__ dy,
+                                                     const T* __restrict__ x,
+                                                     const float* __restrict__ g,
+                                                     const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd,
+                                                     const T* __restrict__ dres,
+                                                     T* __restrict__ dx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)ROWS_PER_BLOCK + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float mu = mean[r], rs = rstd[r];
+  float dxh[NCH][8], xh[NCH][8];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int c = ch * 256 + lane * 8;
+    float gy[8], xv[8], gg[8];
+    ld8(dy + r * d + c, gy);
+    ld8(x + r * d + c, xv);
+    ldf8(g + c, gg);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      dxh[ch][j] = gy[j] * gg[j];
+      xh[ch][j] = (xv[j] - mu) * rs;
+      s1 += dxh[ch][j];
+      s2 += dxh[ch][j] * xh[ch][j];
+    }
+  }
+  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int c = ch * 256 + lane * 8;
+    float o[8], rr[8];
+    if (dres) ld8(dres + r * d + c, rr);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = rs * (dxh[ch][j] - m1 - xh[ch][j] * m2) + (dres ? rr[j] : 0.f);
+    st8(dx + r * d + c, o);
+  }
+}
+
+template <typename T>
+bool ln_vec_ok(int64_t d, const void* p0, const void* p1, const void* p2) {
+  const uintptr_t m = reinterpret_cast<uintptr_t>(p0) | reinterpret_cast<uintptr_t>(p1) |
+                      reinterpret_cast<uintptr_t>(p2);
+  return d % 256 == 0 && d / 256 >= 1 && d / 256 <= 4 && (m & 31) == 0;
+}
+
 // out[t,:] = wte[tok[t],:] + wpe[t % seq,:]   (fp32 master tables)
 template <typename T>
 __global__ void __launch_bounds__(256) embed_fwd_kernel(int64_t T_, int d, int seq,
@@ -346,7 +473,18 @@ extern "C" int pc_layernorm_fwd(int dtype, int64_t rows, int64_t d, const void* 
                                 float* rstd, float eps, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= 0) return PC_OK;
-  PP_DISPATCH_FB(dtype, T, ln_fwd_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, beta, static_cast<T*>(y), mean, rstd, eps));
+  PP_DISPATCH_FB(dtype, T,
+    if (ln_vec_ok<T>(d, x, y, gamma) && (reinterpret_cast<uintptr_t>(beta) & 31) == 0) {
+      const unsigned nb = row_blocks(rows);
+      switch (d / 256) {
+        case 1: ln_fwd_vec<T, 1><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, beta, static_cast<T*>(y), mean, rstd, eps); break;
+        case 2: ln_fwd_vec<T, 2><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, beta, static_cast<T*>(y), mean, rstd, eps); break;
+        case 3: ln_fwd_vec<T, 3><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, beta, static_cast<T*>(y), mean, rstd, eps); break;
+        default: ln_fwd_vec<T, 4><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, beta, static_cast<T*>(y), mean, rstd, eps); break;
+      }
+    } else {
+      ln_fwd_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, beta, static_cast<T*>(y), mean, rstd, eps);
+    });
   return check_launch("layernorm_fwd");
 }
 
@@ -364,7 +502,18 @@ extern "C" int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= 0) return PC_OK;
   PP_DISPATCH_FB(dtype, T,
-    ln_bwd_dx_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
+    if (ln_vec_ok<T>(d, dy, x, dx) && ((reinterpret_cast<uintptr_t>(gamma) | reinterpret_cast<uintptr_t>(dres)) & 31) == 0) {
+      const unsigned nb = row_blocks(rows);
+      const T* dr = static_cast<const T*>(dres);
+      switch (d / 256) {
+        case 1: ln_bwd_dx_vec<T, 1><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, dr, static_cast<T*>(dx)); break;
+        case 2: ln_bwd_dx_vec<T, 2><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, dr, static_cast<T*>(dx)); break;
+        case 3: ln_bwd_dx_vec<T, 3><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, dr, static_cast<T*>(dx)); break;
+        default: ln_bwd_dx_vec<T, 4><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, dr, static_cast<T*>(dx)); break;
+      }
+    } else {
+      ln_bwd_dx_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
+    }
     if (!colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), mean, rstd, dgamma, dbeta, 0, ws, ws_bytes, st))
       ln_bwd_param_kernel<T><<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), mean, rstd, dgamma, dbeta));
   return check_launch("layernorm_bwd");

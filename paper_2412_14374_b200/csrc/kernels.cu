@@ -136,12 +136,39 @@ __global__ void __launch_bounds__(1024) col_sum_kernel(int64_t rows, int64_t col
   }
 }
 
-// Two-stage deterministic column reduction over many CTAs.
-// Stage 1: grid (ceil(cols/64), R); a warp covers 64 columns (2 per lane) and
-// strides over the CTA's row chunk; the 8 warps combine in fixed order into
-// ws[chunk][col] (and ws2 for the LayerNorm second statistic).
+// Deterministic column reduction over many CTAs, one launch.
+// grid (ceil(cols/256), R): a warp covers 256 columns (8 per lane, one 16 B
+// load for bf16) and strides over the CTA's row chunk; the 8 warps combine in
+// fixed order into ws[chunk][col]; the last CTA of a column group (arrival
+// counter) folds the R partials in chunk order.
 // MODE 0: s1 = sum x.   MODE 1 (LayerNorm params): s1 = sum dy*xhat, s2 = sum dy
 // with xhat = (x - mean[r]) * rstd[r].
+constexpr int CR_COLS = 256;
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, int64_t c, int64_t cols, bool vec, float* v) {
+  if (vec && c + 8 <= cols) {
+    if (sizeof(T) == 2) {
+      const uint4 u = *reinterpret_cast<const uint4*>(p + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        v[2 * j] = f.x;
+        v[2 * j + 1] = f.y;
+      }
+    } else {
+      const float4 x0 = *reinterpret_cast<const float4*>(p + c);
+      const float4 x1 = *reinterpret_cast<const float4*>(p + c + 4);
+      v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+      v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = c + j < cols ? static_cast<float>(ldv(p, c + j)) : 0.f;
+  }
+}
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols, int64_t chunk,
                                                      const T* __restrict__ a, int64_t lda,
@@ -153,38 +180,39 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
                                                      unsigned int* __restrict__ counters,
                                                      float* __restrict__ out1,
                                                      float* __restrict__ out2, int accumulate) {
-  __shared__ float sm1[8][64], sm2[8][64];
+  __shared__ float sm1[8][CR_COLS], sm2[MODE == 1 ? 8 : 1][CR_COLS];
+  __shared__ unsigned int s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c0 = blockIdx.x * 64ll + lane * 2;
+  const int64_t c0 = blockIdx.x * static_cast<int64_t>(CR_COLS) + lane * 8;
   const int64_t r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
-  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+  const bool vec = (lda % 8 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) &&
+                   (MODE == 0 || (reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  float s1[8] = {}, s2[8] = {};
   for (int64_t r = r0 + w; r < r1; r += 8) {
-    const T* ar = a + r * lda;
-    const float v0 = c0 < cols ? static_cast<float>(ldv(ar, c0)) : 0.f;
-    const float v1 = c0 + 1 < cols ? static_cast<float>(ldv(ar, c0 + 1)) : 0.f;
+    float v[8];
+    load8(a + r * lda, c0, cols, vec, v);
     if (MODE == 0) {
-      a0 += v0;
-      a1 += v1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s1[j] += v[j];
     } else {
-      const T* xr = x + r * lda;
+      float xv[8];
+      load8(x + r * lda, c0, cols, vec, xv);
       const float mu = mean[r], rs = rstd[r];
-      const float x0 = c0 < cols ? (static_cast<float>(ldv(xr, c0)) - mu) * rs : 0.f;
-      const float x1 = c0 + 1 < cols ? (static_cast<float>(ldv(xr, c0 + 1)) - mu) * rs : 0.f;
-      a0 += v0 * x0;
-      a1 += v1 * x1;
-      b0 += v0;
-      b1 += v1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s1[j] += v[j] * ((xv[j] - mu) * rs);
+        s2[j] += v[j];
+      }
     }
   }
-  sm1[w][lane * 2] = a0;
-  sm1[w][lane * 2 + 1] = a1;
-  if (MODE == 1) {
-    sm2[w][lane * 2] = b0;
-    sm2[w][lane * 2 + 1] = b1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sm1[w][lane * 8 + j] = s1[j];
+    if (MODE == 1) sm2[w][lane * 8 + j] = s2[j];
   }
   __syncthreads();
-  if (threadIdx.x < 64) {
-    const int64_t c = blockIdx.x * 64ll + threadIdx.x;
+  {
+    const int64_t c = blockIdx.x * static_cast<int64_t>(CR_COLS) + threadIdx.x;
     float t1 = 0.f, t2 = 0.f;
     for (int k = 0; k < 8; ++k) {
       t1 += sm1[k][threadIdx.x];
@@ -195,30 +223,24 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
       if (MODE == 1) ws2[blockIdx.y * cols + c] = t2;
     }
   }
-  // Last CTA of this column group folds the per-chunk partials in chunk order
-  // (fixed order => bitwise reproducible) and re-arms the counter.
-  __shared__ unsigned int s_last;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&counters[blockIdx.x], 1u) == gridDim.y - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x < 64) {
-    const int64_t c = blockIdx.x * 64ll + threadIdx.x;
-    if (c < cols) {
-      float t1 = 0.f, t2 = 0.f;
-      for (int k = 0; k < static_cast<int>(gridDim.y); ++k) {
-        t1 += __ldcg(ws1 + k * cols + c);
-        if (MODE == 1) t2 += __ldcg(ws2 + k * cols + c);
-      }
-      out1[c] = accumulate ? out1[c] + t1 : t1;
-      if (MODE == 1) out2[c] = t2;
+  const int64_t c = blockIdx.x * static_cast<int64_t>(CR_COLS) + threadIdx.x;
+  if (c < cols) {
+    float t1 = 0.f, t2 = 0.f;
+    for (int k = 0; k < static_cast<int>(gridDim.y); ++k) {
+      t1 += __ldcg(ws1 + k * cols + c);
+      if (MODE == 1) t2 += __ldcg(ws2 + k * cols + c);
     }
+    out1[c] = accumulate ? out1[c] + t1 : t1;
+    if (MODE == 1) out2[c] = t2;
   }
   if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
-
 
 template <typename T>
 __global__ void copy2d_kernel(int64_t rows, int64_t cols, const T* __restrict__ src, int64_t lds,
@@ -290,13 +312,13 @@ bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda
                    const float* mean, const float* rstd, float* out1, float* out2,
                    int accumulate, void* ws, int64_t ws_bytes, cudaStream_t st) {
   if (ws == nullptr || ws_bytes < colred_ws_bytes(rows, cols) || rows <= 0 ||
-      (cols + 63) / 64 > COLRED_COUNTERS)
+      (cols + CR_COLS - 1) / CR_COLS > COLRED_COUNTERS)
     return false;
   const int64_t R = colred_chunks(rows), chunk = (rows + R - 1) / R;
   unsigned int* ctr = static_cast<unsigned int*>(ws);
   float* w1 = reinterpret_cast<float*>(ctr + COLRED_COUNTERS);
   float* w2 = w1 + R * cols;
-  dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(R));
+  dim3 grid(static_cast<unsigned>((cols + CR_COLS - 1) / CR_COLS), static_cast<unsigned>(R));
   if (mode == 0)
     colred_stage1<T, 0><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2,
                                                ctr, out1, out2, accumulate);

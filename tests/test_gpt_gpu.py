@@ -266,3 +266,44 @@ def test_cuda_graph_replay_matches_eager():
     assert np.array_equal(r.losses.cpu().numpy(), e2.losses)
     for q in e2.grads:
         assert np.array_equal(r.grads[q].cpu().numpy(), e2.grads[q]), q
+
+
+@pytest.mark.parametrize("d", [96, 256, 768, 1024])
+@pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_layernorm_vectorised_paths(d, dt, tol):
+    import ctypes
+    rows = 200
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((rows, d))
+    g, b = rng.standard_normal(d), rng.standard_normal(d)
+    dy = rng.standard_normal((rows, d))
+    res = rng.standard_normal((rows, d))
+    tx, tdy, tres = _t(x, dt), _t(dy, dt), _t(res, dt)
+    xq, dyq, resq = (t.double().cpu().numpy() for t in (tx, tdy, tres))
+    y, cache = gpt.layer_norm(xq, g, b)
+    dx, dg, db = gpt.layer_norm_bwd(dyq, g, cache)
+    tg_, tb = _t(g), _t(b)
+    ty = torch.empty_like(tx)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    pc = _lib.PC_F32 if dt == torch.float32 else _lib.PC_BF16
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("pc_layernorm_fwd", pc, rows, d, tx.data_ptr(), tg_.data_ptr(), tb.data_ptr(),
+              ty.data_ptr(), mean.data_ptr(), rstd.data_ptr(), 1e-5, st)
+    nb = ctypes.c_int64()
+    _lib.call("pc_reduce_workspace_bytes", rows, d, ctypes.byref(nb))
+    ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")
+    tdx = torch.empty_like(tx)
+    tdg, tdb = torch.empty(d, device="cuda"), torch.empty(d, device="cuda")
+    _lib.call("pc_layernorm_bwd", pc, rows, d, tdy.data_ptr(), tx.data_ptr(), tg_.data_ptr(),
+              mean.data_ptr(), rstd.data_ptr(), tres.data_ptr(), tdx.data_ptr(), tdg.data_ptr(),
+              tdb.data_ptr(), ws.data_ptr(), nb.value, st)
+    cs = torch.empty(d, device="cuda")
+    _lib.call("pc_col_sum", pc, _lib.PC_F32, rows, d, tdy.data_ptr(), d, cs.data_ptr(), 0,
+              ws.data_ptr(), nb.value, st)
+    torch.cuda.synchronize()
+    assert ffn.rel(ty.double().cpu().numpy(), y) < tol
+    assert ffn.rel(tdx.double().cpu().numpy(), dx + resq) < tol
+    assert ffn.rel(tdg.cpu().numpy(), dg) < tol
+    assert ffn.rel(tdb.cpu().numpy(), db) < tol
+    assert ffn.rel(cs.cpu().numpy(), dyq.sum(0)) < 1e-5
