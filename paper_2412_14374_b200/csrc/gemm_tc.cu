@@ -35,6 +35,7 @@ constexpr int TC_MN_CHUNK_BYTES = TC_BK * 128;  // one 64-wide MN box of BK rows
 
 struct TcEpi {
   int tma_c;  // C written through smem + TMA bulk tensor store
+  int tma_u;  // GELU/RELU pre-activation (aux_out) through smem + TMA as well
   void* C;
   int64_t ldc;
   const float* bias;
@@ -118,8 +119,11 @@ __device__ __forceinline__ void store16(void* base, bool f32, int64_t off, int n
   }
 }
 
+// Applies the fused epilogue to 16 accumulator values of (row, col..col+15).
+// store_c: write C here (direct path).  pre != nullptr: the pre-activation of
+// GELU/RELU is returned there (staged for a TMA store) instead of stored.
 __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, float* v,
-                                           bool store_c) {
+                                           bool store_c, float* pre) {
   const int nvalid = min(16, ep.N - col);
   const bool f32 = ep.out_f32 != 0;
   const int fl = ep.flags;
@@ -132,10 +136,24 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
     return;
   }
   if (fl & PC_EPI_BIAS) {
-    for (int i = 0; i < 16; ++i) v[i] += i < nvalid ? ep.bias[col + i] : 0.f;
+    const float* bp = ep.bias + col;
+    if (nvalid == 16 && (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 b4 = reinterpret_cast<const float4*>(bp)[i];
+        v[4 * i] += b4.x; v[4 * i + 1] += b4.y; v[4 * i + 2] += b4.z; v[4 * i + 3] += b4.w;
+      }
+    } else {
+      for (int i = 0; i < 16; ++i) v[i] += i < nvalid ? bp[i] : 0.f;
+    }
   }
   if (fl & (PC_EPI_GELU | PC_EPI_RELU)) {
-    store16(ep.aux_out, f32, static_cast<int64_t>(row) * ep.ldaux_out + col, nvalid, v);
+    if (pre) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pre[i] = v[i];
+    } else {
+      store16(ep.aux_out, f32, static_cast<int64_t>(row) * ep.ldaux_out + col, nvalid, v);
+    }
     if (fl & PC_EPI_GELU) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = gelu_tanh_fast(v[i]);
@@ -165,11 +183,26 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
 __device__ __forceinline__ uint4* stage_chunk(uint8_t* stg, int r, int j) {
   return reinterpret_cast<uint4*>(stg + r * 128 + ((j ^ (r & 7)) << 4));
 }
+// ... and inside a 64B-swizzled [32 x 64 B] tile (bf16 boxes of 32 columns).
+__device__ __forceinline__ uint4* stage_chunk64(uint8_t* stg, int r, int j) {
+  return reinterpret_cast<uint4*>(stg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ void stage_bf16_row32(uint8_t* stg, int r, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+    *stage_chunk64(stg, r, j) = u;
+  }
+}
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, TcEpi ep) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmU,
+                   int M, int N, int K, TcEpi ep) {
   using Cfg = TcCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -300,47 +333,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tmem_ld16(tb + cc + 16, r + 16);
         tc_wait_ld();
         float* v = reinterpret_cast<float*>(r);
+        float pre[32];
+        const bool stage_u = ep.tma_u != 0;
         if (row < M) {
-          if (n0 + cc < N) epilogue16(ep, row, n0 + cc, v, !tma);
-          if (n0 + cc + 16 < N) epilogue16(ep, row, n0 + cc + 16, v + 16, !tma);
+          if (n0 + cc < N) epilogue16(ep, row, n0 + cc, v, !tma, stage_u ? pre : nullptr);
+          if (n0 + cc + 16 < N)
+            epilogue16(ep, row, n0 + cc + 16, v + 16, !tma, stage_u ? pre + 16 : nullptr);
         }
         if (!tma) continue;
+        if (lane == 0) bulk_wait_read0();   // previous chunk's stores have read the stage
+        __syncwarp();
         if (f32) {
-          // 32 fp32 = one 128 B staging row per thread; one TMA box per chunk
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
+          // 32 fp32 = one 128 B row per thread, 128B-swizzled box {32 cols, 32 rows}
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             *stage_chunk(stg, lane, j) = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
-            bulk_commit();
-          }
         } else {
-          // 32 bf16 = half a staging row; a 64-column box is stored per two chunks
-          const int sub = (c >> 5) & 1;
-          if (sub == 0) {
-            if (lane == 0) bulk_wait_read0();
-            __syncwarp();
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 u;
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
-            *stage_chunk(stg, lane, 4 * sub + j) = u;
-          }
-          if (sub == 1 || c + 32 >= HALF) {
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmC, stg, n0 + cc - 32 * sub, m0 + q * 32);
-              bulk_commit();
-            }
-          }
+          // 32 bf16 = one 64 B row per thread, 64B-swizzled box {32 cols, 32 rows};
+          // the pre-activation goes to the second half of the stage
+          stage_bf16_row32(stg, lane, v);
+          if (stage_u) stage_bf16_row32(stg + 2048, lane, pre);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+          if (stage_u) tma_store_2d(&tmU, stg + 2048, n0 + cc, m0 + q * 32);
+          bulk_commit();
         }
       }
       tc_fence_before();
@@ -397,8 +416,9 @@ int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int
   return PC_OK;
 }
 
-// Store-side tensor map for C: [M, N] row-major, boxes of 128 B x 32 rows
-// (64 bf16 or 32 fp32 columns), 128B swizzle matching the staging tiles.
+// Store-side tensor map for C (or the pre-activation): [M, N] row-major, boxes
+// of 32 columns x 32 rows: fp32 -> 128 B rows, 128B swizzle; bf16 -> 64 B rows,
+// 64B swizzle -- matching the epilogue staging tiles.
 int make_tmap_c(CUtensorMap* m, void* ptr, int64_t N, int64_t M, int64_t ldc, bool f32) {
   auto enc = tmap_encoder();
   if (!enc) {
@@ -408,12 +428,12 @@ int make_tmap_c(CUtensorMap* m, void* ptr, int64_t N, int64_t M, int64_t ldc, bo
   const int es = f32 ? 4 : 2;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc * es)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32u};
+  cuuint32_t box[2] = {32u, 32u};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled (C) failed (%d)", static_cast<int>(r));
     return PC_ERR_CUDA;
@@ -425,8 +445,8 @@ int g_force_bn = 0;
 int g_tma_store = 1;
 
 template <int BN, bool A_MN, bool B_MN>
-int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, int M, int N,
-              int K, const TcEpi& ep, cudaStream_t st) {
+int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+              const CUtensorMap& tu, int M, int N, int K, const TcEpi& ep, cudaStream_t st) {
   using Cfg = TcCfg<BN>;
   static bool attr_set = false;  // benign race: idempotent attribute write
   if (!attr_set) {
@@ -436,17 +456,18 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
   }
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, M, N, K, ep);
+  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, M, N, K, ep);
   return check_launch("tc_gemm_kernel");
 }
 
 template <int BN>
 int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
-                    const CUtensorMap& tc, int M, int N, int K, const TcEpi& ep, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, tc, M, N, K, ep, st);
-  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, tc, M, N, K, ep, st);
-  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, tc, M, N, K, ep, st);
-  return launch_tc<BN, true, true>(ta, tb, tc, M, N, K, ep, st);
+                    const CUtensorMap& tc, const CUtensorMap& tu, int M, int N, int K,
+                    const TcEpi& ep, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, tc, tu, M, N, K, ep, st);
+  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, tc, tu, M, N, K, ep, st);
+  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, tc, tu, M, N, K, ep, st);
+  return launch_tc<BN, true, true>(ta, tb, tc, tu, M, N, K, ep, st);
 }
 
 }  // namespace
@@ -484,24 +505,30 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   else
     rc = make_tmap(&tb, B, N, K, ldb, TC_BK);
   if (rc) return rc;
-  // C through smem + TMA store when legal: 16 B aligned rows, no read-modify-
-  // write epilogue, and bf16 boxes (64 columns) never straddle the two column
-  // halves drained by different warp groups (BN >= 128).
+  // C (and a GELU/RELU pre-activation) through smem + TMA store when legal:
+  // 16 B aligned rows and no read-modify-write epilogue.
   const int es = out_f32 ? 4 : 2;
-  const bool tma_c = g_tma_store && !(epi & PC_EPI_ACCUM) && (out_f32 || bn >= 128) &&
+  const bool tma_c = g_tma_store && !(epi & PC_EPI_ACCUM) &&
                      (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
-  CUtensorMap tc;
+  const bool tma_u = tma_c && !out_f32 && (epi & (PC_EPI_GELU | PC_EPI_RELU)) &&
+                     (reinterpret_cast<uintptr_t>(aux_out) & 15) == 0 && (ldaux_out * 2) % 16 == 0;
+  CUtensorMap tc, tu;
   memset(&tc, 0, sizeof(tc));
+  memset(&tu, 0, sizeof(tu));
   if (tma_c) {
     rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0);
     if (rc) return rc;
   }
-  TcEpi ep{tma_c ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux, aux_out, ldaux_out,
-           static_cast<int>(M), static_cast<int>(N), epi, out_f32};
+  if (tma_u) {
+    rc = make_tmap_c(&tu, aux_out, N, M, ldaux_out, false);
+    if (rc) return rc;
+  }
+  TcEpi ep{tma_c ? 1 : 0, tma_u ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
+           aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi, out_f32};
   switch (bn) {
-    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, (int)M, (int)N, (int)K, ep, st);
-    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, tc, (int)M, (int)N, (int)K, ep, st);
-    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, tc, (int)M, (int)N, (int)K, ep, st);
+    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
+    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
+    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
     default: set_error("gemm: bad tile width %d", bn); return PC_ERR_ARG;
   }
 }
