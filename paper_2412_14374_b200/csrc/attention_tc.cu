@@ -267,6 +267,179 @@ __global__ void __launch_bounds__(256) fa_fwd(const bf16* __restrict__ qkv, int6
   }
 }
 
+// Forward with 32 query rows per warp (two m16 tiles): every K / V fragment
+// loaded from shared memory feeds two MMAs, halving ldmatrix traffic per
+// flop.  4 warps x 32 rows = 128 rows per CTA.  Used for head_dim 64.
+template <int HD>
+struct Fwd2Cfg {
+  static constexpr int BM = 128, BN = 64, NT = 128, LDS = HD + 8;
+  static constexpr int SMEM = (BM + 4 * BN) * LDS * 2;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(128) fa_fwd2(const bf16* __restrict__ qkv, int64_t ldq,
+                                               bf16* __restrict__ o, int64_t ldo,
+                                               float* __restrict__ lse, int H, int S, float sl2) {
+  using C = Fwd2Cfg<HD>;
+  constexpr int BM = C::BM, BN = C::BN, LDS = C::LDS, NT = C::NT;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  bf16* sQ = reinterpret_cast<bf16*>(smraw);
+  bf16* sK = sQ + BM * LDS;
+  bf16* sV = sK + 2 * BN * LDS;
+  const int nqb = (S + BM - 1) / BM;
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
+  const int b = blockIdx.y / H, h = blockIdx.y % H;
+  const int d = H * HD;
+  const bf16* Qg = qkv + static_cast<int64_t>(b) * S * ldq + h * HD;
+  const bf16* Kg = Qg + d;
+  const bf16* Vg = Qg + 2 * d;
+  const int q0 = qb * BM;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  const int mi = lane >> 3, r8 = lane & 7;
+  const int kend = min(S, q0 + BM);
+  const int nkb = (kend + BN - 1) / BN;
+  const int wrow0 = q0 + warp * 32;
+
+  load_tile<BM, HD, NT>(sQ, Qg + static_cast<int64_t>(q0) * ldq, ldq, S - q0);
+  cp_commit();
+  load_tile<BN, HD, NT>(sK, Kg, ldq, S);
+  load_tile<BN, HD, NT>(sV, Vg, ldq, S);
+  cp_commit();
+  cp_wait<1>();
+  __syncthreads();
+  uint32_t qf[2][HD / 16][4];
+  load_afrags<HD>(qf[0], sQ, warp * 32, lane);
+  load_afrags<HD>(qf[1], sQ, warp * 32 + 16, lane);
+
+  float oacc[2][HD / 8][4];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) oacc[t][i][0] = oacc[t][i][1] = oacc[t][i][2] = oacc[t][i][3] = 0.f;
+  float m[2][2] = {{-INFINITY, -INFINITY}, {-INFINITY, -INFINITY}};
+  float l[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+
+  for (int kb = 0; kb < nkb; ++kb) {
+    if (kb + 1 < nkb) {
+      const int n1 = (kb + 1) * BN;
+      load_tile<BN, HD, NT>(sK + ((kb + 1) & 1) * BN * LDS, Kg + static_cast<int64_t>(n1) * ldq, ldq, S - n1);
+      load_tile<BN, HD, NT>(sV + ((kb + 1) & 1) * BN * LDS, Vg + static_cast<int64_t>(n1) * ldq, ldq, S - n1);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const int n0 = kb * BN;
+    const bf16* sKb = sK + (kb & 1) * BN * LDS;
+    const bf16* sVb = sV + (kb & 1) * BN * LDS;
+    if (n0 <= wrow0 + 31 && wrow0 < S) {
+      float sc[2][BN / 8][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int i = 0; i < BN / 8; ++i) sc[t][i][0] = sc[t][i][1] = sc[t][i][2] = sc[t][i][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+        for (int np = 0; np < BN / 16; ++np) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(b0, b1, b2, b3,
+                  smem_u32(sKb + ((2 * np + (mi >> 1)) * 8 + r8) * LDS + kk * 16 + (mi & 1) * 8));
+          mma16816(sc[0][2 * np], qf[0][kk], b0, b1);
+          mma16816(sc[0][2 * np + 1], qf[0][kk], b2, b3);
+          mma16816(sc[1][2 * np], qf[1][kk], b0, b1);
+          mma16816(sc[1][2 * np + 1], qf[1][kk], b2, b3);
+        }
+      }
+      const bool diag = n0 + BN > wrow0;  // some key > some row in this block
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int rowA = wrow0 + t * 16 + g, rowB = rowA + 8;
+        float bmA = -INFINITY, bmB = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < BN / 8; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float v = sc[t][nt][e] * sl2;
+            if (diag || n0 + BN > S) {
+              const int row = e < 2 ? rowA : rowB;
+              const int key = n0 + nt * 8 + tg * 2 + (e & 1);
+              if (key > row || key >= S) v = -INFINITY;
+            }
+            sc[t][nt][e] = v;
+          }
+          bmA = fmaxf(bmA, fmaxf(sc[t][nt][0], sc[t][nt][1]));
+          bmB = fmaxf(bmB, fmaxf(sc[t][nt][2], sc[t][nt][3]));
+        }
+        const float nA = fmaxf(m[t][0], quad_max(bmA)), nB = fmaxf(m[t][1], quad_max(bmB));
+        const float refA = nA == -INFINITY ? 0.f : nA, refB = nB == -INFINITY ? 0.f : nB;
+        const float cA = exp2f(m[t][0] - refA), cB = exp2f(m[t][1] - refB);
+        m[t][0] = nA;
+        m[t][1] = nB;
+        float sumA = 0.f, sumB = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < BN / 8; ++nt) {
+          sc[t][nt][0] = exp2f(sc[t][nt][0] - refA);
+          sc[t][nt][1] = exp2f(sc[t][nt][1] - refA);
+          sc[t][nt][2] = exp2f(sc[t][nt][2] - refB);
+          sc[t][nt][3] = exp2f(sc[t][nt][3] - refB);
+          sumA += sc[t][nt][0] + sc[t][nt][1];
+          sumB += sc[t][nt][2] + sc[t][nt][3];
+        }
+        l[t][0] = l[t][0] * cA + sumA;
+        l[t][1] = l[t][1] * cB + sumB;
+#pragma unroll
+        for (int i = 0; i < HD / 8; ++i) {
+          oacc[t][i][0] *= cA; oacc[t][i][1] *= cA;
+          oacc[t][i][2] *= cB; oacc[t][i][3] *= cB;
+        }
+      }
+      // O += P V for both row tiles, sharing every V fragment
+#pragma unroll
+      for (int k2 = 0; k2 < BN / 16; ++k2) {
+        uint32_t a0[4] = {pack2(sc[0][2 * k2][0], sc[0][2 * k2][1]), pack2(sc[0][2 * k2][2], sc[0][2 * k2][3]),
+                          pack2(sc[0][2 * k2 + 1][0], sc[0][2 * k2 + 1][1]),
+                          pack2(sc[0][2 * k2 + 1][2], sc[0][2 * k2 + 1][3])};
+        uint32_t a1[4] = {pack2(sc[1][2 * k2][0], sc[1][2 * k2][1]), pack2(sc[1][2 * k2][2], sc[1][2 * k2][3]),
+                          pack2(sc[1][2 * k2 + 1][0], sc[1][2 * k2 + 1][1]),
+                          pack2(sc[1][2 * k2 + 1][2], sc[1][2 * k2 + 1][3])};
+#pragma unroll
+        for (int dp = 0; dp < HD / 16; ++dp) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(b0, b1, b2, b3,
+                    smem_u32(sVb + (k2 * 16 + (mi & 1) * 8 + r8) * LDS + dp * 16 + (mi >> 1) * 8));
+          mma16816(oacc[0][2 * dp], a0, b0, b1);
+          mma16816(oacc[0][2 * dp + 1], a0, b2, b3);
+          mma16816(oacc[1][2 * dp], a1, b0, b1);
+          mma16816(oacc[1][2 * dp + 1], a1, b2, b3);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  bf16* ob = o + static_cast<int64_t>(b) * S * ldo + h * HD;
+  float* lb = lse + (static_cast<int64_t>(b) * H + h) * S;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int rowA = wrow0 + t * 16 + g, rowB = rowA + 8;
+    const float LA = quad_sum(l[t][0]), LB = quad_sum(l[t][1]);
+    const float iA = LA > 0.f ? 1.f / LA : 0.f, iB = LB > 0.f ? 1.f / LB : 0.f;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      const int col = i * 8 + tg * 2;
+      if (rowA < S)
+        *reinterpret_cast<uint32_t*>(ob + static_cast<int64_t>(rowA) * ldo + col) = pack2(oacc[t][i][0] * iA, oacc[t][i][1] * iA);
+      if (rowB < S)
+        *reinterpret_cast<uint32_t*>(ob + static_cast<int64_t>(rowB) * ldo + col) = pack2(oacc[t][i][2] * iB, oacc[t][i][3] * iB);
+    }
+    if (tg == 0) {
+      if (rowA < S) lb[rowA] = (m[t][0] + log2f(LA)) * LN2;
+      if (rowB < S) lb[rowB] = (m[t][1] + log2f(LB)) * LN2;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- backward
 
 template <int HD>
@@ -506,8 +679,26 @@ int set_smem(int bytes) {
 }
 
 template <int HD>
+int fwd2_impl(int B, int H, int S, const void* qkv, int64_t ldq, void* o, int64_t ldo, float* lse,
+              cudaStream_t st) {
+  using C = Fwd2Cfg<HD>;
+  int rc = set_smem<fa_fwd2<HD>>(C::SMEM);
+  if (rc) return rc;
+  dim3 grid((S + C::BM - 1) / C::BM, B * H);
+  const float sl2 = LOG2E / sqrtf(static_cast<float>(HD));
+  fa_fwd2<HD><<<grid, C::NT, C::SMEM, st>>>(static_cast<const bf16*>(qkv), ldq,
+                                             static_cast<bf16*>(o), ldo, lse, H, S, sl2);
+  return check_launch("fa_fwd2");
+}
+
+int g_fwd_variant = 2;
+
+template <int HD>
 int fwd_impl(int B, int H, int S, const void* qkv, int64_t ldq, void* o, int64_t ldo, float* lse,
              cudaStream_t st) {
+  if constexpr (HD == 64) {
+    if (g_fwd_variant == 2) return fwd2_impl<HD>(B, H, S, qkv, ldq, o, ldo, lse, st);
+  }
   using C = FwdCfg<HD>;
   int rc = set_smem<fa_fwd<HD>>(C::SMEM);
   if (rc) return rc;
