@@ -53,7 +53,8 @@ struct TcCfg {
   static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + TC_EPI_WARPS * TC_STAGE_BYTES +
                                1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int TMEM_COLS = 2 * BN;
+  // two accumulators of BN fp32 columns, rounded up to a legal power-of-2 allocation
+  static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
 
 __device__ __forceinline__ void load16(const void* base, bool f32, int64_t off, int nvalid,
@@ -480,14 +481,25 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   PP_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
   int bn = g_force_bn;
   if (bn == 0) {
+    // Pick the tile width maximising (wave efficiency x per-tile efficiency):
+    // tiles / (waves * SMs) penalises a last partial wave (e.g. 192 tiles on
+    // 148 SMs), the per-tile factor reflects measured mainloop efficiency.
     const int sms = num_sms();
     const int64_t mt = (M + TC_BM - 1) / TC_BM;
-    if (N >= 256 && mt * ((N + 255) / 256) >= sms)
-      bn = 256;
-    else if (N >= 128 && mt * ((N + 127) / 128) >= sms / 2)
-      bn = 128;
-    else
-      bn = 64;
+    const int cands[4] = {256, 192, 128, 64};
+    const double tile_eff[4] = {1.0, 0.95, 0.8, 0.45};
+    double best = -1.0;
+    for (int i = 0; i < 4; ++i) {
+      const int c = cands[i];
+      if (c > 64 && N < c / 2) continue;
+      const int64_t tiles = mt * ((N + c - 1) / c);
+      const int64_t waves = (tiles + sms - 1) / sms;
+      const double score = static_cast<double>(tiles) / (waves * sms) * tile_eff[i];
+      if (score > best + 1e-9) {
+        best = score;
+        bn = c;
+      }
+    }
   }
   // op(A) is [M,K]: transA=0 -> stored [M,K] (K-major); transA=1 -> stored [K,M] (MN-major).
   // op(B) is [K,N]: transB=0 -> stored [K,N] (MN-major); transB=1 -> stored [N,K] (K-major).
@@ -527,6 +539,7 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
            aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi, out_f32};
   switch (bn) {
     case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
+    case 192: return dispatch_majors<192>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
     case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
     case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
     default: set_error("gemm: bad tile width %d", bn); return PC_ERR_ARG;
@@ -536,8 +549,8 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
 }  // namespace pp200
 
 extern "C" int pc_gemm_set_tile_n(int bn) {
-  if (bn != 0 && bn != 64 && bn != 128 && bn != 256) {
-    pp200::set_error("tile width must be 0, 64, 128 or 256");
+  if (bn != 0 && bn != 64 && bn != 128 && bn != 192 && bn != 256) {
+    pp200::set_error("tile width must be 0, 64, 128, 192 or 256");
     return PC_ERR_ARG;
   }
   pp200::g_force_bn = bn;

@@ -52,7 +52,7 @@ def make_operands(M, N, K, ta, tb, dtype, seed=0):
 
 @pytest.mark.parametrize("tma", [1, 0])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("bn", [64, 128, 192, 256])
 @pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (200, 136, 72), (1024, 768, 768)])
 def test_bf16_tcgen05_majors(ta, tb, bn, shape, tma):
     M, N, K = shape

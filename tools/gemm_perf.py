@@ -40,7 +40,7 @@ for name, M, N, K, ta, tb in SHAPES:
     opB = B.t() if tb else B
     g = lambda: torch.matmul(opA, opB, out=C)
     res = {}
-    for bn in (0, 64, 128, 256):
+    for bn in (0, 64, 128, 192, 256):
         _lib.call("pc_gemm_set_tile_n", bn)
         ms = bench(f)
         res[bn] = 2 * M * N * K / ms / 1e9
