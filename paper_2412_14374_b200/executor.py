@@ -757,6 +757,11 @@ class PipelineEngine:
                         counting)
         if ctl.faults:
             raise ctl.faults[0]
+        # send-completion events recorded into the graph cannot be queried; every
+        # replay runs the sends to completion, so the captured buffers are free.
+        for ch in self._channels.values():
+            if isinstance(ch, NcclChannel):
+                ch.sent.clear()
         act.store.flush()
         tl_on, act.timeline = act.timeline, False   # timestamps are read after a replay
         result = self._gather(actors, stats, strict_store=False, to_host=False)
