@@ -126,7 +126,8 @@ int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const void* qkv, in
 int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const void* qkv, int64_t ld_qkv,
                      const void* o, const void* dO, int64_t ld_o, const float* lse, float* delta,
                      void* dqkv, int64_t ld_dqkv, void* stream);
-/* 0 = auto (tensor-core path for bf16 when supported), 1 = force exact SIMT. Test hook. */
+/* 0 = auto (bf16: tcgen05 forward + mma.sync backward when supported), 1 = force exact SIMT,
+ * 2 = force the mma.sync forward. Test hook. */
 int pc_attention_set_impl(int impl);
 
 /* ---- inter-stage transport (Channel, executor.py:201-254) over NCCL ---- */

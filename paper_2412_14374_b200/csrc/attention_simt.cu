@@ -269,7 +269,7 @@ int attention_bwd_simt(int dtype, int B, int H, int S, int hd, const void* qkv, 
 
 using namespace pp200;
 
-static int g_attn_impl = 0;  // 0 auto, 1 force SIMT
+static int g_attn_impl = 0;  // 0 auto (tcgen05 fwd), 1 force SIMT, 2 force mma.sync
 
 extern "C" int pc_attention_set_impl(int impl) {
   g_attn_impl = impl;
@@ -283,6 +283,9 @@ int attention_bwd_tc(int B, int H, int S, int hd, const void* qkv, int64_t ld_qk
                      const void* dO, int64_t ld_o, const float* lse, float* delta, void* dqkv,
                      int64_t ld_dqkv, cudaStream_t st);
 bool attention_tc_supported(int hd, int64_t ld_qkv, int64_t ld_o);
+bool attention_tc5_supported(int hd, int64_t ld_qkv, int64_t ld_o, const void* qkv, const void* o);
+int attention_fwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, void* o, int64_t ld_o,
+                      float* lse, cudaStream_t st);
 }  // namespace pp200
 
 extern "C" int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const void* qkv,
@@ -290,7 +293,9 @@ extern "C" int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const vo
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   PP_CHECK_ARG(B > 0 && H > 0 && S > 0 && hd > 0 && hd <= 32 * 8, "attention: bad dims");
   PP_CHECK_ARG(dtype == PC_F32 || dtype == PC_BF16, "attention: f32/bf16 only");
-  if (dtype == PC_BF16 && g_attn_impl == 0 && attention_tc_supported(hd, ld_qkv, ld_o))
+  if (dtype == PC_BF16 && g_attn_impl == 0 && attention_tc5_supported(hd, ld_qkv, ld_o, qkv, o))
+    return attention_fwd_tc5(B, H, S, qkv, ld_qkv, o, ld_o, lse, st);
+  if (dtype == PC_BF16 && g_attn_impl != 1 && attention_tc_supported(hd, ld_qkv, ld_o))
     return attention_fwd_tc(B, H, S, hd, qkv, ld_qkv, o, ld_o, lse, st);
   return attention_fwd_simt(dtype, B, H, S, hd, qkv, ld_qkv, o, ld_o, lse, st);
 }
@@ -302,7 +307,7 @@ extern "C" int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const vo
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   PP_CHECK_ARG(B > 0 && H > 0 && S > 0 && hd > 0 && hd <= 32 * 8, "attention: bad dims");
   PP_CHECK_ARG(dtype == PC_F32 || dtype == PC_BF16, "attention: f32/bf16 only");
-  if (dtype == PC_BF16 && g_attn_impl == 0 && attention_tc_supported(hd, ld_qkv, ld_o))
+  if (dtype == PC_BF16 && g_attn_impl != 1 && attention_tc_supported(hd, ld_qkv, ld_o))
     return attention_bwd_tc(B, H, S, hd, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv, st);
   int rc = attention_delta(dtype, B, H, S, hd, o, dO, ld_o, delta, st);
   if (rc) return rc;

@@ -473,6 +473,8 @@ int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorM
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn() { return tmap_encoder(); }
+
 int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
                  const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                  int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,

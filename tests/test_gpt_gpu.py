@@ -92,9 +92,10 @@ def _t(x, dt=torch.float32):
 
 
 @pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
-@pytest.mark.parametrize("impl", [0, 1])
-def test_attention_kernels(dt, tol, impl):
-    B, H, S, hd = 2, 3, 80, 64
+@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("S", [80, 256])
+def test_attention_kernels(dt, tol, impl, S):
+    B, H, hd = 2, 3, 64
     rng = np.random.default_rng(3)
     qkv = rng.standard_normal((B * S, 3 * H * hd)) * 0.5
     do = rng.standard_normal((B * S, H * hd))

@@ -23,10 +23,10 @@ for (B, H, S, hd) in [(8, 12, 1024, 64), (4, 16, 2048, 128), (8, 16, 1024, 64)]:
     f = lambda: _lib.call("pc_attention_fwd", 2, B, H, S, hd, qkv.data_ptr(), 3 * d, o.data_ptr(), d, lse.data_ptr(), st)
     b = lambda: _lib.call("pc_attention_bwd", 2, B, H, S, hd, qkv.data_ptr(), 3 * d, o.data_ptr(), do.data_ptr(), d, lse.data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, st)
     flops_f = 4 * B * H * S * S * hd / 2  # causal
-    for impl in (0, 1):
+    for impl in (0, 2):
         _lib.call("pc_attention_set_impl", impl)
-        tf = bench(f, 5 if impl else 20); tb = bench(b, 3 if impl else 20)
-        print(f"B{B} H{H} S{S} hd{hd} {'tc' if impl == 0 else 'simt'}: fwd {tf:.3f} ms ({flops_f/tf/1e9:.0f} TF/s) bwd {tb:.3f} ms ({2.5*flops_f/tb/1e9:.0f} TF/s eq)", flush=True)
+        tf = bench(f, 20); tb = bench(b, 20)
+        print(f"B{B} H{H} S{S} hd{hd} {['tcgen05', 'simt', 'mma.sync'][impl]}: fwd {tf:.3f} ms ({flops_f/tf/1e9:.0f} TF/s) bwd {tb:.3f} ms ({2.5*flops_f/tb/1e9:.0f} TF/s eq)", flush=True)
     _lib.call("pc_attention_set_impl", 0)
     # flash (sdpa) reference timing
     q = qkv[:, :d].view(B, S, H, hd).transpose(1, 2); k = qkv[:, d:2*d].view(B, S, H, hd).transpose(1, 2); v = qkv[:, 2*d:].view(B, S, H, hd).transpose(1, 2)
