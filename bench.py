@@ -274,8 +274,6 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="issue every step from Python instead of replaying the captured graph")
-    ap.add_argument("--graph", action="store_true",
-                    help="also replay captured graphs when N > 1")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -302,9 +300,7 @@ def main():
     tokens_dev = torch.from_numpy(tokens_host).to(dev)
     tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
     eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
-    # Multi-process graph replay (NCCL sends/recvs captured per rank) is still
-    # under validation; N>1 issues eagerly from Python unless --graph is given.
-    use_graph = (not args.no_graph) and (world == 1 or args.graph)
+    use_graph = not args.no_graph
     for _ in range(2):   # eager warm-up: NCCL connections, kernel attributes, allocator
         eng.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False)
     torch.cuda.synchronize()
@@ -414,10 +410,17 @@ def main():
             "wall_s": round(wall, 3),
         }
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
+        # Captured graphs hold references to the per-channel NCCL communicators;
+        # tearing those down blocks, so ranks leave right after a final barrier
+        # (process exit releases every GPU resource).
         dist.barrier()
-        dist.destroy_process_group()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
+    if use_graph:
+        del cap
+    eng.close()
     return 0
 
 
