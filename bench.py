@@ -46,9 +46,23 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+# In-situ rates calibrated from tools/profile_step.py (C2, P=1): block GEMMs
+# ~0.6 PFLOP/s, the large-N LM-head GEMMs ~0.95, attention ~0.1 (fwd+bwd
+# equivalent), bandwidth-bound elementwise / norm / loss work ~3 TB/s.
+_GEMM_RATE, _HEAD_RATE, _ATTN_RATE, _HBM_RATE = 0.6e15, 0.95e15, 0.1e15, 3e12
+
+
 def block_costs(cfg):
-    blk = cfg.block_fwd_flops()
-    return [float(cfg.tokens * cfg.d_model)] + [blk] * cfg.layers + [cfg.head_fwd_flops()]
+    """Per-block fwd+bwd time estimates (s) for stage balancing: FLOPs alone
+    over-weight the LM head, whose GEMMs run much faster than attention."""
+    T, d, f, V, S = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.vocab, cfg.seq_len
+    gemm = 3 * 2.0 * T * (4 * d * d + 2 * d * f)
+    attn = 3.5 * 2.0 * T * S * d            # causal fwd + recomputing bwd
+    elem = 2 * 20.0 * T * d + 2 * 6.0 * T * f  # LN, residuals, GELU, bias grads (bytes)
+    blk = gemm / _GEMM_RATE + attn / _ATTN_RATE + elem / _HBM_RATE
+    head = 3 * 2.0 * T * d * V / _HEAD_RATE + 3 * 2.0 * T * V / _HBM_RATE
+    emb = 4.0 * T * d * 4 / _HBM_RATE
+    return [emb] + [blk] * cfg.layers + [head]
 
 
 def build_plan(P, cfg_kw, M, mode="bf16"):

@@ -27,7 +27,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn();
 namespace {
 
 using bf16 = __nv_bfloat16;
-constexpr int F_BM = 128, F_BN = 64, F_HD = 64, F_STAGES = 3, F_THREADS = 256;
+constexpr int F_BM = 128, F_BN = 64, F_HD = 64, F_STAGES = 2, F_THREADS = 256;
 constexpr int F_Q_BYTES = F_BM * F_HD * 2;    // 16 KB
 constexpr int F_KV_BYTES = F_BN * F_HD * 2;   // 8 KB
 constexpr int F_P_BYTES = F_BM * F_BN * 2;    // 16 KB
@@ -51,7 +51,7 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__global__ void __launch_bounds__(F_THREADS, 1)
+__global__ void __launch_bounds__(F_THREADS, 2)
     fa_fwd_tc5(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, int64_t ldo,
                float* __restrict__ lse, int H, int S, float sl2) {
   extern __shared__ uint8_t smem_raw[];
@@ -164,18 +164,26 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         sv[i] = v;
         mx = fmaxf(mx, v);
       }
+      // Lazy rescaling (FA4): keep the running reference max unless the row
+      // max grows by more than 8 (log2 units, P <= 256 stays exact enough in
+      // bf16); O and l only need a correction when the reference moves.
       const float mn = fmaxf(m, mx);
-      const float ref = mn == -INFINITY ? 0.f : mn;
-      const float corr = ex2(m - ref);
+      float corr = 1.f;
+      if (j == 0 || m == -INFINITY) {
+        m = mn == -INFINITY ? 0.f : mn;
+        corr = 0.f;  // nothing accumulated yet
+      } else if (mn > m + 8.f) {
+        corr = ex2(m - mn);
+        m = mn;
+      }
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < F_BN; ++i) {
-        const float p = ex2(sv[i] - ref);
+        const float p = ex2(sv[i] - m);
         sv[i] = p;
         sum += p;
       }
       l = l * corr + sum;
-      m = mn;
       // P row -> smem, K-major with 128B swizzle (8 chunks of 8 bf16)
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -187,7 +195,7 @@ __global__ void __launch_bounds__(F_THREADS, 1)
       }
       fence_proxy_async_smem();
       // rescale O by corr (PV_{j-1} is complete: covered by the S_j commit)
-      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
+      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f && l > 0.f)) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t orr[16];
