@@ -240,6 +240,349 @@ __global__ void __launch_bounds__(F_THREADS, 2)
   if (warp == 2) tmem_dealloc(tmem, 128);
 }
 
+
+// ------------------------------------------------------------------ backward
+// Writes 16 bf16 (two 16 B chunks, logical chunk index c2 and c2+1) of row r
+// into a 128B-swizzled [rows x 64] K-major tile.
+__device__ __forceinline__ void st_row16(uint8_t* tile, int r, int c2, const float* v) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint4 u;
+    __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hp[k] = __floats2bfloat162_rn(v[8 * h + 2 * k], v[8 * h + 2 * k + 1]);
+    *reinterpret_cast<uint4*>(tile + r * 128 + (((c2 + h) ^ (r & 7)) << 4)) = u;
+  }
+}
+
+__device__ __forceinline__ void store_row64(bf16* dst, const uint32_t* acc, float scale) {
+  uint4 u[8];
+  __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(u);
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    hp[k] = __floats2bfloat162_rn(__uint_as_float(acc[2 * k]) * scale, __uint_as_float(acc[2 * k + 1]) * scale);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) reinterpret_cast<uint4*>(dst)[k] = u[k];
+}
+
+constexpr int B_KEYS = 128, B_Q = 64;  // dK/dV: 128 keys per CTA, 64-query blocks
+constexpr int BKV_SMEM = 2 * 16384 /*K,V*/ + 2 * 2 * 8192 /*Q,dO stages*/ + 2 * 16384 /*P^T,dS^T*/ + 1024 + 256;
+
+// dK, dV for 128 keys of one (batch, head): S^T = K Q^T and dP^T = V dO^T per
+// 64-query block (TMEM), P^T / dS^T built by one thread per key row, then
+// dV += P^T dO and dK += dS^T Q (TMEM accumulators).
+__global__ void __launch_bounds__(F_THREADS, 1)
+    fa_bwd_dkdv_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
+                    const float* __restrict__ lse, const float* __restrict__ delta,
+                    bf16* __restrict__ dqkv, int64_t ldd, int H, int S, float sl2, float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + 16384;
+  uint8_t* sQ = sV + 16384;      // [2][64 x 64]
+  uint8_t* sG = sQ + 2 * 8192;   // dO, [2][64 x 64]
+  uint8_t* sPt = sG + 2 * 8192;  // P^T  [128 keys x 64 q]
+  uint8_t* sDt = sPt + 16384;    // dS^T [128 keys x 64 q]
+  uint64_t* bar_kv = reinterpret_cast<uint64_t*>(sDt + 16384);
+  uint64_t* q_full = bar_kv + 1;
+  uint64_t* q_empty = q_full + 2;
+  uint64_t* s_full = q_empty + 2;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* done = p_full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;  // early key blocks see the most query blocks: launch first
+  const int b = blockIdx.y / H, h = blockIdx.y % H;
+  const int d = H * F_HD;
+  const int k0 = kb * B_KEYS;
+  const int brow = b * S;
+  const int qbeg = k0 / B_Q, nqb = (S + B_Q - 1) / B_Q;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tg);
+    mbar_init(bar_kv, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tSt = tmem, tPt = tmem + 64, tdV = tmem + 128, tdK = tmem + 192;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bar_kv, 2 * 16384);
+      for (int hf = 0; hf < 2; ++hf) {
+        tma_load_2d(sK + hf * 8192, &tq, bar_kv, d + h * F_HD, brow + k0 + hf * 64);
+        tma_load_2d(sV + hf * 8192, &tq, bar_kv, 2 * d + h * F_HD, brow + k0 + hf * 64);
+      }
+      for (int qb = qbeg, i = 0; qb < nqb; ++qb, ++i) {
+        const int st = i & 1;
+        mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * 8192);
+        tma_load_2d(sQ + st * 8192, &tq, &q_full[st], h * F_HD, brow + qb * B_Q);
+        tma_load_2d(sG + st * 8192, &tg, &q_full[st], h * F_HD, brow + qb * B_Q);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_T = umma_idesc_bf16(128, B_Q, 0, 0);   // K/V x (Q/dO)^T, N = 64 queries
+      constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // P^T/dS^T x (dO/Q), N = 64 dims
+      mbar_wait(bar_kv, 0);
+      tc_fence_after();
+      const uint32_t ka = smem_u32(sK), va = smem_u32(sV), pa = smem_u32(sPt), da = smem_u32(sDt);
+      for (int qb = qbeg, i = 0; qb < nqb; ++qb, ++i) {
+        const int st = i & 1;
+        mbar_wait(&q_full[st], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sQ + st * 8192), ga = smem_u32(sG + st * 8192);
+#pragma unroll
+        for (int k = 0; k < F_HD / 16; ++k) {
+          tc_mma_f16(tSt, umma_sdesc_sw128(ka + k * 32, 16, 1024), umma_sdesc_sw128(qa + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
+          tc_mma_f16(tPt, umma_sdesc_sw128(va + k * 32, 16, 1024), umma_sdesc_sw128(ga + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
+        }
+        tc_commit(s_full);
+        mbar_wait(p_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < B_Q / 16; ++k) {
+          const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+          tc_mma_f16(tdV, umma_sdesc_sw128(pa + k * 32, 16, 1024), umma_sdesc_sw128(ga + k * 2048, 8192, 1024), ID_A, acc);
+          tc_mma_f16(tdK, umma_sdesc_sw128(da + k * 32, 16, 1024), umma_sdesc_sw128(qa + k * 2048, 8192, 1024), ID_A, acc);
+        }
+        tc_commit(&q_empty[st]);
+      }
+      tc_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int r = qw * 32 + lane;  // key row in the tile
+    const int key = k0 + r;
+    const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
+    const float* Lr = lse + (static_cast<int64_t>(b) * H + h) * S;
+    const float* Dr = delta + (static_cast<int64_t>(b) * H + h) * S;
+    for (int qb = qbeg, i = 0; qb < nqb; ++qb, ++i) {
+      mbar_wait(s_full, i & 1);
+      tc_fence_after();
+      const int m0 = qb * B_Q;
+#pragma unroll
+      for (int c = 0; c < B_Q / 16; ++c) {
+        uint32_t sr[16], dr[16];
+        tmem_ld16(tSt + lo + c * 16, sr);
+        tmem_ld16(tPt + lo + c * 16, dr);
+        tc_wait_ld();
+        float pv[16], dv[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int q = m0 + c * 16 + e;
+          const bool ok = q >= key && q < S;
+          const float lq = ok ? __ldg(Lr + q) * 1.4426950408889634f : 0.f;
+          const float p = ok ? ex2(__uint_as_float(sr[e]) * sl2 - lq) : 0.f;
+          pv[e] = p;
+          dv[e] = ok ? p * (__uint_as_float(dr[e]) - __ldg(Dr + q)) : 0.f;
+        }
+        st_row16(sPt, r, 2 * c, pv);
+        st_row16(sDt, r, 2 * c, dv);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    uint32_t acc[64];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld16(tdV + lo + c * 16, acc + c * 16);
+    tc_wait_ld();
+    bf16* base = dqkv + static_cast<int64_t>(brow + key) * ldd + h * F_HD;
+    if (key < S) store_row64(base + 2 * d, acc, 1.f);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld16(tdK + lo + c * 16, acc + c * 16);
+    tc_wait_ld();
+    if (key < S) store_row64(base + d, acc, scale);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 256);
+}
+
+constexpr int BQ_SMEM = 2 * 16384 /*Q,dO*/ + 2 * 2 * 8192 /*K,V stages*/ + 16384 /*dS*/ + 1024 + 256;
+
+// dQ for 128 queries of one (batch, head): S = Q K^T, dP = dO V^T per 64-key
+// block, dS by one thread per query row, dQ += dS K (TMEM accumulator).
+__global__ void __launch_bounds__(F_THREADS, 1)
+    fa_bwd_dq_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
+                  const float* __restrict__ lse, const float* __restrict__ delta,
+                  bf16* __restrict__ dqkv, int64_t ldd, int H, int S, float sl2, float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sG = sQ + 16384;
+  uint8_t* sK = sG + 16384;       // [2][64 x 64]
+  uint8_t* sV = sK + 2 * 8192;    // [2][64 x 64]
+  uint8_t* sD = sV + 2 * 8192;    // dS [128 q x 64 keys]
+  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sD + 16384);
+  uint64_t* kv_full = bar_q + 1;
+  uint64_t* kv_empty = kv_full + 2;
+  uint64_t* s_full = kv_empty + 2;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* done = p_full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (S + F_BM - 1) / F_BM;
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
+  const int b = blockIdx.y / H, h = blockIdx.y % H;
+  const int d = H * F_HD;
+  const int q0 = qb * F_BM;
+  const int brow = b * S;
+  const int nkb = (min(S, q0 + F_BM) + F_BN - 1) / F_BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tg);
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tP = tmem + 64, tdQ = tmem + 128;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bar_q, 2 * 16384);
+      for (int hf = 0; hf < 2; ++hf) {
+        tma_load_2d(sQ + hf * 8192, &tq, bar_q, h * F_HD, brow + q0 + hf * 64);
+        tma_load_2d(sG + hf * 8192, &tg, bar_q, h * F_HD, brow + q0 + hf * 64);
+      }
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * 8192);
+        tma_load_2d(sK + st * 8192, &tq, &kv_full[st], d + h * F_HD, brow + j * F_BN);
+        tma_load_2d(sV + st * 8192, &tq, &kv_full[st], 2 * d + h * F_HD, brow + j * F_BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_T = umma_idesc_bf16(128, F_BN, 0, 0);  // Q/dO x (K/V)^T
+      constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // dS x K (MN-major)
+      mbar_wait(bar_q, 0);
+      tc_fence_after();
+      const uint32_t qa = smem_u32(sQ), ga = smem_u32(sG), dsa = smem_u32(sD);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ka = smem_u32(sK + st * 8192), va = smem_u32(sV + st * 8192);
+#pragma unroll
+        for (int k = 0; k < F_HD / 16; ++k) {
+          tc_mma_f16(tS, umma_sdesc_sw128(qa + k * 32, 16, 1024), umma_sdesc_sw128(ka + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
+          tc_mma_f16(tP, umma_sdesc_sw128(ga + k * 32, 16, 1024), umma_sdesc_sw128(va + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
+        }
+        tc_commit(s_full);
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < F_BN / 16; ++k)
+          tc_mma_f16(tdQ, umma_sdesc_sw128(dsa + k * 32, 16, 1024), umma_sdesc_sw128(ka + k * 2048, 8192, 1024), ID_A,
+                     (j > 0 || k > 0) ? 1u : 0u);
+        tc_commit(&kv_empty[st]);
+      }
+      tc_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int r = qw * 32 + lane;
+    const int row = q0 + r;
+    const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
+    const int64_t vrow = (static_cast<int64_t>(b) * H + h) * S + row;
+    const float l2 = row < S ? lse[vrow] * 1.4426950408889634f : 0.f;
+    const float dl = row < S ? delta[vrow] : 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      const int n0 = j * F_BN;
+#pragma unroll
+      for (int c = 0; c < F_BN / 16; ++c) {
+        uint32_t sr[16], dr[16];
+        tmem_ld16(tS + lo + c * 16, sr);
+        tmem_ld16(tP + lo + c * 16, dr);
+        tc_wait_ld();
+        float dsv[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int key = n0 + c * 16 + e;
+          const bool ok = key <= row && key < S && row < S;
+          const float p = ok ? ex2(__uint_as_float(sr[e]) * sl2 - l2) : 0.f;
+          dsv[e] = ok ? p * (__uint_as_float(dr[e]) - dl) : 0.f;
+        }
+        st_row16(sD, r, 2 * c, dsv);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    uint32_t acc[64];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld16(tdQ + lo + c * 16, acc + c * 16);
+    tc_wait_ld();
+    if (row < S) store_row64(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD, acc, scale);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 256);
+}
+
+int make_tmap_rows64(CUtensorMap* m, const void* base, int64_t ld, int64_t rows) {
+  auto enc = tmap_encoder_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return PC_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, 64u};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (attention) failed (%d)", static_cast<int>(r));
+    return PC_ERR_CUDA;
+  }
+  return PC_OK;
+}
 }  // namespace
 
 bool attention_tc5_supported(int hd, int64_t ld_qkv, int64_t ld_o, const void* qkv, const void* o) {
@@ -277,4 +620,38 @@ int attention_fwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, void
   return check_launch("fa_fwd_tc5");
 }
 
+}  // namespace pp200
+
+namespace pp200 {
+int attention_delta(int dtype, int B, int H, int S, int hd, const void* o, const void* dO,
+                    int64_t ld_o, float* delta, cudaStream_t st);
+
+int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, const void* o,
+                      const void* dO, int64_t ld_o, const float* lse, float* delta, void* dqkv,
+                      int64_t ld_dqkv, cudaStream_t st) {
+  int rc = attention_delta(PC_BF16, B, H, S, F_HD, o, dO, ld_o, delta, st);
+  if (rc) return rc;
+  CUtensorMap tq, tg;
+  rc = make_tmap_rows64(&tq, qkv, ld_qkv, static_cast<int64_t>(B) * S);
+  if (rc) return rc;
+  rc = make_tmap_rows64(&tg, dO, ld_o, static_cast<int64_t>(B) * S);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dkdv_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, BKV_SMEM));
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dq_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, BQ_SMEM));
+    attr = true;
+  }
+  const float scale = 1.f / sqrtf(static_cast<float>(F_HD));
+  const float sl2 = scale * 1.4426950408889634f;
+  dim3 g1((S + B_KEYS - 1) / B_KEYS, B * H);
+  fa_bwd_dkdv_tc5<<<g1, F_THREADS, BKV_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
+                                                    ld_dqkv, H, S, sl2, scale);
+  rc = check_launch("fa_bwd_dkdv_tc5");
+  if (rc) return rc;
+  dim3 g2((S + F_BM - 1) / F_BM, B * H);
+  fa_bwd_dq_tc5<<<g2, F_THREADS, BQ_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
+                                                 ld_dqkv, H, S, sl2, scale);
+  return check_launch("fa_bwd_dq_tc5");
+}
 }  // namespace pp200
