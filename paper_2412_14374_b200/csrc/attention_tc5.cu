@@ -271,7 +271,7 @@ constexpr int BKV_SMEM = 2 * 16384 /*K,V*/ + 2 * 2 * 8192 /*Q,dO stages*/ + 2 * 
 // dK, dV for 128 keys of one (batch, head): S^T = K Q^T and dP^T = V dO^T per
 // 64-query block (TMEM), P^T / dS^T built by one thread per key row, then
 // dV += P^T dO and dK += dS^T Q (TMEM accumulators).
-__global__ void __launch_bounds__(F_THREADS, 1)
+__global__ void __launch_bounds__(F_THREADS, 2)
     fa_bwd_dkdv_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                     const float* __restrict__ lse, const float* __restrict__ delta,
                     bf16* __restrict__ dqkv, int64_t ldd, int H, int S, float sl2, float scale) {
@@ -376,21 +376,41 @@ __global__ void __launch_bounds__(F_THREADS, 1)
       mbar_wait(s_full, i & 1);
       tc_fence_after();
       const int m0 = qb * B_Q;
-#pragma unroll
+      // lse / delta of this query block: every thread reads the same 64 values
+      // (16 B broadcast loads; the block never straddles the end of a batch row
+      // range because S is a multiple of 8)
+      const bool full = m0 + B_Q <= S && (S % 4) == 0;
+#pragma unroll 1
       for (int c = 0; c < B_Q / 16; ++c) {
         uint32_t sr[16], dr[16];
         tmem_ld16(tSt + lo + c * 16, sr);
         tmem_ld16(tPt + lo + c * 16, dr);
+        float lq[16], dq[16];
+        if (full) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(Lr + m0 + c * 16) + v);
+            const float4 g = __ldg(reinterpret_cast<const float4*>(Dr + m0 + c * 16) + v);
+            lq[4 * v] = a.x; lq[4 * v + 1] = a.y; lq[4 * v + 2] = a.z; lq[4 * v + 3] = a.w;
+            dq[4 * v] = g.x; dq[4 * v + 1] = g.y; dq[4 * v + 2] = g.z; dq[4 * v + 3] = g.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int q = m0 + c * 16 + e;
+            lq[e] = q < S ? __ldg(Lr + q) : 0.f;
+            dq[e] = q < S ? __ldg(Dr + q) : 0.f;
+          }
+        }
         tc_wait_ld();
         float pv[16], dv[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int q = m0 + c * 16 + e;
           const bool ok = q >= key && q < S;
-          const float lq = ok ? __ldg(Lr + q) * 1.4426950408889634f : 0.f;
-          const float p = ok ? ex2(__uint_as_float(sr[e]) * sl2 - lq) : 0.f;
+          const float p = ok ? ex2(__uint_as_float(sr[e]) * sl2 - lq[e] * 1.4426950408889634f) : 0.f;
           pv[e] = p;
-          dv[e] = ok ? p * (__uint_as_float(dr[e]) - __ldg(Dr + q)) : 0.f;
+          dv[e] = ok ? p * (__uint_as_float(dr[e]) - dq[e]) : 0.f;
         }
         st_row16(sPt, r, 2 * c, pv);
         st_row16(sDt, r, 2 * c, dv);

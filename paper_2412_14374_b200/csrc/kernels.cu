@@ -188,7 +188,20 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
   const bool vec = (lda % 8 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) &&
                    (MODE == 0 || (reinterpret_cast<uintptr_t>(x) & 15) == 0);
   float s1[8] = {}, s2[8] = {};
-  for (int64_t r = r0 + w; r < r1; r += 8) {
+  int64_t r = r0 + w;
+  if (MODE == 0) {
+    // 4 independent rows in flight per iteration (latency-bound otherwise)
+    for (; r + 24 < r1; r += 32) {
+      float v0[8], v1[8], v2[8], v3[8];
+      load8(a + r * lda, c0, cols, vec, v0);
+      load8(a + (r + 8) * lda, c0, cols, vec, v1);
+      load8(a + (r + 16) * lda, c0, cols, vec, v2);
+      load8(a + (r + 24) * lda, c0, cols, vec, v3);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s1[j] += (v0[j] + v1[j]) + (v2[j] + v3[j]);
+    }
+  }
+  for (; r < r1; r += 8) {
     float v[8];
     load8(a + r * lda, c0, cols, vec, v);
     if (MODE == 0) {
