@@ -49,6 +49,9 @@ enum pc_dtype { PC_F32 = 0, PC_F64 = 1, PC_BF16 = 2, PC_I32 = 3 };
 #define PC_EPI_ACCUM 16     /* C += acc (fp32 C; in-place gradient accumulation)  */
 #define PC_EPI_RELU 32      /* aux_out = acc; C = max(acc, 0)  (executor.py:70-71) */
 #define PC_EPI_RELU_GRAD 64 /* C = acc * (aux[m,n] > 0)        (executor.py:89-90) */
+#define PC_EPI_SPLITK_ZERO_C 128 /* caller guarantees an fp32 C filled with zeros: the
+                                    kernel may split K in two halves reduce-added into C
+                                    (deterministic: two terms onto 0 commute) */
 
 const char* pc_last_error(void);
 int pc_version(void);

@@ -23,6 +23,7 @@ EPI_GELU_GRAD = 8
 EPI_ACCUM = 16
 EPI_RELU = 32
 EPI_RELU_GRAD = 64
+EPI_SPLITK_ZERO_C = 128
 
 _c_i = ctypes.c_int
 _c_i64 = ctypes.c_int64

@@ -96,6 +96,14 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, 
       "r"(smem_u32(src)), "r"(x), "r"(y)
       : "memory");
 }
+// smem -> global element-wise add (fp32) through TMA.
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* src, int x, int y) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(src)), "r"(x), "r"(y)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

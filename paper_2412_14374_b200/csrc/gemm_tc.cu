@@ -34,6 +34,7 @@ constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_MN_CHUNK_BYTES = TC_BK * 128;  // one 64-wide MN box of BK rows
 
 struct TcEpi {
+  int ksplit;  // 1, or 2: two K halves reduce-added (TMA add) onto a zero-filled fp32 C
   int tma_c;  // C written through smem + TMA bulk tensor store
   int tma_u;  // GELU/RELU pre-activation (aux_out) through smem + TMA as well
   void* C;
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + TC_BM - 1) / TC_BM, num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
+  const int num_units = num_tiles * ep.ksplit;
   const int nk = (K + TC_BK - 1) / TC_BK;
 
   if (warp == 0 && lane == 0) {
@@ -246,9 +248,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int t = u % num_tiles, sp = u / num_tiles;
         const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = sp * nk / ep.ksplit; kb < (sp + 1) * nk / ep.ksplit; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           uint8_t* a = sA + stage * TC_A_BYTES;
@@ -280,11 +283,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int sp = u / num_tiles;
+        const int kb0 = sp * nk / ep.ksplit, kb1 = (sp + 1) * nk / ep.ksplit;
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * TC_A_BYTES);
@@ -295,7 +300,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                      : umma_sdesc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_sdesc_sw128(b_addr + k * 2048, TC_MN_CHUNK_BYTES, 1024)
                                      : umma_sdesc_sw128(b_addr + k * 32, 16, 1024);
-            tc_mma_f16(d, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+            tc_mma_f16(d, ad, bd, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -319,7 +324,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool tma = ep.tma_c != 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      const int t = u % num_tiles;
       const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * BN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
@@ -358,7 +364,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+          if (ep.ksplit > 1)
+            tma_reduce_add_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+          else
+            tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
           if (stage_u) tma_store_2d(&tmU, stg + 2048, n0 + cc, m0 + q * 32);
           bulk_commit();
         }
@@ -455,7 +464,7 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr_set = true;
   }
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN) * ep.ksplit;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, M, N, K, ep);
   return check_launch("tc_gemm_kernel");
@@ -537,7 +546,14 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     rc = make_tmap_c(&tu, aux_out, N, M, ldaux_out, false);
     if (rc) return rc;
   }
-  TcEpi ep{tma_c ? 1 : 0, tma_u ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
+  // Deterministic split-K (exactly 2 halves onto a zero-filled fp32 C) when the
+  // caller allows it and the tile count leaves most SMs idle.
+  int ksplit = 1;
+  if ((epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c && K >= 2 * TC_BK * 8) {
+    const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
+    if (tiles * 2 <= num_sms()) ksplit = 2;
+  }
+  TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
            aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi, out_f32};
   switch (bn) {
     case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);

@@ -513,13 +513,13 @@ class DeviceOps:
         else:
             dout = dz
         # MLP
-        self._gemm(f32, 1, 0, d, f, T, dout, d, sv["gu"], f, gs("w_fc2"), f)
+        self._gemm(f32, 1, 0, d, f, T, dout, d, sv["gu"], f, gs("w_fc2"), f, _lib.EPI_SPLITK_ZERO_C)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dout.data_ptr(), d,
              gs("b_fc2").data_ptr(), 0, *self.red_ws(T, d), self.st)
         du = self.empty((T, f), act)
         self._gemm(act, 0, 0, T, f, d, dout, d, sl("w_fc2"), f, du, f, _lib.EPI_GELU_GRAD,
                    aux=sv["u"], ldaux=f)
-        self._gemm(f32, 1, 0, f, d, T, du, f, sv["a2"], d, gs("w_fc1"), d)
+        self._gemm(f32, 1, 0, f, d, T, du, f, sv["a2"], d, gs("w_fc1"), d, _lib.EPI_SPLITK_ZERO_C)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, f, du.data_ptr(), f,
              gs("b_fc1").data_ptr(), 0, *self.red_ws(T, f), self.st)
         da2 = self.empty((T, d), act)
@@ -530,7 +530,7 @@ class DeviceOps:
              dout.data_ptr(), dh1.data_ptr(), gs("ln2_g").data_ptr(), gs("ln2_b").data_ptr(),
              *self.red_ws(T, d), self.st)
         # attention
-        self._gemm(f32, 1, 0, d, d, T, dh1, d, sv["o"], d, gs("w_o"), d)
+        self._gemm(f32, 1, 0, d, d, T, dh1, d, sv["o"], d, gs("w_o"), d, _lib.EPI_SPLITK_ZERO_C)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dh1.data_ptr(), d,
              gs("b_o").data_ptr(), 0, *self.red_ws(T, d), self.st)
         do = self.empty((T, d), act)
@@ -540,7 +540,7 @@ class DeviceOps:
         call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
              cfg.head_dim, sv["qkv"].data_ptr(), 3 * d, sv["o"].data_ptr(), do.data_ptr(), d,
              sv["lse"].data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, self.st)
-        self._gemm(f32, 1, 0, 3 * d, d, T, dqkv, 3 * d, sv["a"], d, gs("w_qkv"), d)
+        self._gemm(f32, 1, 0, 3 * d, d, T, dqkv, 3 * d, sv["a"], d, gs("w_qkv"), d, _lib.EPI_SPLITK_ZERO_C)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, 3 * d, dqkv.data_ptr(), 3 * d,
              gs("b_qkv").data_ptr(), 0, *self.red_ws(T, 3 * d), self.st)
         da = self.empty((T, d), act)
@@ -584,7 +584,7 @@ class DeviceOps:
         self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V, wte, d, dh, d)
         dw = self.zeros((layout_size(self._elay),), torch.float32)
         self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
-                   self._slice(dw, self._elay, "wte"), d)
+                   self._slice(dw, self._elay, "wte"), d, _lib.EPI_SPLITK_ZERO_C)
         return (dh, dw)
 
 

@@ -118,3 +118,19 @@ def test_epilogues(dtype):
     run_gemm(A, B, 0, 1, M, N, K, torch.float32, epi=_lib.EPI_ACCUM, C=acc)
     torch.cuda.synchronize()
     assert rel(acc, want) < (1e-5 if dtype != torch.bfloat16 else 1e-5)
+
+
+@pytest.mark.parametrize("shape", [(768, 768, 8192), (256, 192, 4096), (200, 72, 2000)])
+def test_splitk_zero_c_deterministic(shape):
+    """The split-K hint (two K halves reduce-added onto a zero C) is exact to the
+    reference and bitwise reproducible run to run."""
+    M, N, K = shape
+    A, B, ref = make_operands(M, N, K, 1, 0, torch.bfloat16, seed=5)
+    outs = []
+    for _ in range(3):
+        C = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+        run_gemm(A, B, 1, 0, M, N, K, torch.float32, epi=_lib.EPI_SPLITK_ZERO_C, C=C)
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert rel(outs[0], ref) < 1e-5
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
