@@ -37,6 +37,7 @@ struct TcEpi {
   int ksplit;  // 1, or 2: two K halves reduce-added (TMA add) onto a zero-filled fp32 C
   int tma_c;  // C written through smem + TMA bulk tensor store
   int tma_u;  // GELU/RELU pre-activation (aux_out) through smem + TMA as well
+  int tma_a;  // residual / activation-derivative input (aux) read through TMA boxes
   void* C;
   int64_t ldc;
   const float* bias;
@@ -125,7 +126,7 @@ __device__ __forceinline__ void store16(void* base, bool f32, int64_t off, int n
 // store_c: write C here (direct path).  pre != nullptr: the pre-activation of
 // GELU/RELU is returned there (staged for a TMA store) instead of stored.
 __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, float* v,
-                                           bool store_c, float* pre) {
+                                           bool store_c, float* pre, const float* aux_pre) {
   const int nvalid = min(16, ep.N - col);
   const bool f32 = ep.out_f32 != 0;
   const int fl = ep.flags;
@@ -166,7 +167,12 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
   }
   if (fl & (PC_EPI_RESIDUAL | PC_EPI_GELU_GRAD | PC_EPI_RELU_GRAD)) {
     float a[16];
-    load16(ep.aux, f32, static_cast<int64_t>(row) * ep.ldaux + col, nvalid, a);
+    if (aux_pre) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = aux_pre[i];
+    } else {
+      load16(ep.aux, f32, static_cast<int64_t>(row) * ep.ldaux + col, nvalid, a);
+    }
     if (fl & PC_EPI_RESIDUAL) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] += a[i];
@@ -204,7 +210,7 @@ template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmU,
-                   int M, int N, int K, TcEpi ep) {
+                   const __grid_constant__ CUtensorMap tmX, int M, int N, int K, TcEpi ep) {
   using Cfg = TcCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -217,7 +223,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xbar = tempty + 2;  // one aux-tile barrier per epilogue warp
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + TC_EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + TC_BM - 1) / TC_BM, num_n = (N + BN - 1) / BN;
@@ -236,6 +243,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], TC_EPI_WARPS);
     }
+    for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&xbar[w], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tslot, Cfg::TMEM_COLS);
@@ -322,6 +330,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint8_t* stg = sEpi + (warp - 4) * TC_STAGE_BYTES;
     const bool f32 = ep.out_f32 != 0;
     const bool tma = ep.tma_c != 0;
+    const bool tma_x = ep.tma_a != 0;
+    uint8_t* xstg = stg + 2048;              // aux box (bf16 32x32, 64B swizzle)
+    uint64_t* xb = &xbar[warp - 4];
+    uint32_t xphase = 0;
     int acc = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
@@ -332,20 +344,47 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int row = m0 + q * 32 + lane;
       const uint32_t tb =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+      if (tma_x && lane == 0) {  // prefetch the first aux box of this tile
+        mbar_expect_tx(xb, 2048);
+        tma_load_2d(xstg, &tmX, xb, n0 + half * HALF, m0 + q * 32);
+      }
 #pragma unroll 1
       for (int c = 0; c < HALF; c += 32) {
         const int cc = half * HALF + c;
         uint32_t r[32];
         tmem_ld16(tb + cc, r);
         tmem_ld16(tb + cc + 16, r + 16);
+        float xa[32];
+        if (tma_x) {
+          mbar_wait(xb, xphase);
+          xphase ^= 1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 u = *stage_chunk64(xstg, lane, j);
+            const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 f2 = __bfloat1622float2(hx[k]);
+              xa[8 * j + 2 * k] = f2.x;
+              xa[8 * j + 2 * k + 1] = f2.y;
+            }
+          }
+          __syncwarp();
+          if (lane == 0 && c + 32 < HALF) {  // prefetch the next chunk's box
+            mbar_expect_tx(xb, 2048);
+            tma_load_2d(xstg, &tmX, xb, n0 + cc + 32, m0 + q * 32);
+          }
+        }
         tc_wait_ld();
         float* v = reinterpret_cast<float*>(r);
         float pre[32];
         const bool stage_u = ep.tma_u != 0;
         if (row < M) {
-          if (n0 + cc < N) epilogue16(ep, row, n0 + cc, v, !tma, stage_u ? pre : nullptr);
+          if (n0 + cc < N)
+            epilogue16(ep, row, n0 + cc, v, !tma, stage_u ? pre : nullptr, tma_x ? xa : nullptr);
           if (n0 + cc + 16 < N)
-            epilogue16(ep, row, n0 + cc + 16, v + 16, !tma, stage_u ? pre + 16 : nullptr);
+            epilogue16(ep, row, n0 + cc + 16, v + 16, !tma, stage_u ? pre + 16 : nullptr,
+                       tma_x ? xa + 16 : nullptr);
         }
         if (!tma) continue;
         if (lane == 0) bulk_wait_read0();   // previous chunk's stores have read the stage
@@ -456,7 +495,8 @@ int g_tma_store = 1;
 
 template <int BN, bool A_MN, bool B_MN>
 int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-              const CUtensorMap& tu, int M, int N, int K, const TcEpi& ep, cudaStream_t st) {
+              const CUtensorMap& tu, const CUtensorMap& tx, int M, int N, int K, const TcEpi& ep,
+              cudaStream_t st) {
   using Cfg = TcCfg<BN>;
   static bool attr_set = false;  // benign race: idempotent attribute write
   if (!attr_set) {
@@ -466,18 +506,18 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
   }
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN) * ep.ksplit;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, M, N, K, ep);
+  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, tx, M, N, K, ep);
   return check_launch("tc_gemm_kernel");
 }
 
 template <int BN>
 int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
-                    const CUtensorMap& tc, const CUtensorMap& tu, int M, int N, int K,
-                    const TcEpi& ep, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, tc, tu, M, N, K, ep, st);
-  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, tc, tu, M, N, K, ep, st);
-  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, tc, tu, M, N, K, ep, st);
-  return launch_tc<BN, true, true>(ta, tb, tc, tu, M, N, K, ep, st);
+                    const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, int M,
+                    int N, int K, const TcEpi& ep, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  return launch_tc<BN, true, true>(ta, tb, tc, tu, tx, M, N, K, ep, st);
 }
 
 }  // namespace
@@ -535,9 +575,19 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
                      (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
   const bool tma_u = tma_c && !out_f32 && (epi & (PC_EPI_GELU | PC_EPI_RELU)) &&
                      (reinterpret_cast<uintptr_t>(aux_out) & 15) == 0 && (ldaux_out * 2) % 16 == 0;
-  CUtensorMap tc, tu;
+  // aux (residual / activation-derivative input) through TMA boxes in the free
+  // half of the bf16 staging tile (never together with a staged pre-activation)
+  const bool tma_a = tma_c && !out_f32 && !tma_u &&
+                     (epi & (PC_EPI_RESIDUAL | PC_EPI_GELU_GRAD | PC_EPI_RELU_GRAD)) &&
+                     (reinterpret_cast<uintptr_t>(aux) & 15) == 0 && (ldaux * 2) % 16 == 0;
+  CUtensorMap tc, tu, tx;
   memset(&tc, 0, sizeof(tc));
   memset(&tu, 0, sizeof(tu));
+  memset(&tx, 0, sizeof(tx));
+  if (tma_a) {
+    rc = make_tmap_c(&tx, const_cast<void*>(aux), N, M, ldaux, false);
+    if (rc) return rc;
+  }
   if (tma_c) {
     rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0);
     if (rc) return rc;
@@ -553,13 +603,13 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
     if (tiles * 2 <= num_sms()) ksplit = 2;
   }
-  TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
+  TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, tma_a ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
            aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi, out_f32};
   switch (bn) {
-    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
-    case 192: return dispatch_majors<192>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
-    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
-    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, tc, tu, (int)M, (int)N, (int)K, ep, st);
+    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
+    case 192: return dispatch_majors<192>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
+    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
+    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
     default: set_error("gemm: bad tile width %d", bn); return PC_ERR_ARG;
   }
 }
