@@ -66,8 +66,14 @@ int pc_gemm(int dtype_in, int dtype_out, int transA, int transB, int64_t M, int6
             int epilogue, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
             int64_t ldaux_out, void* stream);
 
-/* Force the tcgen05 GEMM tile width (0 = heuristic, else 64/128/256). Test hook. */
+/* Force the tcgen05 GEMM tile width (0 = heuristic, else 64/128/192/256). Test hook. */
 int pc_gemm_set_tile_n(int bn);
+/* CTA-pair (cta_group::2, 256-row tiles over two SMs) selection: 0 = heuristic,
+ * 1 = never, 2 = whenever the tile allows it (128/256; 192 with a K-major B).  Test hook. */
+int pc_gemm_set_cta_pair(int mode);
+/* Profiling ablation of the tcgen05 GEMM (outputs are garbage while set):
+ * bit0 = skip the epilogue work, bit1 = skip the operand TMA loads. */
+int pc_gemm_set_ablation(int bits);
 /* 1 (default) = write C through smem + TMA bulk store when legal; 0 = direct stores. Test hook. */
 int pc_gemm_set_tma_store(int on);
 

@@ -29,7 +29,8 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int TC_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr int TC_EPI_WARPS = 8;
-constexpr int TC_STAGE_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B
+constexpr int TC_STAGE_BYTES = 8192;  // per epilogue warp: two 4 KB staging buffers
+constexpr int TC_SMEM_MAX = 232448;   // 227 KB opt-in dynamic smem per block
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_MN_CHUNK_BYTES = TC_BK * 128;  // one 64-wide MN box of BK rows
 
@@ -38,6 +39,7 @@ struct TcEpi {
   int tma_c;  // C written through smem + TMA bulk tensor store
   int tma_u;  // GELU/RELU pre-activation (aux_out) through smem + TMA as well
   int tma_a;  // residual / activation-derivative input (aux) read through TMA boxes
+  int cw64;   // plain bf16 C in 64-column chunks (128 B rows, SW128 boxes)
   void* C;
   int64_t ldc;
   const float* bias;
@@ -48,11 +50,16 @@ struct TcEpi {
   int M, N, flags, out_f32;
 };
 
-template <int BN>
+// CG = 1: one CTA owns a 128 x BN tile.  CG = 2: a cluster pair owns a
+// 256 x BN tile through cta_group::2 MMAs -- each CTA stages its own 128 rows
+// of A and half (BN/2 rows) of B, so per-SM operand traffic drops by a third.
+template <int BN, int CG>
 struct TcCfg {
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int B_ROWS = BN / CG;
+  static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
   static constexpr int STAGE_BYTES = TC_A_BYTES + B_BYTES;
-  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES =
+      (TC_SMEM_MAX - TC_EPI_WARPS * TC_STAGE_BYTES - 1024 - 256) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + TC_EPI_WARPS * TC_STAGE_BYTES +
                                1024 /*align*/ + 256 /*barriers*/;
   // two accumulators of BN fp32 columns, rounded up to a legal power-of-2 allocation
@@ -206,13 +213,27 @@ __device__ __forceinline__ void stage_bf16_row32(uint8_t* stg, int r, const floa
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// Epilogue warp hands a drained TMEM accumulator back to the (leader's) MMA warp.
+template <int CG>
+__device__ __forceinline__ void release_acc(uint64_t* bar, int lane) {
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) {
+    if constexpr (CG == 2)
+      mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+    else
+      mbar_arrive(bar);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmU,
                    const __grid_constant__ CUtensorMap tmX, int M, int N, int K, TcEpi ep) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
+  static_assert(!B_MN || Cfg::B_ROWS % 64 == 0, "MN-major B needs 64-wide chunks per CTA");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -226,8 +247,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* xbar = tempty + 2;  // one aux-tile barrier per epilogue warp
   uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + TC_EPI_WARPS);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_m = (M + TC_BM - 1) / TC_BM, num_n = (N + BN - 1) / BN;
+  // warp index through a shuffle so the compiler knows it is warp-uniform and
+  // keeps the MMA warp's descriptors in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = MMA leader of the pair
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;   // pair (cluster) index / count
+  const int num_m = (M + TC_BM * CG - 1) / (TC_BM * CG), num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_units = num_tiles * ep.ksplit;
   const int nk = (K + TC_BK - 1) / TC_BK;
@@ -241,14 +267,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], TC_EPI_WARPS);
+      mbar_init(&tempty[a], CG * TC_EPI_WARPS);  // every epilogue warp of the pair
     }
     for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&xbar[w], 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tslot, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      tmem_alloc_pair(tslot, Cfg::TMEM_COLS);
+    else
+      tmem_alloc(tslot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tslot;
 
@@ -256,29 +288,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      // the leader's full barrier counts both CTAs' bytes (one expect_tx)
+      auto load = [&](void* dst, const CUtensorMap* tm, int stg, int x, int y) {
+        if constexpr (CG == 2)
+          tma_load_2d_pair(dst, tm, mapa_shared(smem_u32(&full[stg]), 0), x, y);
+        else
+          tma_load_2d(dst, tm, &full[stg], x, y);
+      };
+      for (int u = cid; u < num_units; u += ncl) {
         const int t = u % num_tiles, sp = u / num_tiles;
-        const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * BN;
+        const int m0 = (t % num_m) * TC_BM * CG + static_cast<int>(rank) * TC_BM;
+        const int nb = (t / num_m) * BN + static_cast<int>(rank) * Cfg::B_ROWS;
         for (int kb = sp * nk / ep.ksplit; kb < (sp + 1) * nk / ep.ksplit; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          if (ep.flags & (1 << 17)) {  // profiling ablation: no operand traffic
+            if (rank == 0) mbar_arrive(&full[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          if (rank == 0) mbar_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
           uint8_t* a = sA + stage * TC_A_BYTES;
           uint8_t* b = sB + stage * Cfg::B_BYTES;
           const int k0 = kb * TC_BK;
           if (!A_MN) {
-            tma_load_2d(a, &tmA, &full[stage], k0, m0);
+            load(a, &tmA, stage, k0, m0);
           } else {
 #pragma unroll
             for (int j = 0; j < TC_BM / 64; ++j)
-              tma_load_2d(a + j * TC_MN_CHUNK_BYTES, &tmA, &full[stage], m0 + 64 * j, k0);
+              load(a + j * TC_MN_CHUNK_BYTES, &tmA, stage, m0 + 64 * j, k0);
           }
           if (!B_MN) {
-            tma_load_2d(b, &tmB, &full[stage], k0, n0);
+            load(b, &tmB, stage, k0, nb);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(b + j * TC_MN_CHUNK_BYTES, &tmB, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
+              load(b + j * TC_MN_CHUNK_BYTES, &tmB, stage, nb + 64 * j, k0);
           }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if constexpr (CG == 2) {
+        // drain: every MMA commit multicast into this CTA's ring has landed
+        for (int i = 0; i < STAGES; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -287,11 +345,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    // MMA issuer: the whole warp walks the ring (warp-uniform control flow), one
+    // elected lane issues.  Descriptors are built once; a k-step or a stage is
+    // a plain add on the 14-bit start-address field (smem offsets < 256 KB).
+    if (rank == 0) {
+      constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM * CG, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      constexpr uint64_t A_KSTEP = A_MN ? (2048 >> 4) : (32 >> 4);
+      constexpr uint64_t B_KSTEP = B_MN ? (2048 >> 4) : (32 >> 4);
+      const uint64_t a_desc0 = A_MN ? umma_sdesc_sw128(smem_u32(sA), TC_MN_CHUNK_BYTES, 1024)
+                                    : umma_sdesc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = B_MN ? umma_sdesc_sw128(smem_u32(sB), TC_MN_CHUNK_BYTES, 1024)
+                                    : umma_sdesc_sw128(smem_u32(sB), 16, 1024);
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = cid; u < num_units; u += ncl) {
         const int sp = u / num_tiles;
         const int kb0 = sp * nk / ep.ksplit, kb1 = (sp + 1) * nk / ep.ksplit;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -300,25 +367,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * TC_A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (TC_A_BYTES >> 4));
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (Cfg::B_BYTES >> 4));
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) {
-            const uint64_t ad = A_MN ? umma_sdesc_sw128(a_addr + k * 2048, TC_MN_CHUNK_BYTES, 1024)
-                                     : umma_sdesc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? umma_sdesc_sw128(b_addr + k * 2048, TC_MN_CHUNK_BYTES, 1024)
-                                     : umma_sdesc_sw128(b_addr + k * 32, 16, 1024);
-            tc_mma_f16(d, ad, bd, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < TC_BK / 16; ++k) {
+              const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+              if constexpr (CG == 2)
+                tc_mma_f16_pair(d, ad + k * A_KSTEP, bd + k * B_KSTEP, IDESC, accum);
+              else
+                tc_mma_f16(d, ad + k * A_KSTEP, bd + k * B_KSTEP, IDESC, accum);
+            }
+            if constexpr (CG == 2)
+              tc_commit_pair(&empty[stage]);
+            else
+              tc_commit(&empty[stage]);
           }
-          tc_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if (elect_one()) {
+          if constexpr (CG == 2)
+            tc_commit_pair(&tfull[acc]);
+          else
+            tc_commit(&tfull[acc]);
+        }
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
+      }
+      if constexpr (CG == 2) {
+        // both CTAs' epilogues have released both accumulators
+        for (int i = 0; i < 2; ++i) {
+          mbar_wait(&tempty[acc], aphase ^ 1);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {
@@ -327,41 +414,98 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int q = warp & 3;
     const int half = (warp - 4) >> 2;
     constexpr int HALF = BN / 2;
-    uint8_t* stg = sEpi + (warp - 4) * TC_STAGE_BYTES;
+    // per-warp ring of two 4 KB staging buffers: the TMA store of chunk i
+    // drains while chunk i+1 is staged; a buffer is rewritten only after the
+    // store two chunks back has finished reading it.
+    uint8_t* stg0 = sEpi + (warp - 4) * TC_STAGE_BYTES;
     const bool f32 = ep.out_f32 != 0;
     const bool tma = ep.tma_c != 0;
     const bool tma_x = ep.tma_a != 0;
-    uint8_t* xstg = stg + 2048;              // aux box (bf16 32x32, 64B swizzle)
+    const bool stage_u = ep.tma_u != 0;
+    // plain bf16 C: 64-column chunks staged as full 128 B rows (SW128 boxes),
+    // dealt round-robin to the two warp groups; otherwise 32-column chunks of
+    // each group's half of the tile
+    const bool wide = ep.cw64 != 0;
+    const int cstart = wide ? half * 64 : half * HALF;
+    const int cstep = wide ? 128 : 32;
+    const int cstop = wide ? BN : half * HALF + HALF;
     uint64_t* xb = &xbar[warp - 4];
     uint32_t xphase = 0;
+    uint32_t nchunk = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = cid; u < num_units; u += ncl) {
       const int t = u % num_tiles;
-      const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * BN;
+      const int m0 = (t % num_m) * TC_BM * CG + static_cast<int>(rank) * TC_BM;
+      const int n0 = (t / num_m) * BN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
+      const int cend = (ep.flags & (1 << 16)) ? cstart : cstop;  // profiling ablation: no epilogue work
       const uint32_t tb =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
-      if (tma_x && lane == 0) {  // prefetch the first aux box of this tile
+      // the accumulator goes back to the MMA warp as soon as it is in registers
+      uint64_t* rel = &tempty[acc];
+      if (tma_x && lane == 0 && cend > cstart) {  // prefetch the first aux box of this tile
         mbar_expect_tx(xb, 2048);
-        tma_load_2d(xstg, &tmX, xb, n0 + half * HALF, m0 + q * 32);
+        tma_load_2d(stg0 + (nchunk & 1) * 4096 + 2048, &tmX, xb, n0 + cstart, m0 + q * 32);
       }
 #pragma unroll 1
-      for (int c = 0; c < HALF; c += 32) {
-        const int cc = half * HALF + c;
+      for (int cc = cstart; cc < cend; cc += cstep) {
+        const uint32_t my = nchunk++;
+        uint8_t* stg = stg0 + (my & 1) * 4096;
+        const bool last = cc + cstep >= cend;
+        if (wide) {
+          uint32_t r[64];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) tmem_ld16(tb + cc + 16 * h, r + 16 * h);
+          tc_wait_ld();
+          if (last) release_acc<CG>(rel, lane);
+          float* v = reinterpret_cast<float*>(r);
+          if (ep.flags & PC_EPI_BIAS) {  // the only epilogue on this path
+            const float* bp = ep.bias + n0 + cc;
+            if (n0 + cc + 64 <= N) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float4 b4 = reinterpret_cast<const float4*>(bp)[i];
+                v[4 * i] += b4.x; v[4 * i + 1] += b4.y; v[4 * i + 2] += b4.z; v[4 * i + 3] += b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) v[i] += n0 + cc + i < N ? bp[i] : 0.f;
+            }
+          }
+          if (lane == 0) bulk_wait_read1();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4 w;
+            __nv_bfloat162* hw = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              hw[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+            *stage_chunk(stg, lane, j) = w;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+            bulk_commit();
+          }
+          continue;
+        }
         uint32_t r[32];
         tmem_ld16(tb + cc, r);
         tmem_ld16(tb + cc + 16, r + 16);
         float xa[32];
         if (tma_x) {
+          uint8_t* xstg = stg + 2048;  // aux box (bf16 32x32, 64B swizzle)
           mbar_wait(xb, xphase);
           xphase ^= 1;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const uint4 u = *stage_chunk64(xstg, lane, j);
-            const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&u);
+            const uint4 w = *stage_chunk64(xstg, lane, j);
+            const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float2 f2 = __bfloat1622float2(hx[k]);
@@ -370,15 +514,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
           __syncwarp();
-          if (lane == 0 && c + 32 < HALF) {  // prefetch the next chunk's box
+          if (lane == 0 && !last) {  // prefetch the next chunk's box into the other buffer
             mbar_expect_tx(xb, 2048);
-            tma_load_2d(xstg, &tmX, xb, n0 + cc + 32, m0 + q * 32);
+            tma_load_2d(stg0 + ((my + 1) & 1) * 4096 + 2048, &tmX, xb, n0 + cc + 32, m0 + q * 32);
           }
         }
         tc_wait_ld();
+        if (last) release_acc<CG>(rel, lane);
         float* v = reinterpret_cast<float*>(r);
         float pre[32];
-        const bool stage_u = ep.tma_u != 0;
         if (row < M) {
           if (n0 + cc < N)
             epilogue16(ep, row, n0 + cc, v, !tma, stage_u ? pre : nullptr, tma_x ? xa : nullptr);
@@ -387,7 +531,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                        tma_x ? xa + 16 : nullptr);
         }
         if (!tma) continue;
-        if (lane == 0) bulk_wait_read0();   // previous chunk's stores have read the stage
+        if (lane == 0) bulk_wait_read1();  // the store two chunks back has read this buffer
         __syncwarp();
         if (f32) {
           // 32 fp32 = one 128 B row per thread, 128B-swizzled box {32 cols, 32 rows}
@@ -396,7 +540,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             *stage_chunk(stg, lane, j) = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
         } else {
           // 32 bf16 = one 64 B row per thread, 64B-swizzled box {32 cols, 32 rows};
-          // the pre-activation goes to the second half of the stage
+          // the pre-activation goes to the second half of the buffer
           stage_bf16_row32(stg, lane, v);
           if (stage_u) stage_bf16_row32(stg + 2048, lane, pre);
         }
@@ -411,9 +555,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           bulk_commit();
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (cend <= cstart) release_acc<CG>(rel, lane);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
@@ -422,8 +564,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -468,7 +616,8 @@ int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int
 // Store-side tensor map for C (or the pre-activation): [M, N] row-major, boxes
 // of 32 columns x 32 rows: fp32 -> 128 B rows, 128B swizzle; bf16 -> 64 B rows,
 // 64B swizzle -- matching the epilogue staging tiles.
-int make_tmap_c(CUtensorMap* m, void* ptr, int64_t N, int64_t M, int64_t ldc, bool f32) {
+int make_tmap_c(CUtensorMap* m, void* ptr, int64_t N, int64_t M, int64_t ldc, bool f32,
+                bool wide = false) {
   auto enc = tmap_encoder();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -477,11 +626,12 @@ int make_tmap_c(CUtensorMap* m, void* ptr, int64_t N, int64_t M, int64_t ldc, bo
   const int es = f32 ? 4 : 2;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc * es)};
-  cuuint32_t box[2] = {32u, 32u};
+  // wide: bf16 boxes of 64 columns (128 B rows, 128B swizzle)
+  cuuint32_t box[2] = {wide ? 64u : 32u, 32u};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   (f32 || wide) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled (C) failed (%d)", static_cast<int>(r));
@@ -492,32 +642,77 @@ int make_tmap_c(CUtensorMap* m, void* ptr, int64_t N, int64_t M, int64_t ldc, bo
 
 int g_force_bn = 0;
 int g_tma_store = 1;
+int g_cta_pair = 0;  // 0 auto, 1 never, 2 always (where the tile allows it)
+int g_ablate = 0;    // profiling: bit0 skip epilogue work, bit1 skip operand loads
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
               const CUtensorMap& tu, const CUtensorMap& tx, int M, int N, int K, const TcEpi& ep,
               cudaStream_t st) {
-  using Cfg = TcCfg<BN>;
-  static bool attr_set = false;  // benign race: idempotent attribute write
-  if (!attr_set) {
-    PP_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    attr_set = true;
+  using Cfg = TcCfg<BN, CG>;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG>;
+  static int max_units = 0;  // benign race: idempotent attribute write / query
+  if (!max_units) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    int mu = num_sms();
+    if (CG == 2) {
+      PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t q{};
+      cudaLaunchAttribute qa[1];
+      q.gridDim = dim3(2 * (num_sms() / 2));
+      q.blockDim = dim3(TC_THREADS);
+      q.dynamicSmemBytes = Cfg::SMEM;
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 2;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int nc = 0;
+      PP_CUDA_TRY(cudaOccupancyMaxActiveClusters(&nc, kern, &q));
+      mu = nc > 0 ? nc : num_sms() / 2;  // co-resident pairs
+    }
+    max_units = mu;
   }
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN) * ep.ksplit;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_gemm_kernel<BN, A_MN, B_MN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, tx, M, N, K, ep);
+  const int units = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN) * ep.ksplit;
+  const int groups = units < max_units ? units : max_units;
+  if constexpr (CG == 1) {
+    kern<<<groups, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, tx, M, N, K, ep);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(2 * groups);
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tu, tx, M, N, K, ep));
+  }
   return check_launch("tc_gemm_kernel");
 }
 
-template <int BN>
+template <int BN, int CG>
 int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
                     const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, int M,
                     int N, int K, const TcEpi& ep, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-  if (a_mn && !b_mn) return launch_tc<BN, true, false>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-  return launch_tc<BN, true, true>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  if constexpr ((BN / CG) % 64 != 0) {  // MN-major B needs 64-wide chunks per CTA
+    if (b_mn) {
+      set_error("gemm: tile %d x cta_group %d needs a K-major B", BN, CG);
+      return PC_ERR_ARG;
+    }
+    if (!a_mn) return launch_tc<BN, false, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+    return launch_tc<BN, true, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  } else {
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  if (!a_mn && b_mn) return launch_tc<BN, false, true, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  if (a_mn && !b_mn) return launch_tc<BN, true, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  return launch_tc<BN, true, true, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  }
 }
 
 }  // namespace
@@ -530,27 +725,38 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
                  int64_t ldaux_out, cudaStream_t st) {
   PP_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem");
   PP_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
-  int bn = g_force_bn;
-  if (bn == 0) {
-    // Pick the tile width maximising (wave efficiency x per-tile efficiency):
-    // tiles / (waves * SMs) penalises a last partial wave (e.g. 192 tiles on
-    // 148 SMs), the per-tile factor reflects measured mainloop efficiency.
-    const int sms = num_sms();
-    const int64_t mt = (M + TC_BM - 1) / TC_BM;
-    const int cands[4] = {256, 192, 128, 64};
-    const double tile_eff[4] = {1.0, 0.95, 0.8, 0.45};
-    double best = -1.0;
-    for (int i = 0; i < 4; ++i) {
-      const int c = cands[i];
-      if (c > 64 && N < c / 2) continue;
-      const int64_t tiles = mt * ((N + c - 1) / c);
-      const int64_t waves = (tiles + sms - 1) / sms;
-      const double score = static_cast<double>(tiles) / (waves * sms) * tile_eff[i];
-      if (score > best + 1e-9) {
-        best = score;
-        bn = c;
-      }
+  // Pick (tile width, CTA pair) maximising wave efficiency x per-tile
+  // efficiency: useful area / (waves x slots x tile area) penalises a last
+  // partial wave (e.g. 192 tiles on 148 SMs) and padding; the per-tile factor
+  // is the measured mainloop efficiency of that tile shape.
+  struct Cand { int bn, cg; double eff; };
+  const Cand cands[7] = {{256, 2, 1.0}, {192, 2, 0.97}, {256, 1, 0.88}, {192, 1, 0.85},
+                         {128, 2, 0.78}, {128, 1, 0.75}, {64, 1, 0.45}};
+  const bool b_kmajor = transB != 0;
+  const int sms = num_sms();
+  int bn = 0, cg = 1;
+  double best = -1.0;
+  for (const Cand& c : cands) {
+    if (g_force_bn && c.bn != g_force_bn) continue;
+    if (g_cta_pair == 1 && c.cg == 2) continue;
+    if (g_cta_pair == 2 && c.cg == 1 && c.bn != 64) continue;
+    if (c.cg == 2 && (c.bn / 2) % 64 != 0 && !b_kmajor) continue;
+    if (!g_force_bn && c.bn > 64 && N < c.bn / 2) continue;
+    if (!g_force_bn && c.cg == 2 && M <= TC_BM) continue;
+    const int64_t tm = TC_BM * c.cg;
+    const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
+    const int64_t slots = sms / c.cg;
+    const int64_t waves = (tiles + slots - 1) / slots;
+    const double score = static_cast<double>(M) * N / (static_cast<double>(waves) * slots * tm * c.bn) * c.eff;
+    if (score > best + 1e-9) {
+      best = score;
+      bn = c.bn;
+      cg = c.cg;
     }
+  }
+  if (bn == 0) {  // forced combination not realisable (e.g. pair 192 with MN-major B)
+    bn = g_force_bn ? g_force_bn : 128;
+    cg = 1;
   }
   // op(A) is [M,K]: transA=0 -> stored [M,K] (K-major); transA=1 -> stored [K,M] (MN-major).
   // op(B) is [K,N]: transB=0 -> stored [K,N] (MN-major); transB=1 -> stored [N,K] (K-major).
@@ -564,7 +770,7 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     rc = make_tmap(&ta, A, M, K, lda, TC_BK);
   if (rc) return rc;
   if (!b_mn)
-    rc = make_tmap(&tb, B, K, N, ldb, bn);
+    rc = make_tmap(&tb, B, K, N, ldb, bn / cg);
   else
     rc = make_tmap(&tb, B, N, K, ldb, TC_BK);
   if (rc) return rc;
@@ -588,29 +794,36 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     rc = make_tmap_c(&tx, const_cast<void*>(aux), N, M, ldaux, false);
     if (rc) return rc;
   }
+  // Deterministic split-K (exactly 2 halves onto a zero-filled fp32 C) when the
+  // caller allows it and the tile count leaves most SMs idle.
+  int ksplit = 1;
+  if ((epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c && K >= 2 * TC_BK * 8) {
+    const int64_t tiles = ((M + TC_BM * cg - 1) / (TC_BM * cg)) * ((N + bn - 1) / bn);
+    if (tiles * 2 <= num_sms() / cg) ksplit = 2;
+  }
+  const bool cw64 = tma_c && !out_f32 && ksplit == 1 &&
+                    (epi & ~PC_EPI_BIAS) == 0 &&
+                    (!(epi & PC_EPI_BIAS) || (reinterpret_cast<uintptr_t>(bias) & 15) == 0);
   if (tma_c) {
-    rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0);
+    rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0, cw64);
     if (rc) return rc;
   }
   if (tma_u) {
     rc = make_tmap_c(&tu, aux_out, N, M, ldaux_out, false);
     if (rc) return rc;
   }
-  // Deterministic split-K (exactly 2 halves onto a zero-filled fp32 C) when the
-  // caller allows it and the tile count leaves most SMs idle.
-  int ksplit = 1;
-  if ((epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c && K >= 2 * TC_BK * 8) {
-    const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
-    if (tiles * 2 <= num_sms()) ksplit = 2;
-  }
-  TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, tma_a ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
-           aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi, out_f32};
-  switch (bn) {
-    case 256: return dispatch_majors<256>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
-    case 192: return dispatch_majors<192>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
-    case 128: return dispatch_majors<128>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
-    case 64: return dispatch_majors<64>(a_mn, b_mn, ta, tb, tc, tu, tx, (int)M, (int)N, (int)K, ep, st);
-    default: set_error("gemm: bad tile width %d", bn); return PC_ERR_ARG;
+  TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, tma_a ? 1 : 0, cw64 ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
+           aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi | (g_ablate << 16), out_f32};
+  const int iM = static_cast<int>(M), iN = static_cast<int>(N), iK = static_cast<int>(K);
+  switch (bn * 4 + cg) {
+    case 256 * 4 + 2: return dispatch_majors<256, 2>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 192 * 4 + 2: return dispatch_majors<192, 2>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 128 * 4 + 2: return dispatch_majors<128, 2>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 256 * 4 + 1: return dispatch_majors<256, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 192 * 4 + 1: return dispatch_majors<192, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 128 * 4 + 1: return dispatch_majors<128, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 64 * 4 + 1: return dispatch_majors<64, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    default: set_error("gemm: bad tile %d x cta_group %d", bn, cg); return PC_ERR_ARG;
   }
 }
 
@@ -622,6 +835,22 @@ extern "C" int pc_gemm_set_tile_n(int bn) {
     return PC_ERR_ARG;
   }
   pp200::g_force_bn = bn;
+  return PC_OK;
+}
+
+extern "C" int pc_gemm_set_cta_pair(int mode) {
+  if (mode < 0 || mode > 2) {
+    pp200::set_error("cta pair mode must be 0 (auto), 1 (never) or 2 (always)");
+    return PC_ERR_ARG;
+  }
+  pp200::g_cta_pair = mode;
+  return PC_OK;
+}
+
+// Profiling ablation (results are garbage while set): bit0 = skip the epilogue
+// work, bit1 = skip the operand TMA loads.
+extern "C" int pc_gemm_set_ablation(int bits) {
+  pp200::g_ablate = bits & 3;
   return PC_OK;
 }
 

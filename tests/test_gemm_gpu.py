@@ -50,21 +50,36 @@ def make_operands(M, N, K, ta, tb, dtype, seed=0):
     return A, B, opA @ opB
 
 
+class forced:
+    """Pin the GEMM tile width / CTA-pair mode / store path for one block."""
+
+    def __init__(self, bn=0, pair=0, tma=1):
+        self.v = (bn, pair, tma)
+
+    def __enter__(self):
+        bn, pair, tma = self.v
+        _lib.call("pc_gemm_set_tile_n", bn)
+        _lib.call("pc_gemm_set_cta_pair", pair)
+        _lib.call("pc_gemm_set_tma_store", tma)
+
+    def __exit__(self, *a):
+        _lib.call("pc_gemm_set_tile_n", 0)
+        _lib.call("pc_gemm_set_cta_pair", 0)
+        _lib.call("pc_gemm_set_tma_store", 1)
+
+
 @pytest.mark.parametrize("tma", [1, 0])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("bn", [64, 128, 192, 256])
-@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (200, 136, 72), (1024, 768, 768)])
-def test_bf16_tcgen05_majors(ta, tb, bn, shape, tma):
+@pytest.mark.parametrize("bn,pair", [(64, 1), (128, 1), (192, 1), (256, 1), (128, 2), (192, 2),
+                                     (256, 2)])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (200, 136, 72), (1024, 768, 768),
+                                   (392, 200, 136)])
+def test_bf16_tcgen05_majors(ta, tb, bn, pair, shape, tma):
     M, N, K = shape
     A, B, ref = make_operands(M, N, K, ta, tb, torch.bfloat16)
-    _lib.call("pc_gemm_set_tile_n", bn)
-    _lib.call("pc_gemm_set_tma_store", tma)
-    try:
+    with forced(bn, pair, tma):
         C32 = run_gemm(A, B, ta, tb, M, N, K, torch.float32)
         C16 = run_gemm(A, B, ta, tb, M, N, K, torch.bfloat16)
-    finally:
-        _lib.call("pc_gemm_set_tile_n", 0)
-        _lib.call("pc_gemm_set_tma_store", 1)
     torch.cuda.synchronize()
     assert rel(C32, ref) < 1e-5
     assert rel(C16, ref) < 1e-2
@@ -88,9 +103,15 @@ def test_simt_gemm(dtype, tol, ta, tb):
     assert rel(C, ref) < tol
 
 
+@pytest.mark.parametrize("pair", [0, 2])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-def test_epilogues(dtype):
-    M, N, K = 256, 192, 128
+def test_epilogues(dtype, pair):
+    with forced(0, pair):
+        _epilogues(dtype)
+
+
+def _epilogues(dtype):
+    M, N, K = 512, 192, 128
     A, B, ref = make_operands(M, N, K, 0, 1, dtype, seed=2)
     out = torch.bfloat16 if dtype == torch.bfloat16 else torch.float32
     tol = 2e-2 if dtype == torch.bfloat16 else 1e-5
@@ -120,17 +141,19 @@ def test_epilogues(dtype):
     assert rel(acc, want) < (1e-5 if dtype != torch.bfloat16 else 1e-5)
 
 
+@pytest.mark.parametrize("pair", [1, 2])
 @pytest.mark.parametrize("shape", [(768, 768, 8192), (256, 192, 4096), (200, 72, 2000)])
-def test_splitk_zero_c_deterministic(shape):
+def test_splitk_zero_c_deterministic(shape, pair):
     """The split-K hint (two K halves reduce-added onto a zero C) is exact to the
     reference and bitwise reproducible run to run."""
     M, N, K = shape
     A, B, ref = make_operands(M, N, K, 1, 0, torch.bfloat16, seed=5)
     outs = []
-    for _ in range(3):
-        C = torch.zeros(M, N, device="cuda", dtype=torch.float32)
-        run_gemm(A, B, 1, 0, M, N, K, torch.float32, epi=_lib.EPI_SPLITK_ZERO_C, C=C)
-        outs.append(C)
+    with forced(0, pair):
+        for _ in range(3):
+            C = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+            run_gemm(A, B, 1, 0, M, N, K, torch.float32, epi=_lib.EPI_SPLITK_ZERO_C, C=C)
+            outs.append(C)
     torch.cuda.synchronize()
     assert rel(outs[0], ref) < 1e-5
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
