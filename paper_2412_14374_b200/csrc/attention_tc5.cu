@@ -5,17 +5,19 @@
 //
 // One CTA = 128 query rows of one (batch, head); 8 warps:
 //   warp 0      TMA producer: Q tile once, then K/V tiles of 64 keys into a
-//               3-deep 128B-swizzled smem ring
-//   warp 1      single-thread tcgen05.mma issuer:
-//                 S = Q K^T   (M=128, N=64 keys, K=64)  -> TMEM cols [0, 64)
-//                 O += P V    (M=128, N=64 dims, K=64)  -> TMEM cols [64, 128)
-//   warp 2      TMEM allocator (128 columns: 2 CTAs fit per SM)
+//               128B-swizzled smem ring
+//   warp 1      single-thread tcgen05.mma issuer, one key block ahead:
+//                 S_j = Q K_j^T  (M=128, N=64 keys, K=64) -> TMEM S[j % 2]
+//                 O  += P_j V_j  (M=128, N=64 dims, K=64) -> TMEM O
+//               S_{j+1} is issued before PV_j, so the tensor core computes
+//               the next scores while the softmax warps work on block j.
+//   warp 2      TMEM allocator (256 columns: S0, S1, O; 2 CTAs fit per SM)
 //   warps 4..7  softmax: one thread owns one query row (TMEM lane), so row
-//               max / sum need no shuffles; P is written as bf16 into a
-//               128B-swizzled K-major smem tile (the MMA's A operand), O is
-//               rescaled in TMEM when the running max moves.
-// Ordering: the commit after S_{j+1} also covers PV_j, so when the softmax
-// warps see S_{j+1} ready they may overwrite P and rescale O.
+//               max / sum need no shuffles; P_j is written as bf16 into the
+//               128B-swizzled K-major smem tile P[j % 2] (the MMA's A operand);
+//               O is rescaled in TMEM when the running max moves.
+// Barriers: s_full[i] (S_j landed), p_full[i] (P_j staged), pv_done[i]
+// (PV_j retired: P[i] reusable, O up to date).
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -27,11 +29,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn();
 namespace {
 
 using bf16 = __nv_bfloat16;
-constexpr int F_BM = 128, F_BN = 64, F_HD = 64, F_STAGES = 2, F_THREADS = 256;
+constexpr int F_BM = 128, F_BN = 64, F_HD = 64, F_STAGES = 3, F_THREADS = 256;
 constexpr int F_Q_BYTES = F_BM * F_HD * 2;    // 16 KB
 constexpr int F_KV_BYTES = F_BN * F_HD * 2;   // 8 KB
 constexpr int F_P_BYTES = F_BM * F_BN * 2;    // 16 KB
-constexpr int F_SMEM = F_Q_BYTES + 2 * F_STAGES * F_KV_BYTES + F_P_BYTES + 1024 + 256;
+constexpr int F_SMEM = F_Q_BYTES + 2 * F_STAGES * F_KV_BYTES + 2 * F_P_BYTES + 1024 + 256;
 constexpr float F_LN2 = 0.6931471805599453f;
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
@@ -44,6 +46,25 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 }
 __device__ __forceinline__ void tc_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// Paired fp32 arithmetic (FFMA2 / FADD2 on sm_100a) on two floats in a b64.
+__device__ __forceinline__ uint64_t pack_f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack_f2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
 }
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -61,12 +82,13 @@ __global__ void __launch_bounds__(F_THREADS, 2)
   uint8_t* sK = sQ + F_Q_BYTES;
   uint8_t* sV = sK + F_STAGES * F_KV_BYTES;
   uint8_t* sP = sV + F_STAGES * F_KV_BYTES;
-  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sP + F_P_BYTES);
+  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sP + 2 * F_P_BYTES);
   uint64_t* kv_full = bar_q + 1;
   uint64_t* kv_empty = kv_full + F_STAGES;
-  uint64_t* s_full = kv_empty + F_STAGES;
-  uint64_t* p_full = s_full + 1;
-  uint64_t* o_done = p_full + 1;
+  uint64_t* s_full = kv_empty + F_STAGES;  // [2]
+  uint64_t* p_full = s_full + 2;           // [2]
+  uint64_t* pv_done = p_full + 2;          // [2]
+  uint64_t* o_done = pv_done + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -85,17 +107,20 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+    }
     mbar_init(o_done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tslot, 128);
+  if (warp == 2) tmem_alloc(tslot, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tO = tmem + 64;
+  const uint32_t tS = tmem, tO = tmem + 128;  // S[i] at tS + 64 i
 
   if (warp == 0) {
     if (lane == 0) {
@@ -117,25 +142,33 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       constexpr uint32_t ID_O = umma_idesc_bf16(F_BM, F_HD, 0, 1);  // P K-major, V MN-major
       mbar_wait(bar_q, 0);
       tc_fence_after();
-      const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
-      for (int j = 0; j < nkb; ++j) {
+      const uint32_t q_addr = smem_u32(sQ);
+      auto issue_s = [&](int j) {  // S_j = Q K_j^T into S[j % 2]
         const int s = j % F_STAGES;
         mbar_wait(&kv_full[s], (j / F_STAGES) & 1);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + s * F_KV_BYTES);
-        const uint32_t v_addr = smem_u32(sV + s * F_KV_BYTES);
 #pragma unroll
         for (int k = 0; k < F_HD / 16; ++k)
-          tc_mma_f16(tS, umma_sdesc_sw128(q_addr + k * 32, 16, 1024),
+          tc_mma_f16(tS + (j & 1) * 64, umma_sdesc_sw128(q_addr + k * 32, 16, 1024),
                      umma_sdesc_sw128(k_addr + k * 32, 16, 1024), ID_S, k > 0 ? 1u : 0u);
-        tc_commit(s_full);
-        mbar_wait(p_full, j & 1);
+        tc_commit(&s_full[j & 1]);
+      };
+      issue_s(0);
+      for (int j = 0; j < nkb; ++j) {
+        // S[(j+1) % 2] was last read by softmax j-1, which finished before PV_{j-1}
+        if (j + 1 < nkb) issue_s(j + 1);
+        const int s = j % F_STAGES;
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
+        const uint32_t p_addr = smem_u32(sP + (j & 1) * F_P_BYTES);
+        const uint32_t v_addr = smem_u32(sV + s * F_KV_BYTES);
 #pragma unroll
         for (int k = 0; k < F_BN / 16; ++k)
           tc_mma_f16(tO, umma_sdesc_sw128(p_addr + k * 32, 16, 1024),
                      umma_sdesc_sw128(v_addr + k * 2048, 8192, 1024), ID_O,
                      (j > 0 || k > 0) ? 1u : 0u);
+        tc_commit(&pv_done[j & 1]);
         tc_commit(&kv_empty[s]);
       }
       tc_commit(o_done);
@@ -147,23 +180,29 @@ __global__ void __launch_bounds__(F_THREADS, 2)
     const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nkb; ++j) {
-      mbar_wait(s_full, j & 1);
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       uint32_t sr[64];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16(tS + lane_off + c * 16, sr + c * 16);
+      for (int c = 0; c < 4; ++c) tmem_ld16(tS + (j & 1) * 64 + lane_off + c * 16, sr + c * 16);
       tc_wait_ld();
       float* sv = reinterpret_cast<float*>(sr);
       const int n0 = j * F_BN;
       const bool edge = n0 + F_BN - 1 > q0 || n0 + F_BN > S;  // diagonal or ragged block
-      float mx = -INFINITY;
+      // max of the raw scores (the positive scale commutes with max), 8
+      // independent chains; masked entries become -inf
+      float mx8[8];
 #pragma unroll
-      for (int i = 0; i < F_BN; ++i) {
-        float v = sv[i] * sl2;
-        if (edge && (n0 + i > row || n0 + i >= S)) v = -INFINITY;
-        sv[i] = v;
-        mx = fmaxf(mx, v);
+      for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+      if (edge) {
+#pragma unroll
+        for (int i = 0; i < F_BN; ++i)
+          if (n0 + i > row || n0 + i >= S) sv[i] = -INFINITY;
       }
+#pragma unroll
+      for (int i = 0; i < F_BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], sv[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
       // Lazy rescaling (FA4): keep the running reference max unless the row
       // max grows by more than 8 (log2 units, P <= 256 stays exact enough in
       // bf16); O and l only need a correction when the reference moves.
@@ -176,26 +215,41 @@ __global__ void __launch_bounds__(F_THREADS, 2)
         corr = ex2(m - mn);
         m = mn;
       }
-      float sum = 0.f;
+      // p = 2^(s * scale - m): one paired FMA per two scores, paired sums
+      const uint64_t sc2 = pack_f2(sl2, sl2), nm2 = pack_f2(-m, -m);
+      uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-      for (int i = 0; i < F_BN; ++i) {
-        const float p = ex2(sv[i] - m);
-        sv[i] = p;
-        sum += p;
+      for (int i = 0; i < F_BN; i += 2) {
+        float p0, p1;
+        unpack_f2(ffma2(pack_f2(sv[i], sv[i + 1]), sc2, nm2), p0, p1);
+        p0 = ex2(p0);
+        p1 = ex2(p1);
+        sv[i] = p0;
+        sv[i + 1] = p1;
+        acc2[(i >> 1) & 3] = fadd2(acc2[(i >> 1) & 3], pack_f2(p0, p1));
       }
+      float sa[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) unpack_f2(acc2[k], sa[2 * k], sa[2 * k + 1]);
+      const float sum = ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
       l = l * corr + sum;
+      // P[j % 2] was read by PV_{j-2}
+      if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
       // P row -> smem, K-major with 128B swizzle (8 chunks of 8 bf16)
+      uint8_t* sPj = sP + (j & 1) * F_P_BYTES;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint4 u;
         __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
         for (int k = 0; k < 4; ++k) hp[k] = __floats2bfloat162_rn(sv[8 * c + 2 * k], sv[8 * c + 2 * k + 1]);
-        *reinterpret_cast<uint4*>(sP + r * 128 + ((c ^ (r & 7)) << 4)) = u;
+        *reinterpret_cast<uint4*>(sPj + r * 128 + ((c ^ (r & 7)) << 4)) = u;
       }
       fence_proxy_async_smem();
-      // rescale O by corr (PV_{j-1} is complete: covered by the S_j commit)
+      // rescale O by corr once PV_{j-1} has retired
       if (j > 0 && __any_sync(0xffffffffu, corr != 1.f && l > 0.f)) {
+        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t orr[16];
@@ -209,7 +263,7 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
     mbar_wait(o_done, 0);
     tc_fence_after();
@@ -237,7 +291,7 @@ __global__ void __launch_bounds__(F_THREADS, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 128);
+  if (warp == 2) tmem_dealloc(tmem, 256);
 }
 
 

@@ -734,7 +734,13 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
                          {128, 2, 0.78}, {128, 1, 0.75}, {64, 1, 0.45}};
   const bool b_kmajor = transB != 0;
   const int sms = num_sms();
-  int bn = 0, cg = 1;
+  const int es = out_f32 ? 4 : 2;
+  const bool tma_c = g_tma_store && !(epi & PC_EPI_ACCUM) &&
+                     (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
+  // deterministic split-K: exactly 2 K halves reduce-added onto a zero-filled
+  // fp32 C (0 + a + b == 0 + b + a bitwise), only when the caller allows it
+  const bool can_split = (epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c && K >= 2 * TC_BK * 8;
+  int bn = 0, cg = 1, ksplit = 1;
   double best = -1.0;
   for (const Cand& c : cands) {
     if (g_force_bn && c.bn != g_force_bn) continue;
@@ -746,17 +752,23 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     const int64_t tm = TC_BM * c.cg;
     const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
     const int64_t slots = sms / c.cg;
-    const int64_t waves = (tiles + slots - 1) / slots;
-    const double score = static_cast<double>(M) * N / (static_cast<double>(waves) * slots * tm * c.bn) * c.eff;
-    if (score > best + 1e-9) {
-      best = score;
-      bn = c.bn;
-      cg = c.cg;
+    for (int ks = 1; ks <= (can_split ? 2 : 1); ++ks) {
+      const int64_t waves = (tiles * ks + slots - 1) / slots;
+      const double score = static_cast<double>(M) * N * ks /
+                           (static_cast<double>(waves) * slots * tm * c.bn) * c.eff *
+                           (ks > 1 ? 0.97 : 1.0);
+      if (score > best + 1e-9) {
+        best = score;
+        bn = c.bn;
+        cg = c.cg;
+        ksplit = ks;
+      }
     }
   }
   if (bn == 0) {  // forced combination not realisable (e.g. pair 192 with MN-major B)
     bn = g_force_bn ? g_force_bn : 128;
     cg = 1;
+    ksplit = 1;
   }
   // op(A) is [M,K]: transA=0 -> stored [M,K] (K-major); transA=1 -> stored [K,M] (MN-major).
   // op(B) is [K,N]: transB=0 -> stored [K,N] (MN-major); transB=1 -> stored [N,K] (K-major).
@@ -774,11 +786,8 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   else
     rc = make_tmap(&tb, B, N, K, ldb, TC_BK);
   if (rc) return rc;
-  // C (and a GELU/RELU pre-activation) through smem + TMA store when legal:
-  // 16 B aligned rows and no read-modify-write epilogue.
-  const int es = out_f32 ? 4 : 2;
-  const bool tma_c = g_tma_store && !(epi & PC_EPI_ACCUM) &&
-                     (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
+  // C (and a GELU/RELU pre-activation) goes through smem + TMA store when
+  // legal (tma_c above: 16 B aligned rows, no read-modify-write epilogue).
   const bool tma_u = tma_c && !out_f32 && (epi & (PC_EPI_GELU | PC_EPI_RELU)) &&
                      (reinterpret_cast<uintptr_t>(aux_out) & 15) == 0 && (ldaux_out * 2) % 16 == 0;
   // aux (residual / activation-derivative input) through TMA boxes in the free
@@ -793,13 +802,6 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   if (tma_a) {
     rc = make_tmap_c(&tx, const_cast<void*>(aux), N, M, ldaux, false);
     if (rc) return rc;
-  }
-  // Deterministic split-K (exactly 2 halves onto a zero-filled fp32 C) when the
-  // caller allows it and the tile count leaves most SMs idle.
-  int ksplit = 1;
-  if ((epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c && K >= 2 * TC_BK * 8) {
-    const int64_t tiles = ((M + TC_BM * cg - 1) / (TC_BM * cg)) * ((N + bn - 1) / bn);
-    if (tiles * 2 <= num_sms() / cg) ksplit = 2;
   }
   const bool cw64 = tma_c && !out_f32 && ksplit == 1 &&
                     (epi & ~PC_EPI_BIAS) == 0 &&

@@ -8,6 +8,10 @@ from paper_2412_14374_b200 import _lib
 
 SHAPES = [("fwd qkv", 8192, 2304, 768, 0, 1), ("fwd fc2", 8192, 768, 3072, 0, 1),
           ("sq 8192", 8192, 8192, 8192, 0, 1)]
+if len(sys.argv) > 1 and sys.argv[1] == "wgrad":  # MN-major operands vs a K-major control
+    SHAPES = [("wg fc2", 768, 3072, 8192, 1, 0), ("wg fc2 K", 768, 3072, 8192, 0, 1),
+              ("wg fc1", 3072, 768, 8192, 1, 0), ("wg fc1 K", 3072, 768, 8192, 0, 1),
+              ("wg fc1 AK", 3072, 768, 8192, 0, 0), ("wg fc1 BK", 3072, 768, 8192, 1, 1)]
 
 
 def bench(fn, iters=20):
@@ -30,7 +34,7 @@ for name, M, N, K, ta, tb in SHAPES:
     st = torch.cuda.current_stream().cuda_stream
     f = lambda: _lib.call("pc_gemm", 2, 2, ta, tb, M, N, K, A.data_ptr(), A.stride(0), B.data_ptr(),
                           B.stride(0), C.data_ptr(), C.stride(0), 0, None, None, 0, None, 0, st)
-    for bn, pair in ((256, 2), (192, 2), (256, 1), (192, 1), (128, 1)):
+    for bn, pair in ((256, 2), (128, 2), (256, 1), (128, 1)):
         _lib.call("pc_gemm_set_tile_n", bn)
         _lib.call("pc_gemm_set_cta_pair", pair)
         out = []
