@@ -189,11 +189,11 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
             continue
         A = torch.randn((K, Mm) if ta else (Mm, K), device="cuda").bfloat16()
         B = torch.randn((N, K) if tb else (K, N), device="cuda").bfloat16()
-        out_f32 = ta == 1
-        C = torch.empty(Mm, N, device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
+        out_f32 = ta == 1  # weight gradients: fp32 with the split-K hint, as device.py issues them
+        C = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
         args = (_lib.PC_BF16, _lib.PC_F32 if out_f32 else _lib.PC_BF16, ta, tb, Mm, N, K,
-                A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, 0, None,
-                None, 0, None, 0, st.cuda_stream)
+                A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N,
+                _lib.EPI_SPLITK_ZERO_C if out_f32 else 0, None, None, 0, None, 0, st.cuda_stream)
         for _ in range(3):
             _lib.call("pc_gemm", *args)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
