@@ -311,7 +311,8 @@ extern "C" int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const vo
   PP_CHECK_ARG(B > 0 && H > 0 && S > 0 && hd > 0 && hd <= 32 * 8, "attention: bad dims");
   PP_CHECK_ARG(dtype == PC_F32 || dtype == PC_BF16, "attention: f32/bf16 only");
   if (dtype == PC_BF16 && g_attn_impl == 0 && attention_tc5_supported(hd, ld_qkv, ld_o, qkv, dO) &&
-      (reinterpret_cast<uintptr_t>(dqkv) & 15) == 0 && (ld_dqkv * 2) % 16 == 0)
+      (reinterpret_cast<uintptr_t>(dqkv) & 15) == 0 && (ld_dqkv * 2) % 16 == 0 && S % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(lse) & 15) == 0 && (reinterpret_cast<uintptr_t>(delta) & 15) == 0)
     return attention_bwd_tc5(B, H, S, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv, st);
   if (dtype == PC_BF16 && g_attn_impl != 1 && attention_tc_supported(hd, ld_qkv, ld_o))
     return attention_bwd_tc(B, H, S, hd, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv, st);

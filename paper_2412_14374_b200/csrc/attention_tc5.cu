@@ -66,6 +66,11 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -296,36 +301,46 @@ __global__ void __launch_bounds__(F_THREADS, 2)
 
 
 // ------------------------------------------------------------------ backward
-// Writes 16 bf16 (two 16 B chunks, logical chunk index c2 and c2+1) of row r
-// into a 128B-swizzled [rows x 64] K-major tile.
-__device__ __forceinline__ void st_row16(uint8_t* tile, int r, int c2, const float* v) {
+constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 3, BKV_THREADS = 384, BKV_EW = 8;
+constexpr int BKV_SMEM = 2 * 16384 /*K,V*/ + BKV_STAGES * 2 * 8192 /*Q,dO*/ +
+                         2 * 2 * 16384 /*P^T,dS^T x2*/ + BKV_STAGES * 512 /*lse,delta*/ + 1024 + 256;
+
+// 32 bf16 (four 16 B chunks starting at logical chunk c4) of row r of a
+// 128B-swizzled [rows x 64] K-major tile.
+__device__ __forceinline__ void st_row32(uint8_t* tile, int r, int c4, const float* v) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < 4; ++h) {
     uint4 u;
     __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
     for (int k = 0; k < 4; ++k) hp[k] = __floats2bfloat162_rn(v[8 * h + 2 * k], v[8 * h + 2 * k + 1]);
-    *reinterpret_cast<uint4*>(tile + r * 128 + (((c2 + h) ^ (r & 7)) << 4)) = u;
+    *reinterpret_cast<uint4*>(tile + r * 128 + (((c4 + h) ^ (r & 7)) << 4)) = u;
   }
 }
 
-__device__ __forceinline__ void store_row64(bf16* dst, const uint32_t* acc, float scale) {
-  uint4 u[8];
+__device__ __forceinline__ void store_row32(bf16* dst, const uint32_t* acc, float scale) {
+  uint4 u[4];
   __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(u);
 #pragma unroll
-  for (int k = 0; k < 32; ++k)
+  for (int k = 0; k < 16; ++k)
     hp[k] = __floats2bfloat162_rn(__uint_as_float(acc[2 * k]) * scale, __uint_as_float(acc[2 * k + 1]) * scale);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) reinterpret_cast<uint4*>(dst)[k] = u[k];
+  for (int k = 0; k < 4; ++k) reinterpret_cast<uint4*>(dst)[k] = u[k];
 }
 
-constexpr int B_KEYS = 128, B_Q = 64;  // dK/dV: 128 keys per CTA, 64-query blocks
-constexpr int BKV_SMEM = 2 * 16384 /*K,V*/ + 2 * 2 * 8192 /*Q,dO stages*/ + 2 * 16384 /*P^T,dS^T*/ + 1024 + 256;
-
-// dK, dV for 128 keys of one (batch, head): S^T = K Q^T and dP^T = V dO^T per
-// 64-query block (TMEM), P^T / dS^T built by one thread per key row, then
-// dV += P^T dO and dK += dS^T Q (TMEM accumulators).
-__global__ void __launch_bounds__(F_THREADS, 2)
+// dK, dV for 128 keys of one (batch, head), one CTA per SM, 12 warps:
+//   warp 0      TMA producer: K, V once; per 64-query block Q, dO (tensor
+//               maps) and its lse / delta rows (bulk copies) into a 3-deep ring
+//   warp 1      MMA issuer, one query block ahead of the elementwise warps:
+//                 S^T_i = K Q_i^T, dP^T_i = V dO_i^T  -> TMEM buffer i % 2
+//                 dV += P^T_i dO_i, dK += dS^T_i Q_i  -> TMEM accumulators
+//   warp 2      TMEM allocator (512 columns: S^T/dP^T x2, dV, dK)
+//   warps 4..11 elementwise: two warps per TMEM lane quarter (one key row per
+//               thread, 32 of the 64 queries each) build P^T = exp2(S^T*c - lse)
+//               and dS^T = P^T (dP^T - delta) into 128B-swizzled smem tiles
+// Barriers: s_full / s_free (scores landed / read out of TMEM), p_full (P^T,
+// dS^T staged), pv_done (dV/dK MMAs of block i retired: tiles reusable).
+__global__ void __launch_bounds__(BKV_THREADS, 1)
     fa_bwd_dkdv_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                     const float* __restrict__ lse, const float* __restrict__ delta,
                     bf16* __restrict__ dqkv, int64_t ldd, int H, int S, float sl2, float scale) {
@@ -334,45 +349,55 @@ __global__ void __launch_bounds__(F_THREADS, 2)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + 16384;
-  uint8_t* sQ = sV + 16384;      // [2][64 x 64]
-  uint8_t* sG = sQ + 2 * 8192;   // dO, [2][64 x 64]
-  uint8_t* sPt = sG + 2 * 8192;  // P^T  [128 keys x 64 q]
-  uint8_t* sDt = sPt + 16384;    // dS^T [128 keys x 64 q]
-  uint64_t* bar_kv = reinterpret_cast<uint64_t*>(sDt + 16384);
+  uint8_t* sQ = sV + 16384;                // [ST][64 x 64]
+  uint8_t* sG = sQ + BKV_STAGES * 8192;    // dO [ST][64 x 64]
+  uint8_t* sPt = sG + BKV_STAGES * 8192;   // P^T  [2][128 keys x 64 q]
+  uint8_t* sDt = sPt + 2 * 16384;          // dS^T [2][128 keys x 64 q]
+  float* sLD = reinterpret_cast<float*>(sDt + 2 * 16384);  // [ST][lse 64 | delta 64]
+  uint64_t* bar_kv = reinterpret_cast<uint64_t*>(sLD + BKV_STAGES * 128);
   uint64_t* q_full = bar_kv + 1;
-  uint64_t* q_empty = q_full + 2;
-  uint64_t* s_full = q_empty + 2;
-  uint64_t* p_full = s_full + 1;
-  uint64_t* done = p_full + 1;
+  uint64_t* q_empty = q_full + BKV_STAGES;
+  uint64_t* s_full = q_empty + BKV_STAGES;  // [2]
+  uint64_t* s_free = s_full + 2;            // [2]
+  uint64_t* p_full = s_free + 2;            // [2]
+  uint64_t* pv_done = p_full + 2;           // [2]
+  uint64_t* done = pv_done + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x;  // early key blocks see the most query blocks: launch first
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;  // early key blocks see the most query blocks: launched first
   const int b = blockIdx.y / H, h = blockIdx.y % H;
   const int d = H * F_HD;
   const int k0 = kb * B_KEYS;
   const int brow = b * S;
   const int qbeg = k0 / B_Q, nqb = (S + B_Q - 1) / B_Q;
+  const int n = nqb - qbeg;
+  const int64_t vbase = (static_cast<int64_t>(b) * H + h) * S;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tg);
     mbar_init(bar_kv, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < BKV_STAGES; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], BKV_EW);
+      mbar_init(&p_full[i], BKV_EW);
+      mbar_init(&pv_done[i], 1);
+    }
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tslot, 256);
+  if (warp == 2) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tSt = tmem, tPt = tmem + 64, tdV = tmem + 128, tdK = tmem + 192;
+  const uint32_t tdV = tmem + 256, tdK = tmem + 320;  // S^T_i at tmem + 128 i, dP^T_i at + 64
 
   if (warp == 0) {
     if (lane == 0) {
@@ -381,146 +406,207 @@ __global__ void __launch_bounds__(F_THREADS, 2)
         tma_load_2d(sK + hf * 8192, &tq, bar_kv, d + h * F_HD, brow + k0 + hf * 64);
         tma_load_2d(sV + hf * 8192, &tq, bar_kv, 2 * d + h * F_HD, brow + k0 + hf * 64);
       }
-      for (int qb = qbeg, i = 0; qb < nqb; ++qb, ++i) {
-        const int st = i & 1;
-        mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], 2 * 8192);
-        tma_load_2d(sQ + st * 8192, &tq, &q_full[st], h * F_HD, brow + qb * B_Q);
-        tma_load_2d(sG + st * 8192, &tg, &q_full[st], h * F_HD, brow + qb * B_Q);
+      for (int i = 0; i < n; ++i) {
+        const int st = i % BKV_STAGES;
+        const int m0 = (qbeg + i) * B_Q;
+        const uint32_t lbytes = static_cast<uint32_t>(min(B_Q, S - m0)) * 4;  // S % 4 == 0
+        mbar_wait(&q_empty[st], ((i / BKV_STAGES) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * 8192 + 2 * lbytes);
+        tma_load_2d(sQ + st * 8192, &tq, &q_full[st], h * F_HD, brow + m0);
+        tma_load_2d(sG + st * 8192, &tg, &q_full[st], h * F_HD, brow + m0);
+        bulk_load(sLD + st * 128, lse + vbase + m0, lbytes, &q_full[st]);
+        bulk_load(sLD + st * 128 + 64, delta + vbase + m0, lbytes, &q_full[st]);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t ID_T = umma_idesc_bf16(128, B_Q, 0, 0);   // K/V x (Q/dO)^T, N = 64 queries
-      constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // P^T/dS^T x (dO/Q), N = 64 dims
-      mbar_wait(bar_kv, 0);
+    constexpr uint32_t ID_T = umma_idesc_bf16(128, B_Q, 0, 0);   // K/V x (Q/dO)^T, N = 64 queries
+    constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // P^T/dS^T x (dO/Q), N = 64 dims
+    mbar_wait(bar_kv, 0);
+    tc_fence_after();
+    const uint64_t kd = umma_sdesc_sw128(smem_u32(sK), 16, 1024);
+    const uint64_t vd = umma_sdesc_sw128(smem_u32(sV), 16, 1024);
+    const uint64_t qd = umma_sdesc_sw128(smem_u32(sQ), 16, 1024);       // K-major view
+    const uint64_t gd = umma_sdesc_sw128(smem_u32(sG), 16, 1024);
+    const uint64_t qn = umma_sdesc_sw128(smem_u32(sQ), 8192, 1024);     // MN-major view
+    const uint64_t gn = umma_sdesc_sw128(smem_u32(sG), 8192, 1024);
+    const uint64_t pd = umma_sdesc_sw128(smem_u32(sPt), 16, 1024);
+    const uint64_t dd = umma_sdesc_sw128(smem_u32(sDt), 16, 1024);
+    auto issue_s = [&](int i) {
+      const int st = i % BKV_STAGES, bf = i & 1;
+      mbar_wait(&q_full[st], (i / BKV_STAGES) & 1);
+      if (i >= 2) mbar_wait(&s_free[bf], ((i - 2) >> 1) & 1);
       tc_fence_after();
-      const uint32_t ka = smem_u32(sK), va = smem_u32(sV), pa = smem_u32(sPt), da = smem_u32(sDt);
-      for (int qb = qbeg, i = 0; qb < nqb; ++qb, ++i) {
-        const int st = i & 1;
-        mbar_wait(&q_full[st], (i >> 1) & 1);
-        tc_fence_after();
-        const uint32_t qa = smem_u32(sQ + st * 8192), ga = smem_u32(sG + st * 8192);
+      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+      const uint32_t tS = tmem + bf * 128;
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < F_HD / 16; ++k) {
-          tc_mma_f16(tSt, umma_sdesc_sw128(ka + k * 32, 16, 1024), umma_sdesc_sw128(qa + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
-          tc_mma_f16(tPt, umma_sdesc_sw128(va + k * 32, 16, 1024), umma_sdesc_sw128(ga + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
+          tc_mma_f16(tS, kd + 2 * k, qd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          tc_mma_f16(tS + 64, vd + 2 * k, gd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
         }
-        tc_commit(s_full);
-        mbar_wait(p_full, i & 1);
-        tc_fence_after();
+        tc_commit(&s_full[bf]);
+      }
+      __syncwarp();
+    };
+    if (n > 0) issue_s(0);
+    for (int i = 0; i < n; ++i) {
+      if (i + 1 < n) issue_s(i + 1);
+      const int st = i % BKV_STAGES, bf = i & 1;
+      mbar_wait(&p_full[bf], (i >> 1) & 1);
+      tc_fence_after();
+      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+      const uint64_t po = static_cast<uint64_t>(bf * (16384 >> 4));
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < B_Q / 16; ++k) {
           const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-          tc_mma_f16(tdV, umma_sdesc_sw128(pa + k * 32, 16, 1024), umma_sdesc_sw128(ga + k * 2048, 8192, 1024), ID_A, acc);
-          tc_mma_f16(tdK, umma_sdesc_sw128(da + k * 32, 16, 1024), umma_sdesc_sw128(qa + k * 2048, 8192, 1024), ID_A, acc);
+          tc_mma_f16(tdV, pd + po + 2 * k, gn + so + 128 * k, ID_A, acc);
+          tc_mma_f16(tdK, dd + po + 2 * k, qn + so + 128 * k, ID_A, acc);
         }
+        tc_commit(&pv_done[bf]);
         tc_commit(&q_empty[st]);
       }
-      tc_commit(done);
+      __syncwarp();
     }
+    if (elect_one()) tc_commit(done);
+    __syncwarp();
   } else if (warp >= 4) {
-    const int qw = warp & 3;
-    const int r = qw * 32 + lane;  // key row in the tile
+    const int qw = warp & 3;            // TMEM lane quarter
+    const int hf = (warp - 4) >> 2;     // which 32 of the 64 queries
+    const int cb = hf * 32;
+    const int r = qw * 32 + lane;       // key row in the tile
     const int key = k0 + r;
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
-    const float* Lr = lse + (static_cast<int64_t>(b) * H + h) * S;
-    const float* Dr = delta + (static_cast<int64_t>(b) * H + h) * S;
-    for (int qb = qbeg, i = 0; qb < nqb; ++qb, ++i) {
-      mbar_wait(s_full, i & 1);
+    const uint64_t sc2 = pack_f2(sl2, sl2);
+    for (int i = 0; i < n; ++i) {
+      const int st = i % BKV_STAGES, bf = i & 1;
+      const int m0 = (qbeg + i) * B_Q;
+      mbar_wait(&s_full[bf], (i >> 1) & 1);
       tc_fence_after();
-      const int m0 = qb * B_Q;
-      // lse / delta of this query block: every thread reads the same 64 values
-      // (16 B broadcast loads; the block never straddles the end of a batch row
-      // range because S is a multiple of 8)
-      const bool full = m0 + B_Q <= S && (S % 4) == 0;
-#pragma unroll 1
-      for (int c = 0; c < B_Q / 16; ++c) {
-        uint32_t sr[16], dr[16];
-        tmem_ld16(tSt + lo + c * 16, sr);
-        tmem_ld16(tPt + lo + c * 16, dr);
-        float lq[16], dq[16];
-        if (full) {
+      uint32_t sr[32], pr[32];
+      const uint32_t tS = tmem + bf * 128 + lo + cb;
+      tmem_ld16(tS, sr);
+      tmem_ld16(tS + 16, sr + 16);
+      tmem_ld16(tS + 64, pr);
+      tmem_ld16(tS + 80, pr + 16);
+      tc_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[bf]);  // the MMA warp may refill this buffer
+      mbar_wait(&q_full[st], (i / BKV_STAGES) & 1);  // lse / delta rows visible
+      const float* Ls = sLD + st * 128 + cb;
+      const float* Ds = Ls + 64;
+      float pv[32], dv[32];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(Lr + m0 + c * 16) + v);
-            const float4 g = __ldg(reinterpret_cast<const float4*>(Dr + m0 + c * 16) + v);
-            lq[4 * v] = a.x; lq[4 * v + 1] = a.y; lq[4 * v + 2] = a.z; lq[4 * v + 3] = a.w;
-            dq[4 * v] = g.x; dq[4 * v + 1] = g.y; dq[4 * v + 2] = g.z; dq[4 * v + 3] = g.w;
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int q = m0 + c * 16 + e;
-            lq[e] = q < S ? __ldg(Lr + q) : 0.f;
-            dq[e] = q < S ? __ldg(Dr + q) : 0.f;
-          }
-        }
-        tc_wait_ld();
-        float pv[16], dv[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int q = m0 + c * 16 + e;
-          const bool ok = q >= key && q < S;
-          const float p = ok ? ex2(__uint_as_float(sr[e]) * sl2 - lq[e] * 1.4426950408889634f) : 0.f;
-          pv[e] = p;
-          dv[e] = ok ? p * (__uint_as_float(dr[e]) - dq[e]) : 0.f;
-        }
-        st_row16(sPt, r, 2 * c, pv);
-        st_row16(sDt, r, 2 * c, dv);
+      for (int g = 0; g < 8; ++g) {
+        const float4 l4 = reinterpret_cast<const float4*>(Ls)[g];
+        const float4 d4 = reinterpret_cast<const float4*>(Ds)[g];
+        const uint64_t nl01 = pack_f2(-l4.x * 1.4426950408889634f, -l4.y * 1.4426950408889634f);
+        const uint64_t nl23 = pack_f2(-l4.z * 1.4426950408889634f, -l4.w * 1.4426950408889634f);
+        float a0, a1, a2, a3;
+        unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * g]), __uint_as_float(sr[4 * g + 1])), sc2, nl01), a0, a1);
+        unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * g + 2]), __uint_as_float(sr[4 * g + 3])), sc2, nl23), a2, a3);
+        const float p0 = ex2(a0), p1 = ex2(a1), p2 = ex2(a2), p3 = ex2(a3);
+        float e0, e1, e2, e3;
+        unpack_f2(fadd2(pack_f2(__uint_as_float(pr[4 * g]), __uint_as_float(pr[4 * g + 1])),
+                        pack_f2(-d4.x, -d4.y)), e0, e1);
+        unpack_f2(fadd2(pack_f2(__uint_as_float(pr[4 * g + 2]), __uint_as_float(pr[4 * g + 3])),
+                        pack_f2(-d4.z, -d4.w)), e2, e3);
+        float f0, f1, f2, f3;
+        unpack_f2(fmul2(pack_f2(p0, p1), pack_f2(e0, e1)), f0, f1);
+        unpack_f2(fmul2(pack_f2(p2, p3), pack_f2(e2, e3)), f2, f3);
+        pv[4 * g] = p0; pv[4 * g + 1] = p1; pv[4 * g + 2] = p2; pv[4 * g + 3] = p3;
+        dv[4 * g] = f0; dv[4 * g + 1] = f1; dv[4 * g + 2] = f2; dv[4 * g + 3] = f3;
       }
+      // causal / ragged mask: only blocks reaching below the diagonal or past S
+      if (m0 + cb < key || m0 + cb + 32 > S) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int q = m0 + cb + e;
+          if (q < key || q >= S) {
+            pv[e] = 0.f;
+            dv[e] = 0.f;
+          }
+        }
+      }
+      if (i >= 2) mbar_wait(&pv_done[bf], ((i - 2) >> 1) & 1);  // tiles of block i-2 consumed
+      st_row32(sPt + bf * 16384, r, cb / 8, pv);
+      st_row32(sDt + bf * 16384, r, cb / 8, dv);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[bf]);
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    uint32_t acc[64];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld16(tdV + lo + c * 16, acc + c * 16);
+    uint32_t acc[32];
+    bf16* base = dqkv + static_cast<int64_t>(brow + key) * ldd + h * F_HD + cb;
+    tmem_ld16(tdV + lo + cb, acc);
+    tmem_ld16(tdV + lo + cb + 16, acc + 16);
     tc_wait_ld();
-    bf16* base = dqkv + static_cast<int64_t>(brow + key) * ldd + h * F_HD;
-    if (key < S) store_row64(base + 2 * d, acc, 1.f);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld16(tdK + lo + c * 16, acc + c * 16);
+    if (key < S) store_row32(base + 2 * d, acc, 1.f);
+    tmem_ld16(tdK + lo + cb, acc);
+    tmem_ld16(tdK + lo + cb + 16, acc + 16);
     tc_wait_ld();
-    if (key < S) store_row64(base + d, acc, scale);
+    if (key < S) store_row32(base + d, acc, scale);
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 256);
+  if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-constexpr int BQ_SMEM = 2 * 16384 /*Q,dO*/ + 2 * 2 * 8192 /*K,V stages*/ + 16384 /*dS*/ + 1024 + 256;
+constexpr int BQ_STAGES = 3, BQ_THREADS = 384, BQ_EW = 8;
+constexpr int BQ_SMEM = 3 * 16384 /*Q,dO,O*/ + BQ_STAGES * 2 * 8192 /*K,V*/ + 2 * 16384 /*dS x2*/ +
+                        128 * 2 * 4 /*delta halves*/ + 1024 + 256;
 
-// dQ for 128 queries of one (batch, head): S = Q K^T, dP = dO V^T per 64-key
-// block, dS by one thread per query row, dQ += dS K (TMEM accumulator).
-__global__ void __launch_bounds__(F_THREADS, 1)
+// 16 B chunk j (8 bf16) of row r in a [128 x 64] bf16 tile loaded as two
+// 128B-swizzled 64-row TMA boxes.
+__device__ __forceinline__ uint4 ld_chunk128(const uint8_t* tile, int r, int j) {
+  return *reinterpret_cast<const uint4*>(tile + (r >> 6) * 8192 + (r & 63) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+// dQ for 128 queries of one (batch, head), one CTA per SM, 12 warps; also
+// produces delta = rowsum(dO o O) for these rows (consumed by the dK/dV
+// kernel that runs next):
+//   warp 0      TMA producer: Q, dO, O once; K/V blocks of 64 keys (3-deep ring)
+//   warp 1      MMA issuer, one key block ahead of the elementwise warps:
+//                 S_j = Q K_j^T, dP_j = dO V_j^T -> TMEM buffer j % 2
+//                 dQ += dS_j K_j                 -> TMEM accumulator
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4..11 elementwise: two warps per TMEM lane quarter (one query row
+//               per thread, 32 of the 64 keys each) build
+//               dS = exp2(S*c - lse) (dP - delta) into 128B-swizzled smem
+__global__ void __launch_bounds__(BQ_THREADS, 1)
     fa_bwd_dq_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
-                  const float* __restrict__ lse, const float* __restrict__ delta,
-                  bf16* __restrict__ dqkv, int64_t ldd, int H, int S, float sl2, float scale) {
+                  const __grid_constant__ CUtensorMap to, const float* __restrict__ lse,
+                  float* __restrict__ delta, bf16* __restrict__ dqkv, int64_t ldd, int H, int S,
+                  float sl2, float scale) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
   uint8_t* sG = sQ + 16384;
-  uint8_t* sK = sG + 16384;       // [2][64 x 64]
-  uint8_t* sV = sK + 2 * 8192;    // [2][64 x 64]
-  uint8_t* sD = sV + 2 * 8192;    // dS [128 q x 64 keys]
-  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sD + 16384);
+  uint8_t* sO = sG + 16384;
+  uint8_t* sK = sO + 16384;                // [ST][64 x 64]
+  uint8_t* sV = sK + BQ_STAGES * 8192;     // [ST][64 x 64]
+  uint8_t* sD = sV + BQ_STAGES * 8192;     // dS [2][128 q x 64 keys]
+  float* sDelta = reinterpret_cast<float*>(sD + 2 * 16384);  // [2][128] half-row partials
+  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sDelta + 256);
   uint64_t* kv_full = bar_q + 1;
-  uint64_t* kv_empty = kv_full + 2;
-  uint64_t* s_full = kv_empty + 2;
-  uint64_t* p_full = s_full + 1;
-  uint64_t* done = p_full + 1;
+  uint64_t* kv_empty = kv_full + BQ_STAGES;
+  uint64_t* s_full = kv_empty + BQ_STAGES;  // [2]
+  uint64_t* s_free = s_full + 2;            // [2]
+  uint64_t* p_full = s_free + 2;            // [2]
+  uint64_t* pv_done = p_full + 2;           // [2]
+  uint64_t* done = pv_done + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = (S + F_BM - 1) / F_BM;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int nqt = (S + F_BM - 1) / F_BM;
+  const int qb = nqt - 1 - static_cast<int>(blockIdx.x);  // long (late) tiles first
   const int b = blockIdx.y / H, h = blockIdx.y % H;
   const int d = H * F_HD;
   const int q0 = qb * F_BM;
@@ -530,112 +616,175 @@ __global__ void __launch_bounds__(F_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tg);
+    tma_prefetch_desc(&to);
     mbar_init(bar_q, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < BQ_STAGES; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], BQ_EW);
+      mbar_init(&p_full[i], BQ_EW);
+      mbar_init(&pv_done[i], 1);
+    }
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tslot, 256);
+  if (warp == 2) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tP = tmem + 64, tdQ = tmem + 128;
+  const uint32_t tdQ = tmem + 256;  // S_j at tmem + 128 (j % 2), dP_j at + 64
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_q, 2 * 16384);
+      mbar_expect_tx(bar_q, 3 * 16384);
       for (int hf = 0; hf < 2; ++hf) {
         tma_load_2d(sQ + hf * 8192, &tq, bar_q, h * F_HD, brow + q0 + hf * 64);
         tma_load_2d(sG + hf * 8192, &tg, bar_q, h * F_HD, brow + q0 + hf * 64);
+        tma_load_2d(sO + hf * 8192, &to, bar_q, h * F_HD, brow + q0 + hf * 64);
       }
       for (int j = 0; j < nkb; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % BQ_STAGES;
+        mbar_wait(&kv_empty[st], ((j / BQ_STAGES) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * 8192);
         tma_load_2d(sK + st * 8192, &tq, &kv_full[st], d + h * F_HD, brow + j * F_BN);
         tma_load_2d(sV + st * 8192, &tq, &kv_full[st], 2 * d + h * F_HD, brow + j * F_BN);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t ID_T = umma_idesc_bf16(128, F_BN, 0, 0);  // Q/dO x (K/V)^T
-      constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // dS x K (MN-major)
-      mbar_wait(bar_q, 0);
+    constexpr uint32_t ID_T = umma_idesc_bf16(128, F_BN, 0, 0);  // Q/dO x (K/V)^T
+    constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // dS x K (MN-major)
+    mbar_wait(bar_q, 0);
+    tc_fence_after();
+    const uint64_t qd = umma_sdesc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t gd = umma_sdesc_sw128(smem_u32(sG), 16, 1024);
+    const uint64_t kd = umma_sdesc_sw128(smem_u32(sK), 16, 1024);     // K-major view
+    const uint64_t vd = umma_sdesc_sw128(smem_u32(sV), 16, 1024);
+    const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), 8192, 1024);   // MN-major view
+    const uint64_t dd = umma_sdesc_sw128(smem_u32(sD), 16, 1024);
+    auto issue_s = [&](int j) {
+      const int st = j % BQ_STAGES, bf = j & 1;
+      mbar_wait(&kv_full[st], (j / BQ_STAGES) & 1);
+      if (j >= 2) mbar_wait(&s_free[bf], ((j - 2) >> 1) & 1);
       tc_fence_after();
-      const uint32_t qa = smem_u32(sQ), ga = smem_u32(sG), dsa = smem_u32(sD);
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t ka = smem_u32(sK + st * 8192), va = smem_u32(sV + st * 8192);
+      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+      const uint32_t tS = tmem + bf * 128;
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < F_HD / 16; ++k) {
-          tc_mma_f16(tS, umma_sdesc_sw128(qa + k * 32, 16, 1024), umma_sdesc_sw128(ka + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
-          tc_mma_f16(tP, umma_sdesc_sw128(ga + k * 32, 16, 1024), umma_sdesc_sw128(va + k * 32, 16, 1024), ID_T, k > 0 ? 1u : 0u);
+          tc_mma_f16(tS, qd + 2 * k, kd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          tc_mma_f16(tS + 64, gd + 2 * k, vd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
         }
-        tc_commit(s_full);
-        mbar_wait(p_full, j & 1);
-        tc_fence_after();
+        tc_commit(&s_full[bf]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nkb; ++j) {
+      if (j + 1 < nkb) issue_s(j + 1);
+      const int st = j % BQ_STAGES, bf = j & 1;
+      mbar_wait(&p_full[bf], (j >> 1) & 1);
+      tc_fence_after();
+      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+      const uint64_t po = static_cast<uint64_t>(bf * (16384 >> 4));
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < F_BN / 16; ++k)
-          tc_mma_f16(tdQ, umma_sdesc_sw128(dsa + k * 32, 16, 1024), umma_sdesc_sw128(ka + k * 2048, 8192, 1024), ID_A,
-                     (j > 0 || k > 0) ? 1u : 0u);
+          tc_mma_f16(tdQ, dd + po + 2 * k, kn + so + 128 * k, ID_A, (j > 0 || k > 0) ? 1u : 0u);
+        tc_commit(&pv_done[bf]);
         tc_commit(&kv_empty[st]);
       }
-      tc_commit(done);
+      __syncwarp();
     }
+    if (elect_one()) tc_commit(done);
+    __syncwarp();
   } else if (warp >= 4) {
-    const int qw = warp & 3;
-    const int r = qw * 32 + lane;
+    const int qw = warp & 3;           // TMEM lane quarter
+    const int hf = (warp - 4) >> 2;    // which 32 of the 64 keys / head dims
+    const int cb = hf * 32;
+    const int r = qw * 32 + lane;      // query row in the tile
     const int row = q0 + r;
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const int64_t vrow = (static_cast<int64_t>(b) * H + h) * S + row;
-    const float l2 = row < S ? lse[vrow] * 1.4426950408889634f : 0.f;
-    const float dl = row < S ? delta[vrow] : 0.f;
-    for (int j = 0; j < nkb; ++j) {
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      const int n0 = j * F_BN;
+    // delta = rowsum(dO o O): each warp half sums 32 head dims, fixed-order combine
+    mbar_wait(bar_q, 0);
+    float part = 0.f;
 #pragma unroll
-      for (int c = 0; c < F_BN / 16; ++c) {
-        uint32_t sr[16], dr[16];
-        tmem_ld16(tS + lo + c * 16, sr);
-        tmem_ld16(tP + lo + c * 16, dr);
-        tc_wait_ld();
-        float dsv[16];
+    for (int jj = 0; jj < 4; ++jj) {
+      const uint4 ov = ld_chunk128(sO, r, hf * 4 + jj);
+      const uint4 gv = ld_chunk128(sG, r, hf * 4 + jj);
+      const __nv_bfloat162* oh = reinterpret_cast<const __nv_bfloat162*>(&ov);
+      const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gv);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int key = n0 + c * 16 + e;
-          const bool ok = key <= row && key < S && row < S;
-          const float p = ok ? ex2(__uint_as_float(sr[e]) * sl2 - l2) : 0.f;
-          dsv[e] = ok ? p * (__uint_as_float(dr[e]) - dl) : 0.f;
-        }
-        st_row16(sD, r, 2 * c, dsv);
+      for (int k = 0; k < 4; ++k) {
+        const float2 of = __bfloat1622float2(oh[k]), gf = __bfloat1622float2(gh[k]);
+        part = fmaf(of.x, gf.x, part);
+        part = fmaf(of.y, gf.y, part);
       }
+    }
+    sDelta[hf * 128 + r] = part;
+    asm volatile("bar.sync 1, %0;" ::"n"(BQ_EW * 32) : "memory");  // elementwise warps only
+    const float dl = sDelta[r] + sDelta[128 + r];
+    if (hf == 0 && row < S) delta[vrow] = dl;
+    const float nl2 = row < S ? -lse[vrow] * 1.4426950408889634f : 0.f;
+    const uint64_t sc2 = pack_f2(sl2, sl2), nl22 = pack_f2(nl2, nl2), nd2 = pack_f2(-dl, -dl);
+    for (int j = 0; j < nkb; ++j) {
+      const int bf = j & 1;
+      const int n0 = j * F_BN;
+      mbar_wait(&s_full[bf], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[32], pr[32];
+      const uint32_t tS = tmem + bf * 128 + lo + cb;
+      tmem_ld16(tS, sr);
+      tmem_ld16(tS + 16, sr + 16);
+      tmem_ld16(tS + 64, pr);
+      tmem_ld16(tS + 80, pr + 16);
+      tc_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[bf]);
+      float dv[32];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        float a0, a1, e0, e1, f0, f1;
+        unpack_f2(ffma2(pack_f2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2, nl22), a0, a1);
+        const float p0 = ex2(a0), p1 = ex2(a1);
+        unpack_f2(fadd2(pack_f2(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1])), nd2), e0, e1);
+        unpack_f2(fmul2(pack_f2(p0, p1), pack_f2(e0, e1)), f0, f1);
+        dv[e] = f0;
+        dv[e + 1] = f1;
+      }
+      // causal / ragged mask: only blocks crossing the diagonal or the sequence end
+      if (n0 + cb + 31 > row || n0 + cb + 32 > S || row >= S) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int key = n0 + cb + e;
+          if (key > row || key >= S || row >= S) dv[e] = 0.f;
+        }
+      }
+      if (j >= 2) mbar_wait(&pv_done[bf], ((j - 2) >> 1) & 1);
+      st_row32(sD + bf * 16384, r, cb / 8, dv);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[bf]);
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    uint32_t acc[64];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld16(tdQ + lo + c * 16, acc + c * 16);
+    uint32_t acc[32];
+    tmem_ld16(tdQ + lo + cb, acc);
+    tmem_ld16(tdQ + lo + cb + 16, acc + 16);
     tc_wait_ld();
-    if (row < S) store_row64(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD, acc, scale);
+    if (row < S) store_row32(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD + cb, acc, scale);
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 256);
+  if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
 int make_tmap_rows64(CUtensorMap* m, const void* base, int64_t ld, int64_t rows) {
@@ -697,18 +846,15 @@ int attention_fwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, void
 }  // namespace pp200
 
 namespace pp200 {
-int attention_delta(int dtype, int B, int H, int S, int hd, const void* o, const void* dO,
-                    int64_t ld_o, float* delta, cudaStream_t st);
-
 int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, const void* o,
                       const void* dO, int64_t ld_o, const float* lse, float* delta, void* dqkv,
                       int64_t ld_dqkv, cudaStream_t st) {
-  int rc = attention_delta(PC_BF16, B, H, S, F_HD, o, dO, ld_o, delta, st);
-  if (rc) return rc;
-  CUtensorMap tq, tg;
-  rc = make_tmap_rows64(&tq, qkv, ld_qkv, static_cast<int64_t>(B) * S);
+  CUtensorMap tq, tg, to;
+  int rc = make_tmap_rows64(&tq, qkv, ld_qkv, static_cast<int64_t>(B) * S);
   if (rc) return rc;
   rc = make_tmap_rows64(&tg, dO, ld_o, static_cast<int64_t>(B) * S);
+  if (rc) return rc;
+  rc = make_tmap_rows64(&to, o, ld_o, static_cast<int64_t>(B) * S);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
@@ -718,14 +864,15 @@ int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, cons
   }
   const float scale = 1.f / sqrtf(static_cast<float>(F_HD));
   const float sl2 = scale * 1.4426950408889634f;
-  dim3 g1((S + B_KEYS - 1) / B_KEYS, B * H);
-  fa_bwd_dkdv_tc5<<<g1, F_THREADS, BKV_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
-                                                    ld_dqkv, H, S, sl2, scale);
-  rc = check_launch("fa_bwd_dkdv_tc5");
-  if (rc) return rc;
+  // dQ first: it also writes delta = rowsum(dO o O), which dK/dV consume
   dim3 g2((S + F_BM - 1) / F_BM, B * H);
-  fa_bwd_dq_tc5<<<g2, F_THREADS, BQ_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
-                                                 ld_dqkv, H, S, sl2, scale);
-  return check_launch("fa_bwd_dq_tc5");
+  fa_bwd_dq_tc5<<<g2, BQ_THREADS, BQ_SMEM, st>>>(tq, tg, to, lse, delta, static_cast<bf16*>(dqkv),
+                                                  ld_dqkv, H, S, sl2, scale);
+  rc = check_launch("fa_bwd_dq_tc5");
+  if (rc) return rc;
+  dim3 g1((S + B_KEYS - 1) / B_KEYS, B * H);
+  fa_bwd_dkdv_tc5<<<g1, BKV_THREADS, BKV_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
+                                                      ld_dqkv, H, S, sl2, scale);
+  return check_launch("fa_bwd_dkdv_tc5");
 }
 }  // namespace pp200
