@@ -301,31 +301,43 @@ __global__ void __launch_bounds__(F_THREADS, 2)
 
 
 // ------------------------------------------------------------------ backward
-constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 3, BKV_THREADS = 384, BKV_EW = 8;
+// NG elementwise warps per TMEM lane quarter, each owning CW = 64 / NG columns
+constexpr int BW_NG = 4, BW_CW = 64 / BW_NG;
+constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 3, BKV_EW = 4 * BW_NG, BKV_THREADS = 128 + 32 * BKV_EW;
 constexpr int BKV_SMEM = 2 * 16384 /*K,V*/ + BKV_STAGES * 2 * 8192 /*Q,dO*/ +
                          2 * 2 * 16384 /*P^T,dS^T x2*/ + BKV_STAGES * 512 /*lse,delta*/ + 1024 + 256;
 
-// 32 bf16 (four 16 B chunks starting at logical chunk c4) of row r of a
+// NC * 8 bf16 (NC 16 B chunks starting at logical chunk c0) of row r of a
 // 128B-swizzled [rows x 64] K-major tile.
-__device__ __forceinline__ void st_row32(uint8_t* tile, int r, int c4, const float* v) {
+template <int NC>
+__device__ __forceinline__ void st_row_chunks(uint8_t* tile, int r, int c0, const float* v) {
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
+  for (int h = 0; h < NC; ++h) {
     uint4 u;
     __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
     for (int k = 0; k < 4; ++k) hp[k] = __floats2bfloat162_rn(v[8 * h + 2 * k], v[8 * h + 2 * k + 1]);
-    *reinterpret_cast<uint4*>(tile + r * 128 + (((c4 + h) ^ (r & 7)) << 4)) = u;
+    *reinterpret_cast<uint4*>(tile + r * 128 + (((c0 + h) ^ (r & 7)) << 4)) = u;
   }
 }
 
-__device__ __forceinline__ void store_row32(bf16* dst, const uint32_t* acc, float scale) {
-  uint4 u[4];
+// NC * 8 fp32 accumulator values -> bf16 (scaled) in global memory.
+template <int NC>
+__device__ __forceinline__ void store_row_chunks(bf16* dst, const uint32_t* acc, float scale) {
+  uint4 u[NC];
   __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(u);
 #pragma unroll
-  for (int k = 0; k < 16; ++k)
+  for (int k = 0; k < 4 * NC; ++k)
     hp[k] = __floats2bfloat162_rn(__uint_as_float(acc[2 * k]) * scale, __uint_as_float(acc[2 * k + 1]) * scale);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) reinterpret_cast<uint4*>(dst)[k] = u[k];
+  for (int k = 0; k < NC; ++k) reinterpret_cast<uint4*>(dst)[k] = u[k];
+}
+
+// CW fp32 columns of one TMEM lane into registers (CW = 16 or 32).
+template <int CW>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
+#pragma unroll
+  for (int i = 0; i < CW / 16; ++i) tmem_ld16(taddr + 16 * i, r + 16 * i);
 }
 
 // dK, dV for 128 keys of one (batch, head), one CTA per SM, 12 warps:
@@ -335,8 +347,8 @@ __device__ __forceinline__ void store_row32(bf16* dst, const uint32_t* acc, floa
 //                 S^T_i = K Q_i^T, dP^T_i = V dO_i^T  -> TMEM buffer i % 2
 //                 dV += P^T_i dO_i, dK += dS^T_i Q_i  -> TMEM accumulators
 //   warp 2      TMEM allocator (512 columns: S^T/dP^T x2, dV, dK)
-//   warps 4..11 elementwise: two warps per TMEM lane quarter (one key row per
-//               thread, 32 of the 64 queries each) build P^T = exp2(S^T*c - lse)
+//   warps 4..   elementwise: BW_NG warps per TMEM lane quarter (one key row
+//               per thread, 64 / BW_NG queries each) build P^T = exp2(S^T*c - lse)
 //               and dS^T = P^T (dP^T - delta) into 128B-swizzled smem tiles
 // Barriers: s_full / s_free (scores landed / read out of TMEM), p_full (P^T,
 // dS^T staged), pv_done (dV/dK MMAs of block i retired: tiles reusable).
@@ -471,10 +483,10 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
     if (elect_one()) tc_commit(done);
     __syncwarp();
   } else if (warp >= 4) {
-    const int qw = warp & 3;            // TMEM lane quarter
-    const int hf = (warp - 4) >> 2;     // which 32 of the 64 queries
-    const int cb = hf * 32;
-    const int r = qw * 32 + lane;       // key row in the tile
+    constexpr int CW = BW_CW;
+    const int qw = warp & 3;                 // TMEM lane quarter
+    const int cb = ((warp - 4) >> 2) * CW;   // first of this warp's CW queries / head dims
+    const int r = qw * 32 + lane;            // key row in the tile
     const int key = k0 + r;
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
@@ -483,12 +495,10 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
       const int m0 = (qbeg + i) * B_Q;
       mbar_wait(&s_full[bf], (i >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[32], pr[32];
+      uint32_t sr[CW], pr[CW];
       const uint32_t tS = tmem + bf * 128 + lo + cb;
-      tmem_ld16(tS, sr);
-      tmem_ld16(tS + 16, sr + 16);
-      tmem_ld16(tS + 64, pr);
-      tmem_ld16(tS + 80, pr + 16);
+      tmem_ld_cols<CW>(tS, sr);
+      tmem_ld_cols<CW>(tS + 64, pr);
       tc_wait_ld();
       tc_fence_before();
       __syncwarp();
@@ -496,9 +506,9 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
       mbar_wait(&q_full[st], (i / BKV_STAGES) & 1);  // lse / delta rows visible
       const float* Ls = sLD + st * 128 + cb;
       const float* Ds = Ls + 64;
-      float pv[32], dv[32];
+      float pv[CW], dv[CW];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
+      for (int g = 0; g < CW / 4; ++g) {
         const float4 l4 = reinterpret_cast<const float4*>(Ls)[g];
         const float4 d4 = reinterpret_cast<const float4*>(Ds)[g];
         const uint64_t nl01 = pack_f2(-l4.x * 1.4426950408889634f, -l4.y * 1.4426950408889634f);
@@ -519,9 +529,9 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
         dv[4 * g] = f0; dv[4 * g + 1] = f1; dv[4 * g + 2] = f2; dv[4 * g + 3] = f3;
       }
       // causal / ragged mask: only blocks reaching below the diagonal or past S
-      if (m0 + cb < key || m0 + cb + 32 > S) {
+      if (m0 + cb < key || m0 + cb + CW > S) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < CW; ++e) {
           const int q = m0 + cb + e;
           if (q < key || q >= S) {
             pv[e] = 0.f;
@@ -530,8 +540,8 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
         }
       }
       if (i >= 2) mbar_wait(&pv_done[bf], ((i - 2) >> 1) & 1);  // tiles of block i-2 consumed
-      st_row32(sPt + bf * 16384, r, cb / 8, pv);
-      st_row32(sDt + bf * 16384, r, cb / 8, dv);
+      st_row_chunks<CW / 8>(sPt + bf * 16384, r, cb / 8, pv);
+      st_row_chunks<CW / 8>(sDt + bf * 16384, r, cb / 8, dv);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
@@ -539,16 +549,14 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    uint32_t acc[32];
+    uint32_t acc[CW];
     bf16* base = dqkv + static_cast<int64_t>(brow + key) * ldd + h * F_HD + cb;
-    tmem_ld16(tdV + lo + cb, acc);
-    tmem_ld16(tdV + lo + cb + 16, acc + 16);
+    tmem_ld_cols<CW>(tdV + lo + cb, acc);
     tc_wait_ld();
-    if (key < S) store_row32(base + 2 * d, acc, 1.f);
-    tmem_ld16(tdK + lo + cb, acc);
-    tmem_ld16(tdK + lo + cb + 16, acc + 16);
+    if (key < S) store_row_chunks<CW / 8>(base + 2 * d, acc, 1.f);
+    tmem_ld_cols<CW>(tdK + lo + cb, acc);
     tc_wait_ld();
-    if (key < S) store_row32(base + d, acc, scale);
+    if (key < S) store_row_chunks<CW / 8>(base + d, acc, scale);
   }
 
   tc_fence_before();
@@ -557,9 +565,9 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-constexpr int BQ_STAGES = 3, BQ_THREADS = 384, BQ_EW = 8;
+constexpr int BQ_STAGES = 3, BQ_EW = 4 * BW_NG, BQ_THREADS = 128 + 32 * BQ_EW;
 constexpr int BQ_SMEM = 3 * 16384 /*Q,dO,O*/ + BQ_STAGES * 2 * 8192 /*K,V*/ + 2 * 16384 /*dS x2*/ +
-                        128 * 2 * 4 /*delta halves*/ + 1024 + 256;
+                        128 * BW_NG * 4 /*delta partials*/ + 1024 + 256;
 
 // 16 B chunk j (8 bf16) of row r in a [128 x 64] bf16 tile loaded as two
 // 128B-swizzled 64-row TMA boxes.
@@ -575,8 +583,8 @@ __device__ __forceinline__ uint4 ld_chunk128(const uint8_t* tile, int r, int j) 
 //                 S_j = Q K_j^T, dP_j = dO V_j^T -> TMEM buffer j % 2
 //                 dQ += dS_j K_j                 -> TMEM accumulator
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4..11 elementwise: two warps per TMEM lane quarter (one query row
-//               per thread, 32 of the 64 keys each) build
+//   warps 4..   elementwise: BW_NG warps per TMEM lane quarter (one query
+//               row per thread, 64 / BW_NG keys each) build
 //               dS = exp2(S*c - lse) (dP - delta) into 128B-swizzled smem
 __global__ void __launch_bounds__(BQ_THREADS, 1)
     fa_bwd_dq_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
@@ -592,8 +600,8 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   uint8_t* sK = sO + 16384;                // [ST][64 x 64]
   uint8_t* sV = sK + BQ_STAGES * 8192;     // [ST][64 x 64]
   uint8_t* sD = sV + BQ_STAGES * 8192;     // dS [2][128 q x 64 keys]
-  float* sDelta = reinterpret_cast<float*>(sD + 2 * 16384);  // [2][128] half-row partials
-  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sDelta + 256);
+  float* sDelta = reinterpret_cast<float*>(sD + 2 * 16384);  // [BW_NG][128] row partials
+  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sDelta + 128 * BW_NG);
   uint64_t* kv_full = bar_q + 1;
   uint64_t* kv_empty = kv_full + BQ_STAGES;
   uint64_t* s_full = kv_empty + BQ_STAGES;  // [2]
@@ -702,20 +710,21 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
     if (elect_one()) tc_commit(done);
     __syncwarp();
   } else if (warp >= 4) {
-    const int qw = warp & 3;           // TMEM lane quarter
-    const int hf = (warp - 4) >> 2;    // which 32 of the 64 keys / head dims
-    const int cb = hf * 32;
-    const int r = qw * 32 + lane;      // query row in the tile
+    constexpr int CW = BW_CW;
+    const int qw = warp & 3;               // TMEM lane quarter
+    const int grp = (warp - 4) >> 2;       // column group
+    const int cb = grp * CW;               // first of this warp's CW keys / head dims
+    const int r = qw * 32 + lane;          // query row in the tile
     const int row = q0 + r;
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const int64_t vrow = (static_cast<int64_t>(b) * H + h) * S + row;
-    // delta = rowsum(dO o O): each warp half sums 32 head dims, fixed-order combine
+    // delta = rowsum(dO o O): each column group sums CW head dims, fixed-order combine
     mbar_wait(bar_q, 0);
     float part = 0.f;
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const uint4 ov = ld_chunk128(sO, r, hf * 4 + jj);
-      const uint4 gv = ld_chunk128(sG, r, hf * 4 + jj);
+    for (int jj = 0; jj < CW / 8; ++jj) {
+      const uint4 ov = ld_chunk128(sO, r, cb / 8 + jj);
+      const uint4 gv = ld_chunk128(sG, r, cb / 8 + jj);
       const __nv_bfloat162* oh = reinterpret_cast<const __nv_bfloat162*>(&ov);
       const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gv);
 #pragma unroll
@@ -725,10 +734,12 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
         part = fmaf(of.y, gf.y, part);
       }
     }
-    sDelta[hf * 128 + r] = part;
+    sDelta[grp * 128 + r] = part;
     asm volatile("bar.sync 1, %0;" ::"n"(BQ_EW * 32) : "memory");  // elementwise warps only
-    const float dl = sDelta[r] + sDelta[128 + r];
-    if (hf == 0 && row < S) delta[vrow] = dl;
+    float dl = 0.f;
+#pragma unroll
+    for (int g = 0; g < BW_NG; ++g) dl += sDelta[g * 128 + r];
+    if (grp == 0 && row < S) delta[vrow] = dl;
     const float nl2 = row < S ? -lse[vrow] * 1.4426950408889634f : 0.f;
     const uint64_t sc2 = pack_f2(sl2, sl2), nl22 = pack_f2(nl2, nl2), nd2 = pack_f2(-dl, -dl);
     for (int j = 0; j < nkb; ++j) {
@@ -736,19 +747,17 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       const int n0 = j * F_BN;
       mbar_wait(&s_full[bf], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[32], pr[32];
+      uint32_t sr[CW], pr[CW];
       const uint32_t tS = tmem + bf * 128 + lo + cb;
-      tmem_ld16(tS, sr);
-      tmem_ld16(tS + 16, sr + 16);
-      tmem_ld16(tS + 64, pr);
-      tmem_ld16(tS + 80, pr + 16);
+      tmem_ld_cols<CW>(tS, sr);
+      tmem_ld_cols<CW>(tS + 64, pr);
       tc_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[bf]);
-      float dv[32];
+      float dv[CW];
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
+      for (int e = 0; e < CW; e += 2) {
         float a0, a1, e0, e1, f0, f1;
         unpack_f2(ffma2(pack_f2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2, nl22), a0, a1);
         const float p0 = ex2(a0), p1 = ex2(a1);
@@ -758,15 +767,15 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
         dv[e + 1] = f1;
       }
       // causal / ragged mask: only blocks crossing the diagonal or the sequence end
-      if (n0 + cb + 31 > row || n0 + cb + 32 > S || row >= S) {
+      if (n0 + cb + CW - 1 > row || n0 + cb + CW > S || row >= S) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < CW; ++e) {
           const int key = n0 + cb + e;
           if (key > row || key >= S || row >= S) dv[e] = 0.f;
         }
       }
       if (j >= 2) mbar_wait(&pv_done[bf], ((j - 2) >> 1) & 1);
-      st_row32(sD + bf * 16384, r, cb / 8, dv);
+      st_row_chunks<CW / 8>(sD + bf * 16384, r, cb / 8, dv);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
@@ -774,11 +783,11 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    uint32_t acc[32];
-    tmem_ld16(tdQ + lo + cb, acc);
-    tmem_ld16(tdQ + lo + cb + 16, acc + 16);
+    uint32_t acc[CW];
+    tmem_ld_cols<CW>(tdQ + lo + cb, acc);
     tc_wait_ld();
-    if (row < S) store_row32(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD + cb, acc, scale);
+    if (row < S)
+      store_row_chunks<CW / 8>(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD + cb, acc, scale);
   }
 
   tc_fence_before();
