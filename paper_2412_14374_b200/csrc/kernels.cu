@@ -242,15 +242,69 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int64_t c = blockIdx.x * static_cast<int64_t>(CR_COLS) + threadIdx.x;
-  if (c < cols) {
-    float t1 = 0.f, t2 = 0.f;
-    for (int k = 0; k < static_cast<int>(gridDim.y); ++k) {
-      t1 += __ldcg(ws1 + k * cols + c);
-      if (MODE == 1) t2 += __ldcg(ws2 + k * cols + c);
+  // Parallel fold of the gridDim.y partial rows, deterministic whichever CTA
+  // arrives last: warp w sums partial rows w, w+8, ... (ascending) for 8
+  // columns per lane, then the 8 warp sums combine in warp order.
+  {
+    // partial rows w, w+8, ... in batches of 4 (loads of a batch in flight
+    // together), added in ascending order
+    float f1[8] = {}, f2[8] = {};
+    const bool v4 = (cols % 4) == 0 && c0 + 8 <= cols;
+    const int R = static_cast<int>(gridDim.y);
+    for (int k0 = w; k0 < R; k0 += 32) {
+      float4 a4[4][2], b4[4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = k0 + 8 * i;
+        if (k < R && v4) {
+          a4[i][0] = __ldcg(reinterpret_cast<const float4*>(ws1 + k * cols + c0));
+          a4[i][1] = __ldcg(reinterpret_cast<const float4*>(ws1 + k * cols + c0 + 4));
+          if (MODE == 1) {
+            b4[i][0] = __ldcg(reinterpret_cast<const float4*>(ws2 + k * cols + c0));
+            b4[i][1] = __ldcg(reinterpret_cast<const float4*>(ws2 + k * cols + c0 + 4));
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = k0 + 8 * i;
+        if (k >= R) break;
+        if (v4) {
+          f1[0] += a4[i][0].x; f1[1] += a4[i][0].y; f1[2] += a4[i][0].z; f1[3] += a4[i][0].w;
+          f1[4] += a4[i][1].x; f1[5] += a4[i][1].y; f1[6] += a4[i][1].z; f1[7] += a4[i][1].w;
+          if (MODE == 1) {
+            f2[0] += b4[i][0].x; f2[1] += b4[i][0].y; f2[2] += b4[i][0].z; f2[3] += b4[i][0].w;
+            f2[4] += b4[i][1].x; f2[5] += b4[i][1].y; f2[6] += b4[i][1].z; f2[7] += b4[i][1].w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (c0 + j < cols) {
+              f1[j] += __ldcg(ws1 + k * cols + c0 + j);
+              if (MODE == 1) f2[j] += __ldcg(ws2 + k * cols + c0 + j);
+            }
+          }
+        }
+      }
     }
-    out1[c] = accumulate ? out1[c] + t1 : t1;
-    if (MODE == 1) out2[c] = t2;
+    __syncthreads();  // sm1 / sm2 are reused
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sm1[w][lane * 8 + j] = f1[j];
+      if (MODE == 1) sm2[w][lane * 8 + j] = f2[j];
+    }
+    __syncthreads();
+    const int64_t c = blockIdx.x * static_cast<int64_t>(CR_COLS) + threadIdx.x;
+    if (c < cols) {
+      float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        t1 += sm1[k][threadIdx.x];
+        if (MODE == 1) t2 += sm2[k][threadIdx.x];
+      }
+      out1[c] = accumulate ? out1[c] + t1 : t1;
+      if (MODE == 1) out2[c] = t2;
+    }
   }
   if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
@@ -327,7 +381,12 @@ bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda
   if (ws == nullptr || ws_bytes < colred_ws_bytes(rows, cols) || rows <= 0 ||
       (cols + CR_COLS - 1) / CR_COLS > COLRED_COUNTERS)
     return false;
-  const int64_t R = colred_chunks(rows), chunk = (rows + R - 1) / R;
+  // about two CTAs per SM in total: enough rows per CTA to amortise its
+  // partial write / fence / arrival, enough CTAs to fill the machine
+  const int64_t cblocks = (cols + CR_COLS - 1) / CR_COLS;
+  int64_t R = (2 * num_sms() + cblocks - 1) / cblocks;
+  R = R < 1 ? 1 : (R > colred_chunks(rows) ? colred_chunks(rows) : R);
+  const int64_t chunk = (rows + R - 1) / R;
   unsigned int* ctr = static_cast<unsigned int*>(ws);
   float* w1 = reinterpret_cast<float*>(ctr + COLRED_COUNTERS);
   float* w2 = w1 + R * cols;
