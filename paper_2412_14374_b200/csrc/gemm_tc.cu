@@ -77,6 +77,7 @@ __device__ __forceinline__ void load16(const void* base, bool f32, int64_t off, 
         v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
       }
     } else {
+#pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = i < nvalid ? p[i] : 0.f;
     }
   } else {
@@ -94,6 +95,7 @@ __device__ __forceinline__ void load16(const void* base, bool f32, int64_t off, 
         }
       }
     } else {
+#pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = i < nvalid ? __bfloat162float(p[i]) : 0.f;
     }
   }
@@ -109,7 +111,9 @@ __device__ __forceinline__ void store16(void* base, bool f32, int64_t off, int n
         reinterpret_cast<float4*>(p)[i] =
             make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     } else {
-      for (int i = 0; i < nvalid; ++i) p[i] = v[i];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)  // fixed trip count: v stays in registers
+        if (i < nvalid) p[i] = v[i];
     }
   } else {
     __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + off;
@@ -124,16 +128,22 @@ __device__ __forceinline__ void store16(void* base, bool f32, int64_t off, int n
         reinterpret_cast<uint4*>(p)[i] = t;
       }
     } else {
-      for (int i = 0; i < nvalid; ++i) p[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < nvalid) p[i] = __float2bfloat16_rn(v[i]);
     }
   }
 }
 
 // Applies the fused epilogue to 16 accumulator values of (row, col..col+15).
-// store_c: write C here (direct path).  pre != nullptr: the pre-activation of
-// GELU/RELU is returned there (staged for a TMA store) instead of stored.
+// store_c: write C here (direct path).  stage_pre: the pre-activation of
+// GELU/RELU is returned in pre (staged for a TMA store) instead of stored.
+// have_aux: the aux input was already read (TMA box) into aux_pre.  The arrays
+// are always real register arrays (never selected against nullptr), so they
+// stay out of local memory.
 __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, float* v,
-                                           bool store_c, float* pre, const float* aux_pre) {
+                                           bool store_c, bool stage_pre, float* pre,
+                                           bool have_aux, const float* aux_pre) {
   const int nvalid = min(16, ep.N - col);
   const bool f32 = ep.out_f32 != 0;
   const int fl = ep.flags;
@@ -154,11 +164,12 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
         v[4 * i] += b4.x; v[4 * i + 1] += b4.y; v[4 * i + 2] += b4.z; v[4 * i + 3] += b4.w;
       }
     } else {
+#pragma unroll
       for (int i = 0; i < 16; ++i) v[i] += i < nvalid ? bp[i] : 0.f;
     }
   }
   if (fl & (PC_EPI_GELU | PC_EPI_RELU)) {
-    if (pre) {
+    if (stage_pre) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) pre[i] = v[i];
     } else {
@@ -174,7 +185,7 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
   }
   if (fl & (PC_EPI_RESIDUAL | PC_EPI_GELU_GRAD | PC_EPI_RELU_GRAD)) {
     float a[16];
-    if (aux_pre) {
+    if (have_aux) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) a[i] = aux_pre[i];
     } else {
@@ -497,7 +508,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint32_t r[32];
         tmem_ld16(tb + cc, r);
         tmem_ld16(tb + cc + 16, r + 16);
-        float xa[32];
+        // aux input (TMA box) and staged pre-activation are never both used:
+        // one register array serves either role
+        float xu[32];
         if (tma_x) {
           uint8_t* xstg = stg + 2048;  // aux box (bf16 32x32, 64B swizzle)
           mbar_wait(xb, xphase);
@@ -509,8 +522,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float2 f2 = __bfloat1622float2(hx[k]);
-              xa[8 * j + 2 * k] = f2.x;
-              xa[8 * j + 2 * k + 1] = f2.y;
+              xu[8 * j + 2 * k] = f2.x;
+              xu[8 * j + 2 * k + 1] = f2.y;
             }
           }
           __syncwarp();
@@ -522,13 +535,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_wait_ld();
         if (last) release_acc<CG>(rel, lane);
         float* v = reinterpret_cast<float*>(r);
-        float pre[32];
         if (row < M) {
           if (n0 + cc < N)
-            epilogue16(ep, row, n0 + cc, v, !tma, stage_u ? pre : nullptr, tma_x ? xa : nullptr);
+            epilogue16(ep, row, n0 + cc, v, !tma, stage_u, xu, tma_x, xu);
           if (n0 + cc + 16 < N)
-            epilogue16(ep, row, n0 + cc + 16, v + 16, !tma, stage_u ? pre + 16 : nullptr,
-                       tma_x ? xa + 16 : nullptr);
+            epilogue16(ep, row, n0 + cc + 16, v + 16, !tma, stage_u, xu + 16, tma_x, xu + 16);
         }
         if (!tma) continue;
         if (lane == 0) bulk_wait_read1();  // the store two chunks back has read this buffer
@@ -542,7 +553,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // 32 bf16 = one 64 B row per thread, 64B-swizzled box {32 cols, 32 rows};
           // the pre-activation goes to the second half of the buffer
           stage_bf16_row32(stg, lane, v);
-          if (stage_u) stage_bf16_row32(stg + 2048, lane, pre);
+          if (stage_u) stage_bf16_row32(stg + 2048, lane, xu);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -799,19 +810,19 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   memset(&tc, 0, sizeof(tc));
   memset(&tu, 0, sizeof(tu));
   memset(&tx, 0, sizeof(tx));
+  // plain / bias-only bf16 C: 64-column epilogue chunks (128 B rows, SW128)
+  const bool cw64 = tma_c && !out_f32 && ksplit == 1 && (epi & ~PC_EPI_BIAS) == 0 &&
+                    (!(epi & PC_EPI_BIAS) || (reinterpret_cast<uintptr_t>(bias) & 15) == 0);
   if (tma_a) {
     rc = make_tmap_c(&tx, const_cast<void*>(aux), N, M, ldaux, false);
     if (rc) return rc;
   }
-  const bool cw64 = tma_c && !out_f32 && ksplit == 1 &&
-                    (epi & ~PC_EPI_BIAS) == 0 &&
-                    (!(epi & PC_EPI_BIAS) || (reinterpret_cast<uintptr_t>(bias) & 15) == 0);
-  if (tma_c) {
-    rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0, cw64);
-    if (rc) return rc;
-  }
   if (tma_u) {
     rc = make_tmap_c(&tu, aux_out, N, M, ldaux_out, false);
+    if (rc) return rc;
+  }
+  if (tma_c) {
+    rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0, cw64);
     if (rc) return rc;
   }
   TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, tma_a ? 1 : 0, cw64 ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
