@@ -72,7 +72,8 @@ int pc_gemm_set_tile_n(int bn);
  * 1 = never, 2 = whenever the tile allows it (128/256; 192 with a K-major B).  Test hook. */
 int pc_gemm_set_cta_pair(int mode);
 /* Profiling ablation of the tcgen05 GEMM (outputs are garbage while set):
- * bit0 = skip the epilogue work, bit1 = skip the operand TMA loads. */
+ * bit0 = skip the epilogue work, bit1 = skip the operand TMA loads, bit2 = skip the
+ * epilogue's aux-input TMA loads. */
 int pc_gemm_set_ablation(int bits);
 /* 1 (default) = write C through smem + TMA bulk store when legal; 0 = direct stores. Test hook. */
 int pc_gemm_set_tma_store(int on);

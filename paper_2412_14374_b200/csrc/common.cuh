@@ -88,6 +88,63 @@ __device__ __forceinline__ float gelu_tanh_grad_fast(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
 }
 
+// Paired fp32 arithmetic (FFMA2 / FADD2 on sm_100a) on two floats in a b64.
+__device__ __forceinline__ uint64_t pack_f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack_f2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// Paired GELU / GELU' on two values (same tanh form as gelu_tanh_fast /
+// gelu_tanh_grad_fast, refactored to 5 / 9 paired ops):
+//   u = x (k0 + k0 k1 x^2),  gelu = hx + hx tanh(u)  with hx = x / 2
+//   gelu' = (1 + t) / 2 + hx (1 - t^2) (k0 + 3 k0 k1 x^2)
+__device__ __forceinline__ void gelu_pair(float& a, float& b) {
+  const uint64_t x = pack_f2(a, b);
+  const uint64_t x2 = fmul2(x, x);
+  const uint64_t u = fmul2(x, ffma2(x2, pack_f2(0.0356774081f, 0.0356774081f),
+                                    pack_f2(0.7978845608f, 0.7978845608f)));
+  float u0, u1;
+  unpack_f2(u, u0, u1);
+  const uint64_t t = pack_f2(tanh_fast(u0), tanh_fast(u1));
+  const uint64_t hx = fmul2(x, pack_f2(0.5f, 0.5f));
+  unpack_f2(ffma2(hx, t, hx), a, b);
+}
+// (a, b) *= gelu'(x0, x1)
+__device__ __forceinline__ void mul_gelu_grad_pair(float& a, float& b, float x0, float x1) {
+  const uint64_t x = pack_f2(x0, x1);
+  const uint64_t x2 = fmul2(x, x);
+  const uint64_t u = fmul2(x, ffma2(x2, pack_f2(0.0356774081f, 0.0356774081f),
+                                    pack_f2(0.7978845608f, 0.7978845608f)));
+  float u0, u1;
+  unpack_f2(u, u0, u1);
+  const uint64_t t = pack_f2(tanh_fast(u0), tanh_fast(u1));
+  const uint64_t hx = fmul2(x, pack_f2(0.5f, 0.5f));
+  const uint64_t s = ffma2(t, pack_f2(-1.f, -1.f) , pack_f2(0.f, 0.f));      // -t
+  const uint64_t om = ffma2(s, t, pack_f2(1.f, 1.f));                         // 1 - t^2
+  const uint64_t da = ffma2(x2, pack_f2(0.1070322243f, 0.1070322243f),
+                            pack_f2(0.7978845608f, 0.7978845608f));          // k0 + 3 k0 k1 x^2
+  const uint64_t g = ffma2(fmul2(hx, om), da, ffma2(t, pack_f2(0.5f, 0.5f), pack_f2(0.5f, 0.5f)));
+  unpack_f2(fmul2(pack_f2(a, b), g), a, b);
+}
+
 // TMA bulk tensor store (smem -> global) and its bulk-group bookkeeping.
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int x, int y) {
   asm volatile(

@@ -27,9 +27,12 @@ namespace {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int TC_THREADS = 384;  // 4 control warps + 8 epilogue warps
-constexpr int TC_EPI_WARPS = 8;
-constexpr int TC_STAGE_BYTES = 8192;  // per epilogue warp: two 4 KB staging buffers
+// Epilogue: TC_EPI_G warps per TMEM lane quarter, each with TC_EPI_BUFS 4 KB
+// staging buffers (a ring when 2: the store of chunk i drains while i+1 stages)
+constexpr int TC_EPI_G = 2, TC_EPI_BUFS = 2;
+constexpr int TC_EPI_WARPS = 4 * TC_EPI_G;
+constexpr int TC_THREADS = 128 + 32 * TC_EPI_WARPS;  // 4 control warps + epilogue warps
+constexpr int TC_STAGE_BYTES = 4096 * TC_EPI_BUFS;
 constexpr int TC_SMEM_MAX = 232448;   // 227 KB opt-in dynamic smem per block
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_MN_CHUNK_BYTES = TC_BK * 128;  // one 64-wide MN box of BK rows
@@ -59,9 +62,9 @@ struct TcCfg {
   static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
   static constexpr int STAGE_BYTES = TC_A_BYTES + B_BYTES;
   static constexpr int STAGES =
-      (TC_SMEM_MAX - TC_EPI_WARPS * TC_STAGE_BYTES - 1024 - 256) / STAGE_BYTES;
+      (TC_SMEM_MAX - TC_EPI_WARPS * TC_STAGE_BYTES - 1024 - 512) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + TC_EPI_WARPS * TC_STAGE_BYTES +
-                               1024 /*align*/ + 256 /*barriers*/;
+                               1024 /*align*/ + 512 /*barriers*/;
   // two accumulators of BN fp32 columns, rounded up to a legal power-of-2 allocation
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
@@ -177,7 +180,7 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
     }
     if (fl & PC_EPI_GELU) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = gelu_tanh_fast(v[i]);
+      for (int i = 0; i < 16; i += 2) gelu_pair(v[i], v[i + 1]);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
@@ -196,7 +199,7 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
       for (int i = 0; i < 16; ++i) v[i] += a[i];
     } else if (fl & PC_EPI_GELU_GRAD) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] *= gelu_tanh_grad_fast(a[i]);
+      for (int i = 0; i < 16; i += 2) mul_gelu_grad_pair(v[i], v[i + 1], a[i], a[i + 1]);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = a[i] > 0.f ? v[i] : 0.f;
@@ -224,6 +227,49 @@ __device__ __forceinline__ void stage_bf16_row32(uint8_t* stg, int r, const floa
   }
 }
 
+// Epilogue kinds, one kernel instantiation each so that every kernel carries
+// only its own epilogue code (the MMA and producer warps share the SM's
+// instruction cache with it):
+//   EK_PLAIN    bf16 C (+ bias), 64-column chunks
+//   EK_ACT      bf16 C = act(acc + bias) and the pre-activation U, 64-column chunks
+//   EK_AUX      bf16 C = (acc + bias) op aux with aux read as TMA boxes, 64-column chunks
+//   EK_GENERIC  everything else (fp32 C, split-K, accumulate, direct stores), 32 columns
+constexpr int EK_PLAIN = 0, EK_ACT = 1, EK_AUX = 2, EK_GENERIC = 3;
+
+// v[0..63] += bias[col..col+63] (columns >= N get nothing)
+__device__ __forceinline__ void add_bias64(float* v, const float* bias, int col, int N) {
+  const float* bp = bias + col;
+  if (col + 64 <= N) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float4 b4 = reinterpret_cast<const float4*>(bp)[i];
+      v[4 * i] += b4.x; v[4 * i + 1] += b4.y; v[4 * i + 2] += b4.z; v[4 * i + 3] += b4.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] += col + i < N ? bp[i] : 0.f;
+  }
+}
+// 64 fp32 -> bf16, one 128 B row of a 128B-swizzled [32 x 128 B] staging tile
+__device__ __forceinline__ void stage_bf16_row64(uint8_t* stg, int r, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint4 w;
+    __nv_bfloat162* hw = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hw[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+    *stage_chunk(stg, r, j) = w;
+  }
+}
+
+// Before restaging a buffer: the bulk store that last read it has finished.
+__device__ __forceinline__ void bulk_wait_read_ring() {
+  if constexpr (TC_EPI_BUFS == 2)
+    bulk_wait_read1();
+  else
+    bulk_wait_read0();
+}
+
 // Epilogue warp hands a drained TMEM accumulator back to the (leader's) MMA warp.
 template <int CG>
 __device__ __forceinline__ void release_acc(uint64_t* bar, int lane) {
@@ -237,7 +283,7 @@ __device__ __forceinline__ void release_acc(uint64_t* bar, int lane) {
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int CG>
+template <int BN, bool A_MN, bool B_MN, int CG, int EK>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmU,
@@ -423,8 +469,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // 8 epilogue warps: warp & 3 selects the TMEM lane quarter (rows), the
     // warp-group half selects which half of the tile's columns it drains.
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
-    constexpr int HALF = BN / 2;
+    const int grp = (warp - 4) >> 2;  // column group within the lane quarter
     // per-warp ring of two 4 KB staging buffers: the TMA store of chunk i
     // drains while chunk i+1 is staged; a buffer is rewritten only after the
     // store two chunks back has finished reading it.
@@ -432,14 +477,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool f32 = ep.out_f32 != 0;
     const bool tma = ep.tma_c != 0;
     const bool tma_x = ep.tma_a != 0;
+    const bool skip_x = (ep.flags & (1 << 18)) != 0;  // profiling ablation: aux never loaded
     const bool stage_u = ep.tma_u != 0;
-    // plain bf16 C: 64-column chunks staged as full 128 B rows (SW128 boxes),
-    // dealt round-robin to the two warp groups; otherwise 32-column chunks of
-    // each group's half of the tile
-    const bool wide = ep.cw64 != 0;
-    const int cstart = wide ? half * 64 : half * HALF;
-    const int cstep = wide ? 128 : 32;
-    const int cstop = wide ? BN : half * HALF + HALF;
+    // chunks (64 columns as full 128 B rows for the specialised kinds, 32 for
+    // the generic one) dealt round-robin to the warp groups of a lane quarter
+    constexpr bool wide = EK != EK_GENERIC;
+    constexpr int CW = wide ? 64 : 32;
+    const int cstart = grp * CW;
+    constexpr int cstep = CW * TC_EPI_G;
+    const int cstop = BN;
     uint64_t* xb = &xbar[warp - 4];
     uint32_t xphase = 0;
     uint32_t nchunk = 0;
@@ -457,54 +503,152 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
       // the accumulator goes back to the MMA warp as soon as it is in registers
       uint64_t* rel = &tempty[acc];
-      if (tma_x && lane == 0 && cend > cstart) {  // prefetch the first aux box of this tile
-        mbar_expect_tx(xb, 2048);
-        tma_load_2d(stg0 + (nchunk & 1) * 4096 + 2048, &tmX, xb, n0 + cstart, m0 + q * 32);
+      if (tma_x && !skip_x && lane == 0 && cend > cstart) {  // prefetch the first aux box of this tile
+        if constexpr (EK == EK_AUX) {
+          if (nchunk == 0) {  // later tiles: prefetched by the previous tile's last chunk
+            mbar_expect_tx(xb, 4096);
+            tma_load_2d(stg0, &tmX, xb, n0 + cstart, m0 + q * 32);
+          }
+        } else {
+          mbar_expect_tx(xb, 2048);
+          tma_load_2d(stg0 + (TC_EPI_BUFS == 2 ? (nchunk & 1) * 4096 : 0) + 2048, &tmX, xb, n0 + cstart,
+                      m0 + q * 32);
+        }
       }
+      if constexpr (EK == EK_PLAIN) {
 #pragma unroll 1
-      for (int cc = cstart; cc < cend; cc += cstep) {
-        const uint32_t my = nchunk++;
-        uint8_t* stg = stg0 + (my & 1) * 4096;
-        const bool last = cc + cstep >= cend;
-        if (wide) {
+        for (int cc = cstart; cc < cend; cc += cstep) {
+          const uint32_t my = nchunk++;
+          uint8_t* stg = stg0 + (TC_EPI_BUFS == 2 ? (my & 1) * 4096 : 0);
           uint32_t r[64];
 #pragma unroll
           for (int h = 0; h < 4; ++h) tmem_ld16(tb + cc + 16 * h, r + 16 * h);
           tc_wait_ld();
-          if (last) release_acc<CG>(rel, lane);
+          if (cc + cstep >= cend) release_acc<CG>(rel, lane);
           float* v = reinterpret_cast<float*>(r);
-          if (ep.flags & PC_EPI_BIAS) {  // the only epilogue on this path
-            const float* bp = ep.bias + n0 + cc;
-            if (n0 + cc + 64 <= N) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float4 b4 = reinterpret_cast<const float4*>(bp)[i];
-                v[4 * i] += b4.x; v[4 * i + 1] += b4.y; v[4 * i + 2] += b4.z; v[4 * i + 3] += b4.w;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 64; ++i) v[i] += n0 + cc + i < N ? bp[i] : 0.f;
-            }
-          }
-          if (lane == 0) bulk_wait_read1();
+          if (ep.flags & PC_EPI_BIAS) add_bias64(v, ep.bias, n0 + cc, N);
+          if (lane == 0) bulk_wait_read_ring();
           __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint4 w;
-            __nv_bfloat162* hw = reinterpret_cast<__nv_bfloat162*>(&w);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              hw[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
-            *stage_chunk(stg, lane, j) = w;
-          }
+          stage_bf16_row64(stg, lane, v);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
             bulk_commit();
           }
-          continue;
         }
+      } else if constexpr (EK == EK_ACT) {
+        // U (pre-activation) staged in buffer B, C in buffer A, one bulk group
+        // each: before restaging either, the group two back has been read
+        uint8_t* sA = stg0;
+        uint8_t* sB = stg0 + 4096;
+        const bool gelu = (ep.flags & PC_EPI_GELU) != 0;
+#pragma unroll 1
+        for (int cc = cstart; cc < cend; cc += cstep) {
+          uint32_t r[64];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) tmem_ld16(tb + cc + 16 * h, r + 16 * h);
+          tc_wait_ld();
+          if (cc + cstep >= cend) release_acc<CG>(rel, lane);
+          float* v = reinterpret_cast<float*>(r);
+          if (ep.flags & PC_EPI_BIAS) add_bias64(v, ep.bias, n0 + cc, N);
+          if (lane == 0) bulk_wait_read1();
+          __syncwarp();
+          stage_bf16_row64(sB, lane, v);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmU, sB, n0 + cc, m0 + q * 32);
+            bulk_commit();
+          }
+          if (gelu) {
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) gelu_pair(v[i], v[i + 1]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+          if (lane == 0) bulk_wait_read1();
+          __syncwarp();
+          stage_bf16_row64(sA, lane, v);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, sA, n0 + cc, m0 + q * 32);
+            bulk_commit();
+          }
+        }
+      } else if constexpr (EK == EK_AUX) {
+        // Buffers alternate per chunk: chunk i finds its aux box in X = buf[i&1],
+        // consumes it, then stages C(i) in X.  Before computing, it requests the
+        // next box (rest of this tile, else the first box of this warp's next
+        // tile) into the other buffer, once C(i-1) has left it.
+        const int op = (ep.flags & PC_EPI_RESIDUAL) ? 0 : ((ep.flags & PC_EPI_GELU_GRAD) ? 1 : 2);
+#pragma unroll 1
+        for (int cc = cstart; cc < cend; cc += cstep) {
+          const uint32_t my = nchunk++;
+          uint8_t* X = stg0 + (my & 1) * 4096;
+          uint8_t* Y = stg0 + ((my + 1) & 1) * 4096;
+          const bool last = cc + cstep >= cend;
+          int nx_n = -1, nx_m = 0;
+          if (!last) {
+            nx_n = n0 + cc + cstep;
+            nx_m = m0 + q * 32;
+          } else if (u + ncl < num_units) {
+            const int t2 = (u + ncl) % num_tiles;
+            nx_n = (t2 / num_m) * BN + cstart;
+            nx_m = (t2 % num_m) * TC_BM * CG + static_cast<int>(rank) * TC_BM + q * 32;
+          }
+          uint32_t r[64];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) tmem_ld16(tb + cc + 16 * h, r + 16 * h);
+          if (!skip_x) mbar_wait(xb, xphase);  // aux(i) has landed in X
+          xphase ^= 1;
+          if (lane == 0) bulk_wait_read0();  // C(i-1) has left Y
+          __syncwarp();
+          if (lane == 0 && nx_n >= 0 && !skip_x) {
+            mbar_expect_tx(xb, 4096);
+            tma_load_2d(Y, &tmX, xb, nx_n, nx_m);
+          }
+          tc_wait_ld();
+          if (last) release_acc<CG>(rel, lane);
+          float* v = reinterpret_cast<float*>(r);
+          if (ep.flags & PC_EPI_BIAS) add_bias64(v, ep.bias, n0 + cc, N);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 w = *stage_chunk(X, lane, j);
+            const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 a2 = __bfloat1622float2(hx[k]);
+              float& v0 = v[8 * j + 2 * k];
+              float& v1 = v[8 * j + 2 * k + 1];
+              if (op == 0) {
+                v0 += a2.x;
+                v1 += a2.y;
+              } else if (op == 1) {
+                mul_gelu_grad_pair(v0, v1, a2.x, a2.y);
+              } else {
+                v0 = a2.x > 0.f ? v0 : 0.f;
+                v1 = a2.y > 0.f ? v1 : 0.f;
+              }
+            }
+          }
+          __syncwarp();  // every lane has read X
+          stage_bf16_row64(X, lane, v);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, X, n0 + cc, m0 + q * 32);
+            bulk_commit();
+          }
+        }
+      } else {
+#pragma unroll 1
+      for (int cc = cstart; cc < cend; cc += cstep) {
+        const uint32_t my = nchunk++;
+        uint8_t* stg = stg0 + (TC_EPI_BUFS == 2 ? (my & 1) * 4096 : 0);
+        const bool last = cc + cstep >= cend;
         uint32_t r[32];
         tmem_ld16(tb + cc, r);
         tmem_ld16(tb + cc + 16, r + 16);
@@ -513,7 +657,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         float xu[32];
         if (tma_x) {
           uint8_t* xstg = stg + 2048;  // aux box (bf16 32x32, 64B swizzle)
-          mbar_wait(xb, xphase);
+          if (!skip_x) mbar_wait(xb, xphase);
           xphase ^= 1;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -527,9 +671,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
           __syncwarp();
-          if (lane == 0 && !last) {  // prefetch the next chunk's box into the other buffer
+          if (lane == 0 && !last && !skip_x) {  // prefetch the next chunk's box into the other buffer
             mbar_expect_tx(xb, 2048);
-            tma_load_2d(stg0 + ((my + 1) & 1) * 4096 + 2048, &tmX, xb, n0 + cc + 32, m0 + q * 32);
+            tma_load_2d(stg0 + (TC_EPI_BUFS == 2 ? ((my + 1) & 1) * 4096 : 0) + 2048, &tmX, xb,
+                        n0 + cc + cstep, m0 + q * 32);
           }
         }
         tc_wait_ld();
@@ -542,7 +687,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             epilogue16(ep, row, n0 + cc + 16, v + 16, !tma, stage_u, xu + 16, tma_x, xu + 16);
         }
         if (!tma) continue;
-        if (lane == 0) bulk_wait_read1();  // the store two chunks back has read this buffer
+        if (lane == 0) bulk_wait_read_ring();  // the store that last used this buffer has read it
         __syncwarp();
         if (f32) {
           // 32 fp32 = one 128 B row per thread, 128B-swizzled box {32 cols, 32 rows}
@@ -565,6 +710,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (stage_u) tma_store_2d(&tmU, stg + 2048, n0 + cc, m0 + q * 32);
           bulk_commit();
         }
+      }
       }
       if (cend <= cstart) release_acc<CG>(rel, lane);
       acc ^= 1;
@@ -656,12 +802,12 @@ int g_tma_store = 1;
 int g_cta_pair = 0;  // 0 auto, 1 never, 2 always (where the tile allows it)
 int g_ablate = 0;    // profiling: bit0 skip epilogue work, bit1 skip operand loads
 
-template <int BN, bool A_MN, bool B_MN, int CG>
+template <int BN, bool A_MN, bool B_MN, int CG, int EK>
 int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
               const CUtensorMap& tu, const CUtensorMap& tx, int M, int N, int K, const TcEpi& ep,
               cudaStream_t st) {
   using Cfg = TcCfg<BN, CG>;
-  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG>;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG, EK>;
   static int max_units = 0;  // benign race: idempotent attribute write / query
   if (!max_units) {
     PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
@@ -707,8 +853,22 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
   return check_launch("tc_gemm_kernel");
 }
 
+// A_MN is only ever used by weight gradients (fp32 C): generic epilogue only.
+template <int BN, int CG, bool B_MN>
+int dispatch_ek(bool a_mn, int ek, const CUtensorMap& ta, const CUtensorMap& tb,
+                const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, int M, int N,
+                int K, const TcEpi& ep, cudaStream_t st) {
+  if (a_mn) return launch_tc<BN, true, B_MN, CG, EK_GENERIC>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  switch (ek) {
+    case EK_PLAIN: return launch_tc<BN, false, B_MN, CG, EK_PLAIN>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+    case EK_ACT: return launch_tc<BN, false, B_MN, CG, EK_ACT>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+    case EK_AUX: return launch_tc<BN, false, B_MN, CG, EK_AUX>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+    default: return launch_tc<BN, false, B_MN, CG, EK_GENERIC>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  }
+}
+
 template <int BN, int CG>
-int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+int dispatch_majors(bool a_mn, bool b_mn, int ek, const CUtensorMap& ta, const CUtensorMap& tb,
                     const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, int M,
                     int N, int K, const TcEpi& ep, cudaStream_t st) {
   if constexpr ((BN / CG) % 64 != 0) {  // MN-major B needs 64-wide chunks per CTA
@@ -716,13 +876,10 @@ int dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorM
       set_error("gemm: tile %d x cta_group %d needs a K-major B", BN, CG);
       return PC_ERR_ARG;
     }
-    if (!a_mn) return launch_tc<BN, false, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-    return launch_tc<BN, true, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+    return dispatch_ek<BN, CG, false>(a_mn, ek, ta, tb, tc, tu, tx, M, N, K, ep, st);
   } else {
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-  if (!a_mn && b_mn) return launch_tc<BN, false, true, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-  if (a_mn && !b_mn) return launch_tc<BN, true, false, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-  return launch_tc<BN, true, true, CG>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+    if (b_mn) return dispatch_ek<BN, CG, true>(a_mn, ek, ta, tb, tc, tu, tx, M, N, K, ep, st);
+    return dispatch_ek<BN, CG, false>(a_mn, ek, ta, tb, tc, tu, tx, M, N, K, ep, st);
   }
 }
 
@@ -810,15 +967,27 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   memset(&tc, 0, sizeof(tc));
   memset(&tu, 0, sizeof(tu));
   memset(&tx, 0, sizeof(tx));
-  // plain / bias-only bf16 C: 64-column epilogue chunks (128 B rows, SW128)
-  const bool cw64 = tma_c && !out_f32 && ksplit == 1 && (epi & ~PC_EPI_BIAS) == 0 &&
-                    (!(epi & PC_EPI_BIAS) || (reinterpret_cast<uintptr_t>(bias) & 15) == 0);
+  // epilogue kind: the specialised 64-column kinds need bf16 C through TMA, no
+  // split / accumulate, a 16 B aligned bias, and U / aux through TMA as well
+  const bool bias_ok = !(epi & PC_EPI_BIAS) || (reinterpret_cast<uintptr_t>(bias) & 15) == 0;
+  const bool spec = tma_c && !out_f32 && ksplit == 1 && bias_ok && !a_mn;
+  const int aux_ops = epi & (PC_EPI_RESIDUAL | PC_EPI_GELU_GRAD | PC_EPI_RELU_GRAD);
+  int ek = EK_GENERIC;
+  if (spec && (epi & ~PC_EPI_BIAS) == 0)
+    ek = EK_PLAIN;
+  else if (spec && tma_u && (epi & ~(PC_EPI_BIAS | PC_EPI_GELU | PC_EPI_RELU)) == 0 &&
+           (epi & (PC_EPI_GELU | PC_EPI_RELU)) != (PC_EPI_GELU | PC_EPI_RELU))
+    ek = EK_ACT;
+  else if (spec && tma_a && (epi & ~(PC_EPI_BIAS | aux_ops)) == 0 &&
+           (aux_ops == PC_EPI_RESIDUAL || aux_ops == PC_EPI_GELU_GRAD || aux_ops == PC_EPI_RELU_GRAD))
+    ek = EK_AUX;
+  const bool cw64 = ek != EK_GENERIC;
   if (tma_a) {
-    rc = make_tmap_c(&tx, const_cast<void*>(aux), N, M, ldaux, false);
+    rc = make_tmap_c(&tx, const_cast<void*>(aux), N, M, ldaux, false, cw64);
     if (rc) return rc;
   }
   if (tma_u) {
-    rc = make_tmap_c(&tu, aux_out, N, M, ldaux_out, false);
+    rc = make_tmap_c(&tu, aux_out, N, M, ldaux_out, false, cw64);
     if (rc) return rc;
   }
   if (tma_c) {
@@ -829,13 +998,13 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
            aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi | (g_ablate << 16), out_f32};
   const int iM = static_cast<int>(M), iN = static_cast<int>(N), iK = static_cast<int>(K);
   switch (bn * 4 + cg) {
-    case 256 * 4 + 2: return dispatch_majors<256, 2>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 192 * 4 + 2: return dispatch_majors<192, 2>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 128 * 4 + 2: return dispatch_majors<128, 2>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 256 * 4 + 1: return dispatch_majors<256, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 192 * 4 + 1: return dispatch_majors<192, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 128 * 4 + 1: return dispatch_majors<128, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 64 * 4 + 1: return dispatch_majors<64, 1>(a_mn, b_mn, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 256 * 4 + 2: return dispatch_majors<256, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 192 * 4 + 2: return dispatch_majors<192, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 128 * 4 + 2: return dispatch_majors<128, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 256 * 4 + 1: return dispatch_majors<256, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 192 * 4 + 1: return dispatch_majors<192, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 128 * 4 + 1: return dispatch_majors<128, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 64 * 4 + 1: return dispatch_majors<64, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
     default: set_error("gemm: bad tile %d x cta_group %d", bn, cg); return PC_ERR_ARG;
   }
 }
@@ -863,7 +1032,7 @@ extern "C" int pc_gemm_set_cta_pair(int mode) {
 // Profiling ablation (results are garbage while set): bit0 = skip the epilogue
 // work, bit1 = skip the operand TMA loads.
 extern "C" int pc_gemm_set_ablation(int bits) {
-  pp200::g_ablate = bits & 3;
+  pp200::g_ablate = bits & 7;
   return PC_OK;
 }
 

@@ -42,11 +42,11 @@ for name, M, N, K, ta, tb, epi, has_aux, has_u in cases:
                   aux.data_ptr() if aux is not None else None, N,
                   U.data_ptr() if U is not None else None, N, st)
     out = []
-    for ab in (0, 1):
+    for ab in (0, 1, 4):
         _lib.call("pc_gemm_set_ablation", ab)
         out.append((bench(lambda: run(epi)), bench(lambda: run(0))))
     _lib.call("pc_gemm_set_ablation", 0)
     fl = 2.0 * M * N * K
-    (fe, fp), (ne, np_) = out
+    (fe, fp), (ne, np_), (xe, _) = out
     print(f"{name:22s} fused {fe:6.1f} us ({fl / fe / 1e6:5.0f} TF/s)  plain {fp:6.1f} us  "
-          f"| no-epi: fused {ne:6.1f}  plain {np_:6.1f}", flush=True)
+          f"| no-epi: fused {ne:6.1f}  plain {np_:6.1f} | no aux loads: fused {xe:6.1f}", flush=True)
