@@ -321,6 +321,28 @@ __global__ void copy2d_kernel(int64_t rows, int64_t cols, const T* __restrict__ 
   }
 }
 
+// dst[r, c] = src[c, r] through 32 x 32 shared-memory tiles: coalesced reads
+// and writes (the naive copy2d transpose strides one side).
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_tiled_kernel(int64_t rows, int64_t cols,
+                                                              const T* __restrict__ src, int64_t lds,
+                                                              T* __restrict__ dst, int64_t ldd) {
+  __shared__ T tile[32][33];
+  const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;  // dst tile origin
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;    // 32 x 8 threads
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {  // src rows c0.., src cols r0..
+    const int64_t sr = c0 + ty + k, sc = r0 + tx;
+    if (sr < cols && sc < rows) tile[ty + k][tx] = src[sr * lds + sc];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t dr = r0 + ty + k, dc = c0 + tx;
+    if (dr < rows && dc < cols) dst[dr * ldd + dc] = tile[tx][ty + k];
+  }
+}
+
 // acc[i] += part[i]; acc fp32/fp64, part same or bf16.  Vectorised for fp32.
 template <typename A, typename P>
 __global__ void accumulate_kernel(int64_t n, A* __restrict__ acc, const P* __restrict__ part) {
@@ -488,6 +510,11 @@ extern "C" int pc_copy2d(int dtype, int64_t rows, int64_t cols, const void* src,
   if (dtype == PC_I32) {
     copy2d_kernel<int32_t><<<grid_for(rows * cols, 256), 256, 0, st>>>(rows, cols, static_cast<const int32_t*>(src), lds, trans, static_cast<int32_t*>(dst), ldd);
     return check_launch("copy2d");
+  }
+  if (trans) {
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    PP_DISPATCH3(dtype, T, transpose_tiled_kernel<T><<<grid, 256, 0, st>>>(rows, cols, static_cast<const T*>(src), lds, static_cast<T*>(dst), ldd));
+    return check_launch("transpose");
   }
   PP_DISPATCH3(dtype, T, copy2d_kernel<T><<<grid_for(rows * cols, 256), 256, 0, st>>>(rows, cols, static_cast<const T*>(src), lds, trans, static_cast<T*>(dst), ldd));
   return check_launch("copy2d");

@@ -85,6 +85,11 @@ class Param:
 
     master: torch.Tensor
     shadow: torch.Tensor | None = None
+    # bf16 shadow with each GPT block matrix stored transposed (same flat
+    # offsets), built lazily once per step (DeviceOps.step_epoch) for the
+    # data-gradient GEMMs
+    shadow_t: torch.Tensor | None = None
+    shadow_t_epoch: int = -1
 
     def compute(self) -> torch.Tensor:
         return self.shadow if self.shadow is not None else self.master
@@ -139,6 +144,7 @@ class DeviceOps:
             self._blay = {False: gpt.block_layout(False), True: gpt.block_layout(True)}
         self._emb_ws = None
         self._red = None
+        self.step_epoch = 0  # bumped by the executor at every step
 
     # ------------------------------------------------------------------ alloc
     def red_ws(self, rows: int, cols: int) -> tuple[int, int]:
@@ -394,6 +400,25 @@ class DeviceOps:
         off, dims = layout[name]
         return flat[off:off + math.prod(dims)].view(*dims)
 
+    _BLOCK_MATS = ("w_qkv", "w_o", "w_fc1", "w_fc2")
+
+    def _shadow_t(self, w: "Param", lay) -> torch.Tensor:
+        """Transposed bf16 copies of the block matrices (W^T at W's offset), so
+        the dX GEMMs read B K-major and can use the CTA-pair tiles.  Cached on
+        the Param: one set of transposes per block per step."""
+        if w.shadow_t is None or w.shadow_t_epoch != self.step_epoch:
+            wt = self.empty(w.shadow.shape, torch.bfloat16)
+            for name in self._BLOCK_MATS:
+                off, (r, c) = lay[name]
+                call("pc_copy2d", _lib.PC_BF16, c, r, w.shadow[off:].data_ptr(), c, 1,
+                     wt[off:].data_ptr(), r, self.st)
+            w.shadow_t, w.shadow_t_epoch = wt, self.step_epoch
+        return w.shadow_t
+
+    def _slice_t(self, flat: torch.Tensor, layout, name):
+        off, (r, c) = layout[name]
+        return flat[off:off + r * c].view(c, r)
+
     def _gemm(self, out_dtype, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, epi=0, bias=None,
               aux=None, ldaux=0, aux_out=None, ldaux_out=0):
         call("pc_gemm", self.mode.pc_act, _PC[out_dtype], ta, tb, M, N, K, A.data_ptr(), lda,
@@ -503,6 +528,13 @@ class DeviceOps:
         f32 = torch.float32
         sl = lambda name: self._slice(W, lay, name)
         ms = lambda name: self._slice(Mst, lay, name)
+        # dX GEMMs: B = W^T read K-major from the transposed shadow (bf16 mode),
+        # else W read MN-major
+        if w.shadow is not None:
+            Wt = self._shadow_t(w, lay)
+            wB = lambda name: (1, self._slice_t(Wt, lay, name), lay[name][1][0])
+        else:
+            wB = lambda name: (0, sl(name), lay[name][1][1])
         dW = self.zeros((layout_size(lay),), f32)
         gs = lambda name: self._slice(dW, lay, name)
         if final:
@@ -517,13 +549,15 @@ class DeviceOps:
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dout.data_ptr(), d,
              gs("b_fc2").data_ptr(), 0, *self.red_ws(T, d), self.st)
         du = self.empty((T, f), act)
-        self._gemm(act, 0, 0, T, f, d, dout, d, sl("w_fc2"), f, du, f, _lib.EPI_GELU_GRAD,
+        tb, B, ldb = wB("w_fc2")
+        self._gemm(act, 0, tb, T, f, d, dout, d, B, ldb, du, f, _lib.EPI_GELU_GRAD,
                    aux=sv["u"], ldaux=f)
         self._gemm(f32, 1, 0, f, d, T, du, f, sv["a2"], d, gs("w_fc1"), d, _lib.EPI_SPLITK_ZERO_C)
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, f, du.data_ptr(), f,
              gs("b_fc1").data_ptr(), 0, *self.red_ws(T, f), self.st)
         da2 = self.empty((T, d), act)
-        self._gemm(act, 0, 0, T, d, f, du, f, sl("w_fc1"), d, da2, d)
+        tb, B, ldb = wB("w_fc1")
+        self._gemm(act, 0, tb, T, d, f, du, f, B, ldb, da2, d)
         dh1 = self.empty((T, d), act)
         call("pc_layernorm_bwd", self.mode.pc_act, T, d, da2.data_ptr(), sv["h1"].data_ptr(),
              ms("ln2_g").data_ptr(), sv["mean2"].data_ptr(), sv["rstd2"].data_ptr(),
@@ -534,7 +568,8 @@ class DeviceOps:
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dh1.data_ptr(), d,
              gs("b_o").data_ptr(), 0, *self.red_ws(T, d), self.st)
         do = self.empty((T, d), act)
-        self._gemm(act, 0, 0, T, d, d, dh1, d, sl("w_o"), d, do, d)
+        tb, B, ldb = wB("w_o")
+        self._gemm(act, 0, tb, T, d, d, dh1, d, B, ldb, do, d)
         dqkv = self.empty((T, 3 * d), act)
         delta = self.empty((cfg.microbatch_size * H * cfg.seq_len,), f32)
         call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
@@ -544,7 +579,8 @@ class DeviceOps:
         call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, 3 * d, dqkv.data_ptr(), 3 * d,
              gs("b_qkv").data_ptr(), 0, *self.red_ws(T, 3 * d), self.st)
         da = self.empty((T, d), act)
-        self._gemm(act, 0, 0, T, d, 3 * d, dqkv, 3 * d, sl("w_qkv"), d, da, d)
+        tb, B, ldb = wB("w_qkv")
+        self._gemm(act, 0, tb, T, d, 3 * d, dqkv, 3 * d, B, ldb, da, d)
         dh = self.empty((T, d), act)
         call("pc_layernorm_bwd", self.mode.pc_act, T, d, da.data_ptr(), h.data_ptr(),
              ms("ln1_g").data_ptr(), sv["mean1"].data_ptr(), sv["rstd1"].data_ptr(),

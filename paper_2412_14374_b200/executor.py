@@ -646,6 +646,8 @@ class PipelineEngine:
         tokens = p.graph.producer(x_in).attr_or("token_ids", 0) == 1
         mbs = split_batch(batch, M)
         is_gpt = self.gpt is not None
+        for act in actors.values():  # per-step caches on parameters start over
+            act.ops.step_epoch += 1
         for bid, buf in tg.buffers.items():
             if buf.producer is not None or buf.home not in actors:
                 continue
