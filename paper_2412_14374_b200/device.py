@@ -402,13 +402,13 @@ class DeviceOps:
 
     _BLOCK_MATS = ("w_qkv", "w_o", "w_fc1", "w_fc2")
 
-    def _shadow_t(self, w: "Param", lay) -> torch.Tensor:
+    def _shadow_t(self, w: "Param", lay, names=_BLOCK_MATS) -> torch.Tensor:
         """Transposed bf16 copies of the block matrices (W^T at W's offset), so
         the dX GEMMs read B K-major and can use the CTA-pair tiles.  Cached on
         the Param: one set of transposes per block per step."""
         if w.shadow_t is None or w.shadow_t_epoch != self.step_epoch:
             wt = self.empty(w.shadow.shape, torch.bfloat16)
-            for name in self._BLOCK_MATS:
+            for name in names:
                 off, (r, c) = lay[name]
                 call("pc_copy2d", _lib.PC_BF16, c, r, w.shadow[off:].data_ptr(), c, 1,
                      wt[off:].data_ptr(), r, self.st)
@@ -616,8 +616,13 @@ class DeviceOps:
         w0: Param = env[op.operands[1]]
         T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
         dh = self.empty((T, d), self.mode.act)
-        wte = self._slice(w0.compute(), self._elay, "wte")
-        self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V, wte, d, dh, d)
+        if w0.shadow is not None:  # B = wte^T, K-major, from the transposed shadow
+            wt = self._shadow_t(w0, self._elay, ("wte",))
+            self._gemm(self.mode.act, 0, 1, T, d, V, dlogits, V,
+                       self._slice_t(wt, self._elay, "wte"), V, dh, d)
+        else:
+            wte = self._slice(w0.compute(), self._elay, "wte")
+            self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V, wte, d, dh, d)
         dw = self.zeros((layout_size(self._elay),), torch.float32)
         self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
                    self._slice(dw, self._elay, "wte"), d, _lib.EPI_SPLITK_ZERO_C)
