@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(F_THREADS, 2)
 // ------------------------------------------------------------------ backward
 // NG elementwise warps per TMEM lane quarter, each owning CW = 64 / NG columns
 constexpr int BW_NG = 4, BW_CW = 64 / BW_NG;
-constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 3, BKV_EW = 4 * BW_NG, BKV_THREADS = 128 + 32 * BKV_EW;
+constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 5, BKV_EW = 4 * BW_NG, BKV_THREADS = 128 + 32 * BKV_EW;
+// score buffers (S/dP pairs of 64 + 64 TMEM columns): the MMA warp keeps the
+// score MMAs up to three blocks ahead of the elementwise warps
+constexpr int B_SBUF = 3;
 constexpr int BKV_SMEM = 2 * 16384 /*K,V*/ + BKV_STAGES * 2 * 8192 /*Q,dO*/ +
                          2 * 2 * 16384 /*P^T,dS^T x2*/ + BKV_STAGES * 512 /*lse,delta*/ + 1024 + 256;
 
@@ -345,9 +348,9 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   uint64_t* bar_kv = reinterpret_cast<uint64_t*>(sLD + BKV_STAGES * 128);
   uint64_t* q_full = bar_kv + 1;
   uint64_t* q_empty = q_full + BKV_STAGES;
-  uint64_t* s_full = q_empty + BKV_STAGES;  // [2]
-  uint64_t* s_free = s_full + 2;            // [2]
-  uint64_t* p_full = s_free + 2;            // [2]
+  uint64_t* s_full = q_empty + BKV_STAGES;  // [B_SBUF]
+  uint64_t* s_free = s_full + B_SBUF;       // [B_SBUF]
+  uint64_t* p_full = s_free + B_SBUF;       // [2]
   uint64_t* pv_done = p_full + 2;           // [2]
   uint64_t* done = pv_done + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
@@ -371,9 +374,11 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < B_SBUF; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], BKV_EW);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&p_full[i], BKV_EW);
       mbar_init(&pv_done[i], 1);
     }
@@ -385,7 +390,8 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tdV = tmem + 256, tdK = tmem + 320;  // S^T_i at tmem + 128 i, dP^T_i at + 64
+  // S^T of block i at tmem + 128 (i % B_SBUF), dP^T at + 64; then dV, dK
+  const uint32_t tdV = tmem + 128 * B_SBUF, tdK = tdV + 64;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -420,25 +426,24 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
     const uint64_t pd = umma_sdesc_sw128(smem_u32(sPt), 16, 1024);
     const uint64_t dd = umma_sdesc_sw128(smem_u32(sDt), 16, 1024);
     auto issue_s = [&](int i) {
-      const int st = i % BKV_STAGES, bf = i & 1;
+      const int st = i % BKV_STAGES, sb = i % B_SBUF;
       mbar_wait(&q_full[st], (i / BKV_STAGES) & 1);
-      if (i >= 2) mbar_wait(&s_free[bf], ((i - 2) >> 1) & 1);
+      if (i >= B_SBUF) mbar_wait(&s_free[sb], ((i - B_SBUF) / B_SBUF) & 1);
       tc_fence_after();
       const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-      const uint32_t tS = tmem + bf * 128;
+      const uint32_t tS = tmem + sb * 128;
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < F_HD / 16; ++k) {
           tc_mma_f16(tS, kd + 2 * k, qd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
           tc_mma_f16(tS + 64, vd + 2 * k, gd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
         }
-        tc_commit(&s_full[bf]);
+        tc_commit(&s_full[sb]);
       }
       __syncwarp();
     };
-    if (n > 0) issue_s(0);
+    for (int i = 0; i < B_SBUF && i < n; ++i) issue_s(i);
     for (int i = 0; i < n; ++i) {
-      if (i + 1 < n) issue_s(i + 1);
       const int st = i % BKV_STAGES, bf = i & 1;
       mbar_wait(&p_full[bf], (i >> 1) & 1);
       tc_fence_after();
@@ -455,6 +460,7 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
         tc_commit(&q_empty[st]);
       }
       __syncwarp();
+      if (i + B_SBUF < n) issue_s(i + B_SBUF);  // into the buffer block i released
     }
     if (elect_one()) tc_commit(done);
     __syncwarp();
@@ -467,18 +473,18 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
     for (int i = 0; i < n; ++i) {
-      const int st = i % BKV_STAGES, bf = i & 1;
+      const int st = i % BKV_STAGES, bf = i & 1, sb = i % B_SBUF;
       const int m0 = (qbeg + i) * B_Q;
-      mbar_wait(&s_full[bf], (i >> 1) & 1);
+      mbar_wait(&s_full[sb], (i / B_SBUF) & 1);
       tc_fence_after();
       uint32_t sr[CW], pr[CW];
-      const uint32_t tS = tmem + bf * 128 + lo + cb;
+      const uint32_t tS = tmem + sb * 128 + lo + cb;
       tmem_ld_cols<CW>(tS, sr);
       tmem_ld_cols<CW>(tS + 64, pr);
       tc_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[bf]);  // the MMA warp may refill this buffer
+      if (lane == 0) mbar_arrive(&s_free[sb]);  // the MMA warp may refill this buffer
       mbar_wait(&q_full[st], (i / BKV_STAGES) & 1);  // lse / delta rows visible
       const float* Ls = sLD + st * 128 + cb;
       const float* Ds = Ls + 64;
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-constexpr int BQ_STAGES = 3, BQ_EW = 4 * BW_NG, BQ_THREADS = 128 + 32 * BQ_EW;
+constexpr int BQ_STAGES = 5, BQ_EW = 4 * BW_NG, BQ_THREADS = 128 + 32 * BQ_EW;
 constexpr int BQ_SMEM = 3 * 16384 /*Q,dO,O*/ + BQ_STAGES * 2 * 8192 /*K,V*/ + 2 * 16384 /*dS x2*/ +
                         128 * BW_NG * 4 /*delta partials*/ + 1024 + 256;
 
@@ -580,9 +586,9 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   uint64_t* bar_q = reinterpret_cast<uint64_t*>(sDelta + 128 * BW_NG);
   uint64_t* kv_full = bar_q + 1;
   uint64_t* kv_empty = kv_full + BQ_STAGES;
-  uint64_t* s_full = kv_empty + BQ_STAGES;  // [2]
-  uint64_t* s_free = s_full + 2;            // [2]
-  uint64_t* p_full = s_free + 2;            // [2]
+  uint64_t* s_full = kv_empty + BQ_STAGES;  // [B_SBUF]
+  uint64_t* s_free = s_full + B_SBUF;       // [B_SBUF]
+  uint64_t* p_full = s_free + B_SBUF;       // [2]
   uint64_t* pv_done = p_full + 2;           // [2]
   uint64_t* done = pv_done + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
@@ -606,9 +612,11 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < B_SBUF; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], BQ_EW);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&p_full[i], BQ_EW);
       mbar_init(&pv_done[i], 1);
     }
@@ -620,7 +628,7 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tdQ = tmem + 256;  // S_j at tmem + 128 (j % 2), dP_j at + 64
+  const uint32_t tdQ = tmem + 128 * B_SBUF;  // S_j at tmem + 128 (j % B_SBUF), dP_j at + 64
 
   if (warp == 0) {
     if (lane == 0) {
@@ -650,25 +658,24 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
     const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), 8192, 1024);   // MN-major view
     const uint64_t dd = umma_sdesc_sw128(smem_u32(sD), 16, 1024);
     auto issue_s = [&](int j) {
-      const int st = j % BQ_STAGES, bf = j & 1;
+      const int st = j % BQ_STAGES, sb = j % B_SBUF;
       mbar_wait(&kv_full[st], (j / BQ_STAGES) & 1);
-      if (j >= 2) mbar_wait(&s_free[bf], ((j - 2) >> 1) & 1);
+      if (j >= B_SBUF) mbar_wait(&s_free[sb], ((j - B_SBUF) / B_SBUF) & 1);
       tc_fence_after();
       const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-      const uint32_t tS = tmem + bf * 128;
+      const uint32_t tS = tmem + sb * 128;
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < F_HD / 16; ++k) {
           tc_mma_f16(tS, qd + 2 * k, kd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
           tc_mma_f16(tS + 64, gd + 2 * k, vd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
         }
-        tc_commit(&s_full[bf]);
+        tc_commit(&s_full[sb]);
       }
       __syncwarp();
     };
-    issue_s(0);
+    for (int j = 0; j < B_SBUF && j < nkb; ++j) issue_s(j);
     for (int j = 0; j < nkb; ++j) {
-      if (j + 1 < nkb) issue_s(j + 1);
       const int st = j % BQ_STAGES, bf = j & 1;
       mbar_wait(&p_full[bf], (j >> 1) & 1);
       tc_fence_after();
@@ -682,6 +689,7 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
         tc_commit(&kv_empty[st]);
       }
       __syncwarp();
+      if (j + B_SBUF < nkb) issue_s(j + B_SBUF);  // into the buffer block j released
     }
     if (elect_one()) tc_commit(done);
     __syncwarp();
@@ -719,18 +727,18 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
     const float nl2 = row < S ? -lse[vrow] * 1.4426950408889634f : 0.f;
     const uint64_t sc2 = pack_f2(sl2, sl2), nl22 = pack_f2(nl2, nl2), nd2 = pack_f2(-dl, -dl);
     for (int j = 0; j < nkb; ++j) {
-      const int bf = j & 1;
+      const int bf = j & 1, sb = j % B_SBUF;
       const int n0 = j * F_BN;
-      mbar_wait(&s_full[bf], (j >> 1) & 1);
+      mbar_wait(&s_full[sb], (j / B_SBUF) & 1);
       tc_fence_after();
       uint32_t sr[CW], pr[CW];
-      const uint32_t tS = tmem + bf * 128 + lo + cb;
+      const uint32_t tS = tmem + sb * 128 + lo + cb;
       tmem_ld_cols<CW>(tS, sr);
       tmem_ld_cols<CW>(tS + 64, pr);
       tc_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[bf]);
+      if (lane == 0) mbar_arrive(&s_free[sb]);
       float dv[CW];
 #pragma unroll
       for (int e = 0; e < CW; e += 2) {
