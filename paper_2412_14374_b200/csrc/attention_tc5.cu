@@ -74,8 +74,10 @@ __global__ void __launch_bounds__(F_THREADS, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (S + F_BM - 1) / F_BM;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // long (late) tiles first
-  const int b = blockIdx.y / H, h = blockIdx.y % H;
+  // grid (B*H, tiles): x varies fastest, so every head's longest (latest) tile
+  // launches before any shorter one -- longest-first across the whole grid
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.y);
+  const int b = blockIdx.x / H, h = blockIdx.x % H;
   const int d = H * F_HD;
   const int q0 = qb * F_BM;
   const int brow = b * S;  // first row of this batch in the [B*S, ld] tensors
@@ -357,8 +359,8 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int kb = blockIdx.x;  // early key blocks see the most query blocks: launched first
-  const int b = blockIdx.y / H, h = blockIdx.y % H;
+  const int kb = blockIdx.y;  // early key blocks see the most query blocks: launched first
+  const int b = blockIdx.x / H, h = blockIdx.x % H;
   const int d = H * F_HD;
   const int k0 = kb * B_KEYS;
   const int brow = b * S;
@@ -596,8 +598,8 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int nqt = (S + F_BM - 1) / F_BM;
-  const int qb = nqt - 1 - static_cast<int>(blockIdx.x);  // long (late) tiles first
-  const int b = blockIdx.y / H, h = blockIdx.y % H;
+  const int qb = nqt - 1 - static_cast<int>(blockIdx.y);  // long (late) tiles first
+  const int b = blockIdx.x / H, h = blockIdx.x % H;
   const int d = H * F_HD;
   const int q0 = qb * F_BM;
   const int brow = b * S;
@@ -830,7 +832,7 @@ int attention_fwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, void
     PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM));
     attr = true;
   }
-  dim3 grid((S + F_BM - 1) / F_BM, B * H);
+  dim3 grid(B * H, (S + F_BM - 1) / F_BM);
   const float sl2 = 1.4426950408889634f / sqrtf(static_cast<float>(F_HD));
   fa_fwd_tc5<<<grid, F_THREADS, F_SMEM, st>>>(tm, static_cast<bf16*>(o), ld_o, lse, H, S, sl2);
   return check_launch("fa_fwd_tc5");
@@ -858,12 +860,12 @@ int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, cons
   const float scale = 1.f / sqrtf(static_cast<float>(F_HD));
   const float sl2 = scale * 1.4426950408889634f;
   // dQ first: it also writes delta = rowsum(dO o O), which dK/dV consume
-  dim3 g2((S + F_BM - 1) / F_BM, B * H);
+  dim3 g2(B * H, (S + F_BM - 1) / F_BM);
   fa_bwd_dq_tc5<<<g2, BQ_THREADS, BQ_SMEM, st>>>(tq, tg, to, lse, delta, static_cast<bf16*>(dqkv),
                                                   ld_dqkv, H, S, sl2, scale);
   rc = check_launch("fa_bwd_dq_tc5");
   if (rc) return rc;
-  dim3 g1((S + B_KEYS - 1) / B_KEYS, B * H);
+  dim3 g1(B * H, (S + B_KEYS - 1) / B_KEYS);
   fa_bwd_dkdv_tc5<<<g1, BKV_THREADS, BKV_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
                                                       ld_dqkv, H, S, sl2, scale);
   return check_launch("fa_bwd_dkdv_tc5");
