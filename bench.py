@@ -171,29 +171,45 @@ class ClockSampler:
 
 def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
     """Average achieved TFLOP/s of the tcgen05 GEMM over the shape mix of one
-    stage step, each shape timed with CUDA events on its launch stream (warm,
-    back to back); share of the step it accounts for."""
+    stage step, each GEMM issued exactly as device.py issues it (operand
+    majors, fused epilogue, split-K hint) and timed with CUDA events on its
+    launch stream (warm, back to back); share of the step it accounts for."""
     import torch
     from paper_2412_14374_b200 import _lib
     T, d, f, V = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.vocab
-    # (M, N, K, ta, tb, launches per microbatch per block) for one GPT block fwd+bwd
-    shapes = [(T, 3 * d, d, 0, 1), (T, d, d, 0, 1), (T, f, d, 0, 1), (T, d, f, 0, 1),   # fwd
-              (d, f, T, 1, 0), (T, f, d, 0, 0), (f, d, T, 1, 0), (T, d, f, 0, 0),       # bwd mlp
-              (d, d, T, 1, 0), (T, d, d, 0, 0), (3 * d, d, T, 1, 0), (T, d, 3 * d, 0, 0)]
-    head = [(T, V, d, 0, 1), (T, d, V, 0, 0), (V, d, T, 1, 0)]
+    E = _lib
+    # (M, N, K, transA, transB, epilogue, has_aux, has_u, fp32 out) per GPT block
+    shapes = [(T, 3 * d, d, 0, 1, E.EPI_BIAS, 0, 0, 0),                        # qkv
+              (T, d, d, 0, 1, E.EPI_BIAS | E.EPI_RESIDUAL, 1, 0, 0),            # attn out
+              (T, f, d, 0, 1, E.EPI_BIAS | E.EPI_GELU, 0, 1, 0),                # fc1
+              (T, d, f, 0, 1, E.EPI_BIAS | E.EPI_RESIDUAL, 1, 0, 0),            # fc2
+              (d, f, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                    # dW fc2
+              (T, f, d, 0, 1, E.EPI_GELU_GRAD, 1, 0, 0),                        # dX fc2 (gelu')
+              (f, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                    # dW fc1
+              (T, d, f, 0, 1, 0, 0, 0, 0),                                      # dX fc1
+              (d, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                    # dW out
+              (T, d, d, 0, 1, 0, 0, 0, 0),                                      # dX out
+              (3 * d, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                # dW qkv
+              (T, d, 3 * d, 0, 1, 0, 0, 0, 0)]                                  # dX qkv
+    head = [(T, V, d, 0, 1, 0, 0, 0, 0), (T, d, V, 0, 1, 0, 0, 0, 0),
+            (V, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1)]
     st = torch.cuda.current_stream()
     tot_flops = tot_ms = 0.0
     per = []
-    for (Mm, N, K, ta, tb), count in [(s, stage_blocks) for s in shapes] + [(s, 1 if P == 1 else 0) for s in head]:
+    for (Mm, N, K, ta, tb, epi, has_aux, has_u, f32), count in \
+            [(s, stage_blocks) for s in shapes] + [(s, 1 if P == 1 else 0) for s in head]:
         if count == 0:
             continue
         A = torch.randn((K, Mm) if ta else (Mm, K), device="cuda").bfloat16()
         B = torch.randn((N, K) if tb else (K, N), device="cuda").bfloat16()
-        out_f32 = ta == 1  # weight gradients: fp32 with the split-K hint, as device.py issues them
-        C = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
-        args = (_lib.PC_BF16, _lib.PC_F32 if out_f32 else _lib.PC_BF16, ta, tb, Mm, N, K,
-                A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N,
-                _lib.EPI_SPLITK_ZERO_C if out_f32 else 0, None, None, 0, None, 0, st.cuda_stream)
+        C = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
+        bias = torch.zeros(N, device="cuda")
+        aux = torch.randn(Mm, N, device="cuda").bfloat16() if has_aux else None
+        U = torch.empty(Mm, N, device="cuda", dtype=torch.bfloat16) if has_u else None
+        args = (_lib.PC_BF16, _lib.PC_F32 if f32 else _lib.PC_BF16, ta, tb, Mm, N, K,
+                A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, epi,
+                bias.data_ptr(), aux.data_ptr() if aux is not None else None, N,
+                U.data_ptr() if U is not None else None, N, st.cuda_stream)
         for _ in range(3):
             _lib.call("pc_gemm", *args)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -205,11 +221,11 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         fl = 2.0 * Mm * N * K
-        per.append({"shape": [Mm, N, K, ta, tb], "ms": round(ms, 4),
+        per.append({"shape": [Mm, N, K, ta, tb], "epilogue": epi, "ms": round(ms, 4),
                     "tflops": round(fl / ms / 1e9, 1), "launches_per_mb": count})
         tot_flops += fl * count * M_MICRO
         tot_ms += ms * count * M_MICRO
-        del A, B, C
+        del A, B, C, aux, U
     achieved = tot_flops / tot_ms / 1e9 if tot_ms else 0.0
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": None,
