@@ -550,8 +550,8 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
 }
 
 constexpr int BQ_STAGES = 5, BQ_EW = 4 * BW_NG, BQ_THREADS = 128 + 32 * BQ_EW;
-constexpr int BQ_SMEM = 3 * 16384 /*Q,dO,O*/ + BQ_STAGES * 2 * 8192 /*K,V*/ + 2 * 16384 /*dS x2*/ +
-                        128 * BW_NG * 4 /*delta partials*/ + 1024 + 256;
+constexpr int BQ_SMEM = 2 * 3 * 16384 /*Q,dO,O x2*/ + BQ_STAGES * 2 * 8192 /*K,V*/ +
+                        2 * 16384 /*dS x2*/ + 128 * BW_NG * 4 /*delta partials*/ + 1024 + 256;
 
 // 16 B chunk j (8 bf16) of row r in a [128 x 64] bf16 tile loaded as two
 // 128B-swizzled 64-row TMA boxes.
@@ -559,34 +559,40 @@ __device__ __forceinline__ uint4 ld_chunk128(const uint8_t* tile, int r, int j) 
   return *reinterpret_cast<const uint4*>(tile + (r >> 6) * 8192 + (r & 63) * 128 + ((j ^ (r & 7)) << 4));
 }
 
-// dQ for 128 queries of one (batch, head), one CTA per SM, 12 warps; also
-// produces delta = rowsum(dO o O) for these rows (consumed by the dK/dV
-// kernel that runs next):
-//   warp 0      TMA producer: Q, dO, O once; K/V blocks of 64 keys (3-deep ring)
-//   warp 1      MMA issuer, one key block ahead of the elementwise warps:
-//                 S_j = Q K_j^T, dP_j = dO V_j^T -> TMEM buffer j % 2
-//                 dQ += dS_j K_j                 -> TMEM accumulator
+// dQ for 128-query tiles of one (batch, head), persistent: one CTA per SM
+// walks the tiles longest-first (tile w: query tile nqt-1 - w/BH, head w%BH).
+// Also produces delta = rowsum(dO o O) for its rows (consumed by the dK/dV
+// kernel that runs next).  12 + 4 warps:
+//   warp 0      TMA producer: Q, dO, O of a tile into one of two buffers (the
+//               next tile's are prefetched while this one computes), K/V
+//               blocks of 64 keys through a 5-deep ring
+//   warp 1      MMA issuer, up to three key blocks ahead of the elementwise
+//               warps: S_j = Q K_j^T, dP_j = dO V_j^T -> TMEM buffer j % 3,
+//               dQ += dS_j K_j -> TMEM accumulator
 //   warp 2      TMEM allocator (512 columns)
 //   warps 4..   elementwise: BW_NG warps per TMEM lane quarter (one query
 //               row per thread, 64 / BW_NG keys each) build
 //               dS = exp2(S*c - lse) (dP - delta) into 128B-swizzled smem
+// Ring / buffer phases run on tile-global block counters, so a tile's first
+// blocks reuse buffers the previous tile released.
 __global__ void __launch_bounds__(BQ_THREADS, 1)
     fa_bwd_dq_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                   const __grid_constant__ CUtensorMap to, const float* __restrict__ lse,
-                  float* __restrict__ delta, bf16* __restrict__ dqkv, int64_t ldd, int H, int S,
-                  float sl2, float scale) {
+                  float* __restrict__ delta, bf16* __restrict__ dqkv, int64_t ldd, int BH, int H,
+                  int S, float sl2, float scale) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sG = sQ + 16384;
-  uint8_t* sO = sG + 16384;
-  uint8_t* sK = sO + 16384;                // [ST][64 x 64]
+  uint8_t* sQ = smem;                      // [2][128 x 64]
+  uint8_t* sG = sQ + 2 * 16384;            // dO [2][128 x 64]
+  uint8_t* sO = sG + 2 * 16384;            // O  [2][128 x 64]
+  uint8_t* sK = sO + 2 * 16384;            // [ST][64 x 64]
   uint8_t* sV = sK + BQ_STAGES * 8192;     // [ST][64 x 64]
   uint8_t* sD = sV + BQ_STAGES * 8192;     // dS [2][128 q x 64 keys]
   float* sDelta = reinterpret_cast<float*>(sD + 2 * 16384);  // [BW_NG][128] row partials
-  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sDelta + 128 * BW_NG);
-  uint64_t* kv_full = bar_q + 1;
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sDelta + 128 * BW_NG);  // [2]
+  uint64_t* q_empty = q_full + 2;           // [2]
+  uint64_t* kv_full = q_empty + 2;
   uint64_t* kv_empty = kv_full + BQ_STAGES;
   uint64_t* s_full = kv_empty + BQ_STAGES;  // [B_SBUF]
   uint64_t* s_free = s_full + B_SBUF;       // [B_SBUF]
@@ -598,18 +604,17 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int nqt = (S + F_BM - 1) / F_BM;
-  const int qb = nqt - 1 - static_cast<int>(blockIdx.y);  // long (late) tiles first
-  const int b = blockIdx.x / H, h = blockIdx.x % H;
+  const int items = BH * nqt;
   const int d = H * F_HD;
-  const int q0 = qb * F_BM;
-  const int brow = b * S;
-  const int nkb = (min(S, q0 + F_BM) + F_BN - 1) / F_BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tg);
     tma_prefetch_desc(&to);
-    mbar_init(bar_q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1 + BQ_EW);  // MMA warp (Q, dO) + elementwise warps (O, dO)
+    }
     for (int i = 0; i < BQ_STAGES; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -632,148 +637,187 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   const uint32_t tmem = *tslot;
   const uint32_t tdQ = tmem + 128 * B_SBUF;  // S_j at tmem + 128 (j % B_SBUF), dP_j at + 64
 
+  // tile w -> (batch*head, first query row, key blocks)
+  auto decode = [&](int w, int& bh, int& q0, int& nkb) {
+    const int qt = nqt - 1 - w / BH;
+    bh = w % BH;
+    q0 = qt * F_BM;
+    nkb = (min(S, q0 + F_BM) + F_BN - 1) / F_BN;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_q, 3 * 16384);
-      for (int hf = 0; hf < 2; ++hf) {
-        tma_load_2d(sQ + hf * 8192, &tq, bar_q, h * F_HD, brow + q0 + hf * 64);
-        tma_load_2d(sG + hf * 8192, &tg, bar_q, h * F_HD, brow + q0 + hf * 64);
-        tma_load_2d(sO + hf * 8192, &to, bar_q, h * F_HD, brow + q0 + hf * 64);
-      }
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j % BQ_STAGES;
-        mbar_wait(&kv_empty[st], ((j / BQ_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * 8192);
-        tma_load_2d(sK + st * 8192, &tq, &kv_full[st], d + h * F_HD, brow + j * F_BN);
-        tma_load_2d(sV + st * 8192, &tq, &kv_full[st], 2 * d + h * F_HD, brow + j * F_BN);
+      uint32_t g = 0, ic = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+        int bh, q0, nkb;
+        decode(w, bh, q0, nkb);
+        const int b = bh / H, h = bh % H, brow = b * S;
+        const int qb = ic & 1;
+        mbar_wait(&q_empty[qb], ((ic >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qb], 3 * 16384);
+        for (int hf = 0; hf < 2; ++hf) {
+          tma_load_2d(sQ + qb * 16384 + hf * 8192, &tq, &q_full[qb], h * F_HD, brow + q0 + hf * 64);
+          tma_load_2d(sG + qb * 16384 + hf * 8192, &tg, &q_full[qb], h * F_HD, brow + q0 + hf * 64);
+          tma_load_2d(sO + qb * 16384 + hf * 8192, &to, &q_full[qb], h * F_HD, brow + q0 + hf * 64);
+        }
+        for (int j = 0; j < nkb; ++j, ++g) {
+          const int st = g % BQ_STAGES;
+          mbar_wait(&kv_empty[st], ((g / BQ_STAGES) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * 8192);
+          tma_load_2d(sK + st * 8192, &tq, &kv_full[st], d + h * F_HD, brow + j * F_BN);
+          tma_load_2d(sV + st * 8192, &tq, &kv_full[st], 2 * d + h * F_HD, brow + j * F_BN);
+        }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t ID_T = umma_idesc_bf16(128, F_BN, 0, 0);  // Q/dO x (K/V)^T
     constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // dS x K (MN-major)
-    mbar_wait(bar_q, 0);
-    tc_fence_after();
-    const uint64_t qd = umma_sdesc_sw128(smem_u32(sQ), 16, 1024);
-    const uint64_t gd = umma_sdesc_sw128(smem_u32(sG), 16, 1024);
     const uint64_t kd = umma_sdesc_sw128(smem_u32(sK), 16, 1024);     // K-major view
     const uint64_t vd = umma_sdesc_sw128(smem_u32(sV), 16, 1024);
     const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), 8192, 1024);   // MN-major view
     const uint64_t dd = umma_sdesc_sw128(smem_u32(sD), 16, 1024);
-    auto issue_s = [&](int j) {
-      const int st = j % BQ_STAGES, sb = j % B_SBUF;
-      mbar_wait(&kv_full[st], (j / BQ_STAGES) & 1);
-      if (j >= B_SBUF) mbar_wait(&s_free[sb], ((j - B_SBUF) / B_SBUF) & 1);
+    uint32_t g0 = 0, ic = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+      int bh, q0, nkb;
+      decode(w, bh, q0, nkb);
+      const int qb = ic & 1;
+      mbar_wait(&q_full[qb], (ic >> 1) & 1);
       tc_fence_after();
-      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-      const uint32_t tS = tmem + sb * 128;
-      if (elect_one()) {
+      const uint64_t qd = umma_sdesc_sw128(smem_u32(sQ + qb * 16384), 16, 1024);
+      const uint64_t gd = umma_sdesc_sw128(smem_u32(sG + qb * 16384), 16, 1024);
+      auto issue_s = [&](uint32_t g) {
+        const int st = g % BQ_STAGES, sb = g % B_SBUF;
+        mbar_wait(&kv_full[st], (g / BQ_STAGES) & 1);
+        if (g >= B_SBUF) mbar_wait(&s_free[sb], ((g - B_SBUF) / B_SBUF) & 1);
+        tc_fence_after();
+        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint32_t tS = tmem + sb * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < F_HD / 16; ++k) {
-          tc_mma_f16(tS, qd + 2 * k, kd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
-          tc_mma_f16(tS + 64, gd + 2 * k, vd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          for (int k = 0; k < F_HD / 16; ++k) {
+            tc_mma_f16(tS, qd + 2 * k, kd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+            tc_mma_f16(tS + 64, gd + 2 * k, vd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          }
+          tc_commit(&s_full[sb]);
         }
-        tc_commit(&s_full[sb]);
-      }
-      __syncwarp();
-    };
-    for (int j = 0; j < B_SBUF && j < nkb; ++j) issue_s(j);
-    for (int j = 0; j < nkb; ++j) {
-      const int st = j % BQ_STAGES, bf = j & 1;
-      mbar_wait(&p_full[bf], (j >> 1) & 1);
-      tc_fence_after();
-      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-      const uint64_t po = static_cast<uint64_t>(bf * (16384 >> 4));
-      if (elect_one()) {
+        __syncwarp();
+      };
+      for (int j = 0; j < B_SBUF && j < nkb; ++j) issue_s(g0 + j);
+      for (int j = 0; j < nkb; ++j) {
+        const uint32_t g = g0 + j;
+        const int st = g % BQ_STAGES, pb = g & 1;
+        mbar_wait(&p_full[pb], (g >> 1) & 1);
+        tc_fence_after();
+        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint64_t po = static_cast<uint64_t>(pb * (16384 >> 4));
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < F_BN / 16; ++k)
-          tc_mma_f16(tdQ, dd + po + 2 * k, kn + so + 128 * k, ID_A, (j > 0 || k > 0) ? 1u : 0u);
-        tc_commit(&pv_done[bf]);
-        tc_commit(&kv_empty[st]);
+          for (int k = 0; k < F_BN / 16; ++k)
+            tc_mma_f16(tdQ, dd + po + 2 * k, kn + so + 128 * k, ID_A, (j > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&pv_done[pb]);
+          tc_commit(&kv_empty[st]);
+        }
+        __syncwarp();
+        if (j + B_SBUF < nkb) issue_s(g + B_SBUF);  // into the buffer block j released
+      }
+      if (elect_one()) {
+        tc_commit(&q_empty[qb]);  // Q / dO of this tile no longer read by MMAs
+        tc_commit(done);          // dQ of this tile complete
       }
       __syncwarp();
-      if (j + B_SBUF < nkb) issue_s(j + B_SBUF);  // into the buffer block j released
+      g0 += nkb;
     }
-    if (elect_one()) tc_commit(done);
-    __syncwarp();
   } else if (warp >= 4) {
     constexpr int CW = BW_CW;
     const int qw = warp & 3;               // TMEM lane quarter
     const int grp = (warp - 4) >> 2;       // column group
     const int cb = grp * CW;               // first of this warp's CW keys / head dims
     const int r = qw * 32 + lane;          // query row in the tile
-    const int row = q0 + r;
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
-    const int64_t vrow = (static_cast<int64_t>(b) * H + h) * S + row;
-    // delta = rowsum(dO o O): each column group sums CW head dims, fixed-order combine
-    mbar_wait(bar_q, 0);
-    float part = 0.f;
+    const uint64_t sc2 = pack_f2(sl2, sl2);
+    uint32_t g0 = 0, ic = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+      int bh, q0, nkb;
+      decode(w, bh, q0, nkb);
+      const int b = bh / H, h = bh % H, brow = b * S;
+      const int row = q0 + r;
+      const int64_t vrow = static_cast<int64_t>(bh) * S + row;
+      const int qb = ic & 1;
+      // delta = rowsum(dO o O): each column group sums CW head dims, fixed-order combine
+      mbar_wait(&q_full[qb], (ic >> 1) & 1);
+      float part = 0.f;
 #pragma unroll
-    for (int jj = 0; jj < CW / 8; ++jj) {
-      const uint4 ov = ld_chunk128(sO, r, cb / 8 + jj);
-      const uint4 gv = ld_chunk128(sG, r, cb / 8 + jj);
-      const __nv_bfloat162* oh = reinterpret_cast<const __nv_bfloat162*>(&ov);
-      const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gv);
+      for (int jj = 0; jj < CW / 8; ++jj) {
+        const uint4 ov = ld_chunk128(sO + qb * 16384, r, cb / 8 + jj);
+        const uint4 gv = ld_chunk128(sG + qb * 16384, r, cb / 8 + jj);
+        const __nv_bfloat162* oh = reinterpret_cast<const __nv_bfloat162*>(&ov);
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gv);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 of = __bfloat1622float2(oh[k]), gf = __bfloat1622float2(gh[k]);
-        part = fmaf(of.x, gf.x, part);
-        part = fmaf(of.y, gf.y, part);
-      }
-    }
-    sDelta[grp * 128 + r] = part;
-    asm volatile("bar.sync 1, %0;" ::"n"(BQ_EW * 32) : "memory");  // elementwise warps only
-    float dl = 0.f;
-#pragma unroll
-    for (int g = 0; g < BW_NG; ++g) dl += sDelta[g * 128 + r];
-    if (grp == 0 && row < S) delta[vrow] = dl;
-    const float nl2 = row < S ? -lse[vrow] * 1.4426950408889634f : 0.f;
-    const uint64_t sc2 = pack_f2(sl2, sl2), nl22 = pack_f2(nl2, nl2), nd2 = pack_f2(-dl, -dl);
-    for (int j = 0; j < nkb; ++j) {
-      const int bf = j & 1, sb = j % B_SBUF;
-      const int n0 = j * F_BN;
-      mbar_wait(&s_full[sb], (j / B_SBUF) & 1);
-      tc_fence_after();
-      uint32_t sr[CW], pr[CW];
-      const uint32_t tS = tmem + sb * 128 + lo + cb;
-      tmem_ld_cols<CW>(tS, sr);
-      tmem_ld_cols<CW>(tS + 64, pr);
-      tc_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[sb]);
-      float dv[CW];
-#pragma unroll
-      for (int e = 0; e < CW; e += 2) {
-        float a0, a1, e0, e1, f0, f1;
-        unpack_f2(ffma2(pack_f2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2, nl22), a0, a1);
-        const float p0 = ex2(a0), p1 = ex2(a1);
-        unpack_f2(fadd2(pack_f2(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1])), nd2), e0, e1);
-        unpack_f2(fmul2(pack_f2(p0, p1), pack_f2(e0, e1)), f0, f1);
-        dv[e] = f0;
-        dv[e + 1] = f1;
-      }
-      // causal / ragged mask: only blocks crossing the diagonal or the sequence end
-      if (n0 + cb + CW - 1 > row || n0 + cb + CW > S || row >= S) {
-#pragma unroll
-        for (int e = 0; e < CW; ++e) {
-          const int key = n0 + cb + e;
-          if (key > row || key >= S || row >= S) dv[e] = 0.f;
+        for (int k = 0; k < 4; ++k) {
+          const float2 of = __bfloat1622float2(oh[k]), gf = __bfloat1622float2(gh[k]);
+          part = fmaf(of.x, gf.x, part);
+          part = fmaf(of.y, gf.y, part);
         }
       }
-      if (j >= 2) mbar_wait(&pv_done[bf], ((j - 2) >> 1) & 1);
-      st_row_chunks<CW / 8>(sD + bf * 16384, r, cb / 8, dv);
-      fence_proxy_async_smem();
-      tc_fence_before();
+      sDelta[grp * 128 + r] = part;
+      asm volatile("bar.sync 1, %0;" ::"n"(BQ_EW * 32) : "memory");  // elementwise warps only
+      float dl = 0.f;
+#pragma unroll
+      for (int gi = 0; gi < BW_NG; ++gi) dl += sDelta[gi * 128 + r];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[bf]);
+      if (lane == 0) mbar_arrive(&q_empty[qb]);  // O / dO no longer read here
+      if (grp == 0 && row < S) delta[vrow] = dl;
+      const float nl2 = row < S ? -lse[vrow] * 1.4426950408889634f : 0.f;
+      const uint64_t nl22 = pack_f2(nl2, nl2), nd2 = pack_f2(-dl, -dl);
+      for (int j = 0; j < nkb; ++j) {
+        const uint32_t g = g0 + j;
+        const int pb = g & 1, sb = g % B_SBUF;
+        const int n0 = j * F_BN;
+        mbar_wait(&s_full[sb], (g / B_SBUF) & 1);
+        tc_fence_after();
+        uint32_t sr[CW], pr[CW];
+        const uint32_t tS = tmem + sb * 128 + lo + cb;
+        tmem_ld_cols<CW>(tS, sr);
+        tmem_ld_cols<CW>(tS + 64, pr);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[sb]);
+        float dv[CW];
+#pragma unroll
+        for (int e = 0; e < CW; e += 2) {
+          float a0, a1, e0, e1, f0, f1;
+          unpack_f2(ffma2(pack_f2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2, nl22), a0, a1);
+          const float p0 = ex2(a0), p1 = ex2(a1);
+          unpack_f2(fadd2(pack_f2(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1])), nd2), e0, e1);
+          unpack_f2(fmul2(pack_f2(p0, p1), pack_f2(e0, e1)), f0, f1);
+          dv[e] = f0;
+          dv[e + 1] = f1;
+        }
+        // causal / ragged mask: only blocks crossing the diagonal or the sequence end
+        if (n0 + cb + CW - 1 > row || n0 + cb + CW > S || row >= S) {
+#pragma unroll
+          for (int e = 0; e < CW; ++e) {
+            const int key = n0 + cb + e;
+            if (key > row || key >= S || row >= S) dv[e] = 0.f;
+          }
+        }
+        if (g >= 2) mbar_wait(&pv_done[pb], ((g - 2) >> 1) & 1);
+        st_row_chunks<CW / 8>(sD + pb * 16384, r, cb / 8, dv);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
+      }
+      mbar_wait(done, ic & 1);
+      tc_fence_after();
+      uint32_t acc[CW];
+      tmem_ld_cols<CW>(tdQ + lo + cb, acc);
+      tc_wait_ld();
+      if (row < S)
+        store_row_chunks<CW / 8>(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD + cb, acc, scale);
+      g0 += nkb;
     }
-    mbar_wait(done, 0);
-    tc_fence_after();
-    uint32_t acc[CW];
-    tmem_ld_cols<CW>(tdQ + lo + cb, acc);
-    tc_wait_ld();
-    if (row < S)
-      store_row_chunks<CW / 8>(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD + cb, acc, scale);
   }
 
   tc_fence_before();
@@ -860,9 +904,11 @@ int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, cons
   const float scale = 1.f / sqrtf(static_cast<float>(F_HD));
   const float sl2 = scale * 1.4426950408889634f;
   // dQ first: it also writes delta = rowsum(dO o O), which dK/dV consume
-  dim3 g2(B * H, (S + F_BM - 1) / F_BM);
+  // persistent: one CTA per SM over the (query tile, head) work list
+  const int dq_items = B * H * ((S + F_BM - 1) / F_BM);
+  const int g2 = dq_items < num_sms() ? dq_items : num_sms();
   fa_bwd_dq_tc5<<<g2, BQ_THREADS, BQ_SMEM, st>>>(tq, tg, to, lse, delta, static_cast<bf16*>(dqkv),
-                                                  ld_dqkv, H, S, sl2, scale);
+                                                  ld_dqkv, B * H, H, S, sl2, scale);
   rc = check_launch("fa_bwd_dq_tc5");
   if (rc) return rc;
   dim3 g1(B * H, (S + B_KEYS - 1) / B_KEYS);
