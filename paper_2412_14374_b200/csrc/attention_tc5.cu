@@ -285,7 +285,7 @@ constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 5, BKV_EW = 4 * BW_NG, BKV_TH
 // score buffers (S/dP pairs of 64 + 64 TMEM columns): the MMA warp keeps the
 // score MMAs up to three blocks ahead of the elementwise warps
 constexpr int B_SBUF = 3;
-constexpr int BKV_SMEM = 2 * 16384 /*K,V*/ + BKV_STAGES * 2 * 8192 /*Q,dO*/ +
+constexpr int BKV_SMEM = 2 * 2 * 16384 /*K,V x2*/ + BKV_STAGES * 2 * 8192 /*Q,dO*/ +
                          2 * 2 * 16384 /*P^T,dS^T x2*/ + BKV_STAGES * 512 /*lse,delta*/ + 1024 + 256;
 
 // NC * 8 bf16 (NC 16 B chunks starting at logical chunk c0) of row r of a
@@ -321,34 +321,38 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
   for (int i = 0; i < CW / 16; ++i) tmem_ld16(taddr + 16 * i, r + 16 * i);
 }
 
-// dK, dV for 128 keys of one (batch, head), one CTA per SM, 12 warps:
-//   warp 0      TMA producer: K, V once; per 64-query block Q, dO (tensor
-//               maps) and its lse / delta rows (bulk copies) into a 3-deep ring
-//   warp 1      MMA issuer, one query block ahead of the elementwise warps:
-//                 S^T_i = K Q_i^T, dP^T_i = V dO_i^T  -> TMEM buffer i % 2
-//                 dV += P^T_i dO_i, dK += dS^T_i Q_i  -> TMEM accumulators
-//   warp 2      TMEM allocator (512 columns: S^T/dP^T x2, dV, dK)
+// dK, dV for 128-key tiles, persistent: one CTA per SM walks the tiles
+// longest-first (tile w: key tile w / BH, head w % BH).  12 + 4 warps:
+//   warp 0      TMA producer: K, V of a tile into one of two buffers (the next
+//               tile's prefetched while this one computes); per 64-query block
+//               Q, dO (tensor maps) and its lse / delta rows (bulk copies)
+//               into a 5-deep ring
+//   warp 1      MMA issuer, up to three query blocks ahead of the elementwise
+//               warps: S^T_i = K Q_i^T, dP^T_i = V dO_i^T -> TMEM buffer i % 3;
+//               dV += P^T_i dO_i, dK += dS^T_i Q_i -> TMEM accumulators
+//   warp 2      TMEM allocator (512 columns: S^T/dP^T x3, dV, dK)
 //   warps 4..   elementwise: BW_NG warps per TMEM lane quarter (one key row
 //               per thread, 64 / BW_NG queries each) build P^T = exp2(S^T*c - lse)
 //               and dS^T = P^T (dP^T - delta) into 128B-swizzled smem tiles
-// Barriers: s_full / s_free (scores landed / read out of TMEM), p_full (P^T,
-// dS^T staged), pv_done (dV/dK MMAs of block i retired: tiles reusable).
+// Ring / buffer phases run on tile-global block counters.
 __global__ void __launch_bounds__(BKV_THREADS, 1)
     fa_bwd_dkdv_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                     const float* __restrict__ lse, const float* __restrict__ delta,
-                    bf16* __restrict__ dqkv, int64_t ldd, int H, int S, float sl2, float scale) {
+                    bf16* __restrict__ dqkv, int64_t ldd, int BH, int H, int S, float sl2,
+                    float scale) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sK = smem;
-  uint8_t* sV = sK + 16384;
-  uint8_t* sQ = sV + 16384;                // [ST][64 x 64]
+  uint8_t* sK = smem;                      // [2][128 keys x 64]
+  uint8_t* sV = sK + 2 * 16384;            // [2][128 keys x 64]
+  uint8_t* sQ = sV + 2 * 16384;            // [ST][64 x 64]
   uint8_t* sG = sQ + BKV_STAGES * 8192;    // dO [ST][64 x 64]
   uint8_t* sPt = sG + BKV_STAGES * 8192;   // P^T  [2][128 keys x 64 q]
   uint8_t* sDt = sPt + 2 * 16384;          // dS^T [2][128 keys x 64 q]
   float* sLD = reinterpret_cast<float*>(sDt + 2 * 16384);  // [ST][lse 64 | delta 64]
-  uint64_t* bar_kv = reinterpret_cast<uint64_t*>(sLD + BKV_STAGES * 128);
-  uint64_t* q_full = bar_kv + 1;
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sLD + BKV_STAGES * 128);  // [2]
+  uint64_t* kv_empty = kv_full + 2;         // [2]
+  uint64_t* q_full = kv_empty + 2;
   uint64_t* q_empty = q_full + BKV_STAGES;
   uint64_t* s_full = q_empty + BKV_STAGES;  // [B_SBUF]
   uint64_t* s_free = s_full + B_SBUF;       // [B_SBUF]
@@ -359,19 +363,17 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int kb = blockIdx.y;  // early key blocks see the most query blocks: launched first
-  const int b = blockIdx.x / H, h = blockIdx.x % H;
+  const int nkt = (S + B_KEYS - 1) / B_KEYS, nqb = (S + B_Q - 1) / B_Q;
+  const int items = BH * nkt;
   const int d = H * F_HD;
-  const int k0 = kb * B_KEYS;
-  const int brow = b * S;
-  const int qbeg = k0 / B_Q, nqb = (S + B_Q - 1) / B_Q;
-  const int n = nqb - qbeg;
-  const int64_t vbase = (static_cast<int64_t>(b) * H + h) * S;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tg);
-    mbar_init(bar_kv, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
     for (int i = 0; i < BKV_STAGES; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
@@ -395,152 +397,189 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   // S^T of block i at tmem + 128 (i % B_SBUF), dP^T at + 64; then dV, dK
   const uint32_t tdV = tmem + 128 * B_SBUF, tdK = tdV + 64;
 
+  // tile w -> (batch*head, first key, first query block, query blocks)
+  auto decode = [&](int w, int& bh, int& k0, int& qbeg, int& n) {
+    const int kt = w / BH;  // early key tiles see the most query blocks: first
+    bh = w % BH;
+    k0 = kt * B_KEYS;
+    qbeg = k0 / B_Q;
+    n = nqb - qbeg;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_kv, 2 * 16384);
-      for (int hf = 0; hf < 2; ++hf) {
-        tma_load_2d(sK + hf * 8192, &tq, bar_kv, d + h * F_HD, brow + k0 + hf * 64);
-        tma_load_2d(sV + hf * 8192, &tq, bar_kv, 2 * d + h * F_HD, brow + k0 + hf * 64);
-      }
-      for (int i = 0; i < n; ++i) {
-        const int st = i % BKV_STAGES;
-        const int m0 = (qbeg + i) * B_Q;
-        const uint32_t lbytes = static_cast<uint32_t>(min(B_Q, S - m0)) * 4;  // S % 4 == 0
-        mbar_wait(&q_empty[st], ((i / BKV_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], 2 * 8192 + 2 * lbytes);
-        tma_load_2d(sQ + st * 8192, &tq, &q_full[st], h * F_HD, brow + m0);
-        tma_load_2d(sG + st * 8192, &tg, &q_full[st], h * F_HD, brow + m0);
-        bulk_load(sLD + st * 128, lse + vbase + m0, lbytes, &q_full[st]);
-        bulk_load(sLD + st * 128 + 64, delta + vbase + m0, lbytes, &q_full[st]);
+      uint32_t g = 0, ic = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+        int bh, k0, qbeg, n;
+        decode(w, bh, k0, qbeg, n);
+        const int b = bh / H, h = bh % H, brow = b * S;
+        const int64_t vbase = static_cast<int64_t>(bh) * S;
+        const int kb2 = ic & 1;
+        mbar_wait(&kv_empty[kb2], ((ic >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[kb2], 2 * 16384);
+        for (int hf = 0; hf < 2; ++hf) {
+          tma_load_2d(sK + kb2 * 16384 + hf * 8192, &tq, &kv_full[kb2], d + h * F_HD, brow + k0 + hf * 64);
+          tma_load_2d(sV + kb2 * 16384 + hf * 8192, &tq, &kv_full[kb2], 2 * d + h * F_HD, brow + k0 + hf * 64);
+        }
+        for (int i = 0; i < n; ++i, ++g) {
+          const int st = g % BKV_STAGES;
+          const int m0 = (qbeg + i) * B_Q;
+          const uint32_t lbytes = static_cast<uint32_t>(min(B_Q, S - m0)) * 4;  // S % 4 == 0
+          mbar_wait(&q_empty[st], ((g / BKV_STAGES) & 1) ^ 1);
+          mbar_expect_tx(&q_full[st], 2 * 8192 + 2 * lbytes);
+          tma_load_2d(sQ + st * 8192, &tq, &q_full[st], h * F_HD, brow + m0);
+          tma_load_2d(sG + st * 8192, &tg, &q_full[st], h * F_HD, brow + m0);
+          bulk_load(sLD + st * 128, lse + vbase + m0, lbytes, &q_full[st]);
+          bulk_load(sLD + st * 128 + 64, delta + vbase + m0, lbytes, &q_full[st]);
+        }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t ID_T = umma_idesc_bf16(128, B_Q, 0, 0);   // K/V x (Q/dO)^T, N = 64 queries
     constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // P^T/dS^T x (dO/Q), N = 64 dims
-    mbar_wait(bar_kv, 0);
-    tc_fence_after();
-    const uint64_t kd = umma_sdesc_sw128(smem_u32(sK), 16, 1024);
-    const uint64_t vd = umma_sdesc_sw128(smem_u32(sV), 16, 1024);
     const uint64_t qd = umma_sdesc_sw128(smem_u32(sQ), 16, 1024);       // K-major view
     const uint64_t gd = umma_sdesc_sw128(smem_u32(sG), 16, 1024);
     const uint64_t qn = umma_sdesc_sw128(smem_u32(sQ), 8192, 1024);     // MN-major view
     const uint64_t gn = umma_sdesc_sw128(smem_u32(sG), 8192, 1024);
     const uint64_t pd = umma_sdesc_sw128(smem_u32(sPt), 16, 1024);
     const uint64_t dd = umma_sdesc_sw128(smem_u32(sDt), 16, 1024);
-    auto issue_s = [&](int i) {
-      const int st = i % BKV_STAGES, sb = i % B_SBUF;
-      mbar_wait(&q_full[st], (i / BKV_STAGES) & 1);
-      if (i >= B_SBUF) mbar_wait(&s_free[sb], ((i - B_SBUF) / B_SBUF) & 1);
+    uint32_t g0 = 0, ic = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+      int bh, k0, qbeg, n;
+      decode(w, bh, k0, qbeg, n);
+      const int kb2 = ic & 1;
+      mbar_wait(&kv_full[kb2], (ic >> 1) & 1);
       tc_fence_after();
-      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-      const uint32_t tS = tmem + sb * 128;
-      if (elect_one()) {
+      const uint64_t kd = umma_sdesc_sw128(smem_u32(sK + kb2 * 16384), 16, 1024);
+      const uint64_t vd = umma_sdesc_sw128(smem_u32(sV + kb2 * 16384), 16, 1024);
+      auto issue_s = [&](uint32_t g) {
+        const int st = g % BKV_STAGES, sb = g % B_SBUF;
+        mbar_wait(&q_full[st], (g / BKV_STAGES) & 1);
+        if (g >= B_SBUF) mbar_wait(&s_free[sb], ((g - B_SBUF) / B_SBUF) & 1);
+        tc_fence_after();
+        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint32_t tS = tmem + sb * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < F_HD / 16; ++k) {
-          tc_mma_f16(tS, kd + 2 * k, qd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
-          tc_mma_f16(tS + 64, vd + 2 * k, gd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          for (int k = 0; k < F_HD / 16; ++k) {
+            tc_mma_f16(tS, kd + 2 * k, qd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+            tc_mma_f16(tS + 64, vd + 2 * k, gd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          }
+          tc_commit(&s_full[sb]);
         }
-        tc_commit(&s_full[sb]);
+        __syncwarp();
+      };
+      for (int i = 0; i < B_SBUF && i < n; ++i) issue_s(g0 + i);
+      for (int i = 0; i < n; ++i) {
+        const uint32_t g = g0 + i;
+        const int st = g % BKV_STAGES, pb = g & 1;
+        mbar_wait(&p_full[pb], (g >> 1) & 1);
+        tc_fence_after();
+        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint64_t po = static_cast<uint64_t>(pb * (16384 >> 4));
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < B_Q / 16; ++k) {
+            const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+            tc_mma_f16(tdV, pd + po + 2 * k, gn + so + 128 * k, ID_A, acc);
+            tc_mma_f16(tdK, dd + po + 2 * k, qn + so + 128 * k, ID_A, acc);
+          }
+          tc_commit(&pv_done[pb]);
+          tc_commit(&q_empty[st]);
+        }
+        __syncwarp();
+        if (i + B_SBUF < n) issue_s(g + B_SBUF);  // into the buffer block i released
+      }
+      if (elect_one()) {
+        tc_commit(&kv_empty[kb2]);  // K / V of this tile no longer read
+        tc_commit(done);            // dV / dK of this tile complete
       }
       __syncwarp();
-    };
-    for (int i = 0; i < B_SBUF && i < n; ++i) issue_s(i);
-    for (int i = 0; i < n; ++i) {
-      const int st = i % BKV_STAGES, bf = i & 1;
-      mbar_wait(&p_full[bf], (i >> 1) & 1);
-      tc_fence_after();
-      const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-      const uint64_t po = static_cast<uint64_t>(bf * (16384 >> 4));
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < B_Q / 16; ++k) {
-          const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-          tc_mma_f16(tdV, pd + po + 2 * k, gn + so + 128 * k, ID_A, acc);
-          tc_mma_f16(tdK, dd + po + 2 * k, qn + so + 128 * k, ID_A, acc);
-        }
-        tc_commit(&pv_done[bf]);
-        tc_commit(&q_empty[st]);
-      }
-      __syncwarp();
-      if (i + B_SBUF < n) issue_s(i + B_SBUF);  // into the buffer block i released
+      g0 += n;
     }
-    if (elect_one()) tc_commit(done);
-    __syncwarp();
   } else if (warp >= 4) {
     constexpr int CW = BW_CW;
     const int qw = warp & 3;                 // TMEM lane quarter
     const int cb = ((warp - 4) >> 2) * CW;   // first of this warp's CW queries / head dims
     const int r = qw * 32 + lane;            // key row in the tile
-    const int key = k0 + r;
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
-    for (int i = 0; i < n; ++i) {
-      const int st = i % BKV_STAGES, bf = i & 1, sb = i % B_SBUF;
-      const int m0 = (qbeg + i) * B_Q;
-      mbar_wait(&s_full[sb], (i / B_SBUF) & 1);
-      tc_fence_after();
-      uint32_t sr[CW], pr[CW];
-      const uint32_t tS = tmem + sb * 128 + lo + cb;
-      tmem_ld_cols<CW>(tS, sr);
-      tmem_ld_cols<CW>(tS + 64, pr);
-      tc_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[sb]);  // the MMA warp may refill this buffer
-      mbar_wait(&q_full[st], (i / BKV_STAGES) & 1);  // lse / delta rows visible
-      const float* Ls = sLD + st * 128 + cb;
-      const float* Ds = Ls + 64;
-      float pv[CW], dv[CW];
+    uint32_t g0 = 0, ic = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+      int bh, k0, qbeg, n;
+      decode(w, bh, k0, qbeg, n);
+      const int b = bh / H, h = bh % H, brow = b * S;
+      const int key = k0 + r;
+      for (int i = 0; i < n; ++i) {
+        const uint32_t g = g0 + i;
+        const int st = g % BKV_STAGES, pb = g & 1, sb = g % B_SBUF;
+        const int m0 = (qbeg + i) * B_Q;
+        mbar_wait(&s_full[sb], (g / B_SBUF) & 1);
+        tc_fence_after();
+        uint32_t sr[CW], pr[CW];
+        const uint32_t tS = tmem + sb * 128 + lo + cb;
+        tmem_ld_cols<CW>(tS, sr);
+        tmem_ld_cols<CW>(tS + 64, pr);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[sb]);  // the MMA warp may refill this buffer
+        mbar_wait(&q_full[st], (g / BKV_STAGES) & 1);  // lse / delta rows visible
+        const float* Ls = sLD + st * 128 + cb;
+        const float* Ds = Ls + 64;
+        float pv[CW], dv[CW];
 #pragma unroll
-      for (int g = 0; g < CW / 4; ++g) {
-        const float4 l4 = reinterpret_cast<const float4*>(Ls)[g];
-        const float4 d4 = reinterpret_cast<const float4*>(Ds)[g];
-        const uint64_t nl01 = pack_f2(-l4.x * 1.4426950408889634f, -l4.y * 1.4426950408889634f);
-        const uint64_t nl23 = pack_f2(-l4.z * 1.4426950408889634f, -l4.w * 1.4426950408889634f);
-        float a0, a1, a2, a3;
-        unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * g]), __uint_as_float(sr[4 * g + 1])), sc2, nl01), a0, a1);
-        unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * g + 2]), __uint_as_float(sr[4 * g + 3])), sc2, nl23), a2, a3);
-        const float p0 = ex2(a0), p1 = ex2(a1), p2 = ex2(a2), p3 = ex2(a3);
-        float e0, e1, e2, e3;
-        unpack_f2(fadd2(pack_f2(__uint_as_float(pr[4 * g]), __uint_as_float(pr[4 * g + 1])),
-                        pack_f2(-d4.x, -d4.y)), e0, e1);
-        unpack_f2(fadd2(pack_f2(__uint_as_float(pr[4 * g + 2]), __uint_as_float(pr[4 * g + 3])),
-                        pack_f2(-d4.z, -d4.w)), e2, e3);
-        float f0, f1, f2, f3;
-        unpack_f2(fmul2(pack_f2(p0, p1), pack_f2(e0, e1)), f0, f1);
-        unpack_f2(fmul2(pack_f2(p2, p3), pack_f2(e2, e3)), f2, f3);
-        pv[4 * g] = p0; pv[4 * g + 1] = p1; pv[4 * g + 2] = p2; pv[4 * g + 3] = p3;
-        dv[4 * g] = f0; dv[4 * g + 1] = f1; dv[4 * g + 2] = f2; dv[4 * g + 3] = f3;
-      }
-      // causal / ragged mask: only blocks reaching below the diagonal or past S
-      if (m0 + cb < key || m0 + cb + CW > S) {
+        for (int gi = 0; gi < CW / 4; ++gi) {
+          const float4 l4 = reinterpret_cast<const float4*>(Ls)[gi];
+          const float4 d4 = reinterpret_cast<const float4*>(Ds)[gi];
+          const uint64_t nl01 = pack_f2(-l4.x * 1.4426950408889634f, -l4.y * 1.4426950408889634f);
+          const uint64_t nl23 = pack_f2(-l4.z * 1.4426950408889634f, -l4.w * 1.4426950408889634f);
+          float a0, a1, a2, a3;
+          unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * gi]), __uint_as_float(sr[4 * gi + 1])), sc2, nl01), a0, a1);
+          unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * gi + 2]), __uint_as_float(sr[4 * gi + 3])), sc2, nl23), a2, a3);
+          const float p0 = ex2(a0), p1 = ex2(a1), p2 = ex2(a2), p3 = ex2(a3);
+          float e0, e1, e2, e3;
+          unpack_f2(fadd2(pack_f2(__uint_as_float(pr[4 * gi]), __uint_as_float(pr[4 * gi + 1])),
+                          pack_f2(-d4.x, -d4.y)), e0, e1);
+          unpack_f2(fadd2(pack_f2(__uint_as_float(pr[4 * gi + 2]), __uint_as_float(pr[4 * gi + 3])),
+                          pack_f2(-d4.z, -d4.w)), e2, e3);
+          float f0, f1, f2, f3;
+          unpack_f2(fmul2(pack_f2(p0, p1), pack_f2(e0, e1)), f0, f1);
+          unpack_f2(fmul2(pack_f2(p2, p3), pack_f2(e2, e3)), f2, f3);
+          pv[4 * gi] = p0; pv[4 * gi + 1] = p1; pv[4 * gi + 2] = p2; pv[4 * gi + 3] = p3;
+          dv[4 * gi] = f0; dv[4 * gi + 1] = f1; dv[4 * gi + 2] = f2; dv[4 * gi + 3] = f3;
+        }
+        // causal / ragged mask: only blocks reaching below the diagonal or past S
+        if (m0 + cb < key || m0 + cb + CW > S) {
 #pragma unroll
-        for (int e = 0; e < CW; ++e) {
-          const int q = m0 + cb + e;
-          if (q < key || q >= S) {
-            pv[e] = 0.f;
-            dv[e] = 0.f;
+          for (int e = 0; e < CW; ++e) {
+            const int q = m0 + cb + e;
+            if (q < key || q >= S) {
+              pv[e] = 0.f;
+              dv[e] = 0.f;
+            }
           }
         }
+        if (g >= 2) mbar_wait(&pv_done[pb], ((g - 2) >> 1) & 1);  // tiles of block g-2 consumed
+        st_row_chunks<CW / 8>(sPt + pb * 16384, r, cb / 8, pv);
+        st_row_chunks<CW / 8>(sDt + pb * 16384, r, cb / 8, dv);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
       }
-      if (i >= 2) mbar_wait(&pv_done[bf], ((i - 2) >> 1) & 1);  // tiles of block i-2 consumed
-      st_row_chunks<CW / 8>(sPt + bf * 16384, r, cb / 8, pv);
-      st_row_chunks<CW / 8>(sDt + bf * 16384, r, cb / 8, dv);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[bf]);
+      mbar_wait(done, ic & 1);
+      tc_fence_after();
+      uint32_t acc[CW];
+      bf16* base = dqkv + static_cast<int64_t>(brow + key) * ldd + h * F_HD + cb;
+      tmem_ld_cols<CW>(tdV + lo + cb, acc);
+      tc_wait_ld();
+      if (key < S) store_row_chunks<CW / 8>(base + 2 * d, acc, 1.f);
+      tmem_ld_cols<CW>(tdK + lo + cb, acc);
+      tc_wait_ld();
+      if (key < S) store_row_chunks<CW / 8>(base + d, acc, scale);
+      g0 += n;
     }
-    mbar_wait(done, 0);
-    tc_fence_after();
-    uint32_t acc[CW];
-    bf16* base = dqkv + static_cast<int64_t>(brow + key) * ldd + h * F_HD + cb;
-    tmem_ld_cols<CW>(tdV + lo + cb, acc);
-    tc_wait_ld();
-    if (key < S) store_row_chunks<CW / 8>(base + 2 * d, acc, 1.f);
-    tmem_ld_cols<CW>(tdK + lo + cb, acc);
-    tc_wait_ld();
-    if (key < S) store_row_chunks<CW / 8>(base + d, acc, scale);
   }
 
   tc_fence_before();
@@ -911,9 +950,10 @@ int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, cons
                                                   ld_dqkv, B * H, H, S, sl2, scale);
   rc = check_launch("fa_bwd_dq_tc5");
   if (rc) return rc;
-  dim3 g1(B * H, (S + B_KEYS - 1) / B_KEYS);
+  const int kv_items = B * H * ((S + B_KEYS - 1) / B_KEYS);
+  const int g1 = kv_items < num_sms() ? kv_items : num_sms();
   fa_bwd_dkdv_tc5<<<g1, BKV_THREADS, BKV_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
-                                                      ld_dqkv, H, S, sl2, scale);
+                                                      ld_dqkv, B * H, H, S, sl2, scale);
   return check_launch("fa_bwd_dkdv_tc5");
 }
 }  // namespace pp200
