@@ -47,6 +47,30 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 __device__ __forceinline__ void tc_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// O += A B with A (bf16, K-major, one row per TMEM lane, two values per
+// 32-bit column) read from TMEM and B from shared memory.
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// 16 fp32 -> 8 packed bf16x2 words (lower K index in the low half)
+__device__ __forceinline__ void pack_bf16x16(const float* v, uint32_t* w) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+    w[k] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -286,7 +310,7 @@ constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 5, BKV_EW = 4 * BW_NG, BKV_TH
 // score MMAs up to three blocks ahead of the elementwise warps
 constexpr int B_SBUF = 3;
 constexpr int BKV_SMEM = 2 * 2 * 16384 /*K,V x2*/ + BKV_STAGES * 2 * 8192 /*Q,dO*/ +
-                         2 * 2 * 16384 /*P^T,dS^T x2*/ + BKV_STAGES * 512 /*lse,delta*/ + 1024 + 256;
+                         BKV_STAGES * 512 /*lse,delta*/ + 1024 + 256;
 
 // NC * 8 bf16 (NC 16 B chunks starting at logical chunk c0) of row r of a
 // 128B-swizzled [rows x 64] K-major tile.
@@ -333,8 +357,11 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
 //   warp 2      TMEM allocator (512 columns: S^T/dP^T x3, dV, dK)
 //   warps 4..   elementwise: BW_NG warps per TMEM lane quarter (one key row
 //               per thread, 64 / BW_NG queries each) build P^T = exp2(S^T*c - lse)
-//               and dS^T = P^T (dP^T - delta) into 128B-swizzled smem tiles
-// Ring / buffer phases run on tile-global block counters.
+//               and dS^T = P^T (dP^T - delta) as packed bf16 written back into
+//               TMEM over the scores they came from: the dV / dK MMAs read their
+//               A operand straight from TMEM (query chunk k of 16 at column 16 k)
+// Ring / buffer phases run on tile-global block counters; a score buffer is
+// reused once the dV / dK MMAs that read its P^T / dS^T have retired.
 __global__ void __launch_bounds__(BKV_THREADS, 1)
     fa_bwd_dkdv_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                     const float* __restrict__ lse, const float* __restrict__ delta,
@@ -347,18 +374,15 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   uint8_t* sV = sK + 2 * 16384;            // [2][128 keys x 64]
   uint8_t* sQ = sV + 2 * 16384;            // [ST][64 x 64]
   uint8_t* sG = sQ + BKV_STAGES * 8192;    // dO [ST][64 x 64]
-  uint8_t* sPt = sG + BKV_STAGES * 8192;   // P^T  [2][128 keys x 64 q]
-  uint8_t* sDt = sPt + 2 * 16384;          // dS^T [2][128 keys x 64 q]
-  float* sLD = reinterpret_cast<float*>(sDt + 2 * 16384);  // [ST][lse 64 | delta 64]
+  float* sLD = reinterpret_cast<float*>(sG + BKV_STAGES * 8192);  // [ST][lse 64 | delta 64]
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(sLD + BKV_STAGES * 128);  // [2]
   uint64_t* kv_empty = kv_full + 2;         // [2]
   uint64_t* q_full = kv_empty + 2;
   uint64_t* q_empty = q_full + BKV_STAGES;
-  uint64_t* s_full = q_empty + BKV_STAGES;  // [B_SBUF]
-  uint64_t* s_free = s_full + B_SBUF;       // [B_SBUF]
-  uint64_t* p_full = s_free + B_SBUF;       // [2]
-  uint64_t* pv_done = p_full + 2;           // [2]
-  uint64_t* done = pv_done + 2;
+  uint64_t* s_full = q_empty + BKV_STAGES;  // [B_SBUF] scores landed
+  uint64_t* p_full = s_full + B_SBUF;       // [B_SBUF] P^T / dS^T packed in TMEM
+  uint64_t* pv_done = p_full + B_SBUF;      // [B_SBUF] dV / dK MMAs of the buffer retired
+  uint64_t* done = pv_done + B_SBUF;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
@@ -380,9 +404,6 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
     }
     for (int i = 0; i < B_SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], BKV_EW);
-    }
-    for (int i = 0; i < 2; ++i) {
       mbar_init(&p_full[i], BKV_EW);
       mbar_init(&pv_done[i], 1);
     }
@@ -441,8 +462,6 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
     const uint64_t gd = umma_sdesc_sw128(smem_u32(sG), 16, 1024);
     const uint64_t qn = umma_sdesc_sw128(smem_u32(sQ), 8192, 1024);     // MN-major view
     const uint64_t gn = umma_sdesc_sw128(smem_u32(sG), 8192, 1024);
-    const uint64_t pd = umma_sdesc_sw128(smem_u32(sPt), 16, 1024);
-    const uint64_t dd = umma_sdesc_sw128(smem_u32(sDt), 16, 1024);
     uint32_t g0 = 0, ic = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
       int bh, k0, qbeg, n;
@@ -455,7 +474,8 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
       auto issue_s = [&](uint32_t g) {
         const int st = g % BKV_STAGES, sb = g % B_SBUF;
         mbar_wait(&q_full[st], (g / BKV_STAGES) & 1);
-        if (g >= B_SBUF) mbar_wait(&s_free[sb], ((g - B_SBUF) / B_SBUF) & 1);
+        // the buffer's previous P^T / dS^T have been read by their MMAs
+        if (g >= B_SBUF) mbar_wait(&pv_done[sb], ((g - B_SBUF) / B_SBUF) & 1);
         tc_fence_after();
         const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
         const uint32_t tS = tmem + sb * 128;
@@ -472,19 +492,19 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
       for (int i = 0; i < B_SBUF && i < n; ++i) issue_s(g0 + i);
       for (int i = 0; i < n; ++i) {
         const uint32_t g = g0 + i;
-        const int st = g % BKV_STAGES, pb = g & 1;
-        mbar_wait(&p_full[pb], (g >> 1) & 1);
+        const int st = g % BKV_STAGES, sb = g % B_SBUF;
+        mbar_wait(&p_full[sb], (g / B_SBUF) & 1);
         tc_fence_after();
         const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-        const uint64_t po = static_cast<uint64_t>(pb * (16384 >> 4));
+        const uint32_t tP = tmem + sb * 128;  // P^T chunk k at column 16 k, dS^T at + 64
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < B_Q / 16; ++k) {
             const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-            tc_mma_f16(tdV, pd + po + 2 * k, gn + so + 128 * k, ID_A, acc);
-            tc_mma_f16(tdK, dd + po + 2 * k, qn + so + 128 * k, ID_A, acc);
+            tc_mma_f16_ts(tdV, tP + 16 * k, gn + so + 128 * k, ID_A, acc);
+            tc_mma_f16_ts(tdK, tP + 64 + 16 * k, qn + so + 128 * k, ID_A, acc);
           }
-          tc_commit(&pv_done[pb]);
+          tc_commit(&pv_done[sb]);
           tc_commit(&q_empty[st]);
         }
         __syncwarp();
@@ -512,7 +532,7 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
       const int key = k0 + r;
       for (int i = 0; i < n; ++i) {
         const uint32_t g = g0 + i;
-        const int st = g % BKV_STAGES, pb = g & 1, sb = g % B_SBUF;
+        const int st = g % BKV_STAGES, sb = g % B_SBUF;
         const int m0 = (qbeg + i) * B_Q;
         mbar_wait(&s_full[sb], (g / B_SBUF) & 1);
         tc_fence_after();
@@ -521,9 +541,6 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
         tmem_ld_cols<CW>(tS, sr);
         tmem_ld_cols<CW>(tS + 64, pr);
         tc_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[sb]);  // the MMA warp may refill this buffer
         mbar_wait(&q_full[st], (g / BKV_STAGES) & 1);  // lse / delta rows visible
         const float* Ls = sLD + st * 128 + cb;
         const float* Ds = Ls + 64;
@@ -560,13 +577,17 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
             }
           }
         }
-        if (g >= 2) mbar_wait(&pv_done[pb], ((g - 2) >> 1) & 1);  // tiles of block g-2 consumed
-        st_row_chunks<CW / 8>(sPt + pb * 16384, r, cb / 8, pv);
-        st_row_chunks<CW / 8>(sDt + pb * 16384, r, cb / 8, dv);
-        fence_proxy_async_smem();
+        // packed bf16 back over this group's own score columns (MMA A operands)
+        static_assert(CW == 16, "TMEM-resident P^T assumes 16 columns per warp");
+        uint32_t wv[8];
+        pack_bf16x16(pv, wv);
+        tmem_st8(tS, wv);
+        pack_bf16x16(dv, wv);
+        tmem_st8(tS + 64, wv);
+        tc_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[pb]);
+        if (lane == 0) mbar_arrive(&p_full[sb]);
       }
       mbar_wait(done, ic & 1);
       tc_fence_after();
@@ -590,7 +611,7 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
 
 constexpr int BQ_STAGES = 5, BQ_EW = 4 * BW_NG, BQ_THREADS = 128 + 32 * BQ_EW;
 constexpr int BQ_SMEM = 2 * 3 * 16384 /*Q,dO,O x2*/ + BQ_STAGES * 2 * 8192 /*K,V*/ +
-                        2 * 16384 /*dS x2*/ + 128 * BW_NG * 4 /*delta partials*/ + 1024 + 256;
+                        128 * BW_NG * 4 /*delta partials*/ + 1024 + 256;
 
 // 16 B chunk j (8 bf16) of row r in a [128 x 64] bf16 tile loaded as two
 // 128B-swizzled 64-row TMA boxes.
@@ -611,7 +632,8 @@ __device__ __forceinline__ uint4 ld_chunk128(const uint8_t* tile, int r, int j) 
 //   warp 2      TMEM allocator (512 columns)
 //   warps 4..   elementwise: BW_NG warps per TMEM lane quarter (one query
 //               row per thread, 64 / BW_NG keys each) build
-//               dS = exp2(S*c - lse) (dP - delta) into 128B-swizzled smem
+//               dS = exp2(S*c - lse) (dP - delta) as packed bf16 written back
+//               over their own score columns: the dQ MMA reads A from TMEM
 // Ring / buffer phases run on tile-global block counters, so a tile's first
 // blocks reuse buffers the previous tile released.
 __global__ void __launch_bounds__(BQ_THREADS, 1)
@@ -627,17 +649,15 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   uint8_t* sO = sG + 2 * 16384;            // O  [2][128 x 64]
   uint8_t* sK = sO + 2 * 16384;            // [ST][64 x 64]
   uint8_t* sV = sK + BQ_STAGES * 8192;     // [ST][64 x 64]
-  uint8_t* sD = sV + BQ_STAGES * 8192;     // dS [2][128 q x 64 keys]
-  float* sDelta = reinterpret_cast<float*>(sD + 2 * 16384);  // [BW_NG][128] row partials
+  float* sDelta = reinterpret_cast<float*>(sV + BQ_STAGES * 8192);  // [BW_NG][128] row partials
   uint64_t* q_full = reinterpret_cast<uint64_t*>(sDelta + 128 * BW_NG);  // [2]
   uint64_t* q_empty = q_full + 2;           // [2]
   uint64_t* kv_full = q_empty + 2;
   uint64_t* kv_empty = kv_full + BQ_STAGES;
-  uint64_t* s_full = kv_empty + BQ_STAGES;  // [B_SBUF]
-  uint64_t* s_free = s_full + B_SBUF;       // [B_SBUF]
-  uint64_t* p_full = s_free + B_SBUF;       // [2]
-  uint64_t* pv_done = p_full + 2;           // [2]
-  uint64_t* done = pv_done + 2;
+  uint64_t* s_full = kv_empty + BQ_STAGES;  // [B_SBUF] scores landed
+  uint64_t* p_full = s_full + B_SBUF;       // [B_SBUF] dS packed in TMEM
+  uint64_t* pv_done = p_full + B_SBUF;      // [B_SBUF] dQ MMAs of the buffer retired
+  uint64_t* done = pv_done + B_SBUF;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
@@ -660,9 +680,6 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
     }
     for (int i = 0; i < B_SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], BQ_EW);
-    }
-    for (int i = 0; i < 2; ++i) {
       mbar_init(&p_full[i], BQ_EW);
       mbar_init(&pv_done[i], 1);
     }
@@ -714,7 +731,6 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
     const uint64_t kd = umma_sdesc_sw128(smem_u32(sK), 16, 1024);     // K-major view
     const uint64_t vd = umma_sdesc_sw128(smem_u32(sV), 16, 1024);
     const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), 8192, 1024);   // MN-major view
-    const uint64_t dd = umma_sdesc_sw128(smem_u32(sD), 16, 1024);
     uint32_t g0 = 0, ic = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
       int bh, q0, nkb;
@@ -727,7 +743,8 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       auto issue_s = [&](uint32_t g) {
         const int st = g % BQ_STAGES, sb = g % B_SBUF;
         mbar_wait(&kv_full[st], (g / BQ_STAGES) & 1);
-        if (g >= B_SBUF) mbar_wait(&s_free[sb], ((g - B_SBUF) / B_SBUF) & 1);
+        // the buffer's previous dS has been read by its dQ MMAs
+        if (g >= B_SBUF) mbar_wait(&pv_done[sb], ((g - B_SBUF) / B_SBUF) & 1);
         tc_fence_after();
         const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
         const uint32_t tS = tmem + sb * 128;
@@ -744,16 +761,16 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       for (int j = 0; j < B_SBUF && j < nkb; ++j) issue_s(g0 + j);
       for (int j = 0; j < nkb; ++j) {
         const uint32_t g = g0 + j;
-        const int st = g % BQ_STAGES, pb = g & 1;
-        mbar_wait(&p_full[pb], (g >> 1) & 1);
+        const int st = g % BQ_STAGES, sb = g % B_SBUF;
+        mbar_wait(&p_full[sb], (g / B_SBUF) & 1);
         tc_fence_after();
         const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
-        const uint64_t po = static_cast<uint64_t>(pb * (16384 >> 4));
+        const uint32_t tD = tmem + sb * 128;  // dS key chunk k at column 16 k
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < F_BN / 16; ++k)
-            tc_mma_f16(tdQ, dd + po + 2 * k, kn + so + 128 * k, ID_A, (j > 0 || k > 0) ? 1u : 0u);
-          tc_commit(&pv_done[pb]);
+            tc_mma_f16_ts(tdQ, tD + 16 * k, kn + so + 128 * k, ID_A, (j > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&pv_done[sb]);
           tc_commit(&kv_empty[st]);
         }
         __syncwarp();
@@ -810,7 +827,7 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       const uint64_t nl22 = pack_f2(nl2, nl2), nd2 = pack_f2(-dl, -dl);
       for (int j = 0; j < nkb; ++j) {
         const uint32_t g = g0 + j;
-        const int pb = g & 1, sb = g % B_SBUF;
+        const int sb = g % B_SBUF;
         const int n0 = j * F_BN;
         mbar_wait(&s_full[sb], (g / B_SBUF) & 1);
         tc_fence_after();
@@ -819,9 +836,6 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
         tmem_ld_cols<CW>(tS, sr);
         tmem_ld_cols<CW>(tS + 64, pr);
         tc_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[sb]);
         float dv[CW];
 #pragma unroll
         for (int e = 0; e < CW; e += 2) {
@@ -841,12 +855,15 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
             if (key > row || key >= S || row >= S) dv[e] = 0.f;
           }
         }
-        if (g >= 2) mbar_wait(&pv_done[pb], ((g - 2) >> 1) & 1);
-        st_row_chunks<CW / 8>(sD + pb * 16384, r, cb / 8, dv);
-        fence_proxy_async_smem();
+        // packed bf16 dS back over this group's own score columns (MMA A operand)
+        static_assert(CW == 16, "TMEM-resident dS assumes 16 columns per warp");
+        uint32_t wv[8];
+        pack_bf16x16(dv, wv);
+        tmem_st8(tS, wv);
+        tc_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[pb]);
+        if (lane == 0) mbar_arrive(&p_full[sb]);
       }
       mbar_wait(done, ic & 1);
       tc_fence_after();
