@@ -32,8 +32,7 @@ using bf16 = __nv_bfloat16;
 constexpr int F_BM = 128, F_BN = 64, F_HD = 64, F_STAGES = 3, F_THREADS = 256;
 constexpr int F_Q_BYTES = F_BM * F_HD * 2;    // 16 KB
 constexpr int F_KV_BYTES = F_BN * F_HD * 2;   // 8 KB
-constexpr int F_P_BYTES = F_BM * F_BN * 2;    // 16 KB
-constexpr int F_SMEM = F_Q_BYTES + 2 * F_STAGES * F_KV_BYTES + 2 * F_P_BYTES + 1024 + 256;
+constexpr int F_SMEM = F_Q_BYTES + 2 * F_STAGES * F_KV_BYTES + 1024 + 256;
 constexpr float F_LN2 = 0.6931471805599453f;
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
@@ -86,8 +85,7 @@ __global__ void __launch_bounds__(F_THREADS, 2)
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + F_Q_BYTES;
   uint8_t* sV = sK + F_STAGES * F_KV_BYTES;
-  uint8_t* sP = sV + F_STAGES * F_KV_BYTES;
-  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sP + 2 * F_P_BYTES);
+  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sV + F_STAGES * F_KV_BYTES);
   uint64_t* kv_full = bar_q + 1;
   uint64_t* kv_empty = kv_full + F_STAGES;
   uint64_t* s_full = kv_empty + F_STAGES;  // [2]
@@ -153,6 +151,8 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       auto issue_s = [&](int j) {  // S_j = Q K_j^T into S[j % 2]
         const int s = j % F_STAGES;
         mbar_wait(&kv_full[s], (j / F_STAGES) & 1);
+        // S[j % 2] still holds P_{j-2}: wait until PV_{j-2} has read it
+        if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + s * F_KV_BYTES);
 #pragma unroll
@@ -168,13 +168,12 @@ __global__ void __launch_bounds__(F_THREADS, 2)
         const int s = j % F_STAGES;
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t p_addr = smem_u32(sP + (j & 1) * F_P_BYTES);
         const uint32_t v_addr = smem_u32(sV + s * F_KV_BYTES);
+        const uint32_t tP = tS + (j & 1) * 64;  // P_j packed bf16, key chunk k at column 8 k
 #pragma unroll
         for (int k = 0; k < F_BN / 16; ++k)
-          tc_mma_f16(tO, umma_sdesc_sw128(p_addr + k * 32, 16, 1024),
-                     umma_sdesc_sw128(v_addr + k * 2048, 8192, 1024), ID_O,
-                     (j > 0 || k > 0) ? 1u : 0u);
+          tc_mma_f16_ts(tO, tP + 8 * k, umma_sdesc_sw128(v_addr + k * 2048, 8192, 1024), ID_O,
+                        (j > 0 || k > 0) ? 1u : 0u);
         tc_commit(&pv_done[j & 1]);
         tc_commit(&kv_empty[s]);
       }
@@ -240,19 +239,16 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       for (int k = 0; k < 4; ++k) unpack_f2(acc2[k], sa[2 * k], sa[2 * k + 1]);
       const float sum = ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
       l = l * corr + sum;
-      // P[j % 2] was read by PV_{j-2}
-      if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
-      // P row -> smem, K-major with 128B swizzle (8 chunks of 8 bf16)
-      uint8_t* sPj = sP + (j & 1) * F_P_BYTES;
+      // P row as packed bf16 over the first 32 columns of its own score buffer
+      // (the PV MMA's A operand, read from TMEM)
+      {
+        uint32_t wv[32];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint4 u;
-        __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) hp[k] = __floats2bfloat162_rn(sv[8 * c + 2 * k], sv[8 * c + 2 * k + 1]);
-        *reinterpret_cast<uint4*>(sPj + r * 128 + ((c ^ (r & 7)) << 4)) = u;
+        for (int c = 0; c < 4; ++c) pack_bf16x16(sv + 16 * c, wv + 8 * c);
+        tmem_st16(tS + (j & 1) * 64 + lane_off, wv);
+        tmem_st16(tS + (j & 1) * 64 + lane_off + 16, wv + 16);
+        tc_wait_st();
       }
-      fence_proxy_async_smem();
       // rescale O by corr once PV_{j-1} has retired
       if (j > 0 && __any_sync(0xffffffffu, corr != 1.f && l > 0.f)) {
         mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
