@@ -46,10 +46,10 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
-# In-situ rates calibrated from tools/profile_step.py (C2, P=1): block GEMMs
-# ~0.6 PFLOP/s, the large-N LM-head GEMMs ~0.95, attention ~0.1 (fwd+bwd
-# equivalent), bandwidth-bound elementwise / norm / loss work ~3 TB/s.
-_GEMM_RATE, _HEAD_RATE, _ATTN_RATE, _HBM_RATE = 0.6e15, 0.95e15, 0.1e15, 3e12
+# In-situ rates calibrated from tools/profile_step.py (C2, P=1, round-1 kernels):
+# block GEMMs ~1.05 PFLOP/s, the large-N LM-head GEMMs ~1.2, attention ~0.35
+# (fwd+bwd equivalent), norms / reductions ~3 TB/s, the streaming loss ~6 TB/s.
+_GEMM_RATE, _HEAD_RATE, _ATTN_RATE, _HBM_RATE, _STREAM_RATE = 1.05e15, 1.2e15, 0.35e15, 3e12, 6e12
 
 
 def block_costs(cfg):
@@ -60,7 +60,7 @@ def block_costs(cfg):
     attn = 3.5 * 2.0 * T * S * d            # causal fwd + recomputing bwd
     elem = 2 * 20.0 * T * d + 2 * 6.0 * T * f  # LN, residuals, GELU, bias grads (bytes)
     blk = gemm / _GEMM_RATE + attn / _ATTN_RATE + elem / _HBM_RATE
-    head = 3 * 2.0 * T * d * V / _HEAD_RATE + 3 * 2.0 * T * V / _HBM_RATE
+    head = 3 * 2.0 * T * d * V / _HEAD_RATE + 3 * 2.0 * T * V / _STREAM_RATE
     emb = 4.0 * T * d * 4 / _HBM_RATE
     return [emb] + [blk] * cfg.layers + [head]
 
