@@ -200,6 +200,21 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
 #pragma unroll
       for (int j = 0; j < 8; ++j) s1[j] += (v0[j] + v1[j]) + (v2[j] + v3[j]);
     }
+  } else {
+    // LayerNorm statistics: 2 rows x (dy, x) in flight per iteration
+    for (; r + 8 < r1; r += 16) {
+      float v0[8], x0[8], v1[8], x1[8];
+      load8(a + r * lda, c0, cols, vec, v0);
+      load8(x + r * lda, c0, cols, vec, x0);
+      load8(a + (r + 8) * lda, c0, cols, vec, v1);
+      load8(x + (r + 8) * lda, c0, cols, vec, x1);
+      const float mu0 = mean[r], rs0 = rstd[r], mu1 = mean[r + 8], rs1 = rstd[r + 8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s1[j] += v0[j] * ((x0[j] - mu0) * rs0) + v1[j] * ((x1[j] - mu1) * rs1);
+        s2[j] += v0[j] + v1[j];
+      }
+    }
   }
   for (; r < r1; r += 8) {
     float v[8];
