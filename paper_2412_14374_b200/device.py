@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -144,19 +145,47 @@ class DeviceOps:
             self._blay = {False: gpt.block_layout(False), True: gpt.block_layout(True)}
         self._emb_ws = None
         self._red = None
+        self._red_side = None
+        self._side_stream = None
         self.step_epoch = 0  # bumped by the executor at every step
 
     # ------------------------------------------------------------------ alloc
-    def red_ws(self, rows: int, cols: int) -> tuple[int, int]:
-        """Scratch for the two-stage column reductions (kept per actor; reuse
-        is ordered by the actor's single compute stream)."""
+    def red_ws(self, rows: int, cols: int, side: bool = False) -> tuple[int, int]:
+        """Scratch for the two-stage column reductions, one per stream of the
+        actor (reuse is ordered within each stream)."""
         nb = ctypes.c_int64(0)
         call("pc_reduce_workspace_bytes", rows, cols, ctypes.byref(nb))
-        if self._red is None or self._red.numel() < nb.value:
+        key = "_red_side" if side else "_red"
+        buf = getattr(self, key)
+        if buf is None or buf.numel() < nb.value:
             n = (nb.value + 3) // 4 * 4
-            self._red = self.empty((n,), torch.uint8)
-            call("pc_fill", _lib.PC_F32, n // 4, 0.0, self._red.data_ptr(), self.st)  # counters
-        return self._red.data_ptr(), self._red.numel()
+            buf = self.empty((n,), torch.uint8)
+            call("pc_fill", _lib.PC_F32, n // 4, 0.0, buf.data_ptr(), self.st)  # counters
+            if side:  # the side stream must see the zeroed counters
+                self._fork()
+            setattr(self, key, buf)
+        return buf.data_ptr(), buf.numel()
+
+    def _side(self) -> torch.cuda.Stream:
+        """Second stream of the actor: weight gradients run here, beside the
+        data-gradient chain, and fill the wave tails of its GEMMs."""
+        if self._side_stream is None:
+            if os.environ.get("PP200_SINGLE_STREAM") == "1":  # A/B switch for profiling
+                self._side_stream = self.stream
+            else:
+                self._side_stream = torch.cuda.Stream(device=self.device)
+        return self._side_stream
+
+    def _fork(self):
+        """Side stream waits for everything issued so far on the compute stream."""
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        self._side().wait_event(ev)
+
+    def _join(self):
+        ev = torch.cuda.Event()
+        ev.record(self._side())
+        self.stream.wait_event(ev)
 
     def empty(self, shape, dtype) -> torch.Tensor:
         return torch.empty(shape, dtype=dtype, device=self.device)
@@ -420,10 +449,10 @@ class DeviceOps:
         return flat[off:off + r * c].view(c, r)
 
     def _gemm(self, out_dtype, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, epi=0, bias=None,
-              aux=None, ldaux=0, aux_out=None, ldaux_out=0):
+              aux=None, ldaux=0, aux_out=None, ldaux_out=0, st=None):
         call("pc_gemm", self.mode.pc_act, _PC[out_dtype], ta, tb, M, N, K, A.data_ptr(), lda,
              B.data_ptr(), ldb, C.data_ptr(), ldc, epi, ptr(bias), ptr(aux), ldaux, ptr(aux_out),
-             ldaux_out, self.st)
+             ldaux_out, self.st if st is None else st)
 
     def _embed(self, env):
         cfg = self.gpt
@@ -544,17 +573,24 @@ class DeviceOps:
                  dout.data_ptr(), gs("lnf_g").data_ptr(), gs("lnf_b").data_ptr(), *self.red_ws(T, d), self.st)
         else:
             dout = dz
+        # Weight gradients and their bias sums run on the side stream (they do
+        # not feed the dX chain); each fork orders them after their inputs.
+        sst = self._side().cuda_stream
+
+        def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname):
+            self._fork()
+            self._gemm(f32, 1, 0, M_, N_, T, A, lda, Bm, ldb, gs(wname), N_,
+                       _lib.EPI_SPLITK_ZERO_C, st=sst)
+            call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, M_, A.data_ptr(), lda,
+                 gs(bname).data_ptr(), 0, *self.red_ws(T, M_, side=True), sst)
+
         # MLP
-        self._gemm(f32, 1, 0, d, f, T, dout, d, sv["gu"], f, gs("w_fc2"), f, _lib.EPI_SPLITK_ZERO_C)
-        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dout.data_ptr(), d,
-             gs("b_fc2").data_ptr(), 0, *self.red_ws(T, d), self.st)
+        wgrad(d, f, dout, d, sv["gu"], f, "w_fc2", "b_fc2")
         du = self.empty((T, f), act)
         tb, B, ldb = wB("w_fc2")
         self._gemm(act, 0, tb, T, f, d, dout, d, B, ldb, du, f, _lib.EPI_GELU_GRAD,
                    aux=sv["u"], ldaux=f)
-        self._gemm(f32, 1, 0, f, d, T, du, f, sv["a2"], d, gs("w_fc1"), d, _lib.EPI_SPLITK_ZERO_C)
-        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, f, du.data_ptr(), f,
-             gs("b_fc1").data_ptr(), 0, *self.red_ws(T, f), self.st)
+        wgrad(f, d, du, f, sv["a2"], d, "w_fc1", "b_fc1")
         da2 = self.empty((T, d), act)
         tb, B, ldb = wB("w_fc1")
         self._gemm(act, 0, tb, T, d, f, du, f, B, ldb, da2, d)
@@ -564,9 +600,7 @@ class DeviceOps:
              dout.data_ptr(), dh1.data_ptr(), gs("ln2_g").data_ptr(), gs("ln2_b").data_ptr(),
              *self.red_ws(T, d), self.st)
         # attention
-        self._gemm(f32, 1, 0, d, d, T, dh1, d, sv["o"], d, gs("w_o"), d, _lib.EPI_SPLITK_ZERO_C)
-        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, d, dh1.data_ptr(), d,
-             gs("b_o").data_ptr(), 0, *self.red_ws(T, d), self.st)
+        wgrad(d, d, dh1, d, sv["o"], d, "w_o", "b_o")
         do = self.empty((T, d), act)
         tb, B, ldb = wB("w_o")
         self._gemm(act, 0, tb, T, d, d, dh1, d, B, ldb, do, d)
@@ -575,9 +609,7 @@ class DeviceOps:
         call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
              cfg.head_dim, sv["qkv"].data_ptr(), 3 * d, sv["o"].data_ptr(), do.data_ptr(), d,
              sv["lse"].data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, self.st)
-        self._gemm(f32, 1, 0, 3 * d, d, T, dqkv, 3 * d, sv["a"], d, gs("w_qkv"), d, _lib.EPI_SPLITK_ZERO_C)
-        call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, 3 * d, dqkv.data_ptr(), 3 * d,
-             gs("b_qkv").data_ptr(), 0, *self.red_ws(T, 3 * d), self.st)
+        wgrad(3 * d, d, dqkv, 3 * d, sv["a"], d, "w_qkv", "b_qkv")
         da = self.empty((T, d), act)
         tb, B, ldb = wB("w_qkv")
         self._gemm(act, 0, tb, T, d, 3 * d, dqkv, 3 * d, B, ldb, da, d)
@@ -586,6 +618,7 @@ class DeviceOps:
              ms("ln1_g").data_ptr(), sv["mean1"].data_ptr(), sv["rstd1"].data_ptr(),
              dh1.data_ptr(), dh.data_ptr(), gs("ln1_g").data_ptr(), gs("ln1_b").data_ptr(),
              *self.red_ws(T, d), self.st)
+        self._join()
         return (dh, dW)
 
     def _head_fwd(self, op, env):
