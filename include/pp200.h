@@ -120,6 +120,32 @@ int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const v
                      const float* gamma, const float* mean, const float* rstd, const void* dres,
                      void* dx, float* dgamma, float* dbeta, void* ws, int64_t ws_bytes,
                      void* stream);
+/* ---- Llama-style block pieces (BASELINE config C5; oracle/llama.py) ---- */
+/* y = x * rsqrt(mean(x^2) + eps) * gamma; rstd [rows] fp32 saved (oracle rms_norm). */
+int pc_rmsnorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const float* gamma,
+                   void* y, float* rstd, float eps, void* stream);
+/* dx = dres + RMSNorm_bwd(dy) (dres may be NULL); dgamma written (fp32, deterministic
+ * two-stage reduction in ws, see pc_reduce_workspace_bytes). (oracle rms_norm_bwd) */
+int pc_rmsnorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
+                   const float* gamma, const float* rstd, const void* dres, void* dx,
+                   float* dgamma, void* ws, int64_t ws_bytes, void* stream);
+/* In-place rotate-half rotary embedding of n_heads consecutive head_dim-wide heads per
+ * row (t [rows, ld]), angle = pos[row] * theta^(-2i/head_dim); inverse = 1 applies the
+ * transpose rotation (backward). (oracle rope) */
+int pc_rope(int dtype, int64_t rows, int64_t n_heads, int64_t head_dim, void* t, int64_t ld,
+            const int32_t* pos, float theta, int inverse, void* stream);
+/* m = silu(g) * u for gu = [g | u] (f columns each). (oracle silu) */
+int pc_swiglu_fwd(int dtype, int64_t rows, int64_t f, const void* gu, int64_t ld_gu, void* m,
+                  int64_t ld_m, void* stream);
+/* dgu = [dm * u * silu'(g) | dm * silu(g)]. */
+int pc_swiglu_bwd(int dtype, int64_t rows, int64_t f, const void* gu, int64_t ld_gu,
+                  const void* dm, int64_t ld_dm, void* dgu, int64_t ld_dgu, void* stream);
+/* Grouped-query attention heads: reduce = 0 expands [q(H)|k(Hkv)|v(Hkv)] to
+ * [q(H)|k(H)|v(H)] (query head h reads kv head h / (H/Hkv)); reduce = 1 maps the
+ * expanded gradient back, summing each kv head's group in ascending order. */
+int pc_gqa_kv(int dtype, int64_t rows, int64_t n_heads, int64_t n_kv_heads, int64_t head_dim,
+              const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int reduce,
+              void* stream);
 int pc_embedding_fwd(int dtype, int64_t T, int64_t d, int64_t seq, const int32_t* tokens,
                      const float* wte, const float* wpe, void* out, void* stream);
 int pc_embedding_bwd_workspace_bytes(int64_t T, int64_t* bytes);

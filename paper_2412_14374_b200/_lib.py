@@ -55,6 +55,13 @@ SIGNATURES: dict[str, list] = {
     "pc_layernorm_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_f, _c_p],
     "pc_layernorm_bwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                          _c_p, _c_p, _c_i64, _c_p],
+    "pc_rmsnorm_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_f, _c_p],
+    "pc_rmsnorm_bwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                       _c_i64, _c_p],
+    "pc_rope": [_c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_f, _c_i, _c_p],
+    "pc_swiglu_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p],
+    "pc_swiglu_bwd": [_c_i, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p],
+    "pc_gqa_kv": [_c_i, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i, _c_p],
     "pc_embedding_fwd": [_c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p],
     "pc_embedding_bwd_workspace_bytes": [_c_i64, ctypes.POINTER(_c_i64)],
     "pc_embedding_bwd": [_c_i, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
       load8(x + r * lda, c0, cols, vec, x0);
       load8(a + (r + 8) * lda, c0, cols, vec, v1);
       load8(x + (r + 8) * lda, c0, cols, vec, x1);
-      const float mu0 = mean[r], rs0 = rstd[r], mu1 = mean[r + 8], rs1 = rstd[r + 8];
+      const float mu0 = mean ? mean[r] : 0.f, rs0 = rstd[r], mu1 = mean ? mean[r + 8] : 0.f, rs1 = rstd[r + 8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         s1[j] += v0[j] * ((x0[j] - mu0) * rs0) + v1[j] * ((x1[j] - mu1) * rs1);
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
     } else {
       float xv[8];
       load8(x + r * lda, c0, cols, vec, xv);
-      const float mu = mean[r], rs = rstd[r];
+      const float mu = mean ? mean[r] : 0.f, rs = rstd[r];  // no mean: RMSNorm
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         s1[j] += v[j] * ((xv[j] - mu) * rs);
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
         if (MODE == 1) t2 += sm2[k][threadIdx.x];
       }
       out1[c] = accumulate ? out1[c] + t1 : t1;
-      if (MODE == 1) out2[c] = t2;
+      if (MODE == 1 && out2) out2[c] = t2;
     }
   }
   if (threadIdx.x == 0) counters[blockIdx.x] = 0u;

@@ -29,6 +29,7 @@ from . import _lib
 from ._lib import call
 from .ir import GPTConfig, OpNode, StagePartition, layout_size
 
+RMS_EPS = 1e-5  # oracle/llama.py RMS_EPS
 LN_EPS = 1e-5
 
 _PC = {torch.float32: _lib.PC_F32, torch.float64: _lib.PC_F64, torch.bfloat16: _lib.PC_BF16,
@@ -143,6 +144,8 @@ class DeviceOps:
         if gpt is not None:
             self._elay = gpt.embed_layout()
             self._blay = {False: gpt.block_layout(False), True: gpt.block_layout(True)}
+            if hasattr(gpt, "head_layout"):  # Llama-style: untied LM head
+                self._hlay = gpt.head_layout()
         self._emb_ws = None
         self._red = None
         self._red_side = None
@@ -303,6 +306,18 @@ class DeviceOps:
             env[op.result] = self._head_bwd(op, env)
         elif kind == "embed-grad":
             env[op.result] = self._embed_bwd(op, env)
+        elif kind == "llama-embed":
+            env[op.result] = Act(self._llama_embed(op, env))
+        elif kind == "llama-embed-grad":
+            env[op.result] = self._llama_embed_bwd(op, env)
+        elif kind == "llama-block":
+            self._llama_block_fwd(op, env)
+        elif kind == "llama-block-grad":
+            env[op.result] = self._llama_block_bwd(op, env)
+        elif kind == "llama-head":
+            env[op.result] = self._llama_head_fwd(op, env)
+        elif kind == "llama-head-grad":
+            env[op.result] = self._llama_head_bwd(op, env)
         else:
             raise ValueError(f"no device rule for op kind {kind!r}")
 
@@ -659,6 +674,226 @@ class DeviceOps:
         dw = self.zeros((layout_size(self._elay),), torch.float32)
         self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
                    self._slice(dw, self._elay, "wte"), d, _lib.EPI_SPLITK_ZERO_C)
+        return (dh, dw)
+
+
+    # ------------------------------------------------------- Llama pieces (C5)
+    _LLAMA_MATS = ("w_qkv", "w_o", "w_gu", "w_down")
+
+    def _zeros_cached(self, key: str, shape) -> torch.Tensor:
+        t = getattr(self, key, None)
+        if t is None or tuple(t.shape) != tuple(shape):
+            t = self.zeros(shape, torch.float32)
+            setattr(self, key, t)
+        return t
+
+    def _llama_embed(self, op, env):
+        """h0 = wte[x] (oracle/llama.py llama_step); the embedding kernel with
+        an all-zero position table."""
+        cfg = self.gpt
+        x = tensor_of(env[op.operands[0]])
+        w0: Param = env[op.operands[1]]
+        T, d = cfg.tokens, cfg.d_model
+        out = self.empty((T, d), self.mode.act)
+        zpe = self._zeros_cached("_llama_zpe", (cfg.seq_len, d))
+        call("pc_embedding_fwd", self.mode.pc_act, T, d, cfg.seq_len, x.data_ptr(),
+             self._slice(w0.master, self._elay, "wte").data_ptr(), zpe.data_ptr(),
+             out.data_ptr(), self.st)
+        return out
+
+    def _llama_embed_bwd(self, op, env):
+        cfg = self.gpt
+        g = tensor_of(env[op.operands[0]])
+        x = tensor_of(env[op.operands[1]])
+        T, d = cfg.tokens, cfg.d_model
+        dw = self.zeros((layout_size(self._elay),), torch.float32)
+        if self._emb_ws is None:
+            nb = ctypes.c_int64(0)
+            call("pc_embedding_bwd_workspace_bytes", T, ctypes.byref(nb))
+            self._emb_ws = self.empty((nb.value,), torch.uint8)
+        dpe = self.empty((cfg.seq_len, d), torch.float32)  # no position table: discarded
+        call("pc_embedding_bwd", self.mode.pc_act, T, d, cfg.seq_len, cfg.vocab, x.data_ptr(),
+             g.data_ptr(), self._slice(dw, self._elay, "wte").data_ptr(), dpe.data_ptr(),
+             self._emb_ws.data_ptr(), self._emb_ws.numel(), self.st)
+        self._emb_ws.record_stream(self.stream)
+        return dw
+
+    def _rms(self, x, g, T, d):
+        y = self.empty((T, d), self.mode.act)
+        rstd = self.empty((T,), torch.float32)
+        call("pc_rmsnorm_fwd", self.mode.pc_act, T, d, x.data_ptr(), g.data_ptr(), y.data_ptr(),
+             rstd.data_ptr(), RMS_EPS, self.st)
+        return y, rstd
+
+    def _llama_block_fwd(self, op, env):
+        """oracle/llama.py block_fwd: RMSNorm -> qkv GEMM -> RoPE(q, k) ->
+        GQA causal attention -> o GEMM (+h) -> RMSNorm -> gate/up GEMM ->
+        SwiGLU -> down GEMM (+h1) [-> final RMSNorm]."""
+        cfg = self.gpt
+        final = bool(op.attr("final_ln"))
+        lay = self._blay[final]
+        hv = env[op.operands[0]]
+        if not isinstance(hv, Act):
+            hv = env[op.operands[0]] = Act(tensor_of(hv))
+        h = hv.t
+        w: Param = env[op.operands[1]]
+        pos = tensor_of(env[op.operands[2]])
+        W, Mst = w.compute(), w.master
+        T, d, f = cfg.tokens, cfg.d_model, cfg.d_ff
+        H, Hkv, hd, qw = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.qkv_width
+        act = self.mode.act
+        sl = lambda name: self._slice(W, lay, name)
+        ms = lambda name: self._slice(Mst, lay, name)
+        a, rstd1 = self._rms(h, ms("rms1_g"), T, d)
+        qkv = self.empty((T, qw), act)
+        self._gemm(act, 0, 1, T, qw, d, a, d, sl("w_qkv"), d, qkv, qw)
+        call("pc_rope", self.mode.pc_act, T, H + Hkv, hd, qkv.data_ptr(), qw, pos.data_ptr(),
+             float(cfg.rope_theta), 0, self.st)
+        if Hkv != H:  # grouped-query: expand K/V heads for the attention kernels
+            qkv_att = self.empty((T, 3 * H * hd), act)
+            call("pc_gqa_kv", self.mode.pc_act, T, H, Hkv, hd, qkv.data_ptr(), qw,
+                 qkv_att.data_ptr(), 3 * H * hd, 0, self.st)
+        else:
+            qkv_att = qkv
+        o = self.empty((T, H * hd), act)
+        lse = self.empty((cfg.microbatch_size * H * cfg.seq_len,), torch.float32)
+        call("pc_attention_fwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len, hd,
+             qkv_att.data_ptr(), 3 * H * hd, o.data_ptr(), H * hd, lse.data_ptr(), self.st)
+        h1 = self.empty((T, d), act)
+        self._gemm(act, 0, 1, T, d, H * hd, o, H * hd, sl("w_o"), H * hd, h1, d,
+                   _lib.EPI_RESIDUAL, aux=h, ldaux=d)
+        a2, rstd2 = self._rms(h1, ms("rms2_g"), T, d)
+        gu = self.empty((T, 2 * f), act)
+        self._gemm(act, 0, 1, T, 2 * f, d, a2, d, sl("w_gu"), d, gu, 2 * f)
+        m = self.empty((T, f), act)
+        call("pc_swiglu_fwd", self.mode.pc_act, T, f, gu.data_ptr(), 2 * f, m.data_ptr(), f,
+             self.st)
+        out = self.empty((T, d), act)
+        self._gemm(act, 0, 1, T, d, f, m, f, sl("w_down"), f, out, d, _lib.EPI_RESIDUAL,
+                   aux=h1, ldaux=d)
+        saved = dict(a=a, rstd1=rstd1, qkv_att=qkv_att, o=o, lse=lse, h1=h1, a2=a2,
+                     rstd2=rstd2, gu=gu, m=m)
+        if final:
+            z, rstdf = self._rms(out, ms("rmsf_g"), T, d)
+            saved.update(out=out, rstdf=rstdf)
+            out = z
+        hv.saved[op.id] = saved
+        env[op.result] = Act(out)
+
+    def _llama_block_bwd(self, op, env):
+        """oracle/llama.py block_bwd; dX GEMMs read the transposed bf16 weight
+        shadow (K-major B), weight gradients are split-K onto zeroed fp32."""
+        cfg = self.gpt
+        final = bool(op.attr("final_ln"))
+        lay = self._blay[final]
+        dz = tensor_of(env[op.operands[0]])
+        hv = env[op.operands[1]]
+        h = tensor_of(hv)
+        w: Param = env[op.operands[2]]
+        pos = tensor_of(env[op.operands[3]])
+        sv = hv.saved[f"block{op.attr('layer')}"]
+        W, Mst = w.compute(), w.master
+        T, d, f = cfg.tokens, cfg.d_model, cfg.d_ff
+        H, Hkv, hd, qw = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.qkv_width
+        act, f32 = self.mode.act, torch.float32
+        sl = lambda name: self._slice(W, lay, name)
+        ms = lambda name: self._slice(Mst, lay, name)
+        if w.shadow is not None:
+            Wt = self._shadow_t(w, lay, self._LLAMA_MATS)
+            wB = lambda name: (1, self._slice_t(Wt, lay, name), lay[name][1][0])
+        else:
+            wB = lambda name: (0, sl(name), lay[name][1][1])
+        dW = self.zeros((layout_size(lay),), f32)
+        gs = lambda name: self._slice(dW, lay, name)
+
+        def rms_bwd(dy, x, gname, rstd, dres):
+            dx = self.empty((T, d), act)
+            call("pc_rmsnorm_bwd", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
+                 ms(gname).data_ptr(), rstd.data_ptr(), ptr(dres), dx.data_ptr(),
+                 gs(gname).data_ptr(), *self.red_ws(T, d), self.st)
+            return dx
+
+        def wgrad(M_, N_, A, lda, Bm, ldb, wname):
+            self._gemm(f32, 1, 0, M_, N_, T, A, lda, Bm, ldb, gs(wname), N_,
+                       _lib.EPI_SPLITK_ZERO_C)
+
+        dout = rms_bwd(dz, sv["out"], "rmsf_g", sv["rstdf"], None) if final else dz
+        # MLP
+        wgrad(d, f, dout, d, sv["m"], f, "w_down")
+        dm = self.empty((T, f), act)
+        tb, B, ldb = wB("w_down")
+        self._gemm(act, 0, tb, T, f, d, dout, d, B, ldb, dm, f)
+        dgu = self.empty((T, 2 * f), act)
+        call("pc_swiglu_bwd", self.mode.pc_act, T, f, sv["gu"].data_ptr(), 2 * f, dm.data_ptr(),
+             f, dgu.data_ptr(), 2 * f, self.st)
+        wgrad(2 * f, d, dgu, 2 * f, sv["a2"], d, "w_gu")
+        da2 = self.empty((T, d), act)
+        tb, B, ldb = wB("w_gu")
+        self._gemm(act, 0, tb, T, d, 2 * f, dgu, 2 * f, B, ldb, da2, d)
+        dh1 = rms_bwd(da2, sv["h1"], "rms2_g", sv["rstd2"], dout)
+        # attention
+        wgrad(d, H * hd, dh1, d, sv["o"], H * hd, "w_o")
+        do = self.empty((T, H * hd), act)
+        tb, B, ldb = wB("w_o")
+        self._gemm(act, 0, tb, T, H * hd, d, dh1, d, B, ldb, do, H * hd)
+        dqkv_att = self.empty((T, 3 * H * hd), act)
+        delta = self.empty((cfg.microbatch_size * H * cfg.seq_len,), f32)
+        call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len, hd,
+             sv["qkv_att"].data_ptr(), 3 * H * hd, sv["o"].data_ptr(), do.data_ptr(), H * hd,
+             sv["lse"].data_ptr(), delta.data_ptr(), dqkv_att.data_ptr(), 3 * H * hd, self.st)
+        if Hkv != H:  # sum each kv head's group of query-head gradients
+            dqkv = self.empty((T, qw), act)
+            call("pc_gqa_kv", self.mode.pc_act, T, H, Hkv, hd, dqkv_att.data_ptr(), 3 * H * hd,
+                 dqkv.data_ptr(), qw, 1, self.st)
+        else:
+            dqkv = dqkv_att
+        call("pc_rope", self.mode.pc_act, T, H + Hkv, hd, dqkv.data_ptr(), qw, pos.data_ptr(),
+             float(cfg.rope_theta), 1, self.st)
+        wgrad(qw, d, dqkv, qw, sv["a"], d, "w_qkv")
+        da = self.empty((T, d), act)
+        tb, B, ldb = wB("w_qkv")
+        self._gemm(act, 0, tb, T, d, qw, dqkv, qw, B, ldb, da, d)
+        dh = rms_bwd(da, h, "rms1_g", sv["rstd1"], dh1)
+        return (dh, dW)
+
+    def _llama_head_fwd(self, op, env):
+        cfg = self.gpt
+        hv = env[op.operands[0]]
+        if not isinstance(hv, Act):
+            hv = env[op.operands[0]] = Act(tensor_of(hv))
+        h = hv.t
+        wo: Param = env[op.operands[1]]
+        x = tensor_of(env[op.operands[2]])
+        T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
+        logits = self.empty((T, V), self.mode.act)
+        self._gemm(self.mode.act, 0, 1, T, V, d, h, d,
+                   self._slice(wo.compute(), self._hlay, "w_head"), d, logits, V)
+        rows = self.empty((T,), torch.float32)
+        call("pc_xent_fwd_bwd", self.mode.pc_act, T, V, cfg.seq_len, logits.data_ptr(), V,
+             x.data_ptr(), rows.data_ptr(), self.st)
+        loss = self.empty((), torch.float32)
+        call("pc_sum_f32", T, rows.data_ptr(), loss.data_ptr(), self.st)
+        hv.saved[op.id] = dict(dlogits=logits)
+        return loss
+
+    def _llama_head_bwd(self, op, env):
+        cfg = self.gpt
+        hv = env[op.operands[0]]
+        h = tensor_of(hv)
+        dlogits = hv.saved["head"]["dlogits"]
+        wo: Param = env[op.operands[1]]
+        T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
+        dh = self.empty((T, d), self.mode.act)
+        if wo.shadow is not None:
+            wt = self._shadow_t(wo, self._hlay, ("w_head",))
+            self._gemm(self.mode.act, 0, 1, T, d, V, dlogits, V,
+                       self._slice_t(wt, self._hlay, "w_head"), V, dh, d)
+        else:
+            self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V,
+                       self._slice(wo.compute(), self._hlay, "w_head"), d, dh, d)
+        dw = self.zeros((layout_size(self._hlay),), torch.float32)
+        self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
+                   self._slice(dw, self._hlay, "w_head"), d, _lib.EPI_SPLITK_ZERO_C)
         return (dh, dw)
 
 

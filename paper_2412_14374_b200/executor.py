@@ -642,9 +642,13 @@ class PipelineEngine:
         tg = self.tg
         p = tg.partition
         M = tg.schedule.num_microbatches
-        (x_in,) = sorted(p.graph.inputs)
-        tokens = p.graph.producer(x_in).attr_or("token_ids", 0) == 1
-        mbs = split_batch(batch, M)
+        # one array for a single-input graph, else {input name: array}
+        if isinstance(batch, dict):
+            feeds = {name: split_batch(v, M) for name, v in batch.items()}
+        else:
+            (x_in,) = sorted(p.graph.inputs)
+            feeds = {x_in: split_batch(batch, M)}
+        is_tok = {name: p.graph.producer(name).attr_or("token_ids", 0) == 1 for name in feeds}
         is_gpt = self.gpt is not None
         for act in actors.values():  # per-step caches on parameters start over
             act.ops.step_epoch += 1
@@ -658,8 +662,11 @@ class PipelineEngine:
                 elif buf.kind == OPT_STATE:
                     v = float(lr)
                 else:
-                    v = to_device_input(mbs[buf.meta["microbatch"]], self.mode, act.device,
-                                        tokens)
+                    name = buf.meta.get("value", buf.meta.get("input"))
+                    if name not in feeds:
+                        (name,) = feeds if len(feeds) == 1 else (None,)
+                    v = to_device_input(feeds[name][buf.meta["microbatch"]], self.mode,
+                                        act.device, is_tok[name])
                 act.store.put(bid, v)
 
     def step(self, params, batch, lr: float = 0.1, timeout_s: float = 30.0, delay_fn=None,

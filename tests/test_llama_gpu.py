@@ -1,0 +1,78 @@
+"""BASELINE config C5 shape (Llama-style: RMSNorm, RoPE, grouped-query
+attention, SwiGLU, untied head, position ids sent from stage 0 to every later
+stage) through the GPU runtime vs the float64 oracle (oracle/llama.py).
+
+Reduced width so the oracle finishes in seconds; head_dim 64 so bf16 runs the
+tcgen05 attention kernels.  fp32 at the fp32 tolerance, bf16 at 2e-2
+(max-normalised rel).
+"""
+import numpy as np
+import pytest
+
+from oracle import ffn, llama
+from paper_2412_14374_b200 import comms as C
+from paper_2412_14374_b200 import ir as I
+from paper_2412_14374_b200 import schedules as S
+from paper_2412_14374_b200 import taskgraph as T
+from paper_2412_14374_b200.executor import run_pipelined
+
+pytestmark = pytest.mark.gpu
+
+
+def _costs(cfg):
+    return [float(cfg.tokens * cfg.d_model)] + [cfg.block_fwd_flops()] * cfg.layers + \
+        [cfg.head_fwd_flops()]
+
+
+def run(kw, P, M, mode, fam="1f1b", std=0.05, seed=0, rand_pos=False):
+    base = I.LlamaConfig(**kw, yield_every=kw["layers"] + 2)
+    yields = I.balanced_yields(_costs(base), P) if P > 1 else None
+    cfg = I.LlamaConfig(**kw, yields=yields, yield_every=kw["layers"] + 2,
+                        elem_bytes=2 if mode == "bf16" else 4)
+    p = I.derive_backward(I.partition_stages(I.build_llama(cfg)))
+    s = {"gpipe": lambda: S.gpipe(P, M), "1f1b": lambda: S.one_f_one_b(P, M)}[fam]()
+    tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
+    cp = C.plan_pipeline(tg)
+    oc = dict(layers=cfg.layers, d=cfg.d_model, heads=cfg.n_heads, kv_heads=cfg.n_kv_heads,
+              ff=cfg.d_ff, vocab=cfg.vocab, seq=cfg.seq_len, mbs=cfg.microbatch_size,
+              theta=cfg.rope_theta)
+    rng = np.random.default_rng(seed)
+    params = llama.init_params(oc, rng, std=std)
+    tokens = llama.init_tokens(oc, M, rng)
+    pos = (rng.integers(0, 4 * cfg.seq_len, size=tokens.shape).astype(np.int32) if rand_pos
+           else llama.positions(oc, M))
+    g, l, w = llama.run_reference_llama(params, tokens, pos, oc)
+    rows = M * cfg.microbatch_size
+    res = run_pipelined(cp, tg, {q: v.astype(np.float32) for q, v in params.items()},
+                        {"x": tokens.reshape(rows, cfg.seq_len), "pos": pos.reshape(rows, cfg.seq_len)},
+                        mode=mode, gpt=cfg)
+    err = max([ffn.rel(res.losses, l)] + [ffn.rel(res.grads[q], g[q]) for q in g]
+              + [ffn.rel(res.new_params[q], w[q]) for q in w])
+    return err, cp, res
+
+
+C5S = dict(layers=4, d_model=256, n_heads=4, n_kv_heads=2, d_ff=384, vocab=512, seq_len=128,
+           microbatch_size=2)
+
+
+def test_c5_small_fp32_single_stage():
+    err, _, _ = run(C5S, 1, 2, "fp32", fam="gpipe", std=0.1)
+    assert err < 1e-5
+
+
+def test_c5_small_fp32_random_positions_gpipe():
+    err, cp, _ = run(C5S, 2, 4, "fp32", fam="gpipe", std=0.1, rand_pos=True)
+    assert err < 1e-5
+
+
+def test_c5_small_bf16_1f1b_skip_channels():
+    err, cp, res = run(C5S, 4, 8, "bf16")
+    assert err < 2e-2
+    # positions (and token ids for the loss) travel from stage 0 to every later stage
+    assert (0, 2) in cp.channels and (0, 3) in cp.channels
+    assert res.stats.channel_counts == {k: len(v) for k, v in cp.channels.items()}
+
+
+def test_c5_small_bf16_mha_equivalent():
+    err, _, _ = run(dict(C5S, n_kv_heads=4), 2, 4, "bf16")
+    assert err < 2e-2

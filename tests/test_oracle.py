@@ -139,3 +139,91 @@ def test_gpt_accumulation_linear_in_microbatches():
     assert abs(l1.sum() - l2.sum()) < 1e-10 * abs(l1.sum())
     for q in params:
         assert ffn.rel(g1[q], g2[q]) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# Llama-style oracle (BASELINE C5: RMSNorm, RoPE, GQA, SwiGLU, untied head)
+
+from oracle import llama  # noqa: E402
+
+LTINY = dict(layers=2, d=16, heads=4, kv_heads=2, ff=24, vocab=13, seq=6, mbs=2, theta=10000.0)
+
+
+def _lpos(cfg, rng):
+    # non-trivial position ids (e.g. packed documents) exercise RoPE fully
+    return rng.integers(0, 50, size=(cfg["mbs"], cfg["seq"])).astype(np.int32)
+
+
+def test_llama_oracle_finite_differences():
+    rng = np.random.default_rng(3)
+    params = llama.init_params(LTINY, rng, std=0.3)
+    tokens = llama.init_tokens(LTINY, 1, rng)[0]
+    pos = _lpos(LTINY, rng)
+    _, grads = llama.llama_step(params, tokens, pos, LTINY)
+    eps = 1e-6
+    for q, flat in params.items():
+        idx = rng.choice(flat.size, size=min(25, flat.size), replace=False)
+        for j in idx:
+            saved = flat[j]
+            flat[j] = saved + eps
+            up = llama.llama_step(params, tokens, pos, LTINY)[0]
+            flat[j] = saved - eps
+            dn = llama.llama_step(params, tokens, pos, LTINY)[0]
+            flat[j] = saved
+            fd = (up - dn) / (2 * eps)
+            assert abs(fd - grads[q][j]) <= 1e-6 * max(1.0, abs(fd)), (q, j, fd, grads[q][j])
+
+
+def test_llama_oracle_matches_torch_autograd():
+    torch = pytest.importorskip("torch")
+    F = torch.nn.functional
+    cfg = dict(layers=2, d=32, heads=4, kv_heads=2, ff=40, vocab=29, seq=9, mbs=3, theta=500.0)
+    rng = np.random.default_rng(4)
+    params = llama.init_params(cfg, rng, std=0.2)
+    tokens = llama.init_tokens(cfg, 1, rng)[0]
+    pos = _lpos(cfg, rng)
+    loss, grads = llama.llama_step(params, tokens, pos, cfg)
+
+    tp = {q: torch.tensor(v, dtype=torch.float64, requires_grad=True) for q, v in params.items()}
+    B, S, d, H, Hkv, f = cfg["mbs"], cfg["seq"], cfg["d"], cfg["heads"], cfg["kv_heads"], cfg["ff"]
+    hd = d // H
+
+    def view(flat, layout):
+        return {k: flat[o:o + math.prod(dims)].reshape(dims) for k, (o, dims) in layout.items()}
+
+    def rms(x, g):
+        return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + llama.RMS_EPS) * g
+
+    ang = torch.tensor(pos.reshape(-1), dtype=torch.float64)[:, None] * \
+        cfg["theta"] ** (-torch.arange(0, hd // 2, dtype=torch.float64) * 2.0 / hd)
+    cos, sin = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+
+    def rope(t):  # [T, nh, hd], rotate-half
+        t1, t2 = t[..., :hd // 2], t[..., hd // 2:]
+        return torch.cat([t1 * cos - t2 * sin, t2 * cos + t1 * sin], -1)
+
+    tok = torch.tensor(tokens, dtype=torch.long)
+    h = view(tp["w0"], llama.embed_layout(cfg)[0])["wte"][tok.reshape(-1)]
+    for k in range(1, cfg["layers"] + 1):
+        final = k == cfg["layers"]
+        P = view(tp[f"w{k}"], llama.block_layout(cfg, final)[0])
+        qkv = rms(h, P["rms1_g"]) @ P["w_qkv"].T
+        q = rope(qkv[:, :H * hd].reshape(-1, H, hd))
+        kk = rope(qkv[:, H * hd:(H + Hkv) * hd].reshape(-1, Hkv, hd))
+        v = qkv[:, (H + Hkv) * hd:].reshape(-1, Hkv, hd)
+        q4 = q.reshape(B, S, H, hd).transpose(1, 2)
+        k4 = kk.reshape(B, S, Hkv, hd).transpose(1, 2).repeat_interleave(H // Hkv, dim=1)
+        v4 = v.reshape(B, S, Hkv, hd).transpose(1, 2).repeat_interleave(H // Hkv, dim=1)
+        o = F.scaled_dot_product_attention(q4, k4, v4, is_causal=True)
+        h = h + o.transpose(1, 2).reshape(B * S, H * hd) @ P["w_o"].T
+        gu = rms(h, P["rms2_g"]) @ P["w_gu"].T
+        h = h + (F.silu(gu[:, :f]) * gu[:, f:]) @ P["w_down"].T
+        if final:
+            h = rms(h, P["rmsf_g"])
+    logits = (h @ view(tp["wout"], llama.head_layout(cfg)[0])["w_head"].T).reshape(B, S, -1)
+    tl = F.cross_entropy(logits[:, :-1].reshape(-1, logits.shape[-1]), tok[:, 1:].reshape(-1),
+                         reduction="sum")
+    tl.backward()
+    assert abs(tl.item() - loss) < 1e-10 * abs(loss)
+    for q in params:
+        assert ffn.rel(tp[q].grad.numpy(), grads[q]) < 1e-10, q
