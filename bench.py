@@ -302,6 +302,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--microbatches", type=int, default=M_MICRO)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gantt", default=None, help="write the measured timeline as an SVG Gantt chart")
     ap.add_argument("--no-graph", action="store_true",
                     help="issue every step from Python instead of replaying the captured graph")
     args = ap.parse_args()
@@ -401,7 +402,14 @@ def main():
         dist.all_gather_object(gathered, timeline)
         timeline = [e for part in gathered for e in part]
     from paper_2412_14374_b200.executor import RunStats
+    from paper_2412_14374_b200 import timeline as TL
     bubble = RunStats(timeline=timeline).bubble_fraction(P)
+    # achievable ideal: the plan replayed with the measured task durations and
+    # free transfers / dispatch
+    achievable = TL.replay(cp, TL.task_durations(timeline)).bubble_fraction(P)
+    if args.gantt and rank == 0:
+        with open(args.gantt, "w") as f:
+            f.write(TL.render_svg(timeline, P, title=f"C2 1F1B P={P} M={M} measured,"))
 
     tokens_per_step = M * cfg.tokens
     value = tokens_per_step / (ms / 1000)
@@ -430,7 +438,8 @@ def main():
                        "issue": "cuda-graph replay per actor" if use_graph else "python per op"},
             "model_tflops_per_gpu": round(tflops_gpu, 1),
             "frac_of_bf16_peak": round(tflops_gpu / burst, 4),
-            "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4)},
+            "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4),
+                       "achievable": round(achievable, 4)},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e, 1), "unit": "tokens/s",
