@@ -125,7 +125,8 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list = []  # (arrival time, csv line)
+        self.window = None     # (t0, t1) of the timed region, perf_counter clock
 
     def start(self):
         try:
@@ -140,7 +141,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_first(self, timeout_s: float = 5.0):
+        """nvidia-smi needs up to ~1 s before its first sample: wait for it so a
+        short timed region is still covered."""
+        t_end = time.perf_counter() + timeout_s
+        while self.proc is not None and not self.lines and time.perf_counter() < t_end:
+            time.sleep(0.05)
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -152,7 +160,13 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None and lines:
+            t0, t1 = self.window
+            inside = [x for x in lines if t0 - 0.1 <= x[0] <= t1 + 0.3]
+            # a region shorter than the 200 ms period: the samples nearest to it
+            lines = inside or sorted(lines, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))[:2]
+        for _, ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -359,6 +373,7 @@ def main():
     # ---- device-resident timed region ----
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_first()
     barrier()
     launches0 = _lib.launch_count
     t0 = time.perf_counter()
@@ -369,6 +384,7 @@ def main():
     ev1.record()
     barrier()
     wall = time.perf_counter() - t0
+    clocks.window = (t0, t0 + wall)
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     launches = cap.launches if use_graph else int((_lib.launch_count - launches0) / args.steps)
     clk = clocks.stop()
