@@ -218,9 +218,42 @@ def numerics_docs():
     return out
 
 
+CLI_CONFIGS = [
+    {"version": 1, "model": {"layers": 4, "width": 8, "microbatch_size": 4, "yield_every": 2},
+     "parallel": {"num_actors": 2, "num_microbatches": 4, "schedule": "gpipe"}},
+    {"version": 1, "model": {"layers": 8, "width": 6, "microbatch_size": 2, "yield_every": 2,
+                             "tied_weights": True},
+     "parallel": {"num_actors": 4, "num_microbatches": 8, "schedule": "1f1b"}},
+    {"version": 1, "model": {"layers": 8, "width": 4, "microbatch_size": 2, "yield_every": 1},
+     "parallel": {"num_actors": 2, "num_microbatches": 4, "schedule": "interleaved",
+                  "circular_repeat": 4, "commute_shared_grads": False}},
+]
+
+
+def cli_plan_docs():
+    """sha256 of the three files ``pipecraft plan`` writes (cli.py:194-204)."""
+    import contextlib
+    import io
+    import tempfile
+
+    from pipecraft import cli
+    out = []
+    for doc in CLI_CONFIGS:
+        with tempfile.TemporaryDirectory() as d:
+            cfg_doc = dict(doc, output={"dir": d})
+            with contextlib.redirect_stdout(io.StringIO()):
+                rc = cli.cmd_plan(cli.RunConfig(cfg_doc, pathlib.Path(d)))
+            assert rc == 0
+            files = {n: sha((pathlib.Path(d) / n).read_text())
+                     for n in ("schedule.json", "taskgraph.json", "commplan.json")}
+        out.append({"config": doc, "files": files})
+    return out
+
+
 def main():
     plans = {"ffn": [plan_doc(c) for c in ffn_grid()], "gpt_mirror": gpt_docs(),
-             "random": random_docs(), "crossing": crossing_doc()}
+             "random": random_docs(), "crossing": crossing_doc(),
+             "cli_plan": cli_plan_docs()}
     (OUT / "plans.json").write_text(json.dumps(plans, indent=1, sort_keys=True) + "\n")
     p = I.derive_backward(I.partition_stages(I.build_model(I.ModelConfig(
         layers=4, width=8, microbatch_size=4, yield_every=2))))

@@ -125,3 +125,39 @@ def test_balanced_yields():
     assert I.balanced_yields([1, 4, 4, 4, 4, 9], 3) == (3, 5)
     ys = I.balanced_yields([0.1] + [1.0] * 12 + [4.5], 4)
     assert len(ys) == 3 and ys[-1] == 13
+
+
+@pytest.mark.parametrize("k", range(len(GOLD["cli_plan"])))
+def test_plan_artifacts_match_reference_cli(k, tmp_path):
+    """schedule.json / taskgraph.json / commplan.json byte-identical to what
+    ``pipecraft plan`` writes for the same config (cli.py:194-204)."""
+    from paper_2412_14374_b200 import plan_io
+    doc = GOLD["cli_plan"][k]
+    cfg = plan_io.PlanConfig(dict(doc["config"], output={"dir": str(tmp_path)}), tmp_path)
+    _, s, tg, cp = plan_io.compile_plan(cfg)
+    files = plan_io.write_plan(cfg.out_dir, s, tg, cp)
+    for name, want in doc["files"].items():
+        assert sha(files[name].read_text()) == want, name
+    # the written artifacts load back: schedule file drives an identical plan
+    again = plan_io.PlanConfig(dict(doc["config"], parallel=dict(
+        doc["config"]["parallel"], schedule_file="schedule.json")), tmp_path)
+    _, _, _, cp2 = plan_io.compile_plan(again)
+    assert cp2.to_json_str() == cp.to_json_str()
+    assert plan_io.load_commplan(files["commplan.json"]).to_json_str() == cp.to_json_str()
+
+
+def test_plan_config_errors_cite_fields(tmp_path):
+    from paper_2412_14374_b200 import plan_io
+    base = {"model": {"layers": 4, "width": 4, "microbatch_size": 2, "yield_every": 2},
+            "parallel": {"num_actors": 2, "num_microbatches": 4}}
+    with pytest.raises(plan_io.ConfigError, match="^model.layers"):
+        plan_io.PlanConfig({"model": {"width": 4, "microbatch_size": 2},
+                            "parallel": base["parallel"]})
+    with pytest.raises(plan_io.ConfigError, match="^parallel.schedule:"):
+        plan_io.PlanConfig(dict(base, parallel=dict(base["parallel"], schedule="zb")))
+    with pytest.raises(plan_io.ConfigError, match="^model.yield_every"):
+        plan_io.compile_plan(plan_io.PlanConfig(dict(base, parallel=dict(base["parallel"],
+                                                                          num_actors=4))))
+    with pytest.raises(plan_io.ConfigError, match="^config: invalid JSON"):
+        (tmp_path / "bad.json").write_text("{")
+        plan_io.PlanConfig.load(tmp_path / "bad.json")
