@@ -424,17 +424,23 @@ class DeviceOps:
     def concat_losses(self, parts) -> torch.Tensor:
         return self._concat([tensor_of(p) for p in parts])
 
-    def sgd(self, w, g, lr: float):
-        """executor.py:340-344: w - lr*g (fp32/fp64 master; bf16 shadow refreshed)."""
+    def sgd(self, w, g, lr: float, inplace: bool = False):
+        """executor.py:340-344: w - lr*g (fp32/fp64 master; bf16 shadow refreshed).
+
+        ``inplace``: the update overwrites ``w`` (resident training state,
+        every reader of w is ordered before the update by the task graph)."""
         if isinstance(w, Param):
             master = w.master
-            newm = self.empty(master.shape, master.dtype)
-            shadow = self.empty(master.shape, torch.bfloat16) if w.shadow is not None else None
+            if inplace:
+                newm, shadow = master, w.shadow
+            else:
+                newm = self.empty(master.shape, master.dtype)
+                shadow = self.empty(master.shape, torch.bfloat16) if w.shadow is not None else None
             call("pc_sgd_update", _PC[master.dtype], master.numel(), master.data_ptr(),
                  tensor_of(g).data_ptr(), float(lr), newm.data_ptr(), ptr(shadow), self.st)
-            return Param(newm, shadow)
+            return w if inplace else Param(newm, shadow)
         wt = tensor_of(w)
-        out = self.empty(wt.shape, wt.dtype)
+        out = wt if inplace else self.empty(wt.shape, wt.dtype)
         call("pc_sgd_update", _PC[wt.dtype], wt.numel(), wt.data_ptr(), tensor_of(g).data_ptr(),
              float(lr), out.data_ptr(), None, self.st)
         return out

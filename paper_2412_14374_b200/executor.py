@@ -50,6 +50,7 @@ from .comms import (
     SendWait,
     _brief,
 )
+from .device import _PC as _PC_OF
 from .device import MODES, Act, DeviceOps, Mode, Param, strip, tensor_of, to_device_input, \
     to_device_param
 from .ir import GPTConfig
@@ -382,8 +383,9 @@ class DeviceStore:
 
 class _Actor:
     def __init__(self, actor: int, tg: TaskGraph, ops: DeviceOps, stats: RunStats,
-                 timeline: bool):
+                 timeline: bool, inplace: bool = False):
         self.actor = actor
+        self.inplace = inplace       # resident training state: SGD overwrites the param
         self.tg = tg
         self.device = ops.device
         self.stream = ops.stream
@@ -442,7 +444,7 @@ class _Actor:
             st.put(ex["out"], self.ops.concat_losses([st.get(b, at) for b in ex["parts"]]))
         elif kind == "sgd-update":
             st.put(ex["out"], self.ops.sgd(st.get(ex["param"], at), st.get(ex["grad"], at),
-                                           st.get(ex["lr"], at)))
+                                           st.get(ex["lr"], at), inplace=self.inplace))
         else:
             raise ExecutorFault(f"unknown task payload {kind!r}")
         if self.timeline:
@@ -480,7 +482,7 @@ def _wire_meta_fn(tg: TaskGraph, mode: Mode):
 
 
 def _worker(act: _Actor, instrs, tg: TaskGraph, channels: dict, ctl: _Control, delay_fn,
-            counting):
+            counting, epilogue=None):
     a = act.actor
     try:
         with torch.cuda.device(act.device), torch.cuda.stream(act.stream):
@@ -517,6 +519,8 @@ def _worker(act: _Actor, instrs, tg: TaskGraph, channels: dict, ctl: _Control, d
                 else:
                     raise ExecutorFault(f"actor {a}: unknown instruction {ins!r}")
                 act.last_issued = idx
+            if epilogue is not None:
+                epilogue(act, ctl)
             act.end_event = torch.cuda.Event()
             act.end_event.record(act.stream)
         ctl.heartbeat[a] = "done"
@@ -554,6 +558,29 @@ def exchange_channel_ids(store, tag: str, me: int, channels, new_id) -> dict:
             raw = store.get(key)
         out[(src, dst)] = bytes(raw)
     return out
+
+
+def tied_holders(tg: TaskGraph) -> list:
+    """[(param, low actor, {holder actor: param buffer id})] for parameters held
+    by more than one actor (tied weights).  The reference updates such a
+    parameter only on the actor owning its lowest stage (taskgraph.py:349-361);
+    a multi-step run must carry the new value to the other holders before
+    their next use -- the re-broadcast of SURVEY.md §8(f) item 4."""
+    holders: dict = {}
+    for bid, b in tg.buffers.items():
+        if b.kind == PARAM and b.producer is None:   # seeded copies, not wnew outputs
+            holders.setdefault(b.meta["param"], {})[b.home] = bid
+    out = []
+    for q in sorted(holders):
+        if len(holders[q]) > 1:
+            out.append((q, tg.tasks[f"opt:{q}"].actor, dict(sorted(holders[q].items()))))
+    return out
+
+
+def _clone_value(v):
+    if isinstance(v, Param):
+        return Param(v.master.clone(), None if v.shadow is None else v.shadow.clone())
+    return tensor_of(v).clone()
 
 
 def _dist_world():
@@ -600,14 +627,20 @@ class PipelineEngine:
                 raise ExecutorFault("single-process multi-GPU channels are not supported; "
                                     "launch one process per GPU (torchrun)")
         self._wire_meta = _wire_meta_fn(tg, self.mode)
+        self._resident: dict | None = None   # bid -> device value (load_params)
+        self._tied = tied_holders(tg)
+        self._tied_ch: dict = {}
+        self._tied_ready = False
+        self._captures: list = []
         self._ops = {a: DeviceOps(tg.partition, self.mode, self.devices[a],
                                   torch.cuda.Stream(device=self.devices[a]), gpt)
                      for a in self.local}
         self._channels = self._make_channels()
 
-    def _make_channels(self):
+    def _make_channels(self, keys=None, wire_meta=None):
+        keys = self.cp.channels if keys is None else keys
         if not self.distributed:
-            return {key: LocalChannel(*key) for key in self.cp.channels}
+            return {key: LocalChannel(*key) for key in keys}
         import ctypes
 
         import torch.distributed as dist
@@ -615,6 +648,7 @@ class PipelineEngine:
         tag = next(_ENGINE_IDS)
         me = self.local[0]
         dev = self.devices[me]
+        wire_meta = self._wire_meta if wire_meta is None else wire_meta
 
         def new_id() -> bytes:
             uid = (ctypes.c_char * 128)()
@@ -622,17 +656,98 @@ class PipelineEngine:
             return bytes(uid)
 
         out = {}
-        for (src, dst), raw in exchange_channel_ids(store, f"e{tag}", me, self.cp.channels,
+        for (src, dst), raw in exchange_channel_ids(store, f"e{tag}", me, keys,
                                                     new_id).items():
             idbuf = (ctypes.c_char * 128).from_buffer_copy(raw)
             comm = ctypes.c_void_p()
             with torch.cuda.device(dev):
                 _lib.call("pc_p2p_comm_init", ctypes.byref(comm), 2, idbuf, 0 if me == src else 1)
-            out[(src, dst)] = NcclChannel(src, dst, me, comm, dev, self._wire_meta)
+            out[(src, dst)] = NcclChannel(src, dst, me, comm, dev, wire_meta)
         return out
 
+    # -- resident training state (multi-step) --
+    def load_params(self, params):
+        """Keep ``params`` resident on this process's actors for multi-step
+        training: one private copy per holding actor (executor.py:409-410
+        copies per actor too).  Afterwards ``step(None, batch)`` /
+        ``capture(None, batch)`` train in place: the SGD task overwrites the
+        resident value, and each tied parameter's new value is sent from the
+        actor that updated it to its other holders at the end of the step
+        (one extra message per holder, on its own channel), so step k+1 sees
+        exactly what the reference would seed from step k's ``new_params``."""
+        is_gpt = self.gpt is not None
+        res = {}
+        for bid, buf in self.tg.buffers.items():
+            if buf.kind != PARAM or buf.producer is not None or buf.home not in self.local:
+                continue
+            dev = self.devices[buf.home]
+            with torch.cuda.device(dev):
+                res[bid] = _clone_value(to_device_param(params[buf.meta["param"]], self.mode,
+                                                        dev, is_gpt))
+        for d in {self.devices[a] for a in self.local}:
+            torch.cuda.synchronize(d)
+        self._resident = res
+        if not self._tied_ready:   # every rank takes this branch once (same channel tags)
+            self._tied_ready = True
+            keys = sorted({(low, h) for _, low, hs in self._tied for h in hs if h != low})
+            g = self.tg.partition.graph
+
+            def meta(bid):
+                return tuple(g.spec_of(bid.split(":", 1)[1]).dims), self.mode.master
+            if keys:
+                self._tied_ch = self._make_channels(keys, meta)
+
+    def state_dict(self, to_host: bool = True) -> dict:
+        """{param: current value} for the parameters this process updates
+        (each taken from the actor owning its lowest stage)."""
+        if self._resident is None:
+            raise ExecutorFault("no resident parameters: call load_params first")
+        out = {}
+        for bid, v in self._resident.items():
+            b = self.tg.buffers[bid]
+            q = b.meta["param"]
+            if self.tg.tasks[f"opt:{q}"].actor != b.home:
+                continue
+            t = v.master if isinstance(v, Param) else tensor_of(v)
+            out[q] = t.detach().cpu().numpy() if to_host else t
+        return out
+
+    def _rebroadcast(self, act, ctl):
+        """End-of-step epilogue in resident mode: low actor -> other holders."""
+        a = act.actor
+        for seq, (q, low, hs) in enumerate(self._tied):
+            if a == low:
+                src = self._resident[hs[low]]
+                t = src.master if isinstance(src, Param) else tensor_of(src)
+                for h in hs:
+                    if h == low:
+                        continue
+                    ch = self._tied_ch[(low, h)]
+                    ch.send(seq, f"wnew:{q}", t, act.stream)
+                    if isinstance(ch, NcclChannel):
+                        act.stream.wait_event(ch.sent[seq])   # joins the send stream
+            elif a in hs:
+                ch = self._tied_ch[(low, a)]
+                ch.post_recv(seq, f"wnew:{q}", act.stream)
+                _, buf = ch.recv(seq, ctl, a, act.stream)
+                dst = self._resident[hs[a]]
+                m = dst.master if isinstance(dst, Param) else tensor_of(dst)
+                m.copy_(buf)
+                if isinstance(dst, Param) and dst.shadow is not None:
+                    _lib.call("pc_cast", _PC_OF[m.dtype], _lib.PC_BF16, m.numel(), m.data_ptr(),
+                              dst.shadow.data_ptr(), act.stream.cuda_stream)
+
     def close(self):
-        for ch in self._channels.values():
+        # graphs that captured NCCL work pin their communicators: release the
+        # graphs first, then destroy
+        for cs in self._captures:
+            if cs.graph is not None:
+                cs.graph.reset()
+                cs.graph = None
+        self._captures.clear()
+        for d in {self.devices[a] for a in self.local}:
+            torch.cuda.synchronize(d)
+        for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             if isinstance(ch, NcclChannel) and ch.comm:
                 _lib.call("pc_p2p_destroy", ch.comm)
                 ch.comm = None
@@ -650,6 +765,8 @@ class PipelineEngine:
             feeds = {x_in: split_batch(batch, M)}
         is_tok = {name: p.graph.producer(name).attr_or("token_ids", 0) == 1 for name in feeds}
         is_gpt = self.gpt is not None
+        if params is None and self._resident is None:
+            raise ExecutorFault("params=None needs resident parameters (load_params)")
         for act in actors.values():  # per-step caches on parameters start over
             act.ops.step_epoch += 1
         for bid, buf in tg.buffers.items():
@@ -658,7 +775,8 @@ class PipelineEngine:
             act = actors[buf.home]
             with torch.cuda.device(act.device), torch.cuda.stream(act.stream):
                 if buf.kind == PARAM:
-                    v = to_device_param(params[buf.meta["param"]], self.mode, act.device, is_gpt)
+                    v = (self._resident[bid] if params is None else
+                         to_device_param(params[buf.meta["param"]], self.mode, act.device, is_gpt))
                 elif buf.kind == OPT_STATE:
                     v = float(lr)
                 else:
@@ -675,9 +793,11 @@ class PipelineEngine:
         stats = RunStats()
         tl = self.timeline if timeline is None else timeline
         ctl = _Control(timeout_s)
-        for ch in self._channels.values():
+        resident = params is None
+        for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             ch.reset()
-        actors = {a: _Actor(a, self.tg, self._ops[a], stats, tl) for a in self.local}
+        actors = {a: _Actor(a, self.tg, self._ops[a], stats, tl, inplace=resident)
+                  for a in self.local}
         for a, act in actors.items():
             # params / inputs are copied on the current stream; the actor stream waits
             with torch.cuda.device(act.device):
@@ -698,7 +818,8 @@ class PipelineEngine:
             stats.driver_messages += 1  # program dispatch
             w = threading.Thread(target=_worker, name=f"actor-{a}",
                                  args=(actors[a], self.cp.programs[a].instrs, self.tg,
-                                       self._channels, ctl, delay_fn, counting), daemon=True)
+                                       self._channels, ctl, delay_fn, counting,
+                                       self._rebroadcast if resident else None), daemon=True)
             workers.append(w)
             w.start()
         for w in workers:
@@ -712,7 +833,7 @@ class PipelineEngine:
         if ctl.faults:
             raise ctl.faults[0]
         self._wait_devices(actors, ctl)
-        for key, ch in self._channels.items():
+        for key, ch in list(self._channels.items()) + list(self._tied_ch.items()):
             if not ch.drained():
                 raise ChannelOrderFault(f"channel {key} holds undelivered messages at step end")
         # after the device finished, in-flight sends are complete: final flush
@@ -737,9 +858,10 @@ class PipelineEngine:
         a = self.local[0]
         stats = RunStats()
         ctl = _Control(timeout_s)
-        for ch in self._channels.values():
+        resident = params is None
+        for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             ch.reset()
-        act = _Actor(a, self.tg, self._ops[a], stats, timeline)
+        act = _Actor(a, self.tg, self._ops[a], stats, timeline, inplace=resident)
         actors = {a: act}
         with torch.cuda.device(act.device):
             act.stream.wait_stream(torch.cuda.current_stream(act.device))
@@ -763,12 +885,12 @@ class PipelineEngine:
             torch.cuda.synchronize()
             with torch.cuda.graph(graph, stream=act.stream):
                 _worker(act, self.cp.programs[a].instrs, self.tg, self._channels, ctl, None,
-                        counting)
+                        counting, self._rebroadcast if resident else None)
         if ctl.faults:
             raise ctl.faults[0]
         # send-completion events recorded into the graph cannot be queried; every
         # replay runs the sends to completion, so the captured buffers are free.
-        for ch in self._channels.values():
+        for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             if isinstance(ch, NcclChannel):
                 ch.sent.clear()
         act.store.flush()
@@ -776,11 +898,12 @@ class PipelineEngine:
         result = self._gather(actors, stats, strict_store=False, to_host=False)
         act.timeline = tl_on
         cs = CapturedStep(self, graph, act, inputs, result)
+        self._captures.append(cs)
         cs.launches = _lib.launch_count - launches0   # libpp200 calls recorded per replay
         return cs
 
     def _abort_channels(self):
-        for ch in self._channels.values():
+        for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             ch.abort()
 
     def _wait_devices(self, actors, ctl: _Control):
@@ -867,6 +990,8 @@ class CapturedStep:
             dst.copy_(src.to(dst.dtype) if src.dtype != dst.dtype else src, non_blocking=True)
 
     def replay(self, batch=None):
+        if self.graph is None:
+            raise ExecutorFault("captured step was released (engine closed)")
         if batch is not None:
             self.set_inputs(batch)
         self.graph.replay()

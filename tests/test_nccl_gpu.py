@@ -33,7 +33,34 @@ def _worker(rank, world, port, case, q):
         from paper_2412_14374_b200 import ir as I
         from paper_2412_14374_b200 import schedules as S
         from paper_2412_14374_b200 import taskgraph as T
-        from paper_2412_14374_b200.executor import run_pipelined
+        from paper_2412_14374_b200.executor import PipelineEngine, run_pipelined
+        if case == "ffn-train":
+            # resident multi-step training: eager step, then a captured graph
+            # replayed twice; the tied w0 is re-broadcast 0 -> P-1 every step
+            L, M, K = 2 * world, 4, 3
+            p = I.derive_backward(I.partition_stages(I.build_model(I.ModelConfig(
+                layers=L, width=16, microbatch_size=8, yield_every=2, tied_weights=True))))
+            s = S.one_f_one_b(world, M)
+            tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
+            cp = C.plan_pipeline(tg)
+            rng = np.random.default_rng(0)
+            params = ffn.init_params({q: p.graph.spec_of(q).dims for q in p.graph.params}, rng)
+            batches = [ffn.init_batch(M, 8, 16, rng) for _ in range(K)]
+            eng = PipelineEngine(cp, tg, mode="fp64")
+            eng.load_params(params)
+            losses = [eng.step(None, batches[0], lr=0.01).losses]
+            cs = eng.capture(None, batches[1], lr=0.01)
+            for k in (1, 2):
+                r = cs.replay(torch.from_numpy(batches[k]))
+                losses.append(None if r.losses is None else r.losses.cpu().numpy())
+            state = eng.state_dict()
+            eng.close()
+            ref, ref_losses = dict(params), []
+            for k in range(K):
+                _, lk, ref = ffn.run_reference_ffn(ref, batches[k], M, L, True, lr=0.01)
+                ref_losses.append(lk)
+            q.put((rank, state, losses, ref, ref_losses))
+            return
         if case == "ffn":
             L, M = 2 * world, 4
             p = I.derive_backward(I.partition_stages(I.build_model(I.ModelConfig(
@@ -111,3 +138,18 @@ def test_two_gpu_nccl_pipeline_matches_oracle(case, tol):
         assert ffn.rel(new[q], w_ref[q]) < tol, q
     assert counts == plan_counts
     assert drv == 2 * world
+
+
+def test_two_gpu_resident_training_rebroadcasts_tied_weight():
+    outs = _run("ffn-train", 2)
+    from oracle import ffn
+    state, losses = {}, None
+    for rank, st, ls, ref, ref_losses in outs:
+        state.update(st)
+        if ls[0] is not None:
+            losses = ls
+    assert sorted(state) == sorted(ref)
+    for k in range(3):
+        assert ffn.rel(losses[k], ref_losses[k]) < 1e-12, k
+    for q in ref:
+        assert ffn.rel(state[q], ref[q]) < 1e-12, q
