@@ -345,15 +345,19 @@ def main():
     tokens_dev = torch.from_numpy(tokens_host).to(dev)
     tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
     eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
+    # resident training state: every step (eager or replayed) is a real SGD
+    # step on the previous step's weights, tied w0 re-broadcast included
+    eng.load_params(params)
+    del params
     use_graph = not args.no_graph
     for _ in range(2):   # eager warm-up: NCCL connections, kernel attributes, allocator
-        eng.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False)
+        eng.step(None, tokens_dev, lr=1e-4, timeout_s=600, to_host=False)
     torch.cuda.synchronize()
     if use_graph:
-        cap = eng.capture(params, tokens_dev, lr=1e-4)
+        cap = eng.capture(None, tokens_dev, lr=1e-4)
         run = lambda b: cap.replay(None if b is tokens_dev else b)
     else:
-        run = lambda b: eng.step(params, b, lr=1e-4, timeout_s=600, to_host=False)
+        run = lambda b: eng.step(None, b, lr=1e-4, timeout_s=600, to_host=False)
     for _ in range(max(args.warmup, 3)):
         run(tokens_dev)
     torch.cuda.synchronize()
@@ -404,14 +408,14 @@ def main():
     # ---- one instrumented step (same warmed engine) for the bubble ----
     barrier()
     if use_graph:
-        cap_tl = eng.capture(params, tokens_dev, lr=1e-4, timeline=True)
+        cap_tl = eng.capture(None, tokens_dev, lr=1e-4, timeline=True)
         barrier()
         cap_tl.replay()
         barrier()
         timeline = cap_tl.timeline()
-        del cap_tl
+        cap_tl.release()
     else:
-        timeline = eng.step(params, tokens_dev, lr=1e-4, timeout_s=600, to_host=False,
+        timeline = eng.step(None, tokens_dev, lr=1e-4, timeout_s=600, to_host=False,
                             timeline=True).stats.timeline
     if world > 1:
         gathered = [None] * world
@@ -451,7 +455,9 @@ def main():
                        "microbatches": M, "microbatch_size": cfg.microbatch_size,
                        "schedule": "1f1b", "stages": P, "yields": list(cfg.yields or []),
                        "parallelism": f"pp{P}", "l2": "inputs > L2 (no flush needed)",
-                       "issue": "cuda-graph replay per actor" if use_graph else "python per op"},
+                       "issue": "cuda-graph replay per actor" if use_graph else "python per op",
+                       "training": "resident params, in-place SGD each step"
+                                   + (", tied w0 re-broadcast to the head stage" if P > 1 else "")},
             "model_tflops_per_gpu": round(tflops_gpu, 1),
             "frac_of_bf16_peak": round(tflops_gpu / burst, 4),
             "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4),

@@ -997,6 +997,15 @@ class CapturedStep:
         self.graph.replay()
         return self.result
 
+    def release(self):
+        """Free the graph (and its hold on the NCCL communicators) now."""
+        if self.graph is not None:
+            torch.cuda.synchronize(self.act.device)
+            self.graph.reset()
+            self.graph = None
+        if self in self.engine._captures:
+            self.engine._captures.remove(self)
+
     def timeline(self) -> list:
         """(actor, kind, uid, start_ms, end_ms) of the last replay, when the
         step was captured with ``timeline=True`` (timestamp kernels in the graph)."""
