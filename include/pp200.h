@@ -66,6 +66,11 @@ int pc_gemm(int dtype_in, int dtype_out, int transA, int transB, int64_t M, int6
             int epilogue, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
             int64_t ldaux_out, void* stream);
 
+/* The tcgen05 tile choice pc_gemm makes for a bf16 problem (transB as pc_gemm; split_ok =
+ * the caller passes PC_EPI_SPLITK_ZERO_C with fp32 C): tile width, CTA pair (1 or 2),
+ * K split (1 or 2).  Lets a caller fuse accumulation only where the GEMM is unsplit. */
+int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_ok, int* bn,
+                        int* cta_pair, int* ksplit);
 /* Force the tcgen05 GEMM tile width (0 = heuristic, else 64/128/192/256). Test hook. */
 int pc_gemm_set_tile_n(int bn);
 /* CTA-pair (cta_group::2, 256-row tiles over two SMs) selection: 0 = heuristic,
@@ -120,6 +125,12 @@ int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const v
                      const float* gamma, const float* mean, const float* rstd, const void* dres,
                      void* dx, float* dgamma, float* dbeta, void* ws, int64_t ws_bytes,
                      void* stream);
+/* As pc_layernorm_bwd; accumulate = 1 adds dgamma / dbeta onto the fp32 gradient
+ * accumulators (acc + partial, the grad-merge add fused into the reduction; needs ws). */
+int pc_layernorm_bwd_acc(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
+                         const float* gamma, const float* mean, const float* rstd,
+                         const void* dres, void* dx, float* dgamma, float* dbeta, int accumulate,
+                         void* ws, int64_t ws_bytes, void* stream);
 /* ---- Llama-style block pieces (BASELINE config C5; oracle/llama.py) ---- */
 /* y = x * rsqrt(mean(x^2) + eps) * gamma; rstd [rows] fp32 saved (oracle rms_norm). */
 int pc_rmsnorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const float* gamma,

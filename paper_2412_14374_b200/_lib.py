@@ -38,6 +38,8 @@ SIGNATURES: dict[str, list] = {
     "pc_gemm": [_c_i, _c_i, _c_i, _c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64,
                 _c_p, _c_i64, _c_i, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p],
     "pc_gemm_set_tile_n": [_c_i],
+    "pc_gemm_tile_choice": [_c_i, _c_i64, _c_i64, _c_i64, _c_i, ctypes.POINTER(_c_i),
+                            ctypes.POINTER(_c_i), ctypes.POINTER(_c_i)],
     "pc_gemm_set_tma_store": [_c_i],
     "pc_gemm_set_cta_pair": [_c_i],
     "pc_gemm_set_ablation": [_c_i],
@@ -55,6 +57,8 @@ SIGNATURES: dict[str, list] = {
     "pc_layernorm_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_f, _c_p],
     "pc_layernorm_bwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                          _c_p, _c_p, _c_i64, _c_p],
+    "pc_layernorm_bwd_acc": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                             _c_p, _c_p, _c_i, _c_p, _c_i64, _c_p],
     "pc_rmsnorm_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_f, _c_p],
     "pc_rmsnorm_bwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                        _c_i64, _c_p],
@@ -124,7 +128,7 @@ def exported_symbols() -> list[str]:
 
 
 # C-ABI calls that launch at least one kernel, counted for bench.py's gpu_launches.
-_NON_LAUNCH = {"pc_version", "pc_device_sm_count", "pc_gemm_set_tile_n", "pc_attention_set_impl",
+_NON_LAUNCH = {"pc_version", "pc_device_sm_count", "pc_gemm_set_tile_n", "pc_gemm_tile_choice", "pc_attention_set_impl",
                "pc_gemm_set_tma_store", "pc_gemm_set_cta_pair", "pc_gemm_set_ablation",
                "pc_embedding_bwd_workspace_bytes", "pc_reduce_workspace_bytes", "pc_p2p_available", "pc_p2p_unique_id",
                "pc_p2p_comm_init", "pc_p2p_abort", "pc_p2p_destroy"}

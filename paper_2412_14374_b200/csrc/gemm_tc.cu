@@ -151,6 +151,7 @@ __device__ __forceinline__ void epilogue16(const TcEpi& ep, int row, int col, fl
   const bool f32 = ep.out_f32 != 0;
   const int fl = ep.flags;
   if (fl & PC_EPI_ACCUM) {
+    if (!store_c) return;  // staged: the TMA reduce-add does C += v
     float old[16];
     load16(ep.C, true, static_cast<int64_t>(row) * ep.ldc + col, nvalid, old);
 #pragma unroll
@@ -703,7 +704,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (ep.ksplit > 1)
+          if (ep.ksplit > 1 || (ep.flags & PC_EPI_ACCUM))
             tma_reduce_add_2d(&tmC, stg, n0 + cc, m0 + q * 32);
           else
             tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
@@ -887,27 +888,19 @@ int dispatch_majors(bool a_mn, bool b_mn, int ek, const CUtensorMap& ta, const C
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn() { return tmap_encoder(); }
 
-int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
-                 const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                 int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
-                 int64_t ldaux_out, cudaStream_t st) {
-  PP_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem");
-  PP_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
-  // Pick (tile width, CTA pair) maximising wave efficiency x per-tile
-  // efficiency: useful area / (waves x slots x tile area) penalises a last
-  // partial wave (e.g. 192 tiles on 148 SMs) and padding; the per-tile factor
-  // is the measured mainloop efficiency of that tile shape.
+// Pick (tile width, CTA pair, K split) maximising wave efficiency x per-tile
+// efficiency: useful area / (waves x slots x tile area) penalises a last
+// partial wave (e.g. 192 tiles on 148 SMs) and padding; the per-tile factor
+// is the measured mainloop efficiency of that tile shape.  Deterministic
+// split-K: exactly 2 K halves reduce-added onto a zero-filled fp32 C
+// (0 + a + b == 0 + b + a bitwise), only when the caller allows it.
+static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool can_split,
+                         int* bn_out, int* cg_out, int* ks_out) {
   struct Cand { int bn, cg; double eff; };
   const Cand cands[7] = {{256, 2, 1.0}, {192, 2, 0.97}, {256, 1, 0.88}, {192, 1, 0.85},
                          {128, 2, 0.78}, {128, 1, 0.75}, {64, 1, 0.45}};
-  const bool b_kmajor = transB != 0;
   const int sms = num_sms();
-  const int es = out_f32 ? 4 : 2;
-  const bool tma_c = g_tma_store && !(epi & PC_EPI_ACCUM) &&
-                     (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
-  // deterministic split-K: exactly 2 K halves reduce-added onto a zero-filled
-  // fp32 C (0 + a + b == 0 + b + a bitwise), only when the caller allows it
-  const bool can_split = (epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c && K >= 2 * TC_BK * 8;
+  can_split = can_split && K >= 2 * TC_BK * 8;
   int bn = 0, cg = 1, ksplit = 1;
   double best = -1.0;
   for (const Cand& c : cands) {
@@ -938,6 +931,28 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     cg = 1;
     ksplit = 1;
   }
+  *bn_out = bn;
+  *cg_out = cg;
+  *ks_out = ksplit;
+}
+
+int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                 const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                 int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
+                 int64_t ldaux_out, cudaStream_t st) {
+  PP_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem");
+  PP_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
+  PP_CHECK_ARG(!((epi & PC_EPI_ACCUM) && (epi & PC_EPI_SPLITK_ZERO_C)),
+               "gemm: accumulate and split-K onto zeros are exclusive");
+  const int es = out_f32 ? 4 : 2;
+  // C through smem + TMA: plain store, or (fp32 accumulate / split-K) a TMA
+  // reduce-add at L2 -- C += tile in one fp32 add per element, so an
+  // unsplit accumulate equals storing the product and adding it after
+  const bool tma_c = g_tma_store && (!(epi & PC_EPI_ACCUM) || out_f32) &&
+                     (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
+  const bool can_split = (epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c;
+  int bn, cg, ksplit;
+  choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit);
   // op(A) is [M,K]: transA=0 -> stored [M,K] (K-major); transA=1 -> stored [K,M] (MN-major).
   // op(B) is [K,N]: transB=0 -> stored [K,N] (MN-major); transB=1 -> stored [N,K] (K-major).
   const bool a_mn = transA != 0;
@@ -1010,6 +1025,13 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
 }
 
 }  // namespace pp200
+
+extern "C" int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_ok,
+                                   int* bn, int* cta_pair, int* ksplit) {
+  PP_CHECK_ARG(M > 0 && N > 0 && K > 0 && bn && cta_pair && ksplit, "gemm_tile_choice: bad args");
+  pp200::choose_tiles(transB != 0, M, N, K, split_ok != 0, bn, cta_pair, ksplit);
+  return PC_OK;
+}
 
 extern "C" int pc_gemm_set_tile_n(int bn) {
   if (bn != 0 && bn != 64 && bn != 128 && bn != 192 && bn != 256) {

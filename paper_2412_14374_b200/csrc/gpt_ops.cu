@@ -493,14 +493,26 @@ template <typename T>
 bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda, const T* x,
                    const float* mean, const float* rstd, float* out1, float* out2,
                    int accumulate, void* ws, int64_t ws_bytes, cudaStream_t st);
+int64_t colred_ws_bytes(int64_t rows, int64_t cols);
 }
 
 extern "C" int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
                                 const float* gamma, const float* mean, const float* rstd,
                                 const void* dres, void* dx, float* dgamma, float* dbeta,
                                 void* ws, int64_t ws_bytes, void* stream) {
+  return pc_layernorm_bwd_acc(dtype, rows, d, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta,
+                              0, ws, ws_bytes, stream);
+}
+
+extern "C" int pc_layernorm_bwd_acc(int dtype, int64_t rows, int64_t d, const void* dy,
+                                    const void* x, const float* gamma, const float* mean,
+                                    const float* rstd, const void* dres, void* dx, float* dgamma,
+                                    float* dbeta, int accumulate, void* ws, int64_t ws_bytes,
+                                    void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= 0) return PC_OK;
+  PP_CHECK_ARG(!accumulate || ws_bytes >= colred_ws_bytes(rows, d),
+               "layernorm_bwd: accumulate needs the reduction workspace");
   PP_DISPATCH_FB(dtype, T,
     if (ln_vec_ok<T>(d, dy, x, dx) && ((reinterpret_cast<uintptr_t>(gamma) | reinterpret_cast<uintptr_t>(dres)) & 31) == 0) {
       const unsigned nb = row_blocks(rows);
@@ -514,7 +526,7 @@ extern "C" int pc_layernorm_bwd(int dtype, int64_t rows, int64_t d, const void* 
     } else {
       ln_bwd_dx_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
     }
-    if (!colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), mean, rstd, dgamma, dbeta, 0, ws, ws_bytes, st))
+    if (!colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), mean, rstd, dgamma, dbeta, accumulate, ws, ws_bytes, st))
       ln_bwd_param_kernel<T><<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), mean, rstd, dgamma, dbeta));
   return check_launch("layernorm_bwd");
 }

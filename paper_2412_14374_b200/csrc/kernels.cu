@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
         if (MODE == 1) t2 += sm2[k][threadIdx.x];
       }
       out1[c] = accumulate ? out1[c] + t1 : t1;
-      if (MODE == 1 && out2) out2[c] = t2;
+      if (MODE == 1 && out2) out2[c] = accumulate ? out2[c] + t2 : t2;
     }
   }
   if (threadIdx.x == 0) counters[blockIdx.x] = 0u;

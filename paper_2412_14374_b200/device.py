@@ -131,6 +131,11 @@ class DeviceOps:
         self.stream = stream
         self.gpt = gpt
         self._plans: dict[int, _StagePlan] = {}
+        # {param-grad value: fp32 accumulator} for the stage-bwd task being run:
+        # the producer adds its partial straight onto the running sum (the
+        # grad-merge `add` that follows becomes a rename, see _Actor.run_task)
+        self.acc_into: dict = {}
+        self.fuse_acc = os.environ.get("PP200_FUSE_ACC", "1") != "0"
         self._consumers = {}
         for op in p.graph.ops:
             for v in op.operands:
@@ -299,7 +304,7 @@ class DeviceOps:
         elif kind == "gpt-block":
             self._block_fwd(op, env)
         elif kind == "gpt-block-grad":
-            env[op.result] = self._block_bwd(op, env)
+            env[op.result] = self._block_bwd(op, env, acc=self._acc_target(op, 1))
         elif kind == "lmhead-xent":
             env[op.result] = self._head_fwd(op, env)
         elif kind == "lmhead-xent-grad":
@@ -562,7 +567,41 @@ class DeviceOps:
         hv.saved[op.id] = saved
         env[op.result] = Act(out)
 
-    def _block_bwd(self, op, env):
+    def _acc_target(self, op, index: int):
+        """The accumulator the ``index``-th tuple element of ``op`` may add
+        onto (its only reader is a tuple-get whose value is in acc_into)."""
+        if not self.acc_into:
+            return None
+        for u in self._consumers.get(op.result, ()):
+            if u.kind == "tuple-get" and u.attr("index") == index and u.result in self.acc_into:
+                return self.acc_into[u.result]
+        return None
+
+    def _wgrad_into(self, M_, N_, K_, A, lda, Bm, ldb, C, acc: bool, side: torch.cuda.Stream):
+        """C (fp32 [M_, N_]) = A^T-ish product, or C += it when ``acc``.  An
+        unsplit GEMM adds through its TMA reduce-add store (C + p, one fp32
+        add -- identical to storing p and adding after); a split one (two K
+        halves) first sums onto zeros in scratch, then one add."""
+        f32 = torch.float32
+        st = side.cuda_stream
+        if not acc:
+            self._gemm(f32, 1, 0, M_, N_, K_, A, lda, Bm, ldb, C, N_, _lib.EPI_SPLITK_ZERO_C, st=st)
+            return
+        bn, cg, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        call("pc_gemm_tile_choice", 0, M_, N_, K_, 1, ctypes.byref(bn), ctypes.byref(cg),
+             ctypes.byref(ks))
+        if ks.value == 1:
+            self._gemm(f32, 1, 0, M_, N_, K_, A, lda, Bm, ldb, C, N_, _lib.EPI_ACCUM, st=st)
+            return
+        scratch = torch.empty((M_, N_), dtype=f32, device=self.device)
+        call("pc_fill", _lib.PC_F32, scratch.numel(), 0.0, scratch.data_ptr(), st)
+        self._gemm(f32, 1, 0, M_, N_, K_, A, lda, Bm, ldb, scratch, N_, _lib.EPI_SPLITK_ZERO_C,
+                   st=st)
+        call("pc_accumulate", _lib.PC_F32, _lib.PC_F32, scratch.numel(), C.data_ptr(),
+             scratch.data_ptr(), st)
+        scratch.record_stream(side)
+
+    def _block_bwd(self, op, env, acc=None):
         cfg = self.gpt
         final = bool(op.attr("final_ln"))
         lay = self._blay[final]
@@ -585,13 +624,15 @@ class DeviceOps:
             wB = lambda name: (1, self._slice_t(Wt, lay, name), lay[name][1][0])
         else:
             wB = lambda name: (0, sl(name), lay[name][1][1])
-        dW = self.zeros((layout_size(lay),), f32)
+        fused = acc is not None
+        dW = acc if fused else self.zeros((layout_size(lay),), f32)
         gs = lambda name: self._slice(dW, lay, name)
         if final:
             dout = self.empty((T, d), act)
-            call("pc_layernorm_bwd", self.mode.pc_act, T, d, dz.data_ptr(), sv["out"].data_ptr(),
+            call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, dz.data_ptr(), sv["out"].data_ptr(),
                  ms("lnf_g").data_ptr(), sv["meanf"].data_ptr(), sv["rstdf"].data_ptr(), None,
-                 dout.data_ptr(), gs("lnf_g").data_ptr(), gs("lnf_b").data_ptr(), *self.red_ws(T, d), self.st)
+                 dout.data_ptr(), gs("lnf_g").data_ptr(), gs("lnf_b").data_ptr(), int(fused),
+                 *self.red_ws(T, d), self.st)
         else:
             dout = dz
         # Weight gradients and their bias sums run on the side stream (they do
@@ -600,10 +641,9 @@ class DeviceOps:
 
         def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname):
             self._fork()
-            self._gemm(f32, 1, 0, M_, N_, T, A, lda, Bm, ldb, gs(wname), N_,
-                       _lib.EPI_SPLITK_ZERO_C, st=sst)
+            self._wgrad_into(M_, N_, T, A, lda, Bm, ldb, gs(wname), fused, self._side())
             call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, M_, A.data_ptr(), lda,
-                 gs(bname).data_ptr(), 0, *self.red_ws(T, M_, side=True), sst)
+                 gs(bname).data_ptr(), int(fused), *self.red_ws(T, M_, side=True), sst)
 
         # MLP
         wgrad(d, f, dout, d, sv["gu"], f, "w_fc2", "b_fc2")
@@ -616,10 +656,10 @@ class DeviceOps:
         tb, B, ldb = wB("w_fc1")
         self._gemm(act, 0, tb, T, d, f, du, f, B, ldb, da2, d)
         dh1 = self.empty((T, d), act)
-        call("pc_layernorm_bwd", self.mode.pc_act, T, d, da2.data_ptr(), sv["h1"].data_ptr(),
+        call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, da2.data_ptr(), sv["h1"].data_ptr(),
              ms("ln2_g").data_ptr(), sv["mean2"].data_ptr(), sv["rstd2"].data_ptr(),
              dout.data_ptr(), dh1.data_ptr(), gs("ln2_g").data_ptr(), gs("ln2_b").data_ptr(),
-             *self.red_ws(T, d), self.st)
+             int(fused), *self.red_ws(T, d), self.st)
         # attention
         wgrad(d, d, dh1, d, sv["o"], d, "w_o", "b_o")
         do = self.empty((T, d), act)
@@ -635,10 +675,10 @@ class DeviceOps:
         tb, B, ldb = wB("w_qkv")
         self._gemm(act, 0, tb, T, d, 3 * d, dqkv, 3 * d, B, ldb, da, d)
         dh = self.empty((T, d), act)
-        call("pc_layernorm_bwd", self.mode.pc_act, T, d, da.data_ptr(), h.data_ptr(),
+        call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, da.data_ptr(), h.data_ptr(),
              ms("ln1_g").data_ptr(), sv["mean1"].data_ptr(), sv["rstd1"].data_ptr(),
              dh1.data_ptr(), dh.data_ptr(), gs("ln1_g").data_ptr(), gs("ln1_b").data_ptr(),
-             *self.red_ws(T, d), self.st)
+             int(fused), *self.red_ws(T, d), self.st)
         self._join()
         return (dh, dW)
 

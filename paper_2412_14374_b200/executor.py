@@ -399,6 +399,11 @@ class _Actor:
             self.ts = torch.empty(n, dtype=torch.int64, device=self.device)
         self.end_event = None
         self.last_issued = -1
+        # grad-merge adds of this actor by their partial (rhs) operand, and the
+        # partials a producer already added onto the running sum
+        self._add_by_rhs = {t.exec["rhs"]: (t.uid, t.exec["lhs"]) for t in tg.tasks.values()
+                            if t.actor == actor and t.exec.get("type") == "add"}
+        self.fused: set = set()
 
     def stamp(self, slot: int):
         _lib.call("pc_timestamp", self.ts.data_ptr() + 8 * slot, self.stream.cuda_stream)
@@ -433,13 +438,25 @@ class _Actor:
             env = {v: st.get(bid, at) for v, bid in ex["feeds"].items()}
             if ex["stash_in"]:
                 env.update(st.get(ex["stash_in"], at))
-            self.ops.run_ops(prog.ops, env)
+            acc = self._fusable_accumulators(ex) if self.ops.fuse_acc else {}
+            self.ops.acc_into = acc
+            try:
+                self.ops.run_ops(prog.ops, env)
+            finally:
+                self.ops.acc_into = {}
             for v, bid in ex["outs"].items():
                 st.put(bid, env[v])
+                if v in acc and isinstance(env[v], torch.Tensor) and env[v] is acc[v]:
+                    self.fused.add(bid)
         elif kind == "add":
             lhs = ex["lhs"]
-            st.put(ex["out"], self.ops.add(st.get(lhs, at), st.get(ex["rhs"], at),
-                                           inplace=self._may_overwrite(lhs, task.uid)))
+            if ex["rhs"] in self.fused:   # its producer already added it onto lhs
+                self.fused.discard(ex["rhs"])
+                st.get(ex["rhs"], at)
+                st.put(ex["out"], st.get(lhs, at))
+            else:
+                st.put(ex["out"], self.ops.add(st.get(lhs, at), st.get(ex["rhs"], at),
+                                               inplace=self._may_overwrite(lhs, task.uid)))
         elif kind == "concat":
             st.put(ex["out"], self.ops.concat_losses([st.get(b, at) for b in ex["parts"]]))
         elif kind == "sgd-update":
@@ -450,6 +467,28 @@ class _Actor:
         if self.timeline:
             self.stamp(s0 + 1)
             self.events.append((task.kind if task.is_loop else "aux", task.uid, s0, s0 + 1))
+
+    def _fusable_accumulators(self, ex) -> dict:
+        """{bwd output value: running-sum tensor} for partial gradients whose
+        only reader is the next grad-merge add on this actor, when that add may
+        update its lhs in place and the lhs already exists: the producer then
+        adds its partial onto the lhs itself (acc + p, the same fp32 add) and
+        the add task only renames (taskgraph.py:369-433 order unchanged)."""
+        out = {}
+        for v, bid in ex["outs"].items():
+            hit = self._add_by_rhs.get(bid)
+            if hit is None:
+                continue
+            uid, lhs = hit
+            b = self.tg.buffers[bid]
+            if b.consumers != {uid} or b.is_output or lhs not in self.store.data:
+                continue
+            if not self._may_overwrite(lhs, uid):
+                continue
+            t = self.store.data[lhs]
+            if isinstance(t, torch.Tensor) and t.dtype == torch.float32 and t.dim() == 1:
+                out[v] = t
+        return out
 
     def _may_overwrite(self, bid: str, uid: str) -> bool:
         """True when ``bid``'s only reader is this task, it is not a step output,

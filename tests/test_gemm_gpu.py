@@ -157,3 +157,35 @@ def test_splitk_zero_c_deterministic(shape, pair):
     torch.cuda.synchronize()
     assert rel(outs[0], ref) < 1e-5
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("pair", [1, 2])
+@pytest.mark.parametrize("shape", [(768, 3072, 8192), (200, 136, 1100), (256, 512, 256)])
+def test_accumulate_equals_store_then_add(shape, pair, tma):
+    """fp32 C += op(A) op(B) (TMA reduce-add, or the direct read-modify-write)
+    is bitwise the unsplit product stored, then added onto C."""
+    M, N, K = shape
+    A, B, ref = make_operands(M, N, K, 1, 0, torch.bfloat16, seed=9)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    acc0 = torch.randn(M, N, device="cuda", generator=g)
+    with forced(0, pair, tma):
+        fused = run_gemm(A, B, 1, 0, M, N, K, torch.float32, epi=_lib.EPI_ACCUM, C=acc0.clone())
+        part = run_gemm(A, B, 1, 0, M, N, K, torch.float32)
+    want = acc0.clone()
+    _lib.call("pc_accumulate", _lib.PC_F32, _lib.PC_F32, want.numel(), want.data_ptr(),
+              part.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(fused, want)
+    assert rel(fused - acc0, ref) < 1e-4
+
+
+def test_tile_choice_reports_split():
+    import ctypes
+    bn, cg, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.call("pc_gemm_tile_choice", 0, 768, 768, 8192, 1, ctypes.byref(bn), ctypes.byref(cg),
+              ctypes.byref(ks))
+    assert ks.value == 2 and bn.value in (64, 128, 192, 256)
+    _lib.call("pc_gemm_tile_choice", 0, 768, 768, 8192, 0, ctypes.byref(bn), ctypes.byref(cg),
+              ctypes.byref(ks))
+    assert ks.value == 1
