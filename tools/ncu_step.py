@@ -14,6 +14,8 @@ eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
 eng.step(params, tok, lr=1e-4, timeout_s=600, to_host=False)
 torch.cuda.synchronize()
 n0 = _lib.launch_count
+torch.cuda.profiler.start()   # ncu --profile-from-start off: only this step
 eng.step(params, tok, lr=1e-4, timeout_s=600, to_host=False)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("libpp200 calls per step:", _lib.launch_count - n0)
