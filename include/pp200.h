@@ -52,6 +52,10 @@ enum pc_dtype { PC_F32 = 0, PC_F64 = 1, PC_BF16 = 2, PC_I32 = 3 };
 #define PC_EPI_SPLITK_ZERO_C 128 /* caller guarantees an fp32 C filled with zeros: the
                                     kernel may split K in two halves reduce-added into C
                                     (deterministic: two terms onto 0 commute) */
+#define PC_EPI_SPLITK_ORDERED 256 /* with PC_EPI_ACCUM: the kernel may split K in two
+                                    halves added onto C in a fixed order, (C + h0) + h1,
+                                    sequenced per tile by flags: aux = zeroed uint32 flag
+                                    array, ldaux = its length (>= tiles x 16) */
 
 const char* pc_last_error(void);
 int pc_version(void);

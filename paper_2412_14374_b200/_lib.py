@@ -24,6 +24,7 @@ EPI_ACCUM = 16
 EPI_RELU = 32
 EPI_RELU_GRAD = 64
 EPI_SPLITK_ZERO_C = 128
+EPI_SPLITK_ORDERED = 256
 
 _c_i = ctypes.c_int
 _c_i64 = ctypes.c_int64

@@ -645,6 +645,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
       } else {
+      // ordered split-K accumulate: split 1 adds its half onto C only after
+      // split 0's adds to the same region (this warp's rows x columns) landed
+      const bool ordered = (ep.flags & PC_EPI_SPLITK_ORDERED) && ep.ksplit > 1;
+      unsigned* oflag = static_cast<unsigned*>(const_cast<void*>(ep.aux)) +
+                        ((t * CG + static_cast<int>(rank)) * TC_EPI_WARPS + (warp - 4));
+      if (ordered && u >= num_tiles) {
+        if (lane == 0) {
+          while (ld_acquire_gpu(oflag) == 0u) __nanosleep(100);
+          st_release_gpu(oflag, 0u);  // re-armed for the next launch
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+      }
 #pragma unroll 1
       for (int cc = cstart; cc < cend; cc += cstep) {
         const uint32_t my = nchunk++;
@@ -711,6 +724,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (stage_u) tma_store_2d(&tmU, stg + 2048, n0 + cc, m0 + q * 32);
           bulk_commit();
         }
+      }
+      if (ordered && u < num_tiles && lane == 0) {  // split 0: publish once its adds landed
+        bulk_wait0();
+        fence_proxy_async_global();
+        st_release_gpu(oflag, 1u);
       }
       }
       if (cend <= cstart) release_acc<CG>(rel, lane);
@@ -950,9 +968,18 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   // unsplit accumulate equals storing the product and adding it after
   const bool tma_c = g_tma_store && (!(epi & PC_EPI_ACCUM) || out_f32) &&
                      (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * es) % 16 == 0;
-  const bool can_split = (epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c;
+  const bool ordered = (epi & PC_EPI_SPLITK_ORDERED) && (epi & PC_EPI_ACCUM) && out_f32 && tma_c;
+  PP_CHECK_ARG(!(epi & PC_EPI_SPLITK_ORDERED) ||
+                   ((epi & PC_EPI_ACCUM) && aux != nullptr &&
+                    !(epi & (PC_EPI_RESIDUAL | PC_EPI_GELU_GRAD | PC_EPI_RELU_GRAD))),
+               "gemm: ordered split-K needs accumulate and a flag array in aux");
+  const bool can_split = ((epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c) || ordered;
   int bn, cg, ksplit;
   choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit);
+  if (ordered && ksplit > 1) {
+    const int64_t tiles = ((M + TC_BM * cg - 1) / (TC_BM * cg)) * ((N + bn - 1) / bn);
+    PP_CHECK_ARG(ldaux >= tiles * cg * TC_EPI_WARPS, "gemm: ordered split-K flag array too short");
+  }
   // op(A) is [M,K]: transA=0 -> stored [M,K] (K-major); transA=1 -> stored [K,M] (MN-major).
   // op(B) is [K,N]: transB=0 -> stored [K,N] (MN-major); transB=1 -> stored [N,K] (K-major).
   const bool a_mn = transA != 0;

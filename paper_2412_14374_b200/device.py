@@ -135,6 +135,7 @@ class DeviceOps:
         # the producer adds its partial straight onto the running sum (the
         # grad-merge `add` that follows becomes a rename, see _Actor.run_task)
         self.acc_into: dict = {}
+        self._split_flags = None
         self.fuse_acc = os.environ.get("PP200_FUSE_ACC", "1") != "0"
         self._consumers = {}
         for op in p.graph.ops:
@@ -578,28 +579,22 @@ class DeviceOps:
         return None
 
     def _wgrad_into(self, M_, N_, K_, A, lda, Bm, ldb, C, acc: bool, side: torch.cuda.Stream):
-        """C (fp32 [M_, N_]) = A^T-ish product, or C += it when ``acc``.  An
-        unsplit GEMM adds through its TMA reduce-add store (C + p, one fp32
-        add -- identical to storing p and adding after); a split one (two K
-        halves) first sums onto zeros in scratch, then one add."""
+        """C (fp32 [M_, N_]) = the weight-gradient product, or C += it when
+        ``acc``: the GEMM adds through its TMA reduce-add store -- unsplit,
+        C + p (one fp32 add, bitwise the stored partial added after); split
+        in two K halves, (C + h0) + h1 in that order (flag-sequenced per tile,
+        deterministic)."""
         f32 = torch.float32
         st = side.cuda_stream
         if not acc:
             self._gemm(f32, 1, 0, M_, N_, K_, A, lda, Bm, ldb, C, N_, _lib.EPI_SPLITK_ZERO_C, st=st)
             return
-        bn, cg, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-        call("pc_gemm_tile_choice", 0, M_, N_, K_, 1, ctypes.byref(bn), ctypes.byref(cg),
-             ctypes.byref(ks))
-        if ks.value == 1:
-            self._gemm(f32, 1, 0, M_, N_, K_, A, lda, Bm, ldb, C, N_, _lib.EPI_ACCUM, st=st)
-            return
-        scratch = torch.empty((M_, N_), dtype=f32, device=self.device)
-        call("pc_fill", _lib.PC_F32, scratch.numel(), 0.0, scratch.data_ptr(), st)
-        self._gemm(f32, 1, 0, M_, N_, K_, A, lda, Bm, ldb, scratch, N_, _lib.EPI_SPLITK_ZERO_C,
-                   st=st)
-        call("pc_accumulate", _lib.PC_F32, _lib.PC_F32, scratch.numel(), C.data_ptr(),
-             scratch.data_ptr(), st)
-        scratch.record_stream(side)
+        if self._split_flags is None:   # zero once; every ordered GEMM leaves them zero
+            with torch.cuda.stream(side):
+                self._split_flags = torch.zeros(1 << 16, dtype=torch.int32, device=self.device)
+        self._gemm(f32, 1, 0, M_, N_, K_, A, lda, Bm, ldb, C, N_,
+                   _lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED, aux=self._split_flags,
+                   ldaux=self._split_flags.numel(), st=st)
 
     def _block_bwd(self, op, env, acc=None):
         cfg = self.gpt

@@ -36,7 +36,8 @@ def run_gemm(A, B, ta, tb, M, N, K, out_dtype, epi=0, bias=None, aux=None, aux_o
     st = torch.cuda.current_stream().cuda_stream
     _lib.call("pc_gemm", dt_in, dt_out, ta, tb, M, N, K, _ptr(A), A.stride(0), _ptr(B),
               B.stride(0), _ptr(C), C.stride(0), epi, _ptr(bias), _ptr(aux),
-              aux.stride(0) if aux is not None else 0, _ptr(aux_out),
+              (aux.stride(0) if aux.dim() > 1 else aux.numel()) if aux is not None else 0,
+              _ptr(aux_out),
               aux_out.stride(0) if aux_out is not None else 0, st)
     return C
 
@@ -189,3 +190,41 @@ def test_tile_choice_reports_split():
     _lib.call("pc_gemm_tile_choice", 0, 768, 768, 8192, 0, ctypes.byref(bn), ctypes.byref(cg),
               ctypes.byref(ks))
     assert ks.value == 1
+
+
+@pytest.mark.parametrize("shape", [(768, 768, 8192), (2304, 768, 8192), (768, 3072, 8192)])
+def test_ordered_splitk_accumulate(shape):
+    """C += op(A) op(B) split in two K halves and added in a fixed order,
+    (C + h0) + h1, sequenced per tile by flags: equal to two unsplit
+    half-products added one after the other, run-to-run identical, and the
+    flag array is left zeroed."""
+    import ctypes
+    M, N, K = shape
+    bn, cg, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.call("pc_gemm_tile_choice", 0, M, N, K, 1, ctypes.byref(bn), ctypes.byref(cg),
+              ctypes.byref(ks))
+    assert ks.value == 2
+    A, B, ref = make_operands(M, N, K, 1, 0, torch.bfloat16, seed=4)
+    g = torch.Generator(device="cuda").manual_seed(8)
+    acc0 = torch.randn(M, N, device="cuda", generator=g)
+    flags = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(3):
+        C = acc0.clone()
+        run_gemm(A, B, 1, 0, M, N, K, torch.float32,
+                 epi=_lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED, aux=flags, C=C)
+        outs.append(C)
+    nk = (K + 63) // 64
+    kh = (nk // 2) * 64
+    want = acc0.clone()
+    st = torch.cuda.current_stream().cuda_stream
+    with forced(bn.value, cg.value):
+        for lo, hi in ((0, kh), (kh, K)):
+            h = run_gemm(A[lo:hi], B[lo:hi], 1, 0, M, N, hi - lo, torch.float32)
+            _lib.call("pc_accumulate", _lib.PC_F32, _lib.PC_F32, want.numel(), want.data_ptr(),
+                      h.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    assert torch.equal(outs[0], want)
+    assert int(flags.abs().sum()) == 0
+    assert rel(outs[0] - acc0, ref) < 1e-4

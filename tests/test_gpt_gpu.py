@@ -310,11 +310,13 @@ def test_layernorm_vectorised_paths(d, dt, tol):
     assert ffn.rel(cs.cpu().numpy(), dyq.sum(0)) < 1e-5
 
 
-def test_fused_grad_accumulation_is_bitwise_the_add_chain():
+def test_fused_grad_accumulation_matches_the_add_chain():
     """Block weight / bias / LN gradients added onto the running sum by their
-    producers (GEMM TMA reduce-add, reductions with accumulate) give exactly
-    the grad-merge chain's result (taskgraph.py:369-433); T = 1024 tokens per
-    microbatch so both unsplit and split-K weight GEMMs occur."""
+    producers (GEMM TMA reduce-add, reductions with accumulate) reproduce the
+    grad-merge chain (taskgraph.py:369-433): bitwise where the producer adds
+    one partial (bias, LN, unsplit GEMMs), (acc + h0) + h1 instead of
+    acc + (h0 + h1) for split-K GEMMs; deterministic either way.  T = 1024
+    tokens per microbatch so both kinds of weight GEMM occur."""
     from paper_2412_14374_b200.executor import PipelineEngine
     cfg = I.GPTConfig(layers=4, d_model=128, n_heads=2, d_ff=512, vocab=256, seq_len=256,
                       microbatch_size=4, yields=(3,), yield_every=6, elem_bytes=2)
@@ -324,13 +326,14 @@ def test_fused_grad_accumulation_is_bitwise_the_add_chain():
     params = {q: v.astype(np.float32) for q, v in gpt.init_params(oc, rng, std=0.05).items()}
     tokens = gpt.init_tokens(oc, 4, rng).reshape(16, 256)
     out = []
-    for fuse in (True, False):
+    for fuse in (True, False, True):
         eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
         for ops in eng._ops.values():
             ops.fuse_acc = fuse
         out.append(eng.step(params, tokens))
         eng.close()
-    a, b = out
+    a, b, c = out
     assert np.array_equal(a.losses, b.losses)
     for q in a.grads:
-        assert np.array_equal(a.grads[q], b.grads[q]), (q, ffn.rel(a.grads[q], b.grads[q]))
+        assert ffn.rel(a.grads[q], b.grads[q]) < 1e-6, (q, ffn.rel(a.grads[q], b.grads[q]))
+        assert np.array_equal(a.grads[q], c.grads[q]), q
