@@ -456,6 +456,7 @@ def main():
                        "schedule": "1f1b", "stages": P, "yields": list(cfg.yields or []),
                        "parallelism": f"pp{P}", "l2": "inputs > L2 (no flush needed)",
                        "issue": "cuda-graph replay per actor" if use_graph else "python per op",
+                       "transport": eng.transport if world > 1 else None,
                        "training": "resident params, in-place SGD each step"
                                    + (", tied w0 re-broadcast to the head stage" if P > 1 else "")},
             "model_tflops_per_gpu": round(tflops_gpu, 1),

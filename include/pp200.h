@@ -181,6 +181,20 @@ int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const void* qkv, in
  * 2 = force the mma.sync forward. Test hook. */
 int pc_attention_set_impl(int impl);
 
+/* ---- inter-stage transport over NVLink peer memory (Channel, executor.py:201-254) ----
+ * The receiver allocates one slot per plan message plus flag words (pc_peer_alloc: zeroed
+ * device memory + a 64-byte CUDA IPC handle); the sender maps them (pc_peer_open), has the
+ * producing kernel write the message into the slot (or pc_peer_copy it there), then
+ * pc_stream_write_u32(flag, 1); the receiver's stream pc_stream_wait_u32(flag, 1) and
+ * re-arms the flag with pc_stream_write_u32(flag, 0).  Graph-capturable. */
+int pc_peer_alloc(int64_t bytes, void** ptr, void* handle64);
+int pc_peer_free(void* ptr);
+int pc_peer_open(const void* handle64, void** ptr);
+int pc_peer_close(void* ptr);
+int pc_stream_write_u32(void* addr, uint32_t value, void* stream);
+int pc_stream_wait_u32(void* addr, uint32_t value, void* stream);
+int pc_peer_copy(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* ---- inter-stage transport (Channel, executor.py:201-254) over NCCL ---- */
 int pc_p2p_available(void);
 int pc_p2p_unique_id(void* out128);

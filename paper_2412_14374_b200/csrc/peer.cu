@@ -1,0 +1,92 @@
+// NVLink peer-memory channels: the receiver owns one slot per plan message
+// (CUDA IPC), the sender's producing kernel writes the message straight into
+// that slot over NVLink (or a copy engine moves it when the value was not
+// produced in place), and a flag word per message, written by a stream
+// memory operation ordered after the producer, releases the receiver's
+// stream (cuStreamWaitValue32).  Replaces the reference's Channel
+// (executor.py:201-254) without a separate transfer on the critical path.
+#include "common.cuh"
+
+#include <cuda.h>
+
+using namespace pp200;
+
+namespace {
+
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <typename F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+
+}  // namespace
+
+extern "C" int pc_peer_alloc(int64_t bytes, void** ptr, void* handle64) {
+  PP_CHECK_ARG(bytes > 0 && ptr && handle64, "peer_alloc: bad args");
+  void* p = nullptr;
+  PP_CUDA_TRY(cudaMalloc(&p, static_cast<size_t>(bytes)));
+  PP_CUDA_TRY(cudaMemset(p, 0, static_cast<size_t>(bytes)));
+  cudaIpcMemHandle_t h;
+  PP_CUDA_TRY(cudaIpcGetMemHandle(&h, p));
+  memcpy(handle64, &h, sizeof(h));
+  *ptr = p;
+  return PC_OK;
+}
+
+extern "C" int pc_peer_free(void* ptr) {
+  PP_CUDA_TRY(cudaFree(ptr));
+  return PC_OK;
+}
+
+extern "C" int pc_peer_open(const void* handle64, void** ptr) {
+  PP_CHECK_ARG(handle64 && ptr, "peer_open: bad args");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  PP_CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return PC_OK;
+}
+
+extern "C" int pc_peer_close(void* ptr) {
+  PP_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return PC_OK;
+}
+
+// *addr = value once all prior work on the stream has completed (its memory
+// writes, incl. stores into peer memory, visible first: default memory barrier).
+extern "C" int pc_stream_write_u32(void* addr, uint32_t value, void* stream) {
+  static WriteFn fn = driver_fn<WriteFn>("cuStreamWriteValue32");
+  PP_CHECK_ARG(fn != nullptr, "cuStreamWriteValue32 unavailable");
+  CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value, 0);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuStreamWriteValue32 failed (%d)", static_cast<int>(r));
+    return PC_ERR_CUDA;
+  }
+  return PC_OK;
+}
+
+// Later work on the stream waits until *addr == value.
+extern "C" int pc_stream_wait_u32(void* addr, uint32_t value, void* stream) {
+  static WaitFn fn = driver_fn<WaitFn>("cuStreamWaitValue32");
+  PP_CHECK_ARG(fn != nullptr, "cuStreamWaitValue32 unavailable");
+  CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
+                  CU_STREAM_WAIT_VALUE_EQ);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuStreamWaitValue32 failed (%d)", static_cast<int>(r));
+    return PC_ERR_CUDA;
+  }
+  return PC_OK;
+}
+
+extern "C" int pc_peer_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes <= 0) return PC_OK;
+  PP_CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice,
+                              static_cast<cudaStream_t>(stream)));
+  return PC_OK;
+}

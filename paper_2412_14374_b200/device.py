@@ -81,6 +81,29 @@ class Act:
         self.saved: dict = {}
 
 
+class PeerBuf:
+    """A message slot in another GPU's memory (NVLink peer mapping): the
+    producing kernel of a sent value writes here directly.  Only its address
+    is used (kernels take raw pointers); it is never read on this GPU."""
+
+    __slots__ = ("ptr", "shape", "dtype")
+
+    def __init__(self, ptr: int, shape, dtype):
+        self.ptr, self.shape, self.dtype = ptr, tuple(shape), dtype
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def numel(self) -> int:
+        return math.prod(self.shape)
+
+    def element_size(self) -> int:
+        return torch.empty((), dtype=self.dtype).element_size()
+
+    def is_contiguous(self) -> bool:
+        return True
+
+
 @dataclass
 class Param:
     """A parameter as stored on an actor: fp32 master (+ bf16 shadow in bf16 mode)."""
@@ -135,6 +158,9 @@ class DeviceOps:
         # the producer adds its partial straight onto the running sum (the
         # grad-merge `add` that follows becomes a rename, see _Actor.run_task)
         self.acc_into: dict = {}
+        # {value: PeerBuf} for the task being run: outputs that are sent to a
+        # peer-memory channel are produced straight into the receiver's slot
+        self.place: dict = {}
         self._split_flags = None
         self.fuse_acc = os.environ.get("PP200_FUSE_ACC", "1") != "0"
         self._consumers = {}
@@ -198,6 +224,26 @@ class DeviceOps:
 
     def empty(self, shape, dtype) -> torch.Tensor:
         return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def _out(self, value: str, shape, dtype):
+        """Output buffer of ``value``: its peer slot when placed (directly or
+        through the yield-marker that makes it the stage output), else new."""
+        pb = self.place.get(value)
+        if pb is None and self.place:
+            for u in self._consumers.get(value, ()):
+                if u.kind == "yield-marker" and u.result in self.place:
+                    pb = self.place[u.result]
+        if pb is not None and pb.shape == tuple(shape) and pb.dtype == dtype:
+            return pb
+        return self.empty(shape, dtype)
+
+    def _placed_elem(self, op, index: int, shape, dtype):
+        """As _out for the ``index``-th element of a tuple-valued op."""
+        if self.place:
+            for u in self._consumers.get(op.result, ()):
+                if u.kind == "tuple-get" and u.attr("index") == index and u.result in self.place:
+                    return self._out(u.result, shape, dtype)
+        return self.empty(shape, dtype)
 
     def zeros(self, shape, dtype) -> torch.Tensor:
         t = self.empty(shape, dtype)
@@ -551,7 +597,9 @@ class DeviceOps:
         gu = self.empty((T, f), act)
         self._gemm(act, 0, 1, T, f, d, a2, d, sl("w_fc1"), d, gu, f,
                    _lib.EPI_BIAS | _lib.EPI_GELU, bias=ms("b_fc1"), aux_out=u, ldaux_out=f)
-        out = self.empty((T, d), act)
+        # a block output that leaves the stage is written straight into the
+        # next stage's receive slot (NVLink peer memory) by this GEMM
+        out = self.empty((T, d), act) if final else self._out(op.result, (T, d), act)
         self._gemm(act, 0, 1, T, d, f, gu, f, sl("w_fc2"), f, out, d,
                    _lib.EPI_BIAS | _lib.EPI_RESIDUAL, bias=ms("b_fc2"), aux=h1, ldaux=d)
         saved = dict(a=a, mean1=mean1, rstd1=rstd1, qkv=qkv, o=o, lse=lse, h1=h1, a2=a2,
@@ -669,7 +717,7 @@ class DeviceOps:
         da = self.empty((T, d), act)
         tb, B, ldb = wB("w_qkv")
         self._gemm(act, 0, tb, T, d, 3 * d, dqkv, 3 * d, B, ldb, da, d)
-        dh = self.empty((T, d), act)
+        dh = self._placed_elem(op, 0, (T, d), act)   # into the previous stage's slot when sent
         call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, da.data_ptr(), h.data_ptr(),
              ms("ln1_g").data_ptr(), sv["mean1"].data_ptr(), sv["rstd1"].data_ptr(),
              dh1.data_ptr(), dh.data_ptr(), gs("ln1_g").data_ptr(), gs("ln1_b").data_ptr(),

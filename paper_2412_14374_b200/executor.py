@@ -30,6 +30,8 @@ threads of this process (all on one GPU unless ``devices`` says otherwise).
 from __future__ import annotations
 
 import itertools
+import math
+import os
 import threading
 import time
 from collections import deque
@@ -51,8 +53,8 @@ from .comms import (
     _brief,
 )
 from .device import _PC as _PC_OF
-from .device import MODES, Act, DeviceOps, Mode, Param, strip, tensor_of, to_device_input, \
-    to_device_param
+from .device import MODES, Act, DeviceOps, Mode, Param, PeerBuf, strip, tensor_of, \
+    to_device_input, to_device_param
 from .ir import GPTConfig
 from .taskgraph import GRAD_TOTAL, OPT_STATE, PARAM, STASH, TaskGraph
 
@@ -312,6 +314,108 @@ class NcclChannel:
                 self.comm = None
 
 
+_TYPESTR = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float64: "<f8",
+            torch.int32: "<i4"}
+
+
+class _CAI:
+    """__cuda_array_interface__ view of raw device memory (this GPU's own)."""
+
+    def __init__(self, ptr: int, shape, dtype):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": _TYPESTR[dtype],
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def _slot_layout(bids, wire_meta):
+    """Receiver-slot layout of one channel: flag words first, then one
+    256-byte-aligned slot per message in plan order."""
+    n = len(bids)
+    off = (4 * n + 255) // 256 * 256
+    slots = []
+    for bid in bids:
+        shape, dtype = wire_meta(bid)
+        nb = math.prod(shape) * torch.empty((), dtype=dtype).element_size()
+        slots.append((off, tuple(shape), dtype, nb))
+        off += (nb + 255) // 256 * 256
+    return slots, off
+
+
+class PeerChannel:
+    """One side of a directed channel over NVLink peer memory (same node).
+
+    The receiver owns one slot per message of the plan's channel list plus a
+    flag word per message (``pc_peer_alloc``, CUDA IPC); the sender maps them.
+    SendStart: the value is normally already in the slot (its producing
+    kernel wrote it there, see ``_Actor._placement``), otherwise a copy engine
+    moves it; then a stream memory write sets the flag, ordered after the
+    producer.  RecvWait: the receiver's stream waits for the flag and re-arms
+    it.  No transfer step and no communication kernel remain on the critical
+    path.  A slot is rewritten only in the next step, after the receiver has
+    finished the step that read it (the sender's next step needs this step's
+    last gradient from the receiver).  Reference Channel: executor.py:201-254.
+    """
+
+    def __init__(self, src: int, dst: int, me: int, base: int, bids, slots):
+        self.src, self.dst, self.me = src, dst, me
+        self.base, self.bids, self.slots = base, list(bids), slots
+        self.reset()
+
+    def reset(self):
+        self.last_seq = -1
+        self.in_place = 0   # messages whose producer wrote them into the slot
+        self.copied = 0     # messages moved by a copy engine at SendStart
+
+    def flag(self, seq: int) -> int:
+        return self.base + 4 * seq
+
+    def peer_slot(self, seq: int):
+        off, shape, dtype, _ = self.slots[seq]
+        return PeerBuf(self.base + off, shape, dtype)
+
+    def send(self, seq: int, bid: str, value, stream: torch.cuda.Stream):
+        if seq <= self.last_seq:
+            raise ChannelOrderFault(f"channel {self.src}->{self.dst}: send seq {seq} out of order")
+        self.last_seq = seq
+        if self.bids[seq] != bid:
+            raise ChannelOrderFault(f"channel {self.src}->{self.dst}: seq {seq} carries "
+                                    f"{self.bids[seq]}, not {bid}")
+        off, shape, dtype, nb = self.slots[seq]
+        t = strip(value)
+        if t.data_ptr() != self.base + off:
+            if not isinstance(t, PeerBuf):
+                t = t if t.is_contiguous() else t.contiguous()
+            if t.numel() * t.element_size() != nb:
+                raise ChannelOrderFault(f"channel {self.src}->{self.dst}: {bid} has "
+                                        f"{t.numel() * t.element_size()} bytes, slot {nb}")
+            _lib.call("pc_peer_copy", self.base + off, t.data_ptr(), nb, stream.cuda_stream)
+            self.copied += 1
+        else:
+            self.in_place += 1
+        _lib.call("pc_stream_write_u32", self.flag(seq), 1, stream.cuda_stream)
+
+    def post_recv(self, seq: int, bid: str, stream=None):
+        pass
+
+    def recv(self, seq: int, ctl: _Control, actor: int, stream: torch.cuda.Stream):
+        off, shape, dtype, _ = self.slots[seq]
+        _lib.call("pc_stream_wait_u32", self.flag(seq), 1, stream.cuda_stream)
+        _lib.call("pc_stream_write_u32", self.flag(seq), 0, stream.cuda_stream)
+        t = torch.as_tensor(_CAI(self.base + off, shape, dtype), device=stream.device)
+        return self.bids[seq], (t.view(torch.bfloat16) if dtype == torch.bfloat16 else t)
+
+    def wait_consumed(self, seq: int, ctl: _Control, actor: int, stream):
+        pass
+
+    def is_consumed(self, seq: int) -> bool:
+        return True
+
+    def drained(self) -> bool:
+        return True
+
+    def abort(self):
+        pass
+
+
 # ---------------------------------------------------------------------------
 # Per-actor store (executor.py:257-313)
 
@@ -383,7 +487,7 @@ class DeviceStore:
 
 class _Actor:
     def __init__(self, actor: int, tg: TaskGraph, ops: DeviceOps, stats: RunStats,
-                 timeline: bool, inplace: bool = False):
+                 timeline: bool, inplace: bool = False, instrs=(), channels=None):
         self.actor = actor
         self.inplace = inplace       # resident training state: SGD overwrites the param
         self.tg = tg
@@ -404,6 +508,19 @@ class _Actor:
         self._add_by_rhs = {t.exec["rhs"]: (t.uid, t.exec["lhs"]) for t in tg.tasks.values()
                             if t.actor == actor and t.exec.get("type") == "add"}
         self.fused: set = set()
+        # sent buffers with no reader on this actor whose one channel is a
+        # peer-memory channel: produced straight into the receiver's slot
+        sends: dict = {}
+        for ins in instrs:
+            if isinstance(ins, SendStart):
+                sends.setdefault(ins.buffer, []).append((ins.dst, ins.seq))
+        self._peer_out = {}
+        for bid, dsts in sends.items():
+            ch = (channels or {}).get((actor, dsts[0][0]))
+            b = tg.buffers[bid]
+            if (len(dsts) == 1 and isinstance(ch, PeerChannel) and not b.is_output
+                    and all(tg.tasks[c].actor != actor for c in b.consumers)):
+                self._peer_out[bid] = ch.peer_slot(dsts[0][1])
 
     def stamp(self, slot: int):
         _lib.call("pc_timestamp", self.ts.data_ptr() + 8 * slot, self.stream.cuda_stream)
@@ -428,7 +545,11 @@ class _Actor:
         if kind == "stage-fwd":
             prog = p.fwd_programs[ex["stage"]]
             env = {v: st.get(bid, at) for v, bid in ex["feeds"].items()}
-            self.ops.run_ops(prog.ops, env)
+            self.ops.place = self._placement(ex)
+            try:
+                self.ops.run_ops(prog.ops, env)
+            finally:
+                self.ops.place = {}
             for v, bid in ex["outs"].items():
                 st.put(bid, env[v])
             if ex["stash_out"]:
@@ -440,10 +561,12 @@ class _Actor:
                 env.update(st.get(ex["stash_in"], at))
             acc = self._fusable_accumulators(ex) if self.ops.fuse_acc else {}
             self.ops.acc_into = acc
+            self.ops.place = self._placement(ex)
             try:
                 self.ops.run_ops(prog.ops, env)
             finally:
                 self.ops.acc_into = {}
+                self.ops.place = {}
             for v, bid in ex["outs"].items():
                 st.put(bid, env[v])
                 if v in acc and isinstance(env[v], torch.Tensor) and env[v] is acc[v]:
@@ -467,6 +590,13 @@ class _Actor:
         if self.timeline:
             self.stamp(s0 + 1)
             self.events.append((task.kind if task.is_loop else "aux", task.uid, s0, s0 + 1))
+
+    def _placement(self, ex) -> dict:
+        """{output value: peer slot} for this task's outputs that go to a
+        peer-memory channel (DeviceOps.place)."""
+        if not self._peer_out:
+            return {}
+        return {v: self._peer_out[bid] for v, bid in ex["outs"].items() if bid in self._peer_out}
 
     def _fusable_accumulators(self, ex) -> dict:
         """{bwd output value: running-sum tensor} for partial gradients whose
@@ -634,7 +764,8 @@ class PipelineEngine:
     NCCL communicators are created once; ``step`` runs one training step."""
 
     def __init__(self, cp: CommPlan, tg: TaskGraph, mode: str | Mode = "fp64",
-                 gpt: GPTConfig | None = None, devices=None, timeline: bool = False):
+                 gpt: GPTConfig | None = None, devices=None, timeline: bool = False,
+                 transport: str | None = None):
         if not cp.fused:
             raise ExecutorFault("plan must be fused before execution")
         if not torch.cuda.is_available():
@@ -666,6 +797,18 @@ class PipelineEngine:
                 raise ExecutorFault("single-process multi-GPU channels are not supported; "
                                     "launch one process per GPU (torchrun)")
         self._wire_meta = _wire_meta_fn(tg, self.mode)
+        # inter-process channels: "peer" (NVLink peer memory, producers write
+        # into the receiver's slots) or "nccl" (a communicator per channel)
+        # (peer needs every rank on this node: CUDA IPC + NVLink)
+        one_node = os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")) == \
+            os.environ.get("WORLD_SIZE", "1")
+        self.transport = transport or os.environ.get("PP200_TRANSPORT",
+                                                     "peer" if one_node else "nccl")
+        if self.transport not in ("peer", "nccl"):
+            raise ExecutorFault(f"unknown transport {self.transport!r}")
+        self._peer_allocs: list = []
+        self._peer_opens: list = []
+        self._peer_made = False
         self._resident: dict | None = None   # bid -> device value (load_params)
         self._tied = tied_holders(tg)
         self._tied_ch: dict = {}
@@ -677,6 +820,7 @@ class PipelineEngine:
         self._channels = self._make_channels()
 
     def _make_channels(self, keys=None, wire_meta=None):
+        plan = keys is None
         keys = self.cp.channels if keys is None else keys
         if not self.distributed:
             return {key: LocalChannel(*key) for key in keys}
@@ -688,6 +832,8 @@ class PipelineEngine:
         me = self.local[0]
         dev = self.devices[me]
         wire_meta = self._wire_meta if wire_meta is None else wire_meta
+        if plan and self.transport == "peer":
+            return self._make_peer_channels(store, tag, me, dev)
 
         def new_id() -> bytes:
             uid = (ctypes.c_char * 128)()
@@ -702,6 +848,37 @@ class PipelineEngine:
             with torch.cuda.device(dev):
                 _lib.call("pc_p2p_comm_init", ctypes.byref(comm), 2, idbuf, 0 if me == src else 1)
             out[(src, dst)] = NcclChannel(src, dst, me, comm, dev, wire_meta)
+        return out
+
+    def _make_peer_channels(self, store, tag, me, dev):
+        """Receiver side allocates and publishes its slots first, then every
+        sender maps its channels (so no rank waits on another's mapping)."""
+        import ctypes
+        self._peer_made = True
+        out = {}
+        layout = {key: _slot_layout(bids, self._wire_meta) for key, bids in self.cp.channels.items()}
+        for (src, dst) in sorted(self.cp.channels):
+            if dst != me:
+                continue
+            slots, total = layout[(src, dst)]
+            ptr, h = ctypes.c_void_p(), (ctypes.c_char * 64)()
+            with torch.cuda.device(dev):
+                _lib.call("pc_peer_alloc", total, ctypes.byref(ptr), h)
+            self._peer_allocs.append(ptr.value)
+            store.set(f"pp200/e{tag}/peer/{src}->{dst}", bytes(h))
+            out[(src, dst)] = PeerChannel(src, dst, me, ptr.value, self.cp.channels[(src, dst)],
+                                          slots)
+        for (src, dst) in sorted(self.cp.channels):
+            if src != me:
+                continue
+            slots, _ = layout[(src, dst)]
+            h = (ctypes.c_char * 64).from_buffer_copy(store.get(f"pp200/e{tag}/peer/{src}->{dst}"))
+            ptr = ctypes.c_void_p()
+            with torch.cuda.device(dev):
+                _lib.call("pc_peer_open", h, ctypes.byref(ptr))
+            self._peer_opens.append(ptr.value)
+            out[(src, dst)] = PeerChannel(src, dst, me, ptr.value, self.cp.channels[(src, dst)],
+                                          slots)
         return out
 
     # -- resident training state (multi-step, SURVEY.md §8(f) item 4) --
@@ -790,6 +967,16 @@ class PipelineEngine:
             if isinstance(ch, NcclChannel) and ch.comm:
                 _lib.call("pc_p2p_destroy", ch.comm)
                 ch.comm = None
+        if self._peer_made:
+            self._peer_made = False
+            for ptr in self._peer_opens:
+                _lib.call("pc_peer_close", ptr)
+            self._peer_opens = []
+            import torch.distributed as dist
+            dist.barrier()          # every mapping of this rank's slots is closed
+            for ptr in self._peer_allocs:
+                _lib.call("pc_peer_free", ptr)
+            self._peer_allocs = []
 
     # -- seeding (executor.py:405-414) --
     def _seed(self, actors: dict, params, batch, lr):
@@ -835,7 +1022,8 @@ class PipelineEngine:
         resident = params is None
         for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             ch.reset()
-        actors = {a: _Actor(a, self.tg, self._ops[a], stats, tl, inplace=resident)
+        actors = {a: _Actor(a, self.tg, self._ops[a], stats, tl, inplace=resident,
+                            instrs=self.cp.programs[a].instrs, channels=self._channels)
                   for a in self.local}
         for a, act in actors.items():
             # params / inputs are copied on the current stream; the actor stream waits
@@ -900,7 +1088,8 @@ class PipelineEngine:
         resident = params is None
         for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             ch.reset()
-        act = _Actor(a, self.tg, self._ops[a], stats, timeline, inplace=resident)
+        act = _Actor(a, self.tg, self._ops[a], stats, timeline, inplace=resident,
+                     instrs=self.cp.programs[a].instrs, channels=self._channels)
         actors = {a: act}
         with torch.cuda.device(act.device):
             act.stream.wait_stream(torch.cuda.current_stream(act.device))

@@ -34,6 +34,41 @@ def _worker(rank, world, port, case, q):
         from paper_2412_14374_b200 import schedules as S
         from paper_2412_14374_b200 import taskgraph as T
         from paper_2412_14374_b200.executor import PipelineEngine, run_pipelined
+        if case == "gpt-peer":
+            # the same step over NCCL channels and over NVLink peer-memory slots
+            # (producers write into the receiver's slot): bitwise equal, eager
+            # and as captured CUDA-graph replays of resident training
+            cfg = I.GPTConfig(layers=4, d_model=128, n_heads=2, d_ff=512, vocab=256, seq_len=64,
+                              microbatch_size=2, yields=(2, 3, 5)[:world - 1], yield_every=6)
+            M = 8
+            p = I.derive_backward(I.partition_stages(I.build_gpt(cfg)))
+            s = S.one_f_one_b(world, M)
+            tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
+            cp = C.plan_pipeline(tg)
+            oc = dict(layers=4, d=128, heads=2, ff=512, vocab=256, seq=64, mbs=2)
+            rng = np.random.default_rng(0)
+            params = {k: v.astype(np.float32) for k, v in gpt.init_params(oc, rng, std=0.05).items()}
+            tokens = gpt.init_tokens(oc, M, rng).reshape(M * 2, 64)
+            outs = {}
+            for tr in ("nccl", "peer"):
+                eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg, transport=tr)
+                r = eng.step(params, tokens)
+                eng.load_params(params)
+                eng.step(None, tokens, lr=0.01)
+                cs = eng.capture(None, tokens, lr=0.01)
+                cs.replay()
+                cs.replay()
+                torch.cuda.synchronize()
+                if tr == "peer":
+                    from paper_2412_14374_b200.executor import PeerChannel
+                    sent = [ch for (src, _), ch in eng._channels.items() if src == rank]
+                    assert all(isinstance(ch, PeerChannel) for ch in sent)
+                    assert sum(ch.in_place for ch in sent) > 0
+                outs[tr] = (r.grads, None if r.losses is None else np.asarray(r.losses),
+                            eng.state_dict())
+                eng.close()
+            q.put((rank, outs))
+            return
         if case == "ffn-train":
             # resident multi-step training: eager step, then a captured graph
             # replayed twice; the tied w0 is re-broadcast 0 -> P-1 every step
@@ -153,3 +188,17 @@ def test_two_gpu_resident_training_rebroadcasts_tied_weight():
         assert ffn.rel(losses[k], ref_losses[k]) < 1e-12, k
     for q in ref:
         assert ffn.rel(state[q], ref[q]) < 1e-12, q
+
+
+def test_two_gpu_peer_transport_equals_nccl():
+    outs = _run("gpt-peer", 2)
+    for rank, o in outs:
+        (ga, la, sa), (gb, lb, sb) = o["nccl"], o["peer"]
+        assert sorted(ga) == sorted(gb)
+        for q in ga:
+            assert np.array_equal(ga[q], gb[q]), (rank, q)
+        assert (la is None) == (lb is None)
+        if la is not None:
+            assert np.array_equal(la, lb)
+        for q in sa:
+            assert np.array_equal(sa[q], sb[q]), (rank, q)
