@@ -26,6 +26,7 @@ import subprocess
 import sys
 import threading
 import time
+from pathlib import Path
 
 import numpy as np
 
@@ -183,6 +184,54 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def gemm_shapes(cfg, P):
+    """(M, N, K, transA, transB, epilogue, has_aux, has_u, fp32 out) of every
+    tcgen05 GEMM of one stage step, with launches per microbatch: per GPT
+    block and, on the last stage, the LM head.  Weight gradients accumulate
+    into the running sum (device.py _wgrad_into: TMA reduce-add, ordered
+    split-K) as in every microbatch after the first."""
+    from paper_2412_14374_b200 import _lib as E
+    T, d, f, V = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.vocab
+    WG = E.EPI_ACCUM | E.EPI_SPLITK_ORDERED
+    block = [(T, 3 * d, d, 0, 1, E.EPI_BIAS, 0, 0, 0),                        # qkv
+             (T, d, d, 0, 1, E.EPI_BIAS | E.EPI_RESIDUAL, 1, 0, 0),            # attn out
+             (T, f, d, 0, 1, E.EPI_BIAS | E.EPI_GELU, 0, 1, 0),                # fc1
+             (T, d, f, 0, 1, E.EPI_BIAS | E.EPI_RESIDUAL, 1, 0, 0),            # fc2
+             (d, f, T, 1, 0, WG, 0, 0, 1),                                     # dW fc2
+             (T, f, d, 0, 1, E.EPI_GELU_GRAD, 1, 0, 0),                        # dX fc2 (gelu')
+             (f, d, T, 1, 0, WG, 0, 0, 1),                                     # dW fc1
+             (T, d, f, 0, 1, 0, 0, 0, 0),                                      # dX fc1
+             (d, d, T, 1, 0, WG, 0, 0, 1),                                     # dW out
+             (T, d, d, 0, 1, 0, 0, 0, 0),                                      # dX out
+             (3 * d, d, T, 1, 0, WG, 0, 0, 1),                                 # dW qkv
+             (T, d, 3 * d, 0, 1, 0, 0, 0, 0)]                                  # dX qkv
+    head = [(T, V, d, 0, 1, 0, 0, 0, 0), (T, d, V, 0, 1, 0, 0, 0, 0),
+            (V, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1)]
+    return block, head
+
+
+def gemm_args(shape, st):
+    """Operands and pc_gemm arguments for one entry of gemm_shapes."""
+    import torch
+    from paper_2412_14374_b200 import _lib
+    Mm, N, K, ta, tb, epi, has_aux, has_u, f32 = shape
+    A = torch.randn((K, Mm) if ta else (Mm, K), device="cuda").bfloat16()
+    B = torch.randn((N, K) if tb else (K, N), device="cuda").bfloat16()
+    C = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
+    bias = torch.zeros(N, device="cuda")
+    if epi & _lib.EPI_SPLITK_ORDERED:
+        aux, ldaux = torch.zeros(1 << 16, dtype=torch.int32, device="cuda"), 1 << 16
+    else:
+        aux = torch.randn(Mm, N, device="cuda").bfloat16() if has_aux else None
+        ldaux = N
+    U = torch.empty(Mm, N, device="cuda", dtype=torch.bfloat16) if has_u else None
+    args = (_lib.PC_BF16, _lib.PC_F32 if f32 else _lib.PC_BF16, ta, tb, Mm, N, K,
+            A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, epi,
+            bias.data_ptr(), aux.data_ptr() if aux is not None else None, ldaux,
+            U.data_ptr() if U is not None else None, N, st.cuda_stream)
+    return args, (A, B, C, bias, aux, U)
+
+
 def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
     """Average achieved TFLOP/s of the tcgen05 GEMM over the shape mix of one
     stage step, each GEMM issued exactly as device.py issues it (operand
@@ -190,40 +239,16 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
     launch stream (warm, back to back); share of the step it accounts for."""
     import torch
     from paper_2412_14374_b200 import _lib
-    T, d, f, V = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.vocab
-    E = _lib
-    # (M, N, K, transA, transB, epilogue, has_aux, has_u, fp32 out) per GPT block
-    shapes = [(T, 3 * d, d, 0, 1, E.EPI_BIAS, 0, 0, 0),                        # qkv
-              (T, d, d, 0, 1, E.EPI_BIAS | E.EPI_RESIDUAL, 1, 0, 0),            # attn out
-              (T, f, d, 0, 1, E.EPI_BIAS | E.EPI_GELU, 0, 1, 0),                # fc1
-              (T, d, f, 0, 1, E.EPI_BIAS | E.EPI_RESIDUAL, 1, 0, 0),            # fc2
-              (d, f, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                    # dW fc2
-              (T, f, d, 0, 1, E.EPI_GELU_GRAD, 1, 0, 0),                        # dX fc2 (gelu')
-              (f, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                    # dW fc1
-              (T, d, f, 0, 1, 0, 0, 0, 0),                                      # dX fc1
-              (d, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                    # dW out
-              (T, d, d, 0, 1, 0, 0, 0, 0),                                      # dX out
-              (3 * d, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1),                # dW qkv
-              (T, d, 3 * d, 0, 1, 0, 0, 0, 0)]                                  # dX qkv
-    head = [(T, V, d, 0, 1, 0, 0, 0, 0), (T, d, V, 0, 1, 0, 0, 0, 0),
-            (V, d, T, 1, 0, E.EPI_SPLITK_ZERO_C, 0, 0, 1)]
+    block, head = gemm_shapes(cfg, P)
     st = torch.cuda.current_stream()
     tot_flops = tot_ms = 0.0
     per = []
-    for (Mm, N, K, ta, tb, epi, has_aux, has_u, f32), count in \
-            [(s, stage_blocks) for s in shapes] + [(s, 1 if P == 1 else 0) for s in head]:
+    traffic = gemm_traffic()
+    for shape, count in [(s, stage_blocks) for s in block] + [(s, 1 if P == 1 else 0) for s in head]:
         if count == 0:
             continue
-        A = torch.randn((K, Mm) if ta else (Mm, K), device="cuda").bfloat16()
-        B = torch.randn((N, K) if tb else (K, N), device="cuda").bfloat16()
-        C = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
-        bias = torch.zeros(N, device="cuda")
-        aux = torch.randn(Mm, N, device="cuda").bfloat16() if has_aux else None
-        U = torch.empty(Mm, N, device="cuda", dtype=torch.bfloat16) if has_u else None
-        args = (_lib.PC_BF16, _lib.PC_F32 if f32 else _lib.PC_BF16, ta, tb, Mm, N, K,
-                A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, epi,
-                bias.data_ptr(), aux.data_ptr() if aux is not None else None, N,
-                U.data_ptr() if U is not None else None, N, st.cuda_stream)
+        Mm, N, K, ta, tb, epi = shape[:6]
+        args, keep = gemm_args(shape, st)
         for _ in range(3):
             _lib.call("pc_gemm", *args)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -235,17 +260,38 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         fl = 2.0 * Mm * N * K
-        per.append({"shape": [Mm, N, K, ta, tb], "epilogue": epi, "ms": round(ms, 4),
-                    "tflops": round(fl / ms / 1e9, 1), "launches_per_mb": count})
+        row = {"shape": [Mm, N, K, ta, tb], "epilogue": epi, "ms": round(ms, 4),
+               "tflops": round(fl / ms / 1e9, 1), "launches_per_mb": count}
+        key = f"{Mm}x{N}x{K}:{epi}"
+        if key in traffic:
+            row["dram_bytes"] = traffic[key]
+        per.append(row)
         tot_flops += fl * count * M_MICRO
         tot_ms += ms * count * M_MICRO
-        del A, B, C, aux, U
+        del keep
     achieved = tot_flops / tot_ms / 1e9 if tot_ms else 0.0
+    # DRAM bytes per launch over the same mix, from the committed ncu --set full capture
+    have = [r for r in per if "dram_bytes" in r]
+    tr = (sum(r["dram_bytes"] * r["launches_per_mb"] for r in have) /
+          sum(r["launches_per_mb"] for r in have)) if have and len(have) == len(per) else None
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4),
+            "traffic": None if tr is None else round(tr),
+            "traffic_source": "profiles/r01_ncu_gemm_mix.json (ncu --set full, per launch)"
+            if tr is not None else None,
             "kernel": "tc_gemm_kernel (tcgen05.mma kind::f16, TMA, TMEM)",
             "share_of_step": round(tot_ms / step_ms, 3) if step_ms else None,
             "shapes": per}
+
+
+def gemm_traffic() -> dict:
+    """{"MxNxK:epilogue": dram bytes read + written per launch} from the
+    committed ncu --set full capture of the GEMM mix (tools/ncu_gemm_mix.py)."""
+    p = Path(__file__).resolve().parent / "profiles" / "r01_ncu_gemm_mix.json"
+    try:
+        return {k: v["dram_bytes"] for k, v in json.loads(p.read_text())["shapes"].items()}
+    except (OSError, ValueError, KeyError):
+        return {}
 
 
 def cpu_baseline(cfg_kw, seconds_hint=True):
