@@ -51,6 +51,7 @@ struct TcEpi {
   void* aux_out;
   int64_t ldaux_out;
   int M, N, flags, out_f32;
+  int n_fast;  // tile raster: 1 = consecutive tiles walk N (share the A rows), 0 = walk M
 };
 
 // CG = 1: one CTA owns a 128 x BN tile.  CG = 2: a cluster pair owns a
@@ -355,8 +356,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       };
       for (int u = cid; u < num_units; u += ncl) {
         const int t = u % num_tiles, sp = u / num_tiles;
-        const int m0 = (t % num_m) * TC_BM * CG + static_cast<int>(rank) * TC_BM;
-        const int nb = (t / num_m) * BN + static_cast<int>(rank) * Cfg::B_ROWS;
+        const int mi = ep.n_fast ? t / num_n : t % num_m, ni = ep.n_fast ? t % num_n : t / num_m;
+        const int m0 = mi * TC_BM * CG + static_cast<int>(rank) * TC_BM;
+        const int nb = ni * BN + static_cast<int>(rank) * Cfg::B_ROWS;
         for (int kb = sp * nk / ep.ksplit; kb < (sp + 1) * nk / ep.ksplit; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (ep.flags & (1 << 17)) {  // profiling ablation: no operand traffic
@@ -494,8 +496,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t aphase = 0;
     for (int u = cid; u < num_units; u += ncl) {
       const int t = u % num_tiles;
-      const int m0 = (t % num_m) * TC_BM * CG + static_cast<int>(rank) * TC_BM;
-      const int n0 = (t / num_m) * BN;
+      const int mi = ep.n_fast ? t / num_n : t % num_m, ni = ep.n_fast ? t % num_n : t / num_m;
+      const int m0 = mi * TC_BM * CG + static_cast<int>(rank) * TC_BM;
+      const int n0 = ni * BN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
@@ -976,6 +979,10 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   const bool can_split = ((epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c) || ordered;
   int bn, cg, ksplit;
   choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit);
+  // raster: an A operand far larger than L2 (the LM-head gradients: 824 MB of
+  // logit gradients) is streamed once when the tiles sharing its rows run
+  // together; otherwise walk M (B is the large, reused operand)
+  const bool n_fast = static_cast<double>(M) * K * 2 > 64e6 && M * 2 > N;
   if (ordered && ksplit > 1) {
     const int64_t tiles = ((M + TC_BM * cg - 1) / (TC_BM * cg)) * ((N + bn - 1) / bn);
     PP_CHECK_ARG(ldaux >= tiles * cg * TC_EPI_WARPS, "gemm: ordered split-K flag array too short");
@@ -1037,7 +1044,8 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     if (rc) return rc;
   }
   TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, tma_a ? 1 : 0, cw64 ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
-           aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi | (g_ablate << 16), out_f32};
+           aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi | (g_ablate << 16), out_f32,
+           n_fast ? 1 : 0};
   const int iM = static_cast<int>(M), iN = static_cast<int>(N), iK = static_cast<int>(K);
   switch (bn * 4 + cg) {
     case 256 * 4 + 2: return dispatch_majors<256, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);

@@ -81,6 +81,9 @@ class Act:
         self.saved: dict = {}
 
 
+_ABLATE_BIAS = os.environ.get("PP200_ABLATE_BIAS_GRAD") == "1"
+
+
 class PeerBuf:
     """A message slot in another GPU's memory (NVLink peer mapping): the
     producing kernel of a sent value writes here directly.  Only its address
@@ -685,6 +688,8 @@ class DeviceOps:
         def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname):
             self._fork()
             self._wgrad_into(M_, N_, T, A, lda, Bm, ldb, gs(wname), fused, self._side())
+            if _ABLATE_BIAS:   # profiling only: bias gradients left unset
+                return
             call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, M_, A.data_ptr(), lda,
                  gs(bname).data_ptr(), int(fused), *self.red_ws(T, M_, side=True), sst)
 

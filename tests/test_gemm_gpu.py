@@ -94,6 +94,18 @@ def test_bf16_large_persistent():
     assert rel(C, ref) < 1e-5
 
 
+@pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0), (0, 0)])
+@pytest.mark.parametrize("shape", [(8192, 768, 5000), (5000, 768, 8192), (8200, 200, 4104)])
+def test_bf16_n_raster_large_a(shape, ta, tb):
+    """A operand larger than L2 (the LM-head gradient GEMMs): tiles walk N so
+    the A rows stream from DRAM once; results as with the M raster."""
+    M, N, K = shape
+    A, B, ref = make_operands(M, N, K, ta, tb, torch.bfloat16, seed=6)
+    C = run_gemm(A, B, ta, tb, M, N, K, torch.float32)
+    torch.cuda.synchronize()
+    assert rel(C, ref) < 3e-5   # fp32 accumulation over K = 8192 unit-normal products
+
+
 @pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.float64, 1e-13)])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 def test_simt_gemm(dtype, tol, ta, tb):
