@@ -236,11 +236,12 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
     """Average achieved TFLOP/s of the tcgen05 GEMM over the shape mix of one
     stage step, each GEMM issued exactly as device.py issues it (operand
     majors, fused epilogue, split-K hint) and timed with CUDA events on its
-    launch stream (warm, back to back); share of the step it accounts for."""
+    launch stream (warm, back to back, replayed from a CUDA graph); share of
+    the step it accounts for."""
     import torch
     from paper_2412_14374_b200 import _lib
     block, head = gemm_shapes(cfg, P)
-    st = torch.cuda.current_stream()
+    st = torch.cuda.Stream()
     tot_flops = tot_ms = 0.0
     per = []
     traffic = gemm_traffic()
@@ -249,16 +250,24 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
             continue
         Mm, N, K, ta, tb, epi = shape[:6]
         args, keep = gemm_args(shape, st)
-        for _ in range(3):
-            _lib.call("pc_gemm", *args)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 10
-        e0.record(st)
-        for _ in range(reps):
-            _lib.call("pc_gemm", *args)
-        e1.record(st)
+        # device time of back-to-back launches, issued from a CUDA graph as in
+        # the step (host launch cost would otherwise pace the short GEMMs)
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                _lib.call("pc_gemm", *args)
+            reps = 10
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(reps):
+                    _lib.call("pc_gemm", *args)
+            g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            g.replay()
+            e1.record(st)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
+        del g
         fl = 2.0 * Mm * N * K
         row = {"shape": [Mm, N, K, ta, tb], "epilogue": epi, "ms": round(ms, 4),
                "tflops": round(fl / ms / 1e9, 1), "launches_per_mb": count}
