@@ -52,8 +52,8 @@ enum pc_dtype { PC_F32 = 0, PC_F64 = 1, PC_BF16 = 2, PC_I32 = 3 };
 #define PC_EPI_SPLITK_ZERO_C 128 /* caller guarantees an fp32 C filled with zeros: the
                                     kernel may split K in two halves reduce-added into C
                                     (deterministic: two terms onto 0 commute) */
-#define PC_EPI_SPLITK_ORDERED 256 /* with PC_EPI_ACCUM: the kernel may split K in two
-                                    halves added onto C in a fixed order, (C + h0) + h1,
+#define PC_EPI_SPLITK_ORDERED 256 /* with PC_EPI_ACCUM: the kernel may split K in 2 or 4
+                                    parts added onto C in a fixed order, ((C + h0) + h1)..,
                                     sequenced per tile by flags: aux = zeroed uint32 flag
                                     array, ldaux = its length (>= tiles x 16) */
 
@@ -70,9 +70,10 @@ int pc_gemm(int dtype_in, int dtype_out, int transA, int transB, int64_t M, int6
             int epilogue, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
             int64_t ldaux_out, void* stream);
 
-/* The tcgen05 tile choice pc_gemm makes for a bf16 problem (transB as pc_gemm; split_ok =
- * the caller passes PC_EPI_SPLITK_ZERO_C with fp32 C): tile width, CTA pair (1 or 2),
- * K split (1 or 2).  Lets a caller fuse accumulation only where the GEMM is unsplit. */
+/* The tcgen05 tile choice pc_gemm makes for a bf16 problem (transB as pc_gemm; split_ok:
+ * 0 = no split allowed, 1 = PC_EPI_SPLITK_ZERO_C with fp32 C (K split 1 or 2),
+ * 2 = PC_EPI_ACCUM | PC_EPI_SPLITK_ORDERED (1 or 2)): tile width, CTA pair (1 or 2),
+ * K split. */
 int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_ok, int* bn,
                         int* cta_pair, int* ksplit);
 /* Force the tcgen05 GEMM tile width (0 = heuristic, else 64/128/192/256). Test hook. */

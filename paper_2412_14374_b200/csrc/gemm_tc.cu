@@ -55,14 +55,20 @@ struct TcEpi {
 };
 
 // First k-block of split ``sp`` (sp = ksplit: the end).  Ordered split-K
-// gives split 0 about 6 % fewer k-blocks (nk/16): it finishes first, so its
-// reduce-add into C overlaps split 1's last k-blocks instead of making
-// split 1 wait for it.
+// staggers the split lengths (each dl = nk / (4 ks) k-blocks longer than the
+// previous; ks = 2: 6 % of nk either side of the middle): split s finishes
+// after split s-1, so the earlier reduce-adds overlap the later splits'
+// last k-blocks instead of making them wait.
 __device__ __forceinline__ int k_split_at(int sp, int nk, const TcEpi& ep) {
   if (sp == 0) return 0;
-  if (sp >= ep.ksplit) return nk;
-  const int half = sp * nk / ep.ksplit;
-  return (ep.flags & PC_EPI_SPLITK_ORDERED) ? half - (nk + 15) / 16 : half;
+  const int ks = ep.ksplit;
+  if (sp >= ks) return nk;
+  if (!(ep.flags & PC_EPI_SPLITK_ORDERED)) return sp * nk / ks;
+  // split lengths L0 + s * dl, dl = nk / (4 ks): each split starts its add
+  // about one epilogue after the previous one's
+  const int dl = (nk + 4 * ks - 1) / (4 * ks);
+  const int l0 = (nk - dl * ks * (ks - 1) / 2) / ks;
+  return sp * l0 + dl * sp * (sp - 1) / 2;
 }
 
 // CG = 1: one CTA owns a 128 x BN tile.  CG = 2: a cluster pair owns a
@@ -659,15 +665,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
       } else {
-      // ordered split-K accumulate: split 1 adds its half onto C only after
-      // split 0's adds to the same region (this warp's rows x columns) landed
+      // ordered split-K accumulate: split s adds its part onto C only after
+      // splits 0..s-1 added theirs to the same region (this warp's rows x
+      // columns); the region's flag counts the splits that landed
       const bool ordered = (ep.flags & PC_EPI_SPLITK_ORDERED) && ep.ksplit > 1;
+      const int sp = u / num_tiles;
       unsigned* oflag = static_cast<unsigned*>(const_cast<void*>(ep.aux)) +
                         ((t * CG + static_cast<int>(rank)) * TC_EPI_WARPS + (warp - 4));
-      if (ordered && u >= num_tiles) {
+      if (ordered && sp > 0) {
         if (lane == 0) {
-          while (ld_acquire_gpu(oflag) == 0u) __nanosleep(100);
-          st_release_gpu(oflag, 0u);  // re-armed for the next launch
+          while (ld_acquire_gpu(oflag) != static_cast<unsigned>(sp)) __nanosleep(100);
+          if (sp == ep.ksplit - 1) st_release_gpu(oflag, 0u);  // last: re-armed for the next launch
           fence_proxy_async_global();
         }
         __syncwarp();
@@ -739,10 +747,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           bulk_commit();
         }
       }
-      if (ordered && u < num_tiles && lane == 0) {  // split 0: publish once its adds landed
+      if (ordered && sp < ep.ksplit - 1 && lane == 0) {  // publish once this split's adds landed
         bulk_wait0();
         fence_proxy_async_global();
-        st_release_gpu(oflag, 1u);
+        st_release_gpu(oflag, static_cast<unsigned>(sp + 1));
       }
       }
       if (cend <= cstart) release_acc<CG>(rel, lane);
@@ -927,12 +935,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn() { return tmap_encoder(); }
 // split-K: exactly 2 K halves reduce-added onto a zero-filled fp32 C
 // (0 + a + b == 0 + b + a bitwise), only when the caller allows it.
 static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool can_split,
-                         int* bn_out, int* cg_out, int* ks_out) {
+                         int* bn_out, int* cg_out, int* ks_out, int max_split = 2) {
   struct Cand { int bn, cg; double eff; };
   const Cand cands[7] = {{256, 2, 1.0}, {192, 2, 0.97}, {256, 1, 0.88}, {192, 1, 0.85},
                          {128, 2, 0.78}, {128, 1, 0.75}, {64, 1, 0.45}};
   const int sms = num_sms();
   can_split = can_split && K >= 2 * TC_BK * 8;
+  if (!can_split) max_split = 1;
   int bn = 0, cg = 1, ksplit = 1;
   double best = -1.0;
   for (const Cand& c : cands) {
@@ -945,11 +954,12 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
     const int64_t tm = TC_BM * c.cg;
     const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
     const int64_t slots = sms / c.cg;
-    for (int ks = 1; ks <= (can_split ? 2 : 1); ++ks) {
+    for (int ks = 1; ks <= max_split; ks *= 2) {
+      if (K < static_cast<int64_t>(ks) * TC_BK * 8) break;   // >= 8 k-blocks per split
       const int64_t waves = (tiles * ks + slots - 1) / slots;
       const double score = static_cast<double>(M) * N * ks /
                            (static_cast<double>(waves) * slots * tm * c.bn) * c.eff *
-                           (ks > 1 ? 0.97 : 1.0);
+                           (ks == 1 ? 1.0 : ks == 2 ? 0.97 : 0.90);
       if (score > best + 1e-9) {
         best = score;
         bn = c.bn;
@@ -989,7 +999,9 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
                "gemm: ordered split-K needs accumulate and a flag array in aux");
   const bool can_split = ((epi & PC_EPI_SPLITK_ZERO_C) && out_f32 && tma_c) || ordered;
   int bn, cg, ksplit;
-  choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit);
+  // (the ordered protocol handles 4 splits, but measured on the C2 weight
+  // GEMMs a 4-link add chain costs more than the wave it fills: 2 at most)
+  choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit, 2);
   // raster: an A operand far larger than L2 (the LM-head gradients: 824 MB of
   // logit gradients) is streamed once when the tiles sharing its rows run
   // together; otherwise walk M (B is the large, reused operand)
@@ -1075,7 +1087,7 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
 extern "C" int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_ok,
                                    int* bn, int* cta_pair, int* ksplit) {
   PP_CHECK_ARG(M > 0 && N > 0 && K > 0 && bn && cta_pair && ksplit, "gemm_tile_choice: bad args");
-  pp200::choose_tiles(transB != 0, M, N, K, split_ok != 0, bn, cta_pair, ksplit);
+  pp200::choose_tiles(transB != 0, M, N, K, split_ok != 0, bn, cta_pair, ksplit, 2);
   return PC_OK;
 }
 

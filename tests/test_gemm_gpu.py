@@ -204,16 +204,25 @@ def test_tile_choice_reports_split():
     assert ks.value == 1
 
 
-@pytest.mark.parametrize("shape", [(768, 768, 8192), (2304, 768, 8192), (768, 3072, 8192)])
+def _ordered_bounds(nk, ks):
+    """Split boundaries of the ordered split-K (gemm_tc.cu k_split_at)."""
+    if ks == 1:
+        return [0, nk]
+    dl = (nk + 4 * ks - 1) // (4 * ks)
+    l0 = (nk - dl * ks * (ks - 1) // 2) // ks
+    return [s * l0 + dl * s * (s - 1) // 2 for s in range(ks)] + [nk]
+
+
+@pytest.mark.parametrize("shape", [(768, 768, 8192), (2304, 768, 8192), (768, 3072, 8192),
+                                   (256, 256, 4096)])
 def test_ordered_splitk_accumulate(shape):
-    """C += op(A) op(B) split in two K halves and added in a fixed order,
-    (C + h0) + h1, sequenced per tile by flags: equal to two unsplit
-    half-products added one after the other, run-to-run identical, and the
-    flag array is left zeroed."""
+    """C += op(A) op(B) split in K and added in a fixed order, ((C + h0) + h1)
+    + ..., sequenced per tile by flags: equal to the unsplit part-products
+    added one after the other, run-to-run identical, flags left zeroed."""
     import ctypes
     M, N, K = shape
     bn, cg, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    _lib.call("pc_gemm_tile_choice", 0, M, N, K, 1, ctypes.byref(bn), ctypes.byref(cg),
+    _lib.call("pc_gemm_tile_choice", 0, M, N, K, 2, ctypes.byref(bn), ctypes.byref(cg),
               ctypes.byref(ks))
     assert ks.value == 2
     A, B, ref = make_operands(M, N, K, 1, 0, torch.bfloat16, seed=4)
@@ -226,12 +235,12 @@ def test_ordered_splitk_accumulate(shape):
         run_gemm(A, B, 1, 0, M, N, K, torch.float32,
                  epi=_lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED, aux=flags, C=C)
         outs.append(C)
-    nk = (K + 63) // 64
-    kh = (nk // 2 - (nk + 15) // 16) * 64   # split 0 is ~6 % shorter (gemm_tc.cu k_split_at)
+    bounds = [64 * b for b in _ordered_bounds((K + 63) // 64, ks.value)]
+    bounds[-1] = K
     want = acc0.clone()
     st = torch.cuda.current_stream().cuda_stream
     with forced(bn.value, cg.value):
-        for lo, hi in ((0, kh), (kh, K)):
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
             h = run_gemm(A[lo:hi], B[lo:hi], 1, 0, M, N, hi - lo, torch.float32)
             _lib.call("pc_accumulate", _lib.PC_F32, _lib.PC_F32, want.numel(), want.data_ptr(),
                       h.data_ptr(), st)
