@@ -416,6 +416,13 @@ def main():
     for _ in range(max(args.warmup, 3)):
         run(tokens_dev)
     torch.cuda.synchronize()
+    if os.environ.get("PP200_NCU_ONE_STEP") == "1":
+        # `ncu --profile-from-start off`: the launch list of exactly one timed
+        # step (graph replay); numbers printed by such a run are not bench values
+        torch.cuda.profiler.start()
+        run(tokens_dev)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
 
     def barrier():
         if world > 1:
