@@ -452,7 +452,8 @@ def main():
     wall = time.perf_counter() - t0
     clocks.window = (t0, t0 + wall)
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    launches = cap.launches if use_graph else int((_lib.launch_count - launches0) / args.steps)
+    # kernels per step: the captured graph's kernel nodes (libpp200 calls when eager)
+    launches = cap.kernels if use_graph else int((_lib.launch_count - launches0) / args.steps)
     clk = clocks.stop()
 
     # ---- e2e through the public API: pinned host tokens -> device, losses -> host ----

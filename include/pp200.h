@@ -195,6 +195,8 @@ int pc_peer_close(void* ptr);
 int pc_stream_write_u32(void* addr, uint32_t value, void* stream);
 int pc_stream_wait_u32(void* addr, uint32_t value, void* stream);
 int pc_peer_copy(void* dst, const void* src, int64_t bytes, void* stream);
+/* Kernel nodes of a captured CUDA graph (cudaGraph_t), child graphs included. */
+int pc_graph_kernel_nodes(void* graph, int64_t* n);
 
 /* ---- inter-stage transport (Channel, executor.py:201-254) over NCCL ---- */
 int pc_p2p_available(void);

@@ -9,6 +9,8 @@
 
 #include <cuda.h>
 
+#include <vector>
+
 using namespace pp200;
 
 namespace {
@@ -89,4 +91,46 @@ extern "C" int pc_peer_copy(void* dst, const void* src, int64_t bytes, void* str
   PP_CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice,
                               static_cast<cudaStream_t>(stream)));
   return PC_OK;
+}
+
+// Kernel nodes of a captured CUDA graph (child graphs included): the number of
+// kernels one replay of a captured step launches (bench.py gpu_launches).
+// Driver API: the runtime's node-type query rejects stream-memop nodes.
+using NodesFn = CUresult (*)(CUgraph, CUgraphNode*, size_t*);
+using TypeFn = CUresult (*)(CUgraphNode, CUgraphNodeType*);
+using ChildFn = CUresult (*)(CUgraphNode, CUgraph*);
+
+static int count_kernel_nodes(CUgraph g, int64_t* n) {
+  static NodesFn nodes_fn = driver_fn<NodesFn>("cuGraphGetNodes");
+  static TypeFn type_fn = driver_fn<TypeFn>("cuGraphNodeGetType");
+  static ChildFn child_fn = driver_fn<ChildFn>("cuGraphChildGraphNodeGetGraph");
+  PP_CHECK_ARG(nodes_fn && type_fn && child_fn, "graph node queries unavailable");
+  size_t num = 0;
+  if (nodes_fn(g, nullptr, &num) != CUDA_SUCCESS) {
+    set_error("cuGraphGetNodes failed");
+    return PC_ERR_CUDA;
+  }
+  std::vector<CUgraphNode> nodes(num);
+  if (num && nodes_fn(g, nodes.data(), &num) != CUDA_SUCCESS) {
+    set_error("cuGraphGetNodes failed");
+    return PC_ERR_CUDA;
+  }
+  for (CUgraphNode nd : nodes) {
+    CUgraphNodeType t;
+    if (type_fn(nd, &t) != CUDA_SUCCESS) continue;
+    if (t == CU_GRAPH_NODE_TYPE_KERNEL) {
+      ++*n;
+    } else if (t == CU_GRAPH_NODE_TYPE_GRAPH) {
+      CUgraph child;
+      if (child_fn(nd, &child) == CUDA_SUCCESS)
+        if (int rc = count_kernel_nodes(child, n)) return rc;
+    }
+  }
+  return PC_OK;
+}
+
+extern "C" int pc_graph_kernel_nodes(void* graph, int64_t* n) {
+  PP_CHECK_ARG(graph && n, "graph_kernel_nodes: bad args");
+  *n = 0;
+  return count_kernel_nodes(static_cast<CUgraph>(graph), n);
 }

@@ -1108,7 +1108,7 @@ class PipelineEngine:
             dist.barrier()
         stats.driver_messages += 1
         launches0 = _lib.launch_count
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.device(act.device):
             torch.cuda.synchronize()
             with torch.cuda.graph(graph, stream=act.stream):
@@ -1125,9 +1125,14 @@ class PipelineEngine:
         tl_on, act.timeline = act.timeline, False   # timestamps are read after a replay
         result = self._gather(actors, stats, strict_store=False, to_host=False)
         act.timeline = tl_on
+        import ctypes
+        nk = ctypes.c_int64(0)
+        _lib.call("pc_graph_kernel_nodes", ctypes.c_void_p(graph.raw_cuda_graph()), ctypes.byref(nk))
+        graph.instantiate()
         cs = CapturedStep(self, graph, act, inputs, result)
         self._captures.append(cs)
         cs.launches = _lib.launch_count - launches0   # libpp200 calls recorded per replay
+        cs.kernels = nk.value                         # kernel nodes = kernels per replay
         return cs
 
     def _abort_channels(self):
