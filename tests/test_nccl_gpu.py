@@ -109,12 +109,16 @@ def _worker(rank, world, port, case, q):
             res = run_pipelined(cp, tg, params, batch)
             ref = ffn.run_reference_ffn(params, batch, M, L, True)
         else:
+            # "gpt": 1F1B; "gpt-interleaved": 2 chunks per GPU (4 stages on 2 GPUs),
+            # both channel directions carry two stage boundaries
+            inter = case == "gpt-interleaved"
+            yl = (1, 3, 4) if inter else (2, 3, 5)[:world - 1]
             cfg = I.GPTConfig(layers=4, d_model=128, n_heads=2, d_ff=512, vocab=256, seq_len=64,
-                              microbatch_size=2, yields=(2, 3, 5)[:world - 1] if world > 1 else None,
+                              microbatch_size=2, yields=yl if world > 1 else None,
                               yield_every=6)
             M = 8
             p = I.derive_backward(I.partition_stages(I.build_gpt(cfg)))
-            s = S.one_f_one_b(world, M)
+            s = S.interleaved_1f1b(world, M, 2) if inter else S.one_f_one_b(world, M)
             tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
             cp = C.plan_pipeline(tg)
             oc = dict(layers=4, d=128, heads=2, ff=512, vocab=256, seq=64, mbs=2)
@@ -151,7 +155,7 @@ def _run(case, world):
     return outs
 
 
-@pytest.mark.parametrize("case,tol", [("ffn", 1e-12), ("gpt", 2e-2)])
+@pytest.mark.parametrize("case,tol", [("ffn", 1e-12), ("gpt", 2e-2), ("gpt-interleaved", 2e-2)])
 def test_two_gpu_nccl_pipeline_matches_oracle(case, tol):
     world = 2
     outs = _run(case, world)
