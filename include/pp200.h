@@ -136,6 +136,12 @@ int pc_layernorm_bwd_acc(int dtype, int64_t rows, int64_t d, const void* dy, con
                          const float* gamma, const float* mean, const float* rstd,
                          const void* dres, void* dx, float* dgamma, float* dbeta, int accumulate,
                          void* ws, int64_t ws_bytes, void* stream);
+/* dgamma (+)= sum_r dy * xhat, dbeta (+)= sum_r dy (dbeta may be NULL; mean NULL =
+ * RMSNorm statistics): the LayerNorm parameter gradients alone, so they can run on
+ * another stream than the dx chain (pc_layernorm_bwd_acc with dgamma = dbeta = NULL). */
+int pc_layernorm_param_grads(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
+                             const float* mean, const float* rstd, float* dgamma, float* dbeta,
+                             int accumulate, void* ws, int64_t ws_bytes, void* stream);
 /* ---- Llama-style block pieces (BASELINE config C5; oracle/llama.py) ---- */
 /* y = x * rsqrt(mean(x^2) + eps) * gamma; rstd [rows] fp32 saved (oracle rms_norm). */
 int pc_rmsnorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const float* gamma,

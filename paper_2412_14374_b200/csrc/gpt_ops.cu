@@ -526,9 +526,28 @@ extern "C" int pc_layernorm_bwd_acc(int dtype, int64_t rows, int64_t d, const vo
     } else {
       ln_bwd_dx_kernel<T><<<row_blocks(rows), 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, mean, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
     }
-    if (!colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), mean, rstd, dgamma, dbeta, accumulate, ws, ws_bytes, st))
-      ln_bwd_param_kernel<T><<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), mean, rstd, dgamma, dbeta));
+    if (dgamma == nullptr && dbeta == nullptr) {
+      // dx only: the parameter gradients are reduced elsewhere (pc_layernorm_param_grads)
+    } else if (!colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), mean, rstd, dgamma, dbeta, accumulate, ws, ws_bytes, st)) {
+      ln_bwd_param_kernel<T><<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), mean, rstd, dgamma, dbeta);
+    });
   return check_launch("layernorm_bwd");
+}
+
+extern "C" int pc_layernorm_param_grads(int dtype, int64_t rows, int64_t d, const void* dy,
+                                        const void* x, const float* mean, const float* rstd,
+                                        float* dgamma, float* dbeta, int accumulate, void* ws,
+                                        int64_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= 0) return PC_OK;
+  PP_CHECK_ARG(dgamma != nullptr && ws_bytes >= colred_ws_bytes(rows, d),
+               "layernorm_param_grads: needs dgamma and the reduction workspace");
+  bool ok = false;
+  PP_DISPATCH_FB(dtype, T,
+    ok = colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x),
+                          mean, rstd, dgamma, dbeta, accumulate, ws, ws_bytes, st));
+  PP_CHECK_ARG(ok, "layernorm_param_grads: reduction not launchable");
+  return check_launch("layernorm_param_grads");
 }
 
 extern "C" int pc_embedding_fwd(int dtype, int64_t T_, int64_t d, int64_t seq,

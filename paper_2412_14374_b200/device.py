@@ -82,6 +82,7 @@ class Act:
 
 
 _ABLATE_BIAS = os.environ.get("PP200_ABLATE_BIAS_GRAD") == "1"
+_LN_PARAMS_MAIN = os.environ.get("PP200_LN_PARAMS_MAIN") == "1"   # A/B switch for profiling
 
 
 class PeerBuf:
@@ -673,12 +674,29 @@ class DeviceOps:
         fused = acc is not None
         dW = acc if fused else self.zeros((layout_size(lay),), f32)
         gs = lambda name: self._slice(dW, lay, name)
+        # the side stream's reduction workspace, sized once for the widest sum
+        # (never reallocated while side work may still read it)
+        self.red_ws(T, max(f, 3 * d), side=True)
+
+        def ln_bwd(dy, x, gname, bname, mean, rstd, dres, dx):
+            """LayerNorm backward: dx on the compute stream; gamma / beta
+            gradients (a reduction nothing downstream waits for) beside it on
+            the side stream."""
+            on_side = not _LN_PARAMS_MAIN
+            if on_side:
+                self._fork()
+            call("pc_layernorm_param_grads", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
+                 mean.data_ptr(), rstd.data_ptr(), gs(gname).data_ptr(), gs(bname).data_ptr(),
+                 int(fused), *self.red_ws(T, d, side=on_side),
+                 self._side().cuda_stream if on_side else self.st)
+            call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
+                 ms(gname).data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                 None if dres is None else dres.data_ptr(), dx.data_ptr(), None, None, 0,
+                 *self.red_ws(T, d), self.st)
+
         if final:
             dout = self.empty((T, d), act)
-            call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, dz.data_ptr(), sv["out"].data_ptr(),
-                 ms("lnf_g").data_ptr(), sv["meanf"].data_ptr(), sv["rstdf"].data_ptr(), None,
-                 dout.data_ptr(), gs("lnf_g").data_ptr(), gs("lnf_b").data_ptr(), int(fused),
-                 *self.red_ws(T, d), self.st)
+            ln_bwd(dz, sv["out"], "lnf_g", "lnf_b", sv["meanf"], sv["rstdf"], None, dout)
         else:
             dout = dz
         # Weight gradients and their bias sums run on the side stream (they do
@@ -704,10 +722,7 @@ class DeviceOps:
         tb, B, ldb = wB("w_fc1")
         self._gemm(act, 0, tb, T, d, f, du, f, B, ldb, da2, d)
         dh1 = self.empty((T, d), act)
-        call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, da2.data_ptr(), sv["h1"].data_ptr(),
-             ms("ln2_g").data_ptr(), sv["mean2"].data_ptr(), sv["rstd2"].data_ptr(),
-             dout.data_ptr(), dh1.data_ptr(), gs("ln2_g").data_ptr(), gs("ln2_b").data_ptr(),
-             int(fused), *self.red_ws(T, d), self.st)
+        ln_bwd(da2, sv["h1"], "ln2_g", "ln2_b", sv["mean2"], sv["rstd2"], dout, dh1)
         # attention
         wgrad(d, d, dh1, d, sv["o"], d, "w_o", "b_o")
         do = self.empty((T, d), act)
@@ -723,10 +738,7 @@ class DeviceOps:
         tb, B, ldb = wB("w_qkv")
         self._gemm(act, 0, tb, T, d, 3 * d, dqkv, 3 * d, B, ldb, da, d)
         dh = self._placed_elem(op, 0, (T, d), act)   # into the previous stage's slot when sent
-        call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, da.data_ptr(), h.data_ptr(),
-             ms("ln1_g").data_ptr(), sv["mean1"].data_ptr(), sv["rstd1"].data_ptr(),
-             dh1.data_ptr(), dh.data_ptr(), gs("ln1_g").data_ptr(), gs("ln1_b").data_ptr(),
-             int(fused), *self.red_ws(T, d), self.st)
+        ln_bwd(da, h, "ln1_g", "ln1_b", sv["mean1"], sv["rstd1"], dh1, dh)
         self._join()
         return (dh, dW)
 
