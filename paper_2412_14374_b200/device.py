@@ -777,9 +777,20 @@ class DeviceOps:
         else:
             wte = self._slice(w0.compute(), self._elay, "wte")
             self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V, wte, d, dh, d)
-        dw = self.zeros((layout_size(self._elay),), torch.float32)
-        self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
-                   self._slice(dw, self._elay, "wte"), d, _lib.EPI_SPLITK_ZERO_C)
+        # wte gradient from the GEMM; wpe's part of the tied partial is zero.
+        # Zero-fill only what the GEMM does not overwrite: all of wte when it
+        # splits K (two halves reduce-added onto zeros), else just wpe.
+        dw = self.empty((layout_size(self._elay),), torch.float32)
+        bn, cg, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        call("pc_gemm_tile_choice", 0, V, d, T, 1, ctypes.byref(bn), ctypes.byref(cg),
+             ctypes.byref(ks))
+        wte = self._slice(dw, self._elay, "wte")
+        if ks.value > 1:
+            call("pc_fill", _lib.PC_F32, dw.numel(), 0.0, dw.data_ptr(), self.st)
+        else:  # everything after wte: wpe and the alignment padding
+            tail = dw[self._elay["wte"][0] + wte.numel():]
+            call("pc_fill", _lib.PC_F32, tail.numel(), 0.0, tail.data_ptr(), self.st)
+        self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d, wte, d, _lib.EPI_SPLITK_ZERO_C)
         return (dh, dw)
 
 
