@@ -174,6 +174,11 @@ int pc_embedding_bwd_workspace_bytes(int64_t T, int64_t* bytes);
 int pc_embedding_bwd(int dtype, int64_t T, int64_t d, int64_t seq, int64_t vocab,
                      const int32_t* tokens, const void* dh, float* dwte, float* dwpe,
                      void* workspace, int64_t ws_bytes, void* stream);
+/* As pc_embedding_bwd; accumulate = 1 adds the token-row and position sums onto dwte /
+ * dwpe (the running gradient) instead of overwriting (no zero-fill of dwte). */
+int pc_embedding_bwd_acc(int dtype, int64_t T_, int64_t d, int64_t seq, int64_t vocab,
+                         const int32_t* tokens, const void* dh, float* dwte, float* dwpe,
+                         int accumulate, void* workspace, int64_t ws_bytes, void* stream);
 /* Next-token cross-entropy per row (targets = tokens shifted by one inside each
  * sequence); overwrites logits with dlogits = softmax - onehot. */
 int pc_xent_fwd_bwd(int dtype, int64_t rows, int64_t V, int64_t seq, void* logits, int64_t ld,

@@ -81,6 +81,8 @@ SIGNATURES: dict[str, list] = {
     "pc_embedding_bwd_workspace_bytes": [_c_i64, ctypes.POINTER(_c_i64)],
     "pc_embedding_bwd": [_c_i, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                          _c_i64, _c_p],
+    "pc_embedding_bwd_acc": [_c_i, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_i,
+                             _c_p, _c_i64, _c_p],
     "pc_xent_fwd_bwd": [_c_i, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p],
     "pc_attention_fwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p],
     "pc_attention_bwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p,

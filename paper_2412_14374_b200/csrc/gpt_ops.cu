@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(256) embed_bwd_wte_kernel(int n, int d,
                                                             const int32_t* __restrict__ keys,
                                                             const int32_t* __restrict__ rows,
                                                             const T* __restrict__ dh,
-                                                            float* __restrict__ dwte) {
+                                                            float* __restrict__ dwte,
+                                                            int accumulate) {
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * ROWS_PER_BLOCK + (threadIdx.x >> 5);
   if (i >= n) return;
@@ -289,20 +290,20 @@ __global__ void __launch_bounds__(256) embed_bwd_wte_kernel(int n, int d,
   for (int c = lane; c < d; c += 32) {
     float s = 0.f;
     for (int k = i; k < j; ++k) s += ldf(dh, static_cast<int64_t>(rows[k]) * d + c);
-    out[c] = s;
+    out[c] = accumulate ? out[c] + s : s;
   }
 }
 
 // dwpe[s,c] = sum_b dh[b*seq + s, c]
 template <typename T>
 __global__ void embed_bwd_wpe_kernel(int64_t T_, int d, int seq, const T* __restrict__ dh,
-                                     float* __restrict__ dwpe) {
+                                     float* __restrict__ dwpe, int accumulate) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= static_cast<int64_t>(seq) * d) return;
   const int64_t s = i / d, c = i % d;
   float acc = 0.f;
   for (int64_t t = s; t < T_; t += seq) acc += ldf(dh, t * d + c);
-  dwpe[i] = acc;
+  dwpe[i] = accumulate ? dwpe[i] + acc : acc;
 }
 
 // Per row: online (max, sum) over the vocab, loss = lse - logit[target], then
@@ -575,6 +576,14 @@ extern "C" int pc_embedding_bwd_workspace_bytes(int64_t T_, int64_t* bytes) {
 extern "C" int pc_embedding_bwd(int dtype, int64_t T_, int64_t d, int64_t seq, int64_t vocab,
                                 const int32_t* tokens, const void* dh, float* dwte, float* dwpe,
                                 void* workspace, int64_t ws_bytes, void* stream) {
+  return pc_embedding_bwd_acc(dtype, T_, d, seq, vocab, tokens, dh, dwte, dwpe, 0, workspace,
+                              ws_bytes, stream);
+}
+
+extern "C" int pc_embedding_bwd_acc(int dtype, int64_t T_, int64_t d, int64_t seq,
+                                    int64_t vocab, const int32_t* tokens, const void* dh,
+                                    float* dwte, float* dwpe, int accumulate, void* workspace,
+                                    int64_t ws_bytes, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t need = 0;
   int rc = pc_embedding_bwd_workspace_bytes(T_, &need);
@@ -596,10 +605,10 @@ extern "C" int pc_embedding_bwd(int dtype, int64_t T_, int64_t d, int64_t seq, i
     set_error("embedding_bwd: radix sort failed");
     return PC_ERR_CUDA;
   }
-  PP_CUDA_TRY(cudaMemsetAsync(dwte, 0, static_cast<size_t>(vocab) * d * 4, st));
+  if (!accumulate) PP_CUDA_TRY(cudaMemsetAsync(dwte, 0, static_cast<size_t>(vocab) * d * 4, st));
   PP_DISPATCH_FB(dtype, T,
-    embed_bwd_wte_kernel<T><<<row_blocks(T_), 256, 0, st>>>(n, (int)d, keys_out, vals_out, static_cast<const T*>(dh), dwte);
-    embed_bwd_wpe_kernel<T><<<(unsigned)((seq * d + 255) / 256), 256, 0, st>>>(T_, (int)d, (int)seq, static_cast<const T*>(dh), dwpe));
+    embed_bwd_wte_kernel<T><<<row_blocks(T_), 256, 0, st>>>(n, (int)d, keys_out, vals_out, static_cast<const T*>(dh), dwte, accumulate);
+    embed_bwd_wpe_kernel<T><<<(unsigned)((seq * d + 255) / 256), 256, 0, st>>>(T_, (int)d, (int)seq, static_cast<const T*>(dh), dwpe, accumulate));
   return check_launch("embedding_bwd");
 }
 

@@ -326,6 +326,8 @@ class DeviceOps:
             call("pc_ewise", _lib.EW_RELU_GRAD, _PC[x.dtype], x.numel(), x.data_ptr(),
                  z.data_ptr(), z.numel(), out.data_ptr(), self.st)
             env[op.result] = out
+        elif kind == "add" and self._fused_add(op, env):
+            pass
         elif kind in ("add", "scale", "mul"):
             x, y = tensor_of(a), tensor_of(env[op.operands[1]])
             out = self.empty(x.shape, x.dtype)
@@ -359,9 +361,9 @@ class DeviceOps:
         elif kind == "lmhead-xent":
             env[op.result] = self._head_fwd(op, env)
         elif kind == "lmhead-xent-grad":
-            env[op.result] = self._head_bwd(op, env)
+            env[op.result] = self._head_bwd(op, env, acc=self._acc_for_tuple(op, 1))
         elif kind == "embed-grad":
-            env[op.result] = self._embed_bwd(op, env)
+            env[op.result] = self._embed_bwd(op, env, acc=self._acc_for_value(op.result))
         elif kind == "llama-embed":
             env[op.result] = Act(self._llama_embed(op, env))
         elif kind == "llama-embed-grad":
@@ -543,21 +545,24 @@ class DeviceOps:
              wte.data_ptr(), wpe.data_ptr(), out.data_ptr(), self.st)
         return out
 
-    def _embed_bwd(self, op, env):
+    def _embed_bwd(self, op, env, acc=None):
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
         n = layout_size(self._elay)
-        dw = self.zeros((n,), torch.float32)
+        dw = acc if acc is not None else self.zeros((n,), torch.float32)
         T, d = cfg.tokens, cfg.d_model
         if self._emb_ws is None:
             nb = ctypes.c_int64(0)
             call("pc_embedding_bwd_workspace_bytes", T, ctypes.byref(nb))
             self._emb_ws = self.empty((nb.value,), torch.uint8)
         ws = self._emb_ws
-        call("pc_embedding_bwd", self.mode.pc_act, T, d, cfg.seq_len, cfg.vocab, x.data_ptr(),
-             g.data_ptr(), self._slice(dw, self._elay, "wte").data_ptr(),
-             self._slice(dw, self._elay, "wpe").data_ptr(), ws.data_ptr(), ws.numel(), self.st)
+        # accumulate: onto the running sum when fused, else onto the zeros above
+        # (one zero-fill instead of two)
+        call("pc_embedding_bwd_acc", self.mode.pc_act, T, d, cfg.seq_len, cfg.vocab,
+             x.data_ptr(), g.data_ptr(), self._slice(dw, self._elay, "wte").data_ptr(),
+             self._slice(dw, self._elay, "wpe").data_ptr(), 1, ws.data_ptr(), ws.numel(),
+             self.st)
         ws.record_stream(self.stream)
         return dw
 
@@ -619,6 +624,45 @@ class DeviceOps:
             out = z
         hv.saved[op.id] = saved
         env[op.result] = Act(out)
+
+    def _acc_for_value(self, v: str):
+        """Running sum a parameter partial ``v`` may be added onto: v is a task
+        output in acc_into, or v's only reader is the in-stage ``add`` that
+        merges the tied embedding's partials into such an output (then both
+        partials go onto the sum and the add is a rename, see _fused_add)."""
+        if not self.acc_into:
+            return None
+        if v in self.acc_into:
+            return self.acc_into[v]
+        users = self._consumers.get(v, ())
+        if len(users) == 1 and users[0].kind == "add" and users[0].result in self.acc_into:
+            return self.acc_into[users[0].result]
+        return None
+
+    def _acc_for_tuple(self, op, index: int):
+        if not self.acc_into:
+            return None
+        for u in self._consumers.get(op.result, ()):
+            if u.kind == "tuple-get" and u.attr("index") == index:
+                return self._acc_for_value(u.result)
+        return None
+
+    def _fused_add(self, op, env) -> bool:
+        """The in-stage add of partials already added onto the running sum
+        (or one of them): finish in place and alias the result."""
+        acc = self.acc_into.get(op.result) if self.acc_into else None
+        if acc is None:
+            return False
+        x, y = env[op.operands[0]], env[op.operands[1]]
+        xs, ys = x is acc, y is acc
+        if not (xs or ys):
+            return False
+        if not (xs and ys):
+            other = tensor_of(y if xs else x)
+            call("pc_accumulate", _PC[acc.dtype], _PC[other.dtype], acc.numel(), acc.data_ptr(),
+                 other.data_ptr(), self.st)
+        env[op.result] = acc
+        return True
 
     def _acc_target(self, op, index: int):
         """The accumulator the ``index``-th tuple element of ``op`` may add
@@ -762,7 +806,7 @@ class DeviceOps:
         hv.saved[op.id] = dict(dlogits=logits)
         return loss
 
-    def _head_bwd(self, op, env):
+    def _head_bwd(self, op, env, acc=None):
         cfg = self.gpt
         hv = env[op.operands[0]]
         h = tensor_of(hv)
@@ -777,6 +821,13 @@ class DeviceOps:
         else:
             wte = self._slice(w0.compute(), self._elay, "wte")
             self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V, wte, d, dh, d)
+        if acc is not None:
+            # onto the running sum: the wte rows through the GEMM's TMA
+            # reduce-add store (unsplit: one fp32 add per element); the head's
+            # wpe part is zero, nothing to add
+            self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
+                       self._slice(acc, self._elay, "wte"), d, _lib.EPI_ACCUM)
+            return (dh, acc)
         # wte gradient from the GEMM; wpe's part of the tied partial is zero.
         # Zero-fill only what the GEMM does not overwrite: all of wte when it
         # splits K (two halves reduce-added onto zeros), else just wpe.
