@@ -66,6 +66,10 @@ def block_costs(cfg):
     return [emb] + [blk] * cfg.layers + [head]
 
 
+METRIC = "tokens/s (model TFLOPS/GPU and bubble alongside)"
+WORKLOAD = "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024"
+
+
 def build_plan(P, cfg_kw, M, mode="bf16"):
     from paper_2412_14374_b200 import comms as C
     from paper_2412_14374_b200 import ir as I
@@ -313,9 +317,11 @@ def cpu_baseline(cfg_kw, seconds_hint=True):
     rng = np.random.default_rng(0)
     params = og.init_params(oc, rng)
     tokens = og.init_tokens(oc, 1, rng)
-    t0 = time.perf_counter()
-    og.run_reference_gpt(params, tokens, oc)
-    dt = time.perf_counter() - t0
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=os.cpu_count()):
+        t0 = time.perf_counter()
+        og.run_reference_gpt(params, tokens, oc)
+        dt = time.perf_counter() - t0
     ntok = oc["seq"]
     return {"value": round(ntok / dt, 2), "unit": "tokens/s", "cores": os.cpu_count(),
             "kind": "port",
@@ -334,23 +340,26 @@ def run_reference_impl(args, rank, world):
     rng = np.random.default_rng(0)
     params = og.init_params(oc, rng)
     tokens = og.init_tokens(oc, 1, rng)
-    for _ in range(args.warmup):
-        og.gpt_step(params, tokens[0], oc)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        og.run_reference_gpt(params, tokens, oc)
-        times.append(time.perf_counter() - t0)
+    # all host threads (torchrun sets OMP_NUM_THREADS=1 for its workers)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=os.cpu_count()):
+        for _ in range(args.warmup):
+            og.gpt_step(params, tokens[0], oc)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            og.run_reference_gpt(params, tokens, oc)
+            times.append(time.perf_counter() - t0)
     ms = 1000 * float(np.mean(times))
     tok_s = oc["seq"] / (ms / 1000)
     from paper_2412_14374_b200.ir import GPTConfig
     cfg = GPTConfig(**C2)
     line = {
-        "impl": "reference", "metric": "tokens/s (model TFLOPS/GPU alongside)",
+        "impl": "reference", "metric": METRIC,
         "value": round(tok_s, 2), "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024, 1F1B",
+        "config": {"workload": WORKLOAD, "schedule": "1f1b",
                    "sample": "1 sequence x 1024 tokens per step (bounded CPU sample)"},
         "model_tflops_per_gpu": round(cfg.flops_per_token() * tok_s / 1e12, 5),
         "cpu_baseline": {"value": round(tok_s, 2), "unit": "tokens/s", "cores": os.cpu_count(),
@@ -508,12 +517,12 @@ def main():
         roof["peak_kind"] = peak_kind
         cpu = None if args.no_cpu_baseline else cpu_baseline(C2)
         line = {
-            "metric": "tokens/s (model TFLOPS/GPU and bubble alongside)",
+            "metric": METRIC,
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic tokens, random-init weights",
-            "config": {"workload": "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024",
+            "config": {"workload": WORKLOAD,
                        "global_batch": M * cfg.microbatch_size, "seq_len": cfg.seq_len,
                        "microbatches": M, "microbatch_size": cfg.microbatch_size,
                        "schedule": "1f1b", "stages": P, "yields": list(cfg.yields or []),
