@@ -36,6 +36,11 @@ sys.path.insert(0, ROOT)
 C2 = dict(layers=12, d_model=768, n_heads=12, d_ff=3072, vocab=50304, seq_len=1024,
           microbatch_size=8)
 M_MICRO = 8
+# BASELINE configs[2] (C3, GPT-2 medium; quoted there on 8 stages x 16 microbatches):
+# `--workload C3` runs it on the GPUs given (the default bench line stays C2)
+C3 = dict(C2, layers=24, d_model=1024, n_heads=16, d_ff=4096)
+WORKLOADS = {"C2": (C2, 8, "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024"),
+             "C3": (C3, 16, "C3 gpt2-medium 24L d1024 h16 ff4096 V50304 seq1024")}
 
 
 def peaks():
@@ -236,7 +241,7 @@ def gemm_args(shape, st):
     return args, (A, B, C, bias, aux, U)
 
 
-def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
+def gemm_roofline(cfg, P, stage_blocks, step_ms, peak, M=M_MICRO):
     """Average achieved TFLOP/s of the tcgen05 GEMM over the shape mix of one
     stage step, each GEMM issued exactly as device.py issues it (operand
     majors, fused epilogue, split-K hint) and timed with CUDA events on its
@@ -279,8 +284,8 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak):
         if key in traffic:
             row["dram_bytes"] = traffic[key]
         per.append(row)
-        tot_flops += fl * count * M_MICRO
-        tot_ms += ms * count * M_MICRO
+        tot_flops += fl * count * M
+        tot_ms += ms * count * M
         del keep
     achieved = tot_flops / tot_ms / 1e9 if tot_ms else 0.0
     # DRAM bytes per launch over the same mix, from the committed ncu --set full capture
@@ -378,7 +383,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--microbatches", type=int, default=M_MICRO)
+    ap.add_argument("--microbatches", type=int, default=None,
+                    help="default: the workload's (C2: 8, C3: 16)")
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gantt", default=None, help="write the measured timeline as an SVG Gantt chart")
     ap.add_argument("--no-graph", action="store_true",
@@ -399,8 +406,9 @@ def main():
     from paper_2412_14374_b200.executor import PipelineEngine
 
     P = world
-    M = args.microbatches
-    cfg, tg, cp = build_plan(P, C2, M)
+    wl_kw, wl_m, wl_name = WORKLOADS[args.workload]
+    M = args.microbatches or wl_m
+    cfg, tg, cp = build_plan(P, wl_kw, M)
     dev = torch.device("cuda", local)
     params = init_params_device(cfg, dev)
     rng = np.random.default_rng(1234)
@@ -501,7 +509,7 @@ def main():
     achievable = TL.replay(cp, TL.task_durations(timeline)).bubble_fraction(P)
     if args.gantt and rank == 0:
         with open(args.gantt, "w") as f:
-            f.write(TL.render_svg(timeline, P, title=f"C2 1F1B P={P} M={M} measured,"))
+            f.write(TL.render_svg(timeline, P, title=f"{args.workload} 1F1B P={P} M={M} measured,"))
 
     tokens_per_step = M * cfg.tokens
     value = tokens_per_step / (ms / 1000)
@@ -513,16 +521,16 @@ def main():
 
     if rank == 0:
         stage_blocks = sum(1 for op in tg.partition.fwd_programs[0].ops if op.kind == "gpt-block")
-        roof = gemm_roofline(cfg, P, stage_blocks, ms, burst)
+        roof = gemm_roofline(cfg, P, stage_blocks, ms, burst, M)
         roof["peak_kind"] = peak_kind
-        cpu = None if args.no_cpu_baseline else cpu_baseline(C2)
+        cpu = None if args.no_cpu_baseline else cpu_baseline(wl_kw)
         line = {
             "metric": METRIC,
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic tokens, random-init weights",
-            "config": {"workload": WORKLOAD,
+            "config": {"workload": wl_name,
                        "global_batch": M * cfg.microbatch_size, "seq_len": cfg.seq_len,
                        "microbatches": M, "microbatch_size": cfg.microbatch_size,
                        "schedule": "1f1b", "stages": P, "yields": list(cfg.yields or []),
