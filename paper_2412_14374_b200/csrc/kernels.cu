@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(1024) col_sum_kernel(int64_t rows, int64_t col
 // MODE 0: s1 = sum x.   MODE 1 (LayerNorm params): s1 = sum dy*xhat, s2 = sum dy
 // with xhat = (x - mean[r]) * rstd[r].
 constexpr int CR_COLS = 256;
+constexpr int CR_RAW_ROWS = 16;  // rows per warp loaded at once on the short-chunk path
 
 template <typename T>
 __device__ __forceinline__ void load8(const T* p, int64_t c, int64_t cols, bool vec, float* v) {
@@ -169,7 +170,7 @@ __device__ __forceinline__ void load8(const T* p, int64_t c, int64_t cols, bool 
   }
 }
 
-template <typename T, int MODE>
+template <typename T, int MODE, bool SHORT = false>
 __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols, int64_t chunk,
                                                      const T* __restrict__ a, int64_t lda,
                                                      const T* __restrict__ x,
@@ -189,7 +190,28 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
                    (MODE == 0 || (reinterpret_cast<uintptr_t>(x) & 15) == 0);
   float s1[8] = {}, s2[8] = {};
   int64_t r = r0 + w;
-  if (MODE == 0) {
+  if (SHORT && MODE == 0 && sizeof(T) == 2 && vec && c0 + 8 <= cols && r1 - r0 <= 8 * CR_RAW_ROWS) {
+    // Short chunks (narrow cols give many row chunks): every row of this
+    // warp's share is loaded before any is summed, so the warp waits on one
+    // DRAM round trip instead of one per unrolled group plus its tail.
+    uint4 u[CR_RAW_ROWS];
+#pragma unroll
+    for (int i = 0; i < CR_RAW_ROWS; ++i) {
+      const int64_t rr = r + 8 * i;
+      u[i] = rr < r1 ? *reinterpret_cast<const uint4*>(a + rr * lda + c0) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < CR_RAW_ROWS; ++i) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        s1[2 * j] += f.x;
+        s1[2 * j + 1] += f.y;
+      }
+    }
+    r = r1;
+  } else if (MODE == 0) {
     // 4 independent rows in flight per iteration (latency-bound otherwise)
     for (; r + 24 < r1; r += 32) {
       float v0[8], v1[8], v2[8], v3[8];
@@ -266,10 +288,11 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
     float f1[8] = {}, f2[8] = {};
     const bool v4 = (cols % 4) == 0 && c0 + 8 <= cols;
     const int R = static_cast<int>(gridDim.y);
-    for (int k0 = w; k0 < R; k0 += 32) {
-      float4 a4[4][2], b4[4][2];
+    constexpr int FB = SHORT ? 8 : 4;  // partial rows in flight per warp
+    for (int k0 = w; k0 < R; k0 += 8 * FB) {
+      float4 a4[FB][2], b4[FB][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < FB; ++i) {
         const int k = k0 + 8 * i;
         if (k < R && v4) {
           a4[i][0] = __ldcg(reinterpret_cast<const float4*>(ws1 + k * cols + c0));
@@ -281,7 +304,7 @@ __global__ void __launch_bounds__(256) colred_stage1(int64_t rows, int64_t cols,
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < FB; ++i) {
         const int k = k0 + 8 * i;
         if (k >= R) break;
         if (v4) {
@@ -428,7 +451,13 @@ bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda
   float* w1 = reinterpret_cast<float*>(ctr + COLRED_COUNTERS);
   float* w2 = w1 + R * cols;
   dim3 grid(static_cast<unsigned>((cols + CR_COLS - 1) / CR_COLS), static_cast<unsigned>(R));
-  if (mode == 0)
+  // short row chunks (narrow cols): the variant that loads all of a warp's
+  // rows at once and folds 8 partial rows per warp in flight
+  const bool short_chunks = sizeof(T) == 2 && chunk <= 8 * CR_RAW_ROWS;
+  if (mode == 0 && short_chunks)
+    colred_stage1<T, 0, true><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1,
+                                                     w2, ctr, out1, out2, accumulate);
+  else if (mode == 0)
     colred_stage1<T, 0><<<grid, 256, 0, st>>>(rows, cols, chunk, a, lda, x, mean, rstd, w1, w2,
                                                ctr, out1, out2, accumulate);
   else

@@ -6,6 +6,8 @@ same planner and runtime as the FFN tests: GPipe / 1F1B / interleaved on one
 GPU with local channels, including the non-adjacent token skip to the last
 stage and the commuted tied-weight gradient.
 """
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -308,6 +310,36 @@ def test_layernorm_vectorised_paths(d, dt, tol):
     assert ffn.rel(tdg.cpu().numpy(), dg) < tol
     assert ffn.rel(tdb.cpu().numpy(), db) < tol
     assert ffn.rel(cs.cpu().numpy(), dyq.sum(0)) < 1e-5
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 768), (8192, 2304), (1000, 768), (37, 768),
+                                       (8191, 1024), (8192, 770), (1, 256)])
+def test_col_sum_bf16_shapes_and_determinism(rows, cols):
+    """Bias-gradient column sums (the `sum-to` of executor.py:50-56) at the C2
+    shapes and ragged ones: short row chunks (all of a warp's rows loaded at
+    once), long chunks, column tails; equal to the float64 sum within fp32
+    rounding, bitwise identical run to run, and accumulate = out + sum."""
+    g = torch.Generator(device="cuda").manual_seed(rows * 7 + cols)
+    a = torch.randn(rows, cols, device="cuda", generator=g).to(torch.bfloat16)
+    nb = ctypes.c_int64()
+    _lib.call("pc_reduce_workspace_bytes", rows, cols, ctypes.byref(nb))
+    ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for _ in range(2):
+        o = torch.empty(cols, device="cuda")
+        _lib.call("pc_col_sum", _lib.PC_BF16, _lib.PC_F32, rows, cols, a.data_ptr(), cols,
+                  o.data_ptr(), 0, ws.data_ptr(), nb.value, st)
+        outs.append(o)
+    acc = torch.full((cols,), 0.5, device="cuda")
+    _lib.call("pc_col_sum", _lib.PC_BF16, _lib.PC_F32, rows, cols, a.data_ptr(), cols,
+              acc.data_ptr(), 1, ws.data_ptr(), nb.value, st)
+    torch.cuda.synchronize()
+    ref = a.double().sum(0)
+    err = ((outs[0].double() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-5, err
+    assert torch.equal(outs[0], outs[1])
+    assert torch.allclose(acc, outs[0] + 0.5, rtol=1e-6, atol=1e-5)
 
 
 def test_fused_grad_accumulation_matches_the_add_chain():
