@@ -53,7 +53,7 @@ from .comms import (
     _brief,
 )
 from .device import _PC as _PC_OF
-from .device import MODES, Act, DeviceOps, Mode, Param, PeerBuf, strip, tensor_of, \
+from .device import MODES, Act, DeviceOps, Mode, Param, PeerBuf, Trans, strip, tensor_of, \
     to_device_input, to_device_param
 from .ir import GPTConfig
 from .taskgraph import GRAD_TOTAL, OPT_STATE, PARAM, STASH, TaskGraph
@@ -82,6 +82,7 @@ class RunStats:
     sent_buffers: list = field(default_factory=list)       # (src, dst, buffer id)
     peak_live: dict = field(default_factory=dict)          # actor -> int
     peak_stash: dict = field(default_factory=dict)         # (actor, stage) -> int
+    peak_stash_bytes: dict = field(default_factory=dict)   # actor -> device bytes held in stashes
     final_live: dict = field(default_factory=dict)         # actor -> sorted buffer ids
     timeline: list = field(default_factory=list)           # (actor, kind, uid, start_ms, end_ms)
 
@@ -479,6 +480,47 @@ class DeviceStore:
         for st, n in by_stage.items():
             key = (a, st)
             self.stats.peak_stash[key] = max(self.stats.peak_stash.get(key, 0), n)
+        nbytes = sum(_stash_bytes(self.data[bid]) for bid in self.data if bid in self._stash_stage)
+        self.stats.peak_stash_bytes[a] = max(self.stats.peak_stash_bytes.get(a, 0), nbytes)
+
+
+REMAT_NONE, REMAT_FULL = "none", "full-per-stage"   # simulator.py:48, :132-149
+
+
+def _stash_bytes(stash) -> int:
+    """Device bytes a stash holds (under remat: the retained forward inputs
+    only; the parameter references it carries are not stash memory)."""
+    if isinstance(stash, dict) and "__remat__" in stash:
+        stash = stash["__remat__"][0]
+    seen: dict[int, int] = {}
+
+    def walk(v):
+        if isinstance(v, torch.Tensor):
+            seen[v.data_ptr()] = max(seen.get(v.data_ptr(), 0), v.numel() * v.element_size())
+        elif isinstance(v, Act):
+            walk(v.t)
+            walk(v.saved)
+        elif isinstance(v, Trans):
+            walk(v.base)
+        elif isinstance(v, dict):
+            for x in v.values():
+                walk(x)
+        elif isinstance(v, (tuple, list)):
+            for x in v:
+                walk(x)
+
+    walk(stash)
+    return sum(seen.values())
+
+
+def _retained(v):
+    """A private copy of a forward feed kept for the replay: channel slots and
+    activation buffers are reused once the stage's forward is done."""
+    if isinstance(v, torch.Tensor):
+        return v.clone()
+    if isinstance(v, Act):
+        return Act(v.t.clone())
+    return v
 
 
 # ---------------------------------------------------------------------------
@@ -497,6 +539,7 @@ class _Actor:
         self.store = DeviceStore(actor, tg, stats)
         self.timeline = timeline
         self.events: list = []       # (kind, uid, start slot, end slot)
+        self.remat = REMAT_NONE      # PipelineEngine(remat=...) sets it
         self.ts = None               # int64 device buffer of %globaltimer stamps
         if timeline:
             n = 2 * sum(1 for t in tg.tasks.values() if t.actor == actor) + 1
@@ -545,6 +588,16 @@ class _Actor:
         if kind == "stage-fwd":
             prog = p.fwd_programs[ex["stage"]]
             env = {v: st.get(bid, at) for v, bid in ex["feeds"].items()}
+            kept = None
+            if ex["stash_out"] and self.remat == REMAT_FULL:
+                # full per-stage rematerialisation: keep the forward's feeds only
+                # (boundary activations and batch inputs copied before the
+                # forward runs, since their channel slots are reused; parameters
+                # by reference) and replay the forward inside the backward task
+                # (simulator.py:144-149)
+                params = set(prog.params_used)
+                kept = ({v: _retained(t) for v, t in env.items() if v not in params},
+                        {v: t for v, t in env.items() if v in params})
             self.ops.place = self._placement(ex)
             try:
                 self.ops.run_ops(prog.ops, env)
@@ -552,13 +605,21 @@ class _Actor:
                 self.ops.place = {}
             for v, bid in ex["outs"].items():
                 st.put(bid, env[v])
-            if ex["stash_out"]:
+            if kept is not None:
+                st.put(ex["stash_out"], {"__remat__": kept})
+            elif ex["stash_out"]:
                 st.put(ex["stash_out"], {v: env[v] for v in prog.stash})
         elif kind == "stage-bwd":
             prog = p.bwd_programs[ex["stage"]]
             env = {v: st.get(bid, at) for v, bid in ex["feeds"].items()}
             if ex["stash_in"]:
-                env.update(st.get(ex["stash_in"], at))
+                stash = st.get(ex["stash_in"], at)
+                if "__remat__" in stash:
+                    kept, params = stash["__remat__"]
+                    fenv = {**kept, **params}
+                    self.ops.run_ops(p.fwd_programs[ex["stage"]].ops, fenv)
+                    stash = {v: fenv[v] for v in p.fwd_programs[ex["stage"]].stash}
+                env.update(stash)
             acc = self._fusable_accumulators(ex) if self.ops.fuse_acc else {}
             self.ops.acc_into = acc
             self.ops.place = self._placement(ex)
@@ -765,7 +826,7 @@ class PipelineEngine:
 
     def __init__(self, cp: CommPlan, tg: TaskGraph, mode: str | Mode = "fp64",
                  gpt: GPTConfig | None = None, devices=None, timeline: bool = False,
-                 transport: str | None = None):
+                 transport: str | None = None, remat: str = REMAT_NONE):
         if not cp.fused:
             raise ExecutorFault("plan must be fused before execution")
         if not torch.cuda.is_available():
@@ -774,6 +835,9 @@ class PipelineEngine:
         self.cp, self.tg = cp, tg
         self.mode = MODES[mode] if isinstance(mode, str) else mode
         self.gpt = gpt
+        if remat not in (REMAT_NONE, REMAT_FULL):
+            raise ExecutorFault(f"unknown remat policy {remat!r}")
+        self.remat = remat
         self.P = cp.num_actors
         self.timeline = timeline
         dw = _dist_world()
@@ -1025,6 +1089,8 @@ class PipelineEngine:
         actors = {a: _Actor(a, self.tg, self._ops[a], stats, tl, inplace=resident,
                             instrs=self.cp.programs[a].instrs, channels=self._channels)
                   for a in self.local}
+        for act in actors.values():
+            act.remat = self.remat
         for a, act in actors.items():
             # params / inputs are copied on the current stream; the actor stream waits
             with torch.cuda.device(act.device):
@@ -1090,6 +1156,7 @@ class PipelineEngine:
             ch.reset()
         act = _Actor(a, self.tg, self._ops[a], stats, timeline, inplace=resident,
                      instrs=self.cp.programs[a].instrs, channels=self._channels)
+        act.remat = self.remat
         actors = {a: act}
         with torch.cuda.device(act.device):
             act.stream.wait_stream(torch.cuda.current_stream(act.device))
@@ -1258,7 +1325,8 @@ def split_batch(batch, M: int):
 def run_pipelined(cp: CommPlan, tg: TaskGraph, params, batch, lr: float = 0.1,
                   timeout_s: float = 30.0, delay_fn=None, strict_store: bool = True,
                   mode: str | None = None, gpt: GPTConfig | None = None, devices=None,
-                  timeline: bool = False, to_host: bool = True) -> ExecutionResult:
+                  timeline: bool = False, to_host: bool = True,
+                  remat: str = REMAT_NONE) -> ExecutionResult:
     """Execute a fused plan on B200(s).  Drop-in for executor.py:387-483.
 
     ``mode`` defaults from the parameter dtype (float64 -> "fp64", float32 ->
@@ -1270,7 +1338,8 @@ def run_pipelined(cp: CommPlan, tg: TaskGraph, params, batch, lr: float = 0.1,
         else:
             any_p = next(iter(params.values()))
             mode = "fp32" if getattr(any_p, "dtype", None) in (np.float32, torch.float32) else "fp64"
-    eng = PipelineEngine(cp, tg, mode=mode, gpt=gpt, devices=devices, timeline=timeline)
+    eng = PipelineEngine(cp, tg, mode=mode, gpt=gpt, devices=devices, timeline=timeline,
+                         remat=remat)
     try:
         return eng.step(params, batch, lr=lr, timeout_s=timeout_s, delay_fn=delay_fn,
                         strict_store=strict_store, to_host=to_host)

@@ -369,3 +369,32 @@ def test_fused_grad_accumulation_matches_the_add_chain():
     for q in a.grads:
         assert ffn.rel(a.grads[q], b.grads[q]) < 1e-6, (q, ffn.rel(a.grads[q], b.grads[q]))
         assert np.array_equal(a.grads[q], c.grads[q]), q
+
+
+@pytest.mark.parametrize("mode,fam,P,M,yields", [("bf16", "1f1b", 2, 4, (3,)),
+                                                 ("fp32", "gpipe", 2, 4, (3,)),
+                                                 ("bf16", "1f1b", 4, 8, (2, 3, 5))])
+def test_full_remat_replays_the_forward_bitwise(mode, fam, P, M, yields):
+    """remat="full-per-stage" (the reference simulator's policy,
+    simulator.py:132-149, made real): each stage keeps only its forward feeds
+    and replays the forward inside the backward task.  Deterministic kernels
+    make every gradient, loss and updated parameter bitwise equal to the
+    stashing run, with less stash memory per actor."""
+    from paper_2412_14374_b200.executor import ExecutorFault, PipelineEngine
+    cfg = I.GPTConfig(**TINY, yields=yields, yield_every=TINY["layers"] + 2,
+                      elem_bytes=2 if mode == "bf16" else 4)
+    _, tg, cp = plan(cfg, fam, P, M)
+    oc = oracle_cfg(cfg)
+    rng = np.random.default_rng(5)
+    params = {q: v.astype(np.float32) for q, v in gpt.init_params(oc, rng, std=0.05).items()}
+    tokens = gpt.init_tokens(oc, M, rng).reshape(M * cfg.microbatch_size, cfg.seq_len)
+    a = run_pipelined(cp, tg, params, tokens, mode=mode, gpt=cfg)
+    b = run_pipelined(cp, tg, params, tokens, mode=mode, gpt=cfg, remat="full-per-stage")
+    assert np.array_equal(a.losses, b.losses)
+    for q in a.grads:
+        assert np.array_equal(a.grads[q], b.grads[q]), q
+        assert np.array_equal(a.new_params[q], b.new_params[q]), q
+    for actor in range(P):
+        assert b.stats.peak_stash_bytes[actor] < a.stats.peak_stash_bytes[actor], actor
+    with pytest.raises(ExecutorFault):
+        PipelineEngine(cp, tg, mode=mode, gpt=cfg, remat="selective")
