@@ -388,6 +388,9 @@ def main():
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gantt", default=None, help="write the measured timeline as an SVG Gantt chart")
+    ap.add_argument("--remat", default="none", choices=["none", "full-per-stage"],
+                    help="full-per-stage: stages keep their forward feeds and replay the "
+                         "forward in the backward (model FLOPs unchanged in the metric)")
     ap.add_argument("--no-graph", action="store_true",
                     help="issue every step from Python instead of replaying the captured graph")
     args = ap.parse_args()
@@ -416,7 +419,7 @@ def main():
                                dtype=np.int32)
     tokens_dev = torch.from_numpy(tokens_host).to(dev)
     tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
-    eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
+    eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg, remat=args.remat)
     # resident training state: every step (eager or replayed) is a real SGD
     # step on the previous step's weights, tied w0 re-broadcast included
     eng.load_params(params)
@@ -537,9 +540,11 @@ def main():
                        "parallelism": f"pp{P}", "l2": "inputs > L2 (no flush needed)",
                        "issue": "cuda-graph replay per actor" if use_graph else "python per op",
                        "transport": eng.transport if world > 1 else None,
+                       "remat": args.remat,
                        "training": "resident params, in-place SGD each step"
                                    + (", tied w0 re-broadcast to the head stage" if P > 1 else "")},
             "model_tflops_per_gpu": round(tflops_gpu, 1),
+            "peak_hbm_gb_rank0": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
             "frac_of_bf16_peak": round(tflops_gpu / burst, 4),
             "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4),
                        "achievable": round(achievable, 4)},
