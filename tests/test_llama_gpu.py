@@ -24,7 +24,7 @@ def _costs(cfg):
         [cfg.head_fwd_flops()]
 
 
-def run(kw, P, M, mode, fam="1f1b", std=0.05, seed=0, rand_pos=False):
+def run(kw, P, M, mode, fam="1f1b", std=0.05, seed=0, rand_pos=False, remat="none"):
     base = I.LlamaConfig(**kw, yield_every=kw["layers"] + 2)
     yields = I.balanced_yields(_costs(base), P) if P > 1 else None
     cfg = I.LlamaConfig(**kw, yields=yields, yield_every=kw["layers"] + 2,
@@ -45,7 +45,7 @@ def run(kw, P, M, mode, fam="1f1b", std=0.05, seed=0, rand_pos=False):
     rows = M * cfg.microbatch_size
     res = run_pipelined(cp, tg, {q: v.astype(np.float32) for q, v in params.items()},
                         {"x": tokens.reshape(rows, cfg.seq_len), "pos": pos.reshape(rows, cfg.seq_len)},
-                        mode=mode, gpt=cfg)
+                        mode=mode, gpt=cfg, remat=remat)
     err = max([ffn.rel(res.losses, l)] + [ffn.rel(res.grads[q], g[q]) for q in g]
               + [ffn.rel(res.new_params[q], w[q]) for q in w])
     return err, cp, res
@@ -76,3 +76,15 @@ def test_c5_small_bf16_1f1b_skip_channels():
 def test_c5_small_bf16_mha_equivalent():
     err, _, _ = run(dict(C5S, n_kv_heads=4), 2, 4, "bf16")
     assert err < 2e-2
+
+
+def test_c5_small_bf16_full_remat_with_skip_channels():
+    """Full per-stage remat on the Llama graph: the replayed forward reads the
+    retained copies of the skip-channel positions / token ids; bitwise equal
+    to the stashing run."""
+    err_a, _, a = run(C5S, 4, 8, "bf16")
+    err_b, _, b = run(C5S, 4, 8, "bf16", remat="full-per-stage")
+    assert err_b < 2e-2
+    assert np.array_equal(a.losses, b.losses)
+    for q in a.grads:
+        assert np.array_equal(a.grads[q], b.grads[q]), q
