@@ -39,8 +39,25 @@ M_MICRO = 8
 # BASELINE configs[2] (C3, GPT-2 medium; quoted there on 8 stages x 16 microbatches):
 # `--workload C3` runs it on the GPUs given (the default bench line stays C2)
 C3 = dict(C2, layers=24, d_model=1024, n_heads=16, d_ff=4096)
-WORKLOADS = {"C2": (C2, 8, "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024"),
-             "C3": (C3, 16, "C3 gpt2-medium 24L d1024 h16 ff4096 V50304 seq1024")}
+# BASELINE configs[3] (C4, GPT-3 1.3B shape: head_dim 128, quoted on 8 GPUs with interleaved
+# 1F1B, 2 virtual stages per GPU, 32 microbatches) and configs[4] (C5, Llama-3-8B shape:
+# RMSNorm / RoPE / GQA 32:8 / SwiGLU, untied head, position ids as skip tensors from stage 0
+# to every later stage, 8-stage 1F1B, 16 microbatches).  `--workload C4|C5` runs them on the
+# GPUs given (one pipeline stage -- or V virtual stages -- per GPU).
+C4 = dict(layers=24, d_model=2048, n_heads=16, d_ff=8192, vocab=50304, seq_len=2048,
+          microbatch_size=4)
+C5 = dict(layers=32, d_model=4096, n_heads=32, n_kv_heads=8, d_ff=14336, vocab=128256,
+          seq_len=4096, microbatch_size=1)
+WORKLOADS = {
+    "C2": dict(family="gpt", kw=C2, M=8, schedule="1f1b", V=1,
+               name="C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024"),
+    "C3": dict(family="gpt", kw=C3, M=16, schedule="1f1b", V=1,
+               name="C3 gpt2-medium 24L d1024 h16 ff4096 V50304 seq1024"),
+    "C4": dict(family="gpt", kw=C4, M=32, schedule="interleaved", V=2,
+               name="C4 gpt3-1.3B 24L d2048 h16x128 ff8192 V50304 seq2048"),
+    "C5": dict(family="llama", kw=C5, M=16, schedule="1f1b", V=1,
+               name="C5 llama-8B 32L d4096 h32/kv8x128 swiglu14336 V128256 seq4096"),
+}
 
 
 def peaks():
@@ -71,21 +88,40 @@ def block_costs(cfg):
     return [emb] + [blk] * cfg.layers + [head]
 
 
+def llama_block_costs(cfg):
+    """Per-block time estimates (s) for the Llama stack (C5), same rates."""
+    T, d, V, S = cfg.tokens, cfg.d_model, cfg.vocab, cfg.seq_len
+    H, hd, f = cfg.n_heads, cfg.head_dim, cfg.d_ff
+    gemm = 3 * 2.0 * T * d * (cfg.qkv_width + H * hd + 3 * f)
+    attn = 3.5 * 2.0 * T * S * H * hd
+    elem = 2 * 16.0 * T * d + 2 * 8.0 * T * f
+    blk = gemm / _GEMM_RATE + attn / _ATTN_RATE + elem / _HBM_RATE
+    head = 3 * 2.0 * T * d * V / _HEAD_RATE + 3 * 2.0 * T * V / _STREAM_RATE
+    emb = 4.0 * T * d * 4 / _HBM_RATE
+    return [emb] + [blk] * cfg.layers + [head]
+
+
 METRIC = "tokens/s (model TFLOPS/GPU and bubble alongside)"
 WORKLOAD = "C2 gpt2-small 12L d768 h12 ff3072 V50304 seq1024"
 
 
-def build_plan(P, cfg_kw, M, mode="bf16"):
+def build_plan(P, cfg_kw, M, mode="bf16", family="gpt", schedule="1f1b", V=1):
+    """Plan one workload on P GPUs: P stages (1F1B) or P x V virtual stages
+    (interleaved 1F1B), stage boundaries balanced by the cost model."""
     from paper_2412_14374_b200 import comms as C
     from paper_2412_14374_b200 import ir as I
     from paper_2412_14374_b200 import schedules as S
     from paper_2412_14374_b200 import taskgraph as T
-    base = I.GPTConfig(**cfg_kw, yield_every=cfg_kw["layers"] + 2)
-    yields = I.balanced_yields(block_costs(base), P) if P > 1 else None
-    cfg = I.GPTConfig(**cfg_kw, yields=yields, yield_every=cfg_kw["layers"] + 2,
-                      elem_bytes=2 if mode == "bf16" else 4)
-    p = I.derive_backward(I.partition_stages(I.build_gpt(cfg)))
-    s = S.one_f_one_b(P, M)
+    inter = schedule == "interleaved" and P > 1 and V > 1
+    stages = P * V if inter else P
+    Cfg, build = (I.GPTConfig, I.build_gpt) if family == "gpt" else (I.LlamaConfig, I.build_llama)
+    costs_fn = block_costs if family == "gpt" else llama_block_costs
+    base = Cfg(**cfg_kw, yield_every=cfg_kw["layers"] + 2)
+    yields = I.balanced_yields(costs_fn(base), stages) if stages > 1 else None
+    cfg = Cfg(**cfg_kw, yields=yields, yield_every=cfg_kw["layers"] + 2,
+              elem_bytes=2 if mode == "bf16" else 4)
+    p = I.derive_backward(I.partition_stages(build(cfg)))
+    s = S.interleaved_1f1b(P, M, V) if inter else S.one_f_one_b(P, M)
     tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
     cp = C.infer_comms(tg, s)
     rep = C.check_deadlock_free(cp)
@@ -94,7 +130,7 @@ def build_plan(P, cfg_kw, M, mode="bf16"):
 
 
 def init_params_device(cfg, device, seed=0):
-    """N(0, 0.02) weights (out projections / sqrt(2L)), LN gamma=1, on device."""
+    """N(0, 0.02) weights (GPT: out projections / sqrt(2L)), norm gains 1, on device."""
     import torch
     from paper_2412_14374_b200 import _lib
     from paper_2412_14374_b200.device import Param
@@ -113,7 +149,7 @@ def init_params_device(cfg, device, seed=0):
             if name.endswith("_g"):
                 m[off:off + sz] = 1.0
             elif name.startswith("w"):
-                std = 0.02 / np.sqrt(2 * cfg.layers) if name in ("w_o", "w_fc2") else 0.02
+                std = 0.02 / np.sqrt(2 * cfg.layers) if name in ("w_o", "w_fc2", "w_down") else 0.02
                 m[off:off + sz] = torch.randn(sz, device=device, generator=g) * std
         sh = torch.empty(n, device=device, dtype=torch.bfloat16)
         _lib.call("pc_cast", _lib.PC_F32, _lib.PC_BF16, n, m.data_ptr(), sh.data_ptr(), st)
@@ -122,6 +158,8 @@ def init_params_device(cfg, device, seed=0):
     out["w0"] = make(cfg.embed_layout(), None)
     for k in range(1, cfg.layers + 1):
         out[f"w{k}"] = make(cfg.block_layout(k == cfg.layers), None)
+    if hasattr(cfg, "head_layout"):   # Llama: untied LM head
+        out["wout"] = make(cfg.head_layout(), None)
     return out
 
 
@@ -386,6 +424,10 @@ def main():
     ap.add_argument("--microbatches", type=int, default=None,
                     help="default: the workload's (C2: 8, C3: 16)")
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--schedule", default=None, choices=["1f1b", "interleaved"],
+                    help="default: the workload's (C4: interleaved)")
+    ap.add_argument("--virtual", type=int, default=None,
+                    help="virtual stages per GPU for interleaved 1F1B (default: the workload's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gantt", default=None, help="write the measured timeline as an SVG Gantt chart")
     ap.add_argument("--remat", default="none", choices=["none", "full-per-stage"],
@@ -409,16 +451,30 @@ def main():
     from paper_2412_14374_b200.executor import PipelineEngine
 
     P = world
-    wl_kw, wl_m, wl_name = WORKLOADS[args.workload]
-    M = args.microbatches or wl_m
-    cfg, tg, cp = build_plan(P, wl_kw, M)
+    wl = WORKLOADS[args.workload]
+    wl_kw, wl_name = wl["kw"], wl["name"]
+    M = args.microbatches or wl["M"]
+    Vv = args.virtual if args.virtual is not None else wl["V"]
+    sched = args.schedule or wl["schedule"]
+    cfg, tg, cp = build_plan(P, wl_kw, M, family=wl["family"], schedule=sched, V=Vv)
+    sched_used = "interleaved" if (sched == "interleaved" and P > 1 and Vv > 1) else "1f1b"
     dev = torch.device("cuda", local)
     params = init_params_device(cfg, dev)
     rng = np.random.default_rng(1234)
     tokens_host = rng.integers(0, cfg.vocab, size=(M * cfg.microbatch_size, cfg.seq_len),
                                dtype=np.int32)
-    tokens_dev = torch.from_numpy(tokens_host).to(dev)
-    tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
+    if wl["family"] == "llama":
+        # token ids + position ids (the skip tensors every later stage reads)
+        pos_host = np.tile(np.arange(cfg.seq_len, dtype=np.int32), (M * cfg.microbatch_size, 1))
+        tokens_dev = {"x": torch.from_numpy(tokens_host).to(dev),
+                      "pos": torch.from_numpy(pos_host).to(dev)}
+        tokens_pinned = {"x": torch.from_numpy(tokens_host).pin_memory(),
+                         "pos": torch.from_numpy(pos_host).pin_memory()}
+        h2d_bytes = int(tokens_host.nbytes + pos_host.nbytes)
+    else:
+        tokens_dev = torch.from_numpy(tokens_host).to(dev)
+        tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
+        h2d_bytes = int(tokens_host.nbytes)
     eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg, remat=args.remat)
     # resident training state: every step (eager or replayed) is a real SGD
     # step on the previous step's weights, tied w0 re-broadcast included
@@ -457,6 +513,7 @@ def main():
         return t.item()
 
     # ---- device-resident timed region ----
+    torch.cuda.reset_peak_memory_stats(dev)
     clocks = ClockSampler(local)
     clocks.start()
     clocks.wait_first()
@@ -472,6 +529,9 @@ def main():
     wall = time.perf_counter() - t0
     clocks.window = (t0, t0 + wall)
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    # peak HBM of the timed steps: torch allocations (the graph pool, params,
+    # activations) plus this rank's peer receive slots (cudaMalloc'd outside torch)
+    peak_hbm = torch.cuda.max_memory_allocated(dev) + eng.peer_bytes
     # kernels per step: the captured graph's kernel nodes (libpp200 calls when eager)
     launches = cap.kernels if use_graph else int((_lib.launch_count - launches0) / args.steps)
     clk = clocks.stop()
@@ -520,10 +580,14 @@ def main():
     flops_step = cfg.flops_per_token() * tokens_per_step
     tflops_gpu = flops_step / (ms / 1000) / P / 1e12
     burst, sustained, hbm, peak_kind = peaks()
-    ideal = (P - 1) / (M + P - 1)
+    Vi = Vv if sched_used == "interleaved" else 1
+    ideal = (P - 1) / (Vi * M + P - 1)   # simulator.py:346-348
 
     if rank == 0:
-        stage_blocks = sum(1 for op in tg.partition.fwd_programs[0].ops if op.kind == "gpt-block")
+        # blocks on rank 0: its stages are s = 0, P, 2P, ... (schedules.py:60-61)
+        fp = tg.partition.fwd_programs
+        stage_blocks = sum(1 for st in range(0, len(fp), P) for op in fp[st].ops
+                           if op.kind in ("gpt-block", "llama-block"))
         roof = gemm_roofline(cfg, P, stage_blocks, ms, burst, M)
         roof["peak_kind"] = peak_kind
         cpu = None if args.no_cpu_baseline else cpu_baseline(wl_kw)
@@ -536,7 +600,9 @@ def main():
             "config": {"workload": wl_name,
                        "global_batch": M * cfg.microbatch_size, "seq_len": cfg.seq_len,
                        "microbatches": M, "microbatch_size": cfg.microbatch_size,
-                       "schedule": "1f1b", "stages": P, "yields": list(cfg.yields or []),
+                       "schedule": sched_used, "virtual_stages_per_gpu": Vv if sched_used ==
+                       "interleaved" else 1, "stages": len(tg.partition.fwd_programs),
+                       "yields": list(cfg.yields or []),
                        "parallelism": f"pp{P}", "l2": "inputs > L2 (no flush needed)",
                        "issue": "cuda-graph replay per actor" if use_graph else "python per op",
                        "transport": eng.transport if world > 1 else None,
@@ -544,14 +610,16 @@ def main():
                        "training": "resident params, in-place SGD each step"
                                    + (", tied w0 re-broadcast to the head stage" if P > 1 else "")},
             "model_tflops_per_gpu": round(tflops_gpu, 1),
-            "peak_hbm_gb_rank0": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
+            "peak_hbm_gb_rank0": round(peak_hbm / 1e9, 2),
+            "peak_hbm_covers": "timed steps: torch allocator peak (reset before the timed region) "
+                               "+ peer receive slots; excludes NCCL-internal buffers",
             "frac_of_bf16_peak": round(tflops_gpu / burst, 4),
             "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4),
                        "achievable": round(achievable, 4)},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e, 1), "unit": "tokens/s",
-                    "h2d_bytes_per_step": int(tokens_host.nbytes), "d2h_bytes_per_step": 4 * M},
+                    "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 4 * M},
             "gpu_launches": launches,
             "clocks": clk,
             "wall_s": round(wall, 3),

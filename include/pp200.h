@@ -189,8 +189,20 @@ int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const void* qkv, in
 int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const void* qkv, int64_t ld_qkv,
                      const void* o, const void* dO, int64_t ld_o, const float* lse, float* delta,
                      void* dqkv, int64_t ld_dqkv, void* stream);
-/* 0 = auto (bf16: tcgen05 forward + mma.sync backward when supported), 1 = force exact SIMT,
- * 2 = force the mma.sync forward. Test hook. */
+/* Grouped-query causal attention (SURVEY §8(b) pc_attention_fwd/bwd with Hkv): qkv packs H
+ * query heads, then Hkv key heads, then Hkv value heads, each hd columns; query head h reads
+ * kv head h / (H / Hkv); dqkv has qkv's layout and a kv head's gradient sums its group
+ * (oracle/llama.py gqa_attention[_bwd]).  Replaces the `matmul` + softmax numpy expressions
+ * of a stage forward (executor.py:66-67) for the attention blocks.  bf16 head_dim 64 / 128:
+ * tcgen05 kernels; Hkv == H otherwise also served by the legacy / SIMT kernels. */
+int pc_attention_gqa_fwd(int dtype, int B, int H, int Hkv, int S, int hd, const void* qkv,
+                         int64_t ld_qkv, void* o, int64_t ld_o, float* lse, void* stream);
+int pc_attention_gqa_bwd(int dtype, int B, int H, int Hkv, int S, int hd, const void* qkv,
+                         int64_t ld_qkv, const void* o, const void* dO, int64_t ld_o,
+                         const float* lse, float* delta, void* dqkv, int64_t ld_dqkv,
+                         void* stream);
+/* 0 = auto (bf16: tcgen05 for head_dim 64 / 128), 1 = force exact SIMT,
+ * 2 = force the mma.sync kernels. Test hook. */
 int pc_attention_set_impl(int impl);
 
 /* ---- inter-stage transport over NVLink peer memory (Channel, executor.py:201-254) ----
@@ -206,6 +218,10 @@ int pc_peer_close(void* ptr);
 int pc_stream_write_u32(void* addr, uint32_t value, void* stream);
 int pc_stream_wait_u32(void* addr, uint32_t value, void* stream);
 int pc_peer_copy(void* dst, const void* src, int64_t bytes, void* stream);
+/* Abort (Channel faults, executor.py:185-197, :443-451): set n flag words to value from a
+ * stream that is not blocked, releasing a receiver stream parked in pc_stream_wait_u32 on a
+ * message that will never arrive, so the device drains and the fault can surface. */
+int pc_peer_release(void* flags, int64_t n, uint32_t value, void* stream);
 /* Kernel nodes of a captured CUDA graph (cudaGraph_t), child graphs included. */
 int pc_graph_kernel_nodes(void* graph, int64_t* n);
 

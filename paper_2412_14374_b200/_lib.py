@@ -59,6 +59,7 @@ SIGNATURES: dict[str, list] = {
     "pc_stream_write_u32": [_c_p, ctypes.c_uint32, _c_p],
     "pc_stream_wait_u32": [_c_p, ctypes.c_uint32, _c_p],
     "pc_peer_copy": [_c_p, _c_p, _c_i64, _c_p],
+    "pc_peer_release": [_c_p, _c_i64, ctypes.c_uint32, _c_p],
     "pc_graph_kernel_nodes": [_c_p, ctypes.POINTER(_c_i64)],
     "pc_sgd_update": [_c_i, _c_i64, _c_p, _c_p, _c_d, _c_p, _c_p, _c_p],
     "pc_cast": [_c_i, _c_i, _c_i64, _c_p, _c_p, _c_p],
@@ -87,6 +88,10 @@ SIGNATURES: dict[str, list] = {
     "pc_attention_fwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p],
     "pc_attention_bwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p,
                          _c_p, _c_p, _c_i64, _c_p],
+    "pc_attention_gqa_fwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_i64, _c_p,
+                             _c_p],
+    "pc_attention_gqa_bwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_p, _c_i64,
+                             _c_p, _c_p, _c_p, _c_i64, _c_p],
     "pc_attention_set_impl": [_c_i],
     "pc_p2p_available": [],
     "pc_p2p_unique_id": [_c_p],

@@ -283,41 +283,69 @@ int attention_bwd_tc(int B, int H, int S, int hd, const void* qkv, int64_t ld_qk
                      const void* dO, int64_t ld_o, const float* lse, float* delta, void* dqkv,
                      int64_t ld_dqkv, cudaStream_t st);
 bool attention_tc_supported(int hd, int64_t ld_qkv, int64_t ld_o);
-bool attention_tc5_supported(int hd, int64_t ld_qkv, int64_t ld_o, const void* qkv, const void* o);
-int attention_fwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, void* o, int64_t ld_o,
-                      float* lse, cudaStream_t st);
-int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, const void* o,
-                      const void* dO, int64_t ld_o, const float* lse, float* delta, void* dqkv,
-                      int64_t ld_dqkv, cudaStream_t st);
+bool attention_tc5_supported(int hd, int H, int Hkv, int64_t ld_qkv, int64_t ld_o, const void* qkv,
+                             const void* o);
+int attention_fwd_tc5(int B, int H, int Hkv, int S, int hd, const void* qkv, int64_t ld_qkv, void* o,
+                      int64_t ld_o, float* lse, cudaStream_t st);
+int attention_bwd_tc5(int B, int H, int Hkv, int S, int hd, const void* qkv, int64_t ld_qkv,
+                      const void* o, const void* dO, int64_t ld_o, const float* lse, float* delta,
+                      void* dqkv, int64_t ld_dqkv, cudaStream_t st);
 }  // namespace pp200
 
-extern "C" int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const void* qkv,
-                                int64_t ld_qkv, void* o, int64_t ld_o, float* lse, void* stream) {
+extern "C" int pc_attention_gqa_fwd(int dtype, int B, int H, int Hkv, int S, int hd,
+                                    const void* qkv, int64_t ld_qkv, void* o, int64_t ld_o,
+                                    float* lse, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  PP_CHECK_ARG(B > 0 && H > 0 && S > 0 && hd > 0 && hd <= 32 * 8, "attention: bad dims");
+  PP_CHECK_ARG(B > 0 && H > 0 && Hkv > 0 && H % Hkv == 0 && S > 0 && hd > 0 && hd <= 32 * 8,
+               "attention: bad dims");
   PP_CHECK_ARG(dtype == PC_F32 || dtype == PC_BF16, "attention: f32/bf16 only");
-  if (dtype == PC_BF16 && g_attn_impl == 0 && attention_tc5_supported(hd, ld_qkv, ld_o, qkv, o))
-    return attention_fwd_tc5(B, H, S, qkv, ld_qkv, o, ld_o, lse, st);
+  if (dtype == PC_BF16 && g_attn_impl == 0 &&
+      attention_tc5_supported(hd, H, Hkv, ld_qkv, ld_o, qkv, o))
+    return attention_fwd_tc5(B, H, Hkv, S, hd, qkv, ld_qkv, o, ld_o, lse, st);
+  if (Hkv != H) {
+    set_error("attention: grouped-query heads need the tcgen05 path (bf16, head_dim 64/128)");
+    return PC_ERR_UNSUPPORTED;
+  }
   if (dtype == PC_BF16 && g_attn_impl != 1 && attention_tc_supported(hd, ld_qkv, ld_o))
     return attention_fwd_tc(B, H, S, hd, qkv, ld_qkv, o, ld_o, lse, st);
   return attention_fwd_simt(dtype, B, H, S, hd, qkv, ld_qkv, o, ld_o, lse, st);
 }
 
-extern "C" int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const void* qkv,
-                                int64_t ld_qkv, const void* o, const void* dO, int64_t ld_o,
-                                const float* lse, float* delta, void* dqkv, int64_t ld_dqkv,
-                                void* stream) {
+extern "C" int pc_attention_gqa_bwd(int dtype, int B, int H, int Hkv, int S, int hd,
+                                    const void* qkv, int64_t ld_qkv, const void* o, const void* dO,
+                                    int64_t ld_o, const float* lse, float* delta, void* dqkv,
+                                    int64_t ld_dqkv, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  PP_CHECK_ARG(B > 0 && H > 0 && S > 0 && hd > 0 && hd <= 32 * 8, "attention: bad dims");
+  PP_CHECK_ARG(B > 0 && H > 0 && Hkv > 0 && H % Hkv == 0 && S > 0 && hd > 0 && hd <= 32 * 8,
+               "attention: bad dims");
   PP_CHECK_ARG(dtype == PC_F32 || dtype == PC_BF16, "attention: f32/bf16 only");
-  if (dtype == PC_BF16 && g_attn_impl == 0 && attention_tc5_supported(hd, ld_qkv, ld_o, qkv, dO) &&
+  if (dtype == PC_BF16 && g_attn_impl == 0 &&
+      attention_tc5_supported(hd, H, Hkv, ld_qkv, ld_o, qkv, dO) &&
       (reinterpret_cast<uintptr_t>(dqkv) & 15) == 0 && (ld_dqkv * 2) % 16 == 0 && S % 4 == 0 &&
       (reinterpret_cast<uintptr_t>(lse) & 15) == 0 && (reinterpret_cast<uintptr_t>(delta) & 15) == 0)
-    return attention_bwd_tc5(B, H, S, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv, st);
+    return attention_bwd_tc5(B, H, Hkv, S, hd, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv,
+                             st);
+  if (Hkv != H) {
+    set_error("attention: grouped-query heads need the tcgen05 path (bf16, head_dim 64/128, S %% 4 == 0)");
+    return PC_ERR_UNSUPPORTED;
+  }
   if (dtype == PC_BF16 && g_attn_impl != 1 && attention_tc_supported(hd, ld_qkv, ld_o))
     return attention_bwd_tc(B, H, S, hd, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv, st);
   int rc = attention_delta(dtype, B, H, S, hd, o, dO, ld_o, delta, st);
   if (rc) return rc;
   return attention_bwd_simt(dtype, B, H, S, hd, qkv, ld_qkv, dO, ld_o, lse, delta, dqkv, ld_dqkv,
                             st);
+}
+
+extern "C" int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const void* qkv,
+                                int64_t ld_qkv, void* o, int64_t ld_o, float* lse, void* stream) {
+  return pc_attention_gqa_fwd(dtype, B, H, H, S, hd, qkv, ld_qkv, o, ld_o, lse, stream);
+}
+
+extern "C" int pc_attention_bwd(int dtype, int B, int H, int S, int hd, const void* qkv,
+                                int64_t ld_qkv, const void* o, const void* dO, int64_t ld_o,
+                                const float* lse, float* delta, void* dqkv, int64_t ld_dqkv,
+                                void* stream) {
+  return pc_attention_gqa_bwd(dtype, B, H, H, S, hd, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv,
+                              ld_dqkv, stream);
 }

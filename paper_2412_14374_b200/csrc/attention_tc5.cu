@@ -1,23 +1,22 @@
-// tcgen05 causal flash-attention forward (bf16, head_dim 64), sm_100a.
+// tcgen05 causal flash attention, forward and backward, bf16, sm_100a.
 //
-// Semantics: oracle/gpt.py `attention` (exact softmax, causal), same layout
-// contract as attention_tc.cu (qkv [B*S, ld], o [B*S, ld_o], lse [B,H,S]).
+// Semantics: oracle/gpt.py `attention` / `attention_bwd` (exact softmax,
+// causal) and, with fewer key/value heads than query heads, oracle/llama.py
+// `gqa_attention` (query head h reads kv head h / (H / Hkv); a kv head's
+// gradient is the sum over its query heads).  Templated on the head dim
+// HD in {64, 128} (GPT-2 configs C1-C3: 64; GPT-3 1.3B / Llama-8B, C4 / C5: 128).
 //
-// One CTA = 128 query rows of one (batch, head); 8 warps:
-//   warp 0      TMA producer: Q tile once, then K/V tiles of 64 keys into a
-//               128B-swizzled smem ring
-//   warp 1      single-thread tcgen05.mma issuer, one key block ahead:
-//                 S_j = Q K_j^T  (M=128, N=64 keys, K=64) -> TMEM S[j % 2]
-//                 O  += P_j V_j  (M=128, N=64 dims, K=64) -> TMEM O
-//               S_{j+1} is issued before PV_j, so the tensor core computes
-//               the next scores while the softmax warps work on block j.
-//   warp 2      TMEM allocator (256 columns: S0, S1, O; 2 CTAs fit per SM)
-//   warps 4..7  softmax: one thread owns one query row (TMEM lane), so row
-//               max / sum need no shuffles; P_j is written as bf16 into the
-//               128B-swizzled K-major smem tile P[j % 2] (the MMA's A operand);
-//               O is rescaled in TMEM when the running max moves.
-// Barriers: s_full[i] (S_j landed), p_full[i] (P_j staged), pv_done[i]
-// (PV_j retired: P[i] reusable, O up to date).
+// Layout contract (the stage activations): one packed
+// projection buffer qkv [B*S, ld] holding H query heads, then Hkv key heads,
+// then Hkv value heads, each HD columns wide; o [B*S, ld_o]; lse / delta
+// [B, H, S] fp32; the gradient dqkv has qkv's layout.  Grouped-query heads
+// are addressed in the TMA coordinates: no K/V expansion and no separate
+// group reduction (the dK/dV kernel accumulates a kv head's whole group in
+// TMEM).
+//
+// Every operand tile is a set of 128B-swizzled K-major "panels" of 64
+// columns (one TMA box is 64 columns x 64 rows); a head of HD columns is
+// HD / 64 panels side by side in shared memory.
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -29,11 +28,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn();
 namespace {
 
 using bf16 = __nv_bfloat16;
-constexpr int F_BM = 128, F_BN = 64, F_HD = 64, F_STAGES = 3, F_THREADS = 256;
-constexpr int F_Q_BYTES = F_BM * F_HD * 2;    // 16 KB
-constexpr int F_KV_BYTES = F_BN * F_HD * 2;   // 8 KB
-constexpr int F_SMEM = F_Q_BYTES + 2 * F_STAGES * F_KV_BYTES + 1024 + 256;
 constexpr float F_LN2 = 0.6931471805599453f;
+constexpr float F_LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -76,39 +72,83 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__global__ void __launch_bounds__(F_THREADS, 2)
+// Column of the first element of query head h / kv head hk (K or V) in qkv.
+struct Heads {
+  int H, Hkv, G, hd;
+  __device__ __forceinline__ int qcol(int h) const { return h * hd; }
+  __device__ __forceinline__ int kcol(int hk) const { return (H + hk) * hd; }
+  __device__ __forceinline__ int vcol(int hk) const { return (H + Hkv + hk) * hd; }
+};
+
+// K-major descriptor of k-step k (16 elements of the contraction dim) of a
+// tile made of 64-column panels `panel_bytes` apart.
+__device__ __forceinline__ uint64_t kmajor_step(uint32_t base, int k, uint32_t panel_bytes) {
+  return umma_sdesc_sw128(base + (k >> 2) * panel_bytes + (k & 3) * 32, 16, 1024);
+}
+
+// ------------------------------------------------------------------ forward
+// One CTA = 128 query rows of one (batch, head); 8 warps:
+//   warp 0      TMA producer: Q tile once, then K/V blocks of 64 keys into a
+//               128B-swizzled smem ring
+//   warp 1      single-thread tcgen05.mma issuer, one key block ahead:
+//                 S_j = Q K_j^T  (M=128, N=64 keys, K=HD) -> TMEM S[j % 2]
+//                 O  += P_j V_j  (M=128, N=HD dims, K=64) -> TMEM O
+//               S_{j+1} is issued before PV_j, so the tensor core computes
+//               the next scores while the softmax warps work on block j.
+//   warp 2      TMEM allocator (256 columns: S0, S1, O; two CTAs fit per SM
+//               and share the tensor core, hiding each other's softmax)
+//   warps 4..7  softmax: one thread owns one query row (TMEM lane), so row
+//               max / sum need no shuffles; P_j is written back as packed bf16
+//               over its own score columns (the PV MMA reads A from TMEM);
+//               O is rescaled in TMEM when the running max moves.
+template <int HD>
+struct Fwd {
+  static constexpr int BM = 128, BN = 64, THREADS = 256;
+  static constexpr int NP = HD / 64;                   // 64-column panels per head
+  static constexpr int STAGES = HD == 64 ? 3 : 2;
+  static constexpr int Q_PANEL = BM * 64 * 2;          // 16 KB
+  static constexpr int KV_PANEL = BN * 64 * 2;         // 8 KB
+  static constexpr int Q_BYTES = NP * Q_PANEL;
+  static constexpr int KV_BYTES = NP * KV_PANEL;
+  static constexpr int SMEM = Q_BYTES + 2 * STAGES * KV_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 256;                // S0 | S1 | O (HD <= 128)
+};
+
+template <int HD>
+__global__ void __launch_bounds__(256, 2)
     fa_fwd_tc5(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, int64_t ldo,
-               float* __restrict__ lse, int H, int S, float sl2) {
+               float* __restrict__ lse, Heads hs, int S, float sl2) {
+  using K = Fwd<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + F_Q_BYTES;
-  uint8_t* sV = sK + F_STAGES * F_KV_BYTES;
-  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sV + F_STAGES * F_KV_BYTES);
+  uint8_t* sK = sQ + K::Q_BYTES;
+  uint8_t* sV = sK + K::STAGES * K::KV_BYTES;
+  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sV + K::STAGES * K::KV_BYTES);
   uint64_t* kv_full = bar_q + 1;
-  uint64_t* kv_empty = kv_full + F_STAGES;
-  uint64_t* s_full = kv_empty + F_STAGES;  // [2]
-  uint64_t* p_full = s_full + 2;           // [2]
-  uint64_t* pv_done = p_full + 2;          // [2]
+  uint64_t* kv_empty = kv_full + K::STAGES;
+  uint64_t* s_full = kv_empty + K::STAGES;  // [2]
+  uint64_t* p_full = s_full + 2;            // [2]
+  uint64_t* pv_done = p_full + 2;           // [2]
   uint64_t* o_done = pv_done + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = (S + F_BM - 1) / F_BM;
+  const int H = hs.H;
+  const int nqb = (S + K::BM - 1) / K::BM;
   // grid (B*H, tiles): x varies fastest, so every head's longest (latest) tile
   // launches before any shorter one -- longest-first across the whole grid
   const int qb = nqb - 1 - static_cast<int>(blockIdx.y);
-  const int b = blockIdx.x / H, h = blockIdx.x % H;
-  const int d = H * F_HD;
-  const int q0 = qb * F_BM;
+  const int b = blockIdx.x / H, h = blockIdx.x % H, hk = h / hs.G;
+  const int q0 = qb * K::BM;
   const int brow = b * S;  // first row of this batch in the [B*S, ld] tensors
-  const int nkb = (min(S, q0 + F_BM) + F_BN - 1) / F_BN;
+  const int nkb = (min(S, q0 + K::BM) + K::BN - 1) / K::BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
     mbar_init(bar_q, 1);
-    for (int s = 0; s < F_STAGES; ++s) {
+    for (int s = 0; s < K::STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
@@ -120,7 +160,7 @@ __global__ void __launch_bounds__(F_THREADS, 2)
     mbar_init(o_done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tslot, 256);
+  if (warp == 2) tmem_alloc(tslot, K::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -129,51 +169,59 @@ __global__ void __launch_bounds__(F_THREADS, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_q, F_Q_BYTES);
-      tma_load_2d(sQ, &tm, bar_q, h * F_HD, brow + q0);
-      tma_load_2d(sQ + F_Q_BYTES / 2, &tm, bar_q, h * F_HD, brow + q0 + 64);
+      mbar_expect_tx(bar_q, K::Q_BYTES);
+#pragma unroll
+      for (int p = 0; p < K::NP; ++p)
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_2d(sQ + p * K::Q_PANEL + hf * (K::Q_PANEL / 2), &tm, bar_q, hs.qcol(h) + 64 * p,
+                      brow + q0 + 64 * hf);
       for (int j = 0; j < nkb; ++j) {
-        const int s = j % F_STAGES;
-        const uint32_t ph = (j / F_STAGES) & 1;
+        const int s = j % K::STAGES;
+        const uint32_t ph = (j / K::STAGES) & 1;
         mbar_wait(&kv_empty[s], ph ^ 1);
-        mbar_expect_tx(&kv_full[s], 2 * F_KV_BYTES);
-        tma_load_2d(sK + s * F_KV_BYTES, &tm, &kv_full[s], d + h * F_HD, brow + j * F_BN);
-        tma_load_2d(sV + s * F_KV_BYTES, &tm, &kv_full[s], 2 * d + h * F_HD, brow + j * F_BN);
+        mbar_expect_tx(&kv_full[s], 2 * K::KV_BYTES);
+#pragma unroll
+        for (int p = 0; p < K::NP; ++p) {
+          tma_load_2d(sK + s * K::KV_BYTES + p * K::KV_PANEL, &tm, &kv_full[s],
+                      hs.kcol(hk) + 64 * p, brow + j * K::BN);
+          tma_load_2d(sV + s * K::KV_BYTES + p * K::KV_PANEL, &tm, &kv_full[s],
+                      hs.vcol(hk) + 64 * p, brow + j * K::BN);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t ID_S = umma_idesc_bf16(F_BM, F_BN, 0, 0);  // Q, K both K-major
-      constexpr uint32_t ID_O = umma_idesc_bf16(F_BM, F_HD, 0, 1);  // P K-major, V MN-major
+      constexpr uint32_t ID_S = umma_idesc_bf16(K::BM, K::BN, 0, 0);  // Q, K both K-major
+      constexpr uint32_t ID_O = umma_idesc_bf16(K::BM, HD, 0, 1);     // P K-major, V MN-major
       mbar_wait(bar_q, 0);
       tc_fence_after();
       const uint32_t q_addr = smem_u32(sQ);
       auto issue_s = [&](int j) {  // S_j = Q K_j^T into S[j % 2]
-        const int s = j % F_STAGES;
-        mbar_wait(&kv_full[s], (j / F_STAGES) & 1);
+        const int s = j % K::STAGES;
+        mbar_wait(&kv_full[s], (j / K::STAGES) & 1);
         // S[j % 2] still holds P_{j-2}: wait until PV_{j-2} has read it
         if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + s * F_KV_BYTES);
+        const uint32_t k_addr = smem_u32(sK + s * K::KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < F_HD / 16; ++k)
-          tc_mma_f16(tS + (j & 1) * 64, umma_sdesc_sw128(q_addr + k * 32, 16, 1024),
-                     umma_sdesc_sw128(k_addr + k * 32, 16, 1024), ID_S, k > 0 ? 1u : 0u);
+        for (int k = 0; k < HD / 16; ++k)
+          tc_mma_f16(tS + (j & 1) * 64, kmajor_step(q_addr, k, K::Q_PANEL),
+                     kmajor_step(k_addr, k, K::KV_PANEL), ID_S, k > 0 ? 1u : 0u);
         tc_commit(&s_full[j & 1]);
       };
       issue_s(0);
       for (int j = 0; j < nkb; ++j) {
         // S[(j+1) % 2] was last read by softmax j-1, which finished before PV_{j-1}
         if (j + 1 < nkb) issue_s(j + 1);
-        const int s = j % F_STAGES;
+        const int s = j % K::STAGES;
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV + s * F_KV_BYTES);
+        const uint32_t v_addr = smem_u32(sV + s * K::KV_BYTES);
         const uint32_t tP = tS + (j & 1) * 64;  // P_j packed bf16, key chunk k at column 8 k
 #pragma unroll
-        for (int k = 0; k < F_BN / 16; ++k)
-          tc_mma_f16_ts(tO, tP + 8 * k, umma_sdesc_sw128(v_addr + k * 2048, 8192, 1024), ID_O,
-                        (j > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < K::BN / 16; ++k)
+          tc_mma_f16_ts(tO, tP + 8 * k, umma_sdesc_sw128(v_addr + k * 2048, K::KV_PANEL, 1024),
+                        ID_O, (j > 0 || k > 0) ? 1u : 0u);
         tc_commit(&pv_done[j & 1]);
         tc_commit(&kv_empty[s]);
       }
@@ -193,8 +241,8 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       for (int c = 0; c < 4; ++c) tmem_ld16(tS + (j & 1) * 64 + lane_off + c * 16, sr + c * 16);
       tc_wait_ld();
       float* sv = reinterpret_cast<float*>(sr);
-      const int n0 = j * F_BN;
-      const bool edge = n0 + F_BN - 1 > q0 || n0 + F_BN > S;  // diagonal or ragged block
+      const int n0 = j * K::BN;
+      const bool edge = n0 + K::BN - 1 > q0 || n0 + K::BN > S;  // diagonal or ragged block
       // max of the raw scores (the positive scale commutes with max), 8
       // independent chains; masked entries become -inf
       float mx8[8];
@@ -202,11 +250,11 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
       if (edge) {
 #pragma unroll
-        for (int i = 0; i < F_BN; ++i)
+        for (int i = 0; i < K::BN; ++i)
           if (n0 + i > row || n0 + i >= S) sv[i] = -INFINITY;
       }
 #pragma unroll
-      for (int i = 0; i < F_BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], sv[i]);
+      for (int i = 0; i < K::BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], sv[i]);
       const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
       // Lazy rescaling (FA4): keep the running reference max unless the row
@@ -225,7 +273,7 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       const uint64_t sc2 = pack_f2(sl2, sl2), nm2 = pack_f2(-m, -m);
       uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-      for (int i = 0; i < F_BN; i += 2) {
+      for (int i = 0; i < K::BN; i += 2) {
         float p0, p1;
         unpack_f2(ffma2(pack_f2(sv[i], sv[i + 1]), sc2, nm2), p0, p1);
         p0 = ex2(p0);
@@ -240,7 +288,6 @@ __global__ void __launch_bounds__(F_THREADS, 2)
       const float sum = ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
       l = l * corr + sum;
       // P row as packed bf16 over the first 32 columns of its own score buffer
-      // (the PV MMA's A operand, read from TMEM)
       {
         uint32_t wv[32];
 #pragma unroll
@@ -254,7 +301,7 @@ __global__ void __launch_bounds__(F_THREADS, 2)
         mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < HD / 16; ++c) {
           uint32_t orr[16];
           tmem_ld16(tO + lane_off + c * 16, orr);
           tc_wait_ld();
@@ -271,9 +318,9 @@ __global__ void __launch_bounds__(F_THREADS, 2)
     mbar_wait(o_done, 0);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    bf16* orow = o + static_cast<int64_t>(brow + row) * ldo + h * F_HD;
+    bf16* orow = o + static_cast<int64_t>(brow + row) * ldo + hs.qcol(h);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < HD / 16; ++c) {
       uint32_t orr[16];
       tmem_ld16(tO + lane_off + c * 16, orr);
       tc_wait_ld();
@@ -294,33 +341,14 @@ __global__ void __launch_bounds__(F_THREADS, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 256);
+  if (warp == 2) tmem_dealloc(tmem, K::TMEM_COLS);
 }
 
 
 // ------------------------------------------------------------------ backward
-// NG elementwise warps per TMEM lane quarter, each owning CW = 64 / NG columns
+// NG elementwise warps per TMEM lane quarter, each owning CW = 64 / NG score
+// columns (and HD / NG output columns in the epilogues)
 constexpr int BW_NG = 4, BW_CW = 64 / BW_NG;
-constexpr int B_KEYS = 128, B_Q = 64, BKV_STAGES = 5, BKV_EW = 4 * BW_NG, BKV_THREADS = 128 + 32 * BKV_EW;
-// score buffers (S/dP pairs of 64 + 64 TMEM columns): the MMA warp keeps the
-// score MMAs up to three blocks ahead of the elementwise warps
-constexpr int B_SBUF = 3;
-constexpr int BKV_SMEM = 2 * 2 * 16384 /*K,V x2*/ + BKV_STAGES * 2 * 8192 /*Q,dO*/ +
-                         BKV_STAGES * 512 /*lse,delta*/ + 1024 + 256;
-
-// NC * 8 bf16 (NC 16 B chunks starting at logical chunk c0) of row r of a
-// 128B-swizzled [rows x 64] K-major tile.
-template <int NC>
-__device__ __forceinline__ void st_row_chunks(uint8_t* tile, int r, int c0, const float* v) {
-#pragma unroll
-  for (int h = 0; h < NC; ++h) {
-    uint4 u;
-    __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) hp[k] = __floats2bfloat162_rn(v[8 * h + 2 * k], v[8 * h + 2 * k + 1]);
-    *reinterpret_cast<uint4*>(tile + r * 128 + (((c0 + h) ^ (r & 7)) << 4)) = u;
-  }
-}
 
 // NC * 8 fp32 accumulator values -> bf16 (scaled) in global memory.
 template <int NC>
@@ -334,23 +362,25 @@ __device__ __forceinline__ void store_row_chunks(bf16* dst, const uint32_t* acc,
   for (int k = 0; k < NC; ++k) reinterpret_cast<uint4*>(dst)[k] = u[k];
 }
 
-// CW fp32 columns of one TMEM lane into registers (CW = 16 or 32).
+// CW fp32 columns of one TMEM lane into registers (CW a multiple of 16).
 template <int CW>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
 #pragma unroll
   for (int i = 0; i < CW / 16; ++i) tmem_ld16(taddr + 16 * i, r + 16 * i);
 }
 
-// dK, dV for 128-key tiles, persistent: one CTA per SM walks the tiles
-// longest-first (tile w: key tile w / BH, head w % BH).  12 + 4 warps:
-//   warp 0      TMA producer: K, V of a tile into one of two buffers (the next
-//               tile's prefetched while this one computes); per 64-query block
-//               Q, dO (tensor maps) and its lse / delta rows (bulk copies)
-//               into a 5-deep ring
-//   warp 1      MMA issuer, up to three query blocks ahead of the elementwise
-//               warps: S^T_i = K Q_i^T, dP^T_i = V dO_i^T -> TMEM buffer i % 3;
+// dK, dV for 128-key tiles of one (batch, kv head), persistent: one CTA per SM
+// walks the tiles longest-first (tile w: key tile w / (B Hkv), kv head w % (B Hkv)).
+// A tile's blocks are the 64-query blocks at or after its keys of every query
+// head of the kv head's group, so dK / dV accumulate the group sum in TMEM.
+// 4 + 16 warps:
+//   warp 0      TMA producer: K, V of a tile into one of KVBUF buffers; per
+//               block Q, dO (tensor maps) and its lse / delta rows (bulk
+//               copies) into a STAGES-deep ring
+//   warp 1      MMA issuer, up to SBUF query blocks ahead of the elementwise
+//               warps: S^T_i = K Q_i^T, dP^T_i = V dO_i^T -> TMEM buffer i % SBUF;
 //               dV += P^T_i dO_i, dK += dS^T_i Q_i -> TMEM accumulators
-//   warp 2      TMEM allocator (512 columns: S^T/dP^T x3, dV, dK)
+//   warp 2      TMEM allocator (512 columns: S^T/dP^T x SBUF, dV, dK)
 //   warps 4..   elementwise: BW_NG warps per TMEM lane quarter (one key row
 //               per thread, 64 / BW_NG queries each) build P^T = exp2(S^T*c - lse)
 //               and dS^T = P^T (dP^T - delta) as packed bf16 written back into
@@ -358,49 +388,67 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
 //               A operand straight from TMEM (query chunk k of 16 at column 16 k)
 // Ring / buffer phases run on tile-global block counters; a score buffer is
 // reused once the dV / dK MMAs that read its P^T / dS^T have retired.
-__global__ void __launch_bounds__(BKV_THREADS, 1)
+template <int HD>
+struct BwdKV {
+  static constexpr int KEYS = 128, BQ = 64;
+  static constexpr int NP = HD / 64;
+  static constexpr int SBUF = HD == 64 ? 3 : 2;
+  static constexpr int STAGES = HD == 64 ? 5 : 4;
+  static constexpr int KVBUF = HD == 64 ? 2 : 1;
+  static constexpr int KV_PANEL = KEYS * 64 * 2;   // 16 KB
+  static constexpr int KV_BYTES = NP * KV_PANEL;   // one of K / V
+  static constexpr int Q_PANEL = BQ * 64 * 2;      // 8 KB
+  static constexpr int Q_BYTES = NP * Q_PANEL;     // one of Q / dO per stage
+  static constexpr int EW = 4 * BW_NG, THREADS = 128 + 32 * EW;
+  static constexpr int SMEM = KVBUF * 2 * KV_BYTES + STAGES * 2 * Q_BYTES + STAGES * 512 + 1024 + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
     fa_bwd_dkdv_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                     const float* __restrict__ lse, const float* __restrict__ delta,
-                    bf16* __restrict__ dqkv, int64_t ldd, int BH, int H, int S, float sl2,
+                    bf16* __restrict__ dqkv, int64_t ldd, int B, Heads hs, int S, float sl2,
                     float scale) {
+  using K = BwdKV<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sK = smem;                      // [2][128 keys x 64]
-  uint8_t* sV = sK + 2 * 16384;            // [2][128 keys x 64]
-  uint8_t* sQ = sV + 2 * 16384;            // [ST][64 x 64]
-  uint8_t* sG = sQ + BKV_STAGES * 8192;    // dO [ST][64 x 64]
-  float* sLD = reinterpret_cast<float*>(sG + BKV_STAGES * 8192);  // [ST][lse 64 | delta 64]
-  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sLD + BKV_STAGES * 128);  // [2]
-  uint64_t* kv_empty = kv_full + 2;         // [2]
-  uint64_t* q_full = kv_empty + 2;
-  uint64_t* q_empty = q_full + BKV_STAGES;
-  uint64_t* s_full = q_empty + BKV_STAGES;  // [B_SBUF] scores landed
-  uint64_t* p_full = s_full + B_SBUF;       // [B_SBUF] P^T / dS^T packed in TMEM
-  uint64_t* pv_done = p_full + B_SBUF;      // [B_SBUF] dV / dK MMAs of the buffer retired
-  uint64_t* done = pv_done + B_SBUF;
+  uint8_t* sK = smem;                            // [KVBUF][NP][128 keys x 64]
+  uint8_t* sV = sK + K::KVBUF * K::KV_BYTES;     // [KVBUF][NP][128 keys x 64]
+  uint8_t* sQ = sV + K::KVBUF * K::KV_BYTES;     // [ST][NP][64 x 64]
+  uint8_t* sG = sQ + K::STAGES * K::Q_BYTES;     // dO [ST][NP][64 x 64]
+  float* sLD = reinterpret_cast<float*>(sG + K::STAGES * K::Q_BYTES);  // [ST][lse 64 | delta 64]
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sLD + K::STAGES * 128);  // [KVBUF]
+  uint64_t* kv_empty = kv_full + K::KVBUF;      // [KVBUF]
+  uint64_t* q_full = kv_empty + K::KVBUF;
+  uint64_t* q_empty = q_full + K::STAGES;
+  uint64_t* s_full = q_empty + K::STAGES;       // [SBUF] scores landed
+  uint64_t* p_full = s_full + K::SBUF;          // [SBUF] P^T / dS^T packed in TMEM
+  uint64_t* pv_done = p_full + K::SBUF;         // [SBUF] dV / dK MMAs of the buffer retired
+  uint64_t* done = pv_done + K::SBUF;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int nkt = (S + B_KEYS - 1) / B_KEYS, nqb = (S + B_Q - 1) / B_Q;
-  const int items = BH * nkt;
-  const int d = H * F_HD;
+  const int H = hs.H, G = hs.G;
+  const int nkt = (S + K::KEYS - 1) / K::KEYS, nqb = (S + K::BQ - 1) / K::BQ;
+  const int BHk = B * hs.Hkv;
+  const int items = BHk * nkt;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tg);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < K::KVBUF; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < BKV_STAGES; ++i) {
+    for (int i = 0; i < K::STAGES; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
-    for (int i = 0; i < B_SBUF; ++i) {
+    for (int i = 0; i < K::SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], BKV_EW);
+      mbar_init(&p_full[i], K::EW);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(done, 1);
@@ -411,91 +459,98 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  // S^T of block i at tmem + 128 (i % B_SBUF), dP^T at + 64; then dV, dK
-  const uint32_t tdV = tmem + 128 * B_SBUF, tdK = tdV + 64;
+  // S^T of block i at tmem + 128 (i % SBUF), dP^T at + 64; then dV, dK
+  const uint32_t tdV = tmem + 128 * K::SBUF, tdK = tdV + HD;
 
-  // tile w -> (batch*head, first key, first query block, query blocks)
-  auto decode = [&](int w, int& bh, int& k0, int& qbeg, int& n) {
-    const int kt = w / BH;  // early key tiles see the most query blocks: first
-    bh = w % BH;
-    k0 = kt * B_KEYS;
-    qbeg = k0 / B_Q;
-    n = nqb - qbeg;
+  // tile w -> (batch, kv head, first key, first query block, query blocks per head)
+  auto decode = [&](int w, int& b, int& hk, int& k0, int& qbeg, int& nq) {
+    const int kt = w / BHk;  // early key tiles see the most query blocks: first
+    const int bhk = w % BHk;
+    b = bhk / hs.Hkv;
+    hk = bhk % hs.Hkv;
+    k0 = kt * K::KEYS;
+    qbeg = k0 / K::BQ;
+    nq = nqb - qbeg;
   };
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t g = 0, ic = 0;
       for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
-        int bh, k0, qbeg, n;
-        decode(w, bh, k0, qbeg, n);
-        const int b = bh / H, h = bh % H, brow = b * S;
-        const int64_t vbase = static_cast<int64_t>(bh) * S;
-        const int kb2 = ic & 1;
-        mbar_wait(&kv_empty[kb2], ((ic >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[kb2], 2 * 16384);
-        for (int hf = 0; hf < 2; ++hf) {
-          tma_load_2d(sK + kb2 * 16384 + hf * 8192, &tq, &kv_full[kb2], d + h * F_HD, brow + k0 + hf * 64);
-          tma_load_2d(sV + kb2 * 16384 + hf * 8192, &tq, &kv_full[kb2], 2 * d + h * F_HD, brow + k0 + hf * 64);
-        }
-        for (int i = 0; i < n; ++i, ++g) {
-          const int st = g % BKV_STAGES;
-          const int m0 = (qbeg + i) * B_Q;
-          const uint32_t lbytes = static_cast<uint32_t>(min(B_Q, S - m0)) * 4;  // S % 4 == 0
-          mbar_wait(&q_empty[st], ((g / BKV_STAGES) & 1) ^ 1);
-          mbar_expect_tx(&q_full[st], 2 * 8192 + 2 * lbytes);
-          tma_load_2d(sQ + st * 8192, &tq, &q_full[st], h * F_HD, brow + m0);
-          tma_load_2d(sG + st * 8192, &tg, &q_full[st], h * F_HD, brow + m0);
+        int b, hk, k0, qbeg, nq;
+        decode(w, b, hk, k0, qbeg, nq);
+        const int brow = b * S;
+        const int kb = ic % K::KVBUF;
+        mbar_wait(&kv_empty[kb], ((ic / K::KVBUF) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[kb], 2 * K::KV_BYTES);
+        for (int p = 0; p < K::NP; ++p)
+          for (int hf = 0; hf < 2; ++hf) {
+            const int off = kb * K::KV_BYTES + p * K::KV_PANEL + hf * (K::KV_PANEL / 2);
+            tma_load_2d(sK + off, &tq, &kv_full[kb], hs.kcol(hk) + 64 * p, brow + k0 + hf * 64);
+            tma_load_2d(sV + off, &tq, &kv_full[kb], hs.vcol(hk) + 64 * p, brow + k0 + hf * 64);
+          }
+        for (int i = 0; i < G * nq; ++i, ++g) {
+          const int h = hk * G + i / nq;
+          const int st = g % K::STAGES;
+          const int m0 = (qbeg + i % nq) * K::BQ;
+          const int64_t vbase = (static_cast<int64_t>(b) * H + h) * S;
+          const uint32_t lbytes = static_cast<uint32_t>(min(K::BQ, S - m0)) * 4;  // S % 4 == 0
+          mbar_wait(&q_empty[st], ((g / K::STAGES) & 1) ^ 1);
+          mbar_expect_tx(&q_full[st], 2 * K::Q_BYTES + 2 * lbytes);
+          for (int p = 0; p < K::NP; ++p) {
+            tma_load_2d(sQ + st * K::Q_BYTES + p * K::Q_PANEL, &tq, &q_full[st], hs.qcol(h) + 64 * p, brow + m0);
+            tma_load_2d(sG + st * K::Q_BYTES + p * K::Q_PANEL, &tg, &q_full[st], hs.qcol(h) + 64 * p, brow + m0);
+          }
           bulk_load(sLD + st * 128, lse + vbase + m0, lbytes, &q_full[st]);
           bulk_load(sLD + st * 128 + 64, delta + vbase + m0, lbytes, &q_full[st]);
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t ID_T = umma_idesc_bf16(128, B_Q, 0, 0);   // K/V x (Q/dO)^T, N = 64 queries
-    constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // P^T/dS^T x (dO/Q), N = 64 dims
-    const uint64_t qd = umma_sdesc_sw128(smem_u32(sQ), 16, 1024);       // K-major view
-    const uint64_t gd = umma_sdesc_sw128(smem_u32(sG), 16, 1024);
-    const uint64_t qn = umma_sdesc_sw128(smem_u32(sQ), 8192, 1024);     // MN-major view
-    const uint64_t gn = umma_sdesc_sw128(smem_u32(sG), 8192, 1024);
+    constexpr uint32_t ID_T = umma_idesc_bf16(128, K::BQ, 0, 0);  // K/V x (Q/dO)^T, N = 64 queries
+    constexpr uint32_t ID_A = umma_idesc_bf16(128, HD, 0, 1);     // P^T/dS^T x (dO/Q), N = HD dims
+    const uint64_t qn = umma_sdesc_sw128(smem_u32(sQ), K::Q_PANEL, 1024);  // MN-major views
+    const uint64_t gn = umma_sdesc_sw128(smem_u32(sG), K::Q_PANEL, 1024);
     uint32_t g0 = 0, ic = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
-      int bh, k0, qbeg, n;
-      decode(w, bh, k0, qbeg, n);
-      const int kb2 = ic & 1;
-      mbar_wait(&kv_full[kb2], (ic >> 1) & 1);
+      int b, hk, k0, qbeg, nq;
+      decode(w, b, hk, k0, qbeg, nq);
+      const int n = G * nq;
+      const int kb = ic % K::KVBUF;
+      mbar_wait(&kv_full[kb], (ic / K::KVBUF) & 1);
       tc_fence_after();
-      const uint64_t kd = umma_sdesc_sw128(smem_u32(sK + kb2 * 16384), 16, 1024);
-      const uint64_t vd = umma_sdesc_sw128(smem_u32(sV + kb2 * 16384), 16, 1024);
+      const uint32_t ka = smem_u32(sK + kb * K::KV_BYTES), va = smem_u32(sV + kb * K::KV_BYTES);
       auto issue_s = [&](uint32_t g) {
-        const int st = g % BKV_STAGES, sb = g % B_SBUF;
-        mbar_wait(&q_full[st], (g / BKV_STAGES) & 1);
+        const int st = g % K::STAGES, sb = g % K::SBUF;
+        mbar_wait(&q_full[st], (g / K::STAGES) & 1);
         // the buffer's previous P^T / dS^T have been read by their MMAs
-        if (g >= B_SBUF) mbar_wait(&pv_done[sb], ((g - B_SBUF) / B_SBUF) & 1);
+        if (g >= K::SBUF) mbar_wait(&pv_done[sb], ((g - K::SBUF) / K::SBUF) & 1);
         tc_fence_after();
-        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint32_t qa = smem_u32(sQ + st * K::Q_BYTES), ga = smem_u32(sG + st * K::Q_BYTES);
         const uint32_t tS = tmem + sb * 128;
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < F_HD / 16; ++k) {
-            tc_mma_f16(tS, kd + 2 * k, qd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
-            tc_mma_f16(tS + 64, vd + 2 * k, gd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          for (int k = 0; k < HD / 16; ++k) {
+            tc_mma_f16(tS, kmajor_step(ka, k, K::KV_PANEL), kmajor_step(qa, k, K::Q_PANEL), ID_T,
+                       k > 0 ? 1u : 0u);
+            tc_mma_f16(tS + 64, kmajor_step(va, k, K::KV_PANEL), kmajor_step(ga, k, K::Q_PANEL), ID_T,
+                       k > 0 ? 1u : 0u);
           }
           tc_commit(&s_full[sb]);
         }
         __syncwarp();
       };
-      for (int i = 0; i < B_SBUF && i < n; ++i) issue_s(g0 + i);
+      for (int i = 0; i < K::SBUF && i < n; ++i) issue_s(g0 + i);
       for (int i = 0; i < n; ++i) {
         const uint32_t g = g0 + i;
-        const int st = g % BKV_STAGES, sb = g % B_SBUF;
-        mbar_wait(&p_full[sb], (g / B_SBUF) & 1);
+        const int st = g % K::STAGES, sb = g % K::SBUF;
+        mbar_wait(&p_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
-        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint64_t so = static_cast<uint64_t>(st * (K::Q_BYTES >> 4));
         const uint32_t tP = tmem + sb * 128;  // P^T chunk k at column 16 k, dS^T at + 64
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < B_Q / 16; ++k) {
+          for (int k = 0; k < K::BQ / 16; ++k) {
             const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
             tc_mma_f16_ts(tdV, tP + 16 * k, gn + so + 128 * k, ID_A, acc);
             tc_mma_f16_ts(tdK, tP + 64 + 16 * k, qn + so + 128 * k, ID_A, acc);
@@ -504,40 +559,42 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
           tc_commit(&q_empty[st]);
         }
         __syncwarp();
-        if (i + B_SBUF < n) issue_s(g + B_SBUF);  // into the buffer block i released
+        if (i + K::SBUF < n) issue_s(g + K::SBUF);  // into the buffer block i released
       }
       if (elect_one()) {
-        tc_commit(&kv_empty[kb2]);  // K / V of this tile no longer read
-        tc_commit(done);            // dV / dK of this tile complete
+        tc_commit(&kv_empty[kb]);  // K / V of this tile no longer read
+        tc_commit(done);           // dV / dK of this tile complete
       }
       __syncwarp();
       g0 += n;
     }
   } else if (warp >= 4) {
-    constexpr int CW = BW_CW;
+    constexpr int CW = BW_CW, CO = HD / BW_NG;
     const int qw = warp & 3;                 // TMEM lane quarter
-    const int cb = ((warp - 4) >> 2) * CW;   // first of this warp's CW queries / head dims
+    const int grp = (warp - 4) >> 2;         // column group
+    const int cb = grp * CW;                 // first of this warp's CW queries
     const int r = qw * 32 + lane;            // key row in the tile
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
     uint32_t g0 = 0, ic = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
-      int bh, k0, qbeg, n;
-      decode(w, bh, k0, qbeg, n);
-      const int b = bh / H, h = bh % H, brow = b * S;
+      int b, hk, k0, qbeg, nq;
+      decode(w, b, hk, k0, qbeg, nq);
+      const int brow = b * S;
       const int key = k0 + r;
+      const int n = G * nq;
       for (int i = 0; i < n; ++i) {
         const uint32_t g = g0 + i;
-        const int st = g % BKV_STAGES, sb = g % B_SBUF;
-        const int m0 = (qbeg + i) * B_Q;
-        mbar_wait(&s_full[sb], (g / B_SBUF) & 1);
+        const int st = g % K::STAGES, sb = g % K::SBUF;
+        const int m0 = (qbeg + i % nq) * K::BQ;
+        mbar_wait(&s_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
         uint32_t sr[CW], pr[CW];
         const uint32_t tS = tmem + sb * 128 + lo + cb;
         tmem_ld_cols<CW>(tS, sr);
         tmem_ld_cols<CW>(tS + 64, pr);
         tc_wait_ld();
-        mbar_wait(&q_full[st], (g / BKV_STAGES) & 1);  // lse / delta rows visible
+        mbar_wait(&q_full[st], (g / K::STAGES) & 1);  // lse / delta rows visible
         const float* Ls = sLD + st * 128 + cb;
         const float* Ds = Ls + 64;
         float pv[CW], dv[CW];
@@ -545,8 +602,8 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
         for (int gi = 0; gi < CW / 4; ++gi) {
           const float4 l4 = reinterpret_cast<const float4*>(Ls)[gi];
           const float4 d4 = reinterpret_cast<const float4*>(Ds)[gi];
-          const uint64_t nl01 = pack_f2(-l4.x * 1.4426950408889634f, -l4.y * 1.4426950408889634f);
-          const uint64_t nl23 = pack_f2(-l4.z * 1.4426950408889634f, -l4.w * 1.4426950408889634f);
+          const uint64_t nl01 = pack_f2(-l4.x * F_LOG2E, -l4.y * F_LOG2E);
+          const uint64_t nl23 = pack_f2(-l4.z * F_LOG2E, -l4.w * F_LOG2E);
           float a0, a1, a2, a3;
           unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * gi]), __uint_as_float(sr[4 * gi + 1])), sc2, nl01), a0, a1);
           unpack_f2(ffma2(pack_f2(__uint_as_float(sr[4 * gi + 2]), __uint_as_float(sr[4 * gi + 3])), sc2, nl23), a2, a3);
@@ -587,14 +644,14 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
       }
       mbar_wait(done, ic & 1);
       tc_fence_after();
-      uint32_t acc[CW];
-      bf16* base = dqkv + static_cast<int64_t>(brow + key) * ldd + h * F_HD + cb;
-      tmem_ld_cols<CW>(tdV + lo + cb, acc);
+      uint32_t acc[CO];
+      const int64_t rowoff = static_cast<int64_t>(brow + key) * ldd + grp * CO;
+      tmem_ld_cols<CO>(tdV + lo + grp * CO, acc);
       tc_wait_ld();
-      if (key < S) store_row_chunks<CW / 8>(base + 2 * d, acc, 1.f);
-      tmem_ld_cols<CW>(tdK + lo + cb, acc);
+      if (key < S) store_row_chunks<CO / 8>(dqkv + rowoff + hs.vcol(hk), acc, 1.f);
+      tmem_ld_cols<CO>(tdK + lo + grp * CO, acc);
       tc_wait_ld();
-      if (key < S) store_row_chunks<CW / 8>(base + d, acc, scale);
+      if (key < S) store_row_chunks<CO / 8>(dqkv + rowoff + hs.kcol(hk), acc, scale);
       g0 += n;
     }
   }
@@ -605,23 +662,34 @@ __global__ void __launch_bounds__(BKV_THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-constexpr int BQ_STAGES = 5, BQ_EW = 4 * BW_NG, BQ_THREADS = 128 + 32 * BQ_EW;
-constexpr int BQ_SMEM = 2 * 3 * 16384 /*Q,dO,O x2*/ + BQ_STAGES * 2 * 8192 /*K,V*/ +
-                        128 * BW_NG * 4 /*delta partials*/ + 1024 + 256;
+template <int HD>
+struct BwdQ {
+  static constexpr int BM = 128, BN = 64;
+  static constexpr int NP = HD / 64;
+  static constexpr int SBUF = 3;
+  static constexpr int STAGES = HD == 64 ? 5 : 3;
+  static constexpr int QBUF = HD == 64 ? 2 : 1;
+  static constexpr int Q_PANEL = BM * 64 * 2;     // 16 KB
+  static constexpr int Q_BYTES = NP * Q_PANEL;    // one of Q / dO / O
+  static constexpr int KV_PANEL = BN * 64 * 2;    // 8 KB
+  static constexpr int KV_BYTES = NP * KV_PANEL;  // one of K / V per stage
+  static constexpr int EW = 4 * BW_NG, THREADS = 128 + 32 * EW;
+  static constexpr int SMEM = QBUF * 3 * Q_BYTES + STAGES * 2 * KV_BYTES + 128 * BW_NG * 4 + 1024 + 256;
+};
 
-// 16 B chunk j (8 bf16) of row r in a [128 x 64] bf16 tile loaded as two
-// 128B-swizzled 64-row TMA boxes.
+// 16 B chunk j (8 bf16, j < HD / 8) of row r in a [128 x HD] tile stored as
+// 64-column panels, each loaded as two 128B-swizzled 64-row TMA boxes.
 __device__ __forceinline__ uint4 ld_chunk128(const uint8_t* tile, int r, int j) {
-  return *reinterpret_cast<const uint4*>(tile + (r >> 6) * 8192 + (r & 63) * 128 + ((j ^ (r & 7)) << 4));
+  return *reinterpret_cast<const uint4*>(tile + (j >> 3) * 16384 + (r >> 6) * 8192 + (r & 63) * 128 +
+                                         (((j & 7) ^ (r & 7)) << 4));
 }
 
 // dQ for 128-query tiles of one (batch, head), persistent: one CTA per SM
 // walks the tiles longest-first (tile w: query tile nqt-1 - w/BH, head w%BH).
 // Also produces delta = rowsum(dO o O) for its rows (consumed by the dK/dV
-// kernel that runs next).  12 + 4 warps:
-//   warp 0      TMA producer: Q, dO, O of a tile into one of two buffers (the
-//               next tile's are prefetched while this one computes), K/V
-//               blocks of 64 keys through a 5-deep ring
+// kernel that runs next).  4 + 16 warps:
+//   warp 0      TMA producer: Q, dO, O of a tile into one of QBUF buffers,
+//               K/V blocks of 64 keys (the head's kv head) through a ring
 //   warp 1      MMA issuer, up to three key blocks ahead of the elementwise
 //               warps: S_j = Q K_j^T, dP_j = dO V_j^T -> TMEM buffer j % 3,
 //               dQ += dS_j K_j -> TMEM accumulator
@@ -632,51 +700,53 @@ __device__ __forceinline__ uint4 ld_chunk128(const uint8_t* tile, int r, int j) 
 //               over their own score columns: the dQ MMA reads A from TMEM
 // Ring / buffer phases run on tile-global block counters, so a tile's first
 // blocks reuse buffers the previous tile released.
-__global__ void __launch_bounds__(BQ_THREADS, 1)
+template <int HD>
+__global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
     fa_bwd_dq_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                   const __grid_constant__ CUtensorMap to, const float* __restrict__ lse,
-                  float* __restrict__ delta, bf16* __restrict__ dqkv, int64_t ldd, int BH, int H,
+                  float* __restrict__ delta, bf16* __restrict__ dqkv, int64_t ldd, int BH, Heads hs,
                   int S, float sl2, float scale) {
+  using K = BwdQ<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sQ = smem;                      // [2][128 x 64]
-  uint8_t* sG = sQ + 2 * 16384;            // dO [2][128 x 64]
-  uint8_t* sO = sG + 2 * 16384;            // O  [2][128 x 64]
-  uint8_t* sK = sO + 2 * 16384;            // [ST][64 x 64]
-  uint8_t* sV = sK + BQ_STAGES * 8192;     // [ST][64 x 64]
-  float* sDelta = reinterpret_cast<float*>(sV + BQ_STAGES * 8192);  // [BW_NG][128] row partials
-  uint64_t* q_full = reinterpret_cast<uint64_t*>(sDelta + 128 * BW_NG);  // [2]
-  uint64_t* q_empty = q_full + 2;           // [2]
-  uint64_t* kv_full = q_empty + 2;
-  uint64_t* kv_empty = kv_full + BQ_STAGES;
-  uint64_t* s_full = kv_empty + BQ_STAGES;  // [B_SBUF] scores landed
-  uint64_t* p_full = s_full + B_SBUF;       // [B_SBUF] dS packed in TMEM
-  uint64_t* pv_done = p_full + B_SBUF;      // [B_SBUF] dQ MMAs of the buffer retired
-  uint64_t* done = pv_done + B_SBUF;
+  uint8_t* sQ = smem;                              // [QBUF][NP][128 x 64]
+  uint8_t* sG = sQ + K::QBUF * K::Q_BYTES;         // dO
+  uint8_t* sO = sG + K::QBUF * K::Q_BYTES;         // O
+  uint8_t* sK = sO + K::QBUF * K::Q_BYTES;         // [ST][NP][64 x 64]
+  uint8_t* sV = sK + K::STAGES * K::KV_BYTES;      // [ST][NP][64 x 64]
+  float* sDelta = reinterpret_cast<float*>(sV + K::STAGES * K::KV_BYTES);  // [BW_NG][128] row partials
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sDelta + 128 * BW_NG);  // [QBUF]
+  uint64_t* q_empty = q_full + K::QBUF;         // [QBUF]
+  uint64_t* kv_full = q_empty + K::QBUF;
+  uint64_t* kv_empty = kv_full + K::STAGES;
+  uint64_t* s_full = kv_empty + K::STAGES;  // [SBUF] scores landed
+  uint64_t* p_full = s_full + K::SBUF;      // [SBUF] dS packed in TMEM
+  uint64_t* pv_done = p_full + K::SBUF;     // [SBUF] dQ MMAs of the buffer retired
+  uint64_t* done = pv_done + K::SBUF;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int nqt = (S + F_BM - 1) / F_BM;
+  const int H = hs.H;
+  const int nqt = (S + K::BM - 1) / K::BM;
   const int items = BH * nqt;
-  const int d = H * F_HD;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tg);
     tma_prefetch_desc(&to);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < K::QBUF; ++i) {
       mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1 + BQ_EW);  // MMA warp (Q, dO) + elementwise warps (O, dO)
+      mbar_init(&q_empty[i], 1 + K::EW);  // MMA warp (Q, dO) + elementwise warps (O, dO)
     }
-    for (int i = 0; i < BQ_STAGES; ++i) {
+    for (int i = 0; i < K::STAGES; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < B_SBUF; ++i) {
+    for (int i = 0; i < K::SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], BQ_EW);
+      mbar_init(&p_full[i], K::EW);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(done, 1);
@@ -687,14 +757,14 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tdQ = tmem + 128 * B_SBUF;  // S_j at tmem + 128 (j % B_SBUF), dP_j at + 64
+  const uint32_t tdQ = tmem + 128 * K::SBUF;  // S_j at tmem + 128 (j % SBUF), dP_j at + 64
 
   // tile w -> (batch*head, first query row, key blocks)
   auto decode = [&](int w, int& bh, int& q0, int& nkb) {
     const int qt = nqt - 1 - w / BH;
     bh = w % BH;
-    q0 = qt * F_BM;
-    nkb = (min(S, q0 + F_BM) + F_BN - 1) / F_BN;
+    q0 = qt * K::BM;
+    nkb = (min(S, q0 + K::BM) + K::BN - 1) / K::BN;
   };
 
   if (warp == 0) {
@@ -703,74 +773,80 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
         int bh, q0, nkb;
         decode(w, bh, q0, nkb);
-        const int b = bh / H, h = bh % H, brow = b * S;
-        const int qb = ic & 1;
-        mbar_wait(&q_empty[qb], ((ic >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[qb], 3 * 16384);
-        for (int hf = 0; hf < 2; ++hf) {
-          tma_load_2d(sQ + qb * 16384 + hf * 8192, &tq, &q_full[qb], h * F_HD, brow + q0 + hf * 64);
-          tma_load_2d(sG + qb * 16384 + hf * 8192, &tg, &q_full[qb], h * F_HD, brow + q0 + hf * 64);
-          tma_load_2d(sO + qb * 16384 + hf * 8192, &to, &q_full[qb], h * F_HD, brow + q0 + hf * 64);
-        }
+        const int b = bh / H, h = bh % H, hk = h / hs.G, brow = b * S;
+        const int qb = ic % K::QBUF;
+        mbar_wait(&q_empty[qb], ((ic / K::QBUF) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qb], 3 * K::Q_BYTES);
+        for (int p = 0; p < K::NP; ++p)
+          for (int hf = 0; hf < 2; ++hf) {
+            const int off = qb * K::Q_BYTES + p * K::Q_PANEL + hf * (K::Q_PANEL / 2);
+            const int x = hs.qcol(h) + 64 * p, y = brow + q0 + hf * 64;
+            tma_load_2d(sQ + off, &tq, &q_full[qb], x, y);
+            tma_load_2d(sG + off, &tg, &q_full[qb], x, y);
+            tma_load_2d(sO + off, &to, &q_full[qb], x, y);
+          }
         for (int j = 0; j < nkb; ++j, ++g) {
-          const int st = g % BQ_STAGES;
-          mbar_wait(&kv_empty[st], ((g / BQ_STAGES) & 1) ^ 1);
-          mbar_expect_tx(&kv_full[st], 2 * 8192);
-          tma_load_2d(sK + st * 8192, &tq, &kv_full[st], d + h * F_HD, brow + j * F_BN);
-          tma_load_2d(sV + st * 8192, &tq, &kv_full[st], 2 * d + h * F_HD, brow + j * F_BN);
+          const int st = g % K::STAGES;
+          mbar_wait(&kv_empty[st], ((g / K::STAGES) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * K::KV_BYTES);
+          for (int p = 0; p < K::NP; ++p) {
+            tma_load_2d(sK + st * K::KV_BYTES + p * K::KV_PANEL, &tq, &kv_full[st],
+                        hs.kcol(hk) + 64 * p, brow + j * K::BN);
+            tma_load_2d(sV + st * K::KV_BYTES + p * K::KV_PANEL, &tq, &kv_full[st],
+                        hs.vcol(hk) + 64 * p, brow + j * K::BN);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t ID_T = umma_idesc_bf16(128, F_BN, 0, 0);  // Q/dO x (K/V)^T
-    constexpr uint32_t ID_A = umma_idesc_bf16(128, F_HD, 0, 1);  // dS x K (MN-major)
-    const uint64_t kd = umma_sdesc_sw128(smem_u32(sK), 16, 1024);     // K-major view
-    const uint64_t vd = umma_sdesc_sw128(smem_u32(sV), 16, 1024);
-    const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), 8192, 1024);   // MN-major view
+    constexpr uint32_t ID_T = umma_idesc_bf16(128, K::BN, 0, 0);  // Q/dO x (K/V)^T
+    constexpr uint32_t ID_A = umma_idesc_bf16(128, HD, 0, 1);     // dS x K (MN-major)
+    const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), K::KV_PANEL, 1024);   // MN-major view
     uint32_t g0 = 0, ic = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
       int bh, q0, nkb;
       decode(w, bh, q0, nkb);
-      const int qb = ic & 1;
-      mbar_wait(&q_full[qb], (ic >> 1) & 1);
+      const int qb = ic % K::QBUF;
+      mbar_wait(&q_full[qb], (ic / K::QBUF) & 1);
       tc_fence_after();
-      const uint64_t qd = umma_sdesc_sw128(smem_u32(sQ + qb * 16384), 16, 1024);
-      const uint64_t gd = umma_sdesc_sw128(smem_u32(sG + qb * 16384), 16, 1024);
+      const uint32_t qa = smem_u32(sQ + qb * K::Q_BYTES), ga = smem_u32(sG + qb * K::Q_BYTES);
       auto issue_s = [&](uint32_t g) {
-        const int st = g % BQ_STAGES, sb = g % B_SBUF;
-        mbar_wait(&kv_full[st], (g / BQ_STAGES) & 1);
+        const int st = g % K::STAGES, sb = g % K::SBUF;
+        mbar_wait(&kv_full[st], (g / K::STAGES) & 1);
         // the buffer's previous dS has been read by its dQ MMAs
-        if (g >= B_SBUF) mbar_wait(&pv_done[sb], ((g - B_SBUF) / B_SBUF) & 1);
+        if (g >= K::SBUF) mbar_wait(&pv_done[sb], ((g - K::SBUF) / K::SBUF) & 1);
         tc_fence_after();
-        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint32_t ka = smem_u32(sK + st * K::KV_BYTES), va = smem_u32(sV + st * K::KV_BYTES);
         const uint32_t tS = tmem + sb * 128;
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < F_HD / 16; ++k) {
-            tc_mma_f16(tS, qd + 2 * k, kd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
-            tc_mma_f16(tS + 64, gd + 2 * k, vd + so + 2 * k, ID_T, k > 0 ? 1u : 0u);
+          for (int k = 0; k < HD / 16; ++k) {
+            tc_mma_f16(tS, kmajor_step(qa, k, K::Q_PANEL), kmajor_step(ka, k, K::KV_PANEL), ID_T,
+                       k > 0 ? 1u : 0u);
+            tc_mma_f16(tS + 64, kmajor_step(ga, k, K::Q_PANEL), kmajor_step(va, k, K::KV_PANEL), ID_T,
+                       k > 0 ? 1u : 0u);
           }
           tc_commit(&s_full[sb]);
         }
         __syncwarp();
       };
-      for (int j = 0; j < B_SBUF && j < nkb; ++j) issue_s(g0 + j);
+      for (int j = 0; j < K::SBUF && j < nkb; ++j) issue_s(g0 + j);
       for (int j = 0; j < nkb; ++j) {
         const uint32_t g = g0 + j;
-        const int st = g % BQ_STAGES, sb = g % B_SBUF;
-        mbar_wait(&p_full[sb], (g / B_SBUF) & 1);
+        const int st = g % K::STAGES, sb = g % K::SBUF;
+        mbar_wait(&p_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
-        const uint64_t so = static_cast<uint64_t>(st * (8192 >> 4));
+        const uint64_t so = static_cast<uint64_t>(st * (K::KV_BYTES >> 4));
         const uint32_t tD = tmem + sb * 128;  // dS key chunk k at column 16 k
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < F_BN / 16; ++k)
+          for (int k = 0; k < K::BN / 16; ++k)
             tc_mma_f16_ts(tdQ, tD + 16 * k, kn + so + 128 * k, ID_A, (j > 0 || k > 0) ? 1u : 0u);
           tc_commit(&pv_done[sb]);
           tc_commit(&kv_empty[st]);
         }
         __syncwarp();
-        if (j + B_SBUF < nkb) issue_s(g + B_SBUF);  // into the buffer block j released
+        if (j + K::SBUF < nkb) issue_s(g + K::SBUF);  // into the buffer block j released
       }
       if (elect_one()) {
         tc_commit(&q_empty[qb]);  // Q / dO of this tile no longer read by MMAs
@@ -780,10 +856,10 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       g0 += nkb;
     }
   } else if (warp >= 4) {
-    constexpr int CW = BW_CW;
+    constexpr int CW = BW_CW, CO = HD / BW_NG;
     const int qw = warp & 3;               // TMEM lane quarter
     const int grp = (warp - 4) >> 2;       // column group
-    const int cb = grp * CW;               // first of this warp's CW keys / head dims
+    const int cb = grp * CW;               // first of this warp's CW keys
     const int r = qw * 32 + lane;          // query row in the tile
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
@@ -794,14 +870,14 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       const int b = bh / H, h = bh % H, brow = b * S;
       const int row = q0 + r;
       const int64_t vrow = static_cast<int64_t>(bh) * S + row;
-      const int qb = ic & 1;
-      // delta = rowsum(dO o O): each column group sums CW head dims, fixed-order combine
-      mbar_wait(&q_full[qb], (ic >> 1) & 1);
+      const int qb = ic % K::QBUF;
+      // delta = rowsum(dO o O): each column group sums CO head dims, fixed-order combine
+      mbar_wait(&q_full[qb], (ic / K::QBUF) & 1);
       float part = 0.f;
 #pragma unroll
-      for (int jj = 0; jj < CW / 8; ++jj) {
-        const uint4 ov = ld_chunk128(sO + qb * 16384, r, cb / 8 + jj);
-        const uint4 gv = ld_chunk128(sG + qb * 16384, r, cb / 8 + jj);
+      for (int jj = 0; jj < CO / 8; ++jj) {
+        const uint4 ov = ld_chunk128(sO + qb * K::Q_BYTES, r, grp * (CO / 8) + jj);
+        const uint4 gv = ld_chunk128(sG + qb * K::Q_BYTES, r, grp * (CO / 8) + jj);
         const __nv_bfloat162* oh = reinterpret_cast<const __nv_bfloat162*>(&ov);
         const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gv);
 #pragma unroll
@@ -812,20 +888,20 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
         }
       }
       sDelta[grp * 128 + r] = part;
-      asm volatile("bar.sync 1, %0;" ::"n"(BQ_EW * 32) : "memory");  // elementwise warps only
+      asm volatile("bar.sync 1, %0;" ::"n"(K::EW * 32) : "memory");  // elementwise warps only
       float dl = 0.f;
 #pragma unroll
       for (int gi = 0; gi < BW_NG; ++gi) dl += sDelta[gi * 128 + r];
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_empty[qb]);  // O / dO no longer read here
       if (grp == 0 && row < S) delta[vrow] = dl;
-      const float nl2 = row < S ? -lse[vrow] * 1.4426950408889634f : 0.f;
+      const float nl2 = row < S ? -lse[vrow] * F_LOG2E : 0.f;
       const uint64_t nl22 = pack_f2(nl2, nl2), nd2 = pack_f2(-dl, -dl);
       for (int j = 0; j < nkb; ++j) {
         const uint32_t g = g0 + j;
-        const int sb = g % B_SBUF;
-        const int n0 = j * F_BN;
-        mbar_wait(&s_full[sb], (g / B_SBUF) & 1);
+        const int sb = g % K::SBUF;
+        const int n0 = j * K::BN;
+        mbar_wait(&s_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
         uint32_t sr[CW], pr[CW];
         const uint32_t tS = tmem + sb * 128 + lo + cb;
@@ -863,11 +939,12 @@ __global__ void __launch_bounds__(BQ_THREADS, 1)
       }
       mbar_wait(done, ic & 1);
       tc_fence_after();
-      uint32_t acc[CW];
-      tmem_ld_cols<CW>(tdQ + lo + cb, acc);
+      uint32_t acc[CO];
+      tmem_ld_cols<CO>(tdQ + lo + grp * CO, acc);
       tc_wait_ld();
       if (row < S)
-        store_row_chunks<CW / 8>(dqkv + static_cast<int64_t>(brow + row) * ldd + h * F_HD + cb, acc, scale);
+        store_row_chunks<CO / 8>(dqkv + static_cast<int64_t>(brow + row) * ldd + hs.qcol(h) + grp * CO,
+                                 acc, scale);
       g0 += nkb;
     }
   }
@@ -897,49 +974,30 @@ int make_tmap_rows64(CUtensorMap* m, const void* base, int64_t ld, int64_t rows)
   }
   return PC_OK;
 }
-}  // namespace
 
-bool attention_tc5_supported(int hd, int64_t ld_qkv, int64_t ld_o, const void* qkv, const void* o) {
-  return hd == F_HD && (ld_qkv * 2) % 16 == 0 && (ld_o * 2) % 16 == 0 &&
-         (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0;
-}
-
-int attention_fwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, void* o, int64_t ld_o,
-                      float* lse, cudaStream_t st) {
-  auto enc = tmap_encoder_fn();
-  if (!enc) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return PC_ERR_CUDA;
-  }
+template <int HD>
+int fwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, void* o, int64_t ld_o,
+               float* lse, cudaStream_t st) {
   CUtensorMap tm;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld_qkv), static_cast<cuuint64_t>(B) * S};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_qkv * 2)};
-  cuuint32_t box[2] = {64u, 64u};
-  cuuint32_t es[2] = {1u, 1u};
-  CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides,
-                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled (attention) failed (%d)", static_cast<int>(r));
-    return PC_ERR_CUDA;
-  }
+  int rc = make_tmap_rows64(&tm, qkv, ld_qkv, static_cast<int64_t>(B) * S);
+  if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM));
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd_tc5<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fwd<HD>::SMEM));
     attr = true;
   }
-  dim3 grid(B * H, (S + F_BM - 1) / F_BM);
-  const float sl2 = 1.4426950408889634f / sqrtf(static_cast<float>(F_HD));
-  fa_fwd_tc5<<<grid, F_THREADS, F_SMEM, st>>>(tm, static_cast<bf16*>(o), ld_o, lse, H, S, sl2);
+  dim3 grid(B * hs.H, (S + Fwd<HD>::BM - 1) / Fwd<HD>::BM);
+  const float sl2 = F_LOG2E / sqrtf(static_cast<float>(HD));
+  fa_fwd_tc5<HD><<<grid, Fwd<HD>::THREADS, Fwd<HD>::SMEM, st>>>(tm, static_cast<bf16*>(o), ld_o, lse,
+                                                               hs, S, sl2);
   return check_launch("fa_fwd_tc5");
 }
 
-}  // namespace pp200
-
-namespace pp200 {
-int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, const void* o,
-                      const void* dO, int64_t ld_o, const float* lse, float* delta, void* dqkv,
-                      int64_t ld_dqkv, cudaStream_t st) {
+template <int HD>
+int bwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, const void* o,
+               const void* dO, int64_t ld_o, const float* lse, float* delta, void* dqkv,
+               int64_t ld_dqkv, cudaStream_t st) {
   CUtensorMap tq, tg, to;
   int rc = make_tmap_rows64(&tq, qkv, ld_qkv, static_cast<int64_t>(B) * S);
   if (rc) return rc;
@@ -949,24 +1007,50 @@ int attention_bwd_tc5(int B, int H, int S, const void* qkv, int64_t ld_qkv, cons
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dkdv_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, BKV_SMEM));
-    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dq_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, BQ_SMEM));
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dkdv_tc5<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     BwdKV<HD>::SMEM));
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dq_tc5<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     BwdQ<HD>::SMEM));
     attr = true;
   }
-  const float scale = 1.f / sqrtf(static_cast<float>(F_HD));
-  const float sl2 = scale * 1.4426950408889634f;
-  // dQ first: it also writes delta = rowsum(dO o O), which dK/dV consume
-  // persistent: one CTA per SM over the (query tile, head) work list
-  const int dq_items = B * H * ((S + F_BM - 1) / F_BM);
+  const float scale = 1.f / sqrtf(static_cast<float>(HD));
+  const float sl2 = scale * F_LOG2E;
+  // dQ first: it also writes delta = rowsum(dO o O), which dK/dV consume.
+  // Both persistent: one CTA per SM over their work lists.
+  const int dq_items = B * hs.H * ((S + BwdQ<HD>::BM - 1) / BwdQ<HD>::BM);
   const int g2 = dq_items < num_sms() ? dq_items : num_sms();
-  fa_bwd_dq_tc5<<<g2, BQ_THREADS, BQ_SMEM, st>>>(tq, tg, to, lse, delta, static_cast<bf16*>(dqkv),
-                                                  ld_dqkv, B * H, H, S, sl2, scale);
+  fa_bwd_dq_tc5<HD><<<g2, BwdQ<HD>::THREADS, BwdQ<HD>::SMEM, st>>>(
+      tq, tg, to, lse, delta, static_cast<bf16*>(dqkv), ld_dqkv, B * hs.H, hs, S, sl2, scale);
   rc = check_launch("fa_bwd_dq_tc5");
   if (rc) return rc;
-  const int kv_items = B * H * ((S + B_KEYS - 1) / B_KEYS);
+  const int kv_items = B * hs.Hkv * ((S + BwdKV<HD>::KEYS - 1) / BwdKV<HD>::KEYS);
   const int g1 = kv_items < num_sms() ? kv_items : num_sms();
-  fa_bwd_dkdv_tc5<<<g1, BKV_THREADS, BKV_SMEM, st>>>(tq, tg, lse, delta, static_cast<bf16*>(dqkv),
-                                                      ld_dqkv, B * H, H, S, sl2, scale);
+  fa_bwd_dkdv_tc5<HD><<<g1, BwdKV<HD>::THREADS, BwdKV<HD>::SMEM, st>>>(
+      tq, tg, lse, delta, static_cast<bf16*>(dqkv), ld_dqkv, B, hs, S, sl2, scale);
   return check_launch("fa_bwd_dkdv_tc5");
 }
+}  // namespace
+
+bool attention_tc5_supported(int hd, int H, int Hkv, int64_t ld_qkv, int64_t ld_o, const void* qkv,
+                             const void* o) {
+  return (hd == 64 || hd == 128) && Hkv > 0 && H % Hkv == 0 && (ld_qkv * 2) % 16 == 0 &&
+         (ld_o * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+}
+
+int attention_fwd_tc5(int B, int H, int Hkv, int S, int hd, const void* qkv, int64_t ld_qkv, void* o,
+                      int64_t ld_o, float* lse, cudaStream_t st) {
+  const Heads hs{H, Hkv, H / Hkv, hd};
+  return hd == 64 ? fwd_launch<64>(B, S, hs, qkv, ld_qkv, o, ld_o, lse, st)
+                  : fwd_launch<128>(B, S, hs, qkv, ld_qkv, o, ld_o, lse, st);
+}
+
+int attention_bwd_tc5(int B, int H, int Hkv, int S, int hd, const void* qkv, int64_t ld_qkv,
+                      const void* o, const void* dO, int64_t ld_o, const float* lse, float* delta,
+                      void* dqkv, int64_t ld_dqkv, cudaStream_t st) {
+  const Heads hs{H, Hkv, H / Hkv, hd};
+  return hd == 64 ? bwd_launch<64>(B, S, hs, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv, st)
+                  : bwd_launch<128>(B, S, hs, qkv, ld_qkv, o, dO, ld_o, lse, delta, dqkv, ld_dqkv, st);
+}
+
 }  // namespace pp200

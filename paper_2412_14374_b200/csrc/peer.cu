@@ -134,3 +134,24 @@ extern "C" int pc_graph_kernel_nodes(void* graph, int64_t* n) {
   *n = 0;
   return count_kernel_nodes(static_cast<CUgraph>(graph), n);
 }
+
+// Abort support for the peer transport: set n flag words at `flags` to `value`
+// from a stream that is not blocked (the caller passes a fresh one).  A
+// receiver whose stream is parked in cuStreamWaitValue32 on a flag the sender
+// never wrote (dropped SendStart, dead peer) is released and drains; each
+// released wait re-arms its own flag to 0 as in a normal step.
+using MemsetFn = CUresult (*)(CUdeviceptr, unsigned int, size_t, CUstream);
+
+extern "C" int pc_peer_release(void* flags, int64_t n, uint32_t value, void* stream) {
+  PP_CHECK_ARG(flags && n >= 0, "peer_release: bad args");
+  if (n == 0) return PC_OK;
+  static MemsetFn fn = driver_fn<MemsetFn>("cuMemsetD32Async");
+  PP_CHECK_ARG(fn != nullptr, "cuMemsetD32Async unavailable");
+  CUresult r = fn(reinterpret_cast<CUdeviceptr>(flags), value, static_cast<size_t>(n),
+                  static_cast<CUstream>(stream));
+  if (r != CUDA_SUCCESS) {
+    set_error("cuMemsetD32Async failed (%d)", static_cast<int>(r));
+    return PC_ERR_CUDA;
+  }
+  return PC_OK;
+}

@@ -893,6 +893,13 @@ class DeviceOps:
              rstd.data_ptr(), RMS_EPS, self.st)
         return y, rstd
 
+    def _native_gqa(self) -> bool:
+        """Grouped-query heads go straight to the tcgen05 attention kernels (bf16,
+        head_dim 64 / 128); other modes expand K/V heads (pc_gqa_kv)."""
+        cfg = self.gpt
+        return (self.mode.act == torch.bfloat16 and cfg.head_dim in (64, 128)
+                and cfg.seq_len % 4 == 0)
+
     def _llama_block_fwd(self, op, env):
         """oracle/llama.py block_fwd: RMSNorm -> qkv GEMM -> RoPE(q, k) ->
         GQA causal attention -> o GEMM (+h) -> RMSNorm -> gate/up GEMM ->
@@ -917,16 +924,20 @@ class DeviceOps:
         self._gemm(act, 0, 1, T, qw, d, a, d, sl("w_qkv"), d, qkv, qw)
         call("pc_rope", self.mode.pc_act, T, H + Hkv, hd, qkv.data_ptr(), qw, pos.data_ptr(),
              float(cfg.rope_theta), 0, self.st)
-        if Hkv != H:  # grouped-query: expand K/V heads for the attention kernels
+        if Hkv != H and not self._native_gqa():
+            # grouped-query heads outside the tcgen05 kernels (fp32 parity mode):
+            # expand K/V heads for the multi-head kernels
             qkv_att = self.empty((T, 3 * H * hd), act)
             call("pc_gqa_kv", self.mode.pc_act, T, H, Hkv, hd, qkv.data_ptr(), qw,
                  qkv_att.data_ptr(), 3 * H * hd, 0, self.st)
-        else:
-            qkv_att = qkv
+            Hk_att = H
+        else:   # native: the kernels address kv head h / (H / Hkv) in qkv itself
+            qkv_att, Hk_att = qkv, Hkv
         o = self.empty((T, H * hd), act)
         lse = self.empty((cfg.microbatch_size * H * cfg.seq_len,), torch.float32)
-        call("pc_attention_fwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len, hd,
-             qkv_att.data_ptr(), 3 * H * hd, o.data_ptr(), H * hd, lse.data_ptr(), self.st)
+        call("pc_attention_gqa_fwd", self.mode.pc_act, cfg.microbatch_size, H, Hk_att,
+             cfg.seq_len, hd, qkv_att.data_ptr(), qkv_att.shape[1], o.data_ptr(), H * hd,
+             lse.data_ptr(), self.st)
         h1 = self.empty((T, d), act)
         self._gemm(act, 0, 1, T, d, H * hd, o, H * hd, sl("w_o"), H * hd, h1, d,
                    _lib.EPI_RESIDUAL, aux=h, ldaux=d)
@@ -1004,14 +1015,17 @@ class DeviceOps:
         do = self.empty((T, H * hd), act)
         tb, B, ldb = wB("w_o")
         self._gemm(act, 0, tb, T, H * hd, d, dh1, d, B, ldb, do, H * hd)
-        dqkv_att = self.empty((T, 3 * H * hd), act)
+        qkv_att = sv["qkv_att"]
+        ld_att = qkv_att.shape[1]
+        Hk_att = Hkv if ld_att == qw else H
+        dqkv_att = self.empty((T, ld_att), act)
         delta = self.empty((cfg.microbatch_size * H * cfg.seq_len,), f32)
-        call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len, hd,
-             sv["qkv_att"].data_ptr(), 3 * H * hd, sv["o"].data_ptr(), do.data_ptr(), H * hd,
-             sv["lse"].data_ptr(), delta.data_ptr(), dqkv_att.data_ptr(), 3 * H * hd, self.st)
-        if Hkv != H:  # sum each kv head's group of query-head gradients
+        call("pc_attention_gqa_bwd", self.mode.pc_act, cfg.microbatch_size, H, Hk_att,
+             cfg.seq_len, hd, qkv_att.data_ptr(), ld_att, sv["o"].data_ptr(), do.data_ptr(),
+             H * hd, sv["lse"].data_ptr(), delta.data_ptr(), dqkv_att.data_ptr(), ld_att, self.st)
+        if ld_att != qw:  # expanded heads: sum each kv head's group of query-head gradients
             dqkv = self.empty((T, qw), act)
-            call("pc_gqa_kv", self.mode.pc_act, T, H, Hkv, hd, dqkv_att.data_ptr(), 3 * H * hd,
+            call("pc_gqa_kv", self.mode.pc_act, T, H, Hkv, hd, dqkv_att.data_ptr(), ld_att,
                  dqkv.data_ptr(), qw, 1, self.st)
         else:
             dqkv = dqkv_att

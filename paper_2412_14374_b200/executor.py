@@ -356,9 +356,10 @@ class PeerChannel:
     last gradient from the receiver).  Reference Channel: executor.py:201-254.
     """
 
-    def __init__(self, src: int, dst: int, me: int, base: int, bids, slots):
+    def __init__(self, src: int, dst: int, me: int, base: int, bids, slots, device=None):
         self.src, self.dst, self.me = src, dst, me
         self.base, self.bids, self.slots = base, list(bids), slots
+        self.device = device
         self.reset()
 
     def reset(self):
@@ -414,7 +415,16 @@ class PeerChannel:
         return True
 
     def abort(self):
-        pass
+        """Release this receiver's stream: set every flag word of the channel
+        from a fresh (unblocked) stream, so waits on messages that will never
+        arrive pass and the device drains (the data read is garbage; the step
+        is failing).  The sender side holds no waits on this channel."""
+        if self.me != self.dst or self.device is None:
+            return
+        with torch.cuda.device(self.device):
+            s = torch.cuda.Stream(device=self.device)
+            _lib.call("pc_peer_release", self.base, len(self.bids), 1, s.cuda_stream)
+            s.synchronize()
 
 
 # ---------------------------------------------------------------------------
@@ -435,10 +445,34 @@ class DeviceStore:
         self.received: set[str] = set()
         self._stash_stage = {bid: b.meta["stage"] for bid, b in tg.buffers.items()
                              if b.kind == STASH}
+        # running stash totals, updated on put / removal (not re-walked per put)
+        self._stash_nbytes: dict[str, int] = {}
+        self._stash_total = 0
+        self._stash_count: dict[int, int] = {}
 
     def put(self, bid: str, value):
+        if bid in self.data:
+            self._forget(bid)
         self.data[bid] = value
-        self._track()
+        st = self._stash_stage.get(bid)
+        if st is not None:
+            nb = _stash_bytes(value)
+            self._stash_nbytes[bid] = nb
+            self._stash_total += nb
+            self._stash_count[st] = self._stash_count.get(st, 0) + 1
+        self._track(st)
+
+    def _forget(self, bid: str):
+        """Remove bid from the running stash totals (before it leaves data)."""
+        nb = self._stash_nbytes.pop(bid, None)
+        if nb is not None:
+            self._stash_total -= nb
+            self._stash_count[self._stash_stage[bid]] -= 1
+
+    def _pop(self, bid: str):
+        if bid in self.data:
+            self._forget(bid)
+            del self.data[bid]
 
     def get(self, bid: str, at: str):
         if bid not in self.data:
@@ -455,7 +489,7 @@ class DeviceStore:
         if bid not in self.data:
             raise LivenessFault(f"actor {self.actor} at {at}: delete of absent buffer {bid}")
         if self.sends_done(bid):
-            del self.data[bid]
+            self._pop(bid)
         else:
             self.pending.append(bid)
 
@@ -464,24 +498,22 @@ class DeviceStore:
         while self.pending:
             bid = self.pending.popleft()
             if self.sends_done(bid):
-                self.data.pop(bid, None)
+                self._pop(bid)
             else:
                 keep.append(bid)
         self.pending = keep
 
-    def _track(self):
+    def _track(self, stage):
+        """Peak counters (executor.py:302-313): O(1) per put from the running totals
+        (only the stage of the stash just put can reach a new peak)."""
         a = self.actor
         self.stats.peak_live[a] = max(self.stats.peak_live.get(a, 0), len(self.data))
-        by_stage: dict[int, int] = {}
-        for bid in self.data:
-            st = self._stash_stage.get(bid)
-            if st is not None:
-                by_stage[st] = by_stage.get(st, 0) + 1
-        for st, n in by_stage.items():
-            key = (a, st)
-            self.stats.peak_stash[key] = max(self.stats.peak_stash.get(key, 0), n)
-        nbytes = sum(_stash_bytes(self.data[bid]) for bid in self.data if bid in self._stash_stage)
-        self.stats.peak_stash_bytes[a] = max(self.stats.peak_stash_bytes.get(a, 0), nbytes)
+        if stage is not None:
+            key = (a, stage)
+            self.stats.peak_stash[key] = max(self.stats.peak_stash.get(key, 0),
+                                             self._stash_count[stage])
+            self.stats.peak_stash_bytes[a] = max(self.stats.peak_stash_bytes.get(a, 0),
+                                                 self._stash_total)
 
 
 REMAT_NONE, REMAT_FULL = "none", "full-per-stage"   # simulator.py:48, :132-149
@@ -514,12 +546,13 @@ def _stash_bytes(stash) -> int:
 
 
 def _retained(v):
-    """A private copy of a forward feed kept for the replay: channel slots and
-    activation buffers are reused once the stage's forward is done."""
-    if isinstance(v, torch.Tensor):
-        return v.clone()
+    """A forward feed kept for the replay, by reference: nothing rewrites a feed
+    before its backward in the same step (peer slots are per message and are
+    rewritten only in the next step, NCCL receive buffers and local-channel
+    values are fresh, stage forwards never write their inputs).  An Act's saved
+    tensors are dropped: the replay recomputes them."""
     if isinstance(v, Act):
-        return Act(v.t.clone())
+        return Act(v.t)
     return v
 
 
@@ -873,6 +906,9 @@ class PipelineEngine:
         self._peer_allocs: list = []
         self._peer_opens: list = []
         self._peer_made = False
+        self.peer_bytes = 0     # receive slots this rank allocated (outside torch's allocator)
+        self._faulted = False   # a step raised: streams were released, state is garbage
+        self._tag = next(_ENGINE_IDS)   # same sequence on every rank (engines built in order)
         self._resident: dict | None = None   # bid -> device value (load_params)
         self._tied = tied_holders(tg)
         self._tied_ch: dict = {}
@@ -929,9 +965,10 @@ class PipelineEngine:
             with torch.cuda.device(dev):
                 _lib.call("pc_peer_alloc", total, ctypes.byref(ptr), h)
             self._peer_allocs.append(ptr.value)
+            self.peer_bytes += total
             store.set(f"pp200/e{tag}/peer/{src}->{dst}", bytes(h))
             out[(src, dst)] = PeerChannel(src, dst, me, ptr.value, self.cp.channels[(src, dst)],
-                                          slots)
+                                          slots, dev)
         for (src, dst) in sorted(self.cp.channels):
             if src != me:
                 continue
@@ -1025,8 +1062,15 @@ class PipelineEngine:
                 cs.graph.reset()
                 cs.graph = None
         self._captures.clear()
-        for d in {self.devices[a] for a in self.local}:
-            torch.cuda.synchronize(d)
+        if self._faulted:
+            # released streams drain within seconds; if one does not, leak the
+            # transport state instead of hanging the process on it
+            if not self._drain(30.0):
+                self._peer_made = False
+                return
+        else:
+            for d in {self.devices[a] for a in self.local}:
+                torch.cuda.synchronize(d)
         for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             if isinstance(ch, NcclChannel) and ch.comm:
                 _lib.call("pc_p2p_destroy", ch.comm)
@@ -1036,10 +1080,12 @@ class PipelineEngine:
             for ptr in self._peer_opens:
                 _lib.call("pc_peer_close", ptr)
             self._peer_opens = []
-            import torch.distributed as dist
-            dist.barrier()          # every mapping of this rank's slots is closed
-            for ptr in self._peer_allocs:
-                _lib.call("pc_peer_free", ptr)
+            # free this rank's slots once every mapping of them is closed; a
+            # peer that never gets here (it faulted and could not drain) makes
+            # this rank leak its slots rather than block
+            if self._close_barrier(60.0):
+                for ptr in self._peer_allocs:
+                    _lib.call("pc_peer_free", ptr)
             self._peer_allocs = []
 
     # -- seeding (executor.py:405-414) --
@@ -1080,6 +1126,7 @@ class PipelineEngine:
     def step(self, params, batch, lr: float = 0.1, timeout_s: float = 30.0, delay_fn=None,
              strict_store: bool = True, to_host: bool = True,
              timeline: bool | None = None) -> ExecutionResult:
+        self._check_usable()
         stats = RunStats()
         tl = self.timeline if timeline is None else timeline
         ctl = _Control(timeout_s)
@@ -1124,6 +1171,8 @@ class PipelineEngine:
             dump = ", ".join(f"actor {a}: {ctl.heartbeat.get(a, '?')}" for a in self.local)
             raise LivenessFault(f"watchdog timeout; blocked instructions: {dump}")
         if ctl.faults:
+            # streams may already wait on messages the failed actor will never send
+            self._abort_channels()
             raise ctl.faults[0]
         self._wait_devices(actors, ctl)
         for key, ch in list(self._channels.items()) + list(self._tied_ch.items()):
@@ -1148,6 +1197,7 @@ class PipelineEngine:
         """
         if len(self.local) != 1:
             raise ExecutorFault("graph capture needs exactly one actor per process")
+        self._check_usable()
         a = self.local[0]
         stats = RunStats()
         ctl = _Control(timeout_s)
@@ -1202,9 +1252,47 @@ class PipelineEngine:
         cs.kernels = nk.value                         # kernel nodes = kernels per replay
         return cs
 
+    def _close_barrier(self, timeout_s: float) -> bool:
+        """All ranks reached close() (store counter; bounded, unlike dist.barrier)."""
+        import torch.distributed as dist
+        store = dist.distributed_c10d._get_default_store()
+        key = f"pp200/close/{self._tag}"
+        store.add(key, 1)
+        world = dist.get_world_size()
+        deadline = time.monotonic() + timeout_s
+        while store.add(key, 0) < world:
+            if time.monotonic() > deadline:
+                return False
+            time.sleep(0.002)
+        return True
+
     def _abort_channels(self):
+        """Fault path (executor.py:443-451): NCCL communicators are aborted, peer
+        receivers release their own flag waits, so every stream drains; the
+        engine refuses further steps."""
+        self._faulted = True
         for ch in list(self._channels.values()) + list(self._tied_ch.values()):
-            ch.abort()
+            try:
+                ch.abort()
+            except Exception:  # noqa: BLE001 - best effort, the fault itself is reported
+                pass
+
+    def _check_usable(self):
+        if self._faulted:
+            raise ExecutorFault("engine was aborted by an earlier fault; build a new PipelineEngine")
+
+    def _drain(self, timeout_s: float) -> bool:
+        """Bounded device synchronisation: True when every local device drained."""
+        devs = sorted({self.devices[a] for a in self.local}, key=str)
+        done = threading.Event()
+
+        def sync():
+            for d in devs:
+                torch.cuda.synchronize(d)
+            done.set()
+
+        threading.Thread(target=sync, daemon=True, name="pp200-drain").start()
+        return done.wait(timeout_s)
 
     def _wait_devices(self, actors, ctl: _Control):
         """Device-side watchdog: a stream that never drains (e.g. a receive
@@ -1289,12 +1377,26 @@ class CapturedStep:
             dst = tensor_of(dst)
             dst.copy_(src.to(dst.dtype) if src.dtype != dst.dtype else src, non_blocking=True)
 
-    def replay(self, batch=None):
+    def replay(self, batch=None, timeout_s: float | None = None):
+        """Launch one captured step (asynchronous).  With ``timeout_s`` the call
+        waits for the step and turns a device that does not drain in time into
+        a LivenessFault, after releasing the channels (the graph's watchdog)."""
         if self.graph is None:
             raise ExecutorFault("captured step was released (engine closed)")
+        self.engine._check_usable()
         if batch is not None:
             self.set_inputs(batch)
         self.graph.replay()
+        if timeout_s is not None:
+            ev = torch.cuda.Event()
+            ev.record()
+            deadline = time.monotonic() + timeout_s
+            while not ev.query():
+                if time.monotonic() > deadline:
+                    self.engine._abort_channels()
+                    raise LivenessFault(f"watchdog timeout: captured step of actor "
+                                        f"{self.act.actor} did not finish in {timeout_s} s")
+                time.sleep(0.0005)
         return self.result
 
     def release(self):
