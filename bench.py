@@ -240,6 +240,23 @@ def gemm_shapes(cfg, P):
     from paper_2412_14374_b200 import _lib as E
     T, d, f, V = cfg.tokens, cfg.d_model, cfg.d_ff, cfg.vocab
     WG = E.EPI_ACCUM | E.EPI_SPLITK_ORDERED
+    if hasattr(cfg, "n_kv_heads"):   # Llama block (device.py _llama_block_fwd / _bwd)
+        qw, ho = cfg.qkv_width, cfg.n_heads * cfg.head_dim
+        block = [(T, qw, d, 0, 1, 0, 0, 0, 0),                                 # qkv
+                 (T, d, ho, 0, 1, E.EPI_RESIDUAL, 1, 0, 0),                    # o (+h)
+                 (T, 2 * f, d, 0, 1, 0, 0, 0, 0),                              # gate | up
+                 (T, d, f, 0, 1, E.EPI_RESIDUAL, 1, 0, 0),                     # down (+h1)
+                 (d, f, T, 1, 0, WG, 0, 0, 1),                                 # dW down
+                 (T, f, d, 0, 1, 0, 0, 0, 0),                                  # dX down
+                 (2 * f, d, T, 1, 0, WG, 0, 0, 1),                             # dW gate|up
+                 (T, d, 2 * f, 0, 1, 0, 0, 0, 0),                              # dX gate|up
+                 (d, ho, T, 1, 0, WG, 0, 0, 1),                                # dW o
+                 (T, ho, d, 0, 1, 0, 0, 0, 0),                                 # dX o
+                 (qw, d, T, 1, 0, WG, 0, 0, 1),                                # dW qkv
+                 (T, d, qw, 0, 1, 0, 0, 0, 0)]                                 # dX qkv
+        head = [(T, V, d, 0, 1, 0, 0, 0, 0), (T, d, V, 0, 1, 0, 0, 0, 0),
+                (V, d, T, 1, 0, WG, 0, 0, 1)]
+        return block, head
     block = [(T, 3 * d, d, 0, 1, E.EPI_BIAS, 0, 0, 0),                        # qkv
              (T, d, d, 0, 1, E.EPI_BIAS | E.EPI_RESIDUAL, 1, 0, 0),            # attn out
              (T, f, d, 0, 1, E.EPI_BIAS | E.EPI_GELU, 0, 1, 0),                # fc1
@@ -350,65 +367,91 @@ def gemm_traffic() -> dict:
         return {}
 
 
-def cpu_baseline(cfg_kw, seconds_hint=True):
-    """The numpy float64 oracle (oracle/gpt.py) on a bounded sample of the same
-    workload: one sequence (1 x 1024 tokens) through the full 12-layer model,
-    forward + backward, timed on the host cores."""
-    from oracle import gpt as og
-    oc = dict(layers=cfg_kw["layers"], d=cfg_kw["d_model"], heads=cfg_kw["n_heads"],
-              ff=cfg_kw["d_ff"], vocab=cfg_kw["vocab"], seq=cfg_kw["seq_len"], mbs=1)
-    rng = np.random.default_rng(0)
-    params = og.init_params(oc, rng)
-    tokens = og.init_tokens(oc, 1, rng)
+def _oracle_sample(wl):
+    """Time the float64 numpy oracle (oracle/gpt.py or oracle/llama.py: the
+    reference's run_reference loop, executor.py:117-134, over this model's
+    vocabulary) on a bounded sample of workload ``wl`` on the host cores.
+    C2: the full 12-layer model on one 1024-token sequence.  Larger configs
+    (a full-size sequence alone is minutes to hours of fp64 CPU work): a slice
+    of the same width -- 1 block + embedding + LM head on one shorter
+    sequence -- whose time per token is scaled to the full model by the FLOP
+    ratio (both counted with ir.*Config.flops_per_token).  Returns
+    (tokens/s of the full model, seconds timed, description)."""
     from threadpoolctl import threadpool_limits
+    from paper_2412_14374_b200 import ir as I
+    kw = wl["kw"]
+    llama = wl["family"] == "llama"
+    full = (I.LlamaConfig if llama else I.GPTConfig)(**kw)
+    small = kw is C2
+    layers = kw["layers"] if small else 1
+    seq = kw["seq_len"] if small else 256
+    sample = dict(kw, layers=layers, seq_len=seq, microbatch_size=1)
+    samp = (I.LlamaConfig if llama else I.GPTConfig)(**sample)
+    rng = np.random.default_rng(0)
+    if llama:
+        from oracle import llama as om
+        oc = dict(layers=layers, d=kw["d_model"], heads=kw["n_heads"], kv_heads=kw["n_kv_heads"],
+                  ff=kw["d_ff"], vocab=kw["vocab"], seq=seq, mbs=1, theta=10000.0)
+        params = om.init_params(oc, rng)
+        tokens = om.init_tokens(oc, 1, rng)
+        pos = om.positions(oc, 1)
+        run = lambda: om.run_reference_llama(params, tokens, pos, oc)
+        what = "oracle/llama.py"
+    else:
+        from oracle import gpt as og
+        oc = dict(layers=layers, d=kw["d_model"], heads=kw["n_heads"], ff=kw["d_ff"],
+                  vocab=kw["vocab"], seq=seq, mbs=1)
+        params = og.init_params(oc, rng)
+        tokens = og.init_tokens(oc, 1, rng)
+        run = lambda: og.run_reference_gpt(params, tokens, oc)
+        what = "oracle/gpt.py"
     with threadpool_limits(limits=os.cpu_count()):
         t0 = time.perf_counter()
-        og.run_reference_gpt(params, tokens, oc)
+        run()
         dt = time.perf_counter() - t0
-    ntok = oc["seq"]
-    return {"value": round(ntok / dt, 2), "unit": "tokens/s", "cores": os.cpu_count(),
-            "kind": "port",
-            "sample": f"oracle/gpt.py float64 numpy fwd+bwd+SGD of GPT-2-small, 1 sequence x "
-                      f"{ntok} tokens ({dt:.1f} s)"}
+    tok_s = seq / dt * (samp.flops_per_token() / full.flops_per_token())
+    desc = (f"{what} float64 numpy fwd+bwd+SGD, {layers} block(s) at full width, 1 sequence x "
+            f"{seq} tokens ({dt:.1f} s)")
+    if not small:
+        desc += "; tokens/s scaled to the full model by the FLOP-per-token ratio"
+    return tok_s, dt, desc
+
+
+def cpu_baseline(wl):
+    tok_s, dt, desc = _oracle_sample(wl)
+    return {"value": round(tok_s, 3), "unit": "tokens/s", "cores": os.cpu_count(),
+            "kind": "port", "sample": desc}
 
 
 def run_reference_impl(args, rank, world):
     """--impl reference: the reference's CPU implementation of the path (the
-    numpy oracle port; the Python reference cannot travel to the GPU box)."""
+    numpy oracle port; the Python reference cannot travel to the GPU box),
+    on the host cores, one bounded sample of the workload per step."""
     if rank != 0:
         return 0
-    from oracle import gpt as og
-    oc = dict(layers=C2["layers"], d=C2["d_model"], heads=C2["n_heads"], ff=C2["d_ff"],
-              vocab=C2["vocab"], seq=C2["seq_len"], mbs=1)
-    rng = np.random.default_rng(0)
-    params = og.init_params(oc, rng)
-    tokens = og.init_tokens(oc, 1, rng)
-    # all host threads (torchrun sets OMP_NUM_THREADS=1 for its workers)
-    from threadpoolctl import threadpool_limits
-    with threadpool_limits(limits=os.cpu_count()):
-        for _ in range(args.warmup):
-            og.gpt_step(params, tokens[0], oc)
-        times = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            og.run_reference_gpt(params, tokens, oc)
-            times.append(time.perf_counter() - t0)
-    ms = 1000 * float(np.mean(times))
-    tok_s = oc["seq"] / (ms / 1000)
-    from paper_2412_14374_b200.ir import GPTConfig
-    cfg = GPTConfig(**C2)
+    wl = WORKLOADS[args.workload]
+    for _ in range(min(args.warmup, 1)):
+        _oracle_sample(wl)
+    rates, times, desc = [], [], ""
+    for _ in range(args.steps):
+        tok_s, dt, desc = _oracle_sample(wl)
+        rates.append(tok_s)
+        times.append(dt)
+    tok_s = float(np.mean(rates))
+    from paper_2412_14374_b200 import ir as I
+    cfg = (I.LlamaConfig if wl["family"] == "llama" else I.GPTConfig)(**wl["kw"])
     line = {
         "impl": "reference", "metric": METRIC,
-        "value": round(tok_s, 2), "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+        "value": round(tok_s, 3), "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1000 * float(np.mean(times)), 2),
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "schedule": "1f1b",
-                   "sample": "1 sequence x 1024 tokens per step (bounded CPU sample)"},
+        "config": {"workload": wl["name"], "schedule": wl["schedule"],
+                   "sample": desc + " per step (bounded CPU sample)"},
         "model_tflops_per_gpu": round(cfg.flops_per_token() * tok_s / 1e12, 5),
-        "cpu_baseline": {"value": round(tok_s, 2), "unit": "tokens/s", "cores": os.cpu_count(),
-                         "kind": "port",
-                         "sample": "oracle/gpt.py float64 numpy, 1 x 1024 tokens per step"},
-        "e2e": {"value": round(tok_s, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+        "cpu_baseline": {"value": round(tok_s, 3), "unit": "tokens/s", "cores": os.cpu_count(),
+                         "kind": "port", "sample": desc},
+        "e2e": {"value": round(tok_s, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -590,7 +633,7 @@ def main():
                            if op.kind in ("gpt-block", "llama-block"))
         roof = gemm_roofline(cfg, P, stage_blocks, ms, burst, M)
         roof["peak_kind"] = peak_kind
-        cpu = None if args.no_cpu_baseline else cpu_baseline(wl_kw)
+        cpu = None if args.no_cpu_baseline else cpu_baseline(wl)
         line = {
             "metric": METRIC,
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,

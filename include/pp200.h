@@ -147,7 +147,9 @@ int pc_layernorm_param_grads(int dtype, int64_t rows, int64_t d, const void* dy,
 int pc_rmsnorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const float* gamma,
                    void* y, float* rstd, float eps, void* stream);
 /* dx = dres + RMSNorm_bwd(dy) (dres may be NULL); dgamma written (fp32, deterministic
- * two-stage reduction in ws, see pc_reduce_workspace_bytes). (oracle rms_norm_bwd) */
+ * two-stage reduction in ws, see pc_reduce_workspace_bytes), or not computed when NULL
+ * (pc_layernorm_param_grads with mean = NULL gives it, accumulating, on another stream).
+ * (oracle rms_norm_bwd) */
 int pc_rmsnorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
                    const float* gamma, const float* rstd, const void* dres, void* dx,
                    float* dgamma, void* ws, int64_t ws_bytes, void* stream);
@@ -175,7 +177,8 @@ int pc_embedding_bwd(int dtype, int64_t T, int64_t d, int64_t seq, int64_t vocab
                      const int32_t* tokens, const void* dh, float* dwte, float* dwpe,
                      void* workspace, int64_t ws_bytes, void* stream);
 /* As pc_embedding_bwd; accumulate = 1 adds the token-row and position sums onto dwte /
- * dwpe (the running gradient) instead of overwriting (no zero-fill of dwte). */
+ * dwpe (the running gradient) instead of overwriting (no zero-fill of dwte).  dwpe may be
+ * NULL (no position table). */
 int pc_embedding_bwd_acc(int dtype, int64_t T_, int64_t d, int64_t seq, int64_t vocab,
                          const int32_t* tokens, const void* dh, float* dwte, float* dwpe,
                          int accumulate, void* workspace, int64_t ws_bytes, void* stream);
@@ -218,10 +221,16 @@ int pc_peer_close(void* ptr);
 int pc_stream_write_u32(void* addr, uint32_t value, void* stream);
 int pc_stream_wait_u32(void* addr, uint32_t value, void* stream);
 int pc_peer_copy(void* dst, const void* src, int64_t bytes, void* stream);
-/* Abort (Channel faults, executor.py:185-197, :443-451): set n flag words to value from a
- * stream that is not blocked, releasing a receiver stream parked in pc_stream_wait_u32 on a
- * message that will never arrive, so the device drains and the fault can surface. */
-int pc_peer_release(void* flags, int64_t n, uint32_t value, void* stream);
+/* RecvWait of the peer transport (Channel.recv, executor.py:223-240): a one-thread kernel
+ * on `stream` spins until *flag == 1 (the sender's pc_stream_write_u32), re-arms it to 0
+ * and exits.  It also polls *abort_word_dev (mapped host memory, pc_host_word_alloc):
+ * the watchdog (executor.py:443-451) sets the word from the CPU and the wait ends, so a
+ * message that will never arrive cannot park the device forever. */
+int pc_peer_wait(void* flag, const void* abort_word_dev, void* stream);
+/* 64 zeroed bytes of page-locked host memory mapped for the device: *host for CPU
+ * stores, *dev for kernels. */
+int pc_host_word_alloc(void** host, void** dev);
+int pc_host_word_free(void* host);
 /* Kernel nodes of a captured CUDA graph (cudaGraph_t), child graphs included. */
 int pc_graph_kernel_nodes(void* graph, int64_t* n);
 

@@ -59,7 +59,9 @@ SIGNATURES: dict[str, list] = {
     "pc_stream_write_u32": [_c_p, ctypes.c_uint32, _c_p],
     "pc_stream_wait_u32": [_c_p, ctypes.c_uint32, _c_p],
     "pc_peer_copy": [_c_p, _c_p, _c_i64, _c_p],
-    "pc_peer_release": [_c_p, _c_i64, ctypes.c_uint32, _c_p],
+    "pc_peer_wait": [_c_p, _c_p, _c_p],
+    "pc_host_word_alloc": [ctypes.POINTER(_c_p), ctypes.POINTER(_c_p)],
+    "pc_host_word_free": [_c_p],
     "pc_graph_kernel_nodes": [_c_p, ctypes.POINTER(_c_i64)],
     "pc_sgd_update": [_c_i, _c_i64, _c_p, _c_p, _c_d, _c_p, _c_p, _c_p],
     "pc_cast": [_c_i, _c_i, _c_i64, _c_p, _c_p, _c_p],
@@ -151,7 +153,8 @@ _NON_LAUNCH = {"pc_version", "pc_device_sm_count", "pc_gemm_set_tile_n", "pc_gem
                "pc_embedding_bwd_workspace_bytes", "pc_reduce_workspace_bytes", "pc_p2p_available", "pc_p2p_unique_id",
                "pc_p2p_comm_init", "pc_p2p_abort", "pc_p2p_destroy",
                "pc_peer_alloc", "pc_peer_free", "pc_peer_open", "pc_peer_close",
-               "pc_stream_write_u32", "pc_stream_wait_u32", "pc_graph_kernel_nodes"}
+               "pc_stream_write_u32", "pc_stream_wait_u32", "pc_graph_kernel_nodes",
+               "pc_host_word_alloc", "pc_host_word_free"}
 launch_count = 0
 
 

@@ -608,7 +608,8 @@ extern "C" int pc_embedding_bwd_acc(int dtype, int64_t T_, int64_t d, int64_t se
   if (!accumulate) PP_CUDA_TRY(cudaMemsetAsync(dwte, 0, static_cast<size_t>(vocab) * d * 4, st));
   PP_DISPATCH_FB(dtype, T,
     embed_bwd_wte_kernel<T><<<row_blocks(T_), 256, 0, st>>>(n, (int)d, keys_out, vals_out, static_cast<const T*>(dh), dwte, accumulate);
-    embed_bwd_wpe_kernel<T><<<(unsigned)((seq * d + 255) / 256), 256, 0, st>>>(T_, (int)d, (int)seq, static_cast<const T*>(dh), dwpe, accumulate));
+    if (dwpe)  // NULL: no position table (Llama)
+      embed_bwd_wpe_kernel<T><<<(unsigned)((seq * d + 255) / 256), 256, 0, st>>>(T_, (int)d, (int)seq, static_cast<const T*>(dh), dwpe, accumulate));
   return check_launch("embedding_bwd");
 }
 

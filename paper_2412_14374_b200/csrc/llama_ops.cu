@@ -3,8 +3,12 @@
 // the attention kernels.  Semantics: oracle/llama.py (float64 restatement,
 // pinned by finite differences and torch autograd in tests/test_oracle.py).
 //
-// All kernels are row-parallel and memory-bound (HBM roofline); one warp per
-// row for the norms, one thread per (row, frequency) for RoPE.
+// All kernels are row-parallel and memory-bound (HBM roofline).  bf16 rows
+// whose widths are multiples of 8 take vectorised paths (16-byte loads and
+// stores, coalesced across a warp): one warp per row for the norms, one block
+// per row for RoPE (the row's cos / sin table computed once into shared
+// memory from fp64 angles, then 8 frequencies of one head per thread), 8
+// columns per thread for SwiGLU.  fp32 (parity mode) keeps the scalar kernels.
 #include "common.cuh"
 
 namespace pp200 {
@@ -159,6 +163,181 @@ __global__ void gqa_kv_kernel(int64_t rows, int H, int Hkv, int hd, const T* __r
 
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(h[k]);
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+  return u;
+}
+__device__ __forceinline__ void load_g8(const float* g, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(g)[0], b = reinterpret_cast<const float4*>(g)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// bf16, d % 8 == 0: warp per row, 16-byte chunks
+__global__ void __launch_bounds__(256) rms_fwd_vec(int64_t rows, int d, const bf16* __restrict__ x,
+                                                   const float* __restrict__ g, bf16* __restrict__ y,
+                                                   float* __restrict__ rstd, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(RMS_ROWS_PER_BLOCK) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
+  const int nc = d / 8;
+  float ss = 0.f;
+  for (int c = lane; c < nc; c += 32) {
+    float v[8];
+    unpack8(xr[c], v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ss = fmaf(v[k], v[k], ss);
+  }
+  ss = warp_sum(ss);
+  const float rs = rsqrtf(ss / d + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y + r * d);
+  for (int c = lane; c < nc; c += 32) {
+    float v[8], gv[8];
+    unpack8(xr[c], v);
+    load_g8(g + 8 * c, gv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = v[k] * rs * gv[k];
+    yr[c] = pack8(v);
+  }
+  if (lane == 0) rstd[r] = rs;
+}
+
+// bf16, d % 8 == 0: dx = dres + rstd * (dy*g - xh * mean(dy*g*xh))
+__global__ void __launch_bounds__(256) rms_bwd_dx_vec(int64_t rows, int d, const bf16* __restrict__ dy,
+                                                      const bf16* __restrict__ x,
+                                                      const float* __restrict__ g,
+                                                      const float* __restrict__ rstd,
+                                                      const bf16* __restrict__ dres,
+                                                      bf16* __restrict__ dx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(RMS_ROWS_PER_BLOCK) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float rs = rstd[r];
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + r * d);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
+  const int nc = d / 8;
+  float s = 0.f;
+  for (int c = lane; c < nc; c += 32) {
+    float a[8], b[8], gv[8];
+    unpack8(dyr[c], a);
+    unpack8(xr[c], b);
+    load_g8(g + 8 * c, gv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = fmaf(a[k] * gv[k], b[k] * rs, s);
+  }
+  const float m = warp_sum(s) / d;
+  uint4* dxr = reinterpret_cast<uint4*>(dx + r * d);
+  const uint4* drr = dres ? reinterpret_cast<const uint4*>(dres + r * d) : nullptr;
+  for (int c = lane; c < nc; c += 32) {
+    float a[8], b[8], gv[8], o[8];
+    unpack8(dyr[c], a);
+    unpack8(xr[c], b);
+    load_g8(g + 8 * c, gv);
+    if (drr) {
+      unpack8(drr[c], o);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] += rs * (a[k] * gv[k] - b[k] * rs * m);
+    dxr[c] = pack8(o);
+  }
+}
+
+// bf16, head_dim % 16 == 0, ld % 8 == 0: one block per row.  The row's
+// (cos, sin) per frequency come from fp64 angles (exact for large positions),
+// computed once into shared memory; each thread then rotates 8 frequencies of
+// one head with two 16-byte loads and stores.
+__global__ void __launch_bounds__(128) rope_row_vec(int n_heads, int hd, bf16* __restrict__ t,
+                                                    int64_t ld, const int32_t* __restrict__ pos,
+                                                    double log2_theta, int inverse) {
+  __shared__ float2 cs[128];  // hd <= 256
+  const int half = hd / 2;
+  const int64_t r = blockIdx.x;
+  const double p = static_cast<double>(pos[r]);
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    double sd, cd;
+    sincos(p * exp2(-2.0 * i / hd * log2_theta), &sd, &cd);
+    cs[i] = make_float2(static_cast<float>(cd), static_cast<float>(inverse ? -sd : sd));
+  }
+  __syncthreads();
+  const int per_head = half / 8;
+  bf16* row = t + r * ld;
+  for (int ch = threadIdx.x; ch < n_heads * per_head; ch += blockDim.x) {
+    const int h = ch / per_head, i0 = (ch % per_head) * 8;
+    uint4* pa = reinterpret_cast<uint4*>(row + h * hd + i0);
+    uint4* pb = reinterpret_cast<uint4*>(row + h * hd + half + i0);
+    float a[8], b[8], oa[8], ob[8];
+    unpack8(*pa, a);
+    unpack8(*pb, b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float2 q = cs[i0 + k];
+      oa[k] = a[k] * q.x - b[k] * q.y;
+      ob[k] = b[k] * q.x + a[k] * q.y;
+    }
+    *pa = pack8(oa);
+    *pb = pack8(ob);
+  }
+}
+
+__device__ __forceinline__ float sigmoid_fast(float g) { return 1.f / (1.f + __expf(-g)); }
+
+// bf16, f % 8 == 0 and 16-byte aligned rows: 8 columns per thread
+__global__ void swiglu_fwd_vec(int64_t rows, int f, const bf16* __restrict__ gu, int64_t ld_gu,
+                               bf16* __restrict__ m, int64_t ld_m) {
+  const int nc = f / 8;
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= rows * nc) return;
+  const int64_t r = idx / nc;
+  const int c = static_cast<int>(idx % nc) * 8;
+  float g[8], u[8], o[8];
+  unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + c), g);
+  unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + f + c), u);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoid_fast(g[k]) * u[k];
+  *reinterpret_cast<uint4*>(m + r * ld_m + c) = pack8(o);
+}
+
+__global__ void swiglu_bwd_vec(int64_t rows, int f, const bf16* __restrict__ gu, int64_t ld_gu,
+                               const bf16* __restrict__ dm, int64_t ld_dm, bf16* __restrict__ dgu,
+                               int64_t ld_dgu) {
+  const int nc = f / 8;
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= rows * nc) return;
+  const int64_t r = idx / nc;
+  const int c = static_cast<int>(idx % nc) * 8;
+  float g[8], u[8], d[8], dg[8], du[8];
+  unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + c), g);
+  unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + f + c), u);
+  unpack8(*reinterpret_cast<const uint4*>(dm + r * ld_dm + c), d);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float sg = sigmoid_fast(g[k]);
+    dg[k] = d[k] * u[k] * (sg * (1.f + g[k] * (1.f - sg)));
+    du[k] = d[k] * g[k] * sg;
+  }
+  *reinterpret_cast<uint4*>(dgu + r * ld_dgu + c) = pack8(dg);
+  *reinterpret_cast<uint4*>(dgu + r * ld_dgu + f + c) = pack8(du);
+}
+
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 }  // namespace
 }  // namespace pp200
 
@@ -177,6 +356,11 @@ extern "C" int pc_rmsnorm_fwd(int dtype, int64_t rows, int64_t d, const void* x,
   if (rows <= 0) return PC_OK;
   PP_CHECK_ARG(d > 0, "rmsnorm: bad width");
   const unsigned nb = blocks_for(rows, RMS_ROWS_PER_BLOCK);
+  if (dtype == PC_BF16 && d % 8 == 0 && al16(x) && al16(y) && al16(gamma)) {
+    rms_fwd_vec<<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const bf16*>(x), gamma,
+                                    static_cast<bf16*>(y), rstd, eps);
+    return check_launch("rmsnorm_fwd");
+  }
   PP_DISPATCH_FB2(dtype, T, rms_fwd_kernel<T><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(x), gamma, static_cast<T*>(y), rstd, eps));
   return check_launch("rmsnorm_fwd");
 }
@@ -189,10 +373,18 @@ extern "C" int pc_rmsnorm_bwd(int dtype, int64_t rows, int64_t d, const void* dy
   PP_CHECK_ARG(d > 0, "rmsnorm: bad width");
   const unsigned nb = blocks_for(rows, RMS_ROWS_PER_BLOCK);
   bool ok = true;
+  const bool vec = dtype == PC_BF16 && d % 8 == 0 && al16(dy) && al16(x) && al16(dx) &&
+                   al16(gamma) && (dres == nullptr || al16(dres));
+  // dgamma == NULL: dx only (the gain gradient then comes from
+  // pc_layernorm_param_grads with mean = NULL, e.g. on another stream)
   PP_DISPATCH_FB2(dtype, T,
-    rms_bwd_dx_kernel<T><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
+    if (vec)
+      rms_bwd_dx_vec<<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const bf16*>(dy), static_cast<const bf16*>(x), gamma, rstd, static_cast<const bf16*>(dres), static_cast<bf16*>(dx));
+    else
+      rms_bwd_dx_kernel<T><<<nb, 256, 0, st>>>(rows, (int)d, static_cast<const T*>(dy), static_cast<const T*>(x), gamma, rstd, static_cast<const T*>(dres), static_cast<T*>(dx));
     // dgamma = sum_rows dy * x * rstd: the LayerNorm-statistics reduction without a mean
-    ok = colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), nullptr, rstd, dgamma, nullptr, 0, ws, ws_bytes, st));
+    if (dgamma)
+      ok = colred_launch<T>(1, rows, d, static_cast<const T*>(dy), d, static_cast<const T*>(x), nullptr, rstd, dgamma, nullptr, 0, ws, ws_bytes, st));
   if (!ok) {
     set_error("rmsnorm_bwd: reduction workspace too small (pc_reduce_workspace_bytes)");
     return PC_ERR_ARG;
@@ -207,6 +399,12 @@ extern "C" int pc_rope(int dtype, int64_t rows, int64_t n_heads, int64_t head_di
   PP_CHECK_ARG(head_dim > 0 && head_dim % 2 == 0, "rope: head_dim must be even");
   PP_CHECK_ARG(theta > 1.f, "rope: theta must exceed 1");
   const int64_t n = rows * (head_dim / 2);
+  if (dtype == PC_BF16 && head_dim % 16 == 0 && head_dim <= 256 && ld % 8 == 0 && al16(t)) {
+    rope_row_vec<<<static_cast<unsigned>(rows), 128, 0, st>>>(
+        (int)n_heads, (int)head_dim, static_cast<bf16*>(t), ld, pos, log2(static_cast<double>(theta)),
+        inverse);
+    return check_launch("rope");
+  }
   PP_DISPATCH_FB2(dtype, T, rope_kernel<T><<<blocks_for(n, 256), 256, 0, st>>>(rows, (int)n_heads, (int)head_dim, static_cast<T*>(t), ld, pos, log2(static_cast<double>(theta)), inverse));
   return check_launch("rope");
 }
@@ -215,6 +413,11 @@ extern "C" int pc_swiglu_fwd(int dtype, int64_t rows, int64_t f, const void* gu,
                              void* m, int64_t ld_m, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= 0 || f <= 0) return PC_OK;
+  if (dtype == PC_BF16 && f % 8 == 0 && ld_gu % 8 == 0 && ld_m % 8 == 0 && al16(gu) && al16(m)) {
+    swiglu_fwd_vec<<<blocks_for(rows * (f / 8), 256), 256, 0, st>>>(
+        rows, (int)f, static_cast<const bf16*>(gu), ld_gu, static_cast<bf16*>(m), ld_m);
+    return check_launch("swiglu_fwd");
+  }
   PP_DISPATCH_FB2(dtype, T, swiglu_fwd_kernel<T><<<blocks_for(rows * f, 256), 256, 0, st>>>(rows, (int)f, static_cast<const T*>(gu), ld_gu, static_cast<T*>(m), ld_m));
   return check_launch("swiglu_fwd");
 }
@@ -223,6 +426,13 @@ extern "C" int pc_swiglu_bwd(int dtype, int64_t rows, int64_t f, const void* gu,
                              const void* dm, int64_t ld_dm, void* dgu, int64_t ld_dgu, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= 0 || f <= 0) return PC_OK;
+  if (dtype == PC_BF16 && f % 8 == 0 && ld_gu % 8 == 0 && ld_dm % 8 == 0 && ld_dgu % 8 == 0 &&
+      al16(gu) && al16(dm) && al16(dgu)) {
+    swiglu_bwd_vec<<<blocks_for(rows * (f / 8), 256), 256, 0, st>>>(
+        rows, (int)f, static_cast<const bf16*>(gu), ld_gu, static_cast<const bf16*>(dm), ld_dm,
+        static_cast<bf16*>(dgu), ld_dgu);
+    return check_launch("swiglu_bwd");
+  }
   PP_DISPATCH_FB2(dtype, T, swiglu_bwd_kernel<T><<<blocks_for(rows * f, 256), 256, 0, st>>>(rows, (int)f, static_cast<const T*>(gu), ld_gu, static_cast<const T*>(dm), ld_dm, static_cast<T*>(dgu), ld_dgu));
   return check_launch("swiglu_bwd");
 }

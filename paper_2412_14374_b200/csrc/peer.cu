@@ -135,23 +135,45 @@ extern "C" int pc_graph_kernel_nodes(void* graph, int64_t* n) {
   return count_kernel_nodes(static_cast<CUgraph>(graph), n);
 }
 
-// Abort support for the peer transport: set n flag words at `flags` to `value`
-// from a stream that is not blocked (the caller passes a fresh one).  A
-// receiver whose stream is parked in cuStreamWaitValue32 on a flag the sender
-// never wrote (dropped SendStart, dead peer) is released and drains; each
-// released wait re-arms its own flag to 0 as in a normal step.
-using MemsetFn = CUresult (*)(CUdeviceptr, unsigned int, size_t, CUstream);
-
-extern "C" int pc_peer_release(void* flags, int64_t n, uint32_t value, void* stream) {
-  PP_CHECK_ARG(flags && n >= 0, "peer_release: bad args");
-  if (n == 0) return PC_OK;
-  static MemsetFn fn = driver_fn<MemsetFn>("cuMemsetD32Async");
-  PP_CHECK_ARG(fn != nullptr, "cuMemsetD32Async unavailable");
-  CUresult r = fn(reinterpret_cast<CUdeviceptr>(flags), value, static_cast<size_t>(n),
-                  static_cast<CUstream>(stream));
-  if (r != CUDA_SUCCESS) {
-    set_error("cuMemsetD32Async failed (%d)", static_cast<int>(r));
-    return PC_ERR_CUDA;
+// RecvWait of the peer transport: one thread spins until the message flag
+// (written over NVLink by the sender's stream after its producer) reads 1,
+// re-arms it to 0, and exits; later work on the stream then reads the slot.
+// Every 1024 polls it also reads an abort word in mapped host memory: the
+// engine's watchdog sets it from the CPU (no stream, no CUDA call), so a wait
+// on a message that will never arrive (dropped SendStart, dead peer) ends and
+// the device drains -- a stream-memory-op wait cannot be released that way,
+// since work queued to release it may share the blocked stream's hardware
+// queue.  Graph-capturable (a kernel node).
+__global__ void peer_wait_kernel(unsigned* flag, const volatile unsigned* abort_word) {
+  if (threadIdx.x != 0) return;
+  unsigned n = 0;
+  while (ld_acquire_sys(flag) != 1u) {
+    if ((++n & 1023u) == 0 && *abort_word != 0u) return;
+    __nanosleep(64);
   }
+  *flag = 0u;
+}
+
+extern "C" int pc_peer_wait(void* flag, const void* abort_word_dev, void* stream) {
+  PP_CHECK_ARG(flag && abort_word_dev, "peer_wait: bad args");
+  peer_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<unsigned*>(flag), static_cast<const volatile unsigned*>(abort_word_dev));
+  return check_launch("peer_wait_kernel");
+}
+
+// A zeroed 64-byte word in page-locked, device-mapped host memory: the host
+// writes it with a plain store, kernels read it through *dev.
+extern "C" int pc_host_word_alloc(void** host, void** dev) {
+  PP_CHECK_ARG(host && dev, "host_word_alloc: bad args");
+  void* h = nullptr;
+  PP_CUDA_TRY(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(h, 0, 64);
+  PP_CUDA_TRY(cudaHostGetDevicePointer(dev, h, 0));
+  *host = h;
+  return PC_OK;
+}
+
+extern "C" int pc_host_word_free(void* host) {
+  PP_CUDA_TRY(cudaFreeHost(host));
   return PC_OK;
 }

@@ -367,15 +367,15 @@ class DeviceOps:
         elif kind == "llama-embed":
             env[op.result] = Act(self._llama_embed(op, env))
         elif kind == "llama-embed-grad":
-            env[op.result] = self._llama_embed_bwd(op, env)
+            env[op.result] = self._llama_embed_bwd(op, env, acc=self._acc_for_value(op.result))
         elif kind == "llama-block":
             self._llama_block_fwd(op, env)
         elif kind == "llama-block-grad":
-            env[op.result] = self._llama_block_bwd(op, env)
+            env[op.result] = self._llama_block_bwd(op, env, acc=self._acc_target(op, 1))
         elif kind == "llama-head":
             env[op.result] = self._llama_head_fwd(op, env)
         elif kind == "llama-head-grad":
-            env[op.result] = self._llama_head_bwd(op, env)
+            env[op.result] = self._llama_head_bwd(op, env, acc=self._acc_for_tuple(op, 1))
         else:
             raise ValueError(f"no device rule for op kind {kind!r}")
 
@@ -813,7 +813,8 @@ class DeviceOps:
         dlogits = hv.saved["head"]["dlogits"]
         w0: Param = env[op.operands[1]]
         T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
-        dh = self.empty((T, d), self.mode.act)
+        # the stage input gradient: into the previous stage's slot when sent
+        dh = self._placed_elem(op, 0, (T, d), self.mode.act)
         if w0.shadow is not None:  # B = wte^T, K-major, from the transposed shadow
             wt = self._shadow_t(w0, self._elay, ("wte",))
             self._gemm(self.mode.act, 0, 1, T, d, V, dlogits, V,
@@ -869,19 +870,20 @@ class DeviceOps:
              out.data_ptr(), self.st)
         return out
 
-    def _llama_embed_bwd(self, op, env):
+    def _llama_embed_bwd(self, op, env, acc=None):
+        """Token-row sums of the embedding gradient, onto the running sum when
+        fused (no [vocab, d] zero fill per microbatch), else onto zeros."""
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
         T, d = cfg.tokens, cfg.d_model
-        dw = self.zeros((layout_size(self._elay),), torch.float32)
+        dw = acc if acc is not None else self.zeros((layout_size(self._elay),), torch.float32)
         if self._emb_ws is None:
             nb = ctypes.c_int64(0)
             call("pc_embedding_bwd_workspace_bytes", T, ctypes.byref(nb))
             self._emb_ws = self.empty((nb.value,), torch.uint8)
-        dpe = self.empty((cfg.seq_len, d), torch.float32)  # no position table: discarded
-        call("pc_embedding_bwd", self.mode.pc_act, T, d, cfg.seq_len, cfg.vocab, x.data_ptr(),
-             g.data_ptr(), self._slice(dw, self._elay, "wte").data_ptr(), dpe.data_ptr(),
+        call("pc_embedding_bwd_acc", self.mode.pc_act, T, d, cfg.seq_len, cfg.vocab, x.data_ptr(),
+             g.data_ptr(), self._slice(dw, self._elay, "wte").data_ptr(), None, 1,
              self._emb_ws.data_ptr(), self._emb_ws.numel(), self.st)
         self._emb_ws.record_stream(self.stream)
         return dw
@@ -947,7 +949,8 @@ class DeviceOps:
         m = self.empty((T, f), act)
         call("pc_swiglu_fwd", self.mode.pc_act, T, f, gu.data_ptr(), 2 * f, m.data_ptr(), f,
              self.st)
-        out = self.empty((T, d), act)
+        # the stage output: the down GEMM writes it into the next stage's slot when sent
+        out = self.empty((T, d), act) if final else self._out(op.result, (T, d), act)
         self._gemm(act, 0, 1, T, d, f, m, f, sl("w_down"), f, out, d, _lib.EPI_RESIDUAL,
                    aux=h1, ldaux=d)
         saved = dict(a=a, rstd1=rstd1, qkv_att=qkv_att, o=o, lse=lse, h1=h1, a2=a2,
@@ -959,9 +962,12 @@ class DeviceOps:
         hv.saved[op.id] = saved
         env[op.result] = Act(out)
 
-    def _llama_block_bwd(self, op, env):
+    def _llama_block_bwd(self, op, env, acc=None):
         """oracle/llama.py block_bwd; dX GEMMs read the transposed bf16 weight
-        shadow (K-major B), weight gradients are split-K onto zeroed fp32."""
+        shadow (K-major B).  Weight and RMSNorm-gain gradients run on the side
+        stream beside the dX chain and, when the plan allows (``acc``), add
+        straight onto the fp32 running sum (TMA reduce-add / ordered split-K,
+        accumulating reductions): no per-microbatch zero fill or add pass."""
         cfg = self.gpt
         final = bool(op.attr("final_ln"))
         lay = self._blay[final]
@@ -982,19 +988,26 @@ class DeviceOps:
             wB = lambda name: (1, self._slice_t(Wt, lay, name), lay[name][1][0])
         else:
             wB = lambda name: (0, sl(name), lay[name][1][1])
-        dW = self.zeros((layout_size(lay),), f32)
+        fused = acc is not None
+        dW = acc if fused else self.zeros((layout_size(lay),), f32)
         gs = lambda name: self._slice(dW, lay, name)
+        self.red_ws(T, d, side=True)
 
-        def rms_bwd(dy, x, gname, rstd, dres):
-            dx = self.empty((T, d), act)
+        def rms_bwd(dy, x, gname, rstd, dres, dx=None):
+            self._fork()   # gain gradient beside the dx chain
+            call("pc_layernorm_param_grads", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
+                 None, rstd.data_ptr(), gs(gname).data_ptr(), None, int(fused),
+                 *self.red_ws(T, d, side=True), self._side().cuda_stream)
+            if dx is None:
+                dx = self.empty((T, d), act)
             call("pc_rmsnorm_bwd", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
-                 ms(gname).data_ptr(), rstd.data_ptr(), ptr(dres), dx.data_ptr(),
-                 gs(gname).data_ptr(), *self.red_ws(T, d), self.st)
+                 ms(gname).data_ptr(), rstd.data_ptr(), ptr(dres), dx.data_ptr(), None, None, 0,
+                 self.st)
             return dx
 
         def wgrad(M_, N_, A, lda, Bm, ldb, wname):
-            self._gemm(f32, 1, 0, M_, N_, T, A, lda, Bm, ldb, gs(wname), N_,
-                       _lib.EPI_SPLITK_ZERO_C)
+            self._fork()
+            self._wgrad_into(M_, N_, T, A, lda, Bm, ldb, gs(wname), fused, self._side())
 
         dout = rms_bwd(dz, sv["out"], "rmsf_g", sv["rstdf"], None) if final else dz
         # MLP
@@ -1035,7 +1048,9 @@ class DeviceOps:
         da = self.empty((T, d), act)
         tb, B, ldb = wB("w_qkv")
         self._gemm(act, 0, tb, T, d, qw, dqkv, qw, B, ldb, da, d)
-        dh = rms_bwd(da, h, "rms1_g", sv["rstd1"], dh1)
+        # the stage input gradient: into the previous stage's slot when sent
+        dh = rms_bwd(da, h, "rms1_g", sv["rstd1"], dh1, self._placed_elem(op, 0, (T, d), act))
+        self._join()
         return (dh, dW)
 
     def _llama_head_fwd(self, op, env):
@@ -1058,14 +1073,14 @@ class DeviceOps:
         hv.saved[op.id] = dict(dlogits=logits)
         return loss
 
-    def _llama_head_bwd(self, op, env):
+    def _llama_head_bwd(self, op, env, acc=None):
         cfg = self.gpt
         hv = env[op.operands[0]]
         h = tensor_of(hv)
         dlogits = hv.saved["head"]["dlogits"]
         wo: Param = env[op.operands[1]]
         T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
-        dh = self.empty((T, d), self.mode.act)
+        dh = self._placed_elem(op, 0, (T, d), self.mode.act)
         if wo.shadow is not None:
             wt = self._shadow_t(wo, self._hlay, ("w_head",))
             self._gemm(self.mode.act, 0, 1, T, d, V, dlogits, V,
@@ -1073,9 +1088,12 @@ class DeviceOps:
         else:
             self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V,
                        self._slice(wo.compute(), self._hlay, "w_head"), d, dh, d)
-        dw = self.zeros((layout_size(self._hlay),), torch.float32)
-        self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
-                   self._slice(dw, self._hlay, "w_head"), d, _lib.EPI_SPLITK_ZERO_C)
+        fused = acc is not None
+        dw = acc if fused else self.zeros((layout_size(self._hlay),), torch.float32)
+        self._fork()
+        self._wgrad_into(V, d, T, dlogits, V, h, d, self._slice(dw, self._hlay, "w_head"), fused,
+                         self._side())
+        self._join()
         return (dh, dw)
 
 

@@ -356,10 +356,10 @@ class PeerChannel:
     last gradient from the receiver).  Reference Channel: executor.py:201-254.
     """
 
-    def __init__(self, src: int, dst: int, me: int, base: int, bids, slots, device=None):
+    def __init__(self, src: int, dst: int, me: int, base: int, bids, slots, abort_word):
         self.src, self.dst, self.me = src, dst, me
         self.base, self.bids, self.slots = base, list(bids), slots
-        self.device = device
+        self.abort_host, self.abort_dev = abort_word   # the engine's mapped host word
         self.reset()
 
     def reset(self):
@@ -400,8 +400,9 @@ class PeerChannel:
 
     def recv(self, seq: int, ctl: _Control, actor: int, stream: torch.cuda.Stream):
         off, shape, dtype, _ = self.slots[seq]
-        _lib.call("pc_stream_wait_u32", self.flag(seq), 1, stream.cuda_stream)
-        _lib.call("pc_stream_write_u32", self.flag(seq), 0, stream.cuda_stream)
+        # spin kernel: waits for the flag, re-arms it, and gives up when the
+        # engine's abort word is set (see abort)
+        _lib.call("pc_peer_wait", self.flag(seq), self.abort_dev, stream.cuda_stream)
         t = torch.as_tensor(_CAI(self.base + off, shape, dtype), device=stream.device)
         return self.bids[seq], (t.view(torch.bfloat16) if dtype == torch.bfloat16 else t)
 
@@ -415,16 +416,12 @@ class PeerChannel:
         return True
 
     def abort(self):
-        """Release this receiver's stream: set every flag word of the channel
-        from a fresh (unblocked) stream, so waits on messages that will never
-        arrive pass and the device drains (the data read is garbage; the step
-        is failing).  The sender side holds no waits on this channel."""
-        if self.me != self.dst or self.device is None:
-            return
-        with torch.cuda.device(self.device):
-            s = torch.cuda.Stream(device=self.device)
-            _lib.call("pc_peer_release", self.base, len(self.bids), 1, s.cuda_stream)
-            s.synchronize()
+        """Release this rank's parked receives: a plain CPU store to the engine's
+        mapped abort word ends every pc_peer_wait spin, so the device drains (the
+        data read is garbage; the step is failing).  No stream is involved: work
+        queued to release a blocked stream could share its hardware queue."""
+        import ctypes
+        ctypes.c_uint32.from_address(self.abort_host).value = 1
 
 
 # ---------------------------------------------------------------------------
@@ -906,6 +903,7 @@ class PipelineEngine:
         self._peer_allocs: list = []
         self._peer_opens: list = []
         self._peer_made = False
+        self._abort_word = None  # (host, device) address of the peer waits' abort word
         self.peer_bytes = 0     # receive slots this rank allocated (outside torch's allocator)
         self._faulted = False   # a step raised: streams were released, state is garbage
         self._tag = next(_ENGINE_IDS)   # same sequence on every rank (engines built in order)
@@ -955,6 +953,9 @@ class PipelineEngine:
         sender maps its channels (so no rank waits on another's mapping)."""
         import ctypes
         self._peer_made = True
+        hw, dw = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.call("pc_host_word_alloc", ctypes.byref(hw), ctypes.byref(dw))
+        self._abort_word = (hw.value, dw.value)
         out = {}
         layout = {key: _slot_layout(bids, self._wire_meta) for key, bids in self.cp.channels.items()}
         for (src, dst) in sorted(self.cp.channels):
@@ -968,7 +969,7 @@ class PipelineEngine:
             self.peer_bytes += total
             store.set(f"pp200/e{tag}/peer/{src}->{dst}", bytes(h))
             out[(src, dst)] = PeerChannel(src, dst, me, ptr.value, self.cp.channels[(src, dst)],
-                                          slots, dev)
+                                          slots, self._abort_word)
         for (src, dst) in sorted(self.cp.channels):
             if src != me:
                 continue
@@ -979,7 +980,7 @@ class PipelineEngine:
                 _lib.call("pc_peer_open", h, ctypes.byref(ptr))
             self._peer_opens.append(ptr.value)
             out[(src, dst)] = PeerChannel(src, dst, me, ptr.value, self.cp.channels[(src, dst)],
-                                          slots)
+                                          slots, self._abort_word)
         return out
 
     # -- resident training state (multi-step) --
@@ -1073,7 +1074,9 @@ class PipelineEngine:
                 torch.cuda.synchronize(d)
         for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             if isinstance(ch, NcclChannel) and ch.comm:
-                _lib.call("pc_p2p_destroy", ch.comm)
+                # the device is drained, so nothing is in flight on the pair: a local
+                # abort frees the communicator (ncclCommDestroy can wait on the peer)
+                _lib.call("pc_p2p_abort", ch.comm)
                 ch.comm = None
         if self._peer_made:
             self._peer_made = False
@@ -1087,6 +1090,9 @@ class PipelineEngine:
                 for ptr in self._peer_allocs:
                     _lib.call("pc_peer_free", ptr)
             self._peer_allocs = []
+            if self._abort_word is not None:
+                _lib.call("pc_host_word_free", self._abort_word[0])
+                self._abort_word = None
 
     # -- seeding (executor.py:405-414) --
     def _seed(self, actors: dict, params, batch, lr):
