@@ -186,6 +186,21 @@ int pc_embedding_bwd_acc(int dtype, int64_t T_, int64_t d, int64_t seq, int64_t 
  * sequence); overwrites logits with dlogits = softmax - onehot. */
 int pc_xent_fwd_bwd(int dtype, int64_t rows, int64_t V, int64_t seq, void* logits, int64_t ld,
                     const int32_t* tokens, float* row_loss, void* stream);
+/* Fused LM head + next-token cross-entropy (replaces `sub-sample-loss`, executor.py:72-75,
+ * for the GPT / Llama vocabularies; oracle/gpt.py head_loss).  Forward: logits [T, V] =
+ * h [T, d] x W[V, d]^T (tcgen05), whose epilogue also leaves per-row partial (max, sum exp)
+ * in ws; one streaming pass then writes row_loss [T] and overwrites logits in place with
+ * dlogits = softmax - onehot(next token) (zero rows at each sequence's last position).
+ * ws: pc_lmhead_xent_workspace bytes.  Backward: dh = dlogits W (B read K-major from
+ * W^T [d, V]) and dW (+)= dlogits^T h (fp32; accumulate = 1 adds onto dW). */
+int pc_lmhead_xent_workspace(int64_t T, int64_t V, int64_t d, int64_t* ld_stats, int64_t* bytes);
+int pc_lmhead_xent_fwd(int64_t T, int64_t V, int64_t d, int64_t seq, const void* h, int64_t ldh,
+                       const void* w, int64_t ldw, const int32_t* tokens, void* logits,
+                       int64_t ld_logits, void* ws, int64_t ws_bytes, float* row_loss,
+                       void* stream);
+int pc_lmhead_xent_bwd(int64_t T, int64_t V, int64_t d, const void* dlogits, int64_t ld,
+                       const void* h, int64_t ldh, const void* w_t, int64_t ld_wt, void* dh,
+                       int64_t ld_dh, float* dw, int64_t ld_dw, int accumulate, void* stream);
 /* Causal attention over packed qkv [B*S, ld_qkv]; lse/delta are [B,H,S] fp32. */
 int pc_attention_fwd(int dtype, int B, int H, int S, int hd, const void* qkv, int64_t ld_qkv,
                      void* o, int64_t ld_o, float* lse, void* stream);

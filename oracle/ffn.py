@@ -101,13 +101,63 @@ def ffn_step(params: dict, x: np.ndarray, layers: int, tied: bool):
     return loss, grads
 
 
+def ffn_step_skips(params: dict, x: np.ndarray, layers: int, tied: bool, skips) -> tuple:
+    """ffn_step with differentiable skip connections (ir.ModelConfig.skips): block
+    src's activation a_src = relu(z_src) is added to block dst's input.  The
+    reference has no executor for them (its planner rejects the gradient merge,
+    ir.py:568-571), so this restatement is pinned to torch float64 autograd
+    (tests/test_oracle.py) rather than to reference outputs.  The gradient
+    reaching a_src is the main-path gradient plus the skip partials in
+    ascending destination order (the planner's use order)."""
+    wname = [("w0" if (tied and k == layers - 1) else f"w{k}") for k in range(layers)]
+    hs, zs, acts = [], [], {}
+    h = x
+    for k in range(layers):
+        for src, dst in skips:
+            if dst == k:
+                h = h + acts[src]
+        hs.append(h)
+        z = h @ params[wname[k]]
+        zs.append(z)
+        if k < layers - 1:
+            h = np.maximum(z, 0.0)
+            acts[k] = h
+        else:
+            h = z
+    loss = float(np.asarray(0.5 * np.sum(h * h)))
+    g = h
+    back: dict[int, list] = {}
+    partial: dict[str, list] = {}
+    for k in reversed(range(layers)):
+        if k < layers - 1:
+            for _, extra in sorted(back.get(k, []), key=lambda t: t[0]):
+                g = g + extra
+            g = g * (zs[k] > 0.0)
+        w = params[wname[k]]
+        dx = g @ np.transpose(w)
+        partial.setdefault(wname[k], []).append((k, np.transpose(hs[k]) @ g))
+        for src, dst in skips:
+            if dst == k:
+                back.setdefault(src, []).append((dst, dx))
+        g = dx
+    grads = {}
+    for q, parts in partial.items():
+        parts.sort(key=lambda kv: kv[0])
+        acc = parts[0][1]
+        for _, v in parts[1:]:
+            acc = acc + v
+        grads[q] = acc
+    return loss, grads
+
+
 def run_reference_ffn(params: dict, batch: np.ndarray, M: int, layers: int, tied: bool,
-                      lr: float = 0.1):
+                      lr: float = 0.1, skips=()):
     """executor.py:117-134 on the FFN model: returns (grads, losses, new_params)."""
     grads = {q: np.zeros_like(v) for q, v in params.items()}
     losses = []
     for mb in split_batch(batch, M):
-        loss, g = ffn_step(params, mb, layers, tied)
+        loss, g = (ffn_step_skips(params, mb, layers, tied, skips) if skips
+                   else ffn_step(params, mb, layers, tied))
         losses.append(loss)
         for q in params:
             grads[q] = grads[q] + g[q]

@@ -95,6 +95,11 @@ SIGNATURES: dict[str, list] = {
     "pc_attention_gqa_bwd": [_c_i, _c_i, _c_i, _c_i, _c_i, _c_i, _c_p, _c_i64, _c_p, _c_p, _c_i64,
                              _c_p, _c_p, _c_p, _c_i64, _c_p],
     "pc_attention_set_impl": [_c_i],
+    "pc_lmhead_xent_workspace": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)],
+    "pc_lmhead_xent_fwd": [_c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p,
+                           _c_i64, _c_p, _c_i64, _c_p, _c_p],
+    "pc_lmhead_xent_bwd": [_c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p,
+                           _c_i64, _c_p, _c_i64, _c_i, _c_p],
     "pc_p2p_available": [],
     "pc_p2p_unique_id": [_c_p],
     "pc_p2p_comm_init": [ctypes.POINTER(_c_p), _c_i, _c_p, _c_i],
@@ -154,7 +159,7 @@ _NON_LAUNCH = {"pc_version", "pc_device_sm_count", "pc_gemm_set_tile_n", "pc_gem
                "pc_p2p_comm_init", "pc_p2p_abort", "pc_p2p_destroy",
                "pc_peer_alloc", "pc_peer_free", "pc_peer_open", "pc_peer_close",
                "pc_stream_write_u32", "pc_stream_wait_u32", "pc_graph_kernel_nodes",
-               "pc_host_word_alloc", "pc_host_word_free"}
+               "pc_host_word_alloc", "pc_host_word_free", "pc_lmhead_xent_workspace"}
 launch_count = 0
 
 

@@ -14,7 +14,7 @@ namespace pp200 {
 int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
                  const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                  int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
-                 int64_t ldaux_out, cudaStream_t st);
+                 int64_t ldaux_out, cudaStream_t st, float2* stats = nullptr, int64_t ld_stats = 0);
 
 namespace {
 

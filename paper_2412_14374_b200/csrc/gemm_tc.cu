@@ -52,6 +52,11 @@ struct TcEpi {
   int64_t ldaux_out;
   int M, N, flags, out_f32;
   int n_fast;  // tile raster: 1 = consecutive tiles walk N (share the A rows), 0 = walk M
+  // LM-head softmax statistics (EK_PLAIN only): per row, per (N tile, epilogue
+  // column group), the running (max, sum exp(x - max)) of the bf16-rounded
+  // outputs that group stored -- stats[row * ld_stats + n_tile * TC_EPI_G + group]
+  float2* stats;
+  int ld_stats;
 };
 
 // First k-block of split ``sp`` (sp = ksplit: the end).  Ordered split-K
@@ -537,6 +542,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
       if constexpr (EK == EK_PLAIN) {
+        float xm = -INFINITY, xs = 0.f;   // softmax statistics of this row (ep.stats)
 #pragma unroll 1
         for (int cc = cstart; cc < cend; cc += cstep) {
           const uint32_t my = nchunk++;
@@ -557,7 +563,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
             bulk_commit();
           }
+          if (ep.stats != nullptr) {
+            // online (max, sum exp) over the values as stored (bf16-rounded),
+            // columns past N excluded; exp2 with log2(e) folded into one FMA
+            constexpr float L2E = 1.4426950408889634f;
+            const int nvalid = N - (n0 + cc);
+            float cm = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+              v[i] = i < nvalid ? __bfloat162float(__float2bfloat16_rn(v[i])) : -INFINITY;
+              cm = fmaxf(cm, v[i]);
+            }
+            const float mn = fmaxf(xm, cm);
+            if (mn != -INFINITY) {
+              const float nm = -mn * L2E;
+              float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+              for (int i = 0; i < 64; ++i) {
+                float e;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(v[i], L2E, nm)));
+                part[i & 3] += e;
+              }
+              float sc;
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(sc) : "f"(fmaf(xm, L2E, nm)));
+              xs = xs * sc + ((part[0] + part[1]) + (part[2] + part[3]));
+              xm = mn;
+            }
+          }
         }
+        if (ep.stats != nullptr && row < M)
+          ep.stats[static_cast<int64_t>(row) * ep.ld_stats + ni * TC_EPI_G + grp] = make_float2(xm, xs);
       } else if constexpr (EK == EK_ACT) {
         // U (pre-activation) staged in buffer B, C in buffer A, one bulk group
         // each: before restaging either, the group two back has been read
@@ -985,7 +1020,7 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
 int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
                  const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                  int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
-                 int64_t ldaux_out, cudaStream_t st) {
+                 int64_t ldaux_out, cudaStream_t st, float2* stats, int64_t ld_stats) {
   PP_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem");
   PP_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
   PP_CHECK_ARG(!((epi & PC_EPI_ACCUM) && (epi & PC_EPI_SPLITK_ZERO_C)),
@@ -1070,9 +1105,13 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     rc = make_tmap_c(&tc, C, N, M, ldc, out_f32 != 0, cw64);
     if (rc) return rc;
   }
+  if (stats != nullptr) {
+    PP_CHECK_ARG(ek == EK_PLAIN, "gemm: softmax statistics need a plain bf16 C through TMA");
+    PP_CHECK_ARG(ld_stats >= ((N + bn - 1) / bn) * TC_EPI_G, "gemm: statistics row too short");
+  }
   TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, tma_a ? 1 : 0, cw64 ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
            aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi | (g_ablate << 16), out_f32,
-           n_fast ? 1 : 0};
+           n_fast ? 1 : 0, stats, static_cast<int>(ld_stats)};
   const int iM = static_cast<int>(M), iN = static_cast<int>(N), iK = static_cast<int>(K);
   switch (bn * 4 + cg) {
     case 256 * 4 + 2: return dispatch_majors<256, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);

@@ -186,6 +186,7 @@ class DeviceOps:
         self._red = None
         self._red_side = None
         self._side_stream = None
+        self._xent_ws = None     # LM-head softmax statistics (pc_lmhead_xent_fwd)
         self.step_epoch = 0  # bumped by the executor at every step
 
     # ------------------------------------------------------------------ alloc
@@ -795,16 +796,34 @@ class DeviceOps:
         w0: Param = env[op.operands[1]]
         x = tensor_of(env[op.operands[2]])
         T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
-        logits = self.empty((T, V), self.mode.act)
-        self._gemm(self.mode.act, 0, 1, T, V, d, h, d, self._slice(w0.compute(), self._elay, "wte"),
-                   d, logits, V)
-        rows = self.empty((T,), torch.float32)
-        call("pc_xent_fwd_bwd", self.mode.pc_act, T, V, cfg.seq_len, logits.data_ptr(), V,
-             x.data_ptr(), rows.data_ptr(), self.st)
+        logits, rows = self._lmhead_xent(h, self._slice(w0.compute(), self._elay, "wte"), x)
         loss = self.empty((), torch.float32)
         call("pc_sum_f32", T, rows.data_ptr(), loss.data_ptr(), self.st)
         hv.saved[op.id] = dict(dlogits=logits)
         return loss
+
+    def _lmhead_xent(self, h, w, x):
+        """logits = h W^T with the cross-entropy folded in: (dlogits in place of
+        the logits, per-row losses).  bf16: pc_lmhead_xent_fwd (softmax statistics
+        from the GEMM epilogue, one streaming pass); fp32 parity mode: GEMM then
+        pc_xent_fwd_bwd."""
+        cfg = self.gpt
+        T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
+        logits = self.empty((T, V), self.mode.act)
+        rows = self.empty((T,), torch.float32)
+        if self.mode.act == torch.bfloat16 and V % 8 == 0:
+            if self._xent_ws is None:
+                lds, nb = ctypes.c_int64(), ctypes.c_int64()
+                call("pc_lmhead_xent_workspace", T, V, d, ctypes.byref(lds), ctypes.byref(nb))
+                self._xent_ws = self.empty((nb.value,), torch.uint8)
+            call("pc_lmhead_xent_fwd", T, V, d, cfg.seq_len, h.data_ptr(), d, w.data_ptr(), d,
+                 x.data_ptr(), logits.data_ptr(), V, self._xent_ws.data_ptr(),
+                 self._xent_ws.numel(), rows.data_ptr(), self.st)
+            return logits, rows
+        self._gemm(self.mode.act, 0, 1, T, V, d, h, d, w, d, logits, V)
+        call("pc_xent_fwd_bwd", self.mode.pc_act, T, V, cfg.seq_len, logits.data_ptr(), V,
+             x.data_ptr(), rows.data_ptr(), self.st)
+        return logits, rows
 
     def _head_bwd(self, op, env, acc=None):
         cfg = self.gpt
@@ -1062,12 +1081,7 @@ class DeviceOps:
         wo: Param = env[op.operands[1]]
         x = tensor_of(env[op.operands[2]])
         T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
-        logits = self.empty((T, V), self.mode.act)
-        self._gemm(self.mode.act, 0, 1, T, V, d, h, d,
-                   self._slice(wo.compute(), self._hlay, "w_head"), d, logits, V)
-        rows = self.empty((T,), torch.float32)
-        call("pc_xent_fwd_bwd", self.mode.pc_act, T, V, cfg.seq_len, logits.data_ptr(), V,
-             x.data_ptr(), rows.data_ptr(), self.st)
+        logits, rows = self._lmhead_xent(h, self._slice(wo.compute(), self._hlay, "w_head"), x)
         loss = self.empty((), torch.float32)
         call("pc_sum_f32", T, rows.data_ptr(), loss.data_ptr(), self.st)
         hv.saved[op.id] = dict(dlogits=logits)

@@ -203,3 +203,26 @@ def test_full_remat_matches_reference_fp64(fam, P, M, V, tied):
     assert np.array_equal(a.losses, b.losses)
     for q in a.grads:
         assert np.array_equal(a.grads[q], b.grads[q]), q
+
+
+@pytest.mark.parametrize("fam,P,M,V,tied", [("gpipe", 4, 4, 1, False), ("1f1b", 4, 8, 1, False),
+                                            ("1f1b", 4, 8, 1, True), ("interleaved", 2, 4, 2, False)])
+@pytest.mark.parametrize("remat", ["none", "full-per-stage"])
+def test_differentiable_skips_match_oracle_fp64(fam, P, M, V, tied, remat):
+    """activations joined to non-adjacent later blocks
+    (ir.ModelConfig.skips) -- the activation is sent forward past a stage, its
+    gradient comes back to the producer's stage and is summed there.  fp64
+    results equal the oracle (pinned to torch autograd) to the reference's
+    1e-12 gate, under stashing and full remat."""
+    from test_skips_cpu import SKIPS, plan
+    p, tg, cp = plan(fam, P, M, V, tied=tied)
+    rng = np.random.default_rng(3)
+    dims = {q: p.graph.spec_of(q).dims for q in p.graph.params}
+    params = ffn.init_params(dims, rng)
+    batch = ffn.init_batch(M, 4, 8, rng)
+    g, l, w = ffn.run_reference_ffn(params, batch, M, 6, tied, skips=SKIPS)
+    res = run_pipelined(cp, tg, params, batch, remat=remat)
+    assert ffn.rel(res.losses, l) < 1e-12
+    for q in g:
+        assert ffn.rel(res.grads[q], g[q]) < 1e-12, q
+        assert ffn.rel(res.new_params[q], w[q]) < 1e-12, q

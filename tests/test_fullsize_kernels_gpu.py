@@ -185,3 +185,43 @@ def test_gpt2_small_width_step_matches_oracle():
     for q in g:
         assert ffn.rel(res.grads[q], g[q]) < TOL, (q, ffn.rel(res.grads[q], g[q]))
         assert ffn.rel(res.new_params[q], w[q]) < TOL, q
+
+
+@pytest.mark.parametrize("name,B,S,V,d", [
+    ("C2 LM head (8 x 1024 tokens, vocab 50304, d 768)", 8, 1024, 50304, 768),
+    ("ragged vocab tile, short sequences", 3, 40, 1000, 256),
+    ("C5 LM head slice (1 x 1024 tokens, vocab 128256, d 4096)", 1, 1024, 128256, 4096),
+])
+def test_lmhead_xent_fused(name, B, S, V, d):
+    """pc_lmhead_xent_fwd (softmax statistics from the logits GEMM's epilogue + one
+    streaming pass) and pc_lmhead_xent_bwd against float64: row losses, dlogits
+    (overwriting the logits), dh and dW (onto an existing accumulator)."""
+    T = B * S
+    g = torch.Generator(device="cuda").manual_seed(V + d)
+    h = (torch.randn(T, d, device="cuda", generator=g)).to(torch.bfloat16)
+    w = (torch.randn(V, d, device="cuda", generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
+    tokens = torch.randint(0, V, (B, S), device="cuda", generator=g, dtype=torch.int32)
+    lds, nb = ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("pc_lmhead_xent_workspace", T, V, d, ctypes.byref(lds), ctypes.byref(nb))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    logits = torch.empty(T, V, device="cuda", dtype=torch.bfloat16)
+    rows = torch.empty(T, device="cuda")
+    st = _stream()
+    _lib.call("pc_lmhead_xent_fwd", T, V, d, S, h.data_ptr(), d, w.data_ptr(), d, tokens.data_ptr(),
+              logits.data_ptr(), V, ws.data_ptr(), ws.numel(), rows.data_ptr(), st)
+    wt = w.t().contiguous()
+    dh = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    dw = torch.full((V, d), 0.5, device="cuda")
+    _lib.call("pc_lmhead_xent_bwd", T, V, d, logits.data_ptr(), V, h.data_ptr(), d, wt.data_ptr(), V,
+              dh.data_ptr(), d, dw.data_ptr(), d, 1, st)
+    torch.cuda.synchronize()
+    ref_logits = h.double() @ w.double().t()
+    rl, dl = R.xent_rows(ref_logits, tokens)
+    assert R.rel(rows, rl) < 1e-2, name
+    assert abs(rows.double().sum().item() - rl.sum().item()) < 1e-3 * rl.abs().sum().item(), name
+    assert R.rel(logits, dl) < TOL, name
+    assert torch.count_nonzero(logits.view(B, S, V)[:, -1]).item() == 0
+    rdh = dl @ w.double()
+    rdw = dl.t() @ h.double() + 0.5
+    assert R.rel(dh, rdh) < TOL, name
+    assert R.rel(dw, rdw) < TOL, name

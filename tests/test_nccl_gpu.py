@@ -165,6 +165,23 @@ def _worker(rank, world, port, case, q):
                 ref_losses.append(lk)
             q.put((rank, state, losses, ref, ref_losses))
             return
+        if case == "ffn-skip":
+            # differentiable non-adjacent skips over real channels (peer transport):
+            # activations forward past a stage, their gradients back to the producer
+            import sys as _sys
+            _sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+            from test_skips_cpu import SKIPS, plan
+            M = 8
+            p, tg, cp = plan("1f1b", world, M, yields=(2, 3, 5)[:world - 1])
+            rng = np.random.default_rng(3)
+            params = ffn.init_params({q: p.graph.spec_of(q).dims for q in p.graph.params}, rng)
+            batch = ffn.init_batch(M, 4, 8, rng)
+            res = run_pipelined(cp, tg, params, batch)
+            ref = ffn.run_reference_ffn(params, batch, M, 6, False, skips=SKIPS)
+            q.put((rank, res.grads, None if res.losses is None else np.asarray(res.losses),
+                   res.new_params, ref, dict(res.stats.channel_counts), res.stats.driver_messages,
+                   {k: len(v) for k, v in cp.channels.items()}))
+            return
         if case == "ffn":
             L, M = 2 * world, 4
             p = I.derive_backward(I.partition_stages(I.build_model(I.ModelConfig(
@@ -231,7 +248,8 @@ def _run(case, world):
 
 @pytest.mark.parametrize("case,tol,world", [("ffn", 1e-12, 2), ("gpt", 2e-2, 2),
                                             ("gpt-interleaved", 2e-2, 2), ("ffn", 1e-12, 4),
-                                            ("gpt", 2e-2, 4)])
+                                            ("gpt", 2e-2, 4), ("ffn-skip", 1e-12, 2),
+                                            ("ffn-skip", 1e-12, 4)])
 def test_two_gpu_nccl_pipeline_matches_oracle(case, tol, world):
     outs = _run(case, world)
     grads, new, losses = {}, {}, None
