@@ -57,7 +57,21 @@ WORKLOADS = {
                name="C4 gpt3-1.3B 24L d2048 h16x128 ff8192 V50304 seq2048"),
     "C5": dict(family="llama", kw=C5, M=16, schedule="1f1b", V=1,
                name="C5 llama-8B 32L d4096 h32/kv8x128 swiglu14336 V128256 seq4096"),
+    # The reference's own model (pipecraft ModelConfig: H = relu(H W), summed-square
+    # loss) as the FFN surrogate of C2: 12 blocks of width 768,
+    # 8 microbatches x 8192 rows, float64 -- the reference's arithmetic -- so the
+    # reference's run_reference (oracle/ffn.py, bit-identical to it) is timed on
+    # exactly this configuration by --impl reference --workload FFN-C2.
+    "FFN-C2": dict(family="ffn", kw=dict(layers=12, width=768, microbatch_size=8192), M=8,
+                   schedule="1f1b", V=1,
+                   name="FFN-C2 pipecraft FFN surrogate of C2: 12L w768 rows8192 fp64"),
 }
+
+
+def ffn_flops_per_row(kw) -> float:
+    """Algorithmic FLOPs of one row through the FFN stack, fwd + bwd: 3 GEMMs of
+    2 w^2 per block (the reference's dead first-block dX, ir.py:510-511, not counted)."""
+    return 6.0 * kw["layers"] * kw["width"] ** 2
 
 
 def peaks():
@@ -114,6 +128,18 @@ def build_plan(P, cfg_kw, M, mode="bf16", family="gpt", schedule="1f1b", V=1):
     from paper_2412_14374_b200 import taskgraph as T
     inter = schedule == "interleaved" and P > 1 and V > 1
     stages = P * V if inter else P
+    if family == "ffn":
+        L = cfg_kw["layers"]
+        base = dict(cfg_kw, elem_bytes=8 if mode == "fp64" else (4 if mode == "fp32" else 2))
+        yields = I.balanced_yields([1.0] * L, stages) if stages > 1 else None
+        cfg = I.ModelConfig(**base, yields=yields, yield_every=L)
+        p = I.derive_backward(I.partition_stages(I.build_model(cfg)))
+        s = S.interleaved_1f1b(P, M, V) if inter else S.one_f_one_b(P, M)
+        tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, s)), p)
+        cp = C.infer_comms(tg, s)
+        rep = C.check_deadlock_free(cp)
+        assert rep.ok, str(rep)
+        return cfg, tg, C.fuse(C.insert_deletions(cp, tg), tg)
     Cfg, build = (I.GPTConfig, I.build_gpt) if family == "gpt" else (I.LlamaConfig, I.build_llama)
     costs_fn = block_costs if family == "gpt" else llama_block_costs
     base = Cfg(**cfg_kw, yield_every=cfg_kw["layers"] + 2)
@@ -380,6 +406,20 @@ def _oracle_sample(wl):
     from threadpoolctl import threadpool_limits
     from paper_2412_14374_b200 import ir as I
     kw = wl["kw"]
+    if wl["family"] == "ffn":
+        # one whole microbatch of the same configuration through run_reference
+        from oracle import ffn as of
+        rng = np.random.default_rng(0)
+        L, w, rows = kw["layers"], kw["width"], kw["microbatch_size"]
+        params = of.init_params({f"w{k}": (w, w) for k in range(L)}, rng)
+        batch = of.init_batch(1, rows, w, rng)
+        with threadpool_limits(limits=os.cpu_count()):
+            t0 = time.perf_counter()
+            of.run_reference_ffn(params, batch, 1, L, False)
+            dt = time.perf_counter() - t0
+        return rows / dt, dt, (f"oracle/ffn.py run_reference (bit-identical restatement of "
+                               f"executor.py:117-134, numpy float64), 1 microbatch x {rows} rows "
+                               f"of the same config ({dt:.1f} s)")
     llama = wl["family"] == "llama"
     full = (I.LlamaConfig if llama else I.GPTConfig)(**kw)
     small = kw is C2
@@ -439,7 +479,10 @@ def run_reference_impl(args, rank, world):
         times.append(dt)
     tok_s = float(np.mean(rates))
     from paper_2412_14374_b200 import ir as I
-    cfg = (I.LlamaConfig if wl["family"] == "llama" else I.GPTConfig)(**wl["kw"])
+    if wl["family"] == "ffn":
+        fpt = ffn_flops_per_row(wl["kw"])
+    else:
+        fpt = (I.LlamaConfig if wl["family"] == "llama" else I.GPTConfig)(**wl["kw"]).flops_per_token()
     line = {
         "impl": "reference", "metric": METRIC,
         "value": round(tok_s, 3), "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -447,8 +490,9 @@ def run_reference_impl(args, rank, world):
         "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl["name"], "schedule": wl["schedule"],
+                   "microbatches": wl["M"],
                    "sample": desc + " per step (bounded CPU sample)"},
-        "model_tflops_per_gpu": round(cfg.flops_per_token() * tok_s / 1e12, 5),
+        "model_tflops_per_gpu": round(fpt * tok_s / 1e12, 5),
         "cpu_baseline": {"value": round(tok_s, 3), "unit": "tokens/s", "cores": os.cpu_count(),
                          "kind": "port", "sample": desc},
         "e2e": {"value": round(tok_s, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -499,13 +543,22 @@ def main():
     M = args.microbatches or wl["M"]
     Vv = args.virtual if args.virtual is not None else wl["V"]
     sched = args.schedule or wl["schedule"]
-    cfg, tg, cp = build_plan(P, wl_kw, M, family=wl["family"], schedule=sched, V=Vv)
+    ffn_wl = wl["family"] == "ffn"
+    mode = "fp64" if ffn_wl else "bf16"
+    cfg, tg, cp = build_plan(P, wl_kw, M, mode=mode, family=wl["family"], schedule=sched, V=Vv)
     sched_used = "interleaved" if (sched == "interleaved" and P > 1 and Vv > 1) else "1f1b"
     dev = torch.device("cuda", local)
-    params = init_params_device(cfg, dev)
     rng = np.random.default_rng(1234)
-    tokens_host = rng.integers(0, cfg.vocab, size=(M * cfg.microbatch_size, cfg.seq_len),
-                               dtype=np.int32)
+    if ffn_wl:
+        g = torch.Generator(device=dev).manual_seed(0)
+        w_ = wl_kw["width"]
+        params = {q: torch.randn(w_, w_, device=dev, generator=g, dtype=torch.float64) * 0.4
+                  / np.sqrt(w_) for q in sorted(tg.partition.graph.params)}
+        tokens_host = rng.standard_normal((M * wl_kw["microbatch_size"], w_))
+    else:
+        params = init_params_device(cfg, dev)
+        tokens_host = rng.integers(0, cfg.vocab, size=(M * cfg.microbatch_size, cfg.seq_len),
+                                   dtype=np.int32)
     if wl["family"] == "llama":
         # token ids + position ids (the skip tensors every later stage reads)
         pos_host = np.tile(np.arange(cfg.seq_len, dtype=np.int32), (M * cfg.microbatch_size, 1))
@@ -518,7 +571,14 @@ def main():
         tokens_dev = torch.from_numpy(tokens_host).to(dev)
         tokens_pinned = torch.from_numpy(tokens_host).pin_memory()
         h2d_bytes = int(tokens_host.nbytes)
-    eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg, remat=args.remat)
+    t_start = time.perf_counter()
+
+    def progress(msg):
+        if rank == 0:
+            print(f"[bench {time.perf_counter() - t_start:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+    progress(f"{args.workload}: plan built, {len(tg.partition.fwd_programs)} stages, M={M}")
+    eng = PipelineEngine(cp, tg, mode=mode, gpt=None if ffn_wl else cfg, remat=args.remat)
     # resident training state: every step (eager or replayed) is a real SGD
     # step on the previous step's weights, tied w0 re-broadcast included
     eng.load_params(params)
@@ -527,6 +587,7 @@ def main():
     for _ in range(2):   # eager warm-up: NCCL connections, kernel attributes, allocator
         eng.step(None, tokens_dev, lr=1e-4, timeout_s=600, to_host=False)
     torch.cuda.synchronize()
+    progress("eager warm-up steps done")
     if use_graph:
         cap = eng.capture(None, tokens_dev, lr=1e-4)
         run = lambda b: cap.replay(None if b is tokens_dev else b)
@@ -555,6 +616,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
+    progress("captured, warm")
     # ---- device-resident timed region ----
     torch.cuda.reset_peak_memory_stats(dev)
     clocks = ClockSampler(local)
@@ -579,6 +641,7 @@ def main():
     launches = cap.kernels if use_graph else int((_lib.launch_count - launches0) / args.steps)
     clk = clocks.stop()
 
+    progress(f"timed: {ms:.1f} ms/step")
     # ---- e2e through the public API: pinned host tokens -> device, losses -> host ----
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -617,10 +680,10 @@ def main():
         with open(args.gantt, "w") as f:
             f.write(TL.render_svg(timeline, P, title=f"{args.workload} 1F1B P={P} M={M} measured,"))
 
-    tokens_per_step = M * cfg.tokens
+    tokens_per_step = M * (wl_kw["microbatch_size"] if ffn_wl else cfg.tokens)
     value = tokens_per_step / (ms / 1000)
     e2e = tokens_per_step / (e2e_ms / 1000)
-    flops_step = cfg.flops_per_token() * tokens_per_step
+    flops_step = (ffn_flops_per_row(wl_kw) if ffn_wl else cfg.flops_per_token()) * tokens_per_step
     tflops_gpu = flops_step / (ms / 1000) / P / 1e12
     burst, sustained, hbm, peak_kind = peaks()
     Vi = Vv if sched_used == "interleaved" else 1
@@ -631,18 +694,26 @@ def main():
         fp = tg.partition.fwd_programs
         stage_blocks = sum(1 for st in range(0, len(fp), P) for op in fp[st].ops
                            if op.kind in ("gpt-block", "llama-block"))
-        roof = gemm_roofline(cfg, P, stage_blocks, ms, burst, M)
-        roof["peak_kind"] = peak_kind
+        if ffn_wl:
+            # fp64 DFMA GEMMs: no bf16 tensor-core roofline applies (the FFN workload
+            # exists for the same-config comparison with the reference's CPU path)
+            roof = None
+        else:
+            roof = gemm_roofline(cfg, P, stage_blocks, ms, burst, M)
+            roof["peak_kind"] = peak_kind
         cpu = None if args.no_cpu_baseline else cpu_baseline(wl)
+        mbs_ = wl_kw["microbatch_size"]
+        seq_ = 1 if ffn_wl else cfg.seq_len
         line = {
             "metric": METRIC,
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic tokens, random-init weights",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if ffn_wl else "bf16",
+            "data": ("synthetic N(0,1) rows (tokens = rows), random-init weights" if ffn_wl
+                     else "synthetic tokens, random-init weights"),
             "config": {"workload": wl_name,
-                       "global_batch": M * cfg.microbatch_size, "seq_len": cfg.seq_len,
-                       "microbatches": M, "microbatch_size": cfg.microbatch_size,
+                       "global_batch": M * mbs_, "seq_len": seq_,
+                       "microbatches": M, "microbatch_size": mbs_,
                        "schedule": sched_used, "virtual_stages_per_gpu": Vv if sched_used ==
                        "interleaved" else 1, "stages": len(tg.partition.fwd_programs),
                        "yields": list(cfg.yields or []),
@@ -651,12 +722,13 @@ def main():
                        "transport": eng.transport if world > 1 else None,
                        "remat": args.remat,
                        "training": "resident params, in-place SGD each step"
-                                   + (", tied w0 re-broadcast to the head stage" if P > 1 else "")},
+                                   + (", tied w0 re-broadcast to the head stage"
+                                      if P > 1 and not ffn_wl else "")},
             "model_tflops_per_gpu": round(tflops_gpu, 1),
             "peak_hbm_gb_rank0": round(peak_hbm / 1e9, 2),
             "peak_hbm_covers": "timed steps: torch allocator peak (reset before the timed region) "
                                "+ peer receive slots; excludes NCCL-internal buffers",
-            "frac_of_bf16_peak": round(tflops_gpu / burst, 4),
+            "frac_of_bf16_peak": None if ffn_wl else round(tflops_gpu / burst, 4),
             "bubble": {"measured": round(bubble, 4), "ideal": round(ideal, 4),
                        "achievable": round(achievable, 4)},
             "roofline": roof,

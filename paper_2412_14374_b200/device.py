@@ -83,6 +83,8 @@ class Act:
 
 _ABLATE_BIAS = os.environ.get("PP200_ABLATE_BIAS_GRAD") == "1"
 _LN_PARAMS_MAIN = os.environ.get("PP200_LN_PARAMS_MAIN") == "1"   # A/B switch for profiling
+# A/B switch: 0 = logits GEMM then the stand-alone cross-entropy kernel (pc_xent_fwd_bwd)
+_XENT_FUSED = os.environ.get("PP200_XENT_FUSED", "1") != "0"
 
 
 class PeerBuf:
@@ -811,7 +813,7 @@ class DeviceOps:
         T, d, V = cfg.tokens, cfg.d_model, cfg.vocab
         logits = self.empty((T, V), self.mode.act)
         rows = self.empty((T,), torch.float32)
-        if self.mode.act == torch.bfloat16 and V % 8 == 0:
+        if self.mode.act == torch.bfloat16 and V % 8 == 0 and _XENT_FUSED:
             if self._xent_ws is None:
                 lds, nb = ctypes.c_int64(), ctypes.c_int64()
                 call("pc_lmhead_xent_workspace", T, V, d, ctypes.byref(lds), ctypes.byref(nb))

@@ -1375,9 +1375,16 @@ class CapturedStep:
     def set_inputs(self, batch):
         tg = self.engine.tg
         M = tg.schedule.num_microbatches
-        mbs = split_batch(batch, M)
+        # one array for a single-input graph, else {input name: array} (as _seed)
+        if isinstance(batch, dict):
+            split = {name: split_batch(v, M) for name, v in batch.items()}
+        else:
+            split = {None: split_batch(batch, M)}
         for bid, dst in self.inputs.items():
-            src = mbs[tg.buffers[bid].meta["microbatch"]]
+            meta = tg.buffers[bid].meta
+            name = meta.get("value", meta.get("input"))
+            mbs = split[name] if name in split else split[next(iter(split))]
+            src = mbs[meta["microbatch"]]
             if isinstance(src, np.ndarray):
                 src = torch.from_numpy(np.ascontiguousarray(src))
             dst = tensor_of(dst)
