@@ -654,6 +654,7 @@ def main():
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
+    progress(f"e2e: {e2e_ms:.1f} ms/step")
     # ---- one instrumented step (same warmed engine) for the bubble ----
     barrier()
     if use_graph:
@@ -670,6 +671,7 @@ def main():
         gathered = [None] * world
         dist.all_gather_object(gathered, timeline)
         timeline = [e for part in gathered for e in part]
+    progress("timeline step done")
     from paper_2412_14374_b200.executor import RunStats
     from paper_2412_14374_b200 import timeline as TL
     bubble = RunStats(timeline=timeline).bubble_fraction(P)
@@ -694,6 +696,7 @@ def main():
         fp = tg.partition.fwd_programs
         stage_blocks = sum(1 for st in range(0, len(fp), P) for op in fp[st].ops
                            if op.kind in ("gpt-block", "llama-block"))
+        progress("bubble / achievable computed")
         if ffn_wl:
             # fp64 DFMA GEMMs: no bf16 tensor-core roofline applies (the FFN workload
             # exists for the same-config comparison with the reference's CPU path)
@@ -701,7 +704,9 @@ def main():
         else:
             roof = gemm_roofline(cfg, P, stage_blocks, ms, burst, M)
             roof["peak_kind"] = peak_kind
+        progress("roofline measured")
         cpu = None if args.no_cpu_baseline else cpu_baseline(wl)
+        progress("cpu baseline measured")
         mbs_ = wl_kw["microbatch_size"]
         seq_ = 1 if ffn_wl else cfg.seq_len
         line = {
