@@ -339,6 +339,8 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak, M=M_MICRO):
         if count == 0:
             continue
         Mm, N, K, ta, tb, epi = shape[:6]
+        if os.environ.get("PP200_BENCH_VERBOSE") == "1":
+            print(f"[bench] roofline shape {shape}", file=sys.stderr, flush=True)
         args, keep = gemm_args(shape, st)
         # device time of back-to-back launches, issued from a CUDA graph as in
         # the step (host launch cost would otherwise pace the short GEMMs)

@@ -970,7 +970,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn() { return tmap_encoder(); }
 // split-K: exactly 2 K halves reduce-added onto a zero-filled fp32 C
 // (0 + a + b == 0 + b + a bitwise), only when the caller allows it.
 static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool can_split,
-                         int* bn_out, int* cg_out, int* ks_out, int max_split = 2) {
+                         int* bn_out, int* cg_out, int* ks_out, int max_split = 2,
+                         bool ordered = false) {
   struct Cand { int bn, cg; double eff; };
   const Cand cands[7] = {{256, 2, 1.0}, {192, 2, 0.97}, {256, 1, 0.88}, {192, 1, 0.85},
                          {128, 2, 0.78}, {128, 1, 0.75}, {64, 1, 0.45}};
@@ -995,6 +996,11 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
     const int64_t slots = sms / c.cg;
     for (int ks = 1; ks <= max_split; ks *= 2) {
       if (K < static_cast<int64_t>(ks) * TC_BK * 8) break;   // >= 8 k-blocks per split
+      // Ordered split-K makes split s of a tile wait for split s-1 on another CTA.
+      // With more units than co-resident CTAs a resident CTA can wait on a unit
+      // whose CTA is not resident yet while every resident CTA waits too (a
+      // deadlock, seen on C4's 512-unit weight gradients): one wave only.
+      if (ordered && ks > 1 && tiles * ks > slots) break;
       const int64_t waves = (tiles * ks + slots - 1) / slots;
       const double score = static_cast<double>(M) * N * ks /
                            (static_cast<double>(waves) * slots * tm * c.bn) * c.eff *
@@ -1040,7 +1046,7 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   int bn, cg, ksplit;
   // (the ordered protocol handles 4 splits, but measured on the C2 weight
   // GEMMs a 4-link add chain costs more than the wave it fills: 2 at most)
-  choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit, 2);
+  choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit, 2, ordered);
   // raster: an A operand far larger than L2 (the LM-head gradients: 824 MB of
   // logit gradients) is streamed once when the tiles sharing its rows run
   // together; otherwise walk M (B is the large, reused operand)
@@ -1130,7 +1136,8 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
 extern "C" int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_ok,
                                    int* bn, int* cta_pair, int* ksplit) {
   PP_CHECK_ARG(M > 0 && N > 0 && K > 0 && bn && cta_pair && ksplit, "gemm_tile_choice: bad args");
-  pp200::choose_tiles(transB != 0, M, N, K, split_ok != 0, bn, cta_pair, ksplit, 2);
+  pp200::choose_tiles(transB != 0, M, N, K, split_ok != 0, bn, cta_pair, ksplit, 2,
+                      split_ok == 2);
   return PC_OK;
 }
 
