@@ -515,7 +515,7 @@ def main():
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--schedule", default=None, choices=["1f1b", "interleaved"],
                     help="default: the workload's (C4: interleaved)")
-    ap.add_argument("--virtual", type=int, default=None,
+    ap.add_argument("--vstages", type=int, default=None,
                     help="virtual stages per GPU for interleaved 1F1B (default: the workload's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gantt", default=None, help="write the measured timeline as an SVG Gantt chart")
@@ -543,7 +543,7 @@ def main():
     wl = WORKLOADS[args.workload]
     wl_kw, wl_name = wl["kw"], wl["name"]
     M = args.microbatches or wl["M"]
-    Vv = args.virtual if args.virtual is not None else wl["V"]
+    Vv = args.vstages if args.vstages is not None else wl["V"]
     sched = args.schedule or wl["schedule"]
     ffn_wl = wl["family"] == "ffn"
     mode = "fp64" if ffn_wl else "bf16"

@@ -346,9 +346,12 @@ __global__ void __launch_bounds__(256, 2)
 
 
 // ------------------------------------------------------------------ backward
-// NG elementwise warps per TMEM lane quarter, each owning CW = 64 / NG score
-// columns (and HD / NG output columns in the epilogues)
-constexpr int BW_NG = 4, BW_CW = 64 / BW_NG;
+// NG elementwise warps per TMEM lane quarter.  They form BW_SETS sets that take
+// alternate score blocks (set = block % 2 = its score buffer), so one set's
+// TMEM loads / stores and barrier round trips overlap the other set's math;
+// inside a set each warp owns CW = 64 / (NG / SETS) score columns.  In the
+// epilogues every warp owns HD / NG output columns.
+constexpr int BW_NG = 4, BW_SETS = 2, BW_CW = 64 * BW_SETS / BW_NG;
 
 // NC * 8 fp32 accumulator values -> bf16 (scaled) in global memory.
 template <int NC>
@@ -392,7 +395,7 @@ template <int HD>
 struct BwdKV {
   static constexpr int KEYS = 128, BQ = 64;
   static constexpr int NP = HD / 64;
-  static constexpr int SBUF = HD == 64 ? 3 : 2;
+  static constexpr int SBUF = BW_SETS;  // one score buffer per elementwise set
   static constexpr int STAGES = HD == 64 ? 5 : 4;
   static constexpr int KVBUF = HD == 64 ? 2 : 1;
   static constexpr int KV_PANEL = KEYS * 64 * 2;   // 16 KB
@@ -448,7 +451,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
     }
     for (int i = 0; i < K::SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], K::EW);
+      mbar_init(&p_full[i], K::EW / BW_SETS);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(done, 1);
@@ -571,8 +574,9 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
   } else if (warp >= 4) {
     constexpr int CW = BW_CW, CO = HD / BW_NG;
     const int qw = warp & 3;                 // TMEM lane quarter
-    const int grp = (warp - 4) >> 2;         // column group
-    const int cb = grp * CW;                 // first of this warp's CW queries
+    const int grp = (warp - 4) >> 2;         // warp group: output columns in the epilogue
+    const int set = grp / (BW_NG / BW_SETS); // blocks g with g % 2 == set (score buffer set)
+    const int cb = (grp % (BW_NG / BW_SETS)) * CW;  // first of this warp's CW queries
     const int r = qw * 32 + lane;            // key row in the tile
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
@@ -586,6 +590,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
       for (int i = 0; i < n; ++i) {
         const uint32_t g = g0 + i;
         const int st = g % K::STAGES, sb = g % K::SBUF;
+        if (sb != set) continue;  // the other set's block
         const int m0 = (qbeg + i % nq) * K::BQ;
         mbar_wait(&s_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
@@ -597,7 +602,9 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
         mbar_wait(&q_full[st], (g / K::STAGES) & 1);  // lse / delta rows visible
         const float* Ls = sLD + st * 128 + cb;
         const float* Ds = Ls + 64;
-        float pv[CW], dv[CW];
+        // P^T into sr, dS^T into pr (in place: registers)
+        float* pv = reinterpret_cast<float*>(sr);
+        float* dv = reinterpret_cast<float*>(pr);
 #pragma unroll
         for (int gi = 0; gi < CW / 4; ++gi) {
           const float4 l4 = reinterpret_cast<const float4*>(Ls)[gi];
@@ -630,13 +637,17 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
             }
           }
         }
-        // packed bf16 back over this group's own score columns (MMA A operands)
-        static_assert(CW == 16, "TMEM-resident P^T assumes 16 columns per warp");
-        uint32_t wv[8];
-        pack_bf16x16(pv, wv);
-        tmem_st8(tS, wv);
-        pack_bf16x16(dv, wv);
-        tmem_st8(tS + 64, wv);
+        // packed bf16 back over this group's own score columns (MMA A operands):
+        // query chunk k of 16 at column 16 k
+        static_assert(CW % 16 == 0, "TMEM-resident P^T: whole 16-query chunks per warp");
+#pragma unroll
+        for (int c = 0; c < CW / 16; ++c) {
+          uint32_t wv[8];
+          pack_bf16x16(pv + 16 * c, wv);
+          tmem_st8(tS + 16 * c, wv);
+          pack_bf16x16(dv + 16 * c, wv);
+          tmem_st8(tS + 64 + 16 * c, wv);
+        }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -666,7 +677,7 @@ template <int HD>
 struct BwdQ {
   static constexpr int BM = 128, BN = 64;
   static constexpr int NP = HD / 64;
-  static constexpr int SBUF = 3;
+  static constexpr int SBUF = BW_SETS;  // one score buffer per elementwise set
   static constexpr int STAGES = HD == 64 ? 5 : 3;
   static constexpr int QBUF = HD == 64 ? 2 : 1;
   static constexpr int Q_PANEL = BM * 64 * 2;     // 16 KB
@@ -746,7 +757,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
     }
     for (int i = 0; i < K::SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], K::EW);
+      mbar_init(&p_full[i], K::EW / BW_SETS);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(done, 1);
@@ -858,8 +869,9 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
   } else if (warp >= 4) {
     constexpr int CW = BW_CW, CO = HD / BW_NG;
     const int qw = warp & 3;               // TMEM lane quarter
-    const int grp = (warp - 4) >> 2;       // column group
-    const int cb = grp * CW;               // first of this warp's CW keys
+    const int grp = (warp - 4) >> 2;       // warp group: delta / output columns
+    const int set = grp / (BW_NG / BW_SETS);        // key blocks j with (g % 2) == set
+    const int cb = (grp % (BW_NG / BW_SETS)) * CW;  // first of this warp's CW keys
     const int r = qw * 32 + lane;          // query row in the tile
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
@@ -900,6 +912,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
       for (int j = 0; j < nkb; ++j) {
         const uint32_t g = g0 + j;
         const int sb = g % K::SBUF;
+        if (sb != set) continue;  // the other set's block
         const int n0 = j * K::BN;
         mbar_wait(&s_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
@@ -908,7 +921,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
         tmem_ld_cols<CW>(tS, sr);
         tmem_ld_cols<CW>(tS + 64, pr);
         tc_wait_ld();
-        float dv[CW];
+        float* dv = reinterpret_cast<float*>(sr);  // dS in place
 #pragma unroll
         for (int e = 0; e < CW; e += 2) {
           float a0, a1, e0, e1, f0, f1;
@@ -927,11 +940,15 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
             if (key > row || key >= S || row >= S) dv[e] = 0.f;
           }
         }
-        // packed bf16 dS back over this group's own score columns (MMA A operand)
-        static_assert(CW == 16, "TMEM-resident dS assumes 16 columns per warp");
-        uint32_t wv[8];
-        pack_bf16x16(dv, wv);
-        tmem_st8(tS, wv);
+        // packed bf16 dS back over this group's own score columns (MMA A operand):
+        // key chunk k of 16 at column 16 k
+        static_assert(CW % 16 == 0, "TMEM-resident dS: whole 16-key chunks per warp");
+#pragma unroll
+        for (int c = 0; c < CW / 16; ++c) {
+          uint32_t wv[8];
+          pack_bf16x16(dv + 16 * c, wv);
+          tmem_st8(tS + 16 * c, wv);
+        }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
