@@ -346,12 +346,20 @@ __global__ void __launch_bounds__(256, 2)
 
 
 // ------------------------------------------------------------------ backward
-// NG elementwise warps per TMEM lane quarter.  They form BW_SETS sets that take
-// alternate score blocks (set = block % 2 = its score buffer), so one set's
-// TMEM loads / stores and barrier round trips overlap the other set's math;
-// inside a set each warp owns CW = 64 / (NG / SETS) score columns.  In the
-// epilogues every warp owns HD / NG output columns.
-constexpr int BW_NG = 4, BW_SETS = 2, BW_CW = 64 * BW_SETS / BW_NG;
+// NG elementwise warps per TMEM lane quarter.  With SETS = 2 (head_dim 128) they
+// form two sets that take alternate score blocks (set = block % 2 = its score
+// buffer), so one set's TMEM loads / stores and barrier round trips overlap the
+// other set's math (measured: C4 / C5 backward 355 -> 306 / 670 -> 576 us); with
+// SETS = 1 (head_dim 64) all of them work on every block and three score
+// buffers let the MMA run further ahead (the two-set variant measured slower
+// there, 98 -> 113 us at C2).  Each warp owns CW = 64 * SETS / NG score columns
+// of its blocks; in the epilogues every warp owns HD / NG output columns.
+constexpr int BW_NG = 4;
+template <int HD>
+struct BwSets {
+  static constexpr int SETS = HD == 128 ? 2 : 1;
+  static constexpr int CW = 64 * SETS / BW_NG;
+};
 
 // NC * 8 fp32 accumulator values -> bf16 (scaled) in global memory.
 template <int NC>
@@ -395,7 +403,8 @@ template <int HD>
 struct BwdKV {
   static constexpr int KEYS = 128, BQ = 64;
   static constexpr int NP = HD / 64;
-  static constexpr int SBUF = BW_SETS;  // one score buffer per elementwise set
+  static constexpr int SETS = BwSets<HD>::SETS;
+  static constexpr int SBUF = SETS == 2 ? 2 : 3;  // two sets: one score buffer each
   static constexpr int STAGES = HD == 64 ? 5 : 4;
   static constexpr int KVBUF = HD == 64 ? 2 : 1;
   static constexpr int KV_PANEL = KEYS * 64 * 2;   // 16 KB
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
     }
     for (int i = 0; i < K::SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], K::EW / BW_SETS);
+      mbar_init(&p_full[i], K::EW / K::SETS);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(done, 1);
@@ -572,11 +581,11 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
       g0 += n;
     }
   } else if (warp >= 4) {
-    constexpr int CW = BW_CW, CO = HD / BW_NG;
+    constexpr int CW = BwSets<HD>::CW, CO = HD / BW_NG;
     const int qw = warp & 3;                 // TMEM lane quarter
     const int grp = (warp - 4) >> 2;         // warp group: output columns in the epilogue
-    const int set = grp / (BW_NG / BW_SETS); // blocks g with g % 2 == set (score buffer set)
-    const int cb = (grp % (BW_NG / BW_SETS)) * CW;  // first of this warp's CW queries
+    const int set = grp / (BW_NG / K::SETS); // two sets: blocks g with g % 2 == set
+    const int cb = (grp % (BW_NG / K::SETS)) * CW;  // first of this warp's CW queries
     const int r = qw * 32 + lane;            // key row in the tile
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
@@ -590,7 +599,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
       for (int i = 0; i < n; ++i) {
         const uint32_t g = g0 + i;
         const int st = g % K::STAGES, sb = g % K::SBUF;
-        if (sb != set) continue;  // the other set's block
+        if (K::SETS == 2 && sb != set) continue;  // the other set's block
         const int m0 = (qbeg + i % nq) * K::BQ;
         mbar_wait(&s_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
@@ -677,7 +686,8 @@ template <int HD>
 struct BwdQ {
   static constexpr int BM = 128, BN = 64;
   static constexpr int NP = HD / 64;
-  static constexpr int SBUF = BW_SETS;  // one score buffer per elementwise set
+  static constexpr int SETS = BwSets<HD>::SETS;
+  static constexpr int SBUF = SETS == 2 ? 2 : 3;  // two sets: one score buffer each
   static constexpr int STAGES = HD == 64 ? 5 : 3;
   static constexpr int QBUF = HD == 64 ? 2 : 1;
   static constexpr int Q_PANEL = BM * 64 * 2;     // 16 KB
@@ -757,7 +767,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
     }
     for (int i = 0; i < K::SBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], K::EW / BW_SETS);
+      mbar_init(&p_full[i], K::EW / K::SETS);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(done, 1);
@@ -867,11 +877,11 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
       g0 += nkb;
     }
   } else if (warp >= 4) {
-    constexpr int CW = BW_CW, CO = HD / BW_NG;
+    constexpr int CW = BwSets<HD>::CW, CO = HD / BW_NG;
     const int qw = warp & 3;               // TMEM lane quarter
     const int grp = (warp - 4) >> 2;       // warp group: delta / output columns
-    const int set = grp / (BW_NG / BW_SETS);        // key blocks j with (g % 2) == set
-    const int cb = (grp % (BW_NG / BW_SETS)) * CW;  // first of this warp's CW keys
+    const int set = grp / (BW_NG / K::SETS);        // two sets: key blocks with g % 2 == set
+    const int cb = (grp % (BW_NG / K::SETS)) * CW;  // first of this warp's CW keys
     const int r = qw * 32 + lane;          // query row in the tile
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
@@ -912,7 +922,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
       for (int j = 0; j < nkb; ++j) {
         const uint32_t g = g0 + j;
         const int sb = g % K::SBUF;
-        if (sb != set) continue;  // the other set's block
+        if (K::SETS == 2 && sb != set) continue;  // the other set's block
         const int n0 = j * K::BN;
         mbar_wait(&s_full[sb], (g / K::SBUF) & 1);
         tc_fence_after();
