@@ -337,6 +337,18 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, ui
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(x), "r"(y)
       : "memory");
 }
+// Relaxed arrives: for "these TMEM columns are drained" signals whose data
+// hazard is already closed by tcgen05.wait::ld (+ tcgen05.fence::before_thread_sync):
+// no release fence (a cluster-scope release compiles to MEMBAR.ALL.GPU, which ncu
+// showed stalling the GEMM epilogue warps at every accumulator hand-back).
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
                : "memory");

@@ -301,9 +301,9 @@ __device__ __forceinline__ void release_acc(uint64_t* bar, int lane) {
   __syncwarp();
   if (lane == 0) {
     if constexpr (CG == 2)
-      mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+      mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(bar), 0));
     else
-      mbar_arrive(bar);
+      mbar_arrive_relaxed(bar);
   }
 }
 
