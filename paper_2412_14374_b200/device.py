@@ -82,6 +82,10 @@ class Act:
 
 
 _ABLATE_BIAS = os.environ.get("PP200_ABLATE_BIAS_GRAD") == "1"
+# Profiling ablations (results are garbage while set): comma-separated subset of
+# attn_fwd, attn_bwd, wgrad, lnp (LayerNorm / RMSNorm parameter gradients) --
+# the step time without that work bounds what optimising it can save.
+_ABLATE = set(filter(None, os.environ.get("PP200_ABLATE", "").split(",")))
 _LN_PARAMS_MAIN = os.environ.get("PP200_LN_PARAMS_MAIN") == "1"   # A/B switch for profiling
 # A/B switch: 0 = logits GEMM then the stand-alone cross-entropy kernel (pc_xent_fwd_bwd)
 _XENT_FUSED = os.environ.get("PP200_XENT_FUSED", "1") != "0"
@@ -594,8 +598,9 @@ class DeviceOps:
                    bias=ms("b_qkv"))
         o = self.empty((T, d), act)
         lse = self.empty((cfg.microbatch_size * H * cfg.seq_len,), torch.float32)
-        call("pc_attention_fwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
-             cfg.head_dim, qkv.data_ptr(), 3 * d, o.data_ptr(), d, lse.data_ptr(), self.st)
+        if "attn_fwd" not in _ABLATE:
+            call("pc_attention_fwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
+                 cfg.head_dim, qkv.data_ptr(), 3 * d, o.data_ptr(), d, lse.data_ptr(), self.st)
         h1 = self.empty((T, d), act)
         self._gemm(act, 0, 1, T, d, d, o, d, sl("w_o"), d, h1, d,
                    _lib.EPI_BIAS | _lib.EPI_RESIDUAL, bias=ms("b_o"), aux=h, ldaux=d)
@@ -732,10 +737,11 @@ class DeviceOps:
             on_side = not _LN_PARAMS_MAIN
             if on_side:
                 self._fork()
-            call("pc_layernorm_param_grads", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
-                 mean.data_ptr(), rstd.data_ptr(), gs(gname).data_ptr(), gs(bname).data_ptr(),
-                 int(fused), *self.red_ws(T, d, side=on_side),
-                 self._side().cuda_stream if on_side else self.st)
+            if "lnp" not in _ABLATE:
+                call("pc_layernorm_param_grads", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
+                     mean.data_ptr(), rstd.data_ptr(), gs(gname).data_ptr(), gs(bname).data_ptr(),
+                     int(fused), *self.red_ws(T, d, side=on_side),
+                     self._side().cuda_stream if on_side else self.st)
             call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
                  ms(gname).data_ptr(), mean.data_ptr(), rstd.data_ptr(),
                  None if dres is None else dres.data_ptr(), dx.data_ptr(), None, None, 0,
@@ -752,7 +758,8 @@ class DeviceOps:
 
         def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname):
             self._fork()
-            self._wgrad_into(M_, N_, T, A, lda, Bm, ldb, gs(wname), fused, self._side())
+            if "wgrad" not in _ABLATE:
+                self._wgrad_into(M_, N_, T, A, lda, Bm, ldb, gs(wname), fused, self._side())
             if _ABLATE_BIAS:   # profiling only: bias gradients left unset
                 return
             call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, M_, A.data_ptr(), lda,
@@ -777,9 +784,10 @@ class DeviceOps:
         self._gemm(act, 0, tb, T, d, d, dh1, d, B, ldb, do, d)
         dqkv = self.empty((T, 3 * d), act)
         delta = self.empty((cfg.microbatch_size * H * cfg.seq_len,), f32)
-        call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
-             cfg.head_dim, sv["qkv"].data_ptr(), 3 * d, sv["o"].data_ptr(), do.data_ptr(), d,
-             sv["lse"].data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, self.st)
+        if "attn_bwd" not in _ABLATE:
+            call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
+                 cfg.head_dim, sv["qkv"].data_ptr(), 3 * d, sv["o"].data_ptr(), do.data_ptr(), d,
+                 sv["lse"].data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, self.st)
         wgrad(3 * d, d, dqkv, 3 * d, sv["a"], d, "w_qkv", "b_qkv")
         da = self.empty((T, d), act)
         tb, B, ldb = wB("w_qkv")
