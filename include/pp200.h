@@ -142,6 +142,16 @@ int pc_layernorm_bwd_acc(int dtype, int64_t rows, int64_t d, const void* dy, con
 int pc_layernorm_param_grads(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
                              const float* mean, const float* rstd, float* dgamma, float* dbeta,
                              int accumulate, void* ws, int64_t ws_bytes, void* stream);
+/* LayerNorm backward in one read of dy and x: dx (+ dres) as pc_layernorm_bwd, plus per-CTA
+ * partial rows of dgamma = sum dy*xhat and dbeta = sum dy written to partials [2][n_part][d]
+ * (n_part from pc_layernorm_partial_rows); pc_col_sum (fp32, fixed order, accumulate as
+ * needed, any stream) over each [n_part, d] half finishes the parameter gradients.  bf16/fp32
+ * rows with d % 256 == 0, d <= 1024. */
+int pc_layernorm_partial_rows(int64_t rows, int64_t d, int64_t* n_part);
+int pc_layernorm_bwd_partials(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
+                              const float* gamma, const float* mean, const float* rstd,
+                              const void* dres, void* dx, float* partials, int64_t n_part,
+                              void* stream);
 /* ---- Llama-style block pieces (BASELINE config C5; oracle/llama.py) ---- */
 /* y = x * rsqrt(mean(x^2) + eps) * gamma; rstd [rows] fp32 saved (oracle rms_norm). */
 int pc_rmsnorm_fwd(int dtype, int64_t rows, int64_t d, const void* x, const float* gamma,

@@ -71,6 +71,9 @@ SIGNATURES: dict[str, list] = {
                          _c_p, _c_p, _c_i64, _c_p],
     "pc_layernorm_bwd_acc": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                              _c_p, _c_p, _c_i, _c_p, _c_i64, _c_p],
+    "pc_layernorm_partial_rows": [_c_i64, _c_i64, ctypes.POINTER(_c_i64)],
+    "pc_layernorm_bwd_partials": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                  _c_p, _c_i64, _c_p],
     "pc_layernorm_param_grads": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i,
                                  _c_p, _c_i64, _c_p],
     "pc_rmsnorm_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_f, _c_p],
@@ -159,7 +162,8 @@ _NON_LAUNCH = {"pc_version", "pc_device_sm_count", "pc_gemm_set_tile_n", "pc_gem
                "pc_p2p_comm_init", "pc_p2p_abort", "pc_p2p_destroy",
                "pc_peer_alloc", "pc_peer_free", "pc_peer_open", "pc_peer_close",
                "pc_stream_write_u32", "pc_stream_wait_u32", "pc_graph_kernel_nodes",
-               "pc_host_word_alloc", "pc_host_word_free", "pc_lmhead_xent_workspace"}
+               "pc_host_word_alloc", "pc_host_word_free", "pc_lmhead_xent_workspace",
+               "pc_layernorm_partial_rows"}
 launch_count = 0
 
 

@@ -241,6 +241,87 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_vec(int64_t rows, int d, const 
   }
 }
 
+// LayerNorm backward that also leaves the parameter-gradient partials: each CTA
+// owns a contiguous chunk of rows (warps stride them), computes dx exactly as
+// ln_bwd_dx_vec, and adds dy*xhat and dy of every row it handles into its
+// warp's private shared-memory accumulators (no atomics); the CTA then folds
+// its 8 warps in order and writes one partial row per quantity (pg / pb
+// [gridDim.x, d]).  dy and x are read once; a fixed-order column sum of the
+// partial rows (pc_col_sum, on any stream) finishes dgamma / dbeta.
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) ln_bwd_partials_vec(int64_t rows, int d, int64_t chunk,
+                                                           const T* __restrict__ dy,
+                                                           const T* __restrict__ x,
+                                                           const float* __restrict__ g,
+                                                           const float* __restrict__ mean,
+                                                           const float* __restrict__ rstd,
+                                                           const T* __restrict__ dres,
+                                                           T* __restrict__ dx,
+                                                           float* __restrict__ pg,
+                                                           float* __restrict__ pb) {
+  // [8 warps][2][NCH * 256]; column ch*256 + lane*8 + j lives at ch*256 + j*32 + lane
+  // (consecutive lanes, consecutive banks: conflict-free read-modify-writes)
+  extern __shared__ float acc_sm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* ag = acc_sm + w * 2 * NCH * 256;
+  float* ab = ag + NCH * 256;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ag[ch * 256 + j * 32 + lane] = ab[ch * 256 + j * 32 + lane] = 0.f;
+  const int64_t r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
+  for (int64_t r = r0 + w; r < r1; r += 8) {
+    const float mu = mean[r], rs = rstd[r];
+    float gy[NCH][8], xh[NCH][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int c = ch * 256 + lane * 8;
+      float xv[8], gg[8];
+      ld8(dy + r * d + c, gy[ch]);
+      ld8(x + r * d + c, xv);
+      ldf8(g + c, gg);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        xh[ch][j] = (xv[j] - mu) * rs;
+        const float t = gy[ch][j] * gg[j];
+        s1 += t;
+        s2 += t * xh[ch][j];
+        const int k = ch * 256 + j * 32 + lane;
+        ag[k] = fmaf(gy[ch][j], xh[ch][j], ag[k]);
+        ab[k] += gy[ch][j];
+      }
+    }
+    const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int c = ch * 256 + lane * 8;
+      float o[8], rr[8], gg[8];
+      ldf8(g + c, gg);
+      if (dres) ld8(dres + r * d + c, rr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        o[j] = rs * (gy[ch][j] * gg[j] - m1 - xh[ch][j] * m2) + (dres ? rr[j] : 0.f);
+      st8(dx + r * d + c, o);
+    }
+  }
+  __syncthreads();
+  // fold the 8 warps in order
+  float* og = pg + static_cast<int64_t>(blockIdx.x) * d;
+  float* ob = pb + static_cast<int64_t>(blockIdx.x) * d;
+  for (int c = threadIdx.x; c < d; c += 256) {
+    const int k0 = (c / 256) * 256 + (c % 8) * 32 + (c % 256) / 8;  // storage slot of column c
+    float tg = 0.f, tb = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      tg += acc_sm[k * 2 * NCH * 256 + k0];
+      tb += acc_sm[k * 2 * NCH * 256 + NCH * 256 + k0];
+    }
+    og[c] = tg;
+    ob[c] = tb;
+  }
+}
+
 template <typename T>
 bool ln_vec_ok(int64_t d, const void* p0, const void* p1, const void* p2) {
   const uintptr_t m = reinterpret_cast<uintptr_t>(p0) | reinterpret_cast<uintptr_t>(p1) |
@@ -624,4 +705,66 @@ extern "C" int pc_xent_fwd_bwd(int dtype, int64_t rows, int64_t V, int64_t seq, 
   }
   PP_DISPATCH_FB(dtype, T, xent_kernel<T><<<(unsigned)rows, 512, 0, st>>>(rows, (int)V, (int)seq, static_cast<T*>(logits), ld, tokens, row_loss));
   return check_launch("xent");
+}
+
+namespace pp200 {
+template <typename T, int N>
+int launch_ln_partials(unsigned nb, size_t smem, cudaStream_t st, int64_t rows, int64_t d,
+                       int64_t chunk, const void* dy, const void* x, const float* gamma,
+                       const float* mean, const float* rstd, const T* dr, void* dx, float* pg,
+                       float* pb) {
+  static bool attr = false;
+  if (!attr) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(ln_bwd_partials_vec<T, N>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    attr = true;
+  }
+  ln_bwd_partials_vec<T, N><<<nb, 256, smem, st>>>(rows, (int)d, chunk, static_cast<const T*>(dy),
+                                                   static_cast<const T*>(x), gamma, mean, rstd, dr,
+                                                   static_cast<T*>(dx), pg, pb);
+  return PC_OK;
+}
+}  // namespace pp200
+
+// Number of partial rows pc_layernorm_bwd_partials writes per quantity.
+extern "C" int pc_layernorm_partial_rows(int64_t rows, int64_t d, int64_t* n) {
+  PP_CHECK_ARG(rows > 0 && d > 0 && n, "layernorm_partial_rows: bad args");
+  int64_t r = 4 * static_cast<int64_t>(num_sms());
+  const int64_t cap = (rows + 7) / 8;
+  *n = r < cap ? r : cap;
+  return PC_OK;
+}
+
+extern "C" int pc_layernorm_bwd_partials(int dtype, int64_t rows, int64_t d, const void* dy,
+                                         const void* x, const float* gamma, const float* mean,
+                                         const float* rstd, const void* dres, void* dx,
+                                         float* partials, int64_t n_part, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= 0) return PC_OK;
+  PP_CHECK_ARG(dtype == PC_BF16 || dtype == PC_F32, "layernorm_bwd_partials: f32/bf16 only");
+  PP_CHECK_ARG(partials != nullptr && n_part > 0, "layernorm_bwd_partials: bad partials");
+  const int64_t chunk = (rows + n_part - 1) / n_part;
+  bool ok = true;
+  PP_DISPATCH_FB(dtype, T,
+    if (!ln_vec_ok<T>(d, dy, x, dx) ||
+        ((reinterpret_cast<uintptr_t>(gamma) | reinterpret_cast<uintptr_t>(dres)) & 31) != 0) {
+      ok = false;
+    } else {
+      const int nch = static_cast<int>(d / 256);
+      const size_t smem = static_cast<size_t>(8) * 2 * nch * 256 * 4;
+      const T* dr = static_cast<const T*>(dres);
+      float* pg = partials;
+      float* pb = partials + n_part * d;
+      const unsigned nb = static_cast<unsigned>(n_part);
+      int rc = PC_OK;
+      switch (nch) {
+        case 1: rc = launch_ln_partials<T, 1>(nb, smem, st, rows, d, chunk, dy, x, gamma, mean, rstd, dr, dx, pg, pb); break;
+        case 2: rc = launch_ln_partials<T, 2>(nb, smem, st, rows, d, chunk, dy, x, gamma, mean, rstd, dr, dx, pg, pb); break;
+        case 3: rc = launch_ln_partials<T, 3>(nb, smem, st, rows, d, chunk, dy, x, gamma, mean, rstd, dr, dx, pg, pb); break;
+        default: rc = launch_ln_partials<T, 4>(nb, smem, st, rows, d, chunk, dy, x, gamma, mean, rstd, dr, dx, pg, pb); break;
+      }
+      if (rc) return rc;
+    });
+  PP_CHECK_ARG(ok, "layernorm_bwd_partials: needs 32 B aligned rows with d %% 256 == 0 (d <= 1024)");
+  return check_launch("layernorm_bwd_partials");
 }

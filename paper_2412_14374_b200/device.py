@@ -87,6 +87,11 @@ _ABLATE_BIAS = os.environ.get("PP200_ABLATE_BIAS_GRAD") == "1"
 # the step time without that work bounds what optimising it can save.
 _ABLATE = set(filter(None, os.environ.get("PP200_ABLATE", "").split(",")))
 _LN_PARAMS_MAIN = os.environ.get("PP200_LN_PARAMS_MAIN") == "1"   # A/B switch for profiling
+# A/B switch, off by default: LayerNorm dx + parameter-gradient partial rows in one pass
+# (pc_layernorm_bwd_partials) with the column sums on the side stream.  Measured on C2
+# N=1 it is slower (75.0-75.6 vs 71.3-72.2 ms): the compute-stream kernel loses more to
+# its row-chunked grid than the side-stream reduction it replaces costs.
+_LN_FUSED = os.environ.get("PP200_LN_FUSED", "0") == "1"
 # A/B switch: 0 = logits GEMM then the stand-alone cross-entropy kernel (pc_xent_fwd_bwd)
 _XENT_FUSED = os.environ.get("PP200_XENT_FUSED", "1") != "0"
 
@@ -193,6 +198,7 @@ class DeviceOps:
         self._red_side = None
         self._side_stream = None
         self._xent_ws = None     # LM-head softmax statistics (pc_lmhead_xent_fwd)
+        self._ln_parts: dict = {}  # LayerNorm parameter-gradient partial rows per LayerNorm
         self.step_epoch = 0  # bumped by the executor at every step
 
     # ------------------------------------------------------------------ alloc
@@ -633,6 +639,17 @@ class DeviceOps:
         hv.saved[op.id] = saved
         env[op.result] = Act(out)
 
+    def _ln_partials(self, key: str, rows: int, d: int):
+        """Partial-row buffer [2, n, d] fp32 of one LayerNorm of the block (one per
+        LayerNorm: the side stream may still sum the previous one's rows)."""
+        n = ctypes.c_int64(0)
+        call("pc_layernorm_partial_rows", rows, d, ctypes.byref(n))
+        buf = self._ln_parts.get(key)
+        if buf is None or buf.numel() < 2 * n.value * d:
+            buf = self.empty((2 * n.value * d,), torch.float32)
+            self._ln_parts[key] = buf
+        return buf, n.value
+
     def _acc_for_value(self, v: str):
         """Running sum a parameter partial ``v`` may be added onto: v is a task
         output in acc_into, or v's only reader is the in-stage ``add`` that
@@ -731,9 +748,25 @@ class DeviceOps:
         self.red_ws(T, max(f, 3 * d), side=True)
 
         def ln_bwd(dy, x, gname, bname, mean, rstd, dres, dx):
-            """LayerNorm backward: dx on the compute stream; gamma / beta
-            gradients (a reduction nothing downstream waits for) beside it on
-            the side stream."""
+            """LayerNorm backward: dx on the compute stream; gamma / beta gradients
+            (a reduction nothing downstream waits for) beside it on the side
+            stream.  PP200_LN_FUSED=1: one pass for dx and partial rows of the
+            parameter gradients, their column sums on the side stream."""
+            if _LN_FUSED and "lnp" not in _ABLATE and d % 256 == 0 and d <= 1024:
+                # dx and the parameter-gradient partial rows in one pass on the
+                # compute stream; their fixed-order column sums on the side stream
+                parts, npart = self._ln_partials(gname, T, d)
+                call("pc_layernorm_bwd_partials", self.mode.pc_act, T, d, dy.data_ptr(),
+                     x.data_ptr(), ms(gname).data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                     None if dres is None else dres.data_ptr(), dx.data_ptr(), parts.data_ptr(),
+                     npart, self.st)
+                self._fork()
+                ws = self.red_ws(npart, d, side=True)
+                call("pc_col_sum", _lib.PC_F32, _lib.PC_F32, npart, d, parts.data_ptr(), d,
+                     gs(gname).data_ptr(), int(fused), *ws, sst)
+                call("pc_col_sum", _lib.PC_F32, _lib.PC_F32, npart, d,
+                     parts[npart * d:].data_ptr(), d, gs(bname).data_ptr(), int(fused), *ws, sst)
+                return
             on_side = not _LN_PARAMS_MAIN
             if on_side:
                 self._fork()
@@ -747,6 +780,7 @@ class DeviceOps:
                  None if dres is None else dres.data_ptr(), dx.data_ptr(), None, None, 0,
                  *self.red_ws(T, d), self.st)
 
+        sst = self._side().cuda_stream
         if final:
             dout = self.empty((T, d), act)
             ln_bwd(dz, sv["out"], "lnf_g", "lnf_b", sv["meanf"], sv["rstdf"], None, dout)
@@ -754,7 +788,6 @@ class DeviceOps:
             dout = dz
         # Weight gradients and their bias sums run on the side stream (they do
         # not feed the dX chain); each fork orders them after their inputs.
-        sst = self._side().cuda_stream
 
         def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname):
             self._fork()

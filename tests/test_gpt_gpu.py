@@ -398,3 +398,54 @@ def test_full_remat_replays_the_forward_bitwise(mode, fam, P, M, yields):
         assert b.stats.peak_stash_bytes[actor] < a.stats.peak_stash_bytes[actor], actor
     with pytest.raises(ExecutorFault):
         PipelineEngine(cp, tg, mode=mode, gpt=cfg, remat="selective")
+
+
+@pytest.mark.parametrize("d", [256, 768, 1024])
+@pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_layernorm_bwd_partials_then_col_sum(d, dt, tol):
+    """pc_layernorm_bwd_partials (dx plus per-CTA partial rows of dgamma / dbeta in
+    one read of dy and x) followed by pc_col_sum over the partial rows equals the
+    oracle's LayerNorm backward; deterministic across runs."""
+    rows = 8192 if d == 768 else 300
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((rows, d))
+    g, b = rng.standard_normal(d), rng.standard_normal(d)
+    dy = rng.standard_normal((rows, d))
+    res = rng.standard_normal((rows, d))
+    tx, tdy, tres = _t(x, dt), _t(dy, dt), _t(res, dt)
+    xq, dyq, resq = (t.double().cpu().numpy() for t in (tx, tdy, tres))
+    y, cache = gpt.layer_norm(xq, g, b)
+    dx, dg, db = gpt.layer_norm_bwd(dyq, g, cache)
+    tg_, tb = _t(g), _t(b)
+    ty = torch.empty_like(tx)
+    mean, rstd = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
+    pc = _lib.PC_F32 if dt == torch.float32 else _lib.PC_BF16
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("pc_layernorm_fwd", pc, rows, d, tx.data_ptr(), tg_.data_ptr(), tb.data_ptr(),
+              ty.data_ptr(), mean.data_ptr(), rstd.data_ptr(), 1e-5, st)
+    n = ctypes.c_int64()
+    _lib.call("pc_layernorm_partial_rows", rows, d, ctypes.byref(n))
+    nb = ctypes.c_int64()
+    _lib.call("pc_reduce_workspace_bytes", n.value, d, ctypes.byref(nb))
+    ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        parts = torch.empty(2 * n.value * d, device="cuda")
+        tdx = torch.empty_like(tx)
+        _lib.call("pc_layernorm_bwd_partials", pc, rows, d, tdy.data_ptr(), tx.data_ptr(),
+                  tg_.data_ptr(), mean.data_ptr(), rstd.data_ptr(), tres.data_ptr(),
+                  tdx.data_ptr(), parts.data_ptr(), n.value, st)
+        tdg = torch.full((d,), 0.25, device="cuda")
+        tdb = torch.empty(d, device="cuda")
+        _lib.call("pc_col_sum", _lib.PC_F32, _lib.PC_F32, n.value, d, parts.data_ptr(), d,
+                  tdg.data_ptr(), 1, ws.data_ptr(), nb.value, st)
+        _lib.call("pc_col_sum", _lib.PC_F32, _lib.PC_F32, n.value, d,
+                  parts[n.value * d:].data_ptr(), d, tdb.data_ptr(), 0, ws.data_ptr(), nb.value, st)
+        outs.append((tdx, tdg, tdb))
+    torch.cuda.synchronize()
+    tdx, tdg, tdb = outs[0]
+    assert ffn.rel(tdx.double().cpu().numpy(), dx + resq) < tol
+    assert ffn.rel(tdg.cpu().numpy(), dg + 0.25) < 1e-5
+    assert ffn.rel(tdb.cpu().numpy(), db) < 1e-5
+    for a, c in zip(outs[0], outs[1]):
+        assert torch.equal(a, c)
