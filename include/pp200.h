@@ -232,6 +232,12 @@ int pc_attention_gqa_bwd(int dtype, int B, int H, int Hkv, int S, int hd, const 
 /* 0 = auto (bf16: tcgen05 for head_dim 64 / 128), 1 = force exact SIMT,
  * 2 = force the mma.sync kernels. Test hook. */
 int pc_attention_set_impl(int impl);
+/* Tuning hook for the tcgen05 attention kernels (bench / A-B tools; the
+ * defaults are the measured best).  key 0: head_dim-64 forward design
+ * (1 = S/P-aliased fa_fwd_tc5, 2 = separate P buffers, fa_fwd64_tc5);
+ * key 1: score columns of every 16 whose exp2 runs on the FMA pipe in
+ * fa_fwd64_tc5 (0, 4, 6, 8). */
+int pc_attention_tune(int key, int value);
 
 /* ---- inter-stage transport over NVLink peer memory (Channel, executor.py:201-254) ----
  * The receiver allocates one slot per plan message plus flag words (pc_peer_alloc: zeroed

@@ -277,6 +277,12 @@ extern "C" int pc_attention_set_impl(int impl) {
 }
 
 namespace pp200 {
+int attention_tc5_tune(int key, int value);
+}
+
+extern "C" int pc_attention_tune(int key, int value) { return pp200::attention_tc5_tune(key, value); }
+
+namespace pp200 {
 int attention_fwd_tc(int B, int H, int S, int hd, const void* qkv, int64_t ld_qkv, void* o,
                      int64_t ld_o, float* lse, cudaStream_t st);
 int attention_bwd_tc(int B, int H, int S, int hd, const void* qkv, int64_t ld_qkv, const void* o,

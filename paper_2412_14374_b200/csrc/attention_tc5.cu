@@ -344,6 +344,415 @@ __global__ void __launch_bounds__(256, 2)
   if (warp == 2) tmem_dealloc(tmem, K::TMEM_COLS);
 }
 
+// 2^x on the FMA pipe for a pair of fp32 values (x >= -126: j >= -126 keeps
+// the exponent field of p * 2^j non-negative, p >= 2^-1/2): round-to-nearest
+// split x = j + f (|f| <= 1/2) with the 1.5 * 2^23 shifter, a degree-3
+// minimax polynomial for 2^f (max rel err 7.5e-5, well below the bf16
+// rounding of P), then j added to the exponent field.  Takes part of the
+// exp2 work off the MUFU unit (16 ex2 / SM / clk), which bounds head_dim 64.
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float& y1) {
+  constexpr float SH = 12582912.f;
+  const uint64_t t = fadd2(pack_f2(x0, x1), pack_f2(SH, SH));
+  const uint64_t j = fadd2(t, pack_f2(-SH, -SH));
+  const uint64_t f = ffma2(j, pack_f2(-1.f, -1.f), pack_f2(x0, x1));
+  uint64_t p = ffma2(f, pack_f2(0.05517166f, 0.05517166f), pack_f2(0.24261114f, 0.24261114f));
+  p = ffma2(p, f, pack_f2(0.69326097f, 0.69326097f));
+  p = ffma2(p, f, pack_f2(0.99992806f, 0.99992806f));
+  float t0, t1, p0, p1;
+  unpack_f2(t, t0, t1);
+  unpack_f2(p, p0, p1);
+  y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+  y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+}
+
+// Forward, head_dim 64, persistent.  Measured on fa_fwd_tc5<64> (C2 shape,
+// clock64 / %globaltimer traces and ablations, profiles/r02_attn_fwd64.txt):
+// (1) a one-tile CTA spent ~2.7 us outside its key blocks (setup, Q load, first
+// S, epilogue); (2) with P aliased over S, the MMA warp waited for PV_g to
+// retire before it could issue S_{g+2} into the same columns, a full
+// issue -> execute -> commit round trip per block (the MMA-only pipeline, no
+// softmax math, ran 20.9 us); (3) a lane-0-only MMA / TMA branch made every
+// wait and issue a divergent slow path.  So: two CTAs per SM walk the query
+// tiles longest-first in snake order without draining between tiles (Q
+// double-buffered; the next tile's scores are computed while the current tile
+// finishes); P_g has its own TMEM buffer, so a score buffer is released as
+// soon as the softmax warps have loaded it (s_free) and the MMA warp never
+// waits on a PV; the producer / MMA warps run warp-uniform with one elected
+// issuing lane.  O leaves through a per-warp TMA store (3-D map: rows clipped
+// at the sequence end).  EMU of every 16 score columns take exp2 on the FMA
+// pipe (exp2_poly2).  Ring / buffer phases run on CTA-wide block counters.
+// TMEM (256 columns): S0 @0, S1 @64, P0 @128, P1 @160 (packed bf16), O @192.
+#ifdef PP200_FA_TRACE
+// tools/fa_trace.cu: clock64 stamps per (CTA < 64, event < 8, block < 32)
+__device__ unsigned long long fa_trace_buf[64 * 8 * 32];
+__device__ unsigned long long fa_trace_cta[1024 * 3];  // start / end %globaltimer, smid
+#define FA_T(ev, idx)                                                                          \
+  do {                                                                                         \
+    if (blockIdx.x < 64 && (idx) < 32) fa_trace_buf[(blockIdx.x * 8 + (ev)) * 32 + (idx)] = clock64(); \
+  } while (0)
+__device__ __forceinline__ unsigned long long fa_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#else
+#define FA_T(ev, idx) \
+  do {                \
+  } while (0)
+#endif
+
+struct Fwd64 {
+  static constexpr int BM = 128, BN = 64, THREADS = 256, STAGES = 3;
+  static constexpr int Q_BYTES = BM * 64 * 2;    // 16 KB
+  static constexpr int KV_BYTES = BN * 64 * 2;   // 8 KB (one of K / V)
+  static constexpr int O_WARP = 32 * 128;        // per softmax warp: 32 rows x 64 bf16
+  static constexpr int SMEM = 2 * Q_BYTES + 2 * STAGES * KV_BYTES + 4 * O_WARP + 1024 + 256;
+};
+
+__device__ __forceinline__ void tma_store_3d(const void* tmap, const void* src, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+template <int EMU, int ABL = 0>  // ABL (tools/attn_ab.py): 1 no softmax math, 2 no MMAs
+__global__ void __launch_bounds__(256, 2)
+    fa_fwd64_tc5(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap to,
+                 float* __restrict__ lse, int B, Heads hs, int S, float sl2) {
+  using K = Fwd64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;                                  // [2][128 x 64]
+  uint8_t* sK = sQ + 2 * K::Q_BYTES;                   // [ST][64 x 64]
+  uint8_t* sV = sK + K::STAGES * K::KV_BYTES;          // [ST][64 x 64]
+  uint8_t* sO = sV + K::STAGES * K::KV_BYTES;          // [4 warps][32 x 64] staging
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sO + 4 * K::O_WARP);  // [2]
+  uint64_t* q_empty = q_full + 2;                      // [2]
+  uint64_t* kv_full = q_empty + 2;                     // [ST]
+  uint64_t* kv_empty = kv_full + K::STAGES;            // [ST]
+  uint64_t* s_full = kv_empty + K::STAGES;             // [2] S_g landed
+  uint64_t* s_free = s_full + 2;                       // [2] S_g loaded by every softmax warp
+  uint64_t* p_full = s_free + 2;                       // [2] P_g stored (O rescaled)
+  uint64_t* pv_done = p_full + 2;                      // [2] PV_g retired
+  uint64_t* o_full = pv_done + 2;                      // a tile's O complete
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int H = hs.H, BH = B * H;
+  const int nqt = (S + K::BM - 1) / K::BM;
+  const int items = BH * nqt;
+  const int G = gridDim.x;
+  // k-th tile of this CTA, snake order over the longest-first list
+  auto tile_of = [&](int k) {
+    const int r = k / 2, base = 2 * G * r;
+    return (k & 1) ? base + 2 * G - 1 - static_cast<int>(blockIdx.x) : base + static_cast<int>(blockIdx.x);
+  };
+  auto decode = [&](int w, int& b, int& h, int& q0, int& nkb) {
+    const int qt = nqt - 1 - w / BH;
+    const int bh = w % BH;
+    b = bh / H;
+    h = bh % H;
+    q0 = qt * K::BM;
+    nkb = (min(S, q0 + K::BM) + K::BN - 1) / K::BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm);
+    tma_prefetch_desc(&to);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+    }
+    mbar_init(o_full, 1);
+    for (int s = 0; s < K::STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tP = tmem + 128, tO = tmem + 192;
+#ifdef PP200_FA_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    fa_trace_cta[blockIdx.x * 3] = fa_gtime();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    fa_trace_cta[blockIdx.x * 3 + 2] = smid;
+  }
+#endif
+
+  if (warp == 0) {
+    uint32_t g = 0;
+    for (int k = 0;; ++k) {
+      const int w = tile_of(k);
+      if (w >= items) break;
+      int b, h, q0, nkb;
+      decode(w, b, h, q0, nkb);
+      const int hk = h / hs.G, brow = b * S;
+      const int qb = k & 1;
+      mbar_wait(&q_empty[qb], ((k >> 1) & 1) ^ 1);
+      if (elect_one()) {
+        mbar_expect_tx(&q_full[qb], K::Q_BYTES);
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_2d(sQ + qb * K::Q_BYTES + hf * (K::Q_BYTES / 2), &tm, &q_full[qb], hs.qcol(h),
+                      brow + q0 + 64 * hf);
+      }
+      __syncwarp();
+      for (int j = 0; j < nkb; ++j, ++g) {
+        const int st = g % K::STAGES;
+        mbar_wait(&kv_empty[st], ((g / K::STAGES) & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(&kv_full[st], 2 * K::KV_BYTES);
+          tma_load_2d(sK + st * K::KV_BYTES, &tm, &kv_full[st], hs.kcol(hk), brow + j * K::BN);
+          tma_load_2d(sV + st * K::KV_BYTES, &tm, &kv_full[st], hs.vcol(hk), brow + j * K::BN);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t ID_S = umma_idesc_bf16(K::BM, K::BN, 0, 0);  // Q, K both K-major
+    constexpr uint32_t ID_O = umma_idesc_bf16(K::BM, 64, 0, 1);     // P K-major, V MN-major
+    // S_g = Q K_g^T for block g (tile k, block j) into S[g % 2]
+    auto issue_s = [&](uint32_t g, int k, int j) {
+      const int st = g % K::STAGES, qb = k & 1;
+      if (j == 0) mbar_wait(&q_full[qb], (k >> 1) & 1);
+      mbar_wait(&kv_full[st], (g / K::STAGES) & 1);
+      if (g >= 2) mbar_wait(&s_free[g & 1], ((g - 2) >> 1) & 1);  // S_{g-2} loaded
+      tc_fence_after();
+      const uint32_t q_addr = smem_u32(sQ + qb * K::Q_BYTES), k_addr = smem_u32(sK + st * K::KV_BYTES);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (ABL != 2)
+            tc_mma_f16(tS + (g & 1) * 64, kmajor_step(q_addr, kk, K::Q_BYTES),
+                       kmajor_step(k_addr, kk, K::KV_BYTES), ID_S, kk > 0 ? 1u : 0u);
+        tc_commit(&s_full[g & 1]);
+        FA_T(0, g);
+      }
+      __syncwarp();
+    };
+    // (tile, block) pairs in order; S is issued two pairs ahead, across tiles
+    int kq[3], jq[3], nq[3];  // pairs g, g+1, g+2
+    auto next_pair = [&](int k, int j, int nkb, int& k2, int& j2, int& n2) {
+      k2 = k;
+      j2 = j + 1;
+      n2 = nkb;
+      if (j2 == nkb) {
+        k2 = k + 1;
+        j2 = 0;
+        const int w2 = tile_of(k2);
+        if (w2 >= items) return false;
+        int b2, h2, q02;
+        decode(w2, b2, h2, q02, n2);
+      }
+      return true;
+    };
+    if (tile_of(0) < items) {
+      int b0, h0, q00;
+      kq[0] = 0;
+      jq[0] = 0;
+      decode(tile_of(0), b0, h0, q00, nq[0]);
+      bool have1 = next_pair(kq[0], jq[0], nq[0], kq[1], jq[1], nq[1]);
+      issue_s(0, kq[0], jq[0]);
+      if (have1) issue_s(1, kq[1], jq[1]);
+      bool have2 = have1 && next_pair(kq[1], jq[1], nq[1], kq[2], jq[2], nq[2]);
+      for (uint32_t g = 0;; ++g) {
+        if (have2) issue_s(g + 2, kq[2], jq[2]);  // once softmax g has loaded S_g
+        const int k = kq[0], j = jq[0], nkb = nq[0];
+        const int st = g % K::STAGES;
+        mbar_wait(&p_full[g & 1], (g >> 1) & 1);
+        if (lane == 0) FA_T(1, g);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + st * K::KV_BYTES);
+        const uint32_t tPg = tP + (g & 1) * 32;  // key chunk c of 16 at column 8 c
+        if (elect_one()) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (ABL != 2)
+              tc_mma_f16_ts(tO, tPg + 8 * c, umma_sdesc_sw128(v_addr + c * 2048, K::KV_BYTES, 1024), ID_O,
+                            (j > 0 || c > 0) ? 1u : 0u);
+          tc_commit(&pv_done[g & 1]);
+          tc_commit(&kv_empty[st]);
+          FA_T(2, g);
+          if (j == nkb - 1) {
+            tc_commit(o_full);
+            tc_commit(&q_empty[k & 1]);
+          }
+        }
+        __syncwarp();
+        if (!have1) break;
+        kq[0] = kq[1]; jq[0] = jq[1]; nq[0] = nq[1];
+        kq[1] = kq[2]; jq[1] = jq[2]; nq[1] = nq[2];
+        have1 = have2;
+        if (have2) have2 = next_pair(kq[1], jq[1], nq[1], kq[2], jq[2], nq[2]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int r = qw * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    uint8_t* so = sO + qw * K::O_WARP;
+    const uint64_t sc2 = pack_f2(sl2, sl2);
+    uint32_t g = 0;
+    for (int k = 0;; ++k) {
+      const int w = tile_of(k);
+      if (w >= items) break;
+      int b, h, q0, nkb;
+      decode(w, b, h, q0, nkb);
+      const int row = q0 + r;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkb; ++j, ++g) {
+        mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+        if (threadIdx.x == 128) FA_T(3, g);
+        tc_fence_after();
+        uint32_t sr[64];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld16(tS + (g & 1) * 64 + lane_off + c * 16, sr + c * 16);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[g & 1]);  // the MMA may overwrite S[g % 2]
+        if (threadIdx.x == 128) FA_T(4, g);
+        float* sv = reinterpret_cast<float*>(sr);
+        const int n0 = j * K::BN;
+        if (ABL == 1) {
+          if (g >= 2) mbar_wait(&pv_done[g & 1], ((g - 2) >> 1) & 1);
+          tc_fence_after();
+          tmem_st16(tP + (g & 1) * 32 + lane_off, sr);
+          tmem_st16(tP + (g & 1) * 32 + lane_off + 16, sr + 16);
+          l = 1.f;
+          m = 0.f;
+          tc_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[g & 1]);
+          continue;
+        }
+        if (n0 + K::BN - 1 > q0 || n0 + K::BN > S) {  // diagonal or ragged block
+#pragma unroll
+          for (int i = 0; i < K::BN; ++i)
+            if (n0 + i > row || n0 + i >= S) sv[i] = -INFINITY;
+        }
+        float mx8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < K::BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], sv[i]);
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+        const float mn = fmaxf(m, mx);
+        float corr = 1.f;
+        if (j == 0 || m == -INFINITY) {
+          m = mn == -INFINITY ? 0.f : mn;
+          corr = 0.f;
+        } else if (mn > m + 8.f) {  // lazy rescale (FA4), see fa_fwd_tc5
+          corr = ex2(m - mn);
+          m = mn;
+        }
+        const uint64_t nm2 = pack_f2(-m, -m);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int i = 0; i < K::BN; i += 2) {
+          float p0, p1;
+          unpack_f2(ffma2(pack_f2(sv[i], sv[i + 1]), sc2, nm2), p0, p1);
+          if ((i & 15) < EMU) {
+            exp2_poly2(fmaxf(p0, -126.f), fmaxf(p1, -126.f), p0, p1);
+          } else {
+            p0 = ex2(p0);
+            p1 = ex2(p1);
+          }
+          sv[i] = p0;
+          sv[i + 1] = p1;
+          acc2[(i >> 1) & 3] = fadd2(acc2[(i >> 1) & 3], pack_f2(p0, p1));
+        }
+        float sa[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) unpack_f2(acc2[i], sa[2 * i], sa[2 * i + 1]);
+        l = l * corr + (((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7])));
+        uint32_t wv[32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) pack_bf16x16(sv + 16 * c, wv + 8 * c);
+        if (threadIdx.x == 128) FA_T(5, __float_as_uint(l) == 7u ? 40 : g);
+        // P[g % 2] was last read by PV_{g-2}
+        if (g >= 2) mbar_wait(&pv_done[g & 1], ((g - 2) >> 1) & 1);
+        if (threadIdx.x == 128) FA_T(6, g);
+        tc_fence_after();
+        tmem_st16(tP + (g & 1) * 32 + lane_off, wv);
+        tmem_st16(tP + (g & 1) * 32 + lane_off + 16, wv + 16);
+        // rescale O by corr once PV_{g-1} (same tile) has retired
+        if (j > 0 && __any_sync(0xffffffffu, corr != 1.f && l > 0.f)) {
+          mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t orr[16];
+            tmem_ld16(tO + lane_off + c * 16, orr);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * corr);
+            tmem_st16(tO + lane_off + c * 16, orr);
+          }
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[g & 1]);
+        if (threadIdx.x == 128) FA_T(7, g);
+      }
+      // epilogue: O / l -> bf16 rows in this warp's staging tile -> TMA store.
+      // The next tile's first PV overwrites O only after this warp's next
+      // p_full arrival, which follows the load below.
+      mbar_wait(o_full, k & 1);
+      tc_fence_after();
+      uint32_t orr[64];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tO + lane_off + c * 16, orr + c * 16);
+      tc_wait_ld();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      if (lane == 0) bulk_wait_read0();  // the previous tile's store has left the staging tile
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 u;
+        __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          hp[e] = __floats2bfloat162_rn(__uint_as_float(orr[8 * c + 2 * e]) * inv,
+                                        __uint_as_float(orr[8 * c + 2 * e + 1]) * inv);
+        *reinterpret_cast<uint4*>(so + lane * 128 + ((c ^ (lane & 7)) << 4)) = u;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&to, so, hs.qcol(h), q0 + qw * 32, b);
+        bulk_commit();
+      }
+      if (row < S) lse[(static_cast<int64_t>(b) * H + h) * S + row] = (m + log2f(l)) * F_LN2;
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 256);
+#ifdef PP200_FA_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) fa_trace_cta[blockIdx.x * 3 + 1] = fa_gtime();
+#endif
+}
+
 
 // ------------------------------------------------------------------ backward
 // NG elementwise warps per TMEM lane quarter.  With SETS = 2 (head_dim 128) they
@@ -1002,12 +1411,67 @@ int make_tmap_rows64(CUtensorMap* m, const void* base, int64_t ld, int64_t rows)
   return PC_OK;
 }
 
+int g_fwd64_design = 2;  // pc_attention_tune key 0
+int g_fwd64_emu = 6;     // pc_attention_tune key 1
+
+// O as a 3-D tensor [B][S][ld_o] (rows clipped per sequence), box 64 x 32 x 1.
+int make_tmap_o3(CUtensorMap* m, const void* base, int64_t ld, int S, int B) {
+  auto enc = tmap_encoder_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return PC_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(B)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 2), static_cast<cuuint64_t>(ld * 2 * S)};
+  cuuint32_t box[3] = {64u, 32u, 1u};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (attention O) failed (%d)", static_cast<int>(r));
+    return PC_ERR_CUDA;
+  }
+  return PC_OK;
+}
+
+template <int EMU, int ABL = 0>
+int fwd64_launch(int B, int S, Heads hs, const CUtensorMap& tm, void* o, int64_t ld_o, float* lse,
+                 cudaStream_t st) {
+  CUtensorMap to;
+  int rc = make_tmap_o3(&to, o, ld_o, S, B);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd64_tc5<EMU, ABL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fwd64::SMEM));
+    attr = true;
+  }
+  const int items = B * hs.H * ((S + Fwd64::BM - 1) / Fwd64::BM);
+  const int grid = items < 2 * num_sms() ? items : 2 * num_sms();
+  const float sl2 = F_LOG2E / 8.f;  // 1 / sqrt(64)
+  fa_fwd64_tc5<EMU, ABL><<<grid, Fwd64::THREADS, Fwd64::SMEM, st>>>(tm, to, lse, B, hs, S, sl2);
+  return check_launch("fa_fwd64_tc5");
+}
+
 template <int HD>
 int fwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, void* o, int64_t ld_o,
                float* lse, cudaStream_t st) {
   CUtensorMap tm;
   int rc = make_tmap_rows64(&tm, qkv, ld_qkv, static_cast<int64_t>(B) * S);
   if (rc) return rc;
+  if (HD == 64 && g_fwd64_design == 2) {
+    switch (g_fwd64_emu) {
+      case 0: return fwd64_launch<0>(B, S, hs, tm, o, ld_o, lse, st);
+      case 4: return fwd64_launch<4>(B, S, hs, tm, o, ld_o, lse, st);
+      case 8: return fwd64_launch<8>(B, S, hs, tm, o, ld_o, lse, st);
+      case 10: return fwd64_launch<10>(B, S, hs, tm, o, ld_o, lse, st);
+      case 12: return fwd64_launch<12>(B, S, hs, tm, o, ld_o, lse, st);
+      case 101: return fwd64_launch<0, 1>(B, S, hs, tm, o, ld_o, lse, st);
+      case 102: return fwd64_launch<0, 2>(B, S, hs, tm, o, ld_o, lse, st);
+      default: return fwd64_launch<6>(B, S, hs, tm, o, ld_o, lse, st);
+    }
+  }
   static bool attr = false;
   if (!attr) {
     PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd_tc5<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1057,6 +1521,18 @@ int bwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, const vo
   return check_launch("fa_bwd_dkdv_tc5");
 }
 }  // namespace
+
+int attention_tc5_tune(int key, int value) {
+  if (key == 0 && (value == 1 || value == 2)) {
+    g_fwd64_design = value;
+  } else if (key == 1 && (value == 0 || value == 4 || value == 6 || value == 8 || value == 10 || value == 12 || value == 101 || value == 102)) {
+    g_fwd64_emu = value;
+  } else {
+    set_error("pc_attention_tune: unknown key %d or value %d", key, value);
+    return PC_ERR_ARG;
+  }
+  return PC_OK;
+}
 
 bool attention_tc5_supported(int hd, int H, int Hkv, int64_t ld_qkv, int64_t ld_o, const void* qkv,
                              const void* o) {
