@@ -80,6 +80,8 @@ int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_o
 int pc_gemm_set_tile_n(int bn);
 /* CTA-pair (cta_group::2, 256-row tiles over two SMs) selection: 0 = heuristic,
  * 1 = never, 2 = whenever the tile allows it (128/256; 192 with a K-major B).  Test hook. */
+/* Largest K split the tile chooser may pick (1, 2, 4, 8; default 4).  Tuning hook. */
+int pc_gemm_set_max_split(int ks);
 int pc_gemm_set_cta_pair(int mode);
 /* Profiling ablation of the tcgen05 GEMM (outputs are garbage while set):
  * bit0 = skip the epilogue work, bit1 = skip the operand TMA loads, bit2 = skip the

@@ -224,7 +224,7 @@ def test_ordered_splitk_accumulate(shape):
     bn, cg, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     _lib.call("pc_gemm_tile_choice", 0, M, N, K, 2, ctypes.byref(bn), ctypes.byref(cg),
               ctypes.byref(ks))
-    assert ks.value == 2
+    assert ks.value in (2, 4)  # 4 where two halves leave most SMs idle (768 x 768)
     A, B, ref = make_operands(M, N, K, 1, 0, torch.bfloat16, seed=4)
     g = torch.Generator(device="cuda").manual_seed(8)
     acc0 = torch.randn(M, N, device="cuda", generator=g)

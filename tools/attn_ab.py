@@ -22,51 +22,56 @@ def bench(fn, iters=20):
     return s.elapsed_time(e) / iters
 
 
-what = sys.argv[1] if len(sys.argv) > 1 else "all"
-st = torch.cuda.current_stream().cuda_stream
-torch.manual_seed(0)
-for (name, B, H, S) in [("C2", 8, 12, 1024), ("C3", 8, 16, 1024), ("C2-S1000", 8, 12, 1000)]:
-    hd = 64
-    ld = 3 * H * hd
-    qkv = (torch.randn(B * S, ld, device="cuda") * 0.5).bfloat16()
-    do = torch.randn(B * S, H * hd, device="cuda").bfloat16()
-    flops_f = 4.0 * B * H * S * S * hd / 2
+def main():
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    st = torch.cuda.current_stream().cuda_stream
+    torch.manual_seed(0)
+    for (name, B, H, S) in [("C2", 8, 12, 1024), ("C3", 8, 16, 1024), ("C2-S1000", 8, 12, 1000)]:
+        hd = 64
+        ld = 3 * H * hd
+        qkv = (torch.randn(B * S, ld, device="cuda") * 0.5).bfloat16()
+        do = torch.randn(B * S, H * hd, device="cuda").bfloat16()
+        flops_f = 4.0 * B * H * S * S * hd / 2
 
-    def run_fwd(o, lse):
-        _lib.call("pc_attention_gqa_fwd", 2, B, H, H, S, hd, qkv.data_ptr(), ld, o.data_ptr(), H * hd,
-                  lse.data_ptr(), st)
+        def run_fwd(o, lse):
+            _lib.call("pc_attention_gqa_fwd", 2, B, H, H, S, hd, qkv.data_ptr(), ld, o.data_ptr(), H * hd,
+                      lse.data_ptr(), st)
 
-    def run_bwd(o, lse, delta, dqkv):
-        _lib.call("pc_attention_gqa_bwd", 2, B, H, H, S, hd, qkv.data_ptr(), ld, o.data_ptr(),
-                  do.data_ptr(), H * hd, lse.data_ptr(), delta.data_ptr(), dqkv.data_ptr(), ld, st)
+        def run_bwd(o, lse, delta, dqkv):
+            _lib.call("pc_attention_gqa_bwd", 2, B, H, H, S, hd, qkv.data_ptr(), ld, o.data_ptr(),
+                      do.data_ptr(), H * hd, lse.data_ptr(), delta.data_ptr(), dqkv.data_ptr(), ld, st)
 
-    variants = [(1, 0), (2, 0), (2, 4), (2, 6), (2, 8), (2, 10), (2, 12)]
-    ref = None
-    for (design, emu) in variants:
-        _lib.call("pc_attention_tune", 0, design)
-        _lib.call("pc_attention_tune", 1, emu)
-        o = torch.empty(B * S, H * hd, device="cuda", dtype=torch.bfloat16)
-        lse = torch.empty(B * H * S, device="cuda")
-        run_fwd(o, lse)
-        torch.cuda.synchronize()
-        row = dict(shape=name, design=design, emu=emu)
-        if what in ("fwd", "all"):
-            t = bench(lambda: run_fwd(o, lse))
-            row.update(fwd_us=round(t * 1e3, 2), fwd_tflops=round(flops_f / t / 1e9, 1))
-        if ref is None:
-            ref = (o.clone(), lse.clone())
-        else:
-            row.update(o_nan=int(torch.isnan(o.float()).sum()), lse_nan=int(torch.isnan(lse).sum()),
-                       o_maxdiff=float((o.float() - ref[0].float()).abs().max()),
-                       lse_maxdiff=float((lse - ref[1]).abs().max()))
-        if what in ("bwd", "all"):
-            delta = torch.empty_like(lse)
-            dqkv = torch.empty_like(qkv)
-            t = bench(lambda: run_bwd(o, lse, delta, dqkv))
-            row.update(bwd_us=round(t * 1e3, 2), bwd_tflops=round(2.5 * flops_f / t / 1e9, 1))
-        if name == "small" and emu:
-            bad = torch.isnan(o.float()).any(dim=1).nonzero().flatten().tolist()
-            row.update(nan_rows=bad[:8] + ["..."] + bad[-4:], n_bad=len(bad))
-        print(json.dumps(row), flush=True)
-    _lib.call("pc_attention_tune", 0, 2)
-    _lib.call("pc_attention_tune", 1, 6)
+        variants = [(1, 0), (2, 0), (2, 4), (2, 6), (2, 8), (2, 10), (2, 12)]
+        ref = None
+        for (design, emu) in variants:
+            _lib.call("pc_attention_tune", 0, design)
+            _lib.call("pc_attention_tune", 1, emu)
+            o = torch.empty(B * S, H * hd, device="cuda", dtype=torch.bfloat16)
+            lse = torch.empty(B * H * S, device="cuda")
+            run_fwd(o, lse)
+            torch.cuda.synchronize()
+            row = dict(shape=name, design=design, emu=emu)
+            if what in ("fwd", "all"):
+                t = bench(lambda: run_fwd(o, lse))
+                row.update(fwd_us=round(t * 1e3, 2), fwd_tflops=round(flops_f / t / 1e9, 1))
+            if ref is None:
+                ref = (o.clone(), lse.clone())
+            else:
+                row.update(o_nan=int(torch.isnan(o.float()).sum()), lse_nan=int(torch.isnan(lse).sum()),
+                           o_maxdiff=float((o.float() - ref[0].float()).abs().max()),
+                           lse_maxdiff=float((lse - ref[1]).abs().max()))
+            if what in ("bwd", "all"):
+                delta = torch.empty_like(lse)
+                dqkv = torch.empty_like(qkv)
+                t = bench(lambda: run_bwd(o, lse, delta, dqkv))
+                row.update(bwd_us=round(t * 1e3, 2), bwd_tflops=round(2.5 * flops_f / t / 1e9, 1))
+            if name == "small" and emu:
+                bad = torch.isnan(o.float()).any(dim=1).nonzero().flatten().tolist()
+                row.update(nan_rows=bad[:8] + ["..."] + bad[-4:], n_bad=len(bad))
+            print(json.dumps(row), flush=True)
+        _lib.call("pc_attention_tune", 0, 2)
+        _lib.call("pc_attention_tune", 1, 6)
+
+
+if __name__ == "__main__":
+    main()

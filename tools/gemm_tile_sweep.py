@@ -30,14 +30,18 @@ def t():
     return e0.elapsed_time(e1) / 10 * 1e3
 
 
-print(f"auto: {t():.1f} us")
-for bn in (64, 128, 192, 256):
-    for pair in (1, 2):
-        _lib.call("pc_gemm_set_tile_n", bn)
-        _lib.call("pc_gemm_set_cta_pair", pair)
-        try:
-            print(f"bn={bn} pair={pair}: {t():.1f} us")
-        except Exception as e:  # noqa: BLE001
-            print(f"bn={bn} pair={pair}: {e}")
-_lib.call("pc_gemm_set_tile_n", 0)
-_lib.call("pc_gemm_set_cta_pair", 0)
+splits = [int(x) for x in sys.argv[7].split(",")] if len(sys.argv) > 7 else [2]
+for ks in splits:
+    _lib.call("pc_gemm_set_max_split", ks)
+    print(f"max_split={ks} auto: {t():.1f} us", flush=True)
+    for bn in (64, 128, 192, 256):
+        for pair in (1, 2):
+            _lib.call("pc_gemm_set_tile_n", bn)
+            _lib.call("pc_gemm_set_cta_pair", pair)
+            try:
+                print(f"  max_split={ks} bn={bn} pair={pair}: {t():.1f} us", flush=True)
+            except Exception as e:  # noqa: BLE001
+                print(f"  max_split={ks} bn={bn} pair={pair}: {e}", flush=True)
+    _lib.call("pc_gemm_set_tile_n", 0)
+    _lib.call("pc_gemm_set_cta_pair", 0)
+_lib.call("pc_gemm_set_max_split", 4)
