@@ -1181,6 +1181,12 @@ class PipelineEngine:
             self._abort_channels()
             raise ctl.faults[0]
         self._wait_devices(actors, ctl)
+        if self.distributed and self._peer_faulted():
+            # a released wait on the faulted rank lets its stream run on and send
+            # garbage downstream: this rank finished on it and must not report it
+            self._faulted = True
+            raise LivenessFault("a peer rank faulted in this step (its watchdog fired); "
+                                "results are invalid")
         for key, ch in list(self._channels.items()) + list(self._tied_ch.items()):
             if not ch.drained():
                 raise ChannelOrderFault(f"channel {key} holds undelivered messages at step end")
@@ -1272,11 +1278,26 @@ class PipelineEngine:
             time.sleep(0.002)
         return True
 
+    def _fault_key(self) -> str:
+        return f"pp200/fault/{self._tag}"
+
+    def _peer_faulted(self) -> bool:
+        import torch.distributed as dist
+        return dist.distributed_c10d._get_default_store().check([self._fault_key()])
+
     def _abort_channels(self):
         """Fault path (executor.py:443-451): NCCL communicators are aborted, peer
         receivers release their own flag waits, so every stream drains; the
-        engine refuses further steps."""
+        engine refuses further steps.  Across processes the fault is posted to
+        the rendezvous store first, so a rank whose step completes on the data
+        the released streams sent afterwards raises too."""
         self._faulted = True
+        if self.distributed:
+            try:
+                import torch.distributed as dist
+                dist.distributed_c10d._get_default_store().set(self._fault_key(), "1")
+            except Exception:  # noqa: BLE001 - best effort, the fault itself is reported
+                pass
         for ch in list(self._channels.values()) + list(self._tied_ch.values()):
             try:
                 ch.abort()
