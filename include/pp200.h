@@ -106,6 +106,10 @@ int pc_sum_f32(int64_t n, const float* x, float* out, void* stream);
 /* out[c] (+)= sum_r x[r,c]: "sum-to" (executor.py:50-56) and bias gradients. */
 int pc_col_sum(int dtype_in, int dtype_out, int64_t rows, int64_t cols, const void* x,
                int64_t ldx, void* out, int accumulate, void* ws, int64_t ws_bytes, void* stream);
+/* A/B hook: 1 (default) bf16 column sums (bias / LayerNorm / RMSNorm parameter
+ * gradients) as one-pass cluster reductions (no workspace), 0 the two-stage
+ * workspace kernel below. */
+int pc_colsum_set_cluster(int on);
 /* Scratch for the two-stage (many-CTA, fixed-order) column reductions used by
  * pc_col_sum and pc_layernorm_bwd; with ws == NULL they fall back to one stage. */
 int pc_reduce_workspace_bytes(int64_t rows, int64_t cols, int64_t* bytes);

@@ -100,6 +100,7 @@ SIGNATURES: dict[str, list] = {
     "pc_attention_set_impl": [_c_i],
     "pc_attention_tune": [_c_i, _c_i],
     "pc_gemm_set_max_split": [_c_i],
+    "pc_colsum_set_cluster": [_c_i],
     "pc_lmhead_xent_workspace": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)],
     "pc_lmhead_xent_fwd": [_c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p,
                            _c_i64, _c_p, _c_i64, _c_p, _c_p],
@@ -159,7 +160,7 @@ def exported_symbols() -> list[str]:
 
 # C-ABI calls that launch at least one kernel, counted for bench.py's gpu_launches.
 _NON_LAUNCH = {"pc_version", "pc_device_sm_count", "pc_gemm_set_tile_n", "pc_gemm_tile_choice", "pc_attention_set_impl", "pc_attention_tune",
-               "pc_gemm_set_tma_store", "pc_gemm_set_cta_pair", "pc_gemm_set_max_split", "pc_gemm_set_ablation",
+               "pc_gemm_set_tma_store", "pc_gemm_set_cta_pair", "pc_gemm_set_max_split", "pc_colsum_set_cluster", "pc_gemm_set_ablation",
                "pc_embedding_bwd_workspace_bytes", "pc_reduce_workspace_bytes", "pc_p2p_available", "pc_p2p_unique_id",
                "pc_p2p_comm_init", "pc_p2p_abort", "pc_p2p_destroy",
                "pc_peer_alloc", "pc_peer_free", "pc_peer_open", "pc_peer_close",

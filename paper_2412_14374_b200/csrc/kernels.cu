@@ -418,7 +418,150 @@ __global__ void cast_kernel(int64_t n, const I* __restrict__ in, O* __restrict__
     stv(out, i, static_cast<typename Acc<O>::type>(ldv(in, i)));
 }
 
+// Column sums in one pass with the cross-CTA fold on chip: a cluster of CL CTAs
+// splits the rows of one 64-column slab; each CTA folds its 8 warps x 4 row
+// lanes in fixed order into 64 partials in its shared memory, and cluster rank
+// 0 adds the CL partials in rank order through distributed shared memory.  No
+// workspace, no atomics, deterministic.  Replaces colred_stage1's two global
+// round trips (partials out, last-CTA fold in) -- the bias / LayerNorm
+// parameter reductions were latency-bound at 0.2-0.5 of HBM (profiles/README.md).
+// MODE as colred_stage1.  Needs cols % 8 == 0, lda % 8 == 0, 16 B aligned rows.
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ float ld_shared_cluster_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __bfloat1622float2(h[j]);
+    v[2 * j] = f.x;
+    v[2 * j + 1] = f.y;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) colsum_cluster_kernel(
+    int64_t rows, int64_t cols, const __nv_bfloat16* __restrict__ a, int64_t lda,
+    const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, float* __restrict__ out1, float* __restrict__ out2,
+    int accumulate) {
+  constexpr int U = MODE == 1 ? 4 : 8;  // rows in flight per thread (x 2 tensors in MODE 1)
+  __shared__ float red1[8][4][64];
+  __shared__ float red2[MODE == 1 ? 8 : 1][4][64];
+  __shared__ float part[2][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cg = lane & 7, sub = lane >> 3;  // 8 columns of the slab, one of 4 rows
+  const int64_t c0 = blockIdx.x * 64 + cg * 8;
+  const uint32_t rank = cluster_ctarank(), ncl = cluster_nctarank();
+  const int64_t rpc = (rows + ncl - 1) / ncl;
+  const int64_t r0 = rank * rpc, r1 = min(rows, r0 + rpc);
+  float s1[8] = {}, s2[8] = {};
+  if (c0 < cols) {
+    for (int64_t rb = r0 + sub + 4 * w; rb < r1; rb += 32 * U) {
+      uint4 u[U], ux[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const int64_t r = rb + 32 * i;
+        u[i] = r < r1 ? *reinterpret_cast<const uint4*>(a + r * lda + c0) : make_uint4(0, 0, 0, 0);
+        if (MODE == 1)
+          ux[i] = r < r1 ? *reinterpret_cast<const uint4*>(x + r * lda + c0) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        float v[8];
+        bf16x8_to_f32(u[i], v);
+        if (MODE == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) s1[j] += v[j];
+        } else {
+          const int64_t r = rb + 32 * i;
+          if (r < r1) {
+            float xv[8];
+            bf16x8_to_f32(ux[i], xv);
+            const float mu = mean ? mean[r] : 0.f, rs = rstd[r];  // no mean: RMSNorm
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              s1[j] += v[j] * ((xv[j] - mu) * rs);
+              s2[j] += v[j];
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    red1[w][sub][cg * 8 + j] = s1[j];
+    if (MODE == 1) red2[w][sub][cg * 8 + j] = s2[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        t1 += red1[k][q][threadIdx.x];
+        if (MODE == 1) t2 += red2[k][q][threadIdx.x];
+      }
+    part[0][threadIdx.x] = t1;
+    part[1][threadIdx.x] = t2;
+  }
+  cluster_sync_all();
+  const int64_t c = blockIdx.x * 64 + threadIdx.x;
+  if (rank == 0 && threadIdx.x < 64 && c < cols) {
+    const uint32_t p1 = smem_u32(&part[0][threadIdx.x]), p2 = smem_u32(&part[1][threadIdx.x]);
+    float t1 = 0.f, t2 = 0.f;
+    for (uint32_t q = 0; q < ncl; ++q) {
+      t1 += ld_shared_cluster_f32(mapa_shared(p1, q));
+      if (MODE == 1) t2 += ld_shared_cluster_f32(mapa_shared(p2, q));
+    }
+    out1[c] = accumulate ? out1[c] + t1 : t1;
+    if (MODE == 1 && out2) out2[c] = accumulate ? out2[c] + t2 : t2;
+  }
+  cluster_sync_all();  // peers' partials stay valid until rank 0 has read them
+}
+
+template <int MODE>
+int colsum_cluster_launch(int64_t rows, int64_t cols, const __nv_bfloat16* a, int64_t lda,
+                          const __nv_bfloat16* x, const float* mean, const float* rstd, float* out1,
+                          float* out2, int accumulate, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(colsum_cluster_kernel<MODE>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  // 16 CTAs per slab (non-portable cluster) where each still gets >= 256 rows
+  unsigned cl = 16;
+  while (cl > 1 && rows < static_cast<int64_t>(cl) * 256) cl >>= 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>((cols + 63) / 64), cl, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = cl;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, colsum_cluster_kernel<MODE>, rows, cols, a, lda, x, mean, rstd,
+                                 out1, out2, accumulate));
+  return check_launch("colsum_cluster_kernel");
+}
+
 }  // namespace
+
+int g_colsum_cluster = 1;  // pc_colsum_set_cluster (A/B hook)
 
 int64_t colred_chunks(int64_t rows) {
   int64_t r = (rows + 63) / 64;
@@ -438,6 +581,19 @@ template <typename T>
 bool colred_launch(int mode, int64_t rows, int64_t cols, const T* a, int64_t lda, const T* x,
                    const float* mean, const float* rstd, float* out1, float* out2,
                    int accumulate, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  if constexpr (sizeof(T) == 2) {
+    // one-pass cluster reduction where the layout allows 16 B row loads
+    const bool al = (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+                    (mode == 0 || (reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    if (g_colsum_cluster && rows > 0 && cols % 8 == 0 && lda % 8 == 0 && al) {
+      const auto* ab = reinterpret_cast<const __nv_bfloat16*>(a);
+      const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+      const int rc = mode == 0
+                         ? colsum_cluster_launch<0>(rows, cols, ab, lda, xb, mean, rstd, out1, out2, accumulate, st)
+                         : colsum_cluster_launch<1>(rows, cols, ab, lda, xb, mean, rstd, out1, out2, accumulate, st);
+      return rc == PC_OK;
+    }
+  }
   if (ws == nullptr || ws_bytes < colred_ws_bytes(rows, cols) || rows <= 0 ||
       (cols + CR_COLS - 1) / CR_COLS > COLRED_COUNTERS)
     return false;
@@ -483,6 +639,11 @@ using namespace pp200;
     case PC_BF16: { using T = __nv_bfloat16; __VA_ARGS__; break; }   \
     default: set_error("unsupported dtype %d", dtype); return PC_ERR_UNSUPPORTED; \
   }
+
+extern "C" int pc_colsum_set_cluster(int on) {
+  pp200::g_colsum_cluster = on ? 1 : 0;
+  return PC_OK;
+}
 
 extern "C" int pc_fill(int dtype, int64_t n, double value, void* out, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);

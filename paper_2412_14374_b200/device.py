@@ -94,6 +94,9 @@ _LN_PARAMS_MAIN = os.environ.get("PP200_LN_PARAMS_MAIN") == "1"   # A/B switch f
 _LN_FUSED = os.environ.get("PP200_LN_FUSED", "0") == "1"
 # A/B switch: 0 = logits GEMM then the stand-alone cross-entropy kernel (pc_xent_fwd_bwd)
 _XENT_FUSED = os.environ.get("PP200_XENT_FUSED", "1") != "0"
+# A/B switch: 0 = bf16 column sums through the two-stage workspace kernel instead of
+# the one-pass cluster reduction (pc_colsum_set_cluster)
+_COLSUM_CLUSTER = os.environ.get("PP200_COLSUM_CLUSTER", "1") != "0"
 
 
 class PeerBuf:
@@ -168,6 +171,8 @@ class DeviceOps:
         self.device = device
         self.stream = stream
         self.gpt = gpt
+        if not _COLSUM_CLUSTER:
+            call("pc_colsum_set_cluster", 0)
         self._plans: dict[int, _StagePlan] = {}
         # {param-grad value: fp32 accumulator} for the stage-bwd task being run:
         # the producer adds its partial straight onto the running sum (the

@@ -52,17 +52,29 @@ rows = []
 us = timed(lambda: _lib.call("pc_layernorm_fwd", _lib.PC_BF16, T, d, x.data_ptr(), g_.data_ptr(),
                              b_.data_ptr(), y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), 1e-5, s))
 rows.append(("layernorm_fwd [8192,768]", us, 2 * T * d * 2 + 8 * T))
-us = timed(lambda: _lib.call("pc_layernorm_bwd_acc", _lib.PC_BF16, T, d, dy.data_ptr(), x.data_ptr(),
-                             g_.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(),
-                             dx.data_ptr(), dg.data_ptr(), db.data_ptr(), 1, ws.data_ptr(),
-                             ws.numel(), s))
-rows.append(("layernorm_bwd(+params) [8192,768]", us, 4 * T * d * 2 + 8 * T))
-for n in (768, 2304, 3072):
-    a = torch.randn(T, n, device=dev).to(bf)
-    out = torch.zeros(n, device=dev)
-    us = timed(lambda: _lib.call("pc_col_sum", _lib.PC_BF16, _lib.PC_F32, T, n, a.data_ptr(), n,
-                                 out.data_ptr(), 1, ws.data_ptr(), ws.numel(), s))
-    rows.append((f"bias col_sum [8192,{n}]", us, T * n * 2))
+for cl in (0, 1):  # pc_colsum_set_cluster A/B: two-stage workspace vs one-pass cluster
+    _lib.call("pc_colsum_set_cluster", cl)
+    tag = "cluster" if cl else "2-stage"
+    dg.zero_(); db.zero_()
+    us = timed(lambda: _lib.call("pc_layernorm_bwd_acc", _lib.PC_BF16, T, d, dy.data_ptr(), x.data_ptr(),
+                                 g_.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(),
+                                 dx.data_ptr(), dg.data_ptr(), db.data_ptr(), 1, ws.data_ptr(),
+                                 ws.numel(), s))
+    rows.append((f"layernorm_bwd(+params) [8192,768] {tag}", us, 4 * T * d * 2 + 8 * T))
+    for n in (768, 2304, 3072):
+        torch.manual_seed(n)
+        a = torch.randn(T, n, device=dev).to(bf)
+        out = torch.zeros(n, device=dev)
+        us = timed(lambda: _lib.call("pc_col_sum", _lib.PC_BF16, _lib.PC_F32, T, n, a.data_ptr(), n,
+                                     out.data_ptr(), 1, ws.data_ptr(), ws.numel(), s))
+        out.zero_()
+        _lib.call("pc_col_sum", _lib.PC_BF16, _lib.PC_F32, T, n, a.data_ptr(), n, out.data_ptr(), 0,
+                  ws.data_ptr(), ws.numel(), s)
+        torch.cuda.synchronize()
+        ref = a.double().sum(0)
+        err = float((out.double() - ref).abs().max() / ref.abs().max())
+        rows.append((f"bias col_sum [8192,{n}] {tag} (rel err {err:.1e})", us, T * n * 2))
+_lib.call("pc_colsum_set_cluster", 1)
 logits = torch.randn(T, V, device=dev).to(bf)
 tok = torch.randint(0, V, (T,), device=dev, dtype=torch.int32)
 rl = torch.empty(T, device=dev)
@@ -71,4 +83,4 @@ us = timed(lambda: _lib.call("pc_xent_fwd_bwd", _lib.PC_BF16, T, V, S, logits.da
 rows.append(("xent fwd+bwd [8192,50304]", us, 2 * T * V * 2))
 hbm = peak.get("hbm_gbs", 6546.2)
 for name, us, by in rows:
-    print(f"{name:36s} {us:8.1f} us  {by / us / 1e3:7.0f} GB/s  ({by / us / 1e3 / hbm:.2f} of {hbm:.0f})")
+    print(f"{name:56s} {us:8.1f} us  {by / us / 1e3:7.0f} GB/s  ({by / us / 1e3 / hbm:.2f} of {hbm:.0f})")
