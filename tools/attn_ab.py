@@ -41,7 +41,7 @@ def main():
             _lib.call("pc_attention_gqa_bwd", 2, B, H, H, S, hd, qkv.data_ptr(), ld, o.data_ptr(),
                       do.data_ptr(), H * hd, lse.data_ptr(), delta.data_ptr(), dqkv.data_ptr(), ld, st)
 
-        variants = [(1, 0), (2, 0), (2, 4), (2, 6), (2, 8), (2, 10), (2, 12)]
+        variants = [(1, 0), (2, 0), (2, 4), (2, 6), (2, 8)]
         ref = None
         for (design, emu) in variants:
             _lib.call("pc_attention_tune", 0, design)
