@@ -378,17 +378,26 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak, M=M_MICRO):
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4),
             "traffic": None if tr is None else round(tr),
-            "traffic_source": "profiles/r01_ncu_gemm_mix.json (ncu --set full, per launch)"
+            "traffic_source": f"profiles/{_gemm_mix_file().name} (ncu --set full, per launch)"
             if tr is not None else None,
             "kernel": "tc_gemm_kernel (tcgen05.mma kind::f16, TMA, TMEM)",
             "share_of_step": round(tot_ms / step_ms, 3) if step_ms else None,
             "shapes": per}
 
 
+def _gemm_mix_file() -> Path:
+    """The newest committed ncu --set full capture of the GEMM mix."""
+    d = Path(__file__).resolve().parent / "profiles"
+    for name in ("r02_ncu_gemm_mix.json", "r01_ncu_gemm_mix.json"):
+        if (d / name).exists():
+            return d / name
+    return d / "r02_ncu_gemm_mix.json"
+
+
 def gemm_traffic() -> dict:
     """{"MxNxK:epilogue": dram bytes read + written per launch} from the
     committed ncu --set full capture of the GEMM mix (tools/ncu_gemm_mix.py)."""
-    p = Path(__file__).resolve().parent / "profiles" / "r01_ncu_gemm_mix.json"
+    p = _gemm_mix_file()
     try:
         return {k: v["dram_bytes"] for k, v in json.loads(p.read_text())["shapes"].items()}
     except (OSError, ValueError, KeyError):

@@ -1,7 +1,7 @@
 """Issue every C2 GEMM of one stage step once, exactly as bench.gemm_roofline
 (and device.py) issue them, for an `ncu --set full -k regex:tc_gemm` capture;
 then (here, no GPU) `python tools/ncu_gemm_mix.py --parse rep.csv` writes
-profiles/r01_ncu_gemm_mix.json: DRAM bytes read + written per launch, keyed
+profiles/r02_ncu_gemm_mix.json: DRAM bytes read + written per launch, keyed
 like bench.gemm_traffic().
 
   GPU:  ncu --set full --clock-control none -k regex:tc_gemm -c 15 --csv --page raw \\
@@ -56,7 +56,7 @@ def parse(path):
     doc = {"source": "ncu --set full --clock-control none -k regex:tc_gemm, one launch per "
                      "shape (tools/ncu_gemm_mix.py); cold L2, replayed: compare bytes, not time",
            "shapes": out}
-    dst = pathlib.Path(__file__).resolve().parents[1] / "profiles" / "r01_ncu_gemm_mix.json"
+    dst = pathlib.Path(__file__).resolve().parents[1] / "profiles" / "r02_ncu_gemm_mix.json"
     dst.write_text(json.dumps(doc, indent=1) + "\n")
     print(json.dumps(doc, indent=1))
 
