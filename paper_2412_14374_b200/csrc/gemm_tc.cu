@@ -368,7 +368,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem_base = *tslot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    // warp-uniform producer loop, one elected lane issuing (a lane-0-only
+    // branch makes every barrier wait and TMA issue a divergent slow path;
+    // measured on the attention kernels, profiles/r02_attn_fwd64.txt)
+    {
       int stage = 0;
       uint32_t phase = 0;
       // the leader's full barrier counts both CTAs' bytes (one expect_tx)
@@ -386,31 +389,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = k_split_at(sp, nk, ep), kb_end = k_split_at(sp + 1, nk, ep); kb < kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (ep.flags & (1 << 17)) {  // profiling ablation: no operand traffic
-            if (rank == 0) mbar_arrive(&full[stage]);
+            if (rank == 0 && elect_one()) mbar_arrive(&full[stage]);
+            __syncwarp();
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
             continue;
           }
-          if (rank == 0) mbar_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
-          uint8_t* a = sA + stage * TC_A_BYTES;
-          uint8_t* b = sB + stage * Cfg::B_BYTES;
-          const int k0 = kb * TC_BK;
-          if (!A_MN) {
-            load(a, &tmA, stage, k0, m0);
-          } else {
+          if (elect_one()) {
+            if (rank == 0) mbar_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
+            uint8_t* a = sA + stage * TC_A_BYTES;
+            uint8_t* b = sB + stage * Cfg::B_BYTES;
+            const int k0 = kb * TC_BK;
+            if (!A_MN) {
+              load(a, &tmA, stage, k0, m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < TC_BM / 64; ++j)
-              load(a + j * TC_MN_CHUNK_BYTES, &tmA, stage, m0 + 64 * j, k0);
-          }
-          if (!B_MN) {
-            load(b, &tmB, stage, k0, nb);
-          } else {
+              for (int j = 0; j < TC_BM / 64; ++j)
+                load(a + j * TC_MN_CHUNK_BYTES, &tmA, stage, m0 + 64 * j, k0);
+            }
+            if (!B_MN) {
+              load(b, &tmB, stage, k0, nb);
+            } else {
 #pragma unroll
-            for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-              load(b + j * TC_MN_CHUNK_BYTES, &tmB, stage, nb + 64 * j, k0);
+              for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
+                load(b + j * TC_MN_CHUNK_BYTES, &tmB, stage, nb + 64 * j, k0);
+            }
           }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -976,8 +983,11 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
                          int* bn_out, int* cg_out, int* ks_out, int max_split = 2,
                          bool ordered = false) {
   struct Cand { int bn, cg; double eff; };
+  // per-tile factors re-measured in round 2 after the producer warp went
+  // warp-uniform (tools/gemm_sweep_mix.py, profiles/r02_gemm_sweep_c2.txt): the
+  // narrow tiles gained most (their TMA issue rate per FLOP is highest)
   const Cand cands[7] = {{256, 2, 1.0}, {192, 2, 0.97}, {256, 1, 0.88}, {192, 1, 0.85},
-                         {128, 2, 0.78}, {128, 1, 0.75}, {64, 1, 0.45}};
+                         {128, 2, 0.92}, {128, 1, 0.84}, {64, 1, 0.62}};
   const int sms = num_sms();
   can_split = can_split && K >= 2 * TC_BK * 8;
   if (!can_split) max_split = 1;
@@ -1005,9 +1015,10 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
       // deadlock, seen on C4's 512-unit weight gradients): one wave only.
       if (ordered && ks > 1 && tiles * ks > slots) break;
       const int64_t waves = (tiles * ks + slots - 1) / slots;
+      // split costs: the extra fp32 reduce-adds and, ordered, their chain
       const double score = static_cast<double>(M) * N * ks /
                            (static_cast<double>(waves) * slots * tm * c.bn) * c.eff *
-                           (ks == 1 ? 1.0 : ks == 2 ? 0.97 : 0.90);
+                           (ks == 1 ? 1.0 : ks == 2 ? 0.90 : 0.58);
       if (score > best + 1e-9) {
         best = score;
         bn = c.bn;
