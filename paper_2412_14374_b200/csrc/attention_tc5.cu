@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(256, 2)
   uint64_t* o_done = pv_done + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
   const int H = hs.H;
   const int nqb = (S + K::BM - 1) / K::BM;
   // grid (B*H, tiles): x varies fastest, so every head's longest (latest) tile
@@ -168,17 +169,21 @@ __global__ void __launch_bounds__(256, 2)
   const uint32_t tS = tmem, tO = tmem + 128;  // S[i] at tS + 64 i
 
   if (warp == 0) {
-    if (lane == 0) {
+    // warp-uniform loops, one elected lane issuing (see fa_fwd64_tc5)
+    if (elect_one()) {
       mbar_expect_tx(bar_q, K::Q_BYTES);
 #pragma unroll
       for (int p = 0; p < K::NP; ++p)
         for (int hf = 0; hf < 2; ++hf)
           tma_load_2d(sQ + p * K::Q_PANEL + hf * (K::Q_PANEL / 2), &tm, bar_q, hs.qcol(h) + 64 * p,
                       brow + q0 + 64 * hf);
-      for (int j = 0; j < nkb; ++j) {
-        const int s = j % K::STAGES;
-        const uint32_t ph = (j / K::STAGES) & 1;
-        mbar_wait(&kv_empty[s], ph ^ 1);
+    }
+    __syncwarp();
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j % K::STAGES;
+      const uint32_t ph = (j / K::STAGES) & 1;
+      mbar_wait(&kv_empty[s], ph ^ 1);
+      if (elect_one()) {
         mbar_expect_tx(&kv_full[s], 2 * K::KV_BYTES);
 #pragma unroll
         for (int p = 0; p < K::NP; ++p) {
@@ -188,36 +193,40 @@ __global__ void __launch_bounds__(256, 2)
                       hs.vcol(hk) + 64 * p, brow + j * K::BN);
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t ID_S = umma_idesc_bf16(K::BM, K::BN, 0, 0);  // Q, K both K-major
-      constexpr uint32_t ID_O = umma_idesc_bf16(K::BM, HD, 0, 1);     // P K-major, V MN-major
-      mbar_wait(bar_q, 0);
+    constexpr uint32_t ID_S = umma_idesc_bf16(K::BM, K::BN, 0, 0);  // Q, K both K-major
+    constexpr uint32_t ID_O = umma_idesc_bf16(K::BM, HD, 0, 1);     // P K-major, V MN-major
+    mbar_wait(bar_q, 0);
+    tc_fence_after();
+    const uint32_t q_addr = smem_u32(sQ);
+    auto issue_s = [&](int j) {  // S_j = Q K_j^T into S[j % 2]
+      const int s = j % K::STAGES;
+      mbar_wait(&kv_full[s], (j / K::STAGES) & 1);
+      // S[j % 2] still holds P_{j-2}: wait until PV_{j-2} has read it
+      if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
       tc_fence_after();
-      const uint32_t q_addr = smem_u32(sQ);
-      auto issue_s = [&](int j) {  // S_j = Q K_j^T into S[j % 2]
-        const int s = j % K::STAGES;
-        mbar_wait(&kv_full[s], (j / K::STAGES) & 1);
-        // S[j % 2] still holds P_{j-2}: wait until PV_{j-2} has read it
-        if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + s * K::KV_BYTES);
+      const uint32_t k_addr = smem_u32(sK + s * K::KV_BYTES);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           tc_mma_f16(tS + (j & 1) * 64, kmajor_step(q_addr, k, K::Q_PANEL),
                      kmajor_step(k_addr, k, K::KV_PANEL), ID_S, k > 0 ? 1u : 0u);
         tc_commit(&s_full[j & 1]);
-      };
-      issue_s(0);
-      for (int j = 0; j < nkb; ++j) {
-        // S[(j+1) % 2] was last read by softmax j-1, which finished before PV_{j-1}
-        if (j + 1 < nkb) issue_s(j + 1);
-        const int s = j % K::STAGES;
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV + s * K::KV_BYTES);
-        const uint32_t tP = tS + (j & 1) * 64;  // P_j packed bf16, key chunk k at column 8 k
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nkb; ++j) {
+      // S[(j+1) % 2] was last read by softmax j-1, which finished before PV_{j-1}
+      if (j + 1 < nkb) issue_s(j + 1);
+      const int s = j % K::STAGES;
+      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t v_addr = smem_u32(sV + s * K::KV_BYTES);
+      const uint32_t tP = tS + (j & 1) * 64;  // P_j packed bf16, key chunk k at column 8 k
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < K::BN / 16; ++k)
           tc_mma_f16_ts(tO, tP + 8 * k, umma_sdesc_sw128(v_addr + k * 2048, K::KV_PANEL, 1024),
@@ -225,8 +234,10 @@ __global__ void __launch_bounds__(256, 2)
         tc_commit(&pv_done[j & 1]);
         tc_commit(&kv_empty[s]);
       }
-      tc_commit(o_done);
+      __syncwarp();
     }
+    if (elect_one()) tc_commit(o_done);
+    __syncwarp();
   } else if (warp >= 4) {
     const int qw = warp & 3;              // TMEM lane quarter
     const int r = qw * 32 + lane;          // row within the tile
@@ -895,14 +906,15 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
-      uint32_t g = 0, ic = 0;
-      for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
-        int b, hk, k0, qbeg, nq;
-        decode(w, b, hk, k0, qbeg, nq);
-        const int brow = b * S;
-        const int kb = ic % K::KVBUF;
-        mbar_wait(&kv_empty[kb], ((ic / K::KVBUF) & 1) ^ 1);
+    // warp-uniform loop, one elected lane issuing (see fa_fwd64_tc5)
+    uint32_t g = 0, ic = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+      int b, hk, k0, qbeg, nq;
+      decode(w, b, hk, k0, qbeg, nq);
+      const int brow = b * S;
+      const int kb = ic % K::KVBUF;
+      mbar_wait(&kv_empty[kb], ((ic / K::KVBUF) & 1) ^ 1);
+      if (elect_one()) {
         mbar_expect_tx(&kv_full[kb], 2 * K::KV_BYTES);
         for (int p = 0; p < K::NP; ++p)
           for (int hf = 0; hf < 2; ++hf) {
@@ -910,13 +922,16 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
             tma_load_2d(sK + off, &tq, &kv_full[kb], hs.kcol(hk) + 64 * p, brow + k0 + hf * 64);
             tma_load_2d(sV + off, &tq, &kv_full[kb], hs.vcol(hk) + 64 * p, brow + k0 + hf * 64);
           }
-        for (int i = 0; i < G * nq; ++i, ++g) {
-          const int h = hk * G + i / nq;
-          const int st = g % K::STAGES;
-          const int m0 = (qbeg + i % nq) * K::BQ;
-          const int64_t vbase = (static_cast<int64_t>(b) * H + h) * S;
-          const uint32_t lbytes = static_cast<uint32_t>(min(K::BQ, S - m0)) * 4;  // S % 4 == 0
-          mbar_wait(&q_empty[st], ((g / K::STAGES) & 1) ^ 1);
+      }
+      __syncwarp();
+      for (int i = 0; i < G * nq; ++i, ++g) {
+        const int h = hk * G + i / nq;
+        const int st = g % K::STAGES;
+        const int m0 = (qbeg + i % nq) * K::BQ;
+        const int64_t vbase = (static_cast<int64_t>(b) * H + h) * S;
+        const uint32_t lbytes = static_cast<uint32_t>(min(K::BQ, S - m0)) * 4;  // S % 4 == 0
+        mbar_wait(&q_empty[st], ((g / K::STAGES) & 1) ^ 1);
+        if (elect_one()) {
           mbar_expect_tx(&q_full[st], 2 * K::Q_BYTES + 2 * lbytes);
           for (int p = 0; p < K::NP; ++p) {
             tma_load_2d(sQ + st * K::Q_BYTES + p * K::Q_PANEL, &tq, &q_full[st], hs.qcol(h) + 64 * p, brow + m0);
@@ -925,6 +940,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
           bulk_load(sLD + st * 128, lse + vbase + m0, lbytes, &q_full[st]);
           bulk_load(sLD + st * 128 + 64, delta + vbase + m0, lbytes, &q_full[st]);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
@@ -1198,14 +1214,15 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
-      uint32_t g = 0, ic = 0;
-      for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
-        int bh, q0, nkb;
-        decode(w, bh, q0, nkb);
-        const int b = bh / H, h = bh % H, hk = h / hs.G, brow = b * S;
-        const int qb = ic % K::QBUF;
-        mbar_wait(&q_empty[qb], ((ic / K::QBUF) & 1) ^ 1);
+    // warp-uniform loop, one elected lane issuing (see fa_fwd64_tc5)
+    uint32_t g = 0, ic = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+      int bh, q0, nkb;
+      decode(w, bh, q0, nkb);
+      const int b = bh / H, h = bh % H, hk = h / hs.G, brow = b * S;
+      const int qb = ic % K::QBUF;
+      mbar_wait(&q_empty[qb], ((ic / K::QBUF) & 1) ^ 1);
+      if (elect_one()) {
         mbar_expect_tx(&q_full[qb], 3 * K::Q_BYTES);
         for (int p = 0; p < K::NP; ++p)
           for (int hf = 0; hf < 2; ++hf) {
@@ -1215,9 +1232,12 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
             tma_load_2d(sG + off, &tg, &q_full[qb], x, y);
             tma_load_2d(sO + off, &to, &q_full[qb], x, y);
           }
-        for (int j = 0; j < nkb; ++j, ++g) {
-          const int st = g % K::STAGES;
-          mbar_wait(&kv_empty[st], ((g / K::STAGES) & 1) ^ 1);
+      }
+      __syncwarp();
+      for (int j = 0; j < nkb; ++j, ++g) {
+        const int st = g % K::STAGES;
+        mbar_wait(&kv_empty[st], ((g / K::STAGES) & 1) ^ 1);
+        if (elect_one()) {
           mbar_expect_tx(&kv_full[st], 2 * K::KV_BYTES);
           for (int p = 0; p < K::NP; ++p) {
             tma_load_2d(sK + st * K::KV_BYTES + p * K::KV_PANEL, &tq, &kv_full[st],
@@ -1226,6 +1246,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
                         hs.vcol(hk) + 64 * p, brow + j * K::BN);
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
