@@ -973,26 +973,29 @@ int dispatch_majors(bool a_mn, bool b_mn, int ek, const CUtensorMap& ta, const C
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder_fn() { return tmap_encoder(); }
 
-// Pick (tile width, CTA pair, K split) maximising wave efficiency x per-tile
-// efficiency: useful area / (waves x slots x tile area) penalises a last
-// partial wave (e.g. 192 tiles on 148 SMs) and padding; the per-tile factor
-// is the measured mainloop efficiency of that tile shape.  Deterministic
-// split-K: exactly 2 K halves reduce-added onto a zero-filled fp32 C
-// (0 + a + b == 0 + b + a bitwise), only when the caller allows it.
+// Pick (tile width, CTA pair, K split) minimising a per-SM time model:
+//   waves x (mainloop + epilogue) + the split reduce-adds,
+// mainloop = K-split length x (tile FLOPs / SM peak) / eff(tile) -- the large
+// pair tiles sustain more of the peak on long K (fewer operand bytes per FLOP),
+// the narrow ones lose less to a partial last wave -- and epilogue = the tile's
+// C bytes per SM at ~30 B / clk plus ~1000 cycles; an ordered split adds one
+// epilogue per chain link, an unordered one a single reduce-add.  The factors
+// were fit to tools/gemm_sweep_mix.py over the C2-C5 shapes (round 2,
+// profiles/r02_gemm_sweep_*.txt).  Deterministic split-K: exactly 2 K halves
+// reduce-added onto a zero-filled fp32 C (0 + a + b == 0 + b + a bitwise), or
+// the ordered protocol, only when the caller allows it.  c_bytes: bytes moved
+// per C element by the epilogue (bf16 store 2, fp32 store 4, fp32 add 8).
 static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool can_split,
                          int* bn_out, int* cg_out, int* ks_out, int max_split = 2,
-                         bool ordered = false) {
+                         bool ordered = false, double c_bytes = 2.0) {
   struct Cand { int bn, cg; double eff; };
-  // per-tile factors re-measured in round 2 after the producer warp went
-  // warp-uniform (tools/gemm_sweep_mix.py, profiles/r02_gemm_sweep_c2.txt): the
-  // narrow tiles gained most (their TMA issue rate per FLOP is highest)
-  const Cand cands[7] = {{256, 2, 1.0}, {192, 2, 0.97}, {256, 1, 0.88}, {192, 1, 0.85},
-                         {128, 2, 0.92}, {128, 1, 0.84}, {64, 1, 0.62}};
+  const Cand cands[7] = {{256, 2, 0.95}, {192, 2, 0.85}, {256, 1, 0.80}, {192, 1, 0.80},
+                         {128, 2, 0.80}, {128, 1, 0.75}, {64, 1, 0.55}};
   const int sms = num_sms();
   can_split = can_split && K >= 2 * TC_BK * 8;
   if (!can_split) max_split = 1;
   int bn = 0, cg = 1, ksplit = 1;
-  double best = -1.0;
+  double best = 1e300;
   for (const Cand& c : cands) {
     if (g_force_bn && c.bn != g_force_bn) continue;
     if (g_cta_pair == 1 && c.cg == 2) continue;
@@ -1007,6 +1010,8 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
     const int64_t tm = TC_BM * c.cg;
     const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
     const int64_t slots = sms / c.cg;
+    const double flop_cycles = static_cast<double>(tm) * c.bn * 2.0 / (c.cg * 8192.0);  // per k
+    const double epi = static_cast<double>(tm) * c.bn * c_bytes / c.cg / 30.0 + 1000.0;
     for (int ks = 1; ks <= max_split; ks *= 2) {
       if (K < static_cast<int64_t>(ks) * TC_BK * 8) break;   // >= 8 k-blocks per split
       // Ordered split-K makes split s of a tile wait for split s-1 on another CTA.
@@ -1015,12 +1020,11 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
       // deadlock, seen on C4's 512-unit weight gradients): one wave only.
       if (ordered && ks > 1 && tiles * ks > slots) break;
       const int64_t waves = (tiles * ks + slots - 1) / slots;
-      // split costs: the extra fp32 reduce-adds and, ordered, their chain
-      const double score = static_cast<double>(M) * N * ks /
-                           (static_cast<double>(waves) * slots * tm * c.bn) * c.eff *
-                           (ks == 1 ? 1.0 : ks == 2 ? 0.90 : 0.58);
-      if (score > best + 1e-9) {
-        best = score;
+      const double kper = static_cast<double>((K + ks - 1) / ks);
+      double t = static_cast<double>(waves) * (kper * flop_cycles / c.eff + epi);
+      if (ks > 1) t += (ordered ? ks - 1 : 1) * epi;
+      if (t < best * (1.0 - 1e-9)) {
+        best = t;
         bn = c.bn;
         cg = c.cg;
         ksplit = ks;
@@ -1063,8 +1067,9 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   // 26.4 us and the other weight gradients are unchanged or faster, 8 is slower)
   // unordered split-K onto a zero C is only order-independent for 2 halves
   // (0 + a + b == 0 + b + a): more splits need the ordered protocol
+  const double c_bytes = (epi & PC_EPI_ACCUM) ? 8.0 : out_f32 ? 4.0 : 2.0;
   choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit, ordered ? g_max_split : std::min(g_max_split, 2),
-               ordered);
+               ordered, c_bytes);
   // raster: an A operand far larger than L2 (the LM-head gradients: 824 MB of
   // logit gradients) is streamed once when the tiles sharing its rows run
   // together; otherwise walk M (B is the large, reused operand)
@@ -1155,7 +1160,8 @@ extern "C" int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, 
                                    int* bn, int* cta_pair, int* ksplit) {
   PP_CHECK_ARG(M > 0 && N > 0 && K > 0 && bn && cta_pair && ksplit, "gemm_tile_choice: bad args");
   pp200::choose_tiles(transB != 0, M, N, K, split_ok != 0, bn, cta_pair, ksplit,
-                      split_ok == 2 ? pp200::g_max_split : 2, split_ok == 2);
+                      split_ok == 2 ? pp200::g_max_split : 2, split_ok == 2,
+                      split_ok == 2 ? 8.0 : split_ok ? 4.0 : 2.0);
   return PC_OK;
 }
 
