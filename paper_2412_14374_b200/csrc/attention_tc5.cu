@@ -866,6 +866,12 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
   const int nkt = (S + K::KEYS - 1) / K::KEYS, nqb = (S + K::BQ - 1) / K::BQ;
   const int BHk = B * hs.Hkv;
   const int items = BHk * nkt;
+  // k-th item of this CTA: snake order over the longest-first list (a plain
+  // stride left the first CTAs ~15 % more key blocks than the last)
+  auto snake_item = [&](int k) {
+    const int r = k >> 1, G2 = 2 * static_cast<int>(gridDim.x);
+    return (k & 1) ? G2 * r + G2 - 1 - static_cast<int>(blockIdx.x) : G2 * r + static_cast<int>(blockIdx.x);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
@@ -908,7 +914,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
   if (warp == 0) {
     // warp-uniform loop, one elected lane issuing (see fa_fwd64_tc5)
     uint32_t g = 0, ic = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+    for (int w = snake_item(0); w < items; w = snake_item(++ic)) {
       int b, hk, k0, qbeg, nq;
       decode(w, b, hk, k0, qbeg, nq);
       const int brow = b * S;
@@ -949,7 +955,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
     const uint64_t qn = umma_sdesc_sw128(smem_u32(sQ), K::Q_PANEL, 1024);  // MN-major views
     const uint64_t gn = umma_sdesc_sw128(smem_u32(sG), K::Q_PANEL, 1024);
     uint32_t g0 = 0, ic = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+    for (int w = snake_item(0); w < items; w = snake_item(++ic)) {
       int b, hk, k0, qbeg, nq;
       decode(w, b, hk, k0, qbeg, nq);
       const int n = G * nq;
@@ -1015,7 +1021,7 @@ __global__ void __launch_bounds__(BwdKV<HD>::THREADS, 1)
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
     uint32_t g0 = 0, ic = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+    for (int w = snake_item(0); w < items; w = snake_item(++ic)) {
       int b, hk, k0, qbeg, nq;
       decode(w, b, hk, k0, qbeg, nq);
       const int brow = b * S;
@@ -1177,6 +1183,10 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
   const int H = hs.H;
   const int nqt = (S + K::BM - 1) / K::BM;
   const int items = BH * nqt;
+  auto snake_item = [&](int k) {  // see fa_bwd_dkdv_tc5
+    const int r = k >> 1, G2 = 2 * static_cast<int>(gridDim.x);
+    return (k & 1) ? G2 * r + G2 - 1 - static_cast<int>(blockIdx.x) : G2 * r + static_cast<int>(blockIdx.x);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
@@ -1216,7 +1226,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
   if (warp == 0) {
     // warp-uniform loop, one elected lane issuing (see fa_fwd64_tc5)
     uint32_t g = 0, ic = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+    for (int w = snake_item(0); w < items; w = snake_item(++ic)) {
       int bh, q0, nkb;
       decode(w, bh, q0, nkb);
       const int b = bh / H, h = bh % H, hk = h / hs.G, brow = b * S;
@@ -1254,7 +1264,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
     constexpr uint32_t ID_A = umma_idesc_bf16(128, HD, 0, 1);     // dS x K (MN-major)
     const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), K::KV_PANEL, 1024);   // MN-major view
     uint32_t g0 = 0, ic = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+    for (int w = snake_item(0); w < items; w = snake_item(++ic)) {
       int bh, q0, nkb;
       decode(w, bh, q0, nkb);
       const int qb = ic % K::QBUF;
@@ -1316,7 +1326,7 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
     const uint32_t lo = static_cast<uint32_t>(qw * 32) << 16;
     const uint64_t sc2 = pack_f2(sl2, sl2);
     uint32_t g0 = 0, ic = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++ic) {
+    for (int w = snake_item(0); w < items; w = snake_item(++ic)) {
       int bh, q0, nkb;
       decode(w, bh, q0, nkb);
       const int b = bh / H, h = bh % H, brow = b * S;
