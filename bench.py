@@ -335,23 +335,50 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak, M=M_MICRO):
     tot_flops = tot_ms = 0.0
     per = []
     traffic = gemm_traffic()
+    # GPT blocks issue the attention-output and qkv weight gradients as one
+    # grouped launch (device.py _wgrad_pair_into): time them that way
+    WG = _lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED
+    d = cfg.d_model
+    pair = None
+    if not hasattr(cfg, "n_kv_heads") and (3 * d) % 256 == 0 and \
+            os.environ.get("PP200_WGRAD_PAIR", "1") != "0":
+        wo, wq = (d, d, cfg.tokens, 1, 0, WG, 0, 0, 1), (3 * d, d, cfg.tokens, 1, 0, WG, 0, 0, 1)
+        if wo in block and wq in block:
+            block = [s for s in block if s not in (wo, wq)] + [("pair", 3 * d, d, d, cfg.tokens)]
     for shape, count in [(s, stage_blocks) for s in block] + [(s, 1 if P == 1 else 0) for s in head]:
         if count == 0:
             continue
-        Mm, N, K, ta, tb, epi = shape[:6]
         if os.environ.get("PP200_BENCH_VERBOSE") == "1":
             print(f"[bench] roofline shape {shape}", file=sys.stderr, flush=True)
-        args, keep = gemm_args(shape, st)
+        if shape[0] == "pair":
+            _, M1, M2, N, K = shape
+            A1 = torch.randn(K, M1, device="cuda").bfloat16()
+            A2 = torch.randn(K, M2, device="cuda").bfloat16()
+            B1 = torch.randn(K, N, device="cuda").bfloat16()
+            B2 = torch.randn(K, N, device="cuda").bfloat16()
+            C1 = torch.zeros(M1, N, device="cuda")
+            C2 = torch.zeros(M2, N, device="cuda")
+            flags = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
+            fn = "pc_gemm_wgrad_pair"
+            args = (M1, M2, N, K, A1.data_ptr(), M1, B1.data_ptr(), N, C1.data_ptr(), N,
+                    A2.data_ptr(), M2, B2.data_ptr(), N, C2.data_ptr(), N, WG, flags.data_ptr(),
+                    flags.numel(), st.cuda_stream)
+            keep = (A1, A2, B1, B2, C1, C2, flags)
+            Mm, ta, tb, epi = M1 + M2, 1, 0, WG
+        else:
+            Mm, N, K, ta, tb, epi = shape[:6]
+            fn = "pc_gemm"
+            args, keep = gemm_args(shape, st)
         # device time of back-to-back launches, issued from a CUDA graph as in
         # the step (host launch cost would otherwise pace the short GEMMs)
         with torch.cuda.stream(st):
             for _ in range(3):
-                _lib.call("pc_gemm", *args)
+                _lib.call(fn, *args)
             reps = 10
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=st):
                 for _ in range(reps):
-                    _lib.call("pc_gemm", *args)
+                    _lib.call(fn, *args)
             g.replay()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
@@ -363,9 +390,15 @@ def gemm_roofline(cfg, P, stage_blocks, step_ms, peak, M=M_MICRO):
         fl = 2.0 * Mm * N * K
         row = {"shape": [Mm, N, K, ta, tb], "epilogue": epi, "ms": round(ms, 4),
                "tflops": round(fl / ms / 1e9, 1), "launches_per_mb": count}
-        key = f"{Mm}x{N}x{K}:{epi}"
-        if key in traffic:
-            row["dram_bytes"] = traffic[key]
+        if shape[0] == "pair":
+            row["pair"] = [shape[1], shape[2]]
+            k1, k2 = f"{shape[1]}x{N}x{K}:{epi}", f"{shape[2]}x{N}x{K}:{epi}"
+            if k1 in traffic and k2 in traffic:
+                row["dram_bytes"] = traffic[k1] + traffic[k2]
+        else:
+            key = f"{Mm}x{N}x{K}:{epi}"
+            if key in traffic:
+                row["dram_bytes"] = traffic[key]
         per.append(row)
         tot_flops += fl * count * M
         tot_ms += ms * count * M

@@ -74,6 +74,16 @@ int pc_gemm(int dtype_in, int dtype_out, int transA, int transB, int64_t M, int6
  * 0 = no split allowed, 1 = PC_EPI_SPLITK_ZERO_C with fp32 C (K split 1 or 2),
  * 2 = PC_EPI_ACCUM | PC_EPI_SPLITK_ORDERED (1 or 2)): tile width, CTA pair (1 or 2),
  * K split. */
+/* Two weight gradients in one launch (the attention-output and qkv weights of a
+ * block share N = d_model and K = tokens): C1 (+)= A1^T B1 [M1 x N] and
+ * C2 (+)= A2^T B2 [M2 x N], A / B stored [K, M] / [K, N] bf16 (MN-major), C fp32,
+ * epilogue PC_EPI_ACCUM | PC_EPI_SPLITK_ORDERED (aux = zeroed flag array) or
+ * PC_EPI_SPLITK_ZERO_C.  M1 must fill whole tiles (a multiple of 256).  Replaces two
+ * `matmul`s of the accumulation chain (executor.py:66-67) with the same sums. */
+int pc_gemm_wgrad_pair(int64_t M1, int64_t M2, int64_t N, int64_t K, const void* A1, int64_t lda1,
+                       const void* B1, int64_t ldb1, float* C1, int64_t ldc1, const void* A2,
+                       int64_t lda2, const void* B2, int64_t ldb2, float* C2, int64_t ldc2,
+                       int epilogue, void* aux, int64_t ldaux, void* stream);
 int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_ok, int* bn,
                         int* cta_pair, int* ksplit);
 /* Force the tcgen05 GEMM tile width (0 = heuristic, else 64/128/192/256). Test hook. */

@@ -100,6 +100,8 @@ SIGNATURES: dict[str, list] = {
     "pc_attention_set_impl": [_c_i],
     "pc_attention_tune": [_c_i, _c_i],
     "pc_gemm_set_max_split": [_c_i],
+    "pc_gemm_wgrad_pair": [_c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64,
+                           _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i, _c_p, _c_i64, _c_p],
     "pc_colsum_set_cluster": [_c_i],
     "pc_lmhead_xent_workspace": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)],
     "pc_lmhead_xent_fwd": [_c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p,

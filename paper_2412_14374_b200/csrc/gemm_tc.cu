@@ -59,7 +59,15 @@ struct TcEpi {
   // outputs that group stored -- stats[row * ld_stats + n_tile * TC_EPI_G + group]
   float2* stats;
   int ld_stats;
+  int m2_row0;  // grouped pair (pc_gemm_wgrad_pair): rows >= m2_row0 are problem 2, 0 = one problem
 };
+
+// Second problem of a grouped weight-gradient pair: C2 (+)= op(A2) op(B2) with the
+// same N, K, majors and epilogue; its M tiles follow the first problem's.
+struct TcGroup {
+  CUtensorMap a, b, c;
+};
+
 
 // First k-block of split ``sp`` (sp = ksplit: the end).  Ordered split-K
 // staggers the split lengths (each dl = nk / (4 ks) k-blocks longer than the
@@ -313,7 +321,8 @@ template <int BN, bool A_MN, bool B_MN, int CG, int EK>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmU,
-                   const __grid_constant__ CUtensorMap tmX, int M, int N, int K, TcEpi ep) {
+                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ TcGroup g2, int M,
+                   int N, int K, TcEpi ep) {
   using Cfg = TcCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
   static_assert(!B_MN || Cfg::B_ROWS % 64 == 0, "MN-major B needs 64-wide chunks per CTA");
@@ -344,6 +353,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (ep.m2_row0) {
+      tma_prefetch_desc(&g2.a);
+      tma_prefetch_desc(&g2.b);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -384,7 +397,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int u = cid; u < num_units; u += ncl) {
         const int t = u % num_tiles, sp = u / num_tiles;
         const int mi = ep.n_fast ? t / num_n : t % num_m, ni = ep.n_fast ? t % num_n : t / num_m;
-        const int m0 = mi * TC_BM * CG + static_cast<int>(rank) * TC_BM;
+        // grouped pair: tiles past the first problem's rows read the second's operands
+        const bool p2 = ep.m2_row0 && mi * TC_BM * CG >= ep.m2_row0;
+        const CUtensorMap* pA = p2 ? &g2.a : &tmA;
+        const CUtensorMap* pB = p2 ? &g2.b : &tmB;
+        const int m0 = mi * TC_BM * CG + static_cast<int>(rank) * TC_BM - (p2 ? ep.m2_row0 : 0);
         const int nb = ni * BN + static_cast<int>(rank) * Cfg::B_ROWS;
         for (int kb = k_split_at(sp, nk, ep), kb_end = k_split_at(sp + 1, nk, ep); kb < kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -403,18 +420,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             uint8_t* b = sB + stage * Cfg::B_BYTES;
             const int k0 = kb * TC_BK;
             if (!A_MN) {
-              load(a, &tmA, stage, k0, m0);
+              load(a, pA, stage, k0, m0);
             } else {
 #pragma unroll
               for (int j = 0; j < TC_BM / 64; ++j)
-                load(a + j * TC_MN_CHUNK_BYTES, &tmA, stage, m0 + 64 * j, k0);
+                load(a + j * TC_MN_CHUNK_BYTES, pA, stage, m0 + 64 * j, k0);
             }
             if (!B_MN) {
-              load(b, &tmB, stage, k0, nb);
+              load(b, pB, stage, k0, nb);
             } else {
 #pragma unroll
               for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-                load(b + j * TC_MN_CHUNK_BYTES, &tmB, stage, nb + 64 * j, k0);
+                load(b + j * TC_MN_CHUNK_BYTES, pB, stage, nb + 64 * j, k0);
             }
           }
           __syncwarp();
@@ -530,6 +547,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int mi = ep.n_fast ? t / num_n : t % num_m, ni = ep.n_fast ? t % num_n : t / num_m;
       const int m0 = mi * TC_BM * CG + static_cast<int>(rank) * TC_BM;
       const int n0 = ni * BN;
+      // grouped pair: the second problem's tiles store to its C at local rows
+      const bool p2 = ep.m2_row0 && mi * TC_BM * CG >= ep.m2_row0;
+      const CUtensorMap* pC = p2 ? &g2.c : &tmC;
+      const int m0s = m0 - (p2 ? ep.m2_row0 : 0);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
@@ -569,7 +590,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+            tma_store_2d(pC, stg, n0 + cc, m0s + q * 32);
             bulk_commit();
           }
           if (ep.stats != nullptr) {
@@ -639,7 +660,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, sA, n0 + cc, m0 + q * 32);
+            tma_store_2d(pC, sA, n0 + cc, m0s + q * 32);
             bulk_commit();
           }
         }
@@ -704,7 +725,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, X, n0 + cc, m0 + q * 32);
+            tma_store_2d(pC, X, n0 + cc, m0s + q * 32);
             bulk_commit();
           }
         }
@@ -784,9 +805,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           if (ep.ksplit > 1 || (ep.flags & PC_EPI_ACCUM))
-            tma_reduce_add_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+            tma_reduce_add_2d(pC, stg, n0 + cc, m0s + q * 32);
           else
-            tma_store_2d(&tmC, stg, n0 + cc, m0 + q * 32);
+            tma_store_2d(pC, stg, n0 + cc, m0s + q * 32);
           if (stage_u) tma_store_2d(&tmU, stg + 2048, n0 + cc, m0 + q * 32);
           bulk_commit();
         }
@@ -890,8 +911,8 @@ int g_ablate = 0;    // profiling: bit0 skip epilogue work, bit1 skip operand lo
 
 template <int BN, bool A_MN, bool B_MN, int CG, int EK>
 int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-              const CUtensorMap& tu, const CUtensorMap& tx, int M, int N, int K, const TcEpi& ep,
-              cudaStream_t st) {
+              const CUtensorMap& tu, const CUtensorMap& tx, const TcGroup& g2, int M, int N, int K,
+              const TcEpi& ep, cudaStream_t st) {
   using Cfg = TcCfg<BN, CG>;
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG, EK>;
   static int max_units = 0;  // benign race: idempotent attribute write / query
@@ -920,7 +941,7 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
   const int units = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN) * ep.ksplit;
   const int groups = units < max_units ? units : max_units;
   if constexpr (CG == 1) {
-    kern<<<groups, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, tx, M, N, K, ep);
+    kern<<<groups, TC_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tu, tx, g2, M, N, K, ep);
   } else {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -934,7 +955,7 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tu, tx, M, N, K, ep));
+    PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tu, tx, g2, M, N, K, ep));
   }
   return check_launch("tc_gemm_kernel");
 }
@@ -942,30 +963,30 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
 // A_MN is only ever used by weight gradients (fp32 C): generic epilogue only.
 template <int BN, int CG, bool B_MN>
 int dispatch_ek(bool a_mn, int ek, const CUtensorMap& ta, const CUtensorMap& tb,
-                const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, int M, int N,
+                const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, const TcGroup& g2, int M, int N,
                 int K, const TcEpi& ep, cudaStream_t st) {
-  if (a_mn) return launch_tc<BN, true, B_MN, CG, EK_GENERIC>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+  if (a_mn) return launch_tc<BN, true, B_MN, CG, EK_GENERIC>(ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
   switch (ek) {
-    case EK_PLAIN: return launch_tc<BN, false, B_MN, CG, EK_PLAIN>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-    case EK_ACT: return launch_tc<BN, false, B_MN, CG, EK_ACT>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-    case EK_AUX: return launch_tc<BN, false, B_MN, CG, EK_AUX>(ta, tb, tc, tu, tx, M, N, K, ep, st);
-    default: return launch_tc<BN, false, B_MN, CG, EK_GENERIC>(ta, tb, tc, tu, tx, M, N, K, ep, st);
+    case EK_PLAIN: return launch_tc<BN, false, B_MN, CG, EK_PLAIN>(ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
+    case EK_ACT: return launch_tc<BN, false, B_MN, CG, EK_ACT>(ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
+    case EK_AUX: return launch_tc<BN, false, B_MN, CG, EK_AUX>(ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
+    default: return launch_tc<BN, false, B_MN, CG, EK_GENERIC>(ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
   }
 }
 
 template <int BN, int CG>
 int dispatch_majors(bool a_mn, bool b_mn, int ek, const CUtensorMap& ta, const CUtensorMap& tb,
-                    const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, int M,
+                    const CUtensorMap& tc, const CUtensorMap& tu, const CUtensorMap& tx, const TcGroup& g2, int M,
                     int N, int K, const TcEpi& ep, cudaStream_t st) {
   if constexpr ((BN / CG) % 64 != 0) {  // MN-major B needs 64-wide chunks per CTA
     if (b_mn) {
       set_error("gemm: tile %d x cta_group %d needs a K-major B", BN, CG);
       return PC_ERR_ARG;
     }
-    return dispatch_ek<BN, CG, false>(a_mn, ek, ta, tb, tc, tu, tx, M, N, K, ep, st);
+    return dispatch_ek<BN, CG, false>(a_mn, ek, ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
   } else {
-    if (b_mn) return dispatch_ek<BN, CG, true>(a_mn, ek, ta, tb, tc, tu, tx, M, N, K, ep, st);
-    return dispatch_ek<BN, CG, false>(a_mn, ek, ta, tb, tc, tu, tx, M, N, K, ep, st);
+    if (b_mn) return dispatch_ek<BN, CG, true>(a_mn, ek, ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
+    return dispatch_ek<BN, CG, false>(a_mn, ek, ta, tb, tc, tu, tx, g2, M, N, K, ep, st);
   }
 }
 
@@ -1041,11 +1062,40 @@ static void choose_tiles(bool b_kmajor, int64_t M, int64_t N, int64_t K, bool ca
   *ks_out = ksplit;
 }
 
+// Second problem of a grouped weight-gradient pair (pc_gemm_wgrad_pair).
+struct PairArgs {
+  int64_t M2;
+  const void* A2;
+  int64_t lda2;
+  const void* B2;
+  int64_t ldb2;
+  void* C2;
+  int64_t ldc2;
+};
+
+static int gemm_tc_impl(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                        const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                        int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
+                        int64_t ldaux_out, cudaStream_t st, float2* stats, int64_t ld_stats,
+                        const PairArgs* pair);
+
 int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
                  const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                  int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
                  int64_t ldaux_out, cudaStream_t st, float2* stats, int64_t ld_stats) {
+  return gemm_tc_impl(out_f32, transA, transB, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, aux, ldaux,
+                      aux_out, ldaux_out, st, stats, ld_stats, nullptr);
+}
+
+static int gemm_tc_impl(int out_f32, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                        const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                        int epi, const void* bias, const void* aux, int64_t ldaux, void* aux_out,
+                        int64_t ldaux_out, cudaStream_t st, float2* stats, int64_t ld_stats,
+                        const PairArgs* pair) {
   PP_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem");
+  // a grouped pair runs as one problem of M + M2 rows; tiles past M read / write
+  // the second problem (the first's rows must fill whole tiles)
+  const int64_t Mt = pair ? M + pair->M2 : M;
   PP_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
   PP_CHECK_ARG(!((epi & PC_EPI_ACCUM) && (epi & PC_EPI_SPLITK_ZERO_C)),
                "gemm: accumulate and split-K onto zeros are exclusive");
@@ -1068,14 +1118,18 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
   // unordered split-K onto a zero C is only order-independent for 2 halves
   // (0 + a + b == 0 + b + a): more splits need the ordered protocol
   const double c_bytes = (epi & PC_EPI_ACCUM) ? 8.0 : out_f32 ? 4.0 : 2.0;
-  choose_tiles(transB != 0, M, N, K, can_split, &bn, &cg, &ksplit, ordered ? g_max_split : std::min(g_max_split, 2),
+  choose_tiles(transB != 0, Mt, N, K, can_split, &bn, &cg, &ksplit, ordered ? g_max_split : std::min(g_max_split, 2),
                ordered, c_bytes);
+  if (pair) {
+    PP_CHECK_ARG(M % (TC_BM * cg) == 0 && tma_c && out_f32 && transA && !transB && !(epi & ~(PC_EPI_ACCUM | PC_EPI_SPLITK_ORDERED | PC_EPI_SPLITK_ZERO_C)),
+                 "gemm pair: first problem must fill whole tiles, fp32 TMA C, weight-gradient majors");
+  }
   // raster: an A operand far larger than L2 (the LM-head gradients: 824 MB of
   // logit gradients) is streamed once when the tiles sharing its rows run
   // together; otherwise walk M (B is the large, reused operand)
-  const bool n_fast = static_cast<double>(M) * K * 2 > 64e6 && M * 2 > N;
+  const bool n_fast = static_cast<double>(Mt) * K * 2 > 64e6 && Mt * 2 > N;
   if (ordered && ksplit > 1) {
-    const int64_t tiles = ((M + TC_BM * cg - 1) / (TC_BM * cg)) * ((N + bn - 1) / bn);
+    const int64_t tiles = ((Mt + TC_BM * cg - 1) / (TC_BM * cg)) * ((N + bn - 1) / bn);
     PP_CHECK_ARG(ldaux >= tiles * cg * TC_EPI_WARPS, "gemm: ordered split-K flag array too short");
   }
   // op(A) is [M,K]: transA=0 -> stored [M,K] (K-major); transA=1 -> stored [K,M] (MN-major).
@@ -1139,22 +1193,42 @@ int gemm_bf16_tc(int out_f32, int transA, int transB, int64_t M, int64_t N, int6
     PP_CHECK_ARG(ld_stats >= ((N + bn - 1) / bn) * TC_EPI_G, "gemm: statistics row too short");
   }
   TcEpi ep{ksplit, tma_c ? 1 : 0, tma_u ? 1 : 0, tma_a ? 1 : 0, cw64 ? 1 : 0, C, ldc, static_cast<const float*>(bias), aux, ldaux,
-           aux_out, ldaux_out, static_cast<int>(M), static_cast<int>(N), epi | (g_ablate << 16), out_f32,
-           n_fast ? 1 : 0, stats, static_cast<int>(ld_stats)};
-  const int iM = static_cast<int>(M), iN = static_cast<int>(N), iK = static_cast<int>(K);
+           aux_out, ldaux_out, static_cast<int>(Mt), static_cast<int>(N), epi | (g_ablate << 16), out_f32,
+           n_fast ? 1 : 0, stats, static_cast<int>(ld_stats), pair ? static_cast<int>(M) : 0};
+  TcGroup g2;
+  memset(&g2, 0, sizeof(g2));
+  if (pair) {
+    rc = make_tmap(&g2.a, pair->A2, pair->M2, K, pair->lda2, TC_BK);  // MN-major A2 [K, M2]
+    if (rc) return rc;
+    rc = make_tmap(&g2.b, pair->B2, N, K, pair->ldb2, TC_BK);         // MN-major B2 [K, N]
+    if (rc) return rc;
+    rc = make_tmap_c(&g2.c, pair->C2, N, pair->M2, pair->ldc2, true, cw64);
+    if (rc) return rc;
+  }
+  const int iM = static_cast<int>(Mt), iN = static_cast<int>(N), iK = static_cast<int>(K);
   switch (bn * 4 + cg) {
-    case 256 * 4 + 2: return dispatch_majors<256, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 192 * 4 + 2: return dispatch_majors<192, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 128 * 4 + 2: return dispatch_majors<128, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 256 * 4 + 1: return dispatch_majors<256, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 192 * 4 + 1: return dispatch_majors<192, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 128 * 4 + 1: return dispatch_majors<128, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
-    case 64 * 4 + 1: return dispatch_majors<64, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, iM, iN, iK, ep, st);
+    case 256 * 4 + 2: return dispatch_majors<256, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, g2, iM, iN, iK, ep, st);
+    case 192 * 4 + 2: return dispatch_majors<192, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, g2, iM, iN, iK, ep, st);
+    case 128 * 4 + 2: return dispatch_majors<128, 2>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, g2, iM, iN, iK, ep, st);
+    case 256 * 4 + 1: return dispatch_majors<256, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, g2, iM, iN, iK, ep, st);
+    case 192 * 4 + 1: return dispatch_majors<192, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, g2, iM, iN, iK, ep, st);
+    case 128 * 4 + 1: return dispatch_majors<128, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, g2, iM, iN, iK, ep, st);
+    case 64 * 4 + 1: return dispatch_majors<64, 1>(a_mn, b_mn, ek, ta, tb, tc, tu, tx, g2, iM, iN, iK, ep, st);
     default: set_error("gemm: bad tile %d x cta_group %d", bn, cg); return PC_ERR_ARG;
   }
 }
 
 }  // namespace pp200
+
+extern "C" int pc_gemm_wgrad_pair(int64_t M1, int64_t M2, int64_t N, int64_t K, const void* A1,
+                                  int64_t lda1, const void* B1, int64_t ldb1, float* C1, int64_t ldc1,
+                                  const void* A2, int64_t lda2, const void* B2, int64_t ldb2, float* C2,
+                                  int64_t ldc2, int epilogue, void* aux, int64_t ldaux, void* stream) {
+  PP_CHECK_ARG(M1 > 0 && M2 > 0 && N > 0 && K > 0, "gemm pair: empty problem");
+  const pp200::PairArgs pa{M2, A2, lda2, B2, ldb2, C2, ldc2};
+  return pp200::gemm_tc_impl(1, 1, 0, M1, N, K, A1, lda1, B1, ldb1, C1, ldc1, epilogue, nullptr, aux,
+                             ldaux, nullptr, 0, static_cast<cudaStream_t>(stream), nullptr, 0, &pa);
+}
 
 extern "C" int pc_gemm_tile_choice(int transB, int64_t M, int64_t N, int64_t K, int split_ok,
                                    int* bn, int* cta_pair, int* ksplit) {

@@ -97,6 +97,8 @@ _XENT_FUSED = os.environ.get("PP200_XENT_FUSED", "1") != "0"
 # A/B switch: 0 = bf16 column sums through the two-stage workspace kernel instead of
 # the one-pass cluster reduction (pc_colsum_set_cluster)
 _COLSUM_CLUSTER = os.environ.get("PP200_COLSUM_CLUSTER", "1") != "0"
+# A/B switch: 0 = the attention-output and qkv weight gradients as two GEMMs
+_WGRAD_PAIR = os.environ.get("PP200_WGRAD_PAIR", "1") != "0"
 
 
 class PeerBuf:
@@ -722,6 +724,24 @@ class DeviceOps:
                    _lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED, aux=self._split_flags,
                    ldaux=self._split_flags.numel(), st=st)
 
+    def _wgrad_pair_into(self, M1, M2, N_, K_, A1, lda1, B1, ldb1, C1, A2, lda2, B2, ldb2, C2,
+                         acc: bool, side: torch.cuda.Stream):
+        """Two weight gradients with the same N and K in one launch
+        (pc_gemm_wgrad_pair): the same per-gradient sums as two _wgrad_into
+        calls, the second problem's tiles filling the first's partial wave."""
+        st = side.cuda_stream
+        if acc:
+            if self._split_flags is None:
+                with torch.cuda.stream(side):
+                    self._split_flags = torch.zeros(1 << 16, dtype=torch.int32, device=self.device)
+            epi, aux, ldaux = (_lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED, self._split_flags.data_ptr(),
+                               self._split_flags.numel())
+        else:
+            epi, aux, ldaux = _lib.EPI_SPLITK_ZERO_C, None, 0
+        call("pc_gemm_wgrad_pair", M1, M2, N_, K_, A1.data_ptr(), lda1, B1.data_ptr(), ldb1,
+             C1.data_ptr(), N_, A2.data_ptr(), lda2, B2.data_ptr(), ldb2, C2.data_ptr(), N_, epi, aux,
+             ldaux, st)
+
     def _block_bwd(self, op, env, acc=None):
         cfg = self.gpt
         final = bool(op.attr("final_ln"))
@@ -794,14 +814,18 @@ class DeviceOps:
         # Weight gradients and their bias sums run on the side stream (they do
         # not feed the dX chain); each fork orders them after their inputs.
 
-        def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname):
+        def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname, weight=True):
             self._fork()
-            if "wgrad" not in _ABLATE:
+            if weight and "wgrad" not in _ABLATE:
                 self._wgrad_into(M_, N_, T, A, lda, Bm, ldb, gs(wname), fused, self._side())
             if _ABLATE_BIAS:   # profiling only: bias gradients left unset
                 return
             call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, M_, A.data_ptr(), lda,
                  gs(bname).data_ptr(), int(fused), *self.red_ws(T, M_, side=True), sst)
+
+        # the attention-output and qkv weight gradients share N = d and K = T: one
+        # grouped launch once both inputs exist (dW_o alone left most SMs idle)
+        pair = self.mode.act == torch.bfloat16 and (3 * d) % 256 == 0 and _WGRAD_PAIR
 
         # MLP
         wgrad(d, f, dout, d, sv["gu"], f, "w_fc2", "b_fc2")
@@ -816,7 +840,7 @@ class DeviceOps:
         dh1 = self.empty((T, d), act)
         ln_bwd(da2, sv["h1"], "ln2_g", "ln2_b", sv["mean2"], sv["rstd2"], dout, dh1)
         # attention
-        wgrad(d, d, dh1, d, sv["o"], d, "w_o", "b_o")
+        wgrad(d, d, dh1, d, sv["o"], d, "w_o", "b_o", weight=not pair)
         do = self.empty((T, d), act)
         tb, B, ldb = wB("w_o")
         self._gemm(act, 0, tb, T, d, d, dh1, d, B, ldb, do, d)
@@ -826,7 +850,10 @@ class DeviceOps:
             call("pc_attention_bwd", self.mode.pc_act, cfg.microbatch_size, H, cfg.seq_len,
                  cfg.head_dim, sv["qkv"].data_ptr(), 3 * d, sv["o"].data_ptr(), do.data_ptr(), d,
                  sv["lse"].data_ptr(), delta.data_ptr(), dqkv.data_ptr(), 3 * d, self.st)
-        wgrad(3 * d, d, dqkv, 3 * d, sv["a"], d, "w_qkv", "b_qkv")
+        wgrad(3 * d, d, dqkv, 3 * d, sv["a"], d, "w_qkv", "b_qkv", weight=not pair)
+        if pair and "wgrad" not in _ABLATE:   # after the fork above: dqkv and dh1 exist
+            self._wgrad_pair_into(3 * d, d, d, T, dqkv, 3 * d, sv["a"], d, gs("w_qkv"), dh1, d,
+                                  sv["o"], d, gs("w_o"), fused, self._side())
         da = self.empty((T, d), act)
         tb, B, ldb = wB("w_qkv")
         self._gemm(act, 0, tb, T, d, 3 * d, dqkv, 3 * d, B, ldb, da, d)

@@ -263,3 +263,41 @@ def _ordered_splitk_case(M, N, K):
     assert torch.equal(outs[0], want)
     assert int(flags.abs().sum()) == 0
     assert rel(outs[0] - acc0, ref) < 1e-4
+
+
+@pytest.mark.parametrize("M1,M2,N,K", [(2304, 768, 768, 8192), (256, 200, 192, 1024),
+                                       (1024, 4096, 1024, 8192)])
+@pytest.mark.parametrize("ordered", [False, True])
+def test_wgrad_pair_matches_two_products(M1, M2, N, K, ordered):
+    """pc_gemm_wgrad_pair: C1 (+)= A1^T B1 and C2 (+)= A2^T B2 in one launch (the
+    attention-output + qkv weight gradients of a block), both within fp32
+    rounding of the float64 products, run-to-run identical, flags left zeroed."""
+    g = torch.Generator(device="cuda").manual_seed(M1 + M2 + N)
+    A1 = torch.randn(K, M1, device="cuda", generator=g).to(torch.bfloat16)
+    B1 = torch.randn(K, N, device="cuda", generator=g).to(torch.bfloat16)
+    A2 = torch.randn(K, M2, device="cuda", generator=g).to(torch.bfloat16)
+    B2 = torch.randn(K, N, device="cuda", generator=g).to(torch.bfloat16)
+    acc1 = torch.randn(M1, N, device="cuda", generator=g)
+    acc2 = torch.randn(M2, N, device="cuda", generator=g)
+    flags = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for _ in range(2):
+        if ordered:
+            C1, C2 = acc1.clone(), acc2.clone()
+            epi, aux = _lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED, flags.data_ptr()
+        else:
+            C1, C2 = torch.zeros_like(acc1), torch.zeros_like(acc2)
+            epi, aux = _lib.EPI_SPLITK_ZERO_C, None
+        _lib.call("pc_gemm_wgrad_pair", M1, M2, N, K, A1.data_ptr(), M1, B1.data_ptr(), N,
+                  C1.data_ptr(), N, A2.data_ptr(), M2, B2.data_ptr(), N, C2.data_ptr(), N, epi, aux,
+                  flags.numel(), st)
+        outs.append((C1, C2))
+    torch.cuda.synchronize()
+    ref1 = A1.double().t() @ B1.double()
+    ref2 = A2.double().t() @ B2.double()
+    base1, base2 = (acc1.double(), acc2.double()) if ordered else (0.0, 0.0)
+    assert rel(outs[0][0].double() - base1, ref1) < 1e-4
+    assert rel(outs[0][1].double() - base2, ref2) < 1e-4
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert int(flags.abs().sum()) == 0
