@@ -99,6 +99,9 @@ _XENT_FUSED = os.environ.get("PP200_XENT_FUSED", "1") != "0"
 _COLSUM_CLUSTER = os.environ.get("PP200_COLSUM_CLUSTER", "1") != "0"
 # A/B switch: 0 = the attention-output and qkv weight gradients as two GEMMs
 _WGRAD_PAIR = os.environ.get("PP200_WGRAD_PAIR", "1") != "0"
+# A/B switch: 0 = the compute stream waits for each GPT block's side-stream work
+# (weight / bias / LayerNorm-parameter gradients) before the next block
+_DEFER_JOIN = os.environ.get("PP200_DEFER_JOIN", "1") != "0"
 
 
 class PeerBuf:
@@ -173,6 +176,7 @@ class DeviceOps:
         self.device = device
         self.stream = stream
         self.gpt = gpt
+        self._side_pending = False   # side-stream work not yet joined (run_ops joins it)
         if not _COLSUM_CLUSTER:
             call("pc_colsum_set_cluster", 0)
         self._plans: dict[int, _StagePlan] = {}
@@ -285,6 +289,11 @@ class DeviceOps:
             if k in plan.fused_into_prev:
                 continue
             self._eval(op, env, k, ops, plan)
+        if self._side_pending:
+            # the blocks' side-stream gradient work joins once, at the end of the
+            # stage program (every reader of those gradients comes after it)
+            self._join()
+            self._side_pending = False
         return env
 
     def _plan(self, ops: list[OpNode]) -> _StagePlan:
@@ -566,6 +575,9 @@ class DeviceOps:
         return out
 
     def _embed_bwd(self, op, env, acc=None):
+        if self._side_pending:   # the head weight gradient adds into the same tied sum
+            self._join()
+            self._side_pending = False
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
@@ -859,7 +871,17 @@ class DeviceOps:
         self._gemm(act, 0, tb, T, d, 3 * d, dqkv, 3 * d, B, ldb, da, d)
         dh = self._placed_elem(op, 0, (T, d), act)   # into the previous stage's slot when sent
         ln_bwd(da, h, "ln1_g", "ln1_b", sv["mean1"], sv["rstd1"], dh1, dh)
-        self._join()
+        if _DEFER_JOIN:
+            # the next block's data-gradient chain does not wait for this block's
+            # side-stream work; the allocator keeps every tensor that work reads
+            # until it has run (record_stream), and run_ops joins at the end
+            side = self._side()
+            for t in (dz, dout, du, da2, dh1, dqkv, da, h, *sv.values()):
+                if isinstance(t, torch.Tensor):
+                    t.record_stream(side)
+            self._side_pending = True
+        else:
+            self._join()
         return (dh, dW)
 
     def _head_fwd(self, op, env):
@@ -916,12 +938,22 @@ class DeviceOps:
         else:
             wte = self._slice(w0.compute(), self._elay, "wte")
             self._gemm(self.mode.act, 0, 0, T, d, V, dlogits, V, wte, d, dh, d)
+        # the weight gradient runs on the side stream beside the blocks' backward
+        # (joined at the end of the stage program, or before the embedding
+        # backward adds into the same tied running sum)
+        side = self._side() if _DEFER_JOIN else None
+        sst = side.cuda_stream if side is not None else self.st
+        if side is not None:
+            self._fork()
+            dlogits.record_stream(side)
+            h.record_stream(side)
+            self._side_pending = True
         if acc is not None:
             # onto the running sum: the wte rows through the GEMM's TMA
             # reduce-add store (unsplit: one fp32 add per element); the head's
             # wpe part is zero, nothing to add
             self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
-                       self._slice(acc, self._elay, "wte"), d, _lib.EPI_ACCUM)
+                       self._slice(acc, self._elay, "wte"), d, _lib.EPI_ACCUM, st=sst)
             return (dh, acc)
         # wte gradient from the GEMM; wpe's part of the tied partial is zero.
         # Zero-fill only what the GEMM does not overwrite: all of wte when it
@@ -932,11 +964,12 @@ class DeviceOps:
              ctypes.byref(ks))
         wte = self._slice(dw, self._elay, "wte")
         if ks.value > 1:
-            call("pc_fill", _lib.PC_F32, dw.numel(), 0.0, dw.data_ptr(), self.st)
+            call("pc_fill", _lib.PC_F32, dw.numel(), 0.0, dw.data_ptr(), sst)
         else:  # everything after wte: wpe and the alignment padding
             tail = dw[self._elay["wte"][0] + wte.numel():]
-            call("pc_fill", _lib.PC_F32, tail.numel(), 0.0, tail.data_ptr(), self.st)
-        self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d, wte, d, _lib.EPI_SPLITK_ZERO_C)
+            call("pc_fill", _lib.PC_F32, tail.numel(), 0.0, tail.data_ptr(), sst)
+        self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d, wte, d, _lib.EPI_SPLITK_ZERO_C,
+                   st=sst)
         return (dh, dw)
 
 
@@ -967,6 +1000,9 @@ class DeviceOps:
     def _llama_embed_bwd(self, op, env, acc=None):
         """Token-row sums of the embedding gradient, onto the running sum when
         fused (no [vocab, d] zero fill per microbatch), else onto zeros."""
+        if self._side_pending:   # pending side-stream work may still write gradients
+            self._join()
+            self._side_pending = False
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
@@ -1144,7 +1180,14 @@ class DeviceOps:
         self._gemm(act, 0, tb, T, d, qw, dqkv, qw, B, ldb, da, d)
         # the stage input gradient: into the previous stage's slot when sent
         dh = rms_bwd(da, h, "rms1_g", sv["rstd1"], dh1, self._placed_elem(op, 0, (T, d), act))
-        self._join()
+        if _DEFER_JOIN:   # as in _block_bwd: run_ops joins the side stream at the end
+            side = self._side()
+            for t in (dz, dout, dgu, da2, dh1, dqkv, da, h, *sv.values()):
+                if isinstance(t, torch.Tensor):
+                    t.record_stream(side)
+            self._side_pending = True
+        else:
+            self._join()
         return (dh, dW)
 
     def _llama_head_fwd(self, op, env):
@@ -1182,7 +1225,13 @@ class DeviceOps:
         self._fork()
         self._wgrad_into(V, d, T, dlogits, V, h, d, self._slice(dw, self._hlay, "w_head"), fused,
                          self._side())
-        self._join()
+        if _DEFER_JOIN:   # the blocks' backward does not wait for the head weight gradient
+            side = self._side()
+            dlogits.record_stream(side)
+            h.record_stream(side)
+            self._side_pending = True
+        else:
+            self._join()
         return (dh, dw)
 
 
