@@ -177,6 +177,10 @@ class DeviceOps:
         self.stream = stream
         self.gpt = gpt
         self._side_pending = False   # side-stream work not yet joined (run_ops joins it)
+        # tensors that pending side-stream work reads, kept alive until the join
+        # (not record_stream: under CUDA-graph capture that defers every such free
+        # to the end of the capture, which ran C4 / C3-M64 out of memory)
+        self._side_keep: list = []
         if not _COLSUM_CLUSTER:
             call("pc_colsum_set_cluster", 0)
         self._plans: dict[int, _StagePlan] = {}
@@ -291,9 +295,11 @@ class DeviceOps:
             self._eval(op, env, k, ops, plan)
         if self._side_pending:
             # the blocks' side-stream gradient work joins once, at the end of the
-            # stage program (every reader of those gradients comes after it)
+            # stage program (every reader of those gradients comes after it);
+            # only then may the tensors it reads go back to the allocator
             self._join()
             self._side_pending = False
+            self._side_keep.clear()
         return env
 
     def _plan(self, ops: list[OpNode]) -> _StagePlan:
@@ -578,6 +584,7 @@ class DeviceOps:
         if self._side_pending:   # the head weight gradient adds into the same tied sum
             self._join()
             self._side_pending = False
+            self._side_keep.clear()
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
@@ -874,11 +881,8 @@ class DeviceOps:
         if _DEFER_JOIN:
             # the next block's data-gradient chain does not wait for this block's
             # side-stream work; the allocator keeps every tensor that work reads
-            # until it has run (record_stream), and run_ops joins at the end
-            side = self._side()
-            for t in (dz, dout, du, da2, dh1, dqkv, da, h, *sv.values()):
-                if isinstance(t, torch.Tensor):
-                    t.record_stream(side)
+            # until it has run (kept in _side_keep), and run_ops joins at the end
+            self._side_keep.extend((dz, dout, du, da2, dh1, dqkv, da, h, sv))
             self._side_pending = True
         else:
             self._join()
@@ -945,8 +949,7 @@ class DeviceOps:
         sst = side.cuda_stream if side is not None else self.st
         if side is not None:
             self._fork()
-            dlogits.record_stream(side)
-            h.record_stream(side)
+            self._side_keep.extend((dlogits, h))
             self._side_pending = True
         if acc is not None:
             # onto the running sum: the wte rows through the GEMM's TMA
@@ -1003,6 +1006,7 @@ class DeviceOps:
         if self._side_pending:   # pending side-stream work may still write gradients
             self._join()
             self._side_pending = False
+            self._side_keep.clear()
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
@@ -1181,10 +1185,7 @@ class DeviceOps:
         # the stage input gradient: into the previous stage's slot when sent
         dh = rms_bwd(da, h, "rms1_g", sv["rstd1"], dh1, self._placed_elem(op, 0, (T, d), act))
         if _DEFER_JOIN:   # as in _block_bwd: run_ops joins the side stream at the end
-            side = self._side()
-            for t in (dz, dout, dgu, da2, dh1, dqkv, da, h, *sv.values()):
-                if isinstance(t, torch.Tensor):
-                    t.record_stream(side)
+            self._side_keep.extend((dz, dout, dgu, da2, dh1, dqkv, da, h, sv))
             self._side_pending = True
         else:
             self._join()
@@ -1226,9 +1227,7 @@ class DeviceOps:
         self._wgrad_into(V, d, T, dlogits, V, h, d, self._slice(dw, self._hlay, "w_head"), fused,
                          self._side())
         if _DEFER_JOIN:   # the blocks' backward does not wait for the head weight gradient
-            side = self._side()
-            dlogits.record_stream(side)
-            h.record_stream(side)
+            self._side_keep.extend((dlogits, h))
             self._side_pending = True
         else:
             self._join()
