@@ -1496,8 +1496,6 @@ int fwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, void* o,
       case 0: return fwd64_launch<0>(B, S, hs, tm, o, ld_o, lse, st);
       case 4: return fwd64_launch<4>(B, S, hs, tm, o, ld_o, lse, st);
       case 8: return fwd64_launch<8>(B, S, hs, tm, o, ld_o, lse, st);
-      case 10: return fwd64_launch<10>(B, S, hs, tm, o, ld_o, lse, st);
-      case 12: return fwd64_launch<12>(B, S, hs, tm, o, ld_o, lse, st);
       case 101: return fwd64_launch<0, 1>(B, S, hs, tm, o, ld_o, lse, st);
       case 102: return fwd64_launch<0, 2>(B, S, hs, tm, o, ld_o, lse, st);
       default: return fwd64_launch<6>(B, S, hs, tm, o, ld_o, lse, st);
@@ -1556,7 +1554,7 @@ int bwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, const vo
 int attention_tc5_tune(int key, int value) {
   if (key == 0 && (value == 1 || value == 2)) {
     g_fwd64_design = value;
-  } else if (key == 1 && (value == 0 || value == 4 || value == 6 || value == 8 || value == 10 || value == 12 || value == 101 || value == 102)) {
+  } else if (key == 1 && (value == 0 || value == 4 || value == 6 || value == 8 || value == 101 || value == 102)) {
     g_fwd64_emu = value;
   } else {
     set_error("pc_attention_tune: unknown key %d or value %d", key, value);
