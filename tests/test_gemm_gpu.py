@@ -301,3 +301,43 @@ def test_wgrad_pair_matches_two_products(M1, M2, N, K, ordered):
     assert rel(outs[0][1].double() - base2, ref2) < 1e-4
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     assert int(flags.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("bn,pair", [(256, 2), (256, 1)])
+def test_wgrad_pair_forced_split(bn, pair):
+    """The grouped pair under a forced tile that makes the chooser split K: the
+    ordered split-K flags are indexed by the pair's global tile, so both
+    problems' chains stay sequenced; equal to the fp64 products, deterministic."""
+    import ctypes
+    M1, M2, N, K = 2304, 768, 768, 8192
+    _lib.call("pc_gemm_set_tile_n", bn)
+    _lib.call("pc_gemm_set_cta_pair", pair)
+    try:
+        b_, c_, ks = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.call("pc_gemm_tile_choice", 0, M1 + M2, N, K, 2, ctypes.byref(b_), ctypes.byref(c_),
+                  ctypes.byref(ks))
+        assert ks.value > 1
+        g = torch.Generator(device="cuda").manual_seed(11)
+        A1 = torch.randn(K, M1, device="cuda", generator=g).to(torch.bfloat16)
+        B1 = torch.randn(K, N, device="cuda", generator=g).to(torch.bfloat16)
+        A2 = torch.randn(K, M2, device="cuda", generator=g).to(torch.bfloat16)
+        B2 = torch.randn(K, N, device="cuda", generator=g).to(torch.bfloat16)
+        acc1 = torch.randn(M1, N, device="cuda", generator=g)
+        acc2 = torch.randn(M2, N, device="cuda", generator=g)
+        flags = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        outs = []
+        for _ in range(2):
+            C1, C2 = acc1.clone(), acc2.clone()
+            _lib.call("pc_gemm_wgrad_pair", M1, M2, N, K, A1.data_ptr(), M1, B1.data_ptr(), N,
+                      C1.data_ptr(), N, A2.data_ptr(), M2, B2.data_ptr(), N, C2.data_ptr(), N,
+                      _lib.EPI_ACCUM | _lib.EPI_SPLITK_ORDERED, flags.data_ptr(), flags.numel(), st)
+            outs.append((C1, C2))
+        torch.cuda.synchronize()
+    finally:
+        _lib.call("pc_gemm_set_tile_n", 0)
+        _lib.call("pc_gemm_set_cta_pair", 0)
+    assert rel(outs[0][0].double() - acc1.double(), A1.double().t() @ B1.double()) < 1e-4
+    assert rel(outs[0][1].double() - acc2.double(), A2.double().t() @ B2.double()) < 1e-4
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert int(flags.abs().sum()) == 0
