@@ -1,7 +1,11 @@
 // clock64 / %globaltimer timeline of the persistent head_dim-64 forward
 // (fa_fwd64_tc5): compiled with the kernel source and PP200_FA_TRACE, linked
 // against libpp200.so for the shared helpers.
-// usage: tools/fa_trace [B H S emu]     (build: see tools/README or DESIGN §7)
+// usage: tools/fa_trace [B H S emu]
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//          -I paper_2412_14374_b200/csrc --expt-relaxed-constexpr -o tools/fa_trace \
+//          tools/fa_trace.cu -L paper_2412_14374_b200 -lpp200 -lcuda \
+//          -Xlinker -rpath='$ORIGIN/../paper_2412_14374_b200'
 #define PP200_FA_TRACE 1
 #include "../paper_2412_14374_b200/csrc/attention_tc5.cu"
 #include <algorithm>
