@@ -428,7 +428,10 @@ __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* src, 
       : "memory");
 }
 
-template <int EMU, int ABL = 0>  // ABL (tools/attn_ab.py): 1 no softmax math, 2 no MMAs
+// SPLIT: the S MMAs (warp 1) and the PV MMAs (warp 3) come from two issuing
+// warps, so a PV is never queued behind an S issue that waits for K/V (the
+// MMA-only pipeline, no softmax math: 24.1 -> 17.5 us at C2).
+template <int EMU, int ABL = 0, int SPLIT = 0>  // ABL (tools/attn_ab.py): 1 no softmax math, 2 no MMAs
 __global__ void __launch_bounds__(256, 2)
     fa_fwd64_tc5(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap to,
                  float* __restrict__ lse, int B, Heads hs, int S, float sl2) {
@@ -570,7 +573,18 @@ __global__ void __launch_bounds__(256, 2)
       }
       return true;
     };
-    if (tile_of(0) < items) {
+    if (SPLIT) {
+      uint32_t g = 0;
+      for (int k = 0;; ++k) {
+        const int w = tile_of(k);
+        if (w >= items) break;
+        int b, h, q0, nkb;
+        decode(w, b, h, q0, nkb);
+        for (int j = 0; j < nkb; ++j, ++g) issue_s(g, k, j);
+        if (elect_one()) tc_commit(&q_empty[k & 1]);  // Q is read by the S MMAs only
+        __syncwarp();
+      }
+    } else if (tile_of(0) < items) {
       int b0, h0, q00;
       kq[0] = 0;
       jq[0] = 0;
@@ -608,6 +622,34 @@ __global__ void __launch_bounds__(256, 2)
         kq[1] = kq[2]; jq[1] = jq[2]; nq[1] = nq[2];
         have1 = have2;
         if (have2) have2 = next_pair(kq[1], jq[1], nq[1], kq[2], jq[2], nq[2]);
+      }
+    }
+  } else if (SPLIT && warp == 3) {
+    constexpr uint32_t ID_O = umma_idesc_bf16(K::BM, 64, 0, 1);  // P K-major, V MN-major
+    uint32_t g = 0;
+    for (int k = 0;; ++k) {
+      const int w = tile_of(k);
+      if (w >= items) break;
+      int b, h, q0, nkb;
+      decode(w, b, h, q0, nkb);
+      for (int j = 0; j < nkb; ++j, ++g) {
+        const int st = g % K::STAGES;
+        mbar_wait(&p_full[g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + st * K::KV_BYTES);
+        const uint32_t tPg = tP + (g & 1) * 32;
+        if (elect_one()) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (ABL != 2)
+              tc_mma_f16_ts(tO, tPg + 8 * c, umma_sdesc_sw128(v_addr + c * 2048, K::KV_BYTES, 1024), ID_O,
+                            (j > 0 || c > 0) ? 1u : 0u);
+          tc_commit(&pv_done[g & 1]);
+          // K_g was read by S_g, which retired before the softmax loaded it
+          tc_commit(&kv_empty[st]);
+          if (j == nkb - 1) tc_commit(o_full);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -1442,7 +1484,7 @@ int make_tmap_rows64(CUtensorMap* m, const void* base, int64_t ld, int64_t rows)
   return PC_OK;
 }
 
-int g_fwd64_design = 2;  // pc_attention_tune key 0
+int g_fwd64_design = 3;  // pc_attention_tune key 0
 int g_fwd64_emu = 6;     // pc_attention_tune key 1
 
 // O as a 3-D tensor [B][S][ld_o] (rows clipped per sequence), box 64 x 32 x 1.
@@ -1466,7 +1508,7 @@ int make_tmap_o3(CUtensorMap* m, const void* base, int64_t ld, int S, int B) {
   return PC_OK;
 }
 
-template <int EMU, int ABL = 0>
+template <int EMU, int ABL = 0, int SPLIT = 0>
 int fwd64_launch(int B, int S, Heads hs, const CUtensorMap& tm, void* o, int64_t ld_o, float* lse,
                  cudaStream_t st) {
   CUtensorMap to;
@@ -1474,14 +1516,14 @@ int fwd64_launch(int B, int S, Heads hs, const CUtensorMap& tm, void* o, int64_t
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd64_tc5<EMU, ABL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd64_tc5<EMU, ABL, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      Fwd64::SMEM));
     attr = true;
   }
   const int items = B * hs.H * ((S + Fwd64::BM - 1) / Fwd64::BM);
   const int grid = items < 2 * num_sms() ? items : 2 * num_sms();
   const float sl2 = F_LOG2E / 8.f;  // 1 / sqrt(64)
-  fa_fwd64_tc5<EMU, ABL><<<grid, Fwd64::THREADS, Fwd64::SMEM, st>>>(tm, to, lse, B, hs, S, sl2);
+  fa_fwd64_tc5<EMU, ABL, SPLIT><<<grid, Fwd64::THREADS, Fwd64::SMEM, st>>>(tm, to, lse, B, hs, S, sl2);
   return check_launch("fa_fwd64_tc5");
 }
 
@@ -1491,6 +1533,16 @@ int fwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, void* o,
   CUtensorMap tm;
   int rc = make_tmap_rows64(&tm, qkv, ld_qkv, static_cast<int64_t>(B) * S);
   if (rc) return rc;
+  if (HD == 64 && g_fwd64_design == 3) {
+    switch (g_fwd64_emu) {
+      case 0: return fwd64_launch<0, 0, 1>(B, S, hs, tm, o, ld_o, lse, st);
+      case 4: return fwd64_launch<4, 0, 1>(B, S, hs, tm, o, ld_o, lse, st);
+      case 8: return fwd64_launch<8, 0, 1>(B, S, hs, tm, o, ld_o, lse, st);
+      case 101: return fwd64_launch<0, 1, 1>(B, S, hs, tm, o, ld_o, lse, st);
+      case 102: return fwd64_launch<0, 2, 1>(B, S, hs, tm, o, ld_o, lse, st);
+      default: return fwd64_launch<6, 0, 1>(B, S, hs, tm, o, ld_o, lse, st);
+    }
+  }
   if (HD == 64 && g_fwd64_design == 2) {
     switch (g_fwd64_emu) {
       case 0: return fwd64_launch<0>(B, S, hs, tm, o, ld_o, lse, st);
@@ -1552,7 +1604,7 @@ int bwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, const vo
 }  // namespace
 
 int attention_tc5_tune(int key, int value) {
-  if (key == 0 && (value == 1 || value == 2)) {
+  if (key == 0 && (value >= 1 && value <= 3)) {
     g_fwd64_design = value;
   } else if (key == 1 && (value == 0 || value == 4 || value == 6 || value == 8 || value == 101 || value == 102)) {
     g_fwd64_emu = value;

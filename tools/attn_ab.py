@@ -1,7 +1,7 @@
 """A/B the head_dim-64 attention kernel variants (pc_attention_tune) at the
 C2 / C3 shapes: time (CUDA events, 20 back-to-back launches) and agreement
 with the legacy design (max |o - o_ref|, max |lse - lse_ref|).
-usage: python tools/attn_ab.py [fwd|bwd|all]"""
+usage: python tools/attn_ab.py [fwd|bwd|all] [design,emu ...]  (default: all variants)"""
 import sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import json
@@ -41,7 +41,9 @@ def main():
             _lib.call("pc_attention_gqa_bwd", 2, B, H, H, S, hd, qkv.data_ptr(), ld, o.data_ptr(),
                       do.data_ptr(), H * hd, lse.data_ptr(), delta.data_ptr(), dqkv.data_ptr(), ld, st)
 
-        variants = [(1, 0), (2, 0), (2, 4), (2, 6), (2, 8)]
+        variants = [(1, 0), (2, 6), (3, 6), (2, 101), (3, 101)]
+        if len(sys.argv) > 2:
+            variants = [tuple(int(x) for x in a.split(",")) for a in sys.argv[2:]]
         ref = None
         for (design, emu) in variants:
             _lib.call("pc_attention_tune", 0, design)
@@ -69,7 +71,7 @@ def main():
                 bad = torch.isnan(o.float()).any(dim=1).nonzero().flatten().tolist()
                 row.update(nan_rows=bad[:8] + ["..."] + bad[-4:], n_bad=len(bad))
             print(json.dumps(row), flush=True)
-        _lib.call("pc_attention_tune", 0, 2)
+        _lib.call("pc_attention_tune", 0, 3)
         _lib.call("pc_attention_tune", 1, 6)
 
 
