@@ -114,7 +114,7 @@ struct Fwd {
   static constexpr int TMEM_COLS = 256;                // S0 | S1 | O (HD <= 128)
 };
 
-template <int HD>
+template <int HD, int SPLIT = 0>  // SPLIT: S and PV MMAs from two issuing warps (see fa_fwd64_tc5)
 __global__ void __launch_bounds__(256, 2)
     fa_fwd_tc5(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, int64_t ldo,
                float* __restrict__ lse, Heads hs, int S, float sl2) {
@@ -217,8 +217,12 @@ __global__ void __launch_bounds__(256, 2)
       }
       __syncwarp();
     };
-    issue_s(0);
-    for (int j = 0; j < nkb; ++j) {
+    if (SPLIT) {
+      for (int j = 0; j < nkb; ++j) issue_s(j);
+    } else {
+      issue_s(0);
+    }
+    for (int j = 0; j < nkb && !SPLIT; ++j) {
       // S[(j+1) % 2] was last read by softmax j-1, which finished before PV_{j-1}
       if (j + 1 < nkb) issue_s(j + 1);
       const int s = j % K::STAGES;
@@ -233,6 +237,26 @@ __global__ void __launch_bounds__(256, 2)
                         ID_O, (j > 0 || k > 0) ? 1u : 0u);
         tc_commit(&pv_done[j & 1]);
         tc_commit(&kv_empty[s]);
+      }
+      __syncwarp();
+    }
+    if (!SPLIT && elect_one()) tc_commit(o_done);
+    __syncwarp();
+  } else if (SPLIT && warp == 3) {
+    constexpr uint32_t ID_O = umma_idesc_bf16(K::BM, HD, 0, 1);  // P K-major, V MN-major
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j % K::STAGES;
+      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t v_addr = smem_u32(sV + s * K::KV_BYTES);
+      const uint32_t tP = tS + (j & 1) * 64;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < K::BN / 16; ++k)
+          tc_mma_f16_ts(tO, tP + 8 * k, umma_sdesc_sw128(v_addr + k * 2048, K::KV_PANEL, 1024),
+                        ID_O, (j > 0 || k > 0) ? 1u : 0u);
+        tc_commit(&pv_done[j & 1]);
+        tc_commit(&kv_empty[s]);  // K_j was read by S_j, retired before softmax j
       }
       __syncwarp();
     }
@@ -1486,6 +1510,7 @@ int make_tmap_rows64(CUtensorMap* m, const void* base, int64_t ld, int64_t rows)
 
 int g_fwd64_design = 3;  // pc_attention_tune key 0
 int g_fwd64_emu = 6;     // pc_attention_tune key 1
+int g_fwd_split = 1;     // pc_attention_tune key 2: fa_fwd_tc5 with two issuing warps
 
 // O as a 3-D tensor [B][S][ld_o] (rows clipped per sequence), box 64 x 32 x 1.
 int make_tmap_o3(CUtensorMap* m, const void* base, int64_t ld, int S, int B) {
@@ -1555,14 +1580,20 @@ int fwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, void* o,
   }
   static bool attr = false;
   if (!attr) {
-    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd_tc5<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd_tc5<HD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fwd<HD>::SMEM));
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_fwd_tc5<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      Fwd<HD>::SMEM));
     attr = true;
   }
   dim3 grid(B * hs.H, (S + Fwd<HD>::BM - 1) / Fwd<HD>::BM);
   const float sl2 = F_LOG2E / sqrtf(static_cast<float>(HD));
-  fa_fwd_tc5<HD><<<grid, Fwd<HD>::THREADS, Fwd<HD>::SMEM, st>>>(tm, static_cast<bf16*>(o), ld_o, lse,
-                                                               hs, S, sl2);
+  if (g_fwd_split)
+    fa_fwd_tc5<HD, 1><<<grid, Fwd<HD>::THREADS, Fwd<HD>::SMEM, st>>>(tm, static_cast<bf16*>(o), ld_o, lse,
+                                                                    hs, S, sl2);
+  else
+    fa_fwd_tc5<HD, 0><<<grid, Fwd<HD>::THREADS, Fwd<HD>::SMEM, st>>>(tm, static_cast<bf16*>(o), ld_o, lse,
+                                                                    hs, S, sl2);
   return check_launch("fa_fwd_tc5");
 }
 
@@ -1606,6 +1637,8 @@ int bwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, const vo
 int attention_tc5_tune(int key, int value) {
   if (key == 0 && (value >= 1 && value <= 3)) {
     g_fwd64_design = value;
+  } else if (key == 2 && (value == 0 || value == 1)) {
+    g_fwd_split = value;
   } else if (key == 1 && (value == 0 || value == 4 || value == 6 || value == 8 || value == 101 || value == 102)) {
     g_fwd64_emu = value;
   } else {

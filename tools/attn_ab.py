@@ -1,7 +1,8 @@
 """A/B the head_dim-64 attention kernel variants (pc_attention_tune) at the
 C2 / C3 shapes: time (CUDA events, 20 back-to-back launches) and agreement
 with the legacy design (max |o - o_ref|, max |lse - lse_ref|).
-usage: python tools/attn_ab.py [fwd|bwd|all] [design,emu ...]  (default: all variants)"""
+usage: python tools/attn_ab.py [fwd|bwd|all] [design,emu ...]  (default: all variants)
+       python tools/attn_ab.py fwd128   (head_dim 128 forward, C4 / C5: one vs two issuing warps)"""
 import sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import json
@@ -22,8 +23,40 @@ def bench(fn, iters=20):
     return s.elapsed_time(e) / iters
 
 
+def fwd128():
+    st = torch.cuda.current_stream().cuda_stream
+    torch.manual_seed(0)
+    for (name, B, H, Hkv, S) in [("C4", 4, 16, 16, 2048), ("C5", 1, 32, 8, 4096)]:
+        hd = 128
+        ld = (H + 2 * Hkv) * hd
+        qkv = (torch.randn(B * S, ld, device="cuda") * 0.5).bfloat16()
+        flops = 4.0 * B * H * S * S * hd / 2
+        ref = None
+        for split in (0, 1, 0, 1, 0, 1):
+            _lib.call("pc_attention_tune", 2, split)
+            o = torch.empty(B * S, H * hd, device="cuda", dtype=torch.bfloat16)
+            lse = torch.empty(B * H * S, device="cuda")
+
+            def run():
+                _lib.call("pc_attention_gqa_fwd", 2, B, H, Hkv, S, hd, qkv.data_ptr(), ld, o.data_ptr(), H * hd,
+                          lse.data_ptr(), st)
+            run()
+            torch.cuda.synchronize()
+            t = bench(run)
+            row = dict(shape=name, split=split, fwd_us=round(t * 1e3, 2), fwd_tflops=round(flops / t / 1e9, 1))
+            if ref is None:
+                ref = (o.clone(), lse.clone())
+            else:
+                row.update(o_maxdiff=float((o.float() - ref[0].float()).abs().max()),
+                           lse_maxdiff=float((lse - ref[1]).abs().max()))
+            print(json.dumps(row), flush=True)
+    _lib.call("pc_attention_tune", 2, 1)
+
+
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what == "fwd128":
+        return fwd128()
     st = torch.cuda.current_stream().cuda_stream
     torch.manual_seed(0)
     for (name, B, H, S) in [("C2", 8, 12, 1024), ("C3", 8, 16, 1024), ("C2-S1000", 8, 12, 1000)]:
