@@ -702,6 +702,7 @@ def main():
     # ---- one instrumented step (same warmed engine) for the bubble ----
     barrier()
     if use_graph:
+        cap.release()   # its graph memory pool: the instrumented capture needs its own
         cap_tl = eng.capture(None, tokens_dev, lr=1e-4, timeline=True)
         barrier()
         cap_tl.replay()

@@ -102,6 +102,10 @@ _WGRAD_PAIR = os.environ.get("PP200_WGRAD_PAIR", "1") != "0"
 # A/B switch: 0 = the compute stream waits for each GPT block's side-stream work
 # (weight / bias / LayerNorm-parameter gradients) before the next block
 _DEFER_JOIN = os.environ.get("PP200_DEFER_JOIN", "1") != "0"
+# deferred side-stream pieces (one per block backward / head weight gradient) in
+# flight before the compute stream waits for the oldest: bounds the tensors kept
+# alive for them (a one-stage C5 program would otherwise keep every block's)
+_DEFER_DEPTH = 3
 
 
 class PeerBuf:
@@ -177,10 +181,11 @@ class DeviceOps:
         self.stream = stream
         self.gpt = gpt
         self._side_pending = False   # side-stream work not yet joined (run_ops joins it)
-        # tensors that pending side-stream work reads, kept alive until the join
+        # (event, tensors) per deferred piece of side-stream work: the tensors it
+        # reads stay alive until the compute stream has waited for its event
         # (not record_stream: under CUDA-graph capture that defers every such free
         # to the end of the capture, which ran C4 / C3-M64 out of memory)
-        self._side_keep: list = []
+        self._side_ring: list = []
         if not _COLSUM_CLUSTER:
             call("pc_colsum_set_cluster", 0)
         self._plans: dict[int, _StagePlan] = {}
@@ -293,14 +298,28 @@ class DeviceOps:
             if k in plan.fused_into_prev:
                 continue
             self._eval(op, env, k, ops, plan)
+        # the blocks' side-stream gradient work joins at the end of the stage
+        # program (every reader of those gradients comes after it)
+        self._join_side()
+        return env
+
+    def _defer_side(self, tensors):
+        """Side-stream work just enqueued reads ``tensors``; the compute stream
+        goes on without waiting for it.  Once more than _DEFER_DEPTH pieces are
+        in flight the compute stream waits for the oldest, whose tensors may
+        then go back to the allocator."""
+        ev = torch.cuda.Event()
+        ev.record(self._side())
+        self._side_ring.append((ev, tensors))
+        self._side_pending = True
+        while len(self._side_ring) > _DEFER_DEPTH:
+            self.stream.wait_event(self._side_ring.pop(0)[0])
+
+    def _join_side(self):
         if self._side_pending:
-            # the blocks' side-stream gradient work joins once, at the end of the
-            # stage program (every reader of those gradients comes after it);
-            # only then may the tensors it reads go back to the allocator
             self._join()
             self._side_pending = False
-            self._side_keep.clear()
-        return env
+            self._side_ring.clear()
 
     def _plan(self, ops: list[OpNode]) -> _StagePlan:
         """Peephole fusion over one stage program: matmul -> relu becomes one
@@ -581,10 +600,7 @@ class DeviceOps:
         return out
 
     def _embed_bwd(self, op, env, acc=None):
-        if self._side_pending:   # the head weight gradient adds into the same tied sum
-            self._join()
-            self._side_pending = False
-            self._side_keep.clear()
+        self._join_side()   # the head weight gradient adds into the same tied sum
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
@@ -880,10 +896,9 @@ class DeviceOps:
         ln_bwd(da, h, "ln1_g", "ln1_b", sv["mean1"], sv["rstd1"], dh1, dh)
         if _DEFER_JOIN:
             # the next block's data-gradient chain does not wait for this block's
-            # side-stream work; the allocator keeps every tensor that work reads
-            # until it has run (kept in _side_keep), and run_ops joins at the end
-            self._side_keep.extend((dz, dout, du, da2, dh1, dqkv, da, h, sv))
-            self._side_pending = True
+            # side-stream work; every tensor that work reads stays alive until
+            # the compute stream has waited for it (_defer_side)
+            self._defer_side((dz, dout, du, da2, dh1, dqkv, da, h, sv))
         else:
             self._join()
         return (dh, dW)
@@ -949,14 +964,14 @@ class DeviceOps:
         sst = side.cuda_stream if side is not None else self.st
         if side is not None:
             self._fork()
-            self._side_keep.extend((dlogits, h))
-            self._side_pending = True
         if acc is not None:
             # onto the running sum: the wte rows through the GEMM's TMA
             # reduce-add store (unsplit: one fp32 add per element); the head's
             # wpe part is zero, nothing to add
             self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d,
                        self._slice(acc, self._elay, "wte"), d, _lib.EPI_ACCUM, st=sst)
+            if side is not None:
+                self._defer_side((dlogits, h))
             return (dh, acc)
         # wte gradient from the GEMM; wpe's part of the tied partial is zero.
         # Zero-fill only what the GEMM does not overwrite: all of wte when it
@@ -973,6 +988,8 @@ class DeviceOps:
             call("pc_fill", _lib.PC_F32, tail.numel(), 0.0, tail.data_ptr(), sst)
         self._gemm(torch.float32, 1, 0, V, d, T, dlogits, V, h, d, wte, d, _lib.EPI_SPLITK_ZERO_C,
                    st=sst)
+        if side is not None:
+            self._defer_side((dlogits, h, dw))
         return (dh, dw)
 
 
@@ -1003,10 +1020,7 @@ class DeviceOps:
     def _llama_embed_bwd(self, op, env, acc=None):
         """Token-row sums of the embedding gradient, onto the running sum when
         fused (no [vocab, d] zero fill per microbatch), else onto zeros."""
-        if self._side_pending:   # pending side-stream work may still write gradients
-            self._join()
-            self._side_pending = False
-            self._side_keep.clear()
+        self._join_side()   # pending side-stream work may still write gradients
         cfg = self.gpt
         g = tensor_of(env[op.operands[0]])
         x = tensor_of(env[op.operands[1]])
@@ -1184,9 +1198,8 @@ class DeviceOps:
         self._gemm(act, 0, tb, T, d, qw, dqkv, qw, B, ldb, da, d)
         # the stage input gradient: into the previous stage's slot when sent
         dh = rms_bwd(da, h, "rms1_g", sv["rstd1"], dh1, self._placed_elem(op, 0, (T, d), act))
-        if _DEFER_JOIN:   # as in _block_bwd: run_ops joins the side stream at the end
-            self._side_keep.extend((dz, dout, dgu, da2, dh1, dqkv, da, h, sv))
-            self._side_pending = True
+        if _DEFER_JOIN:   # as in _block_bwd
+            self._defer_side((dz, dout, dgu, da2, dh1, dqkv, da, h, sv))
         else:
             self._join()
         return (dh, dW)
@@ -1227,8 +1240,7 @@ class DeviceOps:
         self._wgrad_into(V, d, T, dlogits, V, h, d, self._slice(dw, self._hlay, "w_head"), fused,
                          self._side())
         if _DEFER_JOIN:   # the blocks' backward does not wait for the head weight gradient
-            self._side_keep.extend((dlogits, h))
-            self._side_pending = True
+            self._defer_side((dlogits, h))
         else:
             self._join()
         return (dh, dw)

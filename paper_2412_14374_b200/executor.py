@@ -1240,9 +1240,16 @@ class PipelineEngine:
         graph = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.device(act.device):
             torch.cuda.synchronize()
-            with torch.cuda.graph(graph, stream=act.stream):
-                _worker(act, self.cp.programs[a].instrs, self.tg, self._channels, ctl, None,
-                        counting, self._rebroadcast if resident else None)
+            try:
+                with torch.cuda.graph(graph, stream=act.stream):
+                    _worker(act, self.cp.programs[a].instrs, self.tg, self._channels, ctl, None,
+                            counting, self._rebroadcast if resident else None)
+            except Exception as e:
+                # a fault inside the worker leaves the capture unjoined, and ending
+                # the capture then fails too: report the fault, not that symptom
+                if ctl.faults:
+                    raise ctl.faults[0] from e
+                raise
         if ctl.faults:
             raise ctl.faults[0]
         # send-completion events recorded into the graph cannot be queried; every
