@@ -88,3 +88,53 @@ def test_c5_small_bf16_full_remat_with_skip_channels():
     assert np.array_equal(a.losses, b.losses)
     for q in a.grads:
         assert np.array_equal(a.grads[q], b.grads[q]), q
+
+
+def test_c5_small_bf16_one_stage_captures():
+    """The bench's sequence on a one-stage Llama program (all blocks' deferred
+    side-stream gradient work in one stage program): resident eager step, a
+    captured step, then a second, instrumented capture -- replays equal the
+    eager step bitwise and the deferred side work stays bounded."""
+    import torch
+    from paper_2412_14374_b200 import device as D
+    from paper_2412_14374_b200.executor import PipelineEngine
+    kw = dict(C5S, layers=6)
+    cfg = I.LlamaConfig(**kw, yield_every=kw["layers"] + 2, elem_bytes=2)
+    p = I.derive_backward(I.partition_stages(I.build_llama(cfg)))
+    tg = T.infer_outer_placement(T.commute_grad_accumulation(T.unroll(p, S.one_f_one_b(1, 4))), p)
+    cp = C.plan_pipeline(tg)
+    oc = dict(layers=cfg.layers, d=cfg.d_model, heads=cfg.n_heads, kv_heads=cfg.n_kv_heads,
+              ff=cfg.d_ff, vocab=cfg.vocab, seq=cfg.seq_len, mbs=cfg.microbatch_size,
+              theta=cfg.rope_theta)
+    rng = np.random.default_rng(3)
+    params = {q: v.astype(np.float32) for q, v in llama.init_params(oc, rng, std=0.05).items()}
+    tokens = llama.init_tokens(oc, 4, rng).reshape(4 * cfg.microbatch_size, cfg.seq_len)
+    pos = llama.positions(oc, 4).reshape(tokens.shape)
+    batch = {"x": torch.tensor(tokens, device="cuda"), "pos": torch.tensor(pos, device="cuda")}
+    seen = []
+    orig = D.DeviceOps._defer_side
+
+    def spy(self, tensors):
+        orig(self, tensors)
+        seen.append(len(self._side_ring))
+    D.DeviceOps._defer_side = spy
+    try:
+        eng = PipelineEngine(cp, tg, mode="bf16", gpt=cfg)
+        eng.load_params(params)
+        e = eng.step(None, batch, lr=0.0, to_host=False)
+        cap = eng.capture(None, batch, lr=0.0)
+        r1 = cap.replay()
+        torch.cuda.synchronize()
+        l1 = r1.losses.cpu().numpy()
+        cap_tl = eng.capture(None, batch, lr=0.0, timeline=True)
+        r2 = cap_tl.replay()
+        torch.cuda.synchronize()
+        assert cap_tl.timeline()
+        l2 = r2.losses.cpu().numpy()
+        cap.release()
+        cap_tl.release()
+    finally:
+        D.DeviceOps._defer_side = orig
+    assert np.array_equal(e.losses.cpu().numpy(), l1)
+    assert np.array_equal(l1, l2)
+    assert seen and max(seen) <= D._DEFER_DEPTH
