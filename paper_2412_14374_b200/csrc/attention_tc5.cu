@@ -1218,7 +1218,7 @@ __device__ __forceinline__ uint4 ld_chunk128(const uint8_t* tile, int r, int j) 
 //               over their own score columns: the dQ MMA reads A from TMEM
 // Ring / buffer phases run on tile-global block counters, so a tile's first
 // blocks reuse buffers the previous tile released.
-template <int HD>
+template <int HD, int SPLIT = 0>  // SPLIT: dQ MMAs from warp 3, S / dP from warp 1
 __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
     fa_bwd_dq_tc5(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tg,
                   const __grid_constant__ CUtensorMap to, const float* __restrict__ lse,
@@ -1357,6 +1357,13 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
         }
         __syncwarp();
       };
+      if (SPLIT) {
+        for (int j = 0; j < nkb; ++j) issue_s(g0 + j);
+        if (elect_one()) tc_commit(&q_empty[qb]);  // Q / dO of this tile no longer read by MMAs
+        __syncwarp();
+        g0 += nkb;
+        continue;
+      }
       for (int j = 0; j < K::SBUF && j < nkb; ++j) issue_s(g0 + j);
       for (int j = 0; j < nkb; ++j) {
         const uint32_t g = g0 + j;
@@ -1379,6 +1386,33 @@ __global__ void __launch_bounds__(BwdQ<HD>::THREADS, 1)
         tc_commit(&q_empty[qb]);  // Q / dO of this tile no longer read by MMAs
         tc_commit(done);          // dQ of this tile complete
       }
+      __syncwarp();
+      g0 += nkb;
+    }
+  } else if (SPLIT && warp == 3) {
+    constexpr uint32_t ID_A = umma_idesc_bf16(128, HD, 0, 1);     // dS x K (MN-major)
+    const uint64_t kn = umma_sdesc_sw128(smem_u32(sK), K::KV_PANEL, 1024);   // MN-major view
+    uint32_t g0 = 0, ic = 0;
+    for (int w = snake_item(0); w < items; w = snake_item(++ic)) {
+      int bh, q0, nkb;
+      decode(w, bh, q0, nkb);
+      for (int j = 0; j < nkb; ++j) {
+        const uint32_t g = g0 + j;
+        const int st = g % K::STAGES, sb = g % K::SBUF;
+        mbar_wait(&p_full[sb], (g / K::SBUF) & 1);
+        tc_fence_after();
+        const uint64_t so = static_cast<uint64_t>(st * (K::KV_BYTES >> 4));
+        const uint32_t tD = tmem + sb * 128;
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < K::BN / 16; ++k)
+            tc_mma_f16_ts(tdQ, tD + 16 * k, kn + so + 128 * k, ID_A, (j > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&pv_done[sb]);
+          tc_commit(&kv_empty[st]);  // K_j / V_j: the S / dP MMAs retired before p_full
+        }
+        __syncwarp();
+      }
+      if (elect_one()) tc_commit(done);  // dQ of this tile complete
       __syncwarp();
       g0 += nkb;
     }
@@ -1511,6 +1545,7 @@ int make_tmap_rows64(CUtensorMap* m, const void* base, int64_t ld, int64_t rows)
 int g_fwd64_design = 3;  // pc_attention_tune key 0
 int g_fwd64_emu = 6;     // pc_attention_tune key 1
 int g_fwd_split = 1;     // pc_attention_tune key 2: fa_fwd_tc5 with two issuing warps
+int g_dq_split = 1;      // pc_attention_tune key 3: fa_bwd_dq_tc5 with two issuing warps
 
 // O as a 3-D tensor [B][S][ld_o] (rows clipped per sequence), box 64 x 32 x 1.
 int make_tmap_o3(CUtensorMap* m, const void* base, int64_t ld, int S, int B) {
@@ -1612,7 +1647,9 @@ int bwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, const vo
   if (!attr) {
     PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dkdv_tc5<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      BwdKV<HD>::SMEM));
-    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dq_tc5<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dq_tc5<HD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     BwdQ<HD>::SMEM));
+    PP_CUDA_TRY(cudaFuncSetAttribute(fa_bwd_dq_tc5<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      BwdQ<HD>::SMEM));
     attr = true;
   }
@@ -1622,8 +1659,12 @@ int bwd_launch(int B, int S, Heads hs, const void* qkv, int64_t ld_qkv, const vo
   // Both persistent: one CTA per SM over their work lists.
   const int dq_items = B * hs.H * ((S + BwdQ<HD>::BM - 1) / BwdQ<HD>::BM);
   const int g2 = dq_items < num_sms() ? dq_items : num_sms();
-  fa_bwd_dq_tc5<HD><<<g2, BwdQ<HD>::THREADS, BwdQ<HD>::SMEM, st>>>(
-      tq, tg, to, lse, delta, static_cast<bf16*>(dqkv), ld_dqkv, B * hs.H, hs, S, sl2, scale);
+  if (g_dq_split)
+    fa_bwd_dq_tc5<HD, 1><<<g2, BwdQ<HD>::THREADS, BwdQ<HD>::SMEM, st>>>(
+        tq, tg, to, lse, delta, static_cast<bf16*>(dqkv), ld_dqkv, B * hs.H, hs, S, sl2, scale);
+  else
+    fa_bwd_dq_tc5<HD, 0><<<g2, BwdQ<HD>::THREADS, BwdQ<HD>::SMEM, st>>>(
+        tq, tg, to, lse, delta, static_cast<bf16*>(dqkv), ld_dqkv, B * hs.H, hs, S, sl2, scale);
   rc = check_launch("fa_bwd_dq_tc5");
   if (rc) return rc;
   const int kv_items = B * hs.Hkv * ((S + BwdKV<HD>::KEYS - 1) / BwdKV<HD>::KEYS);
@@ -1639,6 +1680,8 @@ int attention_tc5_tune(int key, int value) {
     g_fwd64_design = value;
   } else if (key == 2 && (value == 0 || value == 1)) {
     g_fwd_split = value;
+  } else if (key == 3 && (value == 0 || value == 1)) {
+    g_dq_split = value;
   } else if (key == 1 && (value == 0 || value == 4 || value == 6 || value == 8 || value == 101 || value == 102)) {
     g_fwd64_emu = value;
   } else {
