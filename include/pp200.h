@@ -250,10 +250,13 @@ int pc_attention_gqa_bwd(int dtype, int B, int H, int Hkv, int S, int hd, const 
 int pc_attention_set_impl(int impl);
 /* Tuning hook for the tcgen05 attention kernels (bench / A-B tools; the
  * defaults are the measured best).  key 0: head_dim-64 forward design
- * (1 = one-tile-per-CTA fa_fwd_tc5 with P over S, 2 = persistent fa_fwd64_tc5,
- * default); key 1: score columns of every 16 whose exp2 runs on the FMA pipe in
- * fa_fwd64_tc5 (0, 4, 6 default, 8; 101 / 102 = profiling ablations without the
- * softmax math / without the MMAs, results meaningless). */
+ * (1 = one-tile-per-CTA fa_fwd_tc5 with P over S, 2 = persistent fa_fwd64_tc5 with one
+ * MMA-issuing warp, 3 = the same with scores and PV from two issuing warps, default);
+ * key 1: score columns of every 16 whose exp2 runs on the FMA pipe in fa_fwd64_tc5
+ * (0, 4, 6 default, 8; 101 / 102 = profiling ablations without the softmax math /
+ * without the MMAs, results meaningless); key 2: head_dim-128 forward with one (0) or
+ * two (1, default) issuing warps; key 3: backward dQ kernel with one (0) or two (1,
+ * default) issuing warps.  The issuer choices are bitwise identical. */
 int pc_attention_tune(int key, int value);
 
 /* ---- inter-stage transport over NVLink peer memory (Channel, executor.py:201-254) ----
