@@ -158,6 +158,16 @@ int pc_layernorm_bwd_acc(int dtype, int64_t rows, int64_t d, const void* dy, con
 int pc_layernorm_param_grads(int dtype, int64_t rows, int64_t d, const void* dy, const void* x,
                              const float* mean, const float* rstd, float* dgamma, float* dbeta,
                              int accumulate, void* ws, int64_t ws_bytes, void* stream);
+/* One pass for a GPT block's LN2 side-stream sums (bf16, [rows, d], ld = d, 16 B rows):
+ * dgamma / dbeta as pc_layernorm_param_grads, dsum3 (+)= sum_r y3 (the fc2 bias
+ * gradient, y3 = the block's incoming gradient) and dsum4 (+)= sum_r y4 (the
+ * attention-output bias gradient, y4 = LN2's output gradient).  Bitwise equal to
+ * pc_layernorm_param_grads + two pc_col_sum calls; replaces the bias column sums of
+ * the reference backward's `sum-to` rule (executor.py:50-56, 91-92) for those two biases. */
+int pc_layernorm_param_bias_grads(int64_t rows, int64_t d, const void* dy, const void* x,
+                                  const float* mean, const float* rstd, float* dgamma,
+                                  float* dbeta, const void* y3, float* dsum3, const void* y4,
+                                  float* dsum4, int accumulate, void* stream);
 /* LayerNorm backward in one read of dy and x: dx (+ dres) as pc_layernorm_bwd, plus per-CTA
  * partial rows of dgamma = sum dy*xhat and dbeta = sum dy written to partials [2][n_part][d]
  * (n_part from pc_layernorm_partial_rows); pc_col_sum (fp32, fixed order, accumulate as

@@ -76,6 +76,8 @@ SIGNATURES: dict[str, list] = {
                                   _c_p, _c_i64, _c_p],
     "pc_layernorm_param_grads": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i,
                                  _c_p, _c_i64, _c_p],
+    "pc_layernorm_param_bias_grads": [_c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                      _c_p, _c_p, _c_p, _c_i, _c_p],
     "pc_rmsnorm_fwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_f, _c_p],
     "pc_rmsnorm_bwd": [_c_i, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                        _c_i64, _c_p],

@@ -451,27 +451,38 @@ __global__ void __launch_bounds__(256) colsum_cluster_kernel(
     int64_t rows, int64_t cols, const __nv_bfloat16* __restrict__ a, int64_t lda,
     const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, float* __restrict__ out1, float* __restrict__ out2,
-    int accumulate) {
-  constexpr int U = MODE == 1 ? 4 : 8;  // rows in flight per thread (x 2 tensors in MODE 1)
+    int accumulate, const __nv_bfloat16* __restrict__ y3, const __nv_bfloat16* __restrict__ y4,
+    float* __restrict__ out3, float* __restrict__ out4) {
+  // rows in flight per thread: 8 (MODE 0), 4 x 2 tensors (MODE 1), 2 x 4 tensors (MODE 2).
+  // Whatever U, a thread sums its rows r0 + sub + 4 w + 32 k in increasing k, so
+  // MODE 2's four sums equal MODE 1's two and MODE 0's one bit for bit.
+  constexpr int U = MODE == 0 ? 8 : (MODE == 1 ? 4 : 2);
+  constexpr int NS = MODE == 0 ? 1 : (MODE == 1 ? 2 : 4);  // sums per column
   __shared__ float red1[8][4][64];
-  __shared__ float red2[MODE == 1 ? 8 : 1][4][64];
-  __shared__ float part[2][64];
+  __shared__ float red2[MODE >= 1 ? 8 : 1][4][64];
+  __shared__ float red3[MODE == 2 ? 8 : 1][4][64];
+  __shared__ float red4[MODE == 2 ? 8 : 1][4][64];
+  __shared__ float part[NS][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int cg = lane & 7, sub = lane >> 3;  // 8 columns of the slab, one of 4 rows
   const int64_t c0 = blockIdx.x * 64 + cg * 8;
   const uint32_t rank = cluster_ctarank(), ncl = cluster_nctarank();
   const int64_t rpc = (rows + ncl - 1) / ncl;
   const int64_t r0 = rank * rpc, r1 = min(rows, r0 + rpc);
-  float s1[8] = {}, s2[8] = {};
+  float s1[8] = {}, s2[8] = {}, s3[8] = {}, s4[8] = {};
   if (c0 < cols) {
     for (int64_t rb = r0 + sub + 4 * w; rb < r1; rb += 32 * U) {
-      uint4 u[U], ux[U];
+      uint4 u[U], ux[U], u3[U], u4[U];
 #pragma unroll
       for (int i = 0; i < U; ++i) {
         const int64_t r = rb + 32 * i;
         u[i] = r < r1 ? *reinterpret_cast<const uint4*>(a + r * lda + c0) : make_uint4(0, 0, 0, 0);
-        if (MODE == 1)
+        if (MODE >= 1)
           ux[i] = r < r1 ? *reinterpret_cast<const uint4*>(x + r * lda + c0) : make_uint4(0, 0, 0, 0);
+        if (MODE == 2) {
+          u3[i] = r < r1 ? *reinterpret_cast<const uint4*>(y3 + r * lda + c0) : make_uint4(0, 0, 0, 0);
+          u4[i] = r < r1 ? *reinterpret_cast<const uint4*>(y4 + r * lda + c0) : make_uint4(0, 0, 0, 0);
+        }
       }
 #pragma unroll
       for (int i = 0; i < U; ++i) {
@@ -491,6 +502,16 @@ __global__ void __launch_bounds__(256) colsum_cluster_kernel(
               s1[j] += v[j] * ((xv[j] - mu) * rs);
               s2[j] += v[j];
             }
+            if (MODE == 2) {
+              float v3[8], v4[8];
+              bf16x8_to_f32(u3[i], v3);
+              bf16x8_to_f32(u4[i], v4);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                s3[j] += v3[j];
+                s4[j] += v4[j];
+              }
+            }
           }
         }
       }
@@ -499,32 +520,46 @@ __global__ void __launch_bounds__(256) colsum_cluster_kernel(
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     red1[w][sub][cg * 8 + j] = s1[j];
-    if (MODE == 1) red2[w][sub][cg * 8 + j] = s2[j];
+    if (MODE >= 1) red2[w][sub][cg * 8 + j] = s2[j];
+    if (MODE == 2) {
+      red3[w][sub][cg * 8 + j] = s3[j];
+      red4[w][sub][cg * 8 + j] = s4[j];
+    }
   }
   __syncthreads();
   if (threadIdx.x < 64) {
-    float t1 = 0.f, t2 = 0.f;
+    float t1 = 0.f, t2 = 0.f, t3 = 0.f, t4 = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         t1 += red1[k][q][threadIdx.x];
-        if (MODE == 1) t2 += red2[k][q][threadIdx.x];
+        if (MODE >= 1) t2 += red2[k][q][threadIdx.x];
+        if (MODE == 2) {
+          t3 += red3[k][q][threadIdx.x];
+          t4 += red4[k][q][threadIdx.x];
+        }
       }
     part[0][threadIdx.x] = t1;
-    part[1][threadIdx.x] = t2;
+    if (MODE >= 1) part[1][threadIdx.x] = t2;
+    if (MODE == 2) {
+      part[2][threadIdx.x] = t3;
+      part[3][threadIdx.x] = t4;
+    }
   }
   cluster_sync_all();
   const int64_t c = blockIdx.x * 64 + threadIdx.x;
   if (rank == 0 && threadIdx.x < 64 && c < cols) {
-    const uint32_t p1 = smem_u32(&part[0][threadIdx.x]), p2 = smem_u32(&part[1][threadIdx.x]);
-    float t1 = 0.f, t2 = 0.f;
-    for (uint32_t q = 0; q < ncl; ++q) {
-      t1 += ld_shared_cluster_f32(mapa_shared(p1, q));
-      if (MODE == 1) t2 += ld_shared_cluster_f32(mapa_shared(p2, q));
+    float t[NS] = {};
+    for (uint32_t q = 0; q < ncl; ++q)
+#pragma unroll
+      for (int k = 0; k < NS; ++k) t[k] += ld_shared_cluster_f32(mapa_shared(smem_u32(&part[k][threadIdx.x]), q));
+    out1[c] = accumulate ? out1[c] + t[0] : t[0];
+    if (MODE >= 1 && out2) out2[c] = accumulate ? out2[c] + t[1] : t[1];
+    if (MODE == 2) {
+      out3[c] = accumulate ? out3[c] + t[2] : t[2];
+      out4[c] = accumulate ? out4[c] + t[3] : t[3];
     }
-    out1[c] = accumulate ? out1[c] + t1 : t1;
-    if (MODE == 1 && out2) out2[c] = accumulate ? out2[c] + t2 : t2;
   }
   cluster_sync_all();  // peers' partials stay valid until rank 0 has read them
 }
@@ -532,7 +567,9 @@ __global__ void __launch_bounds__(256) colsum_cluster_kernel(
 template <int MODE>
 int colsum_cluster_launch(int64_t rows, int64_t cols, const __nv_bfloat16* a, int64_t lda,
                           const __nv_bfloat16* x, const float* mean, const float* rstd, float* out1,
-                          float* out2, int accumulate, cudaStream_t st) {
+                          float* out2, int accumulate, cudaStream_t st,
+                          const __nv_bfloat16* y3 = nullptr, const __nv_bfloat16* y4 = nullptr,
+                          float* out3 = nullptr, float* out4 = nullptr) {
   static bool attr = false;
   if (!attr) {
     PP_CUDA_TRY(cudaFuncSetAttribute(colsum_cluster_kernel<MODE>,
@@ -555,7 +592,7 @@ int colsum_cluster_launch(int64_t rows, int64_t cols, const __nv_bfloat16* a, in
   cfg.attrs = at;
   cfg.numAttrs = 1;
   PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, colsum_cluster_kernel<MODE>, rows, cols, a, lda, x, mean, rstd,
-                                 out1, out2, accumulate));
+                                 out1, out2, accumulate, y3, y4, out3, out4));
   return check_launch("colsum_cluster_kernel");
 }
 
@@ -643,6 +680,28 @@ using namespace pp200;
 extern "C" int pc_colsum_set_cluster(int on) {
   pp200::g_colsum_cluster = on ? 1 : 0;
   return PC_OK;
+}
+
+// LayerNorm parameter gradients plus two bias gradients in one pass (the GPT
+// block's LN2: dgamma / dbeta from dy and x, and the column sums of the MLP's
+// incoming gradient (b_fc2) and of LN2's output gradient (b_o), all [rows, d]).
+// Bit-identical to pc_layernorm_param_grads + two pc_col_sum calls on the
+// cluster path (same per-thread row order); bf16, d % 8 == 0, 16 B rows only.
+extern "C" int pc_layernorm_param_bias_grads(int64_t rows, int64_t d, const void* dy,
+                                             const void* x, const float* mean, const float* rstd,
+                                             float* dgamma, float* dbeta, const void* y3,
+                                             float* dsum3, const void* y4, float* dsum4,
+                                             int accumulate, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= 0) return PC_OK;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  PP_CHECK_ARG(dgamma && dbeta && dsum3 && dsum4 && rstd && d > 0 && d % 8 == 0 && al16(dy) &&
+                   al16(x) && al16(y3) && al16(y4),
+               "layernorm_param_bias_grads: needs bf16 rows of d %% 8 == 0, 16 B aligned, and all outputs");
+  return colsum_cluster_launch<2>(rows, d, static_cast<const __nv_bfloat16*>(dy), d,
+                                  static_cast<const __nv_bfloat16*>(x), mean, rstd, dgamma, dbeta,
+                                  accumulate, st, static_cast<const __nv_bfloat16*>(y3),
+                                  static_cast<const __nv_bfloat16*>(y4), dsum3, dsum4);
 }
 
 extern "C" int pc_fill(int dtype, int64_t n, double value, void* out, void* stream) {

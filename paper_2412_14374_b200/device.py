@@ -92,6 +92,10 @@ _LN_PARAMS_MAIN = os.environ.get("PP200_LN_PARAMS_MAIN") == "1"   # A/B switch f
 # N=1 it is slower (75.0-75.6 vs 71.3-72.2 ms): the compute-stream kernel loses more to
 # its row-chunked grid than the side-stream reduction it replaces costs.
 _LN_FUSED = os.environ.get("PP200_LN_FUSED", "0") == "1"
+# A/B switch, on by default: a GPT block's LN2 parameter gradients and its fc2 /
+# attention-output bias gradients in one side-stream pass (pc_layernorm_param_bias_grads)
+# instead of three column-sum launches; bitwise equal either way.
+_LN_BIAS_FUSED = os.environ.get("PP200_LN_BIAS_FUSED", "1") != "0"
 # A/B switch: 0 = logits GEMM then the stand-alone cross-entropy kernel (pc_xent_fwd_bwd)
 _XENT_FUSED = os.environ.get("PP200_XENT_FUSED", "1") != "0"
 # A/B switch: 0 = bf16 column sums through the two-stage workspace kernel instead of
@@ -808,11 +812,25 @@ class DeviceOps:
         # (never reallocated while side work may still read it)
         self.red_ws(T, max(f, 3 * d), side=True)
 
-        def ln_bwd(dy, x, gname, bname, mean, rstd, dres, dx):
+        def ln_bwd(dy, x, gname, bname, mean, rstd, dres, dx, biases=None):
             """LayerNorm backward: dx on the compute stream; gamma / beta gradients
             (a reduction nothing downstream waits for) beside it on the side
             stream.  PP200_LN_FUSED=1: one pass for dx and partial rows of the
-            parameter gradients, their column sums on the side stream."""
+            parameter gradients, their column sums on the side stream.  biases =
+            (y3, name3, y4, name4): two bias gradients (column sums of y3 and of
+            y4, which may be dx itself) in the same side-stream pass, after dx."""
+            if biases is not None:
+                y3, n3, y4, n4 = biases
+                call("pc_layernorm_bwd_acc", self.mode.pc_act, T, d, dy.data_ptr(), x.data_ptr(),
+                     ms(gname).data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                     None if dres is None else dres.data_ptr(), dx.data_ptr(), None, None, 0,
+                     *self.red_ws(T, d), self.st)
+                self._fork()
+                call("pc_layernorm_param_bias_grads", T, d, dy.data_ptr(), x.data_ptr(),
+                     mean.data_ptr(), rstd.data_ptr(), gs(gname).data_ptr(), gs(bname).data_ptr(),
+                     y3.data_ptr(), gs(n3).data_ptr(), y4.data_ptr(), gs(n4).data_ptr(), int(fused),
+                     sst)
+                return
             if _LN_FUSED and "lnp" not in _ABLATE and d % 256 == 0 and d <= 1024:
                 # dx and the parameter-gradient partial rows in one pass on the
                 # compute stream; their fixed-order column sums on the side stream
@@ -850,11 +868,11 @@ class DeviceOps:
         # Weight gradients and their bias sums run on the side stream (they do
         # not feed the dX chain); each fork orders them after their inputs.
 
-        def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname, weight=True):
+        def wgrad(M_, N_, A, lda, Bm, ldb, wname, bname, weight=True, bias=True):
             self._fork()
             if weight and "wgrad" not in _ABLATE:
                 self._wgrad_into(M_, N_, T, A, lda, Bm, ldb, gs(wname), fused, self._side())
-            if _ABLATE_BIAS:   # profiling only: bias gradients left unset
+            if _ABLATE_BIAS or not bias:   # _ABLATE_BIAS: profiling only, left unset
                 return
             call("pc_col_sum", self.mode.pc_act, _lib.PC_F32, T, M_, A.data_ptr(), lda,
                  gs(bname).data_ptr(), int(fused), *self.red_ws(T, M_, side=True), sst)
@@ -863,8 +881,13 @@ class DeviceOps:
         # grouped launch once both inputs exist (dW_o alone left most SMs idle)
         pair = self.mode.act == torch.bfloat16 and (3 * d) % 256 == 0 and _WGRAD_PAIR
 
+        # the fc2 and attention-output bias gradients ride on LN2's parameter pass
+        lnb = (_LN_BIAS_FUSED and act == torch.bfloat16 and not _LN_FUSED and not _LN_PARAMS_MAIN
+               and not _ABLATE_BIAS and "lnp" not in _ABLATE and d % 8 == 0
+               and dout.data_ptr() % 16 == 0 and sv["h1"].data_ptr() % 16 == 0)
+
         # MLP
-        wgrad(d, f, dout, d, sv["gu"], f, "w_fc2", "b_fc2")
+        wgrad(d, f, dout, d, sv["gu"], f, "w_fc2", "b_fc2", bias=not lnb)
         du = self.empty((T, f), act)
         tb, B, ldb = wB("w_fc2")
         self._gemm(act, 0, tb, T, f, d, dout, d, B, ldb, du, f, _lib.EPI_GELU_GRAD,
@@ -874,9 +897,10 @@ class DeviceOps:
         tb, B, ldb = wB("w_fc1")
         self._gemm(act, 0, tb, T, d, f, du, f, B, ldb, da2, d)
         dh1 = self.empty((T, d), act)
-        ln_bwd(da2, sv["h1"], "ln2_g", "ln2_b", sv["mean2"], sv["rstd2"], dout, dh1)
+        ln_bwd(da2, sv["h1"], "ln2_g", "ln2_b", sv["mean2"], sv["rstd2"], dout, dh1,
+               biases=(dout, "b_fc2", dh1, "b_o") if lnb else None)
         # attention
-        wgrad(d, d, dh1, d, sv["o"], d, "w_o", "b_o", weight=not pair)
+        wgrad(d, d, dh1, d, sv["o"], d, "w_o", "b_o", weight=not pair, bias=not lnb)
         do = self.empty((T, d), act)
         tb, B, ldb = wB("w_o")
         self._gemm(act, 0, tb, T, d, d, dh1, d, B, ldb, do, d)

@@ -342,6 +342,44 @@ def test_col_sum_bf16_shapes_and_determinism(rows, cols):
     assert torch.allclose(acc, outs[0] + 0.5, rtol=1e-6, atol=1e-5)
 
 
+@pytest.mark.parametrize("rows,d", [(8192, 768), (8192, 1024), (1000, 768), (37, 256), (8191, 2048)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_layernorm_param_bias_grads_equal_the_separate_sums(rows, d, accumulate):
+    """pc_layernorm_param_bias_grads (LN2's dgamma / dbeta plus the fc2 and
+    attention-output bias gradients in one pass) is bitwise equal to
+    pc_layernorm_param_grads + two pc_col_sum calls, with and without
+    accumulation onto a running sum, and within fp32 rounding of fp64."""
+    g = torch.Generator(device="cuda").manual_seed(rows + d)
+    dy, x, y3, y4 = (torch.randn(rows, d, device="cuda", generator=g).to(torch.bfloat16)
+                     for _ in range(4))
+    mean = torch.randn(rows, device="cuda", generator=g) * 0.1
+    rstd = torch.rand(rows, device="cuda", generator=g) + 0.5
+    nb = ctypes.c_int64()
+    _lib.call("pc_reduce_workspace_bytes", rows, d, ctypes.byref(nb))
+    ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    init = torch.randn(4, d, device="cuda", generator=g)
+    sep, one = init.clone(), init.clone()
+    _lib.call("pc_layernorm_param_grads", _lib.PC_BF16, rows, d, dy.data_ptr(), x.data_ptr(),
+              mean.data_ptr(), rstd.data_ptr(), sep[0].data_ptr(), sep[1].data_ptr(), accumulate,
+              ws.data_ptr(), nb.value, st)
+    for i, y in ((2, y3), (3, y4)):
+        _lib.call("pc_col_sum", _lib.PC_BF16, _lib.PC_F32, rows, d, y.data_ptr(), d,
+                  sep[i].data_ptr(), accumulate, ws.data_ptr(), nb.value, st)
+    _lib.call("pc_layernorm_param_bias_grads", rows, d, dy.data_ptr(), x.data_ptr(),
+              mean.data_ptr(), rstd.data_ptr(), one[0].data_ptr(), one[1].data_ptr(),
+              y3.data_ptr(), one[2].data_ptr(), y4.data_ptr(), one[3].data_ptr(), accumulate, st)
+    torch.cuda.synchronize()
+    assert torch.equal(sep, one)
+    xhat = (x.double() - mean.double()[:, None]) * rstd.double()[:, None]
+    ref = torch.stack([(dy.double() * xhat).sum(0), dy.double().sum(0), y3.double().sum(0),
+                       y4.double().sum(0)])
+    if accumulate:
+        ref = ref + init.double()
+    err = ((one.double() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-5, err
+
+
 def test_fused_grad_accumulation_matches_the_add_chain():
     """Block weight / bias / LN gradients added onto the running sum by their
     producers (GEMM TMA reduce-add, reductions with accumulate) reproduce the
