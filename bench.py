@@ -30,6 +30,10 @@ from pathlib import Path
 
 import numpy as np
 
+# NCCL's own log lines (e.g. "NCCL version ..." under NCCL_DEBUG=VERSION) go to stderr, so
+# rank 0's stdout carries only the one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
