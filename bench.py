@@ -30,10 +30,6 @@ from pathlib import Path
 
 import numpy as np
 
-# NCCL's own log lines (e.g. "NCCL version ..." under NCCL_DEBUG=VERSION) go to stderr, so
-# rank 0's stdout carries only the one JSON line
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -553,7 +549,18 @@ def run_reference_impl(args, rank, world):
     return 0
 
 
+def _isolate_stdout():
+    """Native writes to fd 1 (NCCL's "NCCL version" banner, printed with printf under
+    NCCL_DEBUG=WARN / VERSION) go to stderr; Python's sys.stdout keeps the original
+    stdout, so rank 0's stdout carries only the one JSON line."""
+    sys.stdout.flush()
+    keep = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(keep, "w", buffering=1)
+
+
 def main():
+    _isolate_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
