@@ -123,7 +123,8 @@ int pc_colsum_set_cluster(int on);
 /* Scratch for the two-stage (many-CTA, fixed-order) column reductions used by
  * pc_col_sum and pc_layernorm_bwd; with ws == NULL they fall back to one stage. */
 int pc_reduce_workspace_bytes(int64_t rows, int64_t cols, int64_t* bytes);
-/* dst = src or src^T (slice / concat / broadcast materialisation, :78-95). */
+/* dst = src or src^T (slice / concat / broadcast materialisation, :78-95); lds = 0 with
+ * trans = 0 repeats one source row (or one element, cols = 1) into every dst row. */
 int pc_copy2d(int dtype, int64_t rows, int64_t cols, const void* src, int64_t lds, int trans,
               void* dst, int64_t ldd, void* stream);
 /* acc += part in place: the fused fp32 gradient accumulator replacing the

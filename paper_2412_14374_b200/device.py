@@ -499,16 +499,14 @@ class DeviceOps:
     def _broadcast(self, x: torch.Tensor, dims) -> torch.Tensor:
         dims = tuple(dims)
         out = self.empty(dims, x.dtype)
+        # one launch each: a zero source row stride repeats the row (or the scalar)
         if len(dims) == 2 and x.numel() == dims[1]:
-            for r in range(dims[0]):  # small; generic vocabulary only
-                call("pc_copy2d", _PC[x.dtype], 1, dims[1], x.data_ptr(), dims[1], 0,
-                     out[r].data_ptr(), dims[1], self.st)
+            call("pc_copy2d", _PC[x.dtype], dims[0], dims[1], x.data_ptr(), 0, 0,
+                 out.data_ptr(), dims[1], self.st)
             return out
         if x.numel() == 1:
-            flat = out.reshape(-1)
-            for i in range(flat.numel()):
-                call("pc_copy2d", _PC[x.dtype], 1, 1, x.data_ptr(), 1, 0, flat[i].data_ptr(), 1,
-                     self.st)
+            call("pc_copy2d", _PC[x.dtype], out.numel(), 1, x.data_ptr(), 0, 0, out.data_ptr(), 1,
+                 self.st)
             return out
         raise ValueError(f"broadcast {tuple(x.shape)} -> {dims} unsupported on device")
 

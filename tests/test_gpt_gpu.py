@@ -487,3 +487,20 @@ def test_layernorm_bwd_partials_then_col_sum(d, dt, tol):
     assert ffn.rel(tdb.cpu().numpy(), db) < 1e-5
     for a, c in zip(outs[0], outs[1]):
         assert torch.equal(a, c)
+
+
+@pytest.mark.parametrize("dt,pc", [(torch.float64, "PC_F64"), (torch.float32, "PC_F32"),
+                                   (torch.bfloat16, "PC_BF16")])
+def test_copy2d_zero_source_stride_broadcasts(dt, pc):
+    """pc_copy2d with lds = 0 repeats a row (the generic vocabulary's `broadcast`
+    of a [n] value to [m, n], executor.py:78-95) and a scalar (cols = 1), one launch."""
+    st = torch.cuda.current_stream().cuda_stream
+    row = torch.randn(37, device="cuda").to(dt)
+    out = torch.empty(5, 37, device="cuda", dtype=dt)
+    _lib.call("pc_copy2d", getattr(_lib, pc), 5, 37, row.data_ptr(), 0, 0, out.data_ptr(), 37, st)
+    one = torch.randn(1, device="cuda").to(dt)
+    out2 = torch.empty(3, 4, device="cuda", dtype=dt)
+    _lib.call("pc_copy2d", getattr(_lib, pc), 12, 1, one.data_ptr(), 0, 0, out2.data_ptr(), 1, st)
+    torch.cuda.synchronize()
+    assert torch.equal(out, row.expand(5, 37))
+    assert torch.equal(out2, one.expand(3, 4))
