@@ -75,6 +75,30 @@ for cl in (0, 1):  # pc_colsum_set_cluster A/B: two-stage workspace vs one-pass 
         err = float((out.double() - ref).abs().max() / ref.abs().max())
         rows.append((f"bias col_sum [8192,{n}] {tag} (rel err {err:.1e})", us, T * n * 2))
 _lib.call("pc_colsum_set_cluster", 1)
+# a GPT block's LN2 side-stream sums: dgamma / dbeta + the fc2 / attention-output bias sums,
+# three launches (param grads + two column sums) vs one four-sum pass
+y3 = torch.randn(T, d, device=dev).to(bf)
+y4 = torch.randn(T, d, device=dev).to(bf)
+s3, s4 = torch.zeros(d, device=dev), torch.zeros(d, device=dev)
+mean.normal_(0, 0.1)
+rstd.uniform_(0.5, 1.5)
+
+
+def three():
+    _lib.call("pc_layernorm_param_grads", _lib.PC_BF16, T, d, dy.data_ptr(), x.data_ptr(),
+              mean.data_ptr(), rstd.data_ptr(), dg.data_ptr(), db.data_ptr(), 1, ws.data_ptr(),
+              ws.numel(), s)
+    for yy, ss in ((y3, s3), (y4, s4)):
+        _lib.call("pc_col_sum", _lib.PC_BF16, _lib.PC_F32, T, d, yy.data_ptr(), d, ss.data_ptr(), 1,
+                  ws.data_ptr(), ws.numel(), s)
+
+
+us = timed(three)
+rows.append(("LN2 params + 2 bias col_sums [8192,768], 3 launches", us, 4 * T * d * 2 + 8 * T))
+us = timed(lambda: _lib.call("pc_layernorm_param_bias_grads", T, d, dy.data_ptr(), x.data_ptr(),
+                             mean.data_ptr(), rstd.data_ptr(), dg.data_ptr(), db.data_ptr(),
+                             y3.data_ptr(), s3.data_ptr(), y4.data_ptr(), s4.data_ptr(), 1, s))
+rows.append(("LN2 params + 2 bias col_sums [8192,768], one pass", us, 4 * T * d * 2 + 8 * T))
 logits = torch.randn(T, V, device=dev).to(bf)
 tok = torch.randint(0, V, (T,), device=dev, dtype=torch.int32)
 rl = torch.empty(T, device=dev)
